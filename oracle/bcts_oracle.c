@@ -1,0 +1,665 @@
+/*
+ * oracle/bcts_oracle.c -- TEST INFRASTRUCTURE ONLY (never on the product path).
+ *
+ * Plain, slow, obviously-correct CPU implementation of what the hot path
+ * computes: Batch-BFS exhaustive tree search (Alg. 1),
+ * i.e. the d-step Q of Eq. 1 evaluated by recursive DFS,
+ * plus the BCTS correction (Eq. 3, Eq. 5, Prop. 1
+ * P:264-273) and a second, structurally different brute-force enumerator
+ * of all A^d action sequences (Eq. 1 written out literally).
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * `--impl reference` leg may load this library. It shares no code, header,
+ * table or constant generator with paper_2107_01715_b200/csrc (the CUDA path).
+ *
+ * Precision modes (readings R3/R17):
+ *   mode 0 = fp64 reference: rewards, values and penalty in double.
+ *   mode 1 = fp32 mirror   : R_{k+1} = fmaf(g[k], r, R_k), leaf = fmaf(g[d], m, R_d),
+ *                            MLP as a fixed-order fmaf chain; built with
+ *                            -ffp-contract=off so nothing else is fused.
+ * bf16 nets (Nature / Rainbow) always emulate bf16 operands (weights and
+ * hidden activations rounded RNE) with fp64 accumulation.
+ *
+ * Parity pins: see tests/test_oracle_pins.py (W1, W2, C1-chain, SPEC
+ * examples, closed forms, brute force == DFS, torch conv2d cross-check).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <fenv.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define OR_ENV_TABULAR 1
+#define OR_ENV_INT_HASH 2
+#define OR_ENV_ATARI_HASH 3
+#define OR_NET_TABLE 1
+#define OR_NET_MLP2 2
+#define OR_NET_NATURE 3
+#define OR_NET_RAINBOW 4
+
+#define IMG 84
+#define NPIX (IMG * IMG)
+#define MAXA 64
+#define MAXD 12
+
+/* ------------------------------------------------------------------ model */
+typedef struct {
+  int env, A, nS;
+  int32_t *tab_next;      /* [nS*A] */
+  double *tab_reward;     /* [nS*A] */
+  int net;
+  double *tab_q;          /* [nS*A] */
+  /* MLP (fp32 canonical, kept as float for the mirror mode) */
+  int mlp_in, mlp_hidden;
+  float *l1w, *l1b, *l2w, *l2b;
+  /* conv nets: weights rounded to bf16 and stored as double; biases fp32->double */
+  double *c1w, *c1b, *c2w, *c2b, *c3w, *c3b;
+  double *f1w, *f1b, *f2w, *f2b;          /* Nature fc1 / fc2 */
+  double *hvw, *hvb, *haw, *hab;          /* Rainbow fc_h_v / fc_h_a */
+  double *zvw, *zvb, *zaw, *zab;          /* Rainbow fc_z_v / fc_z_a */
+  int atoms;
+  double vmin, vmax;
+} oracle_model;
+
+/* Internal state: the oracle keeps Atari frames as 4 separate planes
+ * (channel, pixel) -- not the packed words of the device layout. */
+typedef struct {
+  int32_t id;                 /* TABULAR */
+  uint32_t s[16];             /* INT_HASH */
+  uint64_t key;               /* ATARI_HASH */
+  uint8_t plane[4][NPIX];     /* ATARI_HASH: plane 0 oldest, 3 newest */
+} ostate;
+
+static uint64_t o_mix64(uint64_t z) {   /* splitmix64 finalizer (ENV_SPEC) */
+  z ^= z >> 30; z *= 0xBF58476D1CE4E5B9ULL;
+  z ^= z >> 27; z *= 0x94D049BB133111EBULL;
+  z ^= z >> 31; return z;
+}
+static uint32_t o_fmix32(uint32_t h) {  /* murmur3 finalizer (ENV_SPEC) */
+  h ^= h >> 16; h *= 0x85EBCA6BU; h ^= h >> 13; h *= 0xC2B2AE35U; h ^= h >> 16; return h;
+}
+static uint32_t o_rotl32(uint32_t x, int r) { return (x << r) | (x >> (32 - r)); }
+
+/* Round a double to the nearest bfloat16 value (8 significant bits), ties to
+ * even, directly from the double (no intermediate fp32). Normal range only. */
+static double bf16_rne(double x) {
+  if (x == 0.0 || !isfinite(x)) return x;
+  int e;
+  double m = frexp(x, &e);           /* x = m * 2^e, 0.5 <= |m| < 1 */
+  double sc = ldexp(m, 8);           /* 128 <= |sc| < 256: 8 significant bits */
+  double r = nearbyint(sc);          /* current rounding mode: to nearest, ties to even */
+  return ldexp(r, e - 8);
+}
+
+double oracle_bf16_round(double x) { return bf16_rne(x); }
+
+static double *dup_bf16(const float *w, long n) {
+  double *o = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+  for (long i = 0; i < n; ++i) o[i] = bf16_rne((double)w[i]);
+  return o;
+}
+static double *dup_f64(const float *w, long n) {
+  double *o = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+  for (long i = 0; i < n; ++i) o[i] = (double)w[i];
+  return o;
+}
+static float *dup_f32(const float *w, long n) {
+  float *o = (float *)malloc(sizeof(float) * (size_t)(n > 0 ? n : 1));
+  memcpy(o, w, sizeof(float) * (size_t)(n > 0 ? n : 0));
+  return o;
+}
+
+void oracle_destroy(oracle_model *m) {
+  if (!m) return;
+  void *ptrs[] = {m->tab_next, m->tab_reward, m->tab_q, m->l1w, m->l1b, m->l2w, m->l2b,
+                  m->c1w, m->c1b, m->c2w, m->c2b, m->c3w, m->c3b, m->f1w, m->f1b, m->f2w, m->f2b,
+                  m->hvw, m->hvb, m->haw, m->hab, m->zvw, m->zvb, m->zaw, m->zab};
+  for (size_t i = 0; i < sizeof(ptrs) / sizeof(ptrs[0]); ++i) free(ptrs[i]);
+  free(m);
+}
+
+/* weights: canonical fp32 blob in synth.inputs.weight_specs order. */
+oracle_model *oracle_create(int env, int A, int nS, const int32_t *tab_next, const double *tab_reward,
+                            int net, const double *tab_q, const float *weights, long n_weights,
+                            int mlp_in, int mlp_hidden, int atoms, double vmin, double vmax) {
+  if (A < 2 || A > MAXA) return NULL;
+  oracle_model *m = (oracle_model *)calloc(1, sizeof(oracle_model));
+  m->env = env; m->A = A; m->nS = nS; m->net = net;
+  m->mlp_in = mlp_in; m->mlp_hidden = mlp_hidden; m->atoms = atoms; m->vmin = vmin; m->vmax = vmax;
+  if (env == OR_ENV_TABULAR) {
+    m->tab_next = (int32_t *)malloc(sizeof(int32_t) * nS * A);
+    m->tab_reward = (double *)malloc(sizeof(double) * nS * A);
+    memcpy(m->tab_next, tab_next, sizeof(int32_t) * nS * A);
+    memcpy(m->tab_reward, tab_reward, sizeof(double) * nS * A);
+  }
+  const float *w = weights;
+  long need = 0;
+  if (net == OR_NET_TABLE) {
+    m->tab_q = (double *)malloc(sizeof(double) * nS * A);
+    memcpy(m->tab_q, tab_q, sizeof(double) * nS * A);
+  } else if (net == OR_NET_MLP2) {
+    long H = mlp_hidden, I = mlp_in;
+    need = H * I + H + A * H + A;
+    if (n_weights != need) { oracle_destroy(m); return NULL; }
+    m->l1w = dup_f32(w, H * I); w += H * I;
+    m->l1b = dup_f32(w, H); w += H;
+    m->l2w = dup_f32(w, A * H); w += A * H;
+    m->l2b = dup_f32(w, A); w += A;
+  } else if (net == OR_NET_NATURE || net == OR_NET_RAINBOW) {
+    long sz[] = {32 * 4 * 8 * 8, 32, 64 * 32 * 4 * 4, 64, 64 * 64 * 3 * 3, 64};
+    need = sz[0] + sz[1] + sz[2] + sz[3] + sz[4] + sz[5];
+    if (net == OR_NET_NATURE) need += 512L * 3136 + 512 + (long)A * 512 + A;
+    else need += 2 * (512L * 3136 + 512) + (long)atoms * 512 + atoms + (long)A * atoms * 512 + (long)A * atoms;
+    if (n_weights != need) { oracle_destroy(m); return NULL; }
+    m->c1w = dup_bf16(w, sz[0]); w += sz[0];
+    m->c1b = dup_f64(w, sz[1]); w += sz[1];
+    m->c2w = dup_bf16(w, sz[2]); w += sz[2];
+    m->c2b = dup_f64(w, sz[3]); w += sz[3];
+    m->c3w = dup_bf16(w, sz[4]); w += sz[4];
+    m->c3b = dup_f64(w, sz[5]); w += sz[5];
+    if (net == OR_NET_NATURE) {
+      m->f1w = dup_bf16(w, 512L * 3136); w += 512L * 3136;
+      m->f1b = dup_f64(w, 512); w += 512;
+      m->f2w = dup_bf16(w, (long)A * 512); w += (long)A * 512;
+      m->f2b = dup_f64(w, A); w += A;
+    } else {
+      m->hvw = dup_bf16(w, 512L * 3136); w += 512L * 3136;
+      m->hvb = dup_f64(w, 512); w += 512;
+      m->haw = dup_bf16(w, 512L * 3136); w += 512L * 3136;
+      m->hab = dup_f64(w, 512); w += 512;
+      m->zvw = dup_bf16(w, (long)atoms * 512); w += (long)atoms * 512;
+      m->zvb = dup_f64(w, atoms); w += atoms;
+      m->zaw = dup_bf16(w, (long)A * atoms * 512); w += (long)A * atoms * 512;
+      m->zab = dup_f64(w, (long)A * atoms); w += (long)A * atoms;
+    }
+  } else {
+    oracle_destroy(m);
+    return NULL;
+  }
+  return m;
+}
+
+/* ------------------------------------------------------- record <-> state */
+long oracle_record_bytes(const oracle_model *m) {
+  if (m->env == OR_ENV_TABULAR) return 4;
+  if (m->env == OR_ENV_INT_HASH) return 64;
+  return 16 + 4L * NPIX;
+}
+
+static void from_record(const oracle_model *m, const uint8_t *rec, ostate *s) {
+  if (m->env == OR_ENV_TABULAR) {
+    memcpy(&s->id, rec, 4);
+  } else if (m->env == OR_ENV_INT_HASH) {
+    memcpy(s->s, rec, 64);
+  } else {
+    memcpy(&s->key, rec, 8);
+    const uint8_t *px = rec + 16;
+    for (int p = 0; p < NPIX; ++p)
+      for (int c = 0; c < 4; ++c) {
+        uint32_t word;
+        memcpy(&word, px + 4 * p, 4);
+        s->plane[c][p] = (uint8_t)((word >> (8 * c)) & 0xFFu);
+      }
+  }
+}
+
+static void to_record(const oracle_model *m, const ostate *s, uint8_t *rec) {
+  if (m->env == OR_ENV_TABULAR) {
+    memcpy(rec, &s->id, 4);
+  } else if (m->env == OR_ENV_INT_HASH) {
+    memcpy(rec, s->s, 64);
+  } else {
+    uint64_t pad = 0;
+    memcpy(rec, &s->key, 8);
+    memcpy(rec + 8, &pad, 8);
+    for (int p = 0; p < NPIX; ++p) {
+      uint32_t word = 0;
+      for (int c = 0; c < 4; ++c) word |= (uint32_t)s->plane[c][p] << (8 * c);
+      memcpy(rec + 16 + 4 * p, &word, 4);
+    }
+  }
+}
+
+/* ------------------------------------------------------------- env step G */
+/* Deterministic forward model (P:44 deterministic transitions; ENV_SPEC in
+ * DESIGN.md §3). Returns 0 on success, -1 on a domain error. */
+static int env_step(const oracle_model *m, const ostate *s, int a, ostate *out, double *r) {
+  if (a < 0 || a >= m->A) return -1;
+  if (m->env == OR_ENV_TABULAR) {
+    if (s->id < 0 || s->id >= m->nS) return -1;
+    out->id = m->tab_next[s->id * m->A + a];
+    *r = m->tab_reward[s->id * m->A + a];
+    return 0;
+  }
+  if (m->env == OR_ENV_INT_HASH) {
+    for (int w = 0; w < 16; ++w) {
+      uint32_t v = s->s[w] ^ o_rotl32(s->s[(w + 1) & 15], 13) ^ (0x9E3779B9U * (uint32_t)(a + 1)) ^
+                   (0x85EBCA6BU * (uint32_t)w);
+      out->s[w] = o_fmix32(v);
+    }
+    uint32_t t = out->s[0] >> 30;
+    *r = (t == 3) ? 1.0 : (t == 0) ? -1.0 : 0.0;
+    return 0;
+  }
+  /* ATARI_HASH: shift the frame stack by one frame; the new newest frame is
+   * the old newest XOR a key-derived noise byte per pixel. */
+  uint64_t k2 = o_mix64(s->key ^ (0x9E3779B97F4A7C15ULL * (uint64_t)(a + 1)));
+  out->key = k2;
+  memcpy(out->plane[0], s->plane[1], NPIX);
+  memcpy(out->plane[1], s->plane[2], NPIX);
+  memcpy(out->plane[2], s->plane[3], NPIX);
+  for (int p = 0; p < NPIX; ++p) {
+    uint8_t noise = (uint8_t)((o_mix64(k2 + (uint64_t)(p / 8)) >> (8 * (p % 8))) & 0xFFu);
+    out->plane[3][p] = s->plane[3][p] ^ noise;
+  }
+  uint64_t t = k2 >> 61;
+  *r = (t == 7) ? 1.0 : (t == 0) ? -1.0 : 0.0;
+  return 0;
+}
+
+int oracle_step(const oracle_model *m, const void *rec_in, int a, void *rec_out, double *r) {
+  ostate *s = (ostate *)malloc(sizeof(ostate)), *o = (ostate *)malloc(sizeof(ostate));
+  from_record(m, (const uint8_t *)rec_in, s);
+  int rc = env_step(m, s, a, o, r);
+  if (rc == 0) to_record(m, o, (uint8_t *)rec_out);
+  free(s); free(o);
+  return rc;
+}
+
+/* -------------------------------------------------------------- value net */
+/* Conv layer, plain definition: out[o][oy][ox] = b[o] + sum_{c,ky,kx}
+ * W[o][c][ky][kx] * in[c][oy*st+ky][ox*st+kx]; then ReLU, then bf16 RNE. */
+static void conv_relu_bf16(const double *in, int C, int H, const double *W, const double *b,
+                           int O, int K, int st, double *out, int OH) {
+  for (int o = 0; o < O; ++o)
+    for (int oy = 0; oy < OH; ++oy)
+      for (int ox = 0; ox < OH; ++ox) {
+        double acc = 0.0;
+        for (int c = 0; c < C; ++c)
+          for (int ky = 0; ky < K; ++ky)
+            for (int kx = 0; kx < K; ++kx)
+              acc += W[((o * C + c) * K + ky) * K + kx] * in[(c * H + oy * st + ky) * H + ox * st + kx];
+        acc += b[o];
+        out[(o * OH + oy) * OH + ox] = bf16_rne(acc > 0.0 ? acc : 0.0);
+      }
+}
+
+/* Linear: y[j] = b[j] + sum_i W[j][i] x[i]; optionally ReLU + bf16 RNE. */
+static void linear(const double *x, int I, const double *W, const double *b, int J, double *y, int relu_bf16) {
+  for (int j = 0; j < J; ++j) {
+    double acc = 0.0;
+    for (int i = 0; i < I; ++i) acc += W[(long)j * I + i] * x[i];
+    acc += b[j];
+    y[j] = relu_bf16 ? bf16_rne(acc > 0.0 ? acc : 0.0) : acc;
+  }
+}
+
+/* Q-hat(s, .) row. Returns 0, or -1 on a domain error. */
+static int qrow(const oracle_model *m, const ostate *s, int mode, double *q) {
+  const int A = m->A;
+  if (m->net == OR_NET_TABLE) {
+    if (s->id < 0 || s->id >= m->nS) return -1;
+    for (int a = 0; a < A; ++a) {
+      double v = m->tab_q[s->id * A + a];
+      q[a] = mode ? (double)(float)v : v;
+    }
+    return 0;
+  }
+  if (m->net == OR_NET_MLP2) {
+    const int I = m->mlp_in, H = m->mlp_hidden;
+    double x[256];
+    float xf[256];
+    for (int j = 0; j < I; ++j) {
+      uint32_t byte = (s->s[(j / 4) & 15] >> (8 * (j % 4))) & 0xFFu;
+      x[j] = (double)byte / 256.0;
+      xf[j] = (float)byte / 256.0f;
+    }
+    if (mode) { /* fp32 mirror: fixed-order fmaf chains starting from the bias */
+      float h[1024];
+      for (int j = 0; j < H; ++j) {
+        float acc = m->l1b[j];
+        for (int i = 0; i < I; ++i) acc = fmaf(m->l1w[(long)j * I + i], xf[i], acc);
+        h[j] = acc > 0.0f ? acc : 0.0f;
+      }
+      for (int a = 0; a < A; ++a) {
+        float acc = m->l2b[a];
+        for (int j = 0; j < H; ++j) acc = fmaf(m->l2w[(long)a * H + j], h[j], acc);
+        q[a] = (double)acc;
+      }
+    } else {
+      double h[1024];
+      for (int j = 0; j < H; ++j) {
+        double acc = (double)m->l1b[j];
+        for (int i = 0; i < I; ++i) acc += (double)m->l1w[(long)j * I + i] * x[i];
+        h[j] = acc > 0.0 ? acc : 0.0;
+      }
+      for (int a = 0; a < A; ++a) {
+        double acc = (double)m->l2b[a];
+        for (int j = 0; j < H; ++j) acc += (double)m->l2w[(long)a * H + j] * h[j];
+        q[a] = acc;
+      }
+    }
+    return 0;
+  }
+  /* Nature-DQN / Rainbow trunk (R15/R17): input bytes, unscaled
+   * (1/255 is folded into conv1 weights). */
+  double *in = (double *)malloc(sizeof(double) * 4 * NPIX);
+  double *h1 = (double *)malloc(sizeof(double) * 32 * 20 * 20);
+  double *h2 = (double *)malloc(sizeof(double) * 64 * 9 * 9);
+  double *h3 = (double *)malloc(sizeof(double) * 64 * 7 * 7);
+  for (int c = 0; c < 4; ++c)
+    for (int p = 0; p < NPIX; ++p) in[c * NPIX + p] = (double)s->plane[c][p];
+  conv_relu_bf16(in, 4, 84, m->c1w, m->c1b, 32, 8, 4, h1, 20);
+  conv_relu_bf16(h1, 32, 20, m->c2w, m->c2b, 64, 4, 2, h2, 9);
+  conv_relu_bf16(h2, 64, 9, m->c3w, m->c3b, 64, 3, 1, h3, 7);
+  /* h3 is already in PyTorch NCHW flatten order: index c*49 + y*7 + x. */
+  if (m->net == OR_NET_NATURE) {
+    double h4[512];
+    linear(h3, 3136, m->f1w, m->f1b, 512, h4, 1);
+    linear(h4, 512, m->f2w, m->f2b, A, q, 0);
+  } else {
+    const int NA = m->atoms;
+    double hv[512], ha[512];
+    double *v = (double *)malloc(sizeof(double) * NA);
+    double *adv = (double *)malloc(sizeof(double) * A * NA);
+    linear(h3, 3136, m->hvw, m->hvb, 512, hv, 1);
+    linear(h3, 3136, m->haw, m->hab, 512, ha, 1);
+    linear(hv, 512, m->zvw, m->zvb, NA, v, 0);
+    linear(ha, 512, m->zaw, m->zab, A * NA, adv, 0);
+    for (int i = 0; i < NA; ++i) {
+      double mean = 0.0;
+      for (int a = 0; a < A; ++a) mean += adv[a * NA + i];
+      mean /= A;
+      for (int a = 0; a < A; ++a) adv[a * NA + i] = v[i] + adv[a * NA + i] - mean;   /* logits */
+    }
+    for (int a = 0; a < A; ++a) {
+      double mx = adv[a * NA];
+      for (int i = 1; i < NA; ++i) mx = adv[a * NA + i] > mx ? adv[a * NA + i] : mx;
+      double den = 0.0, num = 0.0;
+      for (int i = 0; i < NA; ++i) {
+        double e = exp(adv[a * NA + i] - mx);
+        double z = m->vmin + i * (m->vmax - m->vmin) / (NA - 1);
+        den += e;
+        num += z * e;
+      }
+      q[a] = num / den;   /* sum_i z_i softmax_i */
+    }
+    free(v); free(adv);
+  }
+  free(in); free(h1); free(h2); free(h3);
+  if (mode) for (int a = 0; a < A; ++a) q[a] = (double)(float)q[a];
+  return 0;
+}
+
+int oracle_qrow(const oracle_model *m, const void *rec, int mode, double *q_out) {
+  ostate *s = (ostate *)malloc(sizeof(ostate));
+  from_record(m, (const uint8_t *)rec, s);
+  int rc = qrow(m, s, mode, q_out);
+  free(s);
+  return rc;
+}
+
+/* ---------------------------------------------------- discount + accumulate */
+static void discounts(double gamma, int d, double *g) {
+  g[0] = 1.0;
+  for (int k = 1; k <= d; ++k) g[k] = g[k - 1] * gamma;   /* product of k copies of gamma */
+}
+/* R_{k+1} = R_k + gamma^k r_k  (Alg. 1 "Accumulate discounted reward") */
+static double acc_reward(int mode, const double *g, int k, double r, double R) {
+  if (mode) return (double)fmaf((float)g[k], (float)r, (float)R);
+  return R + g[k] * r;
+}
+/* R_d + gamma^d max_a Q(s_d, a)  (Alg. 1 leaf line) */
+static double leaf_total(int mode, const double *g, int d, double mq, double R) {
+  if (mode) return (double)fmaf((float)g[d], (float)mq, (float)R);
+  return R + g[d] * mq;
+}
+static double rowmax(const double *q, int A) {
+  double mx = q[0];
+  for (int a = 1; a < A; ++a) if (q[a] > mx) mx = q[a];
+  return mx;
+}
+static int argmax_low(const double *q, int A) {   /* lowest index attaining the max */
+  int b = 0;
+  for (int a = 1; a < A; ++a) if (q[a] > q[b]) b = a;
+  return b;
+}
+
+/* ----------------------------------------------------------- Eq. 4 / Eq. 5 */
+/* Eq. 5: B = sqrt(log A)(de sqrt(d) - do sqrt(d-1)) - (de - do)/sqrt(8); log = ln (R5). */
+double oracle_penalty_eq5(double de, double dob, int A, int d) {
+  return sqrt(log((double)A)) * (de * sqrt((double)d) - dob * sqrt((double)(d - 1))) - (de - dob) / sqrt(8.0);
+}
+/* Eq. 4: sqrt(2 log A)(se sqrt(d) - so sqrt(d-1)) - (se - so)/2. */
+double oracle_bias_gap_eq4(double so, double se, int A, int d) {
+  return sqrt(2.0 * log((double)A)) * (se * sqrt((double)d) - so * sqrt((double)(d - 1))) - (se - so) / 2.0;
+}
+
+/* --------------------------------------------------------------- the DFS */
+typedef struct {
+  const oracle_model *m;
+  int d, mode;
+  double g[MAXD + 1];
+  ostate *buf;          /* [d+1] per-depth scratch states */
+  double q[MAXA];
+} dfs_ctx;
+
+/* dfs(s, t, R): if t = d: leaf total; else max over a of dfs(s'_a, t+1, R + g[t] r).
+ * Returns the max value and, through *leaf, the lowest leaf index (within the
+ * subtree, base-A digits a_t..a_{d-1}) attaining it. */
+static int dfs(dfs_ctx *c, int t, double R, double *best, long *leaf) {
+  const oracle_model *m = c->m;
+  ostate *s = &c->buf[t];
+  if (t == c->d) {
+    if (qrow(m, s, c->mode, c->q)) return -1;
+    *best = leaf_total(c->mode, c->g, c->d, rowmax(c->q, m->A), R);
+    *leaf = 0;
+    return 0;
+  }
+  double bv = -INFINITY;
+  long bl = 0, span = 1;
+  for (int k = t + 1; k < c->d; ++k) span *= m->A;
+  for (int a = 0; a < m->A; ++a) {
+    double r, v;
+    long lf;
+    if (env_step(m, s, a, &c->buf[t + 1], &r)) return -1;
+    if (dfs(c, t + 1, acc_reward(c->mode, c->g, t, r, R), &v, &lf)) return -1;
+    if (v > bv) { bv = v; bl = (long)a * span + lf; }
+  }
+  *best = bv;
+  *leaf = bl;
+  return 0;
+}
+
+/* BCTS terms at one root: pi_o, delta_o, delta_e, B (Prop. 1, Eq. 5).
+ * delta_a = r(s0,a) + gamma max Q(s1^a, .) - Q(s0, a) with depth-0/1 samples. */
+static int bcts_terms(const oracle_model *m, const ostate *root, int d, int mode, const double *g,
+                      double *terms, double *q0) {
+  const int A = m->A;
+  ostate *s1 = (ostate *)malloc(sizeof(ostate));
+  double q1[MAXA], delta[MAXA];
+  int rc = qrow(m, root, mode, q0);
+  int pio = argmax_low(q0, A);
+  for (int a = 0; a < A && !rc; ++a) {
+    double r;
+    rc = env_step(m, root, a, s1, &r);
+    if (!rc) rc = qrow(m, s1, mode, q1);
+    if (rc) break;
+    double R1 = acc_reward(mode, g, 0, r, 0.0);
+    double one_step = leaf_total(mode, g, 1, rowmax(q1, A), R1);   /* Q-hat_1(s0, a) */
+    delta[a] = mode ? (double)((float)one_step - (float)q0[a]) : one_step - q0[a];
+  }
+  free(s1);
+  if (rc) return rc;
+  double dob = fabs(delta[pio]), sum = 0.0;
+  for (int a = 0; a < A; ++a) if (a != pio) sum += fabs(delta[a]);
+  double de = sum / (A - 1);
+  terms[0] = pio;
+  terms[1] = dob;
+  terms[2] = de;
+  terms[3] = oracle_penalty_eq5(de, dob, A, d);
+  return 0;
+}
+
+/* Eq. 3 with the sweep constant beta: subtract beta*g[d]*B
+ * from every root action != pi_o; beta == 0 or correction off -> vanilla exactly. */
+static void apply_correction(int A, int d, int mode, const double *g, double beta, int corr,
+                             const double *vanilla, const double *terms, double *q) {
+  for (int a = 0; a < A; ++a) q[a] = vanilla[a];
+  if (!corr || beta == 0.0 || d == 0) return;
+  int pio = (int)terms[0];
+  double gd = mode ? (double)(float)g[d] : g[d];
+  double pen = beta * gd * terms[3];
+  for (int a = 0; a < A; ++a)
+    if (a != pio) q[a] = mode ? (double)(float)(vanilla[a] - pen) : vanilla[a] - pen;
+}
+
+/* Full search over n roots (records in ABI format). Outputs (nullable except
+ * actions/root_q): vanilla_q [n*A], terms [n*4] (pi_o, delta_o, delta_e, B),
+ * best_leaf [n*A] (lowest leaf index attaining each vanilla_q entry). */
+int oracle_search(const oracle_model *m, const void *roots, long n_roots, int depth, double gamma,
+                  double beta, int corr, int mode, int threads, int32_t *actions, double *root_q,
+                  double *vanilla_q, double *terms_out, int64_t *best_leaf) {
+  const int A = m->A;
+  if (depth < 0 || depth > MAXD || n_roots < 0) return -1;
+  const long rb = oracle_record_bytes(m);
+  double g[MAXD + 1];
+  discounts(gamma, depth, g);
+  double *van = (double *)malloc(sizeof(double) * (n_roots * A + 1));
+  int64_t *bl = (int64_t *)malloc(sizeof(int64_t) * (n_roots * A + 1));
+  int err = 0;
+  long ntask = n_roots * A;
+  if (threads < 1) threads = 1;
+  if (depth >= 1) {
+#pragma omp parallel for schedule(dynamic, 1) num_threads(threads)
+    for (long task = 0; task < ntask; ++task) {
+      long r = task / A;
+      int a0 = (int)(task % A);
+      dfs_ctx c;
+      c.m = m; c.d = depth; c.mode = mode;
+      memcpy(c.g, g, sizeof(g));
+      c.buf = (ostate *)malloc(sizeof(ostate) * (depth + 1));
+      from_record(m, (const uint8_t *)roots + r * rb, &c.buf[0]);
+      double rr, v = 0.0;
+      long lf = 0;
+      int rc = env_step(m, &c.buf[0], a0, &c.buf[1], &rr);
+      if (!rc) rc = dfs(&c, 1, acc_reward(mode, g, 0, rr, 0.0), &v, &lf);
+      long span = 1;
+      for (int k = 1; k < depth; ++k) span *= A;
+      van[task] = v;
+      bl[task] = (int64_t)a0 * span + lf;
+      if (rc) {
+#pragma omp atomic write
+        err = 1;
+      }
+      free(c.buf);
+    }
+  }
+  if (err) { free(van); free(bl); return -1; }
+  ostate *root = (ostate *)malloc(sizeof(ostate));
+  for (long r = 0; r < n_roots && !err; ++r) {
+    from_record(m, (const uint8_t *)roots + r * rb, root);
+    double q0[MAXA], terms[4] = {0, 0, 0, 0}, q[MAXA];
+    double *vr = van + r * A;
+    if (depth == 0) {          /* d = 0: greedy on Q-hat(s0, .) (R11) */
+      if (qrow(m, root, mode, q0)) { err = 1; break; }
+      for (int a = 0; a < A; ++a) { vr[a] = q0[a]; q[a] = q0[a]; bl[r * A + a] = 0; }
+      terms[0] = argmax_low(q0, A);
+    } else {
+      if (corr && bcts_terms(m, root, depth, mode, g, terms, q0)) { err = 1; break; }
+      apply_correction(A, depth, mode, g, beta, corr, vr, terms, q);
+    }
+    actions[r] = argmax_low(q, A);
+    for (int a = 0; a < A; ++a) root_q[r * A + a] = q[a];
+    if (vanilla_q) for (int a = 0; a < A; ++a) vanilla_q[r * A + a] = vr[a];
+    if (terms_out) for (int k = 0; k < 4; ++k) terms_out[r * 4 + k] = terms[k];
+    if (best_leaf) for (int a = 0; a < A; ++a) best_leaf[r * A + a] = bl[r * A + a];
+  }
+  free(root); free(van); free(bl);
+  return err ? -1 : 0;
+}
+
+/* Node `index` of level `level` below one root: the state reached by the
+ * action sequence given by the base-A digits of index (a_0 most significant,
+ * R1 reading), and its cumulative discounted reward R_level. */
+int oracle_node(const oracle_model *m, const void *root_rec, int level, int64_t index, double gamma,
+                int mode, void *rec_out, double *R_out) {
+  const int A = m->A;
+  if (level < 0 || level > MAXD) return -1;
+  double g[MAXD + 1];
+  discounts(gamma, level, g);
+  ostate *a = (ostate *)malloc(sizeof(ostate)), *b = (ostate *)malloc(sizeof(ostate));
+  from_record(m, (const uint8_t *)root_rec, a);
+  double R = 0.0;
+  int rc = 0;
+  for (int t = 0; t < level && !rc; ++t) {
+    int64_t div = 1;
+    for (int k = t + 1; k < level; ++k) div *= A;
+    int act = (int)((index / div) % A);
+    double r;
+    rc = env_step(m, a, act, b, &r);
+    R = acc_reward(mode, g, t, r, R);
+    ostate *tmp = a; a = b; b = tmp;
+  }
+  if (!rc) { to_record(m, a, (uint8_t *)rec_out); *R_out = R; }
+  free(a); free(b);
+  return rc;
+}
+
+/* Brute force: Eq. 1 literally -- enumerate all A^d action sequences in
+ * lexicographic order (leaf index base A), roll each out from the root, and
+ * take the max over each a_0 block. Same outputs as oracle_search. */
+int oracle_search_bruteforce(const oracle_model *m, const void *roots, long n_roots, int depth,
+                             double gamma, double beta, int corr, int mode, int32_t *actions,
+                             double *root_q, double *vanilla_q, double *terms_out, int64_t *best_leaf) {
+  const int A = m->A;
+  if (depth < 1 || depth > MAXD) return -1;
+  const long rb = oracle_record_bytes(m);
+  double g[MAXD + 1];
+  discounts(gamma, depth, g);
+  int64_t nleaf = 1;
+  for (int k = 0; k < depth; ++k) nleaf *= A;
+  int64_t seg = nleaf / A;
+  uint8_t *rec = (uint8_t *)malloc(rb);
+  ostate *leaf = (ostate *)malloc(sizeof(ostate)), *root = (ostate *)malloc(sizeof(ostate));
+  double q[MAXA], van[MAXA], qq[MAXA], q0[MAXA], terms[4] = {0, 0, 0, 0};
+  int64_t bl[MAXA];
+  int rc = 0;
+  for (long r = 0; r < n_roots && !rc; ++r) {
+    const uint8_t *rr = (const uint8_t *)roots + r * rb;
+    for (int a = 0; a < A; ++a) { van[a] = -INFINITY; bl[a] = 0; }
+    for (int64_t i = 0; i < nleaf && !rc; ++i) {
+      double R;
+      rc = oracle_node(m, rr, depth, i, gamma, mode, rec, &R);
+      if (rc) break;
+      from_record(m, rec, leaf);
+      rc = qrow(m, leaf, mode, q);
+      double tot = leaf_total(mode, g, depth, rowmax(q, A), R);
+      int a0 = (int)(i / seg);
+      if (tot > van[a0]) { van[a0] = tot; bl[a0] = i; }
+    }
+    if (rc) break;
+    from_record(m, rr, root);
+    if (corr) rc = bcts_terms(m, root, depth, mode, g, terms, q0);
+    if (rc) break;
+    apply_correction(A, depth, mode, g, beta, corr, van, terms, qq);
+    actions[r] = argmax_low(qq, A);
+    for (int a = 0; a < A; ++a) root_q[r * A + a] = qq[a];
+    if (vanilla_q) for (int a = 0; a < A; ++a) vanilla_q[r * A + a] = van[a];
+    if (terms_out) for (int k = 0; k < 4; ++k) terms_out[r * 4 + k] = terms[k];
+    if (best_leaf) for (int a = 0; a < A; ++a) best_leaf[r * A + a] = bl[a];
+  }
+  free(rec); free(leaf); free(root);
+  return rc ? -1 : 0;
+}
+
+int oracle_max_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
