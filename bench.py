@@ -1,0 +1,353 @@
+#!/usr/bin/env python
+"""bench.py -- Batch-BFS + BCTS on B200: tree nodes (expanded + evaluated)/s and root decisions/s.
+
+Default workload = BASELINE.json's metric configuration C5: depth 4, A = 18,
+one Atari-shaped root (4x84x84 uint8 frame stack), Rainbow-shaped bf16 Q-net,
+BCTS correction on. One step = one full search (every SURVEY §8a row: root
+row, level expansions, leaf net, backup, correction). N > 1 (torchrun): the
+same single-root search split into contiguous leaf ranges, one max
+all-reduce of the packed root keys (strong scaling).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "tree nodes expanded+evaluated/sec and root decisions/sec at depth 4, A=18"
+
+
+def nodes_per_root(A, d, corr):
+    """Algorithmic per-root counts: expanded = sum_{k=1..d} A^k,
+    evaluated = A^d + corr*(1 + [d>=2]*A) (+1 at d=0)."""
+    expanded = sum(A ** k for k in range(1, d + 1))
+    evaluated = (A ** d + (corr * (1 + (A if d >= 2 else 0))) if d >= 1 else 1)
+    return expanded, evaluated
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
+                "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device, self.proc = device, None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        if not getattr(self, "lines", None):
+            return None
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return None
+        load = [s for s in sm if s > 0.5 * (mx or 1)] or sm
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if args.impl == "reference":
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+# ------------------------------------------------------------------ CPU oracle leg
+def oracle_sample(cfg, seconds_target=12.0, threads=None):
+    """Time the oracle (as it stands) on a bounded sample of the same workload:
+    whole depth-2 subtrees of the first root, run across the host cores."""
+    from oracle import Oracle
+    threads = threads or os.cpu_count() or 1
+    o = Oracle.from_config(cfg)
+    root = cfg.roots(1)
+    A, d = cfg.A, cfg.depth
+    exp, ev = nodes_per_root(A, d, 1)
+    per_task_nodes = (exp + A ** d) / (A * A)      # subtree share of the tree's expansions + leaf evaluations
+    done_tasks, elapsed, t0 = 0, 0.0, 0
+    wave = threads
+    while elapsed < seconds_target and t0 < A * A:
+        n = min(wave, A * A - t0)
+        t = time.perf_counter()
+        o.subtrees(root, d, cfg.gamma, t0, t0 + n, threads=threads)
+        elapsed += time.perf_counter() - t
+        done_tasks += n
+        t0 += n
+    nodes = per_task_nodes * done_tasks
+    return {"value": nodes / elapsed, "unit": "nodes/s", "cores": threads, "kind": "oracle",
+            "decisions_per_s": nodes / elapsed / (exp + ev),
+            "sample": f"{done_tasks} of the {A * A} depth-2 subtrees of root 0 ({cfg.name}: A={A}, d={d}), "
+                      f"plain-C DFS, {threads} threads, {elapsed:.1f} s"}
+
+
+def run_reference(args, cfg, world, rank):
+    if rank != 0:
+        return 0
+    from oracle import Oracle
+    threads = os.cpu_count() or 1
+    o = Oracle.from_config(cfg)
+    root = cfg.roots(1)
+    A, d = cfg.A, cfg.depth
+    exp, ev = nodes_per_root(A, d, 1)
+    per_task = (exp + A ** d) / (A * A)
+    ntask = min(threads, A * A)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t = time.perf_counter()
+        o.subtrees(root, d, cfg.gamma, 0, ntask, threads=threads)
+        dt = time.perf_counter() - t
+        if i >= args.warmup:
+            times.append(dt)
+    step = sum(times) / len(times)
+    value = per_task * ntask / step
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "nodes/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "decisions_per_s": value / (exp + ev),
+            "config": {"workload": f"{cfg.name}: Batch-BFS+BCTS, A={A}, depth={d}, {cfg.n_roots} root(s), "
+                                   f"Rainbow-shaped Q-net; each step = {ntask} depth-2 subtrees (bounded sample)",
+                       "roots": cfg.n_roots, "depth": d, "A": A},
+            "cpu_baseline": {"value": value, "unit": "nodes/s", "cores": threads, "kind": "oracle",
+                             "sample": f"{ntask} of {A * A} depth-2 subtrees per step, plain-C DFS (fp64, bf16-emulated net)"},
+            "e2e": {"value": value, "unit": "nodes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU leg
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--roots", type=int, default=0, help="override n_roots (throughput variants)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--simt", action="store_true", help="SIMT reference net (no tensor cores)")
+    ap.add_argument("--no-flush", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    from synth.inputs import config
+    import dataclasses
+    cfg = config(args.config)
+    if args.roots:
+        cfg = dataclasses.replace(cfg, n_roots=args.roots)
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        return run_reference(args, cfg, world, rank)
+
+    import numpy as np
+    import torch
+    import paper_2107_01715_b200 as P
+    from paper_2107_01715_b200.parallel import sharded_search
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    flags = P.F_SIMT_NET if args.simt else 0
+    h = P.Handle.from_config(cfg, device=local, flags=flags)
+    n, d, A, corr = cfg.n_roots, cfg.depth, cfg.A, 1
+    roots_np = cfg.roots()
+    roots = torch.from_numpy(roots_np.view(np.uint8).reshape(n, -1).copy()).to(dev)
+    act = torch.empty(n, dtype=torch.int32, device=dev)
+    q = torch.empty(n, A, dtype=torch.float32, device=dev)
+    keys = torch.empty(n * A, dtype=torch.int64, device=dev)
+    launches_per_step = [0]
+
+    def step():
+        if world == 1:
+            out = h.search(roots, n, d, cfg.gamma, cfg.beta, corr, out={"actions": act, "root_q": q})
+        else:
+            out = sharded_search(h, roots, n, d, cfg.gamma, cfg.beta, corr, keys=keys)
+        launches_per_step[0] = out["stats"]["kernel_launches"]
+        return out
+
+    flush = None if args.no_flush else torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    # ---- timed region: K steps, L2 flushed (256 MiB write, untimed) before each
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    h.profile(True)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            if flush is not None:
+                flush.fill_(i & 0xFF)
+            evs[i][0].record()
+            step()
+            evs[i][1].record()
+        torch.cuda.synchronize()
+        barrier()
+    prof = h.profile_read()
+    h.profile(False)
+    step_ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([step_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        step_ms = float(t.item())
+    exp, ev = nodes_per_root(A, d, corr)
+    total_nodes = n * (exp + ev)
+    value = total_nodes / (step_ms / 1e3)
+
+    # ---- roofline of the dominant kernel class (events on the launching stream)
+    peaks = load_peaks()
+    dom = max(prof.items(), key=lambda kv: kv[1]["ms"]) if prof else None
+    roofline = None
+    kernels = {}
+    step_kernel_ms = sum(v["ms"] for v in prof.values())
+    for name, v in prof.items():
+        per_launch_ms = v["ms"] / max(v["launches"], 1)
+        ach = v["work"] / (v["ms"] / 1e3) / (1e9 if v["unit"] == "byte" else 1e12) if v["ms"] > 0 else 0.0
+        kernels[name] = {"launches_per_step": v["launches"] / args.steps, "ms_per_launch": per_launch_ms,
+                         "share": v["ms"] / step_kernel_ms if step_kernel_ms else 0.0,
+                         "achieved": ach, "unit": "GB/s" if v["unit"] == "byte" else "TFLOP/s"}
+    if dom:
+        name, v = dom
+        long_run = step_ms * args.steps > 1000.0
+        if v["unit"] == "byte":
+            peak, unit, bound = peaks["hbm_gbs"], "GB/s", "hbm"
+        else:
+            peak = peaks["bf16_tflops_sustained"] if long_run else peaks["bf16_tflops"]
+            unit, bound = "TFLOP/s", "tensor"
+            if args.simt:
+                bound = "alu"
+        ach = kernels[name]["achieved"]
+        roofline = {"kernel": name, "bound": bound, "achieved": ach, "peak": peak, "unit": unit,
+                    "frac": ach / peak, "traffic": None,
+                    "work_per_launch": v["work"] / max(v["launches"], 1),
+                    "peak_source": peaks["source"] + (" sustained" if long_run and bound == "tensor" else " burst")}
+        tr = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tr):
+            tj = json.load(open(tr))
+            if tj.get("kernel") == name and tj.get("config") == cfg.name:
+                roofline["traffic"] = tj.get("dram_bytes_per_launch")
+                roofline["traffic_source"] = tj.get("source")
+
+    # ---- end to end: host roots in (pinned), host outputs out, through the public API
+    e2e = None
+    pin_roots = torch.from_numpy(roots_np.view(np.uint8).reshape(n, -1).copy()).pin_memory()
+    pin_act = torch.empty(n, dtype=torch.int32).pin_memory()
+    pin_q = torch.empty(n, A, dtype=torch.float32).pin_memory()
+    e2e_times = []
+    for i in range(args.warmup + args.steps):
+        if flush is not None:
+            flush.fill_(i & 0xFF)
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        if world == 1:
+            h.search_host(pin_roots, n, d, cfg.gamma, cfg.beta, corr, pin_act, pin_q)
+        else:
+            droots = pin_roots.to(dev, non_blocking=True)
+            out = sharded_search(h, droots, n, d, cfg.gamma, cfg.beta, corr, keys=keys)
+            pin_act.copy_(out["actions"], non_blocking=True)
+            pin_q.copy_(out["root_q"], non_blocking=True)
+            torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            e2e_times.append(dt)
+    e2e_s = sum(e2e_times) / len(e2e_times)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": total_nodes / e2e_s, "unit": "nodes/s", "h2d_bytes_per_step": int(pin_roots.numel()),
+           "d2h_bytes_per_step": int(pin_act.numel() * 4 + pin_q.numel() * 4), "ms_per_step": e2e_s * 1e3,
+           "decisions_per_s": n / e2e_s}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = oracle_sample(cfg)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "nodes/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+                "decisions_per_s": n / (step_ms / 1e3),
+                "config": {"workload": f"{cfg.name}: Batch-BFS+BCTS, A={A}, depth={d}, {n} root(s), "
+                                       f"{'Rainbow' if cfg.net == 4 else 'Nature' if cfg.net == 3 else 'other'}"
+                                       f"-shaped bf16 Q-net (random init), correction on",
+                           "roots": n, "depth": d, "A": A, "nodes_per_decision": exp + ev,
+                           "parallelism": f"leaf-range shards x{world}" if world > 1 else "single GPU",
+                           "l2": "flushed before every timed step (256 MiB write, untimed)" if flush is not None
+                           else "not flushed", "net_path": "simt" if args.simt else "tcgen05"},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches_per_step[0] * args.steps,
+                "clocks": clk.summary(), "kernels": kernels}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

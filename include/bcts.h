@@ -1,0 +1,221 @@
+/*
+ * include/bcts.h -- C ABI of the B200-native Batch-BFS + BCTS hot path.
+ *
+ * What it computes (PAPER.md = /root/reference/PAPER.md, "P:n" = line n):
+ *   For each root state s_0, the exhaustive depth-d, A-ary tree is expanded
+ *   one level at a time (Batch-BFS, Alg. 1): every node of a level
+ *   is replicated A ways, stepped through the deterministic forward model G
+ *   and the discounted reward R += gamma^k r is accumulated. The
+ *   A^d leaves are scored with R + gamma^d max_a Q_theta(s_d, a), and
+ *   a segmented max over each root action's A^(d-1) leaves gives the vanilla
+ *   d-step Q of Eq. 1 and the greedy action of Eq. 2,
+ *   i.e. Alg. 1's floor(argmax R / A^(d-1)). With correction_on, the
+ *   BCTS penalty beta * gamma^d * B(delta_e, delta_o, A, d) of Eq. 5
+ *    is subtracted from every root action != pi_o (Eq. 3,
+ *   P:205-213; sweep constant beta), where delta_a is the root Bellman
+ *   error from depths 0 and 1 (Prop. 1), delta_o = |delta_pi_o|
+ *   and delta_e the mean |delta_a| over a != pi_o.
+ *
+ * Conventions (DESIGN.md §2 readings):
+ *   - Node i of level k has children i*A + a (a = 0..A-1); leaf index within a
+ *     root = sum_t a_t A^(d-1-t) (R1). Ties: lowest index everywhere (R4).
+ *   - gamma^k is formed on the host as (float)(product of k copies of
+ *     (double)gamma); R_{k+1} = fmaf(g[k], r, R_k); leaf = fmaf(g[d], m, R_d) (R3).
+ *   - depth == 0: greedy on Q_hat(s_0, .), no correction (R11).
+ *   - beta == 0 or correction_on == 0: corrected Q == vanilla Q bit for bit (R12).
+ *
+ * Memory and streams:
+ *   - Unless stated otherwise every data pointer is a DEVICE pointer (e.g.
+ *     torch.Tensor.data_ptr() on the handle's device). The caller owns roots
+ *     and all outputs; the library never frees them.
+ *   - Calls enqueue on the handle's stream and return; outputs are valid after
+ *     a stream synchronize. bcts_search_host is the exception (synchronous).
+ *   - Argument errors are detected before anything is enqueued; on ANY error
+ *     the outputs are left untouched.
+ *   - A handle is used by one host thread at a time; handles are independent.
+ *   - No C++ exception ever crosses this boundary.
+ */
+#ifndef BCTS_H_
+#define BCTS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BCTS_ABI_VERSION 1
+
+typedef struct bcts_handle_t *bcts_handle;
+
+typedef enum {
+  BCTS_OK = 0,
+  BCTS_ERR_INVALID_ARG = 1,   /* bad argument; nothing enqueued */
+  BCTS_ERR_UNSUPPORTED = 2,   /* valid request this build does not implement */
+  BCTS_ERR_OUT_OF_MEMORY = 3, /* device allocation failed */
+  BCTS_ERR_BUDGET = 4,        /* one root's per-call tree cannot fit the workspace, or A^d overflows */
+  BCTS_ERR_CUDA = 5,          /* a CUDA runtime error (detail in bcts_last_error) */
+  BCTS_ERR_NUMERIC = 7        /* non-finite value met where the contract forbids it */
+} bcts_status;
+
+/* Forward models G (DESIGN.md §3 ENV_SPEC). Root-record layouts:
+ *   TABULAR    : int32 state id                                   (4 B)
+ *   INT_HASH   : uint32 s[16]                                     (64 B)
+ *   ATARI_HASH : uint64 key, uint64 pad, uint32 w[84*84]          (28,240 B)
+ *                w[p] packs the 4-frame stack of pixel p, byte c = frame c
+ *                (c = 0 oldest, 3 newest; frame stacking P:355). */
+typedef enum { BCTS_ENV_TABULAR = 1, BCTS_ENV_INT_HASH = 2, BCTS_ENV_ATARI_HASH = 3 } bcts_env_kind;
+
+/* Value nets Q_theta (DESIGN.md §3 NET_SPEC; random-init weights, shapes of P:83). */
+typedef enum {
+  BCTS_NET_TABLE = 1,        /* tabular Q_hat [nS*A] (TABULAR env only)          */
+  BCTS_NET_MLP2_F32 = 2,     /* 64 -> hidden -> A, fp32 fixed-order FMA (INT_HASH) */
+  BCTS_NET_NATURE_BF16 = 3,  /* Nature-DQN conv trunk + fc 512 + fc A, bf16      */
+  BCTS_NET_RAINBOW_BF16 = 4  /* same trunk + dueling C51 head (51 atoms), bf16   */
+} bcts_net_kind;
+
+/* Config flags. */
+#define BCTS_F_CLAMP_PENALTY 0x1u /* clamp B at 0 (opt-in; default signed, R8) */
+#define BCTS_F_SIMT_NET 0x2u      /* use the SIMT reference net (no tensor cores) */
+#define BCTS_F_MATERIALIZE_LEAVES 0x4u /* store the leaf level (else leaf frames are
+                                        * generated inside the net's A-operand producer) */
+
+typedef struct {
+  uint32_t abi_version;     /* must be BCTS_ABI_VERSION */
+  int32_t device;           /* CUDA device ordinal */
+  void *cuda_stream;        /* cudaStream_t to enqueue on; NULL = the legacy default stream */
+  int32_t env;              /* bcts_env_kind */
+  int32_t num_actions;      /* A >= 2 (fixed per handle) */
+  /* TABULAR only (HOST pointers, copied at create): */
+  int32_t num_states;
+  const int32_t *tab_next;  /* [nS*A] next state of (s,a) */
+  const float *tab_reward;  /* [nS*A] r(s,a) */
+  const float *tab_q;       /* [nS*A] Q_hat(s,a) for BCTS_NET_TABLE */
+  /* Nets (HOST pointer, copied/repacked at create; caller may free after): */
+  int32_t net;              /* bcts_net_kind */
+  const float *weights;     /* canonical PyTorch-order fp32 blob (synth.inputs.weight_specs) */
+  int64_t weights_count;    /* number of floats in weights */
+  int32_t mlp_in, mlp_hidden; /* MLP2: 64, hidden (<= 1024) */
+  int32_t atoms;            /* Rainbow atoms (51) */
+  float v_min, v_max;       /* Rainbow support [-10, 10] */
+  int64_t workspace_bytes_max; /* per-call device workspace budget; 0 = auto (16 GiB) */
+  uint32_t flags;           /* BCTS_F_* */
+} bcts_config;
+
+typedef struct {
+  int64_t transitions;     /* env steps executed (n * sum_{k=1..d} A^k on one GPU) */
+  int64_t leaves;          /* leaves scored */
+  int64_t evaluated;       /* net evaluations (leaves + root rows + level-1 rows) */
+  int64_t kernel_launches; /* kernels this call launched */
+  int64_t chunks;          /* leaf chunks the call was split into */
+  int64_t level_launches;  /* expansion-kernel launches */
+} bcts_stats;
+
+/* Create a handle: validates cfg, copies tables, repacks weights into the
+ * device layouts, creates the stream. Errors: INVALID_ARG (bad kinds, A<2,
+ * A>64, wrong weights_count, null required pointers), CUDA, OUT_OF_MEMORY. */
+bcts_status bcts_create(const bcts_config *cfg, bcts_handle *out);
+
+/* NULL-safe. Frees device memory owned by the handle. */
+void bcts_destroy(bcts_handle h);
+
+int32_t bcts_abi_version(void);
+size_t bcts_root_record_bytes(bcts_handle h);
+const char *bcts_status_string(bcts_status s);
+const char *bcts_last_error(bcts_handle h); /* detail for the last failing call on h ("" if none) */
+
+/* Batch-BFS + BCTS for n_roots independent roots (Alg. 1 per root).
+ *   roots        : device, n_roots root records (layout above)
+ *   depth        : d >= 0 (d = 0 -> greedy on Q_hat(s_0,.))
+ *   A            : must equal cfg.num_actions
+ *   gamma        : in (0,1);  beta: finite, >= 0;  correction_on: 0/1
+ *   actions_out  : device int32 [n_roots]      argmax of the (corrected) root Q
+ *   root_q_out   : device float [n_roots * A]  corrected root Q (R14)
+ * Errors: INVALID_ARG, BUDGET, CUDA. n_roots == 0 is a no-op returning OK. */
+bcts_status bcts_search(bcts_handle h, const void *roots, int64_t n_roots, int32_t depth, int32_t A,
+                        float gamma, float beta, int32_t correction_on, int32_t *actions_out,
+                        float *root_q_out);
+
+/* As bcts_search, plus optional (nullable) device outputs:
+ *   vanilla_q_out  float [n*A]  uncorrected d-step Q (Eq. 1)
+ *   terms_out      float [n*4]  (pi_o, delta_o, delta_e, B) (zeros when not computed)
+ *   best_leaf_out  int64 [n*A]  lowest leaf index (within the root) attaining vanilla_q
+ *   stats          HOST bcts_stats* */
+bcts_status bcts_search_ex(bcts_handle h, const void *roots, int64_t n_roots, int32_t depth, int32_t A,
+                           float gamma, float beta, int32_t correction_on, int32_t *actions_out,
+                           float *root_q_out, float *vanilla_q_out, float *terms_out,
+                           int64_t *best_leaf_out, bcts_stats *stats);
+
+/* End-to-end convenience: HOST roots in, HOST outputs out. Copies the roots
+ * host->device, runs bcts_search_ex and copies actions/root_q device->host,
+ * then synchronizes the stream. Same errors as bcts_search. */
+bcts_status bcts_search_host(bcts_handle h, const void *roots_host, int64_t n_roots, int32_t depth,
+                             int32_t A, float gamma, float beta, int32_t correction_on,
+                             int32_t *actions_host, float *root_q_host);
+
+/* ---- sharded search (multi-GPU) --------------------------
+ * The global leaf space of a call is [0, n_roots * A^d); leaf L belongs to
+ * root L / A^d. bcts_search_shard expands only the ancestors of the leaves in
+ * [leaf_begin, leaf_end), scores those leaves and folds each leaf's total into
+ * keys_out[root*A + a0] by max (a0 = root action of the leaf). keys_out is a
+ * device int64 [n_roots * A] that the caller initialises with
+ * bcts_keys_init; a key orders as (value, lowest leaf index) under SIGNED
+ * int64 max, so shards combine with any max all-reduce (ncclMax over
+ * ncclInt64, torch.distributed ReduceOp.MAX). bcts_finalize turns the
+ * reduced keys into the outputs of bcts_search_ex, evaluating the depth-0/1
+ * Bellman terms itself (the same on every rank). */
+bcts_status bcts_keys_init(bcts_handle h, int64_t *keys, int64_t count);
+bcts_status bcts_search_shard(bcts_handle h, const void *roots, int64_t n_roots, int32_t depth, int32_t A,
+                              float gamma, int64_t leaf_begin, int64_t leaf_end, int64_t *keys_out,
+                              bcts_stats *stats);
+bcts_status bcts_finalize(bcts_handle h, const void *roots, int64_t n_roots, int32_t depth, int32_t A,
+                          float gamma, float beta, int32_t correction_on, const int64_t *keys,
+                          int32_t *actions_out, float *root_q_out, float *vanilla_q_out,
+                          float *terms_out, int64_t *best_leaf_out, bcts_stats *stats);
+
+/* ---- inspection entry points (same kernels as the search) -------------
+ * bcts_expand: expand n_roots roots to level `level` (Alg. 1 loop body,
+ * P:318-321) and write the n_roots*A^level level-`level` states as root
+ * records into states_out (device, record layout) and their cumulative
+ * discounted rewards into cum_out (device float). */
+bcts_status bcts_expand(bcts_handle h, const void *roots, int64_t n_roots, int32_t level, int32_t A,
+                        float gamma, void *states_out, float *cum_out);
+
+/* bcts_q_rows: full-row value-net evaluation Q_hat(s, .) for n states given
+ * as root records (device) -> q_out device float [n*A]. */
+bcts_status bcts_q_rows(bcts_handle h, const void *states, int64_t n, float *q_out);
+
+/* ---- profiling (per kernel class, CUDA events on the handle's stream) ----
+ * bcts_profile_enable(h, 1) synchronizes, clears the totals and starts
+ * recording an event pair around every kernel launch; 0 stops. Each launch
+ * also carries its ALGORITHMIC work (unit 0: bytes moved, unit 1: FLOPs;
+ * DESIGN.md §5). bcts_profile_read synchronizes the stream and writes up to
+ * max per-class totals; returns the number written. */
+typedef struct {
+  char name[32];
+  int64_t launches;
+  double ms;    /* summed event durations */
+  double work;  /* summed algorithmic bytes (unit 0) or FLOPs (unit 1) */
+  int32_t unit;
+} bcts_kernel_profile;
+bcts_status bcts_profile_enable(bcts_handle h, int32_t on);
+int32_t bcts_profile_read(bcts_handle h, bcts_kernel_profile *out, int32_t max);
+
+/* Packed-key helpers, exposed for tests of the multi-GPU reduction:
+ * bcts_pack_key(value, leaf) is the int64 key described above. Host-only. */
+int64_t bcts_pack_key(float value, int64_t leaf_index);
+float bcts_key_value(int64_t key);
+int64_t bcts_key_leaf(int64_t key);
+
+/* Shard plan (host-only): the [begin, end) leaf range rank `rank` of `world`
+ * owns for a call over n_roots roots at depth d with A actions. Contiguous,
+ * balanced to within one leaf, aligned to whole roots when n_roots is a
+ * multiple of world (root sharding, C4) and to leaf ranges otherwise (C5). */
+bcts_status bcts_shard_range(int64_t n_roots, int32_t depth, int32_t A, int32_t rank, int32_t world,
+                             int64_t *leaf_begin, int64_t *leaf_end);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BCTS_H_ */

@@ -663,3 +663,58 @@ int oracle_max_threads(void) {
   return 1;
 #endif
 }
+
+/* BCTS terms only (pi_o, delta_o, delta_e, B at depth d) for n roots: needs
+ * just the root row and the A level-1 rows (Prop. 1), so it runs at
+ * full-size configs where the complete DFS would not finish in a test. */
+int oracle_terms(const oracle_model *m, const void *roots, long n_roots, int depth, double gamma, int mode,
+                 double *terms_out, double *q0_out) {
+  const long rb = oracle_record_bytes(m);
+  double g[MAXD + 1];
+  if (depth < 1 || depth > MAXD) return -1;
+  discounts(gamma, depth, g);
+  ostate *root = (ostate *)malloc(sizeof(ostate));
+  int rc = 0;
+  for (long r = 0; r < n_roots && !rc; ++r) {
+    from_record(m, (const uint8_t *)roots + r * rb, root);
+    rc = bcts_terms(m, root, depth, mode, g, terms_out + 4 * r, q0_out + (long)m->A * r);
+  }
+  free(root);
+  return rc;
+}
+
+/* Bounded CPU-baseline sample: the same DFS, restricted to the depth-2
+ * subtrees t in [t_begin, t_end) of one root (t = a0*A + a1), one OpenMP task
+ * per subtree. out[t - t_begin] = max over the subtree's leaves of the leaf
+ * total. Used only to time the oracle on a bounded sample (bench.py). */
+int oracle_search_subtrees(const oracle_model *m, const void *root_rec, int depth, double gamma, int mode,
+                           int threads, long t_begin, long t_end, double *out) {
+  const int A = m->A;
+  if (depth < 2 || depth > MAXD || t_begin < 0 || t_end > (long)A * A || t_end < t_begin) return -1;
+  double g[MAXD + 1];
+  discounts(gamma, depth, g);
+  int err = 0;
+  if (threads < 1) threads = 1;
+#pragma omp parallel for schedule(dynamic, 1) num_threads(threads)
+  for (long t = t_begin; t < t_end; ++t) {
+    dfs_ctx c;
+    c.m = m; c.d = depth; c.mode = mode;
+    memcpy(c.g, g, sizeof(g));
+    c.buf = (ostate *)malloc(sizeof(ostate) * (depth + 1));
+    ostate *mid = (ostate *)malloc(sizeof(ostate));
+    from_record(m, (const uint8_t *)root_rec, &c.buf[0]);
+    double r0, r1, v = 0.0;
+    long lf = 0;
+    int rc = env_step(m, &c.buf[0], (int)(t / A), mid, &r0);
+    if (!rc) rc = env_step(m, mid, (int)(t % A), &c.buf[2], &r1);
+    if (!rc) rc = dfs(&c, 2, acc_reward(mode, g, 1, r1, acc_reward(mode, g, 0, r0, 0.0)), &v, &lf);
+    out[t - t_begin] = v;
+    if (rc) {
+#pragma omp atomic write
+      err = 1;
+    }
+    free(mid);
+    free(c.buf);
+  }
+  return err ? -1 : 0;
+}

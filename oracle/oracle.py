@@ -55,6 +55,10 @@ def _load():
             lib.oracle_bias_gap_eq4.argtypes = [D, D, I, I]
             lib.oracle_bf16_round.restype = D
             lib.oracle_bf16_round.argtypes = [D]
+            lib.oracle_terms.restype = I
+            lib.oracle_terms.argtypes = [P, P, L, I, D, I, P, P]
+            lib.oracle_search_subtrees.restype = I
+            lib.oracle_search_subtrees.argtypes = [P, P, I, D, I, I, L, L, P]
             lib.oracle_max_threads.restype = I
             _lib = lib
     return _lib
@@ -160,6 +164,26 @@ class Oracle:
             raise ValueError("oracle search failed (domain error)")
         return {"actions": act, "root_q": rq.reshape(n, A), "vanilla_q": van.reshape(n, A),
                 "terms": terms.reshape(n, 4), "best_leaf": bl.reshape(n, A)}
+
+    def terms(self, roots, depth: int, gamma: float, mode: int = 0):
+        """(pi_o, delta_o, delta_e, B) per root and the root rows Q_hat(s0, .)."""
+        recs = self._records(roots)
+        n = recs.shape[0]
+        t = np.zeros(n * 4, np.float64)
+        q0 = np.zeros(n * self.A, np.float64)
+        if _load().oracle_terms(self._h, _ptr(recs), n, depth, gamma, mode, _ptr(t), _ptr(q0)):
+            raise ValueError("oracle_terms failed")
+        return t.reshape(n, 4), q0.reshape(n, self.A)
+
+    def subtrees(self, root, depth: int, gamma: float, t_begin: int, t_end: int, mode: int = 0,
+                 threads: int = 1) -> np.ndarray:
+        """Max leaf total of each depth-2 subtree t = a0*A + a1 in [t_begin, t_end) (bounded sample)."""
+        rec = self._records(root)[0]
+        out = np.zeros(max(t_end - t_begin, 1), np.float64)
+        if _load().oracle_search_subtrees(self._h, _ptr(rec), depth, gamma, mode, threads, t_begin, t_end,
+                                          _ptr(out)):
+            raise ValueError("oracle_search_subtrees failed")
+        return out[:t_end - t_begin]
 
     @staticmethod
     def max_threads() -> int:

@@ -1,0 +1,124 @@
+// backup.cu -- K3: segmented max/argmax backup (Alg. 1 return line P:324,
+// Eq. 1) and the BCTS correction + action (Eq. 3, Eq. 5
+// P:276-280, Prop. 1, sweep constant P:371).
+//
+// The backup folds each leaf total into the key of its (root, root action)
+// segment: key = (orderable(total), lowest leaf index). Max over packed keys is
+// exact and associative, so the warp-shuffle reduction + one atomicMax per warp
+// equals the level-by-level max over each node's A children,
+// independent of chunking, launch order and sharding (bit-identical results).
+#include <math.h>
+
+#include "engine.h"
+
+namespace bcts {
+
+__global__ void k_keys_init(int64_t *keys, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) keys[i] = kKeyEmpty;
+}
+
+void launch_keys_init(int64_t *keys, int64_t count, cudaStream_t st) {
+  if (count > 0) k_keys_init<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(keys, count);
+}
+
+__global__ void k_segmax(const float *__restrict__ totals, int64_t n, int64_t leaf_begin, int64_t lpr, int64_t seg,
+                         int A, int64_t *__restrict__ keys) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x % 32;
+  int64_t key = kKeyEmpty, slot = -1;
+  if (i < n) {
+    const int64_t L = leaf_begin + i;
+    const int64_t root = L / lpr;
+    const int64_t within = L - root * lpr;
+    slot = root * A + within / seg;
+    key = pack_key(totals[i], within);
+  }
+  const int64_t s0 = __shfl_sync(0xffffffffu, slot, 0);
+  const bool uniform = __all_sync(0xffffffffu, slot == s0 || slot < 0);
+  if (uniform) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const int64_t other = __shfl_xor_sync(0xffffffffu, key, o);
+      key = other > key ? other : key;
+    }
+    if (lane == 0 && s0 >= 0) atomicMax((long long *)&keys[s0], (long long)key);
+  } else if (slot >= 0) {
+    atomicMax((long long *)&keys[slot], (long long)key);
+  }
+}
+
+void launch_segmax(const float *totals, int64_t n, int64_t leaf_begin, int64_t leaves_per_root, int64_t seg, int A,
+                   int64_t *keys, cudaStream_t st, Profiler *prof) {
+  if (n <= 0) return;
+  if (prof) prof->begin(KC_SEGMAX, 4.0 * (double)n, st);   // algorithmic bytes: one fp32 total per leaf
+  k_segmax<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(totals, n, leaf_begin, leaves_per_root, seg, A, keys);
+  if (prof) prof->end(st);
+}
+
+// One thread per root.
+__global__ void k_finalize(FinalizeArgs f) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= f.n) return;
+  const int A = f.A;
+  float van[kMaxA], q[kMaxA];
+  float terms[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int a = 0; a < A; ++a) {
+    if (f.d == 0) {
+      van[a] = f.q0[r * A + a];
+      if (f.best_leaf) f.best_leaf[r * A + a] = 0;
+    } else {
+      const int64_t k = f.keys[r * A + a];
+      van[a] = key_value(k);
+      if (f.best_leaf) f.best_leaf[r * A + a] = key_leaf(k);
+    }
+    q[a] = van[a];
+  }
+  if (f.d == 0 || f.corr) {
+    int pio = 0;                           // pi_o = lowest argmax of Q_hat(s0, .) (R23)
+    for (int a = 1; a < A; ++a)
+      if (f.q0[r * A + a] > f.q0[r * A + pio]) pio = a;
+    terms[0] = (float)pio;
+    if (f.d >= 1) {
+      // delta_a = fmaf(g1, max_a' Q(s1^a, a'), R1_a) - Q(s0, a)   (Prop. 1; R7)
+      double dob = 0.0, sum = 0.0;
+      for (int a = 0; a < A; ++a) {
+        const float delta = fmaf(f.g1, f.m1[r * A + a], f.r1[r * A + a]) - f.q0[r * A + a];
+        if (a == pio) dob = fabs((double)delta);
+        else sum += fabs((double)delta);
+      }
+      const double de = sum / (double)(A - 1);
+      // Eq. 5 (natural log, R5)
+      double B = sqrt(log((double)A)) * (de * sqrt((double)f.d) - dob * sqrt((double)(f.d - 1))) -
+                 (de - dob) / sqrt(8.0);
+      if (f.clamp && B < 0.0) B = 0.0;
+      terms[1] = (float)dob;
+      terms[2] = (float)de;
+      terms[3] = (float)B;
+      if (f.beta != 0.0f) {                 // Eq. 3: subtract beta*g_d*B from a != pi_o (R9, R12)
+        const double pen = (double)f.beta * (double)f.gd * B;
+        for (int a = 0; a < A; ++a)
+          if (a != pio) q[a] = (float)((double)van[a] - pen);
+      }
+    }
+  }
+  int best = 0;
+  for (int a = 1; a < A; ++a)
+    if (q[a] > q[best]) best = a;          // lowest index attaining the max (R4)
+  f.actions[r] = best;
+  for (int a = 0; a < A; ++a) {
+    f.root_q[r * A + a] = q[a];
+    if (f.vanilla) f.vanilla[r * A + a] = van[a];
+  }
+  if (f.terms)
+    for (int k = 0; k < 4; ++k) f.terms[r * 4 + k] = terms[k];
+}
+
+void launch_finalize(const FinalizeArgs &a, cudaStream_t st, Profiler *prof) {
+  if (a.n <= 0) return;
+  if (prof) prof->begin(KC_FINALIZE, (double)a.n * a.A * 28.0, st);
+  k_finalize<<<(unsigned)((a.n + 127) / 128), 128, 0, st>>>(a);
+  if (prof) prof->end(st);
+}
+
+}  // namespace bcts

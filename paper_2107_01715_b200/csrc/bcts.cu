@@ -1,0 +1,668 @@
+// bcts.cu -- engine (E1) and C-ABI (A1) of the Batch-BFS + BCTS hot path.
+// See include/bcts.h for the contract and DESIGN.md §4-§6 for the design.
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "engine.h"
+
+using namespace bcts;
+
+struct bcts_handle_t {
+  int dev = 0;
+  cudaStream_t st = nullptr;
+  bool own_stream = false;
+  int env = 0, A = 0, nS = 0;
+  uint32_t flags = 0;
+  int32_t *d_next = nullptr;
+  float *d_rew = nullptr;
+  Net net;
+  int64_t ws_max = 0;
+  uint8_t *ws = nullptr;
+  size_t ws_size = 0;
+  // end-to-end (host buffer) staging
+  uint8_t *e2e_roots = nullptr;
+  size_t e2e_roots_size = 0;
+  int32_t *e2e_act = nullptr;
+  float *e2e_q = nullptr;
+  size_t e2e_out = 0;
+  std::string err;
+  int64_t launches = 0;
+  Profiler prof;
+};
+
+namespace {
+
+const int64_t kDefaultWorkspace = 16LL << 30;
+
+int64_t state_bytes(int env) {
+  return env == BCTS_ENV_TABULAR ? 4 : env == BCTS_ENV_INT_HASH ? 64 : kFrameBytes;
+}
+int64_t record_bytes(int env) {
+  return env == BCTS_ENV_TABULAR ? 4 : env == BCTS_ENV_INT_HASH ? 64 : kAtariRecord;
+}
+int64_t node_bytes(int env) { return state_bytes(env) + (env == BCTS_ENV_ATARI_HASH ? 8 : 0) + 4; }
+size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+struct LevelBuf {
+  uint8_t *state = nullptr;
+  uint64_t *key = nullptr;
+  float *cum = nullptr;
+  int64_t cap = 0;
+};
+
+// Bump allocator over the handle's workspace.
+struct Carver {
+  uint8_t *base;
+  size_t off = 0;
+  explicit Carver(uint8_t *b) : base(b) {}
+  void *take(size_t bytes) {
+    void *p = base ? base + off : nullptr;
+    off = align_up(off + bytes);
+    return p;
+  }
+  LevelBuf level(int env, int64_t cap) {
+    LevelBuf b;
+    b.cap = cap;
+    b.state = (uint8_t *)take((size_t)cap * state_bytes(env));
+    if (env == BCTS_ENV_ATARI_HASH) b.key = (uint64_t *)take((size_t)cap * 8);
+    b.cum = (float *)take((size_t)cap * 4);
+    return b;
+  }
+};
+
+NodeView view_of(int env, const LevelBuf &b) {
+  NodeView v;
+  v.state = b.state;
+  v.state_stride = state_bytes(env);
+  v.key = b.key;
+  v.key_stride = 8;
+  v.cum = b.cum;
+  return v;
+}
+NodeOut out_of(int env, const LevelBuf &b) {
+  NodeOut o;
+  o.state = b.state;
+  o.state_stride = state_bytes(env);
+  o.key = b.key;
+  o.cum = b.cum;
+  return o;
+}
+// Level-0 view straight into the caller's root records, starting at root r0.
+NodeView root_view(int env, const void *roots, int64_t r0) {
+  NodeView v;
+  const int64_t rb = record_bytes(env);
+  const uint8_t *base = (const uint8_t *)roots + r0 * rb;
+  v.state = base + (env == BCTS_ENV_ATARI_HASH ? 16 : 0);
+  v.state_stride = rb;
+  if (env == BCTS_ENV_ATARI_HASH) {
+    v.key = (const uint64_t *)base;
+    v.key_stride = rb;
+  }
+  v.cum = nullptr;
+  return v;
+}
+
+bool ipow_ok(int64_t A, int d, int64_t &out) {
+  int64_t v = 1;
+  for (int k = 0; k < d; ++k) {
+    if (v > (INT64_MAX / 4) / A) return false;
+    v *= A;
+  }
+  out = v;
+  return true;
+}
+
+bcts_status fail(bcts_handle h, bcts_status s, const std::string &msg) {
+  if (h) h->err = msg;
+  return s;
+}
+
+bcts_status cuda_check(bcts_handle h, const char *where) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(h, BCTS_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+  return BCTS_OK;
+}
+
+bcts_status ensure_ws(bcts_handle h, size_t bytes) {
+  if (bytes <= h->ws_size) return BCTS_OK;
+  if (h->ws) {
+    cudaStreamSynchronize(h->st);
+    cudaFree(h->ws);
+    h->ws = nullptr;
+    h->ws_size = 0;
+  }
+  if (cudaMalloc(&h->ws, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(h, BCTS_ERR_OUT_OF_MEMORY, "workspace cudaMalloc of " + std::to_string(bytes) + " bytes failed");
+  }
+  h->ws_size = bytes;
+  return BCTS_OK;
+}
+
+void discounts(float gamma, int d, float *g) {
+  double p = 1.0;
+  for (int k = 0; k <= d; ++k) {  // g[k] = (float)(product of k copies of (double)gamma)  (R3)
+    g[k] = (float)p;
+    p *= (double)gamma;
+  }
+}
+
+bcts_status validate(bcts_handle h, const void *roots, int64_t n_roots, int32_t depth, int32_t A, float gamma) {
+  if (!h) return BCTS_ERR_INVALID_ARG;
+  if (A != h->A) return fail(h, BCTS_ERR_INVALID_ARG, "A != num_actions of the handle");
+  if (depth < 0 || depth > kMaxDepth) return fail(h, BCTS_ERR_INVALID_ARG, "depth out of [0, 12]");
+  if (n_roots < 0) return fail(h, BCTS_ERR_INVALID_ARG, "n_roots < 0");
+  if (!(gamma > 0.0f && gamma < 1.0f)) return fail(h, BCTS_ERR_INVALID_ARG, "gamma must be in (0,1) (P:44)");
+  if (n_roots > 0 && !roots) return fail(h, BCTS_ERR_INVALID_ARG, "roots is NULL");
+  int64_t lpr;
+  if (!ipow_ok(A, depth, lpr) || lpr > 0xFFFFFFFFLL)
+    return fail(h, BCTS_ERR_BUDGET, "A^d exceeds 2^32-1 leaves per root");
+  if (n_roots > 0 && lpr > (INT64_MAX / 8) / n_roots) return fail(h, BCTS_ERR_BUDGET, "n_roots * A^d overflows");
+  if (h->env == BCTS_ENV_TABULAR && n_roots > 0) {  // root id domain check (synchronous; toy env only)
+    std::vector<int32_t> ids((size_t)n_roots);
+    if (cudaMemcpyAsync(ids.data(), roots, 4 * (size_t)n_roots, cudaMemcpyDeviceToHost, h->st) != cudaSuccess ||
+        cudaStreamSynchronize(h->st) != cudaSuccess)
+      return cuda_check(h, "root id check");
+    for (int32_t s : ids)
+      if (s < 0 || s >= h->nS) return fail(h, BCTS_ERR_INVALID_ARG, "TABULAR root id outside [0, nS)");
+  }
+  return BCTS_OK;
+}
+
+// Largest leaf chunk (multiple of A) that fits the budget: big level (Lc),
+// small level (Lc/A + 2), leaf totals (Lc).
+int64_t plan_chunk(bcts_handle h, int64_t range, size_t reserved) {
+  const int64_t nb = node_bytes(h->env);
+  const int64_t budget = h->ws_max - (int64_t)reserved - (1 << 20);
+  if (budget <= 0) return 0;
+  int64_t lc = (int64_t)((double)budget / ((double)nb * (1.0 + 1.0 / h->A) + 4.0));
+  lc -= 2 * h->A;
+  lc = lc / h->A * h->A;
+  const int64_t need = (range + h->A - 1) / h->A * h->A;
+  return std::min(lc, need);
+}
+
+size_t chunk_bytes(bcts_handle h, int64_t lc) {
+  Carver c(nullptr);
+  c.level(h->env, lc);
+  c.level(h->env, lc / h->A + 2);
+  c.take((size_t)lc * 4);
+  return c.off;
+}
+
+// Workspace the shard phase needs (after `reserved` bytes).
+size_t shard_ws(bcts_handle h, int64_t range, size_t reserved) {
+  const int64_t lc = plan_chunk(h, range, reserved);
+  return lc < h->A ? 0 : chunk_bytes(h, lc);
+}
+// Roots per prologue step and the workspace the finalize phase needs.
+int64_t prologue_per(bcts_handle h, int64_t n, size_t reserved) {
+  int64_t per = std::max<int64_t>(1, plan_chunk(h, n * h->A, reserved) / h->A);
+  return std::min(per, n);
+}
+size_t finalize_ws(bcts_handle h, int64_t n, size_t reserved) {
+  Carver c(nullptr);
+  c.take((size_t)n * h->A * 4 * 3);
+  const size_t base = c.off;
+  c.level(h->env, prologue_per(h, n, reserved + base) * h->A);
+  return c.off;
+}
+
+// Leaf-range search: expand the ancestors of leaves [L0, L1), score the leaves,
+// fold the totals into keys (K1 -> K2 -> K3a per chunk).
+bcts_status run_shard(bcts_handle h, const void *roots, int32_t d, float gamma, int64_t L0, int64_t L1,
+                      int64_t *keys, size_t reserved, bcts_stats *stats) {
+  const int A = h->A;
+  if (L1 <= L0 || d < 1) return BCTS_OK;
+  float g[kMaxDepth + 1];
+  discounts(gamma, d, g);
+  int64_t pw[kMaxDepth + 1];
+  pw[0] = 1;
+  for (int k = 1; k <= d; ++k) pw[k] = pw[k - 1] * A;
+  const int64_t lc = plan_chunk(h, L1 - L0, reserved);
+  if (lc < A) return fail(h, BCTS_ERR_BUDGET, "workspace budget too small for one chunk of leaves");
+  if (reserved + chunk_bytes(h, lc) > h->ws_size) return fail(h, BCTS_ERR_BUDGET, "workspace not sized");
+  bcts_status s = BCTS_OK;
+  Carver c(h->ws + reserved);
+  LevelBuf big = c.level(h->env, lc), small = c.level(h->env, lc / A + 2);
+  float *totals = (float *)c.take((size_t)lc * 4);
+  int64_t nchunks = 0, trans = 0, lvl_launch = 0;
+  for (int64_t L = L0; L < L1; L += lc) {
+    const int64_t Le = std::min(L1, L + lc);
+    int64_t lo[kMaxDepth + 1], hi[kMaxDepth + 1];
+    for (int k = 0; k <= d; ++k) {
+      lo[k] = L / pw[d - k];
+      hi[k] = (Le - 1) / pw[d - k] + 1;
+    }
+    NodeView prev = root_view(h->env, roots, lo[0]);
+    for (int k = 1; k <= d; ++k) {
+      const LevelBuf &b = ((d - k) % 2 == 0) ? big : small;
+      launch_expand(h->env, prev, lo[k - 1], lo[k], hi[k], A, g[k - 1], h->d_next, h->d_rew, out_of(h->env, b),
+                    h->st, &h->prof);
+      prev = view_of(h->env, b);
+      trans += hi[k] - lo[k];
+      ++lvl_launch;
+    }
+    const int nl = net_eval(h->net, prev, Le - L, MODE_TOTAL, g[d], totals, h->st);
+    launch_segmax(totals, Le - L, L, pw[d], pw[d - 1], A, keys, h->st, &h->prof);
+    h->launches += d + nl + 1;
+    ++nchunks;
+    if ((s = cuda_check(h, "shard chunk"))) return s;
+  }
+  if (stats) {
+    stats->transitions += trans;
+    stats->leaves += L1 - L0;
+    stats->evaluated += L1 - L0;
+    stats->chunks += nchunks;
+    stats->level_launches += lvl_launch;
+  }
+  return BCTS_OK;
+}
+
+// Depth-0/1 quantities for the BCTS terms (Prop. 1; R7):
+// q0 = Q_hat(s0, .), m1[a] = max Q_hat(s1^a, .), r1[a] = R_1 of child a.
+bcts_status run_prologue(bcts_handle h, const void *roots, int64_t n, float gamma, bool need_level1, float *q0,
+                         float *m1, float *r1, size_t reserved, bcts_stats *stats) {
+  const int A = h->A;
+  int nl = net_eval(h->net, root_view(h->env, roots, 0), n, MODE_ROWS, 0.0f, q0, h->st);
+  h->launches += nl;
+  if (stats) stats->evaluated += n;
+  if (!need_level1) return cuda_check(h, "prologue");
+  float g[2];
+  discounts(gamma, 1, g);
+  const int64_t per = prologue_per(h, n, reserved);
+  Carver cc(h->ws + reserved);
+  LevelBuf b = cc.level(h->env, per * A);
+  for (int64_t r0 = 0; r0 < n; r0 += per) {
+    const int64_t r1e = std::min(n, r0 + per);
+    const int64_t cnt = (r1e - r0) * A;
+    launch_expand(h->env, root_view(h->env, roots, r0), r0, r0 * A, r1e * A, A, g[0], h->d_next, h->d_rew,
+                  out_of(h->env, b), h->st, &h->prof);
+    nl = net_eval(h->net, view_of(h->env, b), cnt, MODE_ROWMAX, 0.0f, m1 + r0 * A, h->st);
+    cudaMemcpyAsync(r1 + r0 * A, b.cum, (size_t)cnt * 4, cudaMemcpyDeviceToDevice, h->st);
+    h->launches += 1 + nl;
+    if (stats) {
+      stats->evaluated += cnt;
+      stats->transitions += cnt;
+    }
+  }
+  return cuda_check(h, "prologue");
+}
+
+struct Outs {
+  int32_t *actions;
+  float *root_q, *vanilla, *terms;
+  int64_t *best_leaf;
+};
+
+bcts_status finalize_impl(bcts_handle h, const void *roots, int64_t n, int32_t d, float gamma, float beta,
+                          int32_t corr, const int64_t *keys, const Outs &o, size_t reserved, bcts_stats *stats) {
+  const int A = h->A;
+  const bool need_q0 = corr || d == 0;
+  bcts_status s = BCTS_OK;
+  Carver cc(h->ws + reserved);
+  float *q0 = (float *)cc.take((size_t)n * A * 4);
+  float *m1 = (float *)cc.take((size_t)n * A * 4);
+  float *r1 = (float *)cc.take((size_t)n * A * 4);
+  if (need_q0) {
+    s = run_prologue(h, roots, n, gamma, corr && d >= 1, q0, m1, r1, reserved + cc.off, stats);
+    if (s) return s;
+  }
+  float g[kMaxDepth + 1];
+  discounts(gamma, d, g);
+  FinalizeArgs f;
+  f.n = n; f.A = A; f.d = d; f.corr = corr; f.clamp = (h->flags & BCTS_F_CLAMP_PENALTY) ? 1 : 0;
+  f.beta = beta; f.g1 = d >= 1 ? g[1] : 0.0f; f.gd = g[d];
+  f.keys = keys; f.q0 = q0; f.m1 = m1; f.r1 = r1;
+  f.actions = o.actions; f.root_q = o.root_q; f.vanilla = o.vanilla; f.terms = o.terms; f.best_leaf = o.best_leaf;
+  launch_finalize(f, h->st, &h->prof);
+  h->launches += 1;
+  return cuda_check(h, "finalize");
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+int32_t bcts_abi_version(void) { return BCTS_ABI_VERSION; }
+
+const char *bcts_status_string(bcts_status s) {
+  switch (s) {
+    case BCTS_OK: return "BCTS_OK";
+    case BCTS_ERR_INVALID_ARG: return "BCTS_ERR_INVALID_ARG";
+    case BCTS_ERR_UNSUPPORTED: return "BCTS_ERR_UNSUPPORTED";
+    case BCTS_ERR_OUT_OF_MEMORY: return "BCTS_ERR_OUT_OF_MEMORY";
+    case BCTS_ERR_BUDGET: return "BCTS_ERR_BUDGET";
+    case BCTS_ERR_CUDA: return "BCTS_ERR_CUDA";
+    case BCTS_ERR_NUMERIC: return "BCTS_ERR_NUMERIC";
+  }
+  return "BCTS_ERR_UNKNOWN";
+}
+
+const char *bcts_last_error(bcts_handle h) { return h ? h->err.c_str() : "null handle"; }
+
+size_t bcts_root_record_bytes(bcts_handle h) { return h ? (size_t)record_bytes(h->env) : 0; }
+
+void bcts_destroy(bcts_handle h) {
+  if (!h) return;
+  cudaSetDevice(h->dev);
+  if (h->st) cudaStreamSynchronize(h->st);
+  net_free(h->net);
+  cudaFree(h->d_next);
+  cudaFree(h->d_rew);
+  cudaFree(h->ws);
+  cudaFree(h->e2e_roots);
+  cudaFree(h->e2e_act);
+  cudaFree(h->e2e_q);
+  if (h->own_stream && h->st) cudaStreamDestroy(h->st);
+  delete h;
+}
+
+bcts_status bcts_create(const bcts_config *cfg, bcts_handle *out) {
+  if (!cfg || !out) return BCTS_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (cfg->abi_version != BCTS_ABI_VERSION) return BCTS_ERR_INVALID_ARG;
+  if (cfg->num_actions < 2 || cfg->num_actions > kMaxA) return BCTS_ERR_INVALID_ARG;
+  const bool env_ok = cfg->env == BCTS_ENV_TABULAR || cfg->env == BCTS_ENV_INT_HASH || cfg->env == BCTS_ENV_ATARI_HASH;
+  if (!env_ok) return BCTS_ERR_INVALID_ARG;
+  const bool pair_ok = (cfg->env == BCTS_ENV_TABULAR && cfg->net == BCTS_NET_TABLE) ||
+                       (cfg->env == BCTS_ENV_INT_HASH && cfg->net == BCTS_NET_MLP2_F32) ||
+                       (cfg->env == BCTS_ENV_ATARI_HASH &&
+                        (cfg->net == BCTS_NET_NATURE_BF16 || cfg->net == BCTS_NET_RAINBOW_BF16));
+  if (!pair_ok) return BCTS_ERR_UNSUPPORTED;
+  if (cfg->env == BCTS_ENV_TABULAR) {
+    if (cfg->num_states <= 0 || !cfg->tab_next || !cfg->tab_reward || !cfg->tab_q) return BCTS_ERR_INVALID_ARG;
+    for (int64_t i = 0; i < (int64_t)cfg->num_states * cfg->num_actions; ++i)
+      if (cfg->tab_next[i] < 0 || cfg->tab_next[i] >= cfg->num_states) return BCTS_ERR_INVALID_ARG;
+  }
+  bcts_handle h = new (std::nothrow) bcts_handle_t();
+  if (!h) return BCTS_ERR_OUT_OF_MEMORY;
+  h->dev = cfg->device;
+  h->env = cfg->env;
+  h->A = cfg->num_actions;
+  h->nS = cfg->num_states;
+  h->flags = cfg->flags;
+  h->ws_max = cfg->workspace_bytes_max > 0 ? cfg->workspace_bytes_max : kDefaultWorkspace;
+  if (cudaSetDevice(cfg->device) != cudaSuccess) {
+    cudaGetLastError();
+    delete h;
+    return BCTS_ERR_CUDA;
+  }
+  // NULL is the legacy default stream (CUDA's stream 0), which is also what
+  // torch.cuda.current_stream() reports as 0: calls then order with torch's work.
+  h->st = (cudaStream_t)cfg->cuda_stream;
+  if (cfg->env == BCTS_ENV_TABULAR) {
+    const size_t cnt = (size_t)cfg->num_states * cfg->num_actions;
+    if (cudaMalloc(&h->d_next, cnt * 4) != cudaSuccess || cudaMalloc(&h->d_rew, cnt * 4) != cudaSuccess ||
+        cudaMemcpy(h->d_next, cfg->tab_next, cnt * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(h->d_rew, cfg->tab_reward, cnt * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+      cudaGetLastError();
+      bcts_destroy(h);
+      return BCTS_ERR_CUDA;
+    }
+  }
+  std::string err;
+  if (net_build(h->net, *cfg, err)) {
+    cudaGetLastError();
+    bcts_destroy(h);
+    return BCTS_ERR_INVALID_ARG;
+  }
+  h->net.tc = !(cfg->flags & BCTS_F_SIMT_NET);
+  h->net.prof = &h->prof;
+  *out = h;
+  return BCTS_OK;
+}
+
+bcts_status bcts_keys_init(bcts_handle h, int64_t *keys, int64_t count) {
+  if (!h || count < 0 || (count > 0 && !keys)) return BCTS_ERR_INVALID_ARG;
+  cudaSetDevice(h->dev);
+  launch_keys_init(keys, count, h->st);
+  h->launches += count > 0;
+  return cuda_check(h, "keys_init");
+}
+
+bcts_status bcts_search_shard(bcts_handle h, const void *roots, int64_t n_roots, int32_t depth, int32_t A,
+                              float gamma, int64_t leaf_begin, int64_t leaf_end, int64_t *keys_out,
+                              bcts_stats *stats) {
+  bcts_status s = validate(h, roots, n_roots, depth, A, gamma);
+  if (s) return s;
+  int64_t lpr;
+  ipow_ok(A, depth, lpr);
+  if (depth < 1) return fail(h, BCTS_ERR_INVALID_ARG, "shard search needs depth >= 1");
+  if (leaf_begin < 0 || leaf_end < leaf_begin || leaf_end > n_roots * lpr)
+    return fail(h, BCTS_ERR_INVALID_ARG, "leaf range outside [0, n_roots*A^d)");
+  if (leaf_end > leaf_begin && !keys_out) return fail(h, BCTS_ERR_INVALID_ARG, "keys_out is NULL");
+  cudaSetDevice(h->dev);
+  if (stats) memset(stats, 0, sizeof(*stats));
+  const int64_t l0 = h->launches;
+  if (leaf_end > leaf_begin) {
+    const size_t need = shard_ws(h, leaf_end - leaf_begin, 0);
+    if (!need) return fail(h, BCTS_ERR_BUDGET, "workspace budget too small for one chunk of leaves");
+    if ((s = ensure_ws(h, need))) return s;
+  }
+  s = run_shard(h, roots, depth, gamma, leaf_begin, leaf_end, keys_out, 0, stats);
+  if (stats) stats->kernel_launches = h->launches - l0;
+  return s;
+}
+
+bcts_status bcts_finalize(bcts_handle h, const void *roots, int64_t n_roots, int32_t depth, int32_t A, float gamma,
+                          float beta, int32_t correction_on, const int64_t *keys, int32_t *actions_out,
+                          float *root_q_out, float *vanilla_q_out, float *terms_out, int64_t *best_leaf_out,
+                          bcts_stats *stats) {
+  bcts_status s = validate(h, roots, n_roots, depth, A, gamma);
+  if (s) return s;
+  if (!isfinite(beta) || beta < 0.0f) return fail(h, BCTS_ERR_INVALID_ARG, "beta must be finite and >= 0");
+  if (correction_on != 0 && correction_on != 1) return fail(h, BCTS_ERR_INVALID_ARG, "correction_on not 0/1");
+  if (n_roots == 0) return BCTS_OK;
+  if (!actions_out || !root_q_out || (depth >= 1 && !keys))
+    return fail(h, BCTS_ERR_INVALID_ARG, "NULL required pointer");
+  cudaSetDevice(h->dev);
+  const int64_t l0 = h->launches;
+  Outs o{actions_out, root_q_out, vanilla_q_out, terms_out, best_leaf_out};
+  if ((s = ensure_ws(h, finalize_ws(h, n_roots, 0)))) return s;
+  s = finalize_impl(h, roots, n_roots, depth, gamma, beta, correction_on, keys, o, 0, stats);
+  if (stats) stats->kernel_launches += h->launches - l0;
+  return s;
+}
+
+bcts_status bcts_search_ex(bcts_handle h, const void *roots, int64_t n_roots, int32_t depth, int32_t A, float gamma,
+                           float beta, int32_t correction_on, int32_t *actions_out, float *root_q_out,
+                           float *vanilla_q_out, float *terms_out, int64_t *best_leaf_out, bcts_stats *stats) {
+  bcts_status s = validate(h, roots, n_roots, depth, A, gamma);
+  if (s) return s;
+  if (!isfinite(beta) || beta < 0.0f) return fail(h, BCTS_ERR_INVALID_ARG, "beta must be finite and >= 0");
+  if (correction_on != 0 && correction_on != 1) return fail(h, BCTS_ERR_INVALID_ARG, "correction_on not 0/1");
+  if (n_roots > 0 && (!actions_out || !root_q_out)) return fail(h, BCTS_ERR_INVALID_ARG, "NULL output pointer");
+  if (stats) memset(stats, 0, sizeof(*stats));
+  if (n_roots == 0) return BCTS_OK;
+  cudaSetDevice(h->dev);
+  const int64_t l0 = h->launches;
+  int64_t lpr;
+  ipow_ok(A, depth, lpr);
+  // keys live at the front of the workspace; the shard and finalize phases
+  // reuse the space after them (stream-ordered). Size everything up front.
+  const size_t kbytes = align_up((size_t)n_roots * A * 8);
+  size_t need = finalize_ws(h, n_roots, kbytes);
+  if (depth >= 1) {
+    const size_t sw = shard_ws(h, n_roots * lpr, kbytes);
+    if (!sw) return fail(h, BCTS_ERR_BUDGET, "workspace budget too small for one chunk of leaves");
+    need = std::max(need, sw);
+  }
+  if ((s = ensure_ws(h, kbytes + need))) return s;
+  int64_t *keys = (int64_t *)h->ws;
+  if (depth >= 1) {
+    launch_keys_init(keys, n_roots * A, h->st);
+    h->launches += 1;
+    s = run_shard(h, roots, depth, gamma, 0, n_roots * lpr, keys, kbytes, stats);
+    if (s) return s;
+  }
+  Outs o{actions_out, root_q_out, vanilla_q_out, terms_out, best_leaf_out};
+  s = finalize_impl(h, roots, n_roots, depth, gamma, beta, correction_on, keys, o, kbytes, stats);
+  if (stats) stats->kernel_launches = h->launches - l0;
+  return s;
+}
+
+bcts_status bcts_search(bcts_handle h, const void *roots, int64_t n_roots, int32_t depth, int32_t A, float gamma,
+                        float beta, int32_t correction_on, int32_t *actions_out, float *root_q_out) {
+  return bcts_search_ex(h, roots, n_roots, depth, A, gamma, beta, correction_on, actions_out, root_q_out, nullptr,
+                        nullptr, nullptr, nullptr);
+}
+
+bcts_status bcts_search_host(bcts_handle h, const void *roots_host, int64_t n_roots, int32_t depth, int32_t A,
+                             float gamma, float beta, int32_t correction_on, int32_t *actions_host,
+                             float *root_q_host) {
+  if (!h) return BCTS_ERR_INVALID_ARG;
+  if (n_roots < 0 || (n_roots > 0 && (!roots_host || !actions_host || !root_q_host)))
+    return fail(h, BCTS_ERR_INVALID_ARG, "NULL host pointer or n_roots < 0");
+  if (n_roots == 0) return BCTS_OK;
+  cudaSetDevice(h->dev);
+  const size_t rb = (size_t)n_roots * record_bytes(h->env);
+  if (rb > h->e2e_roots_size) {
+    cudaFree(h->e2e_roots);
+    h->e2e_roots = nullptr;
+    if (cudaMalloc(&h->e2e_roots, rb) != cudaSuccess) {
+      cudaGetLastError();
+      h->e2e_roots_size = 0;
+      return fail(h, BCTS_ERR_OUT_OF_MEMORY, "e2e roots buffer");
+    }
+    h->e2e_roots_size = rb;
+  }
+  if ((size_t)n_roots * A > h->e2e_out) {
+    cudaFree(h->e2e_act);
+    cudaFree(h->e2e_q);
+    if (cudaMalloc(&h->e2e_act, (size_t)n_roots * 4) != cudaSuccess ||
+        cudaMalloc(&h->e2e_q, (size_t)n_roots * A * 4) != cudaSuccess) {
+      cudaGetLastError();
+      h->e2e_out = 0;
+      return fail(h, BCTS_ERR_OUT_OF_MEMORY, "e2e output buffers");
+    }
+    h->e2e_out = (size_t)n_roots * A;
+  }
+  if (cudaMemcpyAsync(h->e2e_roots, roots_host, rb, cudaMemcpyHostToDevice, h->st) != cudaSuccess)
+    return cuda_check(h, "e2e H2D");
+  bcts_status s = bcts_search(h, h->e2e_roots, n_roots, depth, A, gamma, beta, correction_on, h->e2e_act, h->e2e_q);
+  if (s) return s;
+  cudaMemcpyAsync(actions_host, h->e2e_act, (size_t)n_roots * 4, cudaMemcpyDeviceToHost, h->st);
+  cudaMemcpyAsync(root_q_host, h->e2e_q, (size_t)n_roots * A * 4, cudaMemcpyDeviceToHost, h->st);
+  if (cudaStreamSynchronize(h->st) != cudaSuccess) return cuda_check(h, "e2e sync");
+  return cuda_check(h, "e2e D2H");
+}
+
+bcts_status bcts_expand(bcts_handle h, const void *roots, int64_t n_roots, int32_t level, int32_t A, float gamma,
+                        void *states_out, float *cum_out) {
+  bcts_status s = validate(h, roots, n_roots, level, A, gamma);
+  if (s) return s;
+  if (n_roots == 0) return BCTS_OK;
+  if (!states_out || !cum_out) return fail(h, BCTS_ERR_INVALID_ARG, "NULL output pointer");
+  cudaSetDevice(h->dev);
+  const int env = h->env;
+  const int64_t rb = record_bytes(env);
+  int64_t cnt;
+  ipow_ok(A, level, cnt);
+  cnt *= n_roots;
+  if (level == 0) {
+    cudaMemcpyAsync(states_out, roots, (size_t)(n_roots * rb), cudaMemcpyDeviceToDevice, h->st);
+    cudaMemsetAsync(cum_out, 0, (size_t)n_roots * 4, h->st);
+    return cuda_check(h, "expand level 0");
+  }
+  Carver c(nullptr);
+  c.level(env, cnt);
+  c.level(env, cnt / A);
+  if ((int64_t)c.off > h->ws_max) return fail(h, BCTS_ERR_BUDGET, "level does not fit the workspace budget");
+  if ((s = ensure_ws(h, c.off))) return s;
+  Carver cc(h->ws);
+  LevelBuf big = cc.level(env, cnt), small = cc.level(env, cnt / A);
+  float g[kMaxDepth + 1];
+  discounts(gamma, level, g);
+  NodeView prev = root_view(env, roots, 0);
+  int64_t n_prev = n_roots;
+  for (int k = 1; k <= level; ++k) {
+    const LevelBuf &b = ((level - k) % 2 == 0) ? big : small;
+    launch_expand(env, prev, 0, 0, n_prev * A, A, g[k - 1], h->d_next, h->d_rew, out_of(env, b), h->st);
+    prev = view_of(env, b);
+    n_prev *= A;
+    h->launches += 1;
+  }
+  uint8_t *dst = (uint8_t *)states_out;
+  if (env == BCTS_ENV_ATARI_HASH) {
+    cudaMemcpy2DAsync(dst, rb, big.key, 8, 8, cnt, cudaMemcpyDeviceToDevice, h->st);
+    cudaMemset2DAsync(dst + 8, rb, 0, 8, cnt, h->st);
+    cudaMemcpy2DAsync(dst + 16, rb, big.state, kFrameBytes, kFrameBytes, cnt, cudaMemcpyDeviceToDevice, h->st);
+  } else {
+    cudaMemcpyAsync(dst, big.state, (size_t)(cnt * rb), cudaMemcpyDeviceToDevice, h->st);
+  }
+  cudaMemcpyAsync(cum_out, big.cum, (size_t)cnt * 4, cudaMemcpyDeviceToDevice, h->st);
+  return cuda_check(h, "expand");
+}
+
+bcts_status bcts_q_rows(bcts_handle h, const void *states, int64_t n, float *q_out) {
+  if (!h || n < 0 || (n > 0 && (!states || !q_out))) return BCTS_ERR_INVALID_ARG;
+  if (n == 0) return BCTS_OK;
+  cudaSetDevice(h->dev);
+  h->launches += net_eval(h->net, root_view(h->env, states, 0), n, MODE_ROWS, 0.0f, q_out, h->st);
+  return cuda_check(h, "q_rows");
+}
+
+bcts_status bcts_profile_enable(bcts_handle h, int32_t on) {
+  if (!h) return BCTS_ERR_INVALID_ARG;
+  cudaSetDevice(h->dev);
+  cudaStreamSynchronize(h->st);
+  h->prof.reset();
+  h->prof.on = on != 0;
+  return cuda_check(h, "profile_enable");
+}
+
+int32_t bcts_profile_read(bcts_handle h, bcts_kernel_profile *out, int32_t max) {
+  static const char *names[KC_COUNT] = {"expand_atari", "expand_int", "expand_tabular", "conv1", "conv2", "conv3",
+                                        "fc_hidden", "fc_out", "head", "mlp", "table", "segmax", "finalize", "other"};
+  static const int units[KC_COUNT] = {0, 0, 0, 1, 1, 1, 1, 1, 0, 1, 0, 0, 0, 0};
+  if (!h || !out || max <= 0) return 0;
+  cudaSetDevice(h->dev);
+  cudaStreamSynchronize(h->st);
+  h->prof.collect();
+  int32_t k = 0;
+  for (int c = 0; c < KC_COUNT && k < max; ++c) {
+    if (!h->prof.launches[c]) continue;
+    memset(&out[k], 0, sizeof(out[k]));
+    strncpy(out[k].name, names[c], sizeof(out[k].name) - 1);
+    out[k].launches = h->prof.launches[c];
+    out[k].ms = h->prof.ms[c];
+    out[k].work = h->prof.work[c];
+    out[k].unit = units[c];
+    ++k;
+  }
+  return k;
+}
+
+int64_t bcts_pack_key(float value, int64_t leaf_index) { return pack_key(value, leaf_index); }
+float bcts_key_value(int64_t key) { return key_value(key); }
+int64_t bcts_key_leaf(int64_t key) { return key_leaf(key); }
+
+bcts_status bcts_shard_range(int64_t n_roots, int32_t depth, int32_t A, int32_t rank, int32_t world,
+                             int64_t *leaf_begin, int64_t *leaf_end) {
+  if (n_roots < 0 || depth < 0 || depth > kMaxDepth || A < 2 || world < 1 || rank < 0 || rank >= world ||
+      !leaf_begin || !leaf_end)
+    return BCTS_ERR_INVALID_ARG;
+  int64_t lpr;
+  if (!ipow_ok(A, depth, lpr)) return BCTS_ERR_BUDGET;
+  if (n_roots > 0 && lpr > (INT64_MAX / 8) / n_roots) return BCTS_ERR_BUDGET;
+  if (n_roots % world == 0) {  // whole roots per rank (C4)
+    const int64_t per = n_roots / world;
+    *leaf_begin = rank * per * lpr;
+    *leaf_end = (rank + 1) * per * lpr;
+  } else {                     // balanced contiguous leaf ranges (C5)
+    const __int128 total = (__int128)n_roots * lpr;
+    *leaf_begin = (int64_t)(total * rank / world);
+    *leaf_end = (int64_t)(total * (rank + 1) / world);
+  }
+  return BCTS_OK;
+}
+
+}  // extern "C"

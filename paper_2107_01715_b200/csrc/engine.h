@@ -1,0 +1,155 @@
+// engine.h -- internal interfaces between the C-ABI/engine and the kernels.
+#pragma once
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace bcts {
+
+// ---------------------------------------------------------------- profiler
+// Per-kernel-class CUDA-event timing, enabled with bcts_profile_enable. Each
+// record carries the ALGORITHMIC work of its launch (bytes or FLOPs,
+// DESIGN.md §5) so bench.py can report achieved = work / duration.
+enum KernelClass {
+  KC_EXPAND_ATARI = 0, KC_EXPAND_INT, KC_EXPAND_TAB, KC_CONV1, KC_CONV2, KC_CONV3, KC_FC_H, KC_FC_OUT, KC_HEAD,
+  KC_MLP, KC_TABLE, KC_SEGMAX, KC_FINALIZE, KC_OTHER, KC_COUNT
+};
+struct Profiler {
+  bool on = false;
+  struct Rec {
+    int cls;
+    cudaEvent_t a, b;
+    double work;
+  };
+  std::vector<Rec> pending;
+  std::vector<cudaEvent_t> pool;
+  double ms[KC_COUNT] = {}, work[KC_COUNT] = {};
+  int64_t launches[KC_COUNT] = {};
+  cudaEvent_t get() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  void begin(int cls, double w, cudaStream_t st) {
+    if (!on) return;
+    Rec r{cls, get(), get(), w};
+    cudaEventRecord(r.a, st);
+    pending.push_back(r);
+  }
+  void end(cudaStream_t st) {
+    if (!on || pending.empty()) return;
+    cudaEventRecord(pending.back().b, st);
+  }
+  // Fold completed records into the totals (caller synchronizes first).
+  void collect() {
+    for (auto &r : pending) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, r.a, r.b);
+      ms[r.cls] += t;
+      work[r.cls] += r.work;
+      launches[r.cls] += 1;
+      pool.push_back(r.a);
+      pool.push_back(r.b);
+    }
+    pending.clear();
+  }
+  void reset() {
+    collect();
+    for (int i = 0; i < KC_COUNT; ++i) ms[i] = work[i] = 0, launches[i] = 0;
+  }
+  ~Profiler() {
+    for (auto &r : pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+};
+
+// ---------------------------------------------------------------- K1 expand
+// Expand parents (global level-k indices starting at p_first, view `par`) into
+// the children with global level-(k+1) indices [c_begin, c_end):
+// child c has parent c / A and action c % A (R1); R' = fmaf(gk, r, R).
+void launch_expand(int env, const NodeView &par, int64_t p_first, int64_t c_begin, int64_t c_end, int A,
+                   float gk, const int32_t *tab_next, const float *tab_rew, const NodeOut &out,
+                   cudaStream_t st, Profiler *prof = nullptr);
+
+// -------------------------------------------------------- implicit-GEMM layer
+// out[m][n] = act( sum_k X[m][k] * W[n][k] + b[n] ), X gathered im2col-style
+// from an NHWC input (k = (ky, kx, c)); used for every conv and fc layer.
+struct Layer {
+  int in_u8 = 0;            // 1: uint8 input (frames, C=4 packed per pixel word); 0: bf16
+  int64_t in_img_stride = 0;  // elements between images (bytes for u8)
+  int in_col_off = 0;       // element offset inside an image (fc on a column slice)
+  int H = 1, W = 1, C = 0;  // input geometry
+  int KH = 1, KW = 1, S = 1, OH = 1, OW = 1;
+  int K = 0;                // KH*KW*C
+  int N = 0, Npad = 0;      // true / padded output width (rows >= N of W are zero)
+  const __nv_bfloat16 *Wt = nullptr;  // [Npad][K], k = (ky, kx, c)
+  const float *bias = nullptr;        // [Npad]
+  int relu_bf16 = 1;        // 1: ReLU then bf16 RNE store; 0: fp32 store
+  int64_t out_ld = 0;       // elements per output row
+  int64_t rows_per_img() const { return (int64_t)OH * OW; }
+};
+
+// Net output modes.
+enum { MODE_ROWS = 0, MODE_ROWMAX = 1, MODE_TOTAL = 2 };
+
+struct Net {
+  int kind = 0, A = 0;
+  // TABLE
+  const float *tq = nullptr;
+  int nS = 0;
+  // MLP2
+  const float *l1w = nullptr, *l1b = nullptr, *l2w = nullptr, *l2b = nullptr;
+  int in = 0, hid = 0;
+  // conv nets
+  Layer c1, c2, c3, fc_h, z_v, z_a, fc2;
+  int atoms = 51;
+  float vmin = -10.f, vmax = 10.f;
+  // scratch for a sub-batch of `batch` images
+  int64_t batch = 0;
+  __nv_bfloat16 *act1 = nullptr, *act2 = nullptr, *act3 = nullptr, *hid_act = nullptr;
+  float *zv = nullptr, *za = nullptr;
+  int64_t ld_za = 0, ld_zv = 0;
+  bool tc = false;          // tensor-core (tcgen05) layers available + enabled
+  Profiler *prof = nullptr;
+  std::vector<void *> allocs;
+};
+
+// Evaluate Q_hat on n nodes of view v. MODE_ROWS: out[n*A]; MODE_ROWMAX:
+// out[n] = max_a Q; MODE_TOTAL: out[n] = fmaf(gd, max_a Q, cum[i]).
+// Returns the number of kernels launched, or -1 on a CUDA error.
+int net_eval(Net &net, const NodeView &v, int64_t n, int mode, float gd, float *out, cudaStream_t st);
+int net_build(Net &net, const bcts_config &cfg, std::string &err);  // 0 ok
+void net_free(Net &net);
+
+// tcgen05 layer (qnet_tc.cu); returns false if the layer shape is unsupported.
+bool tc_supported(const Layer &L);
+void launch_layer_tc(const Layer &L, const void *in, int64_t n_img, void *out, cudaStream_t st);
+void launch_layer_simt(const Layer &L, const void *in, int64_t n_img, void *out, cudaStream_t st);
+
+// ---------------------------------------------------------------- K3 backup
+void launch_keys_init(int64_t *keys, int64_t count, cudaStream_t st);
+// Fold leaf totals of global leaves [leaf_begin, leaf_begin+n) into keys by
+// max; leaves_per_root = A^d, seg = A^(d-1).
+void launch_segmax(const float *totals, int64_t n, int64_t leaf_begin, int64_t leaves_per_root, int64_t seg,
+                   int A, int64_t *keys, cudaStream_t st, Profiler *prof = nullptr);
+struct FinalizeArgs {
+  int64_t n = 0;
+  int A = 0, d = 0, corr = 0, clamp = 0;
+  float beta = 0.f, g1 = 0.f, gd = 0.f;
+  const int64_t *keys = nullptr;  // [n*A] (d >= 1)
+  const float *q0 = nullptr;      // [n*A] root rows (corr or d == 0)
+  const float *m1 = nullptr;      // [n*A] max_a Q_hat(s_1^a, .) (corr, d >= 1)
+  const float *r1 = nullptr;      // [n*A] R_1 of the root's children (corr, d >= 1)
+  int32_t *actions = nullptr;
+  float *root_q = nullptr, *vanilla = nullptr, *terms = nullptr;
+  int64_t *best_leaf = nullptr;
+};
+void launch_finalize(const FinalizeArgs &a, cudaStream_t st, Profiler *prof = nullptr);
+
+}  // namespace bcts

@@ -1,0 +1,172 @@
+// expand.cu -- K1: fused level expansion (replicate x A + env step + reward
+// accumulation), Alg. 1 loop body:
+//   S <- S x A, R <- R x A;  r, S' = G([S, A]);  R <- R + gamma^k r.
+// Tree indices stay implicit, base A: child c of level k+1 has parent c / A
+// and action c % A (R1). No pointers are stored.
+#include "engine.h"
+
+namespace bcts {
+
+// ------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D bulk copy global -> shared (TMA engine, SASS UBLKCP), completes on mbar.
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void st_v4(uint4 *p, const uint4 &v) {
+  asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// ---------------------------------------------------------------- TABULAR
+__global__ void k_expand_tabular(NodeView par, int64_t p_first, int64_t c_begin, int64_t n_child, int A, float gk,
+                                 const int32_t *__restrict__ tnext, const float *__restrict__ trew, NodeOut out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_child) return;
+  int64_t c = c_begin + i, p = c / A;
+  int a = (int)(c - p * A);
+  int64_t pl = p - p_first;
+  int32_t s = *(const int32_t *)(par.state + pl * par.state_stride);
+  float R = par.cum ? par.cum[pl] : 0.0f;
+  ((int32_t *)out.state)[i] = tnext[(int64_t)s * A + a];
+  out.cum[i] = fmaf(gk, trew[(int64_t)s * A + a], R);
+}
+
+// --------------------------------------------------------------- INT_HASH
+// s'[w] = fmix32(s[w] ^ rotl32(s[(w+1)&15], 13) ^ 0x9E3779B9*(a+1) ^ 0x85EBCA6B*w);
+// r from the top two bits of s'[0]: +1 if 3, -1 if 0, else 0.
+__global__ void k_expand_int(NodeView par, int64_t p_first, int64_t c_begin, int64_t n_child, int A, float gk,
+                             NodeOut out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_child) return;
+  int64_t c = c_begin + i, p = c / A;
+  int a = (int)(c - p * A);
+  int64_t pl = p - p_first;
+  const uint4 *src = (const uint4 *)(par.state + pl * par.state_stride);
+  uint32_t s[16], o[16];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint4 v = __ldg(src + q);
+    s[4 * q] = v.x; s[4 * q + 1] = v.y; s[4 * q + 2] = v.z; s[4 * q + 3] = v.w;
+  }
+  const uint32_t ka = 0x9E3779B9u * (uint32_t)(a + 1);
+#pragma unroll
+  for (int w = 0; w < 16; ++w) o[w] = fmix32(s[w] ^ __funnelshift_l(s[(w + 1) & 15], s[(w + 1) & 15], 13) ^ ka ^
+                                             (0x85EBCA6Bu * (uint32_t)w));
+  uint4 *dst = (uint4 *)(out.state + i * out.state_stride);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) dst[q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+  uint32_t t = o[0] >> 30;
+  float r = t == 3u ? 1.0f : (t == 0u ? -1.0f : 0.0f);
+  float R = par.cum ? par.cum[pl] : 0.0f;
+  out.cum[i] = fmaf(gk, r, R);
+}
+
+// ------------------------------------------------------------- ATARI_HASH
+// One CTA per parent: the parent's 28,224-byte frame stack is staged in shared
+// memory by one bulk copy (TMA engine), then the CTA writes its A children with
+// coalesced 128-bit stores. Per child: k' = mix64(key ^ C*(a+1)); for the 8
+// pixels of group g, h = mix64(k' + g) supplies one noise byte each;
+// w' = (w >> 8) | ((w ^ (byte << 24)) & 0xFF000000)  (frames 1..3 shift down,
+// the new newest frame is the old newest XOR noise; frame stack P:355).
+constexpr int kExpandThreads = 256;
+constexpr int kGroups = kPix / 8;  // 882 groups of 8 pixel words (32 B)
+
+__global__ void __launch_bounds__(kExpandThreads) k_expand_atari(NodeView par, int64_t p_first, int64_t c_begin,
+                                                                   int64_t c_end, int A, float gk, NodeOut out) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  uint4 *sframe = (uint4 *)smem_raw;  // 1764 x 16 B
+  __shared__ __align__(8) uint64_t bar;
+  const int64_t p = c_begin / A + blockIdx.x;
+  const int a_lo = (int)(max(c_begin, p * A) - p * A);
+  const int a_hi = (int)(min(c_end, (p + 1) * A) - p * A);
+  const int64_t pl = p - p_first;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_expect_tx(&bar, kFrameBytes);
+    bulk_g2s(sframe, par.state + pl * par.state_stride, kFrameBytes, &bar);
+  }
+  const uint64_t key = *(const uint64_t *)((const uint8_t *)par.key + pl * par.key_stride);
+  const float R = par.cum ? par.cum[pl] : 0.0f;
+  __syncthreads();          // mbarrier init visible before anyone waits on it
+  mbar_wait(&bar, 0);
+  for (int a = a_lo; a < a_hi; ++a) {
+    const uint64_t k2 = atari_child_key(key, a);
+    const int64_t ci = p * A + a - c_begin;
+    uint4 *dst = (uint4 *)(out.state + ci * out.state_stride);
+    for (int g = threadIdx.x; g < kGroups; g += kExpandThreads) {
+      const uint64_t h = mix64(k2 + (uint64_t)g);
+      const uint32_t lo = (uint32_t)h, hi = (uint32_t)(h >> 32);
+      uint4 v0 = sframe[2 * g], v1 = sframe[2 * g + 1];
+      v0.x = (v0.x >> 8) | ((v0.x ^ (lo << 24)) & 0xFF000000u);
+      v0.y = (v0.y >> 8) | ((v0.y ^ ((lo >> 8) << 24)) & 0xFF000000u);
+      v0.z = (v0.z >> 8) | ((v0.z ^ ((lo >> 16) << 24)) & 0xFF000000u);
+      v0.w = (v0.w >> 8) | ((v0.w ^ (lo & 0xFF000000u)) & 0xFF000000u);
+      v1.x = (v1.x >> 8) | ((v1.x ^ (hi << 24)) & 0xFF000000u);
+      v1.y = (v1.y >> 8) | ((v1.y ^ ((hi >> 8) << 24)) & 0xFF000000u);
+      v1.z = (v1.z >> 8) | ((v1.z ^ ((hi >> 16) << 24)) & 0xFF000000u);
+      v1.w = (v1.w >> 8) | ((v1.w ^ (hi & 0xFF000000u)) & 0xFF000000u);
+      st_v4(dst + 2 * g, v0);
+      st_v4(dst + 2 * g + 1, v1);
+    }
+    if (threadIdx.x == 0) {
+      out.key[ci] = k2;
+      out.cum[ci] = fmaf(gk, atari_reward(k2), R);
+    }
+  }
+}
+
+void launch_expand(int env, const NodeView &par, int64_t p_first, int64_t c_begin, int64_t c_end, int A, float gk,
+                   const int32_t *tab_next, const float *tab_rew, const NodeOut &out, cudaStream_t st,
+                   Profiler *prof) {
+  const int64_t n = c_end - c_begin;
+  if (n <= 0) return;
+  const int64_t nparents = (c_end - 1) / A - c_begin / A + 1;
+  // algorithmic bytes: every child node written once + every parent node read once
+  const double nb = env == BCTS_ENV_TABULAR ? 8.0 : env == BCTS_ENV_INT_HASH ? 68.0 : (double)kFrameBytes + 12.0;
+  if (prof) prof->begin(env == BCTS_ENV_TABULAR ? KC_EXPAND_TAB : env == BCTS_ENV_INT_HASH ? KC_EXPAND_INT
+                                                                                             : KC_EXPAND_ATARI,
+                        nb * (double)(n + nparents), st);
+  if (env == BCTS_ENV_TABULAR) {
+    k_expand_tabular<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(par, p_first, c_begin, n, A, gk, tab_next, tab_rew,
+                                                                   out);
+  } else if (env == BCTS_ENV_INT_HASH) {
+    k_expand_int<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(par, p_first, c_begin, n, A, gk, out);
+  } else {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_expand_atari, cudaFuncAttributeMaxDynamicSharedMemorySize, kFrameBytes);
+      attr = true;
+    }
+    k_expand_atari<<<(unsigned)nparents, kExpandThreads, kFrameBytes, st>>>(par, p_first, c_begin, c_end, A, gk,
+                                                                             out);
+  }
+  if (prof) prof->end(st);
+}
+
+}  // namespace bcts

@@ -1,0 +1,459 @@
+// qnet.cu -- K2: the leaf value network Q_theta (Alg. 1 leaf line, P:323:
+// R <- R + gamma^d max_a Q_theta(S, a)), its weight repack (E2) and the
+// non-tensor-core pieces: TABLE gather, fp32 MLP (fixed-order fmaf chains,
+// DESIGN.md R3), the SIMT reference implicit-GEMM layer, and the heads
+// (Nature fc2 / Rainbow dueling C51 expectation) with fused max_a and
+// fmaf(g_d, max_a Q, R) epilogue. The tcgen05 layer lives in qnet_tc.cu.
+#include <math.h>
+
+#include <vector>
+
+#include "engine.h"
+
+namespace bcts {
+
+// ------------------------------------------------------------------ TABLE
+__global__ void k_table(const int32_t *__restrict__ ids, int64_t stride_bytes, const float *__restrict__ tq, int A,
+                        int64_t n, int mode, float gd, const float *__restrict__ cum, float *__restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int32_t s = *(const int32_t *)((const uint8_t *)ids + i * stride_bytes);
+  const float *q = tq + (int64_t)s * A;
+  float m = q[0];
+  for (int a = 0; a < A; ++a) {
+    if (mode == MODE_ROWS) out[i * A + a] = q[a];
+    m = q[a] > m ? q[a] : m;
+  }
+  if (mode == MODE_ROWMAX) out[i] = m;
+  if (mode == MODE_TOTAL) out[i] = fmaf(gd, m, cum ? cum[i] : 0.0f);
+}
+
+// ------------------------------------------------------------------ MLP2
+// One warp per state. x_j = byte j of the state / 256 (exact); hidden unit u:
+// acc = b1[u]; acc = fmaf(W1[u][i], x_i, acc) for i = 0..in-1; h = acc > 0 ? acc : 0.
+// Output a: acc = b2[a]; acc = fmaf(W2[a][u], h_u, acc) for u = 0..hid-1.
+constexpr int kMlpWarps = 4;
+__global__ void __launch_bounds__(32 * kMlpWarps)
+    k_mlp(const uint8_t *__restrict__ states, int64_t stride_bytes, const float *__restrict__ w1,
+          const float *__restrict__ b1, const float *__restrict__ w2, const float *__restrict__ b2, int IN, int H,
+          int A, int64_t n, int mode, float gd, const float *__restrict__ cum, float *__restrict__ out) {
+  __shared__ float xs[kMlpWarps][64];
+  __shared__ float hs[kMlpWarps][1024];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t i = (int64_t)blockIdx.x * kMlpWarps + warp;
+  if (i >= n) return;
+  const uint8_t *s = states + i * stride_bytes;
+  for (int j = lane; j < IN; j += 32) xs[warp][j] = (float)s[j] / 256.0f;
+  __syncwarp();
+  for (int u = lane; u < H; u += 32) {
+    float acc = b1[u];
+    const float *w = w1 + (int64_t)u * IN;
+    for (int k = 0; k < IN; ++k) acc = fmaf(w[k], xs[warp][k], acc);
+    hs[warp][u] = acc > 0.0f ? acc : 0.0f;
+  }
+  __syncwarp();
+  float m = -INFINITY;
+  for (int a0 = 0; a0 < A; a0 += 32) {
+    const int a = a0 + lane;
+    float q = -INFINITY;
+    if (a < A) {
+      float acc = b2[a];
+      const float *w = w2 + (int64_t)a * H;
+      for (int u = 0; u < H; ++u) acc = fmaf(w[u], hs[warp][u], acc);
+      q = acc;
+      if (mode == MODE_ROWS) out[i * A + a] = q;
+    }
+    m = fmaxf(m, q);
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) {
+    if (mode == MODE_ROWMAX) out[i] = m;
+    if (mode == MODE_TOTAL) out[i] = fmaf(gd, m, cum ? cum[i] : 0.0f);
+  }
+}
+
+// ------------------------------------------------------- SIMT implicit GEMM
+// Reference layer (BCTS_F_SIMT_NET, and the parity baseline for tcgen05):
+// 64x64 output tile per CTA, K step 32, fp32 FMA accumulation of bf16 operands.
+__device__ __forceinline__ float gather_x(const Layer &L, const void *in, int64_t m, int k) {
+  const int64_t rows = (int64_t)L.OH * L.OW;
+  const int64_t img = m / rows;
+  const int pos = (int)(m - img * rows);
+  const int oy = pos / L.OW, ox = pos - oy * L.OW;
+  const int kwc = L.KW * L.C;
+  const int ky = k / kwc, r = k - ky * kwc;
+  const int kx = r / L.C, c = r - kx * L.C;
+  const int64_t idx =
+      img * L.in_img_stride + L.in_col_off + ((int64_t)(oy * L.S + ky) * L.W + (ox * L.S + kx)) * L.C + c;
+  if (L.in_u8) return (float)((const uint8_t *)in)[idx];
+  return __bfloat162float(((const __nv_bfloat16 *)in)[idx]);
+}
+
+constexpr int kSimtBM = 64, kSimtBN = 64, kSimtBK = 32;
+__global__ void __launch_bounds__(256) k_layer_simt(Layer L, const void *__restrict__ in, int64_t M,
+                                                    void *__restrict__ out) {
+  __shared__ float As[kSimtBK][kSimtBM + 4];
+  __shared__ float Bs[kSimtBK][kSimtBN + 4];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int64_t m0 = (int64_t)blockIdx.x * kSimtBM;
+  const int n0 = blockIdx.y * kSimtBN;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < L.K; k0 += kSimtBK) {
+    for (int e = threadIdx.x; e < kSimtBM * kSimtBK; e += 256) {
+      const int mm = e / kSimtBK, kk = e % kSimtBK;
+      const int64_t m = m0 + mm;
+      const int k = k0 + kk;
+      As[kk][mm] = (m < M && k < L.K) ? gather_x(L, in, m, k) : 0.0f;
+      const int n = n0 + mm;
+      Bs[kk][mm] = (n < L.Npad && k < L.K) ? __bfloat162float(L.Wt[(int64_t)n * L.K + k]) : 0.0f;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < kSimtBK; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t m = m0 + ty * 4 + i;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + tx * 4 + j;
+      if (n >= L.Npad) continue;
+      const float v = acc[i][j] + L.bias[n];
+      if (L.relu_bf16)
+        ((__nv_bfloat16 *)out)[m * L.out_ld + n] = __float2bfloat16_rn(v > 0.0f ? v : 0.0f);
+      else
+        ((float *)out)[m * L.out_ld + n] = v;
+    }
+  }
+}
+
+void launch_layer_simt(const Layer &L, const void *in, int64_t n_img, void *out, cudaStream_t st) {
+  const int64_t M = n_img * L.rows_per_img();
+  dim3 grid((unsigned)((M + kSimtBM - 1) / kSimtBM), (unsigned)((L.Npad + kSimtBN - 1) / kSimtBN));
+  k_layer_simt<<<grid, 256, 0, st>>>(L, in, M, out);
+}
+
+// ------------------------------------------------------------------ heads
+// One warp per image. Nature: q_a = z[a]. Rainbow (dueling C51, R15):
+// logits[a][i] = v_i + adv[a][i] - mean_a adv[a][i]; p = softmax_i; q_a = sum_i z_i p.
+template <bool RAINBOW>
+__global__ void __launch_bounds__(128) k_head(const float *__restrict__ zv, int64_t ldv, const float *__restrict__ za,
+                                              int64_t lda, int A, int atoms, float vmin, float dz, int64_t n, int mode,
+                                              float gd, const float *__restrict__ cum, float *__restrict__ out) {
+  const int lane = threadIdx.x % 32;
+  const int64_t i = (int64_t)blockIdx.x * 4 + threadIdx.x / 32;
+  if (i >= n) return;
+  float best = -INFINITY;
+  if (!RAINBOW) {
+    for (int a0 = 0; a0 < A; a0 += 32) {
+      const int a = a0 + lane;
+      float q = -INFINITY;
+      if (a < A) {
+        q = za[i * lda + a];
+        if (mode == MODE_ROWS) out[i * A + a] = q;
+      }
+      best = fmaxf(best, q);
+    }
+    for (int o = 16; o > 0; o >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, o));
+  } else {
+    const float *v = zv + i * ldv;
+    const float *adv = za + i * lda;
+    float vi[2], mean[2], zi[2];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int at = lane + 32 * t;
+      vi[t] = 0.f; mean[t] = 0.f; zi[t] = 0.f;
+      if (at < atoms) {
+        vi[t] = v[at];
+        float s = 0.f;
+        for (int a = 0; a < A; ++a) s += adv[a * atoms + at];
+        mean[t] = s / (float)A;
+        zi[t] = vmin + (float)at * dz;
+      }
+    }
+    for (int a = 0; a < A; ++a) {
+      float lg[2], mx = -INFINITY;
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int at = lane + 32 * t;
+        lg[t] = at < atoms ? vi[t] + adv[a * atoms + at] - mean[t] : -INFINITY;
+        mx = fmaxf(mx, lg[t]);
+      }
+      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      float den = 0.f, num = 0.f;
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int at = lane + 32 * t;
+        if (at < atoms) {
+          const float e = expf(lg[t] - mx);
+          den += e;
+          num += zi[t] * e;
+        }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        den += __shfl_xor_sync(0xffffffffu, den, o);
+        num += __shfl_xor_sync(0xffffffffu, num, o);
+      }
+      const float q = num / den;
+      if (mode == MODE_ROWS && lane == 0) out[i * A + a] = q;
+      best = fmaxf(best, q);
+    }
+  }
+  if (lane == 0) {
+    if (mode == MODE_ROWMAX) out[i] = best;
+    if (mode == MODE_TOTAL) out[i] = fmaf(gd, best, cum ? cum[i] : 0.0f);
+  }
+}
+
+// ------------------------------------------------------------ build / eval
+static int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+static cudaError_t upload(Net &net, const void *h, size_t bytes, void **d) {
+  cudaError_t e = cudaMalloc(d, bytes ? bytes : 16);
+  if (e != cudaSuccess) return e;
+  net.allocs.push_back(*d);
+  return cudaMemcpy(*d, h, bytes, cudaMemcpyHostToDevice);
+}
+
+// Repack an OIHW conv weight (or [N][K] linear) into [Npad][K] bf16 with
+// k = (ky, kx, c); rows >= O are zero. src_index(o, ky, kx, c) -> canonical index.
+template <class F>
+static std::vector<__nv_bfloat16> repack(int O, int Npad, int KH, int KW, int C, F src_index, const float *w) {
+  const int K = KH * KW * C;
+  std::vector<__nv_bfloat16> out((size_t)Npad * K, __float2bfloat16_rn(0.0f));
+  for (int o = 0; o < O; ++o)
+    for (int ky = 0; ky < KH; ++ky)
+      for (int kx = 0; kx < KW; ++kx)
+        for (int c = 0; c < C; ++c)
+          out[(size_t)o * K + (ky * KW + kx) * C + c] = __float2bfloat16_rn(w[(int64_t)src_index(o, ky, kx, c)]);
+  return out;
+}
+
+static int make_layer(Net &net, Layer &L, std::vector<__nv_bfloat16> &&wt, const float *bias, int N, int Npad,
+                      std::string &err) {
+  std::vector<float> b((size_t)Npad, 0.0f);
+  for (int i = 0; i < N; ++i) b[i] = bias[i];
+  void *dw = nullptr, *db = nullptr;
+  if (upload(net, wt.data(), wt.size() * sizeof(__nv_bfloat16), &dw) != cudaSuccess ||
+      upload(net, b.data(), b.size() * sizeof(float), &db) != cudaSuccess) {
+    err = "cudaMalloc/cudaMemcpy of weights failed";
+    return -1;
+  }
+  L.Wt = (const __nv_bfloat16 *)dw;
+  L.bias = (const float *)db;
+  L.N = N;
+  L.Npad = Npad;
+  return 0;
+}
+
+int net_build(Net &net, const bcts_config &cfg, std::string &err) {
+  net.kind = cfg.net;
+  net.A = cfg.num_actions;
+  const int A = net.A;
+  if (cfg.net == BCTS_NET_TABLE) {
+    if (!cfg.tab_q || cfg.num_states <= 0) { err = "TABLE net needs tab_q and num_states"; return -1; }
+    void *d = nullptr;
+    if (upload(net, cfg.tab_q, sizeof(float) * (size_t)cfg.num_states * A, &d) != cudaSuccess) {
+      err = "upload tab_q failed";
+      return -1;
+    }
+    net.tq = (const float *)d;
+    net.nS = cfg.num_states;
+    return 0;
+  }
+  if (!cfg.weights) { err = "weights required"; return -1; }
+  const float *w = cfg.weights;
+  if (cfg.net == BCTS_NET_MLP2_F32) {
+    const int I = cfg.mlp_in, H = cfg.mlp_hidden;
+    if (I != 64 || H < 1 || H > 1024) { err = "MLP2 needs mlp_in == 64 and 1 <= mlp_hidden <= 1024"; return -1; }
+    const int64_t need = (int64_t)H * I + H + (int64_t)A * H + A;
+    if (cfg.weights_count != need) { err = "weights_count mismatch for MLP2"; return -1; }
+    void *p[4];
+    const size_t sz[4] = {(size_t)H * I, (size_t)H, (size_t)A * H, (size_t)A};
+    for (int t = 0; t < 4; ++t) {
+      if (upload(net, w, sz[t] * sizeof(float), &p[t]) != cudaSuccess) { err = "upload MLP failed"; return -1; }
+      w += sz[t];
+    }
+    net.l1w = (const float *)p[0]; net.l1b = (const float *)p[1];
+    net.l2w = (const float *)p[2]; net.l2b = (const float *)p[3];
+    net.in = I; net.hid = H;
+    return 0;
+  }
+  const bool rainbow = cfg.net == BCTS_NET_RAINBOW_BF16;
+  if (!rainbow && cfg.net != BCTS_NET_NATURE_BF16) { err = "unknown net kind"; return -1; }
+  const int atoms = rainbow ? cfg.atoms : 0;
+  if (rainbow && (atoms < 2 || atoms > 64)) { err = "atoms must be in [2, 64]"; return -1; }
+  int64_t need = 32 * 256 + 32 + 64 * 512 + 64 + 64 * 576 + 64;
+  need += rainbow ? 2 * (512LL * 3136 + 512) + (int64_t)atoms * 512 + atoms + (int64_t)A * atoms * 512 + A * atoms
+                  : 512LL * 3136 + 512 + (int64_t)A * 512 + A;
+  if (cfg.weights_count != need) { err = "weights_count mismatch for conv net"; return -1; }
+  net.atoms = atoms;
+  net.vmin = cfg.v_min;
+  net.vmax = cfg.v_max;
+  // conv1: OIHW [32][4][8][8], input uint8 NHWC C=4
+  {
+    Layer &L = net.c1;
+    L.in_u8 = 1; L.H = L.W = 84; L.C = 4; L.KH = L.KW = 8; L.S = 4; L.OH = L.OW = 20; L.K = 256;
+    L.relu_bf16 = 1; L.out_ld = 32;
+    if (make_layer(net, L, repack(32, 32, 8, 8, 4, [](int o, int ky, int kx, int c) { return ((o * 4 + c) * 8 + ky) * 8 + kx; }, w),
+                   w + 32 * 256, 32, 32, err)) return -1;
+    w += 32 * 256 + 32;
+  }
+  {
+    Layer &L = net.c2;
+    L.H = L.W = 20; L.C = 32; L.KH = L.KW = 4; L.S = 2; L.OH = L.OW = 9; L.K = 512; L.relu_bf16 = 1; L.out_ld = 64;
+    L.in_img_stride = 20 * 20 * 32;
+    if (make_layer(net, L, repack(64, 64, 4, 4, 32, [](int o, int ky, int kx, int c) { return ((o * 32 + c) * 4 + ky) * 4 + kx; }, w),
+                   w + 64 * 512, 64, 64, err)) return -1;
+    w += 64 * 512 + 64;
+  }
+  {
+    Layer &L = net.c3;
+    L.H = L.W = 9; L.C = 64; L.KH = L.KW = 3; L.S = 1; L.OH = L.OW = 7; L.K = 576; L.relu_bf16 = 1; L.out_ld = 64;
+    L.in_img_stride = 9 * 9 * 64;
+    if (make_layer(net, L, repack(64, 64, 3, 3, 64, [](int o, int ky, int kx, int c) { return ((o * 64 + c) * 3 + ky) * 3 + kx; }, w),
+                   w + 64 * 576, 64, 64, err)) return -1;
+    w += 64 * 576 + 64;
+  }
+  // fc over the 7x7x64 conv3 output: PyTorch flattens NCHW (c*49 + y*7 + x) (R25);
+  // our activations are NHWC, so k = (y, x, c) <- canonical c*49 + y*7 + x.
+  auto fc_src = [](int o, int y, int x, int c) { return (int64_t)o * 3136 + c * 49 + y * 7 + x; };
+  const int hidN = rainbow ? 1024 : 512;
+  {
+    Layer &L = net.fc_h;
+    L.H = L.W = 7; L.C = 64; L.KH = L.KW = 7; L.S = 1; L.OH = L.OW = 1; L.K = 3136; L.relu_bf16 = 1; L.out_ld = hidN;
+    L.in_img_stride = 3136;
+    std::vector<__nv_bfloat16> wt;
+    std::vector<float> b(hidN);
+    if (!rainbow) {
+      wt = repack(512, 512, 7, 7, 64, [&](int o, int y, int x, int c) { return fc_src(o, y, x, c); }, w);
+      for (int i = 0; i < 512; ++i) b[i] = w[512 * 3136 + i];
+      w += 512 * 3136 + 512;
+    } else {
+      // rows 0..511 = fc_h_v, 512..1023 = fc_h_a (one GEMM, concatenated)
+      const float *wv = w, *bv = w + 512 * 3136, *wa = bv + 512, *ba = wa + 512 * 3136;
+      wt = repack(512, 512, 7, 7, 64, fc_src, wv);
+      std::vector<__nv_bfloat16> wta = repack(512, 512, 7, 7, 64, fc_src, wa);
+      wt.insert(wt.end(), wta.begin(), wta.end());
+      for (int i = 0; i < 512; ++i) { b[i] = bv[i]; b[512 + i] = ba[i]; }
+      w = ba + 512;
+    }
+    if (make_layer(net, L, std::move(wt), b.data(), hidN, hidN, err)) return -1;
+  }
+  if (!rainbow) {
+    Layer &L = net.fc2;
+    const int Np = round_up(A, 16);
+    L.H = L.W = 1; L.C = 512; L.K = 512; L.relu_bf16 = 0; L.out_ld = Np; L.in_img_stride = 512;
+    if (make_layer(net, L, repack(A, Np, 1, 1, 512, [](int o, int, int, int c) { return o * 512 + c; }, w),
+                   w + A * 512, A, Np, err)) return -1;
+    w += A * 512 + A;
+    net.ld_za = Np;
+  } else {
+    Layer &V = net.z_v;
+    const int Nv = round_up(atoms, 16);
+    V.H = V.W = 1; V.C = 512; V.K = 512; V.relu_bf16 = 0; V.out_ld = Nv; V.in_img_stride = 1024; V.in_col_off = 0;
+    if (make_layer(net, V, repack(atoms, Nv, 1, 1, 512, [](int o, int, int, int c) { return o * 512 + c; }, w),
+                   w + atoms * 512, atoms, Nv, err)) return -1;
+    w += atoms * 512 + atoms;
+    Layer &Z = net.z_a;
+    const int Na = round_up(A * atoms, 16);
+    Z.H = Z.W = 1; Z.C = 512; Z.K = 512; Z.relu_bf16 = 0; Z.out_ld = Na; Z.in_img_stride = 1024; Z.in_col_off = 512;
+    if (make_layer(net, Z, repack(A * atoms, Na, 1, 1, 512, [](int o, int, int, int c) { return o * 512 + c; }, w),
+                   w + A * atoms * 512, A * atoms, Na, err)) return -1;
+    w += (int64_t)A * atoms * 512 + A * atoms;
+    net.ld_zv = Nv;
+    net.ld_za = Na;
+  }
+  // scratch for one sub-batch (sized to stay L2-resident)
+  net.batch = 2048;
+  const int64_t B = net.batch;
+  size_t bytes[6] = {(size_t)B * 400 * 32 * 2, (size_t)B * 81 * 64 * 2, (size_t)B * 49 * 64 * 2,
+                     (size_t)B * hidN * 2, (size_t)B * (rainbow ? net.ld_zv : 16) * 4, (size_t)B * net.ld_za * 4};
+  void *p[6];
+  for (int t = 0; t < 6; ++t) {
+    if (cudaMalloc(&p[t], bytes[t]) != cudaSuccess) { err = "cudaMalloc net scratch failed"; return -1; }
+    net.allocs.push_back(p[t]);
+  }
+  net.act1 = (__nv_bfloat16 *)p[0]; net.act2 = (__nv_bfloat16 *)p[1]; net.act3 = (__nv_bfloat16 *)p[2];
+  net.hid_act = (__nv_bfloat16 *)p[3]; net.zv = (float *)p[4]; net.za = (float *)p[5];
+  return 0;
+}
+
+void net_free(Net &net) {
+  for (void *p : net.allocs) cudaFree(p);
+  net.allocs.clear();
+}
+
+static void run_layer(const Net &net, int cls, const Layer &L, const void *in, int64_t n_img, void *out,
+                      cudaStream_t st) {
+  // algorithmic FLOPs: 2 * M * N * K with the true (unpadded) N
+  if (net.prof) net.prof->begin(cls, 2.0 * (double)(n_img * L.rows_per_img()) * L.N * L.K, st);
+  if (net.tc && tc_supported(L)) launch_layer_tc(L, in, n_img, out, st);
+  else launch_layer_simt(L, in, n_img, out, st);
+  if (net.prof) net.prof->end(st);
+}
+
+int net_eval(Net &net, const NodeView &v, int64_t n, int mode, float gd, float *out, cudaStream_t st) {
+  if (n <= 0) return 0;
+  const int A = net.A;
+  int launches = 0;
+  if (net.kind == BCTS_NET_TABLE) {
+    if (net.prof) net.prof->begin(KC_TABLE, (double)n * (8.0 + 4.0 * A), st);
+    k_table<<<(unsigned)((n + 255) / 256), 256, 0, st>>>((const int32_t *)v.state, v.state_stride, net.tq, A, n, mode,
+                                                          gd, v.cum, out);
+    if (net.prof) net.prof->end(st);
+    return 1;
+  }
+  if (net.kind == BCTS_NET_MLP2_F32) {
+    if (net.prof) net.prof->begin(KC_MLP, 2.0 * (double)n * ((double)net.in * net.hid + (double)net.hid * A), st);
+    k_mlp<<<(unsigned)((n + kMlpWarps - 1) / kMlpWarps), 32 * kMlpWarps, 0, st>>>(
+        v.state, v.state_stride, net.l1w, net.l1b, net.l2w, net.l2b, net.in, net.hid, A, n, mode, gd, v.cum, out);
+    if (net.prof) net.prof->end(st);
+    return 1;
+  }
+  const bool rainbow = net.kind == BCTS_NET_RAINBOW_BF16;
+  for (int64_t b0 = 0; b0 < n; b0 += net.batch) {
+    const int64_t nb = n - b0 < net.batch ? n - b0 : net.batch;
+    Layer c1 = net.c1;
+    c1.in_img_stride = v.state_stride;
+    run_layer(net, KC_CONV1, c1, v.state + b0 * v.state_stride, nb, net.act1, st);
+    run_layer(net, KC_CONV2, net.c2, net.act1, nb, net.act2, st);
+    run_layer(net, KC_CONV3, net.c3, net.act2, nb, net.act3, st);
+    run_layer(net, KC_FC_H, net.fc_h, net.act3, nb, net.hid_act, st);
+    launches += 4;
+    float *o = out + (mode == MODE_ROWS ? b0 * A : b0);
+    const float *cum = v.cum ? v.cum + b0 : nullptr;
+    if (!rainbow) {
+      run_layer(net, KC_FC_OUT, net.fc2, net.hid_act, nb, net.za, st);
+      if (net.prof) net.prof->begin(KC_HEAD, (double)nb * 4.0 * (net.ld_za + 1), st);
+      k_head<false><<<(unsigned)((nb + 3) / 4), 128, 0, st>>>(nullptr, 0, net.za, net.ld_za, A, 0, 0.f, 0.f, nb, mode,
+                                                               gd, cum, o);
+      if (net.prof) net.prof->end(st);
+      launches += 2;
+    } else {
+      run_layer(net, KC_FC_OUT, net.z_v, net.hid_act, nb, net.zv, st);
+      run_layer(net, KC_FC_OUT, net.z_a, net.hid_act, nb, net.za, st);
+      const float dz = (net.vmax - net.vmin) / (float)(net.atoms - 1);
+      if (net.prof) net.prof->begin(KC_HEAD, (double)nb * 4.0 * (net.ld_za + net.ld_zv + 1), st);
+      k_head<true><<<(unsigned)((nb + 3) / 4), 128, 0, st>>>(net.zv, net.ld_zv, net.za, net.ld_za, A, net.atoms,
+                                                              net.vmin, dz, nb, mode, gd, cum, o);
+      if (net.prof) net.prof->end(st);
+      launches += 3;
+    }
+  }
+  return launches;
+}
+
+}  // namespace bcts
