@@ -95,6 +95,16 @@ struct Layer {
   int64_t rows_per_img() const { return (int64_t)OH * OW; }
 };
 
+// TMA-fed layer (qnet_tma.cu): tensor maps for A (2-D tile or 4-D im2col) and B.
+struct TmaPlan {
+  bool ok = false;
+  int im2col = 0, kb = 64, bn = 64;
+  alignas(64) uint8_t mapA[128];
+  alignas(64) uint8_t mapB[128];
+};
+bool tma_plan(TmaPlan &P, const Layer &L, const void *in, int64_t cap_img);
+void launch_layer_tma(const TmaPlan &P, const Layer &L, int64_t n_img, void *out, cudaStream_t st);
+
 // Net output modes.
 enum { MODE_ROWS = 0, MODE_ROWMAX = 1, MODE_TOTAL = 2 };
 
@@ -110,8 +120,10 @@ struct Net {
   Layer c1, c2, c3, fc_h, z_v, z_a, fc2;
   int atoms = 51;
   float vmin = -10.f, vmax = 10.f;
-  // scratch for a sub-batch of `batch` images
-  int64_t batch = 0;
+  // scratch: trunk sub-batches of `batch` images (conv activations stay
+  // L2-resident), fc layers over `fc_batch` images at a time
+  int64_t batch = 0, fc_batch = 0;
+  TmaPlan p_c2, p_c3, p_fc_h, p_z_v, p_z_a, p_fc2;
   __nv_bfloat16 *act1 = nullptr, *act2 = nullptr, *act3 = nullptr, *hid_act = nullptr;
   float *zv = nullptr, *za = nullptr;
   int64_t ld_za = 0, ld_zv = 0;

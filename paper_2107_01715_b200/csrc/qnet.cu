@@ -376,11 +376,13 @@ int net_build(Net &net, const bcts_config &cfg, std::string &err) {
     net.ld_zv = Nv;
     net.ld_za = Na;
   }
-  // scratch for one sub-batch (sized to stay L2-resident)
+  // scratch: trunk sub-batches of 2048 images (act1/act2 stay L2-resident),
+  // fc layers over 16384 images at a time (enough M tiles to fill 148 SMs)
   net.batch = 2048;
-  const int64_t B = net.batch;
-  size_t bytes[6] = {(size_t)B * 400 * 32 * 2, (size_t)B * 81 * 64 * 2, (size_t)B * 49 * 64 * 2,
-                     (size_t)B * hidN * 2, (size_t)B * (rainbow ? net.ld_zv : 16) * 4, (size_t)B * net.ld_za * 4};
+  net.fc_batch = 16384;
+  const int64_t B = net.batch, FB = net.fc_batch;
+  size_t bytes[6] = {(size_t)B * 400 * 32 * 2, (size_t)B * 81 * 64 * 2, (size_t)FB * 49 * 64 * 2,
+                     (size_t)FB * hidN * 2, (size_t)FB * (rainbow ? net.ld_zv : 16) * 4, (size_t)FB * net.ld_za * 4};
   void *p[6];
   for (int t = 0; t < 6; ++t) {
     if (cudaMalloc(&p[t], bytes[t]) != cudaSuccess) { err = "cudaMalloc net scratch failed"; return -1; }
@@ -388,6 +390,18 @@ int net_build(Net &net, const bcts_config &cfg, std::string &err) {
   }
   net.act1 = (__nv_bfloat16 *)p[0]; net.act2 = (__nv_bfloat16 *)p[1]; net.act3 = (__nv_bfloat16 *)p[2];
   net.hid_act = (__nv_bfloat16 *)p[3]; net.zv = (float *)p[4]; net.za = (float *)p[5];
+  // TMA plans (tensor maps over the fixed scratch buffers; fall back to the
+  // thread-gather tcgen05 layer if the driver entry points are unavailable)
+  tma_plan(net.p_c2, net.c2, net.act1, B);
+  tma_plan(net.p_c3, net.c3, net.act2, B);
+  tma_plan(net.p_fc_h, net.fc_h, net.act3, FB);
+  if (rainbow) {
+    tma_plan(net.p_z_v, net.z_v, net.hid_act, FB);
+    tma_plan(net.p_z_a, net.z_a, net.hid_act, FB);
+  } else {
+    tma_plan(net.p_fc2, net.fc2, net.hid_act, FB);
+  }
+  cudaGetLastError();
   return 0;
 }
 
@@ -397,10 +411,11 @@ void net_free(Net &net) {
 }
 
 static void run_layer(const Net &net, int cls, const Layer &L, const void *in, int64_t n_img, void *out,
-                      cudaStream_t st) {
+                      cudaStream_t st, const TmaPlan *plan = nullptr) {
   // algorithmic FLOPs: 2 * M * N * K with the true (unpadded) N
   if (net.prof) net.prof->begin(cls, 2.0 * (double)(n_img * L.rows_per_img()) * L.N * L.K, st);
-  if (net.tc && tc_supported(L)) launch_layer_tc(L, in, n_img, out, st);
+  if (net.tc && plan && plan->ok) launch_layer_tma(*plan, L, n_img, out, st);
+  else if (net.tc && tc_supported(L)) launch_layer_tc(L, in, n_img, out, st);
   else launch_layer_simt(L, in, n_img, out, st);
   if (net.prof) net.prof->end(st);
 }
@@ -424,31 +439,36 @@ int net_eval(Net &net, const NodeView &v, int64_t n, int mode, float gd, float *
     return 1;
   }
   const bool rainbow = net.kind == BCTS_NET_RAINBOW_BF16;
-  for (int64_t b0 = 0; b0 < n; b0 += net.batch) {
-    const int64_t nb = n - b0 < net.batch ? n - b0 : net.batch;
-    Layer c1 = net.c1;
-    c1.in_img_stride = v.state_stride;
-    run_layer(net, KC_CONV1, c1, v.state + b0 * v.state_stride, nb, net.act1, st);
-    run_layer(net, KC_CONV2, net.c2, net.act1, nb, net.act2, st);
-    run_layer(net, KC_CONV3, net.c3, net.act2, nb, net.act3, st);
-    run_layer(net, KC_FC_H, net.fc_h, net.act3, nb, net.hid_act, st);
-    launches += 4;
-    float *o = out + (mode == MODE_ROWS ? b0 * A : b0);
-    const float *cum = v.cum ? v.cum + b0 : nullptr;
+  for (int64_t f0 = 0; f0 < n; f0 += net.fc_batch) {
+    const int64_t nf = n - f0 < net.fc_batch ? n - f0 : net.fc_batch;
+    // conv trunk in L2-sized sub-batches; conv3 writes into the fc-batch act3 buffer
+    for (int64_t b0 = 0; b0 < nf; b0 += net.batch) {
+      const int64_t nb = nf - b0 < net.batch ? nf - b0 : net.batch;
+      Layer c1 = net.c1;
+      c1.in_img_stride = v.state_stride;
+      run_layer(net, KC_CONV1, c1, v.state + (f0 + b0) * v.state_stride, nb, net.act1, st);
+      run_layer(net, KC_CONV2, net.c2, net.act1, nb, net.act2, st, &net.p_c2);
+      run_layer(net, KC_CONV3, net.c3, net.act2, nb, net.act3 + b0 * 3136, st, &net.p_c3);
+      launches += 3;
+    }
+    run_layer(net, KC_FC_H, net.fc_h, net.act3, nf, net.hid_act, st, &net.p_fc_h);
+    launches += 1;
+    float *o = out + (mode == MODE_ROWS ? f0 * A : f0);
+    const float *cum = v.cum ? v.cum + f0 : nullptr;
     if (!rainbow) {
-      run_layer(net, KC_FC_OUT, net.fc2, net.hid_act, nb, net.za, st);
-      if (net.prof) net.prof->begin(KC_HEAD, (double)nb * 4.0 * (net.ld_za + 1), st);
-      k_head<false><<<(unsigned)((nb + 3) / 4), 128, 0, st>>>(nullptr, 0, net.za, net.ld_za, A, 0, 0.f, 0.f, nb, mode,
+      run_layer(net, KC_FC_OUT, net.fc2, net.hid_act, nf, net.za, st, &net.p_fc2);
+      if (net.prof) net.prof->begin(KC_HEAD, (double)nf * 4.0 * (net.ld_za + 1), st);
+      k_head<false><<<(unsigned)((nf + 3) / 4), 128, 0, st>>>(nullptr, 0, net.za, net.ld_za, A, 0, 0.f, 0.f, nf, mode,
                                                                gd, cum, o);
       if (net.prof) net.prof->end(st);
       launches += 2;
     } else {
-      run_layer(net, KC_FC_OUT, net.z_v, net.hid_act, nb, net.zv, st);
-      run_layer(net, KC_FC_OUT, net.z_a, net.hid_act, nb, net.za, st);
+      run_layer(net, KC_FC_OUT, net.z_v, net.hid_act, nf, net.zv, st, &net.p_z_v);
+      run_layer(net, KC_FC_OUT, net.z_a, net.hid_act, nf, net.za, st, &net.p_z_a);
       const float dz = (net.vmax - net.vmin) / (float)(net.atoms - 1);
-      if (net.prof) net.prof->begin(KC_HEAD, (double)nb * 4.0 * (net.ld_za + net.ld_zv + 1), st);
-      k_head<true><<<(unsigned)((nb + 3) / 4), 128, 0, st>>>(net.zv, net.ld_zv, net.za, net.ld_za, A, net.atoms,
-                                                              net.vmin, dz, nb, mode, gd, cum, o);
+      if (net.prof) net.prof->begin(KC_HEAD, (double)nf * 4.0 * (net.ld_za + net.ld_zv + 1), st);
+      k_head<true><<<(unsigned)((nf + 3) / 4), 128, 0, st>>>(net.zv, net.ld_zv, net.za, net.ld_za, A, net.atoms,
+                                                              net.vmin, dz, nf, mode, gd, cum, o);
       if (net.prof) net.prof->end(st);
       launches += 3;
     }

@@ -1,0 +1,380 @@
+// qnet_tma.cu -- K2 layers whose A operand is a plain TMA load:
+//   * fc layers: A = activations [M][K] (2-D tiled TMA, 128 rows x 64 bf16);
+//   * conv2 / conv3: A = im2col of an NHWC activation tensor (4-D im2col TMA:
+//     one load per (M tile, filter tap) brings 128 output pixels x C channels;
+//     the filter tap is the TMA im2col offset), i.e. implicit GEMM with the
+//     gather done by the TMA engine instead of by threads.
+// B (weights [Npad][K], K-major) streams per k-block with 2-D tiled TMA.
+//
+// Warp roles (192 threads, persistent over tiles):
+//   warp 0     : TMA producer (one elected thread), kStages-deep smem ring
+//   warp 1     : TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 2-5  : epilogue (TMEM -> registers -> bias/ReLU/bf16 -> global),
+//                double-buffered TMEM accumulator so it overlaps the next tile.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+
+#include "engine.h"
+
+namespace bcts {
+namespace {
+
+__device__ __forceinline__ uint32_t saddr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(saddr(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap *map, int x, int y, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(dst),
+      "l"(map), "r"(x), "r"(y), "r"(saddr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_im2col_4d(uint32_t dst, const CUtensorMap *map, int c, int w, int h, int n,
+                                              uint16_t off_w, uint16_t off_h, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(dst),
+      "l"(map), "r"(saddr(bar)), "r"(c), "r"(w), "r"(h), "r"(n), "h"(off_w), "h"(off_h)
+      : "memory");
+}
+
+// tcgen05 shared-memory descriptor, K-major with 128B (KB=64) or 64B (KB=32) swizzle.
+template <int KB>
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)((8 * KB * 2) >> 4) << 32;      // SBO: 8 rows x row bytes
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)(KB == 64 ? 2 : 4) << 61;       // SWIZZLE_128B / SWIZZLE_64B
+  return d;
+}
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t *bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(saddr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+constexpr int kBM = 128;
+constexpr int kThreads = 192;
+
+template <int BN, int KB>
+struct TmaCfg {
+  static constexpr int A_BYTES = kBM * KB * 2;
+  static constexpr int B_BYTES = BN * KB * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (200 * 1024) / STAGE > 8 ? 8 : (200 * 1024) / STAGE;
+  static constexpr uint32_t TCOLS = 2 * BN < 32 ? 32 : 2 * BN;
+  static constexpr int SMEM = STAGES * STAGE + 1024;
+};
+
+// Geometry the producer needs per layer (passed by value).
+struct TmaGeom {
+  int im2col;      // 0: 2-D tiled A, 1: 4-D im2col A
+  int OH, OW, S;   // conv output geometry and stride (im2col)
+  int KW, C;       // filter width and channels (im2col k-block -> (ky, kx, c0))
+};
+
+template <int BN, int KB>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_gemm_tma(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, Layer L,
+               TmaGeom G, int64_t M, void *__restrict__ out, int n_m, int n_n) {
+  using C = TmaCfg<BN, KB>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t full[C::STAGES], empty[C::STAGES], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_slot;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int nk = L.K / KB;
+  const int n_tiles = n_m * n_n;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(&tmem_slot)),
+                 "r"(C::TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t it = 0;
+      const int rows = G.OH * G.OW;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const int mt = tile / n_n, ntile = tile - mt * n_n;
+        const int64_t m0 = (int64_t)mt * kBM;
+        int img = 0, oy = 0, ox = 0;
+        if (G.im2col) {
+          img = (int)(m0 / rows);
+          const int pos = (int)(m0 - (int64_t)img * rows);
+          oy = pos / G.OW;
+          ox = pos - oy * G.OW;
+        }
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % C::STAGES;
+          const uint32_t ph = (it / C::STAGES) & 1u;
+          mbar_wait(&empty[s], ph ^ 1u);
+          const uint32_t sa = saddr(smem + s * C::STAGE);
+          mbar_expect_tx(&full[s], C::STAGE);
+          if (G.im2col) {
+            const int k0 = kb * KB;
+            const int kwc = G.KW * G.C;
+            const int ky = k0 / kwc, r = k0 - ky * kwc;
+            const int kx = r / G.C, c0 = r - kx * G.C;
+            tma_im2col_4d(sa, &mapA, c0, ox * G.S, oy * G.S, img, (uint16_t)kx, (uint16_t)ky, &full[s]);
+          } else {
+            tma_2d(sa, &mapA, kb * KB, (int)m0, &full[s]);
+          }
+          tma_2d(sa + C::A_BYTES, &mapB, kb * KB, ntile * BN, &full[s]);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      uint32_t it = 0, acc_it = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++acc_it) {
+        const int ntile = tile % n_n;
+        const int nt = min(BN, L.Npad - ntile * BN);
+        const uint32_t idesc = idesc_bf16(kBM, nt);
+        const uint32_t a = acc_it & 1u, aph = (acc_it >> 1) & 1u;
+        mbar_wait(&tempty[a], aph ^ 1u);
+        tc_fence_after();
+        const uint32_t d = tmem + a * BN;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % C::STAGES;
+          const uint32_t ph = (it / C::STAGES) & 1u;
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t a0 = saddr(smem + s * C::STAGE), b0 = a0 + C::A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < KB / 16; ++kk)
+            mma_bf16(d, sdesc<KB>(a0 + kk * 32), sdesc<KB>(b0 + kk * 32), idesc, (kb | kk) != 0);
+          mma_commit(&empty[s]);
+        }
+        mma_commit(&tfull[a]);
+      }
+    }
+    __syncwarp();
+  } else {
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    uint32_t acc_it = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++acc_it) {
+      const int mt = tile / n_n, ntile = tile - mt * n_n;
+      const int64_t m = (int64_t)mt * kBM + r;
+      const int n0 = ntile * BN;
+      const int nt = min(BN, L.Npad - n0);
+      const uint32_t a = acc_it & 1u, aph = (acc_it >> 1) & 1u;
+      mbar_wait(&tfull[a], aph);
+      tc_fence_after();
+      const uint32_t trow = tmem + a * BN + ((uint32_t)(q * 32) << 16);
+      for (int c = 0; c < nt; c += 16) {
+        uint32_t v[16];
+        tmem_ld16(trow + (uint32_t)c, v);
+        if (m >= M) continue;
+        const float *bias = L.bias + n0 + c;
+        if (L.relu_bf16) {
+          uint32_t pk[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float x = __uint_as_float(v[2 * i]) + __ldg(bias + 2 * i);
+            const float y = __uint_as_float(v[2 * i + 1]) + __ldg(bias + 2 * i + 1);
+            __nv_bfloat162 hh = __floats2bfloat162_rn(x > 0.0f ? x : 0.0f, y > 0.0f ? y : 0.0f);
+            pk[i] = *(uint32_t *)&hh;
+          }
+          uint4 *dst = (uint4 *)((__nv_bfloat16 *)out + m * L.out_ld + n0 + c);
+          dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        } else {
+          float4 *dst = (float4 *)((float *)out + m * L.out_ld + n0 + c);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            dst[i] = make_float4(__uint_as_float(v[4 * i]) + __ldg(bias + 4 * i),
+                                 __uint_as_float(v[4 * i + 1]) + __ldg(bias + 4 * i + 1),
+                                 __uint_as_float(v[4 * i + 2]) + __ldg(bias + 4 * i + 2),
+                                 __uint_as_float(v[4 * i + 3]) + __ldg(bias + 4 * i + 3));
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[a]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TCOLS));
+  }
+}
+
+// ------------------------------------------------------------- host side
+PFN_cuTensorMapEncodeTiled_v12000 g_encode_tiled = nullptr;
+PFN_cuTensorMapEncodeIm2col_v12000 g_encode_im2col = nullptr;
+
+bool load_driver() {
+  if (g_encode_tiled && g_encode_im2col) return true;
+  cudaDriverEntryPointQueryResult q;
+  void *f = nullptr;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess || !f) return false;
+  g_encode_tiled = (PFN_cuTensorMapEncodeTiled_v12000)f;
+  f = nullptr;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &f, cudaEnableDefault, &q) != cudaSuccess || !f)
+    return false;
+  g_encode_im2col = (PFN_cuTensorMapEncodeIm2col_v12000)f;
+  return true;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int BN, int KB>
+void launch_gemm(const TmaPlan &P, const Layer &L, int64_t M, void *out, cudaStream_t st) {
+  using C = TmaCfg<BN, KB>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_gemm_tma<BN, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    attr = true;
+  }
+  const int n_m = (int)((M + kBM - 1) / kBM), n_n = (L.Npad + BN - 1) / BN;
+  const int grid = (int)std::min<int64_t>((int64_t)n_m * n_n, num_sms());
+  TmaGeom G{P.im2col, L.OH, L.OW, L.S, L.KW, L.C};
+  k_gemm_tma<BN, KB><<<grid, kThreads, C::SMEM, st>>>(*(const CUtensorMap *)P.mapA, *(const CUtensorMap *)P.mapB,
+                                                     L, G, M, out, n_m, n_n);
+}
+
+}  // namespace
+
+// Build the A / B tensor maps of a layer whose input is the fixed buffer `in`
+// holding up to `cap_img` images. Returns false if the layer cannot use TMA.
+bool tma_plan(TmaPlan &P, const Layer &L, const void *in, int64_t cap_img) {
+  P.ok = false;
+  if (L.in_u8 || L.K % 32 || L.Npad % 16 || !load_driver()) return false;
+  const bool conv = !(L.OH == 1 && L.OW == 1 && L.KH == L.H && L.KW == L.W);
+  int KB;
+  if (conv) {
+    if (L.C != 32 && L.C != 64) return false;
+    KB = L.C;
+  } else {
+    KB = 64;
+    if (L.K % 64) return false;
+  }
+  P.kb = KB;
+  P.im2col = conv ? 1 : 0;
+  P.bn = L.Npad <= 32 ? 32 : L.Npad <= 64 ? 64 : 256;
+  const CUtensorMapSwizzle sw = KB == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+  CUtensorMap *ma = (CUtensorMap *)P.mapA, *mb = (CUtensorMap *)P.mapB;
+  CUresult r;
+  if (conv) {
+    cuuint64_t dims[4] = {(cuuint64_t)L.C, (cuuint64_t)L.W, (cuuint64_t)L.H, (cuuint64_t)cap_img};
+    cuuint64_t strides[3] = {(cuuint64_t)L.C * 2, (cuuint64_t)L.W * L.C * 2, (cuuint64_t)L.in_img_stride * 2};
+    int lower[2] = {0, 0};
+    int upper[2] = {-(L.KW - 1), -(L.KH - 1)};
+    cuuint32_t estr[4] = {1, (cuuint32_t)L.S, (cuuint32_t)L.S, 1};
+    r = g_encode_im2col(ma, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(in), dims, strides, lower, upper,
+                        (cuuint32_t)L.C, (cuuint32_t)kBM, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    cuuint64_t dims[2] = {(cuuint64_t)L.K, (cuuint64_t)cap_img};
+    cuuint64_t strides[1] = {(cuuint64_t)L.in_img_stride * 2};
+    cuuint32_t box[2] = {(cuuint32_t)KB, (cuuint32_t)kBM};
+    cuuint32_t estr[2] = {1, 1};
+    r = g_encode_tiled(ma, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                       const_cast<__nv_bfloat16 *>((const __nv_bfloat16 *)in) + L.in_col_off, dims, strides, box, estr,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  if (r != CUDA_SUCCESS) return false;
+  {
+    cuuint64_t dims[2] = {(cuuint64_t)L.K, (cuuint64_t)L.Npad};
+    cuuint64_t strides[1] = {(cuuint64_t)L.K * 2};
+    cuuint32_t box[2] = {(cuuint32_t)KB, (cuuint32_t)P.bn};
+    cuuint32_t estr[2] = {1, 1};
+    r = g_encode_tiled(mb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<__nv_bfloat16 *>(L.Wt), dims, strides, box,
+                       estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  if (r != CUDA_SUCCESS) return false;
+  P.ok = true;
+  return true;
+}
+
+void launch_layer_tma(const TmaPlan &P, const Layer &L, int64_t n_img, void *out, cudaStream_t st) {
+  const int64_t M = n_img * L.rows_per_img();
+  if (M <= 0) return;
+  if (P.kb == 32) {
+    if (P.bn == 64) launch_gemm<64, 32>(P, L, M, out, st);
+    else if (P.bn == 32) launch_gemm<32, 32>(P, L, M, out, st);
+    else launch_gemm<256, 32>(P, L, M, out, st);
+  } else {
+    if (P.bn == 64) launch_gemm<64, 64>(P, L, M, out, st);
+    else if (P.bn == 32) launch_gemm<32, 64>(P, L, M, out, st);
+    else launch_gemm<256, 64>(P, L, M, out, st);
+  }
+}
+
+}  // namespace bcts
