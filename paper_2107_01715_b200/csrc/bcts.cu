@@ -175,14 +175,20 @@ bcts_status validate(bcts_handle h, const void *roots, int64_t n_roots, int32_t 
   return BCTS_OK;
 }
 
-// Largest leaf chunk (multiple of A) that fits the budget: big level (Lc),
-// small level (Lc/A + 2), leaf totals (Lc).
+// Largest leaf chunk (multiple of A) that fits the budget. Materialised
+// leaves: big level (Lc) + small level (Lc/A + 2) + leaf totals (Lc). Fused
+// leaves (conv nets: the leaf level is generated inside the net): big level
+// d-1 (Lc/A + 2) + small level (Lc/A^2 + 2) + totals.
+bool fused_leaves(bcts_handle h) { return net_fuses_leaves(h->net) && h->env == BCTS_ENV_ATARI_HASH; }
+
 int64_t plan_chunk(bcts_handle h, int64_t range, size_t reserved) {
   const int64_t nb = node_bytes(h->env);
   const int64_t budget = h->ws_max - (int64_t)reserved - (1 << 20);
   if (budget <= 0) return 0;
-  int64_t lc = (int64_t)((double)budget / ((double)nb * (1.0 + 1.0 / h->A) + 4.0));
-  lc -= 2 * h->A;
+  const double A = h->A;
+  const double per_leaf = fused_leaves(h) ? nb * (1.0 / A + 1.0 / (A * A)) + 4.0 : nb * (1.0 + 1.0 / A) + 4.0;
+  int64_t lc = (int64_t)((double)budget / per_leaf);
+  lc -= 4 * h->A;
   lc = lc / h->A * h->A;
   const int64_t need = (range + h->A - 1) / h->A * h->A;
   return std::min(lc, need);
@@ -190,8 +196,13 @@ int64_t plan_chunk(bcts_handle h, int64_t range, size_t reserved) {
 
 size_t chunk_bytes(bcts_handle h, int64_t lc) {
   Carver c(nullptr);
-  c.level(h->env, lc);
-  c.level(h->env, lc / h->A + 2);
+  if (fused_leaves(h)) {
+    c.level(h->env, lc / h->A + 2);
+    c.level(h->env, lc / h->A / h->A + 2);
+  } else {
+    c.level(h->env, lc);
+    c.level(h->env, lc / h->A + 2);
+  }
   c.take((size_t)lc * 4);
   return c.off;
 }
@@ -229,8 +240,11 @@ bcts_status run_shard(bcts_handle h, const void *roots, int32_t d, float gamma, 
   if (lc < A) return fail(h, BCTS_ERR_BUDGET, "workspace budget too small for one chunk of leaves");
   if (reserved + chunk_bytes(h, lc) > h->ws_size) return fail(h, BCTS_ERR_BUDGET, "workspace not sized");
   bcts_status s = BCTS_OK;
+  const bool fused = fused_leaves(h);
+  const int dm = fused ? d - 1 : d;   // deepest level materialised in the workspace
   Carver c(h->ws + reserved);
-  LevelBuf big = c.level(h->env, lc), small = c.level(h->env, lc / A + 2);
+  LevelBuf big = fused ? c.level(h->env, lc / A + 2) : c.level(h->env, lc);
+  LevelBuf small = fused ? c.level(h->env, lc / A / A + 2) : c.level(h->env, lc / A + 2);
   float *totals = (float *)c.take((size_t)lc * 4);
   int64_t nchunks = 0, trans = 0, lvl_launch = 0;
   for (int64_t L = L0; L < L1; L += lc) {
@@ -241,17 +255,23 @@ bcts_status run_shard(bcts_handle h, const void *roots, int32_t d, float gamma, 
       hi[k] = (Le - 1) / pw[d - k] + 1;
     }
     NodeView prev = root_view(h->env, roots, lo[0]);
-    for (int k = 1; k <= d; ++k) {
-      const LevelBuf &b = ((d - k) % 2 == 0) ? big : small;
+    for (int k = 1; k <= dm; ++k) {
+      const LevelBuf &b = ((dm - k) % 2 == 0) ? big : small;
       launch_expand(h->env, prev, lo[k - 1], lo[k], hi[k], A, g[k - 1], h->d_next, h->d_rew, out_of(h->env, b),
                     h->st, &h->prof);
       prev = view_of(h->env, b);
       trans += hi[k] - lo[k];
       ++lvl_launch;
     }
-    const int nl = net_eval(h->net, prev, Le - L, MODE_TOTAL, g[d], totals, h->st);
+    int nl;
+    if (fused) {   // leaf level generated inside the net (s2d frames, L2-resident)
+      nl = net_eval_children(h->net, prev, lo[d - 1], L, Le, A, g[d - 1], MODE_TOTAL, g[d], totals, h->st);
+      trans += Le - L;
+    } else {
+      nl = net_eval(h->net, prev, Le - L, MODE_TOTAL, g[d], totals, h->st);
+    }
     launch_segmax(totals, Le - L, L, pw[d], pw[d - 1], A, keys, h->st, &h->prof);
-    h->launches += d + nl + 1;
+    h->launches += dm + nl + 1;
     ++nchunks;
     if ((s = cuda_check(h, "shard chunk"))) return s;
   }
@@ -415,6 +435,7 @@ bcts_status bcts_create(const bcts_config *cfg, bcts_handle *out) {
     return BCTS_ERR_INVALID_ARG;
   }
   h->net.tc = !(cfg->flags & BCTS_F_SIMT_NET);
+  h->net.sw = true;
   h->net.prof = &h->prof;
   *out = h;
   return BCTS_OK;

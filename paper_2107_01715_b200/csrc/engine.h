@@ -77,6 +77,13 @@ void launch_expand(int env, const NodeView &par, int64_t p_first, int64_t c_begi
                    float gk, const int32_t *tab_next, const float *tab_rew, const NodeOut &out,
                    cudaStream_t st, Profiler *prof = nullptr);
 
+// s2d bf16 frames for the conv1 tensor-core layer (expand.cu)
+// planar != 0: write the chunk-planar layout (plane = bytes per 8-channel plane,
+// image stride 8*plane); 0: dense [21][21][64] bf16.
+void launch_s2d_convert(const NodeView &v, int64_t first, int64_t n, void *out, uint32_t planar, cudaStream_t st);
+void launch_expand_s2d(const NodeView &par, int64_t p_first, int64_t c_begin, int64_t c_end, int A, float gk,
+                       void *out, uint32_t planar, float *cum_out, cudaStream_t st, Profiler *prof);
+
 // -------------------------------------------------------- implicit-GEMM layer
 // out[m][n] = act( sum_k X[m][k] * W[n][k] + b[n] ), X gathered im2col-style
 // from an NHWC input (k = (ky, kx, c)); used for every conv and fc layer.
@@ -105,6 +112,20 @@ struct TmaPlan {
 bool tma_plan(TmaPlan &P, const Layer &L, const void *in, int64_t cap_img);
 void launch_layer_tma(const TmaPlan &P, const Layer &L, int64_t n_img, void *out, cudaStream_t st);
 
+// Shifted-window conv layer (qnet_conv.cu): stride-1 conv over a per-image
+// chunk-planar K-major activation (byte(row r, chunk j) = j*plane + r*16).
+struct ConvSW {
+  int N = 0, K = 0, Cin = 0, KH = 0, KW = 0, W_in = 0, OH = 0, OW = 0, n_mt = 0;
+  uint32_t plane = 0, in_img_bytes = 0;        // input: planar, Cin/8 planes
+  uint32_t out_img_bytes = 0, out_plane = 0;   // output layout of the next layer
+  int out_w = 0, out_mode = 0;                 // 0: s2d(2) planar, 1: planar, 2: dense [row][N]
+};
+void launch_conv_sw(const ConvSW &P, const Layer &L, const void *in, int64_t n_img, void *out, cudaStream_t st);
+// planar geometry of the three trunk inputs
+constexpr uint32_t kPlane1 = 536 * 16, kIn1Bytes = 8 * kPlane1;      // s2d(4) frame: 21x21 rows, 64 ch
+constexpr uint32_t kPlane2 = 144 * 16, kIn2Bytes = 16 * kPlane2;     // s2d(2) act1: 10x10 rows, 128 ch
+constexpr uint32_t kPlane3 = 152 * 16, kIn3Bytes = 8 * kPlane3;      // act2: 9x9 rows, 64 ch
+
 // Net output modes.
 enum { MODE_ROWS = 0, MODE_ROWMAX = 1, MODE_TOTAL = 2 };
 
@@ -123,7 +144,13 @@ struct Net {
   // scratch: trunk sub-batches of `batch` images (conv activations stay
   // L2-resident), fc layers over `fc_batch` images at a time
   int64_t batch = 0, fc_batch = 0;
-  TmaPlan p_c2, p_c3, p_fc_h, p_z_v, p_z_a, p_fc2;
+  TmaPlan p_c1, p_c2, p_c3, p_fc_h, p_z_v, p_z_a, p_fc2;
+  __nv_bfloat16 *s2d = nullptr;   // [batch][21][21][64] conv1 input (dense; SIMT / TMA paths)
+  uint8_t *in1p = nullptr, *act1p = nullptr, *act2p = nullptr;  // planar trunk buffers [batch]
+  Layer c2s;                      // conv2 as 2x2 stride-1 over s2d(2) of act1 (shifted windows)
+  ConvSW sw1, sw2, sw3;
+  bool sw = false;                // shifted-window trunk enabled
+  float *leaf_cum = nullptr;      // [fc_batch] R_d of fused-expanded leaves
   __nv_bfloat16 *act1 = nullptr, *act2 = nullptr, *act3 = nullptr, *hid_act = nullptr;
   float *zv = nullptr, *za = nullptr;
   int64_t ld_za = 0, ld_zv = 0;
@@ -136,6 +163,12 @@ struct Net {
 // out[n] = max_a Q; MODE_TOTAL: out[n] = fmaf(gd, max_a Q, cum[i]).
 // Returns the number of kernels launched, or -1 on a CUDA error.
 int net_eval(Net &net, const NodeView &v, int64_t n, int mode, float gd, float *out, cudaStream_t st);
+// Conv nets only: evaluate the children [c_begin, c_end) of the parents in view
+// `par` (global level indices from p_first), generating each child's frames on
+// the fly (fused last-level expansion, gk = g[d-1]); out[i] per MODE.
+bool net_fuses_leaves(const Net &net);
+int net_eval_children(Net &net, const NodeView &par, int64_t p_first, int64_t c_begin, int64_t c_end, int A,
+                      float gk, int mode, float gd, float *out, cudaStream_t st);
 int net_build(Net &net, const bcts_config &cfg, std::string &err);  // 0 ok
 void net_free(Net &net);
 

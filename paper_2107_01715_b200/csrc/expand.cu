@@ -170,3 +170,104 @@ void launch_expand(int env, const NodeView &par, int64_t p_first, int64_t c_begi
 }
 
 }  // namespace bcts
+
+// ================================================================ s2d frames
+// Space-to-depth(4) bf16 layout of a frame stack for the conv1 tensor-core
+// layer: S[Y][X][c'] with Y, X in [0, 21) and c' = (dy*4 + dx)*4 + c holds
+// frame byte c of pixel (4Y+dy, 4X+dx). conv1 (8x8, stride 4, 4 channels)
+// becomes a 2x2 stride-1 conv over 64 channels whose im2col the TMA engine
+// gathers (qnet_tma.cu). The 16 bytes of one (Y, X, dy) row segment are
+// contiguous in the NHWC frame, so each segment converts with one 16-byte
+// load. u8 -> bf16 is exact: f = as_float(0x4B0000bb) - 2^23 (PRMT + FADD).
+namespace bcts {
+
+constexpr int kS2dPix = 21 * 21;              // 441 s2d pixels
+constexpr int kS2dElems = kS2dPix * 64;       // 28,224 bf16 per image
+
+__device__ __forceinline__ uint32_t u8pair_to_bf16x2(uint32_t w, uint32_t i) {
+  const float f0 = __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7540u + i)) - 8388608.0f;
+  const float f1 = __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7540u + i + 1)) - 8388608.0f;
+  return __byte_perm(__float_as_uint(f0), __float_as_uint(f1), 0x7632u);
+}
+__device__ __forceinline__ void u8x16_to_bf16(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3, uint4 &lo,
+                                              uint4 &hi) {
+  lo = make_uint4(u8pair_to_bf16x2(w0, 0), u8pair_to_bf16x2(w0, 2), u8pair_to_bf16x2(w1, 0), u8pair_to_bf16x2(w1, 2));
+  hi = make_uint4(u8pair_to_bf16x2(w2, 0), u8pair_to_bf16x2(w2, 2), u8pair_to_bf16x2(w3, 0), u8pair_to_bf16x2(w3, 2));
+}
+
+// images [first, first + n) of view v -> s2d (one task per (image, s2d pixel, dy))
+__device__ __forceinline__ void s2d_store(void *out, uint32_t planar, int64_t img, int pix, int dy, const uint4 &lo,
+                                          const uint4 &hi) {
+  if (planar) {   // chunk-planar: channels dy*16 .. dy*16+15 = planes 2dy, 2dy+1, row = pix
+    uint8_t *base = (uint8_t *)out + img * (int64_t)(8 * planar) + (int64_t)pix * 16;
+    *(uint4 *)(base + (size_t)(2 * dy) * planar) = lo;
+    *(uint4 *)(base + (size_t)(2 * dy + 1) * planar) = hi;
+  } else {
+    uint4 *dst = (uint4 *)((__nv_bfloat16 *)out + img * kS2dElems + pix * 64 + dy * 16);
+    dst[0] = lo;
+    dst[1] = hi;
+  }
+}
+
+__global__ void k_s2d_convert(NodeView v, int64_t first, int64_t n, void *__restrict__ out, uint32_t planar) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * kS2dPix * 4) return;
+  const int64_t img = t / (kS2dPix * 4);
+  const int rem = (int)(t - img * (kS2dPix * 4));
+  const int pix = rem >> 2, dy = rem & 3;
+  const int Y = pix / 21, X = pix - Y * 21;
+  const uint4 w = __ldg((const uint4 *)(v.state + (first + img) * v.state_stride) + ((4 * Y + dy) * 84 + 4 * X) / 4);
+  uint4 lo, hi;
+  u8x16_to_bf16(w.x, w.y, w.z, w.w, lo, hi);
+  s2d_store(out, planar, img, pix, dy, lo, hi);
+}
+
+void launch_s2d_convert(const NodeView &v, int64_t first, int64_t n, void *out, uint32_t planar, cudaStream_t st) {
+  const int64_t tasks = n * kS2dPix * 4;
+  if (tasks > 0) k_s2d_convert<<<(unsigned)((tasks + 255) / 256), 256, 0, st>>>(v, first, n, out, planar);
+}
+
+// Fused last-level expansion (Alg. 1 loop body at i_d = d-1) that
+// writes each child's frame stack directly as the conv1 input (s2d bf16) plus
+// its R_d: the leaf level is never materialised as uint8 frames in HBM. One
+// task per (child, s2d pixel, dy): the 16 parent bytes come straight from L2
+// (siblings share the parent, which stays cached), one mix64 supplies the 4
+// noise bytes, and the child's 16 bytes convert to 16 bf16.
+__global__ void k_expand_s2d(NodeView par, int64_t p_first, int64_t c_begin, int64_t n, int A, float gk,
+                             void *__restrict__ out, uint32_t planar, float *__restrict__ cum_out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * kS2dPix * 4) return;
+  const int64_t ci = t / (kS2dPix * 4);
+  const int rem = (int)(t - ci * (kS2dPix * 4));
+  const int pix = rem >> 2, dy = rem & 3;
+  const int64_t c = c_begin + ci, p = c / A;
+  const int a = (int)(c - p * A);
+  const int64_t pl = p - p_first;
+  const uint64_t k2 = atari_child_key(*(const uint64_t *)((const uint8_t *)par.key + pl * par.key_stride), a);
+  const int Y = pix / 21, X = pix - Y * 21;
+  const int p0 = (4 * Y + dy) * 84 + 4 * X;                // first of 4 pixels, p0 % 4 == 0
+  const uint4 x = __ldg((const uint4 *)(par.state + pl * par.state_stride) + (p0 >> 2));
+  const uint32_t nz = (uint32_t)(mix64(k2 + (uint64_t)(p0 >> 3)) >> (8 * (p0 & 7)));
+  const uint32_t w0 = (x.x >> 8) | ((x.x ^ (nz << 24)) & 0xFF000000u);
+  const uint32_t w1 = (x.y >> 8) | ((x.y ^ ((nz >> 8) << 24)) & 0xFF000000u);
+  const uint32_t w2 = (x.z >> 8) | ((x.z ^ ((nz >> 16) << 24)) & 0xFF000000u);
+  const uint32_t w3 = (x.w >> 8) | ((x.w ^ (nz & 0xFF000000u)) & 0xFF000000u);
+  uint4 lo, hi;
+  u8x16_to_bf16(w0, w1, w2, w3, lo, hi);
+  s2d_store(out, planar, ci, pix, dy, lo, hi);
+  if (rem == 0) cum_out[ci] = fmaf(gk, atari_reward(k2), par.cum ? par.cum[pl] : 0.0f);
+}
+
+void launch_expand_s2d(const NodeView &par, int64_t p_first, int64_t c_begin, int64_t c_end, int A, float gk,
+                       void *out, uint32_t planar, float *cum_out, cudaStream_t st, Profiler *prof) {
+  const int64_t n = c_end - c_begin;
+  if (n <= 0) return;
+  const int64_t nparents = (c_end - 1) / A - c_begin / A + 1;
+  // algorithmic bytes: parent frames read once + children written (s2d bf16 + R)
+  if (prof) prof->begin(KC_EXPAND_ATARI, (double)nparents * (kFrameBytes + 12) + (double)n * (2.0 * kS2dElems + 4), st);
+  const int64_t tasks = n * kS2dPix * 4;
+  k_expand_s2d<<<(unsigned)((tasks + 255) / 256), 256, 0, st>>>(par, p_first, c_begin, n, A, gk, out, planar, cum_out);
+  if (prof) prof->end(st);
+}
+
+}  // namespace bcts

@@ -302,13 +302,18 @@ int net_build(Net &net, const bcts_config &cfg, std::string &err) {
   net.atoms = atoms;
   net.vmin = cfg.v_min;
   net.vmax = cfg.v_max;
-  // conv1: OIHW [32][4][8][8], input uint8 NHWC C=4
+  // conv1: OIHW [32][4][8][8] over uint8 NHWC frames, computed as a 2x2
+  // stride-1 conv over the space-to-depth(4) bf16 frame S[21][21][64] with
+  // c' = (dy*4 + dx)*4 + c:  W'[o][(ty*2 + tx)*64 + c'] = W[o][c][4ty+dy][4tx+dx].
   {
     Layer &L = net.c1;
-    L.in_u8 = 1; L.H = L.W = 84; L.C = 4; L.KH = L.KW = 8; L.S = 4; L.OH = L.OW = 20; L.K = 256;
-    L.relu_bf16 = 1; L.out_ld = 32;
-    if (make_layer(net, L, repack(32, 32, 8, 8, 4, [](int o, int ky, int kx, int c) { return ((o * 4 + c) * 8 + ky) * 8 + kx; }, w),
-                   w + 32 * 256, 32, 32, err)) return -1;
+    L.H = L.W = 21; L.C = 64; L.KH = L.KW = 2; L.S = 1; L.OH = L.OW = 20; L.K = 256;
+    L.relu_bf16 = 1; L.out_ld = 32; L.in_img_stride = 21 * 21 * 64;
+    auto src = [](int o, int ty, int tx, int cp) {
+      const int c = cp & 3, dx = (cp >> 2) & 3, dy = cp >> 4;
+      return ((o * 4 + c) * 8 + (4 * ty + dy)) * 8 + (4 * tx + dx);
+    };
+    if (make_layer(net, L, repack(32, 32, 2, 2, 64, src, w), w + 32 * 256, 32, 32, err)) return -1;
     w += 32 * 256 + 32;
   }
   {
@@ -317,6 +322,16 @@ int net_build(Net &net, const bcts_config &cfg, std::string &err) {
     L.in_img_stride = 20 * 20 * 32;
     if (make_layer(net, L, repack(64, 64, 4, 4, 32, [](int o, int ky, int kx, int c) { return ((o * 32 + c) * 4 + ky) * 4 + kx; }, w),
                    w + 64 * 512, 64, 64, err)) return -1;
+    // the same conv as a 2x2 stride-1 conv over space-to-depth(2) of act1
+    // (c2 = (dy*2 + dx)*32 + c): W'[o][(ty*2 + tx)*128 + c2] = W[o][c][2ty+dy][2tx+dx]
+    Layer &S = net.c2s;
+    S = L;
+    S.H = S.W = 10; S.C = 128; S.KH = S.KW = 2; S.S = 1;
+    auto src2 = [](int o, int ty, int tx, int c2) {
+      const int c = c2 & 31, dx = (c2 >> 5) & 1, dy = c2 >> 6;
+      return ((o * 32 + c) * 4 + (2 * ty + dy)) * 4 + (2 * tx + dx);
+    };
+    if (make_layer(net, S, repack(64, 64, 2, 2, 128, src2, w), w + 64 * 512, 64, 64, err)) return -1;
     w += 64 * 512 + 64;
   }
   {
@@ -376,22 +391,43 @@ int net_build(Net &net, const bcts_config &cfg, std::string &err) {
     net.ld_zv = Nv;
     net.ld_za = Na;
   }
-  // scratch: trunk sub-batches of 2048 images (act1/act2 stay L2-resident),
-  // fc layers over 16384 images at a time (enough M tiles to fill 148 SMs)
-  net.batch = 2048;
+  // scratch: trunk sub-batches of 1024 images (s2d frames, act1, act2 stay
+  // L2-resident: ~94 MB), fc layers over 16384 images at a time (enough M
+  // tiles to fill 148 SMs)
+  net.batch = 1024;
   net.fc_batch = 16384;
   const int64_t B = net.batch, FB = net.fc_batch;
-  size_t bytes[6] = {(size_t)B * 400 * 32 * 2, (size_t)B * 81 * 64 * 2, (size_t)FB * 49 * 64 * 2,
-                     (size_t)FB * hidN * 2, (size_t)FB * (rainbow ? net.ld_zv : 16) * 4, (size_t)FB * net.ld_za * 4};
-  void *p[6];
-  for (int t = 0; t < 6; ++t) {
+  size_t bytes[11] = {(size_t)B * 400 * 32 * 2, (size_t)B * 81 * 64 * 2, (size_t)FB * 49 * 64 * 2,
+                      (size_t)FB * hidN * 2, (size_t)FB * (rainbow ? net.ld_zv : 16) * 4, (size_t)FB * net.ld_za * 4,
+                      (size_t)B * 21 * 21 * 64 * 2, (size_t)FB * 4, (size_t)B * kIn1Bytes, (size_t)B * kIn2Bytes,
+                      (size_t)B * kIn3Bytes};
+  void *p[11];
+  for (int t = 0; t < 11; ++t) {
     if (cudaMalloc(&p[t], bytes[t]) != cudaSuccess) { err = "cudaMalloc net scratch failed"; return -1; }
     net.allocs.push_back(p[t]);
   }
   net.act1 = (__nv_bfloat16 *)p[0]; net.act2 = (__nv_bfloat16 *)p[1]; net.act3 = (__nv_bfloat16 *)p[2];
   net.hid_act = (__nv_bfloat16 *)p[3]; net.zv = (float *)p[4]; net.za = (float *)p[5];
+  net.s2d = (__nv_bfloat16 *)p[6]; net.leaf_cum = (float *)p[7];
+  net.in1p = (uint8_t *)p[8]; net.act1p = (uint8_t *)p[9]; net.act2p = (uint8_t *)p[10];
+  // shifted-window trunk geometry (qnet_conv.cu)
+  {
+    ConvSW &a = net.sw1;
+    a.N = 32; a.K = 256; a.Cin = 64; a.KH = a.KW = 2; a.W_in = 21; a.OH = a.OW = 20; a.n_mt = (20 * 21 + 127) / 128;
+    a.plane = kPlane1; a.in_img_bytes = kIn1Bytes;
+    a.out_mode = 0; a.out_plane = kPlane2; a.out_w = 10; a.out_img_bytes = kIn2Bytes;
+    ConvSW &b = net.sw2;
+    b.N = 64; b.K = 512; b.Cin = 128; b.KH = b.KW = 2; b.W_in = 10; b.OH = b.OW = 9; b.n_mt = (9 * 10 + 127) / 128;
+    b.plane = kPlane2; b.in_img_bytes = kIn2Bytes;
+    b.out_mode = 1; b.out_plane = kPlane3; b.out_w = 9; b.out_img_bytes = kIn3Bytes;
+    ConvSW &c = net.sw3;
+    c.N = 64; c.K = 576; c.Cin = 64; c.KH = c.KW = 3; c.W_in = 9; c.OH = c.OW = 7; c.n_mt = (7 * 9 + 127) / 128;
+    c.plane = kPlane3; c.in_img_bytes = kIn3Bytes;
+    c.out_mode = 2; c.out_plane = 0; c.out_w = 7; c.out_img_bytes = 3136 * 2;
+  }
   // TMA plans (tensor maps over the fixed scratch buffers; fall back to the
   // thread-gather tcgen05 layer if the driver entry points are unavailable)
+  tma_plan(net.p_c1, net.c1, net.s2d, B);
   tma_plan(net.p_c2, net.c2, net.act1, B);
   tma_plan(net.p_c3, net.c3, net.act2, B);
   tma_plan(net.p_fc_h, net.fc_h, net.act3, FB);
@@ -420,41 +456,53 @@ static void run_layer(const Net &net, int cls, const Layer &L, const void *in, i
   if (net.prof) net.prof->end(st);
 }
 
-int net_eval(Net &net, const NodeView &v, int64_t n, int mode, float gd, float *out, cudaStream_t st) {
-  if (n <= 0) return 0;
+// Conv-net evaluation over n images that come either from a view of frame
+// stacks (`img`, images [0, n)) or are the children [c_begin, c_begin + n) of
+// the parents in `par` (fused last-level expansion). Trunk in L2-sized
+// sub-batches: frames -> s2d bf16 -> conv1 -> conv2 -> conv3 (act3 of the fc
+// batch); then fc_hidden, the output layer(s) and the head.
+static int eval_conv(Net &net, const NodeView *par, const NodeView *img, int64_t p_first, int64_t c_begin, float gk,
+                     int64_t n, int mode, float gd, float *out, cudaStream_t st) {
   const int A = net.A;
-  int launches = 0;
-  if (net.kind == BCTS_NET_TABLE) {
-    if (net.prof) net.prof->begin(KC_TABLE, (double)n * (8.0 + 4.0 * A), st);
-    k_table<<<(unsigned)((n + 255) / 256), 256, 0, st>>>((const int32_t *)v.state, v.state_stride, net.tq, A, n, mode,
-                                                          gd, v.cum, out);
-    if (net.prof) net.prof->end(st);
-    return 1;
-  }
-  if (net.kind == BCTS_NET_MLP2_F32) {
-    if (net.prof) net.prof->begin(KC_MLP, 2.0 * (double)n * ((double)net.in * net.hid + (double)net.hid * A), st);
-    k_mlp<<<(unsigned)((n + kMlpWarps - 1) / kMlpWarps), 32 * kMlpWarps, 0, st>>>(
-        v.state, v.state_stride, net.l1w, net.l1b, net.l2w, net.l2b, net.in, net.hid, A, n, mode, gd, v.cum, out);
-    if (net.prof) net.prof->end(st);
-    return 1;
-  }
   const bool rainbow = net.kind == BCTS_NET_RAINBOW_BF16;
+  int launches = 0;
   for (int64_t f0 = 0; f0 < n; f0 += net.fc_batch) {
     const int64_t nf = n - f0 < net.fc_batch ? n - f0 : net.fc_batch;
-    // conv trunk in L2-sized sub-batches; conv3 writes into the fc-batch act3 buffer
     for (int64_t b0 = 0; b0 < nf; b0 += net.batch) {
       const int64_t nb = nf - b0 < net.batch ? nf - b0 : net.batch;
-      Layer c1 = net.c1;
-      c1.in_img_stride = v.state_stride;
-      run_layer(net, KC_CONV1, c1, v.state + (f0 + b0) * v.state_stride, nb, net.act1, st);
-      run_layer(net, KC_CONV2, net.c2, net.act1, nb, net.act2, st, &net.p_c2);
-      run_layer(net, KC_CONV3, net.c3, net.act2, nb, net.act3 + b0 * 3136, st, &net.p_c3);
-      launches += 3;
+      const bool sw = net.tc && net.sw;
+      void *in1 = sw ? (void *)net.in1p : (void *)net.s2d;
+      const uint32_t planar = sw ? kPlane1 : 0;
+      if (par) {
+        launch_expand_s2d(*par, p_first, c_begin + f0 + b0, c_begin + f0 + b0 + nb, A, gk, in1, planar,
+                          net.leaf_cum + b0, st, net.prof);
+      } else {
+        if (net.prof) net.prof->begin(KC_OTHER, (double)nb * (kFrameBytes + 2.0 * 28224), st);
+        launch_s2d_convert(*img, f0 + b0, nb, in1, planar, st);
+        if (net.prof) net.prof->end(st);
+      }
+      if (sw) {
+        const double fl = 2.0 * (double)nb;
+        if (net.prof) net.prof->begin(KC_CONV1, fl * 400 * 32 * 256, st);
+        launch_conv_sw(net.sw1, net.c1, net.in1p, nb, net.act1p, st);
+        if (net.prof) net.prof->end(st);
+        if (net.prof) net.prof->begin(KC_CONV2, fl * 81 * 64 * 512, st);
+        launch_conv_sw(net.sw2, net.c2s, net.act1p, nb, net.act2p, st);
+        if (net.prof) net.prof->end(st);
+        if (net.prof) net.prof->begin(KC_CONV3, fl * 49 * 64 * 576, st);
+        launch_conv_sw(net.sw3, net.c3, net.act2p, nb, net.act3 + b0 * 3136, st);
+        if (net.prof) net.prof->end(st);
+      } else {
+        run_layer(net, KC_CONV1, net.c1, net.s2d, nb, net.act1, st, &net.p_c1);
+        run_layer(net, KC_CONV2, net.c2, net.act1, nb, net.act2, st, &net.p_c2);
+        run_layer(net, KC_CONV3, net.c3, net.act2, nb, net.act3 + b0 * 3136, st, &net.p_c3);
+      }
+      launches += 4;
     }
     run_layer(net, KC_FC_H, net.fc_h, net.act3, nf, net.hid_act, st, &net.p_fc_h);
     launches += 1;
     float *o = out + (mode == MODE_ROWS ? f0 * A : f0);
-    const float *cum = v.cum ? v.cum + f0 : nullptr;
+    const float *cum = par ? net.leaf_cum : (img->cum ? img->cum + f0 : nullptr);
     if (!rainbow) {
       run_layer(net, KC_FC_OUT, net.fc2, net.hid_act, nf, net.za, st, &net.p_fc2);
       if (net.prof) net.prof->begin(KC_HEAD, (double)nf * 4.0 * (net.ld_za + 1), st);
@@ -474,6 +522,36 @@ int net_eval(Net &net, const NodeView &v, int64_t n, int mode, float gd, float *
     }
   }
   return launches;
+}
+
+bool net_fuses_leaves(const Net &net) {
+  return net.kind == BCTS_NET_NATURE_BF16 || net.kind == BCTS_NET_RAINBOW_BF16;
+}
+
+int net_eval_children(Net &net, const NodeView &par, int64_t p_first, int64_t c_begin, int64_t c_end, int A,
+                      float gk, int mode, float gd, float *out, cudaStream_t st) {
+  (void)A;
+  return eval_conv(net, &par, nullptr, p_first, c_begin, gk, c_end - c_begin, mode, gd, out, st);
+}
+
+int net_eval(Net &net, const NodeView &v, int64_t n, int mode, float gd, float *out, cudaStream_t st) {
+  if (n <= 0) return 0;
+  const int A = net.A;
+  if (net.kind == BCTS_NET_TABLE) {
+    if (net.prof) net.prof->begin(KC_TABLE, (double)n * (8.0 + 4.0 * A), st);
+    k_table<<<(unsigned)((n + 255) / 256), 256, 0, st>>>((const int32_t *)v.state, v.state_stride, net.tq, A, n, mode,
+                                                          gd, v.cum, out);
+    if (net.prof) net.prof->end(st);
+    return 1;
+  }
+  if (net.kind == BCTS_NET_MLP2_F32) {
+    if (net.prof) net.prof->begin(KC_MLP, 2.0 * (double)n * ((double)net.in * net.hid + (double)net.hid * A), st);
+    k_mlp<<<(unsigned)((n + kMlpWarps - 1) / kMlpWarps), 32 * kMlpWarps, 0, st>>>(
+        v.state, v.state_stride, net.l1w, net.l1b, net.l2w, net.l2b, net.in, net.hid, A, n, mode, gd, v.cum, out);
+    if (net.prof) net.prof->end(st);
+    return 1;
+  }
+  return eval_conv(net, nullptr, &v, 0, 0, 0.0f, n, mode, gd, out, st);
 }
 
 }  // namespace bcts

@@ -257,7 +257,7 @@ def test_chunking_and_ragged_bit_identical():
     c5 = Config("C5s", ENV_ATARI_HASH, NET_RAINBOW_BF16, 18, 3, 2, 0.99, 1.0, seed=5, wseed=105)
     r5 = c5.roots()
     a = run(handle(c5), r5, 3, 0.99)
-    b = run(handle(c5, workspace_bytes_max=64 << 20), r5, 3, 0.99)
+    b = run(handle(c5, workspace_bytes_max=8 << 20), r5, 3, 0.99)
     assert b["stats"]["chunks"] > 1
     for k in ("actions", "root_q", "vanilla_q", "best_leaf"):
         np.testing.assert_array_equal(a[k], b[k])
