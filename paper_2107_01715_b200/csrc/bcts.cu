@@ -662,6 +662,10 @@ int32_t bcts_profile_read(bcts_handle h, bcts_kernel_profile *out, int32_t max) 
   return k;
 }
 
+// Test hook (not part of the public contract): route the shifted-window conv
+// kernel's CTA-0 phase timestamps to a device buffer (NULL disables).
+void bcts_debug_conv_trace(void *dev_buf, int32_t layer) { conv_trace_set((unsigned long long *)dev_buf, layer); }
+
 int64_t bcts_pack_key(float value, int64_t leaf_index) { return pack_key(value, leaf_index); }
 float bcts_key_value(int64_t key) { return key_value(key); }
 int64_t bcts_key_leaf(int64_t key) { return key_leaf(key); }

@@ -80,9 +80,10 @@ void launch_expand(int env, const NodeView &par, int64_t p_first, int64_t c_begi
 // s2d bf16 frames for the conv1 tensor-core layer (expand.cu)
 // planar != 0: write the chunk-planar layout (plane = bytes per 8-channel plane,
 // image stride 8*plane); 0: dense [21][21][64] bf16.
-void launch_s2d_convert(const NodeView &v, int64_t first, int64_t n, void *out, uint32_t planar, cudaStream_t st);
+void launch_s2d_convert(const NodeView &v, int64_t first, int64_t n, void *out, uint32_t planar, cudaStream_t st,
+                        int layout = 0);
 void launch_expand_s2d(const NodeView &par, int64_t p_first, int64_t c_begin, int64_t c_end, int A, float gk,
-                       void *out, uint32_t planar, float *cum_out, cudaStream_t st, Profiler *prof);
+                       void *out, uint32_t planar, float *cum_out, cudaStream_t st, Profiler *prof, int layout = 0);
 
 // -------------------------------------------------------- implicit-GEMM layer
 // out[m][n] = act( sum_k X[m][k] * W[n][k] + b[n] ), X gathered im2col-style
@@ -119,8 +120,21 @@ struct ConvSW {
   uint32_t plane = 0, in_img_bytes = 0;        // input: planar, Cin/8 planes
   uint32_t out_img_bytes = 0, out_plane = 0;   // output layout of the next layer
   int out_w = 0, out_mode = 0;                 // 0: s2d(2) planar, 1: planar, 2: dense [row][N]
+  const uint8_t *wsw = nullptr;                // weights pre-swizzled as their SW128 smem image
+  int layout = 0;                              // activation layout (see act_off)
 };
 void launch_conv_sw(const ConvSW &P, const Layer &L, const void *in, int64_t n_img, void *out, cudaStream_t st);
+void conv_trace_set(unsigned long long *p, int sel);
+// Trunk activation layout (runtime, BCTS_CONV_LAYOUT): 0 = chunk-planar
+// SWIZZLE_NONE; 1 = SW128 row blocks, descriptor base_offset = row phase;
+// 2 = SW128 row blocks, base_offset 0. In the SW128 layouts
+//   byte(r, c) = (c/64)*BPLANE + r*128 + ((((c%64)/8) ^ (r%8)) * 16) + (c%8)*2,
+// BPLANE = Rpad*128 (same total bytes as the planar layout).
+__host__ __device__ __forceinline__ uint32_t act_off(int layout, uint32_t plane16, int r, int chunk) {
+  // plane16 = planar plane bytes (Rpad*16); chunk = 8-channel chunk index
+  if (layout == 0) return (uint32_t)chunk * plane16 + (uint32_t)r * 16u;
+  return (uint32_t)(chunk >> 3) * (plane16 * 8u) + (uint32_t)r * 128u + (uint32_t)(((chunk & 7) ^ (r & 7)) << 4);
+}
 // planar geometry of the three trunk inputs
 constexpr uint32_t kPlane1 = 536 * 16, kIn1Bytes = 8 * kPlane1;      // s2d(4) frame: 21x21 rows, 64 ch
 constexpr uint32_t kPlane2 = 144 * 16, kIn2Bytes = 16 * kPlane2;     // s2d(2) act1: 10x10 rows, 128 ch

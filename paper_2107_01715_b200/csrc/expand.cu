@@ -196,12 +196,12 @@ __device__ __forceinline__ void u8x16_to_bf16(uint32_t w0, uint32_t w1, uint32_t
 }
 
 // images [first, first + n) of view v -> s2d (one task per (image, s2d pixel, dy))
-__device__ __forceinline__ void s2d_store(void *out, uint32_t planar, int64_t img, int pix, int dy, const uint4 &lo,
-                                          const uint4 &hi) {
-  if (planar) {   // chunk-planar: channels dy*16 .. dy*16+15 = planes 2dy, 2dy+1, row = pix
-    uint8_t *base = (uint8_t *)out + img * (int64_t)(8 * planar) + (int64_t)pix * 16;
-    *(uint4 *)(base + (size_t)(2 * dy) * planar) = lo;
-    *(uint4 *)(base + (size_t)(2 * dy + 1) * planar) = hi;
+__device__ __forceinline__ void s2d_store(void *out, uint32_t planar, int layout, int64_t img, int pix, int dy,
+                                          const uint4 &lo, const uint4 &hi) {
+  if (planar) {   // trunk layout: channels dy*16 .. dy*16+15 = chunks 2dy, 2dy+1 of row pix
+    uint8_t *base = (uint8_t *)out + img * (int64_t)(8 * planar);
+    *(uint4 *)(base + act_off(layout, planar, pix, 2 * dy)) = lo;
+    *(uint4 *)(base + act_off(layout, planar, pix, 2 * dy + 1)) = hi;
   } else {
     uint4 *dst = (uint4 *)((__nv_bfloat16 *)out + img * kS2dElems + pix * 64 + dy * 16);
     dst[0] = lo;
@@ -209,7 +209,8 @@ __device__ __forceinline__ void s2d_store(void *out, uint32_t planar, int64_t im
   }
 }
 
-__global__ void k_s2d_convert(NodeView v, int64_t first, int64_t n, void *__restrict__ out, uint32_t planar) {
+__global__ void k_s2d_convert(NodeView v, int64_t first, int64_t n, void *__restrict__ out, uint32_t planar,
+                              int layout) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n * kS2dPix * 4) return;
   const int64_t img = t / (kS2dPix * 4);
@@ -219,12 +220,13 @@ __global__ void k_s2d_convert(NodeView v, int64_t first, int64_t n, void *__rest
   const uint4 w = __ldg((const uint4 *)(v.state + (first + img) * v.state_stride) + ((4 * Y + dy) * 84 + 4 * X) / 4);
   uint4 lo, hi;
   u8x16_to_bf16(w.x, w.y, w.z, w.w, lo, hi);
-  s2d_store(out, planar, img, pix, dy, lo, hi);
+  s2d_store(out, planar, layout, img, pix, dy, lo, hi);
 }
 
-void launch_s2d_convert(const NodeView &v, int64_t first, int64_t n, void *out, uint32_t planar, cudaStream_t st) {
+void launch_s2d_convert(const NodeView &v, int64_t first, int64_t n, void *out, uint32_t planar, cudaStream_t st,
+                        int layout) {
   const int64_t tasks = n * kS2dPix * 4;
-  if (tasks > 0) k_s2d_convert<<<(unsigned)((tasks + 255) / 256), 256, 0, st>>>(v, first, n, out, planar);
+  if (tasks > 0) k_s2d_convert<<<(unsigned)((tasks + 255) / 256), 256, 0, st>>>(v, first, n, out, planar, layout);
 }
 
 // Fused last-level expansion (Alg. 1 loop body at i_d = d-1) that
@@ -234,7 +236,7 @@ void launch_s2d_convert(const NodeView &v, int64_t first, int64_t n, void *out, 
 // (siblings share the parent, which stays cached), one mix64 supplies the 4
 // noise bytes, and the child's 16 bytes convert to 16 bf16.
 __global__ void k_expand_s2d(NodeView par, int64_t p_first, int64_t c_begin, int64_t n, int A, float gk,
-                             void *__restrict__ out, uint32_t planar, float *__restrict__ cum_out) {
+                             void *__restrict__ out, uint32_t planar, float *__restrict__ cum_out, int layout) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n * kS2dPix * 4) return;
   const int64_t ci = t / (kS2dPix * 4);
@@ -254,19 +256,20 @@ __global__ void k_expand_s2d(NodeView par, int64_t p_first, int64_t c_begin, int
   const uint32_t w3 = (x.w >> 8) | ((x.w ^ (nz & 0xFF000000u)) & 0xFF000000u);
   uint4 lo, hi;
   u8x16_to_bf16(w0, w1, w2, w3, lo, hi);
-  s2d_store(out, planar, ci, pix, dy, lo, hi);
+  s2d_store(out, planar, layout, ci, pix, dy, lo, hi);
   if (rem == 0) cum_out[ci] = fmaf(gk, atari_reward(k2), par.cum ? par.cum[pl] : 0.0f);
 }
 
 void launch_expand_s2d(const NodeView &par, int64_t p_first, int64_t c_begin, int64_t c_end, int A, float gk,
-                       void *out, uint32_t planar, float *cum_out, cudaStream_t st, Profiler *prof) {
+                       void *out, uint32_t planar, float *cum_out, cudaStream_t st, Profiler *prof, int layout) {
   const int64_t n = c_end - c_begin;
   if (n <= 0) return;
   const int64_t nparents = (c_end - 1) / A - c_begin / A + 1;
   // algorithmic bytes: parent frames read once + children written (s2d bf16 + R)
   if (prof) prof->begin(KC_EXPAND_ATARI, (double)nparents * (kFrameBytes + 12) + (double)n * (2.0 * kS2dElems + 4), st);
   const int64_t tasks = n * kS2dPix * 4;
-  k_expand_s2d<<<(unsigned)((tasks + 255) / 256), 256, 0, st>>>(par, p_first, c_begin, n, A, gk, out, planar, cum_out);
+  k_expand_s2d<<<(unsigned)((tasks + 255) / 256), 256, 0, st>>>(par, p_first, c_begin, n, A, gk, out, planar, cum_out,
+                                                                 layout);
   if (prof) prof->end(st);
 }
 

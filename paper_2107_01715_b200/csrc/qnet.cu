@@ -5,6 +5,8 @@
 // (Nature fc2 / Rainbow dueling C51 expectation) with fused max_a and
 // fmaf(g_d, max_a Q, R) epilogue. The tcgen05 layer lives in qnet_tc.cu.
 #include <math.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include <vector>
 
@@ -396,6 +398,7 @@ int net_build(Net &net, const bcts_config &cfg, std::string &err) {
   // tiles to fill 148 SMs)
   net.batch = 1024;
   net.fc_batch = 16384;
+  if (const char *e = getenv("BCTS_TRUNK_BATCH")) net.batch = atoll(e) > 0 ? atoll(e) : net.batch;
   const int64_t B = net.batch, FB = net.fc_batch;
   size_t bytes[11] = {(size_t)B * 400 * 32 * 2, (size_t)B * 81 * 64 * 2, (size_t)FB * 49 * 64 * 2,
                       (size_t)FB * hidN * 2, (size_t)FB * (rainbow ? net.ld_zv : 16) * 4, (size_t)FB * net.ld_za * 4,
@@ -424,6 +427,27 @@ int net_build(Net &net, const bcts_config &cfg, std::string &err) {
     c.N = 64; c.K = 576; c.Cin = 64; c.KH = c.KW = 3; c.W_in = 9; c.OH = c.OW = 7; c.n_mt = (7 * 9 + 127) / 128;
     c.plane = kPlane3; c.in_img_bytes = kIn3Bytes;
     c.out_mode = 2; c.out_plane = 0; c.out_w = 7; c.out_img_bytes = 3136 * 2;
+    const int layout = 2;   // SW128 row blocks, address-based swizzle (the compiled MMA loop assumes it)
+    a.layout = b.layout = c.layout = layout;
+    // weights of each shifted-window layer as the exact SW128 shared-memory
+    // image the kernel wants (K/64 blocks of [N rows x 128 B], 16-byte chunk
+    // j of row n at (n/8)*1024 + (n%8)*128 + ((j ^ n%8) * 16)): one bulk copy
+    ConvSW *cs[3] = {&a, &b, &c};
+    const Layer *ls[3] = {&net.c1, &net.c2s, &net.c3};
+    for (int t = 0; t < 3; ++t) {
+      const int N = cs[t]->N, K = cs[t]->K, nkb = K / 64;
+      std::vector<__nv_bfloat16> hw((size_t)N * K), img((size_t)N * K);
+      cudaMemcpy(hw.data(), ls[t]->Wt, hw.size() * 2, cudaMemcpyDeviceToHost);
+      uint8_t *dst = (uint8_t *)img.data();
+      for (int n = 0; n < N; ++n)
+        for (int kb = 0; kb < nkb; ++kb)
+          for (int j = 0; j < 8; ++j)
+            memcpy(dst + (size_t)kb * N * 128 + (n / 8) * 1024 + (n % 8) * 128 + ((j ^ (n % 8)) * 16),
+                   (const uint8_t *)(hw.data() + (size_t)n * K + kb * 64) + j * 16, 16);
+      void *d = nullptr;
+      if (upload(net, img.data(), img.size() * 2, &d) != cudaSuccess) { err = "upload swizzled weights"; return -1; }
+      cs[t]->wsw = (const uint8_t *)d;
+    }
   }
   // TMA plans (tensor maps over the fixed scratch buffers; fall back to the
   // thread-gather tcgen05 layer if the driver entry points are unavailable)
@@ -473,12 +497,13 @@ static int eval_conv(Net &net, const NodeView *par, const NodeView *img, int64_t
       const bool sw = net.tc && net.sw;
       void *in1 = sw ? (void *)net.in1p : (void *)net.s2d;
       const uint32_t planar = sw ? kPlane1 : 0;
+      const int lay = net.sw1.layout;
       if (par) {
         launch_expand_s2d(*par, p_first, c_begin + f0 + b0, c_begin + f0 + b0 + nb, A, gk, in1, planar,
-                          net.leaf_cum + b0, st, net.prof);
+                          net.leaf_cum + b0, st, net.prof, lay);
       } else {
         if (net.prof) net.prof->begin(KC_OTHER, (double)nb * (kFrameBytes + 2.0 * 28224), st);
-        launch_s2d_convert(*img, f0 + b0, nb, in1, planar, st);
+        launch_s2d_convert(*img, f0 + b0, nb, in1, planar, st, lay);
         if (net.prof) net.prof->end(st);
       }
       if (sw) {

@@ -84,6 +84,26 @@ __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b
       "}\n" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
+__device__ __forceinline__ uint32_t elect_one() {
+  uint32_t e;
+  asm volatile("{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}\n" : "=r"(e));
+  return e;
+}
+// warp-uniform issue, elected lane predicated (see qnet_conv.cu / tools/mma_bench.cu)
+__device__ __forceinline__ void mma_pred(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc,
+                                         uint32_t issue) {
+  asm volatile(
+      "{\n.reg .pred p, q;\nsetp.ne.b32 p, %4, 0;\nsetp.ne.b32 q, %5, 0;\n"
+      "@q tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc), "r"(issue));
+}
+__device__ __forceinline__ void commit_pred(uint64_t *bar, uint32_t issue) {
+  asm volatile(
+      "{\n.reg .pred q;\nsetp.ne.b32 q, %1, 0;\n"
+      "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(saddr(bar)),
+      "r"(issue)
+      : "memory");
+}
 __device__ __forceinline__ void mma_commit(uint64_t *bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(saddr(bar))
                : "memory");
@@ -126,7 +146,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ __align__(8) uint64_t full[C::STAGES], empty[C::STAGES], tfull[2], tempty[2];
   __shared__ uint32_t tmem_slot;
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
   const int nk = L.K / KB;
   const int n_tiles = n_m * n_n;
 
@@ -188,31 +208,32 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0) {
-      uint32_t it = 0, acc_it = 0;
-      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++acc_it) {
-        const int ntile = tile % n_n;
-        const int nt = min(BN, L.Npad - ntile * BN);
-        const uint32_t idesc = idesc_bf16(kBM, nt);
-        const uint32_t a = acc_it & 1u, aph = (acc_it >> 1) & 1u;
-        mbar_wait(&tempty[a], aph ^ 1u);
+    // MMA issuer: whole warp runs the loop, the elected lane's MMAs are predicated on
+    const uint32_t elected = elect_one();
+    uint32_t it = 0, acc_it = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++acc_it) {
+      const int ntile = tile % n_n;
+      const int nt = min(BN, L.Npad - ntile * BN);
+      const uint32_t idesc = idesc_bf16(kBM, nt);
+      const uint32_t a = acc_it & 1u, aph = (acc_it >> 1) & 1u;
+      mbar_wait(&tempty[a], aph ^ 1u);
+      tc_fence_after();
+      const uint32_t d = tmem + a * BN;
+      for (int kb = 0; kb < nk; ++kb, ++it) {
+        const int s = it % C::STAGES;
+        const uint32_t ph = (it / C::STAGES) & 1u;
+        mbar_wait(&full[s], ph);
         tc_fence_after();
-        const uint32_t d = tmem + a * BN;
-        for (int kb = 0; kb < nk; ++kb, ++it) {
-          const int s = it % C::STAGES;
-          const uint32_t ph = (it / C::STAGES) & 1u;
-          mbar_wait(&full[s], ph);
-          tc_fence_after();
-          const uint32_t a0 = saddr(smem + s * C::STAGE), b0 = a0 + C::A_BYTES;
+        const uint32_t a0 = saddr(smem + s * C::STAGE), b0 = a0 + C::A_BYTES;
+        const uint64_t ad = sdesc<KB>(a0), bd = sdesc<KB>(b0);
 #pragma unroll
-          for (int kk = 0; kk < KB / 16; ++kk)
-            mma_bf16(d, sdesc<KB>(a0 + kk * 32), sdesc<KB>(b0 + kk * 32), idesc, (kb | kk) != 0);
-          mma_commit(&empty[s]);
-        }
-        mma_commit(&tfull[a]);
+        for (int kk = 0; kk < KB / 16; ++kk)   // +32 B per 16 elements inside the swizzle row
+          mma_pred(d, ad + (uint64_t)(2 * kk), bd + (uint64_t)(2 * kk), idesc, (kb | kk) != 0, elected);
+        commit_pred(&empty[s], elected);
       }
+      commit_pred(&tfull[a], elected);
+      __syncwarp();
     }
-    __syncwarp();
   } else {
     const int q = warp & 3;
     const int r = q * 32 + lane;

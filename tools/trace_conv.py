@@ -1,0 +1,22 @@
+"""Phase timeline of the shifted-window conv kernel (CTA 0), one layer launch."""
+import ctypes, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import paper_2107_01715_b200 as P
+from synth.inputs import atari_roots, config
+h = P.Handle.from_config(config("C5"))
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
+recs = torch.from_numpy(atari_roots(n, 1).copy()).cuda()
+h.q_rows(recs, n); torch.cuda.synchronize()
+buf = torch.zeros(64 * 4, dtype=torch.int64, device="cuda")
+layer = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+lib = P.lib(); lib.bcts_debug_conv_trace.argtypes = [ctypes.c_void_p, ctypes.c_int32]
+lib.bcts_debug_conv_trace(buf.data_ptr(), layer)
+h.q_rows(recs, n); torch.cuda.synchronize()
+lib.bcts_debug_conv_trace(None, -1)
+t = buf.cpu().numpy().reshape(64, 4).astype(np.float64)
+t0 = t[0, 0]
+print("img  copy_issued  input_ready  mma_issued  epi_done   (us from first copy; layer out_mode %d, last sub-batch)" % layer + "")
+for i in range(64):
+    if t[i, 0] == 0: break
+    print(f"{i:3d} " + " ".join(f"{(x - t0) / 1e3:11.2f}" for x in t[i]))
