@@ -122,9 +122,13 @@ struct ConvSW {
   int out_w = 0, out_mode = 0;                 // 0: s2d(2) planar, 1: planar, 2: dense [row][N]
   const uint8_t *wsw = nullptr;                // weights pre-swizzled as their SW128 smem image
   int layout = 0;                              // activation layout (see act_off)
+  uint32_t copy_chunks = 1;                    // bulk copies per input image
 };
 void launch_conv_sw(const ConvSW &P, const Layer &L, const void *in, int64_t n_img, void *out, cudaStream_t st);
 void conv_trace_set(unsigned long long *p, int sel);
+// conv1 with the last-level expansion fused in (children [c_begin, c_begin+n) of `par`)
+void launch_conv1_fused(const ConvSW &P, const Layer &L, const NodeView &par, int64_t p_first, int64_t c_begin,
+                        int64_t n_img, int A, float gk, void *out, float *cum_out, cudaStream_t st);
 // Trunk activation layout (runtime, BCTS_CONV_LAYOUT): 0 = chunk-planar
 // SWIZZLE_NONE; 1 = SW128 row blocks, descriptor base_offset = row phase;
 // 2 = SW128 row blocks, base_offset 0. In the SW128 layouts

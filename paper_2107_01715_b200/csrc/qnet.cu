@@ -396,16 +396,19 @@ int net_build(Net &net, const bcts_config &cfg, std::string &err) {
   // scratch: trunk sub-batches of 1024 images (s2d frames, act1, act2 stay
   // L2-resident: ~94 MB), fc layers over 16384 images at a time (enough M
   // tiles to fill 148 SMs)
-  net.batch = 1024;
+  net.batch = 16384;
   net.fc_batch = 16384;
   if (const char *e = getenv("BCTS_TRUNK_BATCH")) net.batch = atoll(e) > 0 ? atoll(e) : net.batch;
   const int64_t B = net.batch, FB = net.fc_batch;
-  size_t bytes[11] = {(size_t)B * 400 * 32 * 2, (size_t)B * 81 * 64 * 2, (size_t)FB * 49 * 64 * 2,
-                      (size_t)FB * hidN * 2, (size_t)FB * (rainbow ? net.ld_zv : 16) * 4, (size_t)FB * net.ld_za * 4,
-                      (size_t)B * 21 * 21 * 64 * 2, (size_t)FB * 4, (size_t)B * kIn1Bytes, (size_t)B * kIn2Bytes,
-                      (size_t)B * kIn3Bytes};
+  const bool simt = (cfg.flags & BCTS_F_SIMT_NET) != 0;   // dense NHWC trunk buffers only for the SIMT path
+  size_t bytes[11] = {simt ? (size_t)B * 400 * 32 * 2 : 0, simt ? (size_t)B * 81 * 64 * 2 : 0,
+                      (size_t)FB * 49 * 64 * 2, (size_t)FB * hidN * 2, (size_t)FB * (rainbow ? net.ld_zv : 16) * 4,
+                      (size_t)FB * net.ld_za * 4, simt ? (size_t)B * 21 * 21 * 64 * 2 : 0, (size_t)FB * 4,
+                      (size_t)B * kIn1Bytes, (size_t)B * kIn2Bytes, (size_t)B * kIn3Bytes};
   void *p[11];
   for (int t = 0; t < 11; ++t) {
+    p[t] = nullptr;
+    if (!bytes[t]) continue;
     if (cudaMalloc(&p[t], bytes[t]) != cudaSuccess) { err = "cudaMalloc net scratch failed"; return -1; }
     net.allocs.push_back(p[t]);
   }
@@ -429,6 +432,9 @@ int net_build(Net &net, const bcts_config &cfg, std::string &err) {
     c.out_mode = 2; c.out_plane = 0; c.out_w = 7; c.out_img_bytes = 3136 * 2;
     const int layout = 2;   // SW128 row blocks, address-based swizzle (the compiled MMA loop assumes it)
     a.layout = b.layout = c.layout = layout;
+    uint32_t chunks = 1;
+    if (const char *e = getenv("BCTS_COPY_CHUNKS")) chunks = (uint32_t)atoi(e) > 0 ? (uint32_t)atoi(e) : 1;
+    a.copy_chunks = b.copy_chunks = c.copy_chunks = chunks;
     // weights of each shifted-window layer as the exact SW128 shared-memory
     // image the kernel wants (K/64 blocks of [N rows x 128 B], 16-byte chunk
     // j of row n at (n/8)*1024 + (n%8)*128 + ((j ^ n%8) * 16)): one bulk copy
@@ -451,9 +457,11 @@ int net_build(Net &net, const bcts_config &cfg, std::string &err) {
   }
   // TMA plans (tensor maps over the fixed scratch buffers; fall back to the
   // thread-gather tcgen05 layer if the driver entry points are unavailable)
-  tma_plan(net.p_c1, net.c1, net.s2d, B);
-  tma_plan(net.p_c2, net.c2, net.act1, B);
-  tma_plan(net.p_c3, net.c3, net.act2, B);
+  if (simt) {   // dense trunk (SIMT reference path only; kept for completeness of the TMA im2col path)
+    tma_plan(net.p_c1, net.c1, net.s2d, B);
+    tma_plan(net.p_c2, net.c2, net.act1, B);
+    tma_plan(net.p_c3, net.c3, net.act2, B);
+  }
   tma_plan(net.p_fc_h, net.fc_h, net.act3, FB);
   if (rainbow) {
     tma_plan(net.p_z_v, net.z_v, net.hid_act, FB);
@@ -498,6 +506,21 @@ static int eval_conv(Net &net, const NodeView *par, const NodeView *img, int64_t
       void *in1 = sw ? (void *)net.in1p : (void *)net.s2d;
       const uint32_t planar = sw ? kPlane1 : 0;
       const int lay = net.sw1.layout;
+      if (par && sw) {   // leaf level generated inside conv1 (never leaves the SM)
+        const double fl = 2.0 * (double)nb;
+        if (net.prof) net.prof->begin(KC_CONV1, fl * 400 * 32 * 256, st);
+        launch_conv1_fused(net.sw1, net.c1, *par, p_first, c_begin + f0 + b0, nb, A, gk, net.act1p, net.leaf_cum + b0,
+                           st);
+        if (net.prof) net.prof->end(st);
+        if (net.prof) net.prof->begin(KC_CONV2, fl * 81 * 64 * 512, st);
+        launch_conv_sw(net.sw2, net.c2s, net.act1p, nb, net.act2p, st);
+        if (net.prof) net.prof->end(st);
+        if (net.prof) net.prof->begin(KC_CONV3, fl * 49 * 64 * 576, st);
+        launch_conv_sw(net.sw3, net.c3, net.act2p, nb, net.act3 + b0 * 3136, st);
+        if (net.prof) net.prof->end(st);
+        launches += 3;
+        continue;
+      }
       if (par) {
         launch_expand_s2d(*par, p_first, c_begin + f0 + b0, c_begin + f0 + b0 + nb, A, gk, in1, planar,
                           net.leaf_cum + b0, st, net.prof, lay);

@@ -135,7 +135,24 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;   // warp 0 producer, warp 1 MMA, warps 2-9 epilogue
+
+// TMEM -> registers without waiting; tmem_wait16 then waits and ties the
+// registers to the wait so no use is scheduled before it.
+__device__ __forceinline__ void tmem_ld16_nw(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait16(uint32_t (&r)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
+               :
+               : "memory");
+}
 
 // Debug phase timestamps (CTA 0 only; BCTS_CONV_TRACE=1): [img][4] =
 // copy issued, input ready (MMA side), MMAs issued, epilogue done.
@@ -178,7 +195,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&in_full[i], 1);
       mbar_init(&in_empty[i], 1);
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 128);
+      mbar_init(&tempty[i], 256);
     }
     mbar_init(&wbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -204,7 +221,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&in_empty[b], ph ^ 1u);
         if (g_trace && P.out_mode == g_trace_sel && blockIdx.x == 0 && i < 64) g_trace[i * 4 + 0] = gtime();
         mbar_expect_tx(&in_full[b], P.in_img_bytes);
-        bulk_g2s(saddr(sIn0 + b * in_stride), in + img * (int64_t)P.in_img_bytes, P.in_img_bytes, &in_full[b]);
+        // the image as several bulk copies in flight (per-request TMA throughput)
+        const uint32_t chunk = (P.in_img_bytes / P.copy_chunks + 15u) & ~15u;
+        for (uint32_t o = 0; o < P.in_img_bytes; o += chunk) {
+          const uint32_t len = min(chunk, P.in_img_bytes - o);
+          bulk_g2s(saddr(sIn0 + b * in_stride) + o, in + img * (int64_t)P.in_img_bytes + o, len, &in_full[b]);
+        }
       }
     }
     __syncwarp();
@@ -248,59 +270,289 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
     }
   } else {
-    const int q4 = warp & 3;
+    // ------------------------------------------------- epilogue: 8 warps = 4 lane quarters x 2 column halves
+    constexpr int HALF = N / 2, NCH = HALF / 16;   // columns per warp, x16 loads per tile
+    const int q4 = warp & 3;                       // TMEM lane quarter this warp may access
+    const int c0 = ((warp - 2) >> 2) * HALF;       // column half
     const int r = q4 * 32 + lane;
+    float bias_r[HALF];
+#pragma unroll
+    for (int c = 0; c < HALF; ++c) bias_r[c] = sbias[c0 + c];
     uint32_t i = 0;
     for (int64_t img = blockIdx.x; img < n_img; img += gridDim.x, ++i) {
       const uint32_t b = i & 1u, ph = (i >> 1) & 1u;
       mbar_wait(&tfull[b], ph);
       tc_fence_after();
-      uint8_t *oimg = out + img * P.out_img_bytes;
-      for (int mt = 0; mt < P.n_mt; ++mt) {
-        const int q = mt * 128 + r;
-        const int oy = q / P.W_in, ox = q - oy * P.W_in;
-        const bool valid = oy < P.OH && ox < P.OW;
-        const uint32_t trow = tmem + b * tcols_img + (uint32_t)(mt * N) + ((uint32_t)(q4 * 32) << 16);
+      uint32_t v[G::N_MT][NCH][16];
+      const uint32_t tbase = tmem + b * tcols_img + ((uint32_t)(q4 * 32) << 16) + (uint32_t)c0;
 #pragma unroll
-        for (int c = 0; c < N; c += 16) {
-          uint32_t v[16];
-          tmem_ld16(trow + (uint32_t)c, v);
-          if (!valid) continue;
+      for (int mt = 0; mt < G::N_MT; ++mt)
+#pragma unroll
+        for (int h = 0; h < NCH; ++h) tmem_ld16_nw(tbase + (uint32_t)(mt * N + h * 16), v[mt][h]);
+#pragma unroll
+      for (int mt = 0; mt < G::N_MT; ++mt)
+#pragma unroll
+        for (int h = 0; h < NCH; ++h) tmem_wait16(v[mt][h]);
+      tc_fence_before();
+      mbar_arrive(&tempty[b]);                     // accumulators may be reused right away
+      uint8_t *oimg = out + img * P.out_img_bytes;
+#pragma unroll
+      for (int mt = 0; mt < G::N_MT; ++mt) {
+        const int q = mt * 128 + r;
+        const int oy = q / G::W_IN, ox = q - oy * G::W_IN;
+        if (oy >= P.OH || ox >= P.OW) continue;
+#pragma unroll
+        for (int h = 0; h < NCH; ++h) {
           uint32_t pk[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
-            const float x = __uint_as_float(v[2 * e]) + sbias[c + 2 * e];
-            const float y = __uint_as_float(v[2 * e + 1]) + sbias[c + 2 * e + 1];
+            const float x = __uint_as_float(v[mt][h][2 * e]) + bias_r[h * 16 + 2 * e];
+            const float y = __uint_as_float(v[mt][h][2 * e + 1]) + bias_r[h * 16 + 2 * e + 1];
             __nv_bfloat162 hh = __floats2bfloat162_rn(x > 0.0f ? x : 0.0f, y > 0.0f ? y : 0.0f);
             pk[e] = *(uint32_t *)&hh;
           }
-          // channels c..c+15 = two 8-channel chunks
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const uint4 val = make_uint4(pk[4 * h], pk[4 * h + 1], pk[4 * h + 2], pk[4 * h + 3]);
-            const int ch = c + 8 * h;           // first channel of this chunk
+          for (int hh2 = 0; hh2 < 2; ++hh2) {
+            const uint4 val = make_uint4(pk[4 * hh2], pk[4 * hh2 + 1], pk[4 * hh2 + 2], pk[4 * hh2 + 3]);
+            const int ch = c0 + h * 16 + 8 * hh2;  // first channel of this 8-channel chunk
             uint8_t *dst;
-            if (P.out_mode == 0) {              // conv2's s2d(2) input (32 ch -> chunk sub*4 + ch/8)
+            if (P.out_mode == 0) {                 // conv2's s2d(2) input (32 ch -> chunk sub*4 + ch/8)
               const int sub = ((oy & 1) << 1) | (ox & 1);
               const int row = (oy >> 1) * P.out_w + (ox >> 1);
               dst = oimg + act_off(P.layout, P.out_plane, row, sub * 4 + (ch >> 3));
-            } else if (P.out_mode == 1) {       // conv3's input
+            } else if (P.out_mode == 1) {          // conv3's input
               const int row = oy * P.out_w + ox;
               dst = oimg + act_off(P.layout, P.out_plane, row, ch >> 3);
-            } else {                            // fc input: dense [(y, x)][64]
+            } else {                               // fc input: dense [(y, x)][64]
               dst = oimg + ((size_t)(oy * P.out_w + ox) * N + ch) * 2;
             }
             *(uint4 *)dst = val;
           }
         }
       }
-      tc_fence_before();
-      mbar_arrive(&tempty[b]);
-      if (g_trace && P.out_mode == g_trace_sel && blockIdx.x == 0 && i < 64 && r == 0) g_trace[i * 4 + 3] = gtime();
+      if (g_trace && P.out_mode == g_trace_sel && blockIdx.x == 0 && i < 64 && r == 0 && c0 == 0)
+        g_trace[i * 4 + 3] = gtime();
     }
   }
   __syncthreads();
   if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tcols));
+  }
+}
+
+// ============================================================ conv1 + fused leaf expansion
+// The last tree level never exists outside shared memory: converter warps
+// build each child's conv1 input (space-to-depth(4) bf16, SW128 row layout)
+// in smem. Per parent (once per A children) they convert its frame stack to
+// dense bf16 s2d and keep its newest frame's bytes; a child then is the
+// parent's bf16 channels shifted by one frame (the ATARI_HASH step: frames
+// 1..3 move down, Alg. 1) plus one new bf16 per pixel,
+// bf16(parent_newest ^ noise). The child's R_d = fmaf(g[d-1], r, R_{d-1}) is
+// written too. MMA / epilogue as in k_conv_sw<G1>. Each CTA owns a contiguous
+// child range so consecutive children share the converted parent.
+//   warp 0: MMA issuer   warps 1-8: epilogue   warps 9-16: converters
+constexpr int kThreadsF = 544;
+constexpr int kConvThreads = 256;
+
+__device__ __forceinline__ uint64_t mix64d(uint64_t z) {
+  z ^= z >> 30; z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27; z *= 0x94D049BB133111EBull;
+  z ^= z >> 31; return z;
+}
+// exact u8 -> bf16 bits in the upper half of the returned float bits
+__device__ __forceinline__ uint32_t u8_f32bits(uint32_t w, uint32_t i) {
+  return __float_as_uint(__uint_as_float(__byte_perm(w, 0x4B000000u, 0x7540u + i)) - 8388608.0f);
+}
+__device__ __forceinline__ uint32_t u8pair_bf16x2(uint32_t w, uint32_t i) {
+  return __byte_perm(u8_f32bits(w, i), u8_f32bits(w, i + 1), 0x7632u);
+}
+__device__ __forceinline__ void conv_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+__global__ void __launch_bounds__(kThreadsF, 1)
+    k_conv1_fused(ConvSW P, const uint8_t *__restrict__ Wsw, const float *__restrict__ bias, NodeView par,
+                  int64_t p_first, int64_t c_begin, int64_t n_img, int A, float gk, uint8_t *__restrict__ out,
+                  float *__restrict__ cum_out) {
+  using G = G1;
+  constexpr int N = G::N;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  constexpr int nkb = 256 / 64;
+  uint8_t *sW = smem;                                           // 16 KB SW128 weights
+  uint8_t *sIn0 = smem + nkb * N * 128;                         // 2 x SW128 s2d child images
+  constexpr uint32_t in_stride = (kIn1Bytes + 1023u) & ~1023u;
+  uint4 *sPar = (uint4 *)(sIn0 + 2 * in_stride);               // parent bf16 s2d, [pix*4 + dy] x 32 B
+  uint32_t *sNew = (uint32_t *)((uint8_t *)sPar + 441 * 4 * 32); // parent newest-frame bytes, 7056 B
+  __shared__ __align__(8) uint64_t in_full[2], in_empty[2], tfull[2], tempty[2], wbar;
+  __shared__ uint32_t tmem_slot;
+  __shared__ float sbias[64];
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
+  constexpr uint32_t tcols_img = G::N_MT * N;                   // 128
+  constexpr uint32_t tcols = 256;
+  const int64_t per = (n_img + gridDim.x - 1) / gridDim.x;
+  const int64_t i0 = (int64_t)blockIdx.x * per, i1 = min(n_img, i0 + per);
+  if (threadIdx.x < N) sbias[threadIdx.x] = bias[threadIdx.x];
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&in_full[i], kConvThreads);
+      mbar_init(&in_empty[i], 1);
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 256);
+    }
+    mbar_init(&wbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(&wbar, (uint32_t)(nkb * N * 128));
+    bulk_g2s(saddr(sW), Wsw, (uint32_t)(nkb * N * 128), &wbar);
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(&tmem_slot)),
+                 "r"(tcols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  if (warp == 0) {
+    // ---------------------------------------------- MMA issuer (identical to k_conv_sw<G1>)
+    constexpr uint32_t idesc = idesc_bf16(128, N);
+    constexpr int TAPS = G::KH * G::KW, KSTEPS = G::CIN / 16;
+    const uint32_t elected = elect_one();
+    mbar_wait(&wbar, 0);
+    const uint64_t wdesc = desc_sw128(saddr(sW));
+    uint32_t i = 0;
+    for (int64_t img = i0; img < i1; ++img, ++i) {
+      const uint32_t b = i & 1u, ph = (i >> 1) & 1u;
+      mbar_wait(&in_full[b], ph);
+      mbar_wait(&tempty[b], ph ^ 1u);
+      tc_fence_after();
+      const uint64_t adesc0 = desc_sw128_win(saddr(sIn0 + b * in_stride), false);
+      const uint32_t d0 = tmem + b * tcols_img;
+#pragma unroll
+      for (int mt = 0; mt < G::N_MT; ++mt)
+#pragma unroll
+        for (int tap = 0; tap < TAPS; ++tap)
+#pragma unroll
+          for (int kk = 0; kk < KSTEPS; ++kk) {
+            const uint32_t a_off = (uint32_t)(kk >> 2) * G::BPLANE +
+                                   (uint32_t)(mt * 128 + (tap / G::KW) * G::W_IN + (tap % G::KW)) * 128u +
+                                   (uint32_t)((kk & 3) * 32);
+            const int k = tap * G::CIN + 16 * kk;
+            const uint32_t w_off = (uint32_t)(k >> 6) * (N * 128) + (uint32_t)((k & 63) * 2);
+            mma_pred(d0 + (uint32_t)(mt * N), adesc0 + (a_off >> 4), wdesc + (w_off >> 4), idesc, (tap | kk) != 0,
+                     elected);
+          }
+      if (g_trace && g_trace_sel == 9 && blockIdx.x == 0 && i < 64 && elected) g_trace[i * 4 + 2] = gtime();
+      commit_pred(&in_empty[b], elected);
+      commit_pred(&tfull[b], elected);
+      __syncwarp();
+    }
+  } else if (warp < 9) {
+    // ---------------------------------------------- epilogue (8 warps) -> conv2's s2d(2) SW128 input
+    constexpr int HALF = N / 2;
+    const int q4 = warp & 3;
+    const int c0 = ((warp - 1) >> 2) * HALF;
+    const int r = q4 * 32 + lane;
+    float bias_r[HALF];
+#pragma unroll
+    for (int c = 0; c < HALF; ++c) bias_r[c] = sbias[c0 + c];
+    uint32_t i = 0;
+    for (int64_t img = i0; img < i1; ++img, ++i) {
+      const uint32_t b = i & 1u, ph = (i >> 1) & 1u;
+      mbar_wait(&tfull[b], ph);
+      tc_fence_after();
+      uint32_t v[G::N_MT][16];
+      const uint32_t tbase = tmem + b * tcols_img + ((uint32_t)(q4 * 32) << 16) + (uint32_t)c0;
+#pragma unroll
+      for (int mt = 0; mt < G::N_MT; ++mt) tmem_ld16_nw(tbase + (uint32_t)(mt * N), v[mt]);
+#pragma unroll
+      for (int mt = 0; mt < G::N_MT; ++mt) tmem_wait16(v[mt]);
+      tc_fence_before();
+      mbar_arrive(&tempty[b]);
+      uint8_t *oimg = out + img * (int64_t)P.out_img_bytes;
+#pragma unroll
+      for (int mt = 0; mt < G::N_MT; ++mt) {
+        const int q = mt * 128 + r;
+        const int oy = q / G::W_IN, ox = q - oy * G::W_IN;
+        if (oy >= 20 || ox >= 20) continue;
+        uint32_t pk[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float x = __uint_as_float(v[mt][2 * e]) + bias_r[2 * e];
+          const float y = __uint_as_float(v[mt][2 * e + 1]) + bias_r[2 * e + 1];
+          __nv_bfloat162 hh = __floats2bfloat162_rn(x > 0.0f ? x : 0.0f, y > 0.0f ? y : 0.0f);
+          pk[e] = *(uint32_t *)&hh;
+        }
+        const int sub = ((oy & 1) << 1) | (ox & 1);
+        const int row = (oy >> 1) * P.out_w + (ox >> 1);
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2)
+          *(uint4 *)(oimg + act_off(2, P.out_plane, row, sub * 4 + ((c0 + 8 * h2) >> 3))) =
+              make_uint4(pk[4 * h2], pk[4 * h2 + 1], pk[4 * h2 + 2], pk[4 * h2 + 3]);
+      }
+      if (g_trace && g_trace_sel == 9 && blockIdx.x == 0 && i < 64 && r == 0 && c0 == 0) g_trace[i * 4 + 3] = gtime();
+    }
+  } else {
+    // ---------------------------------------------- converters (8 warps)
+    const int t = threadIdx.x - 288;   // 0..255
+    uint32_t i = 0;
+    int64_t cur_p = -1;
+    for (int64_t img = i0; img < i1; ++img, ++i) {
+      const int64_t c = c_begin + img, p = c / A;
+      const int a = (int)(c - p * A);
+      const int64_t pl = p - p_first;
+      if (p != cur_p) {   // new parent: convert its frame stack once (global -> smem bf16 s2d)
+        conv_bar();       // every converter is done reading the previous parent
+        const uint8_t *pf = par.state + pl * par.state_stride;
+        for (int task = t; task < 441 * 4; task += kConvThreads) {
+          const int pix = task >> 2, dy = task & 3;
+          const int Y = pix / 21, X = pix - Y * 21;
+          const int p0 = (4 * Y + dy) * 84 + 4 * X;
+          const uint4 x = __ldg((const uint4 *)(pf) + (p0 >> 2));
+          sPar[task * 2] = make_uint4(u8pair_bf16x2(x.x, 0), u8pair_bf16x2(x.x, 2), u8pair_bf16x2(x.y, 0),
+                                      u8pair_bf16x2(x.y, 2));
+          sPar[task * 2 + 1] = make_uint4(u8pair_bf16x2(x.z, 0), u8pair_bf16x2(x.z, 2), u8pair_bf16x2(x.w, 0),
+                                          u8pair_bf16x2(x.w, 2));
+          sNew[p0 >> 2] = __byte_perm(__byte_perm(x.x, x.y, 0x0073u), __byte_perm(x.z, x.w, 0x0073u), 0x5410u);
+        }
+        conv_bar();
+        cur_p = p;
+      }
+      const uint64_t key = *(const uint64_t *)((const uint8_t *)par.key + pl * par.key_stride);
+      const uint64_t k2 = mix64d(key ^ (0x9E3779B97F4A7C15ull * (uint64_t)(a + 1)));
+      if (t == 0) {
+        const uint32_t tt = (uint32_t)(k2 >> 61);
+        const float rw = tt == 7u ? 1.0f : (tt == 0u ? -1.0f : 0.0f);
+        cum_out[img] = fmaf(gk, rw, par.cum ? par.cum[pl] : 0.0f);
+      }
+      const uint32_t b = i & 1u, ph = (i >> 1) & 1u;
+      mbar_wait(&in_empty[b], ph ^ 1u);
+      const bool tr = g_trace && g_trace_sel == 9 && blockIdx.x == 0 && i < 64 && t == 0;
+      if (tr) g_trace[i * 4 + 0] = gtime();
+      uint8_t *dimg = sIn0 + b * in_stride;
+      for (int task = t; task < 441 * 4; task += kConvThreads) {
+        const int pix = task >> 2, dy = task & 3;
+        const int Y = pix / 21, X = pix - Y * 21;
+        const int p0 = (4 * Y + dy) * 84 + 4 * X;                // 4 pixels, p0 % 4 == 0
+        const uint32_t nz = (uint32_t)(mix64d(k2 + (uint64_t)(p0 >> 3)) >> (8 * (p0 & 7)));
+        const uint32_t nb = sNew[p0 >> 2] ^ nz;                  // the 4 new newest-frame bytes
+        const uint4 lo = sPar[task * 2], hi = sPar[task * 2 + 1];
+        // parent pixel j = words (ch0,ch1), (ch2,ch3); child = (ch1,ch2), (ch3,new)
+        const uint4 clo = make_uint4(__byte_perm(lo.x, lo.y, 0x5432u), __byte_perm(lo.y, u8_f32bits(nb, 0), 0x7632u),
+                                     __byte_perm(lo.z, lo.w, 0x5432u), __byte_perm(lo.w, u8_f32bits(nb, 1), 0x7632u));
+        const uint4 chi = make_uint4(__byte_perm(hi.x, hi.y, 0x5432u), __byte_perm(hi.y, u8_f32bits(nb, 2), 0x7632u),
+                                     __byte_perm(hi.z, hi.w, 0x5432u), __byte_perm(hi.w, u8_f32bits(nb, 3), 0x7632u));
+        *(uint4 *)(dimg + act_off(2, kPlane1, pix, 2 * dy)) = clo;
+        *(uint4 *)(dimg + act_off(2, kPlane1, pix, 2 * dy + 1)) = chi;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic stores -> tensor-core reads
+      mbar_arrive(&in_full[b]);
+      if (tr) g_trace[i * 4 + 1] = gtime();
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tcols));
   }
@@ -335,6 +587,20 @@ void launch_n(const ConvSW &P, const Layer &L, const void *in, int64_t n_img, vo
 void conv_trace_set(unsigned long long *p, int sel) {
   cudaMemcpyToSymbol(g_trace, &p, sizeof(p));
   cudaMemcpyToSymbol(g_trace_sel, &sel, sizeof(sel));
+}
+
+void launch_conv1_fused(const ConvSW &P, const Layer &L, const NodeView &par, int64_t p_first, int64_t c_begin,
+                        int64_t n_img, int A, float gk, void *out, float *cum_out, cudaStream_t st) {
+  if (n_img <= 0) return;
+  constexpr int smem = 4 * 32 * 128 + 2 * (int)((kIn1Bytes + 1023u) & ~1023u) + 441 * 4 * 32 + 7056 + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_conv1_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  const int grid = (int)std::min<int64_t>(n_img, num_sms());
+  k_conv1_fused<<<grid, kThreadsF, smem, st>>>(P, P.wsw, L.bias, par, p_first, c_begin, n_img, A, gk, (uint8_t *)out,
+                                               cum_out);
 }
 
 void launch_conv_sw(const ConvSW &P, const Layer &L, const void *in, int64_t n_img, void *out, cudaStream_t st) {

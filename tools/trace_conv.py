@@ -12,11 +12,15 @@ buf = torch.zeros(64 * 4, dtype=torch.int64, device="cuda")
 layer = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 lib = P.lib(); lib.bcts_debug_conv_trace.argtypes = [ctypes.c_void_p, ctypes.c_int32]
 lib.bcts_debug_conv_trace(buf.data_ptr(), layer)
-h.q_rows(recs, n); torch.cuda.synchronize()
+if layer == 9:   # fused conv1: run a real search (d=2 -> 324 leaves per root)
+    roots = torch.from_numpy(config("C5").roots(4).copy()).cuda()
+    h.search(roots, 4, 2, 0.99, 1.0, 1); torch.cuda.synchronize()
+else:
+    h.q_rows(recs, n); torch.cuda.synchronize()
 lib.bcts_debug_conv_trace(None, -1)
 t = buf.cpu().numpy().reshape(64, 4).astype(np.float64)
 t0 = t[0, 0]
-print("img  copy_issued  input_ready  mma_issued  epi_done   (us from first copy; layer out_mode %d, last sub-batch)" % layer + "")
+print("img  t0 t1 t2 t3 [copy_issued/conv_start, input_ready/conv_done, mma_issued, epi_done]   (us from first copy; layer out_mode %d, last sub-batch)" % layer + "")
 for i in range(64):
     if t[i, 0] == 0: break
     print(f"{i:3d} " + " ".join(f"{(x - t0) / 1e3:11.2f}" for x in t[i]))
