@@ -718,3 +718,23 @@ int oracle_search_subtrees(const oracle_model *m, const void *root_rec, int dept
   }
   return err ? -1 : 0;
 }
+
+/* Leaf total of leaf `index` below one root: R_d + gamma^d max_a Q(s_d, a)
+ * with the oracle's own arithmetic (fmaf in the fp32-mirror mode, R3). */
+int oracle_leaf_total(const oracle_model *m, const void *root_rec, int depth, int64_t index, double gamma,
+                      int mode, double *total) {
+  if (depth < 1 || depth > MAXD) return -1;
+  double g[MAXD + 1], q[MAXA], R;
+  discounts(gamma, depth, g);
+  uint8_t *rec = (uint8_t *)malloc(oracle_record_bytes(m));
+  ostate *s = (ostate *)malloc(sizeof(ostate));
+  int rc = oracle_node(m, root_rec, depth, index, gamma, mode, rec, &R);
+  if (!rc) {
+    from_record(m, rec, s);
+    rc = qrow(m, s, mode, q);
+  }
+  if (!rc) *total = leaf_total(mode, g, depth, rowmax(q, m->A), R);
+  free(rec);
+  free(s);
+  return rc;
+}

@@ -59,6 +59,8 @@ def _load():
             lib.oracle_terms.argtypes = [P, P, L, I, D, I, P, P]
             lib.oracle_search_subtrees.restype = I
             lib.oracle_search_subtrees.argtypes = [P, P, I, D, I, I, L, L, P]
+            lib.oracle_leaf_total.restype = I
+            lib.oracle_leaf_total.argtypes = [P, P, I, C.c_int64, D, I, C.POINTER(D)]
             lib.oracle_max_threads.restype = I
             _lib = lib
     return _lib
@@ -164,6 +166,13 @@ class Oracle:
             raise ValueError("oracle search failed (domain error)")
         return {"actions": act, "root_q": rq.reshape(n, A), "vanilla_q": van.reshape(n, A),
                 "terms": terms.reshape(n, 4), "best_leaf": bl.reshape(n, A)}
+
+    def leaf_total(self, root_rec, depth: int, index: int, gamma: float, mode: int = 0) -> float:
+        rec = self._records(root_rec)[0]
+        t = C.c_double()
+        if _load().oracle_leaf_total(self._h, _ptr(rec), depth, int(index), gamma, mode, C.byref(t)):
+            raise ValueError("oracle_leaf_total failed")
+        return t.value
 
     def terms(self, roots, depth: int, gamma: float, mode: int = 0):
         """(pi_o, delta_o, delta_e, B) per root and the root rows Q_hat(s0, .)."""
