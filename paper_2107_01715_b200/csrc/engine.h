@@ -126,6 +126,10 @@ struct ConvSW {
 };
 void launch_conv_sw(const ConvSW &P, const Layer &L, const void *in, int64_t n_img, void *out, cudaStream_t st);
 void conv_trace_set(unsigned long long *p, int sel);
+// conv1, sibling-factorised (shared frames once per parent + new frame per child)
+void launch_conv1_sib(const ConvSW &P, const Layer &L, const uint8_t *wsh, const uint8_t *wnw, const NodeView &par,
+                      int64_t p_first, int64_t c_begin, int64_t n_img, int A, float gk, void *out, float *cum_out,
+                      cudaStream_t st);
 // conv1 with the last-level expansion fused in (children [c_begin, c_begin+n) of `par`)
 void launch_conv1_fused(const ConvSW &P, const Layer &L, const NodeView &par, int64_t p_first, int64_t c_begin,
                         int64_t n_img, int A, float gk, void *out, float *cum_out, cudaStream_t st);
@@ -167,6 +171,7 @@ struct Net {
   uint8_t *in1p = nullptr, *act1p = nullptr, *act2p = nullptr;  // planar trunk buffers [batch]
   Layer c2s;                      // conv2 as 2x2 stride-1 over s2d(2) of act1 (shifted windows)
   ConvSW sw1, sw2, sw3;
+  const uint8_t *w1_shared = nullptr, *w1_new = nullptr;   // sibling-factorised conv1 weights (SW128 images)
   bool sw = false;                // shifted-window trunk enabled
   float *leaf_cum = nullptr;      // [fc_batch] R_d of fused-expanded leaves
   __nv_bfloat16 *act1 = nullptr, *act2 = nullptr, *act3 = nullptr, *hid_act = nullptr;

@@ -316,6 +316,43 @@ int net_build(Net &net, const bcts_config &cfg, std::string &err) {
       return ((o * 4 + c) * 8 + (4 * ty + dy)) * 8 + (4 * tx + dx);
     };
     if (make_layer(net, L, repack(32, 32, 2, 2, 64, src, w), w + 32 * 256, 32, 32, err)) return -1;
+    // sibling-factorised conv1: child frames 0..2 (= parent frames 1..3) and frame 3,
+    // channel order (c, dy, dx) inside an s2d pixel:
+    //   W_shared[o][tap*48 + c*16 + dy*4 + dx] = W[o][c][4ty+dy][4tx+dx]   (c = 0..2)
+    //   W_new[o][tap*16 + dy*4 + dx]           = W[o][3][4ty+dy][4tx+dx]
+    {
+      auto sw_image = [](const std::vector<__nv_bfloat16> &wl, int Nr, int K) {
+        std::vector<__nv_bfloat16> img((size_t)Nr * K);
+        uint8_t *dst = (uint8_t *)img.data();
+        for (int n = 0; n < Nr; ++n)
+          for (int kb = 0; kb < K / 64; ++kb)
+            for (int j = 0; j < 8; ++j)
+              memcpy(dst + (size_t)kb * Nr * 128 + (n / 8) * 1024 + (n % 8) * 128 + ((j ^ (n % 8)) * 16),
+                     (const uint8_t *)(wl.data() + (size_t)n * K + kb * 64) + j * 16, 16);
+        return img;
+      };
+      std::vector<__nv_bfloat16> wsh((size_t)32 * 192), wnw((size_t)32 * 64);
+      for (int o = 0; o < 32; ++o)
+        for (int tap = 0; tap < 4; ++tap) {
+          const int ty = tap >> 1, tx = tap & 1;
+          for (int dy = 0; dy < 4; ++dy)
+            for (int dx = 0; dx < 4; ++dx) {
+              for (int c = 0; c < 3; ++c)
+                wsh[(size_t)o * 192 + tap * 48 + c * 16 + dy * 4 + dx] =
+                    __float2bfloat16_rn(w[((o * 4 + c) * 8 + 4 * ty + dy) * 8 + 4 * tx + dx]);
+              wnw[(size_t)o * 64 + tap * 16 + dy * 4 + dx] =
+                  __float2bfloat16_rn(w[((o * 4 + 3) * 8 + 4 * ty + dy) * 8 + 4 * tx + dx]);
+            }
+        }
+      std::vector<__nv_bfloat16> a = sw_image(wsh, 32, 192), b = sw_image(wnw, 32, 64);
+      void *da = nullptr, *db = nullptr;
+      if (upload(net, a.data(), a.size() * 2, &da) != cudaSuccess || upload(net, b.data(), b.size() * 2, &db) != cudaSuccess) {
+        err = "upload factorised conv1 weights";
+        return -1;
+      }
+      net.w1_shared = (const uint8_t *)da;
+      net.w1_new = (const uint8_t *)db;
+    }
     w += 32 * 256 + 32;
   }
   {
@@ -509,8 +546,8 @@ static int eval_conv(Net &net, const NodeView *par, const NodeView *img, int64_t
       if (par && sw) {   // leaf level generated inside conv1 (never leaves the SM)
         const double fl = 2.0 * (double)nb;
         if (net.prof) net.prof->begin(KC_CONV1, fl * 400 * 32 * 256, st);
-        launch_conv1_fused(net.sw1, net.c1, *par, p_first, c_begin + f0 + b0, nb, A, gk, net.act1p, net.leaf_cum + b0,
-                           st);
+        launch_conv1_sib(net.sw1, net.c1, net.w1_shared, net.w1_new, *par, p_first, c_begin + f0 + b0, nb, A, gk,
+                         net.act1p, net.leaf_cum + b0, st);
         if (net.prof) net.prof->end(st);
         if (net.prof) net.prof->begin(KC_CONV2, fl * 81 * 64 * 512, st);
         launch_conv_sw(net.sw2, net.c2s, net.act1p, nb, net.act2p, st);

@@ -558,6 +558,262 @@ __global__ void __launch_bounds__(kThreadsF, 1)
   }
 }
 
+// ============================================================ conv1, sibling-factorised
+// conv1 is linear in its input and the A children of a parent share three of
+// their four frames (child frames 0..2 = parent frames 1..3, frame stack P:355).
+// Exactly (up to fp32 summation order):
+//   conv1(child_a) = conv1[frames 0..2](shared image of the parent)   (K = 4 taps x 48)
+//                  + conv1[frame 3](new frame of child a)             (K = 4 taps x 16)
+// The shared part P is accumulated in TMEM once per parent; each child costs
+// 16 MMAs for its new frame; the epilogue adds P + C_a + bias, ReLU, bf16.
+// Operands are chunk-planar (SWIZZLE_NONE K-major: 8 bf16 per 16-byte row per
+// plane; any starting row is a valid descriptor = shifted window), channel
+// order inside an s2d(4) pixel (c, dy, dx): plane j of the shared image holds
+// frame c = j/2 at dy in {2(j%2), 2(j%2)+1}; the new image has 2 planes (dy pairs).
+//   warp 0: MMA issuer   warps 1-8: epilogue   warps 9-16: converters
+constexpr uint32_t kSibPlane = 536 * 16;            // rows 0..535 x 16 B
+constexpr uint32_t kSharedBytes = 6 * kSibPlane;    // 51,456
+constexpr uint32_t kNewBytes = 2 * kSibPlane;       // 17,152
+constexpr int kNewRing = 3;
+
+__global__ void __launch_bounds__(kThreadsF, 1)
+    k_conv1_sib(ConvSW P, const uint8_t *__restrict__ Wsh, const uint8_t *__restrict__ Wnw,
+                const float *__restrict__ bias, NodeView par, int64_t p_first, int64_t c_begin, int64_t n_img, int A,
+                float gk, uint8_t *__restrict__ out, float *__restrict__ cum_out) {
+  constexpr int N = 32;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t *sWsh = smem;                              // 3 k-blocks x [32 x 128 B] SW128 (K = 192)
+  uint8_t *sWnw = sWsh + 3 * N * 128;                // 1 k-block (K = 64)
+  uint8_t *sSh = sWnw + N * 128;                     // 2 x shared image
+  uint8_t *sNw = sSh + 2 * kSharedBytes;             // kNewRing x new image
+  uint32_t *sNew3 = (uint32_t *)(sNw + kNewRing * kNewBytes);   // 2 x parent newest-frame bytes (7056 B)
+  __shared__ __align__(8) uint64_t sh_full[2], sh_empty[2], p_full[2], p_empty[2];
+  __shared__ __align__(8) uint64_t n_full[kNewRing], n_empty[kNewRing], c_full[2], c_empty[2], wbar;
+  __shared__ uint32_t tmem_slot;
+  __shared__ float sbias[64];
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
+  const int64_t per = (n_img + gridDim.x - 1) / gridDim.x;
+  const int64_t i0 = (int64_t)blockIdx.x * per, i1 = min(n_img, i0 + per);
+  if (threadIdx.x < N) sbias[threadIdx.x] = bias[threadIdx.x];
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sh_full[i], kConvThreads);
+      mbar_init(&sh_empty[i], 1);
+      mbar_init(&p_full[i], 1);
+      mbar_init(&p_empty[i], 256);
+      mbar_init(&c_full[i], 1);
+      mbar_init(&c_empty[i], 256);
+    }
+    for (int i = 0; i < kNewRing; ++i) {
+      mbar_init(&n_full[i], kConvThreads);
+      mbar_init(&n_empty[i], 1);
+    }
+    mbar_init(&wbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(&wbar, 4u * N * 128);
+    bulk_g2s(saddr(sWsh), Wsh, 3u * N * 128, &wbar);
+    bulk_g2s(saddr(sWnw), Wnw, 1u * N * 128, &wbar);
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(&tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;   // cols [0,256): P[2] (4 tiles x 32 each); [256,512): C[2]
+  const int64_t pfirst_cta = (c_begin + i0) / A;
+
+  if (warp == 0) {
+    // ---------------------------------------------- MMA issuer (whole warp, elected lane issues)
+    constexpr uint32_t idesc = idesc_bf16(128, N);
+    const uint32_t elected = elect_one();
+    mbar_wait(&wbar, 0);
+    const uint64_t wsh = desc_sw128(saddr(sWsh)), wnw = desc_sw128(saddr(sWnw));
+    int64_t cur_p = -1;
+    uint32_t k = 0, j = 0;
+    for (int64_t img = i0; img < i1; ++img, ++j) {
+      const int64_t p = (c_begin + img) / A;
+      if (p != cur_p) {     // shared part of a new parent: 4 tiles x 4 taps x 3 K-steps
+        k = (uint32_t)(p - pfirst_cta);
+        const uint32_t sb = k & 1u, ph = (k >> 1) & 1u;
+        mbar_wait(&sh_full[sb], ph);
+        mbar_wait(&p_empty[sb], ph ^ 1u);
+        tc_fence_after();
+        const uint32_t abase = saddr(sSh + sb * kSharedBytes);
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+          for (int tap = 0; tap < 4; ++tap)
+#pragma unroll
+            for (int kk = 0; kk < 3; ++kk) {
+              const uint32_t a = abase + (uint32_t)(2 * kk) * kSibPlane +
+                                 (uint32_t)(mt * 128 + (tap >> 1) * 21 + (tap & 1)) * 16u;
+              const int kw = tap * 48 + 16 * kk;
+              const uint32_t w_off = (uint32_t)(kw >> 6) * (N * 128) + (uint32_t)((kw & 63) * 2);
+              mma_pred(tmem + sb * 128 + (uint32_t)(mt * N), desc_planar(a, kSibPlane), wsh + (w_off >> 4), idesc,
+                       (tap | kk) != 0, elected);
+            }
+        commit_pred(&sh_empty[sb], elected);
+        commit_pred(&p_full[sb], elected);
+        cur_p = p;
+      }
+      // new frame of child img: 4 tiles x 4 taps x 1 K-step
+      const uint32_t nb = j % kNewRing, nph = (j / kNewRing) & 1u;
+      const uint32_t cb = j & 1u, cph = (j >> 1) & 1u;
+      mbar_wait(&n_full[nb], nph);
+      mbar_wait(&c_empty[cb], cph ^ 1u);
+      tc_fence_after();
+      const uint32_t nbase = saddr(sNw + nb * kNewBytes);
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int tap = 0; tap < 4; ++tap) {
+          const uint32_t a = nbase + (uint32_t)(mt * 128 + (tap >> 1) * 21 + (tap & 1)) * 16u;
+          const uint32_t w_off = (uint32_t)((tap * 16) * 2);
+          mma_pred(tmem + 256 + cb * 128 + (uint32_t)(mt * N), desc_planar(a, kSibPlane), wnw + (w_off >> 4), idesc,
+                   tap != 0, elected);
+        }
+      commit_pred(&n_empty[nb], elected);
+      commit_pred(&c_full[cb], elected);
+      __syncwarp();
+    }
+  } else if (warp < 9) {
+    // ---------------------------------------------- epilogue: relu(P + C_a + b) -> conv2's s2d(2) SW128 input
+    constexpr int HALF = N / 2;
+    const int q4 = warp & 3;
+    const int c0 = ((warp - 1) >> 2) * HALF;
+    const int r = q4 * 32 + lane;
+    float bias_r[HALF];
+#pragma unroll
+    for (int c = 0; c < HALF; ++c) bias_r[c] = sbias[c0 + c];
+    uint32_t j = 0;
+    for (int64_t img = i0; img < i1; ++img, ++j) {
+      const int64_t c = c_begin + img, p = c / A;
+      const uint32_t k = (uint32_t)(p - pfirst_cta), sb = k & 1u, ph = (k >> 1) & 1u;
+      const bool last_of_parent = (img + 1 == i1) || ((c + 1) / A != p);
+      const uint32_t cb = j & 1u, cph = (j >> 1) & 1u;
+      mbar_wait(&p_full[sb], ph);
+      mbar_wait(&c_full[cb], cph);
+      tc_fence_after();
+      const uint32_t lanes = (uint32_t)(q4 * 32) << 16;
+      uint8_t *oimg = out + img * (int64_t)P.out_img_bytes;
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {   // two tiles at a time (register budget)
+        uint32_t vp[2][16], vc[2][16];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int mt = 2 * hf + u;
+          tmem_ld16_nw(tmem + lanes + sb * 128 + (uint32_t)(mt * N + c0), vp[u]);
+          tmem_ld16_nw(tmem + lanes + 256 + cb * 128 + (uint32_t)(mt * N + c0), vc[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          tmem_wait16(vp[u]);
+          tmem_wait16(vc[u]);
+        }
+        if (hf == 1) {
+          tc_fence_before();
+          mbar_arrive(&c_empty[cb]);
+          if (last_of_parent) mbar_arrive(&p_empty[sb]);
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int q = (2 * hf + u) * 128 + r;
+          const int oy = q / 21, ox = q - oy * 21;
+          if (oy >= 20 || ox >= 20) continue;
+          uint32_t pk[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float x = (__uint_as_float(vp[u][2 * e]) + __uint_as_float(vc[u][2 * e])) + bias_r[2 * e];
+            const float y = (__uint_as_float(vp[u][2 * e + 1]) + __uint_as_float(vc[u][2 * e + 1])) + bias_r[2 * e + 1];
+            __nv_bfloat162 hh = __floats2bfloat162_rn(x > 0.0f ? x : 0.0f, y > 0.0f ? y : 0.0f);
+            pk[e] = *(uint32_t *)&hh;
+          }
+          const int sub = ((oy & 1) << 1) | (ox & 1);
+          const int row = (oy >> 1) * P.out_w + (ox >> 1);
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2)
+            *(uint4 *)(oimg + act_off(2, P.out_plane, row, sub * 4 + ((c0 + 8 * h2) >> 3))) =
+                make_uint4(pk[4 * h2], pk[4 * h2 + 1], pk[4 * h2 + 2], pk[4 * h2 + 3]);
+        }
+      }
+    }
+  } else {
+    // ---------------------------------------------- converters (8 warps)
+    const int t = threadIdx.x - 288;   // 0..255
+    int64_t cur_p = -1;
+    uint32_t k = 0, j = 0;
+    for (int64_t img = i0; img < i1; ++img, ++j) {
+      const int64_t c = c_begin + img, p = c / A;
+      const int a = (int)(c - p * A);
+      const int64_t pl = p - p_first;
+      if (p != cur_p) {   // shared image of a new parent + its newest-frame bytes
+        k = (uint32_t)(p - pfirst_cta);
+        const uint32_t sb = k & 1u, ph = (k >> 1) & 1u;
+        mbar_wait(&sh_empty[sb], ph ^ 1u);
+        const uint8_t *pf = par.state + pl * par.state_stride;
+        uint8_t *sh = sSh + sb * kSharedBytes;
+        uint32_t *n3 = sNew3 + sb * (7056 / 4);
+        for (int task = t; task < 441 * 2; task += kConvThreads) {
+          const int pix = task >> 1, dyp = task & 1;
+          const int Y = pix / 21, X = pix - Y * 21;
+          const int pa = (4 * Y + 2 * dyp) * 84 + 4 * X;           // dy = 2*dyp, 2*dyp+1 (4 pixels each)
+          const uint4 x = __ldg((const uint4 *)pf + (pa >> 2));
+          const uint4 y = __ldg((const uint4 *)pf + ((pa + 84) >> 2));
+          // child frame c = parent frame c+1 (bytes 1..3), 8 values per plane row: (dy0: dx0..3, dy1: dx0..3)
+#pragma unroll
+          for (int cc = 0; cc < 3; ++cc) {
+            const uint32_t sel = 0x7540u + (uint32_t)(cc + 1);
+            auto cv = [&](uint32_t w) { return __float_as_uint(__uint_as_float(__byte_perm(w, 0x4B000000u, sel)) - 8388608.0f); };
+            const uint4 v = make_uint4(__byte_perm(cv(x.x), cv(x.y), 0x7632u), __byte_perm(cv(x.z), cv(x.w), 0x7632u),
+                                       __byte_perm(cv(y.x), cv(y.y), 0x7632u), __byte_perm(cv(y.z), cv(y.w), 0x7632u));
+            *(uint4 *)(sh + (size_t)(2 * cc + dyp) * kSibPlane + (size_t)pix * 16) = v;
+          }
+          n3[pa >> 2] = __byte_perm(__byte_perm(x.x, x.y, 0x0073u), __byte_perm(x.z, x.w, 0x0073u), 0x5410u);
+          n3[(pa + 84) >> 2] = __byte_perm(__byte_perm(y.x, y.y, 0x0073u), __byte_perm(y.z, y.w, 0x0073u), 0x5410u);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&sh_full[sb]);
+        conv_bar();       // sNew3 of this parent complete for every converter
+        cur_p = p;
+      }
+      const uint32_t sb = k & 1u;
+      const uint64_t key = *(const uint64_t *)((const uint8_t *)par.key + pl * par.key_stride);
+      const uint64_t k2 = mix64d(key ^ (0x9E3779B97F4A7C15ull * (uint64_t)(a + 1)));
+      if (t == 0) {
+        const uint32_t tt = (uint32_t)(k2 >> 61);
+        const float rw = tt == 7u ? 1.0f : (tt == 0u ? -1.0f : 0.0f);
+        cum_out[img] = fmaf(gk, rw, par.cum ? par.cum[pl] : 0.0f);
+      }
+      const uint32_t nb = j % kNewRing, nph = (j / kNewRing) & 1u;
+      mbar_wait(&n_empty[nb], nph ^ 1u);
+      uint8_t *nw = sNw + nb * kNewBytes;
+      const uint32_t *n3 = sNew3 + sb * (7056 / 4);
+      for (int task = t; task < 441 * 2; task += kConvThreads) {
+        const int pix = task >> 1, dyp = task & 1;
+        const int Y = pix / 21, X = pix - Y * 21;
+        const int pa = (4 * Y + 2 * dyp) * 84 + 4 * X;
+        const int pb = pa + 84;
+        const uint32_t na = (uint32_t)(mix64d(k2 + (uint64_t)(pa >> 3)) >> (8 * (pa & 7)));
+        const uint32_t nbz = (uint32_t)(mix64d(k2 + (uint64_t)(pb >> 3)) >> (8 * (pb & 7)));
+        const uint32_t ba = n3[pa >> 2] ^ na, bb = n3[pb >> 2] ^ nbz;   // child newest-frame bytes
+        const uint4 v = make_uint4(u8pair_bf16x2(ba, 0), u8pair_bf16x2(ba, 2), u8pair_bf16x2(bb, 0), u8pair_bf16x2(bb, 2));
+        *(uint4 *)(nw + (size_t)dyp * kSibPlane + (size_t)pix * 16) = v;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&n_full[nb]);
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
 int num_sms() {
   static int n = 0;
   if (!n) {
@@ -601,6 +857,21 @@ void launch_conv1_fused(const ConvSW &P, const Layer &L, const NodeView &par, in
   const int grid = (int)std::min<int64_t>(n_img, num_sms());
   k_conv1_fused<<<grid, kThreadsF, smem, st>>>(P, P.wsw, L.bias, par, p_first, c_begin, n_img, A, gk, (uint8_t *)out,
                                                cum_out);
+}
+
+void launch_conv1_sib(const ConvSW &P, const Layer &L, const uint8_t *wsh, const uint8_t *wnw, const NodeView &par,
+                      int64_t p_first, int64_t c_begin, int64_t n_img, int A, float gk, void *out, float *cum_out,
+                      cudaStream_t st) {
+  if (n_img <= 0) return;
+  constexpr int smem = 4 * 32 * 128 + 2 * (int)kSharedBytes + kNewRing * (int)kNewBytes + 2 * 7056 + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_conv1_sib, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  const int grid = (int)std::min<int64_t>(n_img, num_sms());
+  k_conv1_sib<<<grid, kThreadsF, smem, st>>>(P, wsh, wnw, L.bias, par, p_first, c_begin, n_img, A, gk,
+                                             (uint8_t *)out, cum_out);
 }
 
 void launch_conv_sw(const ConvSW &P, const Layer &L, const void *in, int64_t n_img, void *out, cudaStream_t st) {
