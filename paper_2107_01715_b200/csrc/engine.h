@@ -122,7 +122,8 @@ struct ConvSW {
   int out_w = 0, out_mode = 0;                 // 0: s2d(2) planar, 1: planar, 2: dense [row][N]
   const uint8_t *wsw = nullptr;                // weights pre-swizzled as their SW128 smem image
   int layout = 0;                              // activation layout (see act_off)
-  uint32_t copy_chunks = 1;                    // bulk copies per input image
+  uint32_t copy_chunks = 1;                    // (unused) bulk copies per input image
+  int in_rows = 0;                             // valid input rows per 64-channel block
 };
 void launch_conv_sw(const ConvSW &P, const Layer &L, const void *in, int64_t n_img, void *out, cudaStream_t st);
 void conv_trace_set(unsigned long long *p, int sel);

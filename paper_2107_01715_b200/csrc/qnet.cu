@@ -219,6 +219,65 @@ __global__ void __launch_bounds__(128) k_head(const float *__restrict__ zv, int6
   }
 }
 
+// Rainbow head, block-staged: 8 leaves per CTA. Their z rows are loaded into
+// shared memory with coalesced float4 loads, then one thread per (leaf, action)
+// computes the softmax expectation over the atoms (mean_a adv[a][i] shared per
+// leaf); fused max_a and fmaf(g_d, max, R_d).
+constexpr int kHeadLeaves = 8;
+template <int ATOMS>
+__global__ void __launch_bounds__(256) k_head_rainbow(const float *__restrict__ zv, int64_t ldv,
+                                                      const float *__restrict__ za, int64_t lda, int A, float vmin,
+                                                      float dz, int64_t n, int mode, float gd,
+                                                      const float *__restrict__ cum, float *__restrict__ out) {
+  extern __shared__ float hsm[];
+  const int AN = (A * ATOMS + 3) & ~3;              // smem row stride (float4 staging; lda >= AN)
+  float *sa = hsm;                                  // [kHeadLeaves][AN]
+  float *svm = sa + kHeadLeaves * AN;               // [kHeadLeaves][ATOMS]: v_i - mean_a adv[a][i]
+  float *sq = svm + kHeadLeaves * ATOMS;            // [kHeadLeaves][A]
+  const int64_t l0 = (int64_t)blockIdx.x * kHeadLeaves;
+  const int nl = n - l0 < kHeadLeaves ? (int)(n - l0) : kHeadLeaves;
+  // coalesced staging (lda and AN are multiples of 4 floats)
+  for (int l = 0; l < nl; ++l) {
+    const float4 *src = (const float4 *)(za + (l0 + l) * lda);
+    float4 *dst = (float4 *)(sa + l * AN);
+    for (int e = threadIdx.x; e < AN / 4; e += blockDim.x) dst[e] = src[e];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < nl * ATOMS; e += blockDim.x) {
+    const int l = e / ATOMS, t = e - l * ATOMS;
+    float s = 0.0f;
+    for (int a = 0; a < A; ++a) s += sa[l * AN + a * ATOMS + t];
+    svm[e] = zv[(l0 + l) * ldv + t] - s / (float)A;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < nl * A; e += blockDim.x) {
+    const int l = e / A, a = e - l * A;
+    const float *ad = sa + l * AN + a * ATOMS;
+    const float *vm = svm + l * ATOMS;
+    float mx = -INFINITY;
+#pragma unroll 17
+    for (int t = 0; t < ATOMS; ++t) mx = fmaxf(mx, vm[t] + ad[t]);
+    float den = 0.0f, num = 0.0f;
+#pragma unroll 17
+    for (int t = 0; t < ATOMS; ++t) {
+      const float ex = expf(vm[t] + ad[t] - mx);
+      den += ex;
+      num += (vmin + (float)t * dz) * ex;
+    }
+    const float q = num / den;
+    sq[e] = q;
+    if (mode == MODE_ROWS) out[(l0 + l) * A + a] = q;
+  }
+  __syncthreads();
+  if (mode != MODE_ROWS && threadIdx.x < nl) {
+    const int l = threadIdx.x;
+    float best = -INFINITY;
+    for (int a = 0; a < A; ++a) best = fmaxf(best, sq[l * A + a]);
+    if (mode == MODE_ROWMAX) out[l0 + l] = best;
+    else out[l0 + l] = fmaf(gd, best, cum ? cum[l0 + l] : 0.0f);
+  }
+}
+
 // ------------------------------------------------------------ build / eval
 static int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
@@ -457,15 +516,15 @@ int net_build(Net &net, const bcts_config &cfg, std::string &err) {
   {
     ConvSW &a = net.sw1;
     a.N = 32; a.K = 256; a.Cin = 64; a.KH = a.KW = 2; a.W_in = 21; a.OH = a.OW = 20; a.n_mt = (20 * 21 + 127) / 128;
-    a.plane = kPlane1; a.in_img_bytes = kIn1Bytes;
+    a.plane = kPlane1; a.in_img_bytes = kIn1Bytes; a.in_rows = 21 * 21;
     a.out_mode = 0; a.out_plane = kPlane2; a.out_w = 10; a.out_img_bytes = kIn2Bytes;
     ConvSW &b = net.sw2;
     b.N = 64; b.K = 512; b.Cin = 128; b.KH = b.KW = 2; b.W_in = 10; b.OH = b.OW = 9; b.n_mt = (9 * 10 + 127) / 128;
-    b.plane = kPlane2; b.in_img_bytes = kIn2Bytes;
+    b.plane = kPlane2; b.in_img_bytes = kIn2Bytes; b.in_rows = 10 * 10;
     b.out_mode = 1; b.out_plane = kPlane3; b.out_w = 9; b.out_img_bytes = kIn3Bytes;
     ConvSW &c = net.sw3;
     c.N = 64; c.K = 576; c.Cin = 64; c.KH = c.KW = 3; c.W_in = 9; c.OH = c.OW = 7; c.n_mt = (7 * 9 + 127) / 128;
-    c.plane = kPlane3; c.in_img_bytes = kIn3Bytes;
+    c.plane = kPlane3; c.in_img_bytes = kIn3Bytes; c.in_rows = 9 * 9;
     c.out_mode = 2; c.out_plane = 0; c.out_w = 7; c.out_img_bytes = 3136 * 2;
     const int layout = 2;   // SW128 row blocks, address-based swizzle (the compiled MMA loop assumes it)
     a.layout = b.layout = c.layout = layout;
@@ -600,8 +659,13 @@ static int eval_conv(Net &net, const NodeView *par, const NodeView *img, int64_t
       run_layer(net, KC_FC_OUT, net.z_a, net.hid_act, nf, net.za, st, &net.p_z_a);
       const float dz = (net.vmax - net.vmin) / (float)(net.atoms - 1);
       if (net.prof) net.prof->begin(KC_HEAD, (double)nf * 4.0 * (net.ld_za + net.ld_zv + 1), st);
-      k_head<true><<<(unsigned)((nf + 3) / 4), 128, 0, st>>>(net.zv, net.ld_zv, net.za, net.ld_za, A, net.atoms,
-                                                              net.vmin, dz, nf, mode, gd, cum, o);
+      if (net.atoms == 51)
+        k_head_rainbow<51><<<(unsigned)((nf + kHeadLeaves - 1) / kHeadLeaves), 256,
+                             (size_t)kHeadLeaves * (((A * 51 + 3) & ~3) + 51 + A) * 4, st>>>(net.zv, net.ld_zv, net.za, net.ld_za,
+                                                                               A, net.vmin, dz, nf, mode, gd, cum, o);
+      else
+        k_head<true><<<(unsigned)((nf + 3) / 4), 128, 0, st>>>(net.zv, net.ld_zv, net.za, net.ld_za, A, net.atoms,
+                                                                net.vmin, dz, nf, mode, gd, cum, o);
       if (net.prof) net.prof->end(st);
       launches += 3;
     }

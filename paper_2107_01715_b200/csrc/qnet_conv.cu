@@ -220,13 +220,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t b = i & 1u, ph = (i >> 1) & 1u;
         mbar_wait(&in_empty[b], ph ^ 1u);
         if (g_trace && P.out_mode == g_trace_sel && blockIdx.x == 0 && i < 64) g_trace[i * 4 + 0] = gtime();
-        mbar_expect_tx(&in_full[b], P.in_img_bytes);
-        // the image as several bulk copies in flight (per-request TMA throughput)
-        const uint32_t chunk = (P.in_img_bytes / P.copy_chunks + 15u) & ~15u;
-        for (uint32_t o = 0; o < P.in_img_bytes; o += chunk) {
-          const uint32_t len = min(chunk, P.in_img_bytes - o);
-          bulk_g2s(saddr(sIn0 + b * in_stride) + o, in + img * (int64_t)P.in_img_bytes + o, len, &in_full[b]);
-        }
+        // only the valid rows of each 64-channel row block cross memory (the
+        // windows of garbage outputs read stale smem rows, which is harmless)
+        const uint32_t blk = P.plane * 8u, valid = (uint32_t)P.in_rows * 128u;
+        const uint32_t nblk = P.in_img_bytes / blk;
+        mbar_expect_tx(&in_full[b], nblk * valid);
+        for (uint32_t q = 0; q < nblk; ++q)
+          bulk_g2s(saddr(sIn0 + b * in_stride) + q * blk, in + img * (int64_t)P.in_img_bytes + q * blk, valid,
+                   &in_full[b]);
       }
     }
     __syncwarp();
@@ -571,12 +572,15 @@ __global__ void __launch_bounds__(kThreadsF, 1)
 // order inside an s2d(4) pixel (c, dy, dx): plane j of the shared image holds
 // frame c = j/2 at dy in {2(j%2), 2(j%2)+1}; the new image has 2 planes (dy pairs).
 //   warp 0: MMA issuer   warps 1-8: epilogue   warps 9-16: converters
+constexpr int kSibThreads = 480;                    // warp 0 MMA, 1-8 epilogue, 9-14 converters
+constexpr int kSibConv = 192;
+__device__ __forceinline__ void sib_bar() { asm volatile("bar.sync 1, 192;" ::: "memory"); }
 constexpr uint32_t kSibPlane = 536 * 16;            // rows 0..535 x 16 B
 constexpr uint32_t kSharedBytes = 6 * kSibPlane;    // 51,456
 constexpr uint32_t kNewBytes = 2 * kSibPlane;       // 17,152
 constexpr int kNewRing = 3;
 
-__global__ void __launch_bounds__(kThreadsF, 1)
+__global__ void __launch_bounds__(kSibThreads, 1)
     k_conv1_sib(ConvSW P, const uint8_t *__restrict__ Wsh, const uint8_t *__restrict__ Wnw,
                 const float *__restrict__ bias, NodeView par, int64_t p_first, int64_t c_begin, int64_t n_img, int A,
                 float gk, uint8_t *__restrict__ out, float *__restrict__ cum_out) {
@@ -588,6 +592,7 @@ __global__ void __launch_bounds__(kThreadsF, 1)
   uint8_t *sSh = sWnw + N * 128;                     // 2 x shared image
   uint8_t *sNw = sSh + 2 * kSharedBytes;             // kNewRing x new image
   uint32_t *sNew3 = (uint32_t *)(sNw + kNewRing * kNewBytes);   // 2 x parent newest-frame bytes (7056 B)
+  uint64_t *sNoise = (uint64_t *)((uint8_t *)sNew3 + 2 * 7056);   // 882 noise words of the current child
   __shared__ __align__(8) uint64_t sh_full[2], sh_empty[2], p_full[2], p_empty[2];
   __shared__ __align__(8) uint64_t n_full[kNewRing], n_empty[kNewRing], c_full[2], c_empty[2], wbar;
   __shared__ uint32_t tmem_slot;
@@ -598,7 +603,7 @@ __global__ void __launch_bounds__(kThreadsF, 1)
   if (threadIdx.x < N) sbias[threadIdx.x] = bias[threadIdx.x];
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&sh_full[i], kConvThreads);
+      mbar_init(&sh_full[i], kSibConv);
       mbar_init(&sh_empty[i], 1);
       mbar_init(&p_full[i], 1);
       mbar_init(&p_empty[i], 256);
@@ -606,7 +611,7 @@ __global__ void __launch_bounds__(kThreadsF, 1)
       mbar_init(&c_empty[i], 256);
     }
     for (int i = 0; i < kNewRing; ++i) {
-      mbar_init(&n_full[i], kConvThreads);
+      mbar_init(&n_full[i], kSibConv);
       mbar_init(&n_empty[i], 1);
     }
     mbar_init(&wbar, 1);
@@ -676,59 +681,66 @@ __global__ void __launch_bounds__(kThreadsF, 1)
           mma_pred(tmem + 256 + cb * 128 + (uint32_t)(mt * N), desc_planar(a, kSibPlane), wnw + (w_off >> 4), idesc,
                    tap != 0, elected);
         }
+      if (g_trace && g_trace_sel == 10 && blockIdx.x == 0 && j < 64 && elected) g_trace[j * 4 + 2] = gtime();
       commit_pred(&n_empty[nb], elected);
       commit_pred(&c_full[cb], elected);
       __syncwarp();
     }
   } else if (warp < 9) {
     // ---------------------------------------------- epilogue: relu(P + C_a + b) -> conv2's s2d(2) SW128 input
+    // P (the parent's shared-frame part) is read from TMEM once per parent and
+    // kept in registers; each child then reads only its own C_a (TMEM reads are
+    // the epilogue's limit).
     constexpr int HALF = N / 2;
     const int q4 = warp & 3;
     const int c0 = ((warp - 1) >> 2) * HALF;
     const int r = q4 * 32 + lane;
-    float bias_r[HALF];
-#pragma unroll
-    for (int c = 0; c < HALF; ++c) bias_r[c] = sbias[c0 + c];
+    const uint32_t lanes = (uint32_t)(q4 * 32) << 16;
+    uint32_t vp[4][16];
+    int64_t cur_p = -1;
     uint32_t j = 0;
     for (int64_t img = i0; img < i1; ++img, ++j) {
       const int64_t c = c_begin + img, p = c / A;
-      const uint32_t k = (uint32_t)(p - pfirst_cta), sb = k & 1u, ph = (k >> 1) & 1u;
-      const bool last_of_parent = (img + 1 == i1) || ((c + 1) / A != p);
+      if (p != cur_p) {
+        const uint32_t k = (uint32_t)(p - pfirst_cta), sb = k & 1u, ph = (k >> 1) & 1u;
+        mbar_wait(&p_full[sb], ph);
+        tc_fence_after();
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) tmem_ld16_nw(tmem + lanes + sb * 128 + (uint32_t)(mt * N + c0), vp[mt]);
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) tmem_wait16(vp[mt]);
+        tc_fence_before();
+        mbar_arrive(&p_empty[sb]);   // the next parent's P may be accumulated now
+        cur_p = p;
+      }
       const uint32_t cb = j & 1u, cph = (j >> 1) & 1u;
-      mbar_wait(&p_full[sb], ph);
       mbar_wait(&c_full[cb], cph);
       tc_fence_after();
-      const uint32_t lanes = (uint32_t)(q4 * 32) << 16;
       uint8_t *oimg = out + img * (int64_t)P.out_img_bytes;
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {   // two tiles at a time (register budget)
-        uint32_t vp[2][16], vc[2][16];
+        uint32_t vc[2][16];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int mt = 2 * hf + u;
-          tmem_ld16_nw(tmem + lanes + sb * 128 + (uint32_t)(mt * N + c0), vp[u]);
-          tmem_ld16_nw(tmem + lanes + 256 + cb * 128 + (uint32_t)(mt * N + c0), vc[u]);
-        }
+        for (int u = 0; u < 2; ++u)
+          tmem_ld16_nw(tmem + lanes + 256 + cb * 128 + (uint32_t)((2 * hf + u) * N + c0), vc[u]);
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          tmem_wait16(vp[u]);
-          tmem_wait16(vc[u]);
-        }
+        for (int u = 0; u < 2; ++u) tmem_wait16(vc[u]);
         if (hf == 1) {
           tc_fence_before();
           mbar_arrive(&c_empty[cb]);
-          if (last_of_parent) mbar_arrive(&p_empty[sb]);
         }
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
-          const int q = (2 * hf + u) * 128 + r;
+          const int mt = 2 * hf + u;
+          const int q = mt * 128 + r;
           const int oy = q / 21, ox = q - oy * 21;
           if (oy >= 20 || ox >= 20) continue;
           uint32_t pk[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
-            const float x = (__uint_as_float(vp[u][2 * e]) + __uint_as_float(vc[u][2 * e])) + bias_r[2 * e];
-            const float y = (__uint_as_float(vp[u][2 * e + 1]) + __uint_as_float(vc[u][2 * e + 1])) + bias_r[2 * e + 1];
+            const float x = (__uint_as_float(vp[mt][2 * e]) + __uint_as_float(vc[u][2 * e])) + sbias[c0 + 2 * e];
+            const float y =
+                (__uint_as_float(vp[mt][2 * e + 1]) + __uint_as_float(vc[u][2 * e + 1])) + sbias[c0 + 2 * e + 1];
             __nv_bfloat162 hh = __floats2bfloat162_rn(x > 0.0f ? x : 0.0f, y > 0.0f ? y : 0.0f);
             pk[e] = *(uint32_t *)&hh;
           }
@@ -740,24 +752,32 @@ __global__ void __launch_bounds__(kThreadsF, 1)
                 make_uint4(pk[4 * h2], pk[4 * h2 + 1], pk[4 * h2 + 2], pk[4 * h2 + 3]);
         }
       }
+      if (g_trace && g_trace_sel == 10 && blockIdx.x == 0 && j < 64 && r == 0 && c0 == 0) g_trace[j * 4 + 3] = gtime();
     }
   } else {
     // ---------------------------------------------- converters (8 warps)
-    const int t = threadIdx.x - 288;   // 0..255
+    const int t = threadIdx.x - 288;   // 0..191
     int64_t cur_p = -1;
     uint32_t k = 0, j = 0;
+    uint64_t pkey = 0;
+    float pcum = 0.0f;
     for (int64_t img = i0; img < i1; ++img, ++j) {
       const int64_t c = c_begin + img, p = c / A;
       const int a = (int)(c - p * A);
       const int64_t pl = p - p_first;
       if (p != cur_p) {   // shared image of a new parent + its newest-frame bytes
+        pkey = *(const uint64_t *)((const uint8_t *)par.key + pl * par.key_stride);   // once per parent
+        pcum = par.cum ? par.cum[pl] : 0.0f;
         k = (uint32_t)(p - pfirst_cta);
         const uint32_t sb = k & 1u, ph = (k >> 1) & 1u;
         mbar_wait(&sh_empty[sb], ph ^ 1u);
         const uint8_t *pf = par.state + pl * par.state_stride;
         uint8_t *sh = sSh + sb * kSharedBytes;
         uint32_t *n3 = sNew3 + sb * (7056 / 4);
-        for (int task = t; task < 441 * 2; task += kConvThreads) {
+#pragma unroll
+        for (int it = 0; it < (441 * 2 + kSibConv - 1) / kSibConv; ++it) {
+          const int task = t + it * kSibConv;
+          if (task >= 441 * 2) break;
           const int pix = task >> 1, dyp = task & 1;
           const int Y = pix / 21, X = pix - Y * 21;
           const int pa = (4 * Y + 2 * dyp) * 84 + 4 * X;           // dy = 2*dyp, 2*dyp+1 (4 pixels each)
@@ -777,34 +797,47 @@ __global__ void __launch_bounds__(kThreadsF, 1)
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive(&sh_full[sb]);
-        conv_bar();       // sNew3 of this parent complete for every converter
+        sib_bar();        // sNew3 of this parent complete for every converter
         cur_p = p;
       }
       const uint32_t sb = k & 1u;
-      const uint64_t key = *(const uint64_t *)((const uint8_t *)par.key + pl * par.key_stride);
-      const uint64_t k2 = mix64d(key ^ (0x9E3779B97F4A7C15ull * (uint64_t)(a + 1)));
+      const uint64_t k2 = mix64d(pkey ^ (0x9E3779B97F4A7C15ull * (uint64_t)(a + 1)));   // child key
       if (t == 0) {
         const uint32_t tt = (uint32_t)(k2 >> 61);
         const float rw = tt == 7u ? 1.0f : (tt == 0u ? -1.0f : 0.0f);
-        cum_out[img] = fmaf(gk, rw, par.cum ? par.cum[pl] : 0.0f);
+        cum_out[img] = fmaf(gk, rw, pcum);   // R_d = fmaf(g[d-1], r, R_{d-1})
       }
       const uint32_t nb = j % kNewRing, nph = (j / kNewRing) & 1u;
+      // the child's 882 noise words (one mix64 per 8-pixel group; each is shared by two tasks)
+      sib_bar();   // previous child's tasks are done reading sNoise
+#pragma unroll
+      for (int it = 0; it < (882 + kSibConv - 1) / kSibConv; ++it) {
+        const int g = t + it * kSibConv;
+        if (g < 882) sNoise[g] = mix64d(k2 + (uint64_t)g);
+      }
       mbar_wait(&n_empty[nb], nph ^ 1u);
+      sib_bar();   // noise table complete
+      const bool tr = g_trace && g_trace_sel == 10 && blockIdx.x == 0 && j < 64 && t == 0;
+      if (tr) g_trace[j * 4 + 0] = gtime();
       uint8_t *nw = sNw + nb * kNewBytes;
       const uint32_t *n3 = sNew3 + sb * (7056 / 4);
-      for (int task = t; task < 441 * 2; task += kConvThreads) {
+#pragma unroll
+      for (int it = 0; it < (441 * 2 + kSibConv - 1) / kSibConv; ++it) {
+        const int task = t + it * kSibConv;
+        if (task >= 441 * 2) break;
         const int pix = task >> 1, dyp = task & 1;
         const int Y = pix / 21, X = pix - Y * 21;
         const int pa = (4 * Y + 2 * dyp) * 84 + 4 * X;
         const int pb = pa + 84;
-        const uint32_t na = (uint32_t)(mix64d(k2 + (uint64_t)(pa >> 3)) >> (8 * (pa & 7)));
-        const uint32_t nbz = (uint32_t)(mix64d(k2 + (uint64_t)(pb >> 3)) >> (8 * (pb & 7)));
+        const uint32_t na = (uint32_t)(sNoise[pa >> 3] >> (8 * (pa & 7)));
+        const uint32_t nbz = (uint32_t)(sNoise[pb >> 3] >> (8 * (pb & 7)));
         const uint32_t ba = n3[pa >> 2] ^ na, bb = n3[pb >> 2] ^ nbz;   // child newest-frame bytes
         const uint4 v = make_uint4(u8pair_bf16x2(ba, 0), u8pair_bf16x2(ba, 2), u8pair_bf16x2(bb, 0), u8pair_bf16x2(bb, 2));
         *(uint4 *)(nw + (size_t)dyp * kSibPlane + (size_t)pix * 16) = v;
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(&n_full[nb]);
+      if (tr) g_trace[j * 4 + 1] = gtime();
     }
   }
   __syncthreads();
@@ -863,14 +896,14 @@ void launch_conv1_sib(const ConvSW &P, const Layer &L, const uint8_t *wsh, const
                       int64_t p_first, int64_t c_begin, int64_t n_img, int A, float gk, void *out, float *cum_out,
                       cudaStream_t st) {
   if (n_img <= 0) return;
-  constexpr int smem = 4 * 32 * 128 + 2 * (int)kSharedBytes + kNewRing * (int)kNewBytes + 2 * 7056 + 1024;
+  constexpr int smem = 4 * 32 * 128 + 2 * (int)kSharedBytes + kNewRing * (int)kNewBytes + 2 * 7056 + 882 * 8 + 1024;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_conv1_sib, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
   const int grid = (int)std::min<int64_t>(n_img, num_sms());
-  k_conv1_sib<<<grid, kThreadsF, smem, st>>>(P, wsh, wnw, L.bias, par, p_first, c_begin, n_img, A, gk,
+  k_conv1_sib<<<grid, kSibThreads, smem, st>>>(P, wsh, wnw, L.bias, par, p_first, c_begin, n_img, A, gk,
                                              (uint8_t *)out, cum_out);
 }
 

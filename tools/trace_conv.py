@@ -12,9 +12,9 @@ buf = torch.zeros(64 * 4, dtype=torch.int64, device="cuda")
 layer = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 lib = P.lib(); lib.bcts_debug_conv_trace.argtypes = [ctypes.c_void_p, ctypes.c_int32]
 lib.bcts_debug_conv_trace(buf.data_ptr(), layer)
-if layer == 9:   # fused conv1: run a real search (d=2 -> 324 leaves per root)
-    roots = torch.from_numpy(config("C5").roots(4).copy()).cuda()
-    h.search(roots, 4, 2, 0.99, 1.0, 1); torch.cuda.synchronize()
+if layer in (9, 10):   # fused conv1: run a real search (d=2 -> 324 leaves per root)
+    roots = torch.from_numpy(config("C5").roots(1).copy()).cuda()
+    h.search(roots, 1, 4, 0.99, 1.0, 1); torch.cuda.synchronize()
 else:
     h.q_rows(recs, n); torch.cuda.synchronize()
 lib.bcts_debug_conv_trace(None, -1)
