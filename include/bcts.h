@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define BCTS_ABI_VERSION 1
+#define BCTS_ABI_VERSION 2   /* 2: env_weights fields + BCTS_ENV_DNN */
 
 typedef struct bcts_handle_t *bcts_handle;
 
@@ -64,13 +64,25 @@ typedef enum {
  *   INT_HASH   : uint32 s[16]                                     (64 B)
  *   ATARI_HASH : uint64 key, uint64 pad, uint32 w[84*84]          (28,240 B)
  *                w[p] packs the 4-frame stack of pixel p, byte c = frame c
- *                (c = 0 oldest, 3 newest; frame stacking P:355). */
-typedef enum { BCTS_ENV_TABULAR = 1, BCTS_ENV_INT_HASH = 2, BCTS_ENV_ATARI_HASH = 3 } bcts_env_kind;
+ *                (c = 0 oldest, 3 newest; frame stacking P:355).
+ *   DNN        : float32 s[100]                                    (400 B)
+ *                random-DNN learned forward model of the runtime study
+ *                (P:340-341): [s; onehot(a)] -> 3 x (Linear 100, ReLU) ->
+ *                Linear 101 = (s', r); fp32, each output one fixed-order
+ *                fmaf chain from the bias over the inputs in index order
+ *                (R27). Weights: bcts_config.env_weights. */
+typedef enum {
+  BCTS_ENV_TABULAR = 1,
+  BCTS_ENV_INT_HASH = 2,
+  BCTS_ENV_ATARI_HASH = 3,
+  BCTS_ENV_DNN = 4
+} bcts_env_kind;
 
 /* Value nets Q_theta (DESIGN.md §3 NET_SPEC; random-init weights, shapes of P:83). */
 typedef enum {
   BCTS_NET_TABLE = 1,        /* tabular Q_hat [nS*A] (TABULAR env only)          */
-  BCTS_NET_MLP2_F32 = 2,     /* 64 -> hidden -> A, fp32 fixed-order FMA (INT_HASH) */
+  BCTS_NET_MLP2_F32 = 2,     /* in -> hidden -> A, fp32 fixed-order FMA: INT_HASH
+                              * (in = 64 state bytes / 256) or DNN (in = 100 floats) */
   BCTS_NET_NATURE_BF16 = 3,  /* Nature-DQN conv trunk + fc 512 + fc A, bf16      */
   BCTS_NET_RAINBOW_BF16 = 4  /* same trunk + dueling C51 head (51 atoms), bf16   */
 } bcts_net_kind;
@@ -96,11 +108,18 @@ typedef struct {
   int32_t net;              /* bcts_net_kind */
   const float *weights;     /* canonical PyTorch-order fp32 blob (synth.inputs.weight_specs) */
   int64_t weights_count;    /* number of floats in weights */
-  int32_t mlp_in, mlp_hidden; /* MLP2: 64, hidden (<= 1024) */
+  int32_t mlp_in, mlp_hidden; /* MLP2: 64 (INT_HASH) or 100 (DNN), hidden (<= 1024) */
   int32_t atoms;            /* Rainbow atoms (51) */
   float v_min, v_max;       /* Rainbow support [-10, 10] */
   int64_t workspace_bytes_max; /* per-call device workspace budget; 0 = auto (16 GiB) */
   uint32_t flags;           /* BCTS_F_* */
+  /* DNN env only (HOST pointer, repacked at create; caller may free after):
+   * canonical fp32 blob g1.w [100][100+A], g1.b [100], g2.w [100][100], g2.b,
+   * g3.w [100][100], g3.b, g4.w [101][100], g4.b [101] (synth.inputs.env_weight_specs).
+   * INVALID_ARG if null or env_weights_count != 40,501 + 100*A (the sum of
+   * those sizes); ignored for the other envs. */
+  const float *env_weights;
+  int64_t env_weights_count;
 } bcts_config;
 
 typedef struct {
@@ -129,7 +148,10 @@ const char *bcts_last_error(bcts_handle h); /* detail for the last failing call 
  *   roots        : device, n_roots root records (layout above)
  *   depth        : d >= 0 (d = 0 -> greedy on Q_hat(s_0,.))
  *   A            : must equal cfg.num_actions
- *   gamma        : in (0,1);  beta: finite, >= 0;  correction_on: 0/1
+ *   gamma        : in (0,1);  beta: finite, >= 0
+ *   correction_on: 0 = vanilla d-step greedy (Eq. 2); 1 = BCTS with the Bellman
+ *                  penalty B of Eq. 5; 2 = BCTS with Lemma 2's exact
+ *                  bias gap B_e - B_o (App. A.2) at sigma = delta/sqrt(2)
  *   actions_out  : device int32 [n_roots]      argmax of the (corrected) root Q
  *   root_q_out   : device float [n_roots * A]  corrected root Q (R14)
  * Errors: INVALID_ARG, BUDGET, CUDA. n_roots == 0 is a no-op returning OK. */

@@ -8,4 +8,5 @@ paper_2107_01715_b200/ and never imports it.
 
 Parity-pin status of every function: DESIGN.md §2 ("Oracle pins").
 """
-from .oracle import Oracle, build, bf16_round, penalty_eq5, bias_gap_eq4, LIB_PATH  # noqa: F401
+from .oracle import (Oracle, build, bf16_round, penalty_eq5, bias_gap_eq4, inv_norm_cdf, B_n, bias_exact,  # noqa: F401
+                     LIB_PATH)

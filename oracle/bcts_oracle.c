@@ -28,6 +28,12 @@
 #include <stdlib.h>
 #include <string.h>
 #include <fenv.h>
+#ifndef M_PI
+#define M_PI 3.14159265358979323846
+#endif
+#ifndef M_E
+#define M_E 2.7182818284590452354
+#endif
 #ifdef _OPENMP
 #include <omp.h>
 #endif
@@ -35,6 +41,8 @@
 #define OR_ENV_TABULAR 1
 #define OR_ENV_INT_HASH 2
 #define OR_ENV_ATARI_HASH 3
+#define OR_ENV_DNN 4          /* random-DNN learned forward model, state = 100 floats */
+#define DNN_S 100
 #define OR_NET_TABLE 1
 #define OR_NET_MLP2 2
 #define OR_NET_NATURE 3
@@ -62,6 +70,8 @@ typedef struct {
   double *zvw, *zvb, *zaw, *zab;          /* Rainbow fc_z_v / fc_z_a */
   int atoms;
   double vmin, vmax;
+  /* random-DNN forward model: g1 [100][100+A], g2 [100][100], g3 [100][100], g4 [101][100] (+ biases) */
+  float *gw[4], *gb[4];
 } oracle_model;
 
 /* Internal state: the oracle keeps Atari frames as 4 separate planes
@@ -71,6 +81,7 @@ typedef struct {
   uint32_t s[16];             /* INT_HASH */
   uint64_t key;               /* ATARI_HASH */
   uint8_t plane[4][NPIX];     /* ATARI_HASH: plane 0 oldest, 3 newest */
+  float x[DNN_S];             /* DNN */
 } ostate;
 
 static uint64_t o_mix64(uint64_t z) {   /* splitmix64 finalizer (ENV_SPEC) */
@@ -114,6 +125,7 @@ static float *dup_f32(const float *w, long n) {
 
 void oracle_destroy(oracle_model *m) {
   if (!m) return;
+  for (int i = 0; i < 4; ++i) { free(m->gw[i]); free(m->gb[i]); }
   void *ptrs[] = {m->tab_next, m->tab_reward, m->tab_q, m->l1w, m->l1b, m->l2w, m->l2b,
                   m->c1w, m->c1b, m->c2w, m->c2b, m->c3w, m->c3b, m->f1w, m->f1b, m->f2w, m->f2b,
                   m->hvw, m->hvb, m->haw, m->hab, m->zvw, m->zvb, m->zaw, m->zab};
@@ -182,10 +194,27 @@ oracle_model *oracle_create(int env, int A, int nS, const int32_t *tab_next, con
   return m;
 }
 
+/* random-DNN forward-model weights (canonical fp32 blob: g1.w, g1.b, g2.w, g2.b, g3.w, g3.b, g4.w, g4.b) */
+int oracle_set_env_weights(oracle_model *m, const float *w, long count) {
+  const int A = m->A;
+  const long sz[8] = {100L * (100 + A), 100, 100L * 100, 100, 100L * 100, 100, 101L * 100, 101};
+  long need = 0;
+  for (int i = 0; i < 8; ++i) need += sz[i];
+  if (m->env != OR_ENV_DNN || count != need) return -1;
+  for (int i = 0; i < 4; ++i) {
+    m->gw[i] = dup_f32(w, sz[2 * i]);
+    w += sz[2 * i];
+    m->gb[i] = dup_f32(w, sz[2 * i + 1]);
+    w += sz[2 * i + 1];
+  }
+  return 0;
+}
+
 /* ------------------------------------------------------- record <-> state */
 long oracle_record_bytes(const oracle_model *m) {
   if (m->env == OR_ENV_TABULAR) return 4;
   if (m->env == OR_ENV_INT_HASH) return 64;
+  if (m->env == OR_ENV_DNN) return 4 * DNN_S;
   return 16 + 4L * NPIX;
 }
 
@@ -194,6 +223,8 @@ static void from_record(const oracle_model *m, const uint8_t *rec, ostate *s) {
     memcpy(&s->id, rec, 4);
   } else if (m->env == OR_ENV_INT_HASH) {
     memcpy(s->s, rec, 64);
+  } else if (m->env == OR_ENV_DNN) {
+    memcpy(s->x, rec, 4 * DNN_S);
   } else {
     memcpy(&s->key, rec, 8);
     const uint8_t *px = rec + 16;
@@ -211,6 +242,8 @@ static void to_record(const oracle_model *m, const ostate *s, uint8_t *rec) {
     memcpy(rec, &s->id, 4);
   } else if (m->env == OR_ENV_INT_HASH) {
     memcpy(rec, s->s, 64);
+  } else if (m->env == OR_ENV_DNN) {
+    memcpy(rec, s->x, 4 * DNN_S);
   } else {
     uint64_t pad = 0;
     memcpy(rec, &s->key, 8);
@@ -226,7 +259,7 @@ static void to_record(const oracle_model *m, const ostate *s, uint8_t *rec) {
 /* ------------------------------------------------------------- env step G */
 /* Deterministic forward model (P:44 deterministic transitions; ENV_SPEC in
  * DESIGN.md §3). Returns 0 on success, -1 on a domain error. */
-static int env_step(const oracle_model *m, const ostate *s, int a, ostate *out, double *r) {
+static int env_step(const oracle_model *m, const ostate *s, int a, ostate *out, double *r, int mode) {
   if (a < 0 || a >= m->A) return -1;
   if (m->env == OR_ENV_TABULAR) {
     if (s->id < 0 || s->id >= m->nS) return -1;
@@ -242,6 +275,56 @@ static int env_step(const oracle_model *m, const ostate *s, int a, ostate *out, 
     }
     uint32_t t = out->s[0] >> 30;
     *r = (t == 3) ? 1.0 : (t == 0) ? -1.0 : 0.0;
+    return 0;
+  }
+  if (m->env == OR_ENV_DNN) {
+    /* random-DNN learned model: x = [s; onehot(a)] -> 3 ReLU layers of
+     * width 100 -> linear 101 = (next state, reward) (R27). fp32 mirror: fixed-order
+     * fmaf chains from the bias over the inputs in index order; fp64 mode: doubles. */
+    const int A = m->A, I1 = DNN_S + A;
+    if (mode) {
+      float in[DNN_S + MAXA], h[2][DNN_S];
+      for (int j = 0; j < I1; ++j) in[j] = j < DNN_S ? s->x[j] : (j - DNN_S == a ? 1.0f : 0.0f);
+      const float *src = in;
+      int nin = I1;
+      for (int L = 0; L < 3; ++L) {
+        float *dst = h[L & 1];
+        for (int u = 0; u < DNN_S; ++u) {
+          float acc = m->gb[L][u];
+          for (int i = 0; i < nin; ++i) acc = fmaf(m->gw[L][(long)u * nin + i], src[i], acc);
+          dst[u] = acc > 0.0f ? acc : 0.0f;
+        }
+        src = dst;
+        nin = DNN_S;
+      }
+      for (int u = 0; u <= DNN_S; ++u) {
+        float acc = m->gb[3][u];
+        for (int i = 0; i < DNN_S; ++i) acc = fmaf(m->gw[3][(long)u * DNN_S + i], src[i], acc);
+        if (u < DNN_S) out->x[u] = acc;
+        else *r = (double)acc;
+      }
+    } else {
+      double in[DNN_S + MAXA], h[2][DNN_S];
+      for (int j = 0; j < I1; ++j) in[j] = j < DNN_S ? (double)s->x[j] : (j - DNN_S == a ? 1.0 : 0.0);
+      const double *src = in;
+      int nin = I1;
+      for (int L = 0; L < 3; ++L) {
+        double *dst = h[L & 1];
+        for (int u = 0; u < DNN_S; ++u) {
+          double acc = (double)m->gb[L][u];
+          for (int i = 0; i < nin; ++i) acc += (double)m->gw[L][(long)u * nin + i] * src[i];
+          dst[u] = acc > 0.0 ? acc : 0.0;
+        }
+        src = dst;
+        nin = DNN_S;
+      }
+      for (int u = 0; u <= DNN_S; ++u) {
+        double acc = (double)m->gb[3][u];
+        for (int i = 0; i < DNN_S; ++i) acc += (double)m->gw[3][(long)u * DNN_S + i] * src[i];
+        if (u < DNN_S) out->x[u] = (float)acc;   /* states are stored as fp32 in both modes */
+        else *r = acc;
+      }
+    }
     return 0;
   }
   /* ATARI_HASH: shift the frame stack by one frame; the new newest frame is
@@ -263,7 +346,7 @@ static int env_step(const oracle_model *m, const ostate *s, int a, ostate *out, 
 int oracle_step(const oracle_model *m, const void *rec_in, int a, void *rec_out, double *r) {
   ostate *s = (ostate *)malloc(sizeof(ostate)), *o = (ostate *)malloc(sizeof(ostate));
   from_record(m, (const uint8_t *)rec_in, s);
-  int rc = env_step(m, s, a, o, r);
+  int rc = env_step(m, s, a, o, r, 1);   /* fp32 mirror for the DNN model */
   if (rc == 0) to_record(m, o, (uint8_t *)rec_out);
   free(s); free(o);
   return rc;
@@ -313,9 +396,14 @@ static int qrow(const oracle_model *m, const ostate *s, int mode, double *q) {
     double x[256];
     float xf[256];
     for (int j = 0; j < I; ++j) {
-      uint32_t byte = (s->s[(j / 4) & 15] >> (8 * (j % 4))) & 0xFFu;
-      x[j] = (double)byte / 256.0;
-      xf[j] = (float)byte / 256.0f;
+      if (m->env == OR_ENV_DNN) {          /* DNN env: the 100 state floats are the features */
+        xf[j] = s->x[j];
+        x[j] = (double)s->x[j];
+      } else {                             /* INT_HASH: byte j / 256 (exact) */
+        uint32_t byte = (s->s[(j / 4) & 15] >> (8 * (j % 4))) & 0xFFu;
+        x[j] = (double)byte / 256.0;
+        xf[j] = (float)byte / 256.0f;
+      }
     }
     if (mode) { /* fp32 mirror: fixed-order fmaf chains starting from the bias */
       float h[1024];
@@ -438,6 +526,56 @@ double oracle_bias_gap_eq4(double so, double se, int A, int d) {
   return sqrt(2.0 * log((double)A)) * (se * sqrt((double)d) - so * sqrt((double)(d - 1))) - (se - so) / 2.0;
 }
 
+/* ------------------------------------------------- Lemma 2 exact biases */
+/* Inverse standard normal CDF: Acklam's rational approximation refined by one
+ * Halley step on erfc (|Phi(z) - p| ~ 1e-15). Independent of the CUDA path,
+ * which uses the CUDA math library's normcdfinv. */
+double oracle_inv_norm_cdf(double p) {
+  static const double a[] = {-3.969683028665376e+01, 2.209460984245205e+02, -2.759285104469687e+02,
+                             1.383577518672690e+02, -3.066479806614716e+01, 2.506628277459239e+00};
+  static const double b[] = {-5.447609879822406e+01, 1.615858368580409e+02, -1.556989798598866e+02,
+                             6.680131188771972e+01, -1.328068155288572e+01};
+  static const double c[] = {-7.784894002430293e-03, -3.223964580411365e-01, -2.400758277161838e+00,
+                             -2.549732539343734e+00, 4.374664141464968e+00, 2.938163982698783e+00};
+  static const double dd[] = {7.784695709041462e-03, 3.224671290700398e-01, 2.445134137142996e+00,
+                              3.754408661907416e+00};
+  if (!(p > 0.0 && p < 1.0)) return NAN;
+  const double plow = 0.02425, phigh = 1 - plow;
+  double x;
+  if (p < plow) {
+    double q = sqrt(-2 * log(p));
+    x = (((((c[0] * q + c[1]) * q + c[2]) * q + c[3]) * q + c[4]) * q + c[5]) /
+        ((((dd[0] * q + dd[1]) * q + dd[2]) * q + dd[3]) * q + 1);
+  } else if (p <= phigh) {
+    double q = p - 0.5, r = q * q;
+    x = (((((a[0] * r + a[1]) * r + a[2]) * r + a[3]) * r + a[4]) * r + a[5]) * q /
+        (((((b[0] * r + b[1]) * r + b[2]) * r + b[3]) * r + b[4]) * r + 1);
+  } else {
+    double q = sqrt(-2 * log(1 - p));
+    x = -(((((c[0] * q + c[1]) * q + c[2]) * q + c[3]) * q + c[4]) * q + c[5]) /
+        ((((dd[0] * q + dd[1]) * q + dd[2]) * q + dd[3]) * q + 1);
+  }
+  /* Halley refinement: e = Phi(x) - p, u = e * sqrt(2 pi) exp(x^2/2) */
+  double e = 0.5 * erfc(-x / sqrt(2.0)) - p;
+  double u = e * sqrt(2 * M_PI) * exp(x * x / 2);
+  return x - u / (1 + x * u / 2);
+}
+
+/* B(n) of App. A.2: 0 if n = 1, else
+ * gamma_EM * Phi^-1(1 - 1/(e n)) + (1 - gamma_EM) * Phi^-1(1 - 1/n). */
+double oracle_B_n(double n) {
+  const double gem = 0.57721566490153286; /* Euler-Mascheroni */
+  if (n <= 1.0) return 0.0;
+  return gem * oracle_inv_norm_cdf(1.0 - 1.0 / (M_E * n)) + (1.0 - gem) * oracle_inv_norm_cdf(1.0 - 1.0 / n);
+}
+
+/* Lemma 2: B_o = sigma_o B(A^(d-1)), B_e = sigma_e B(A^d - A^(d-1));
+ * returns the exact gap B_e - B_o (Eq. 3's subtrahend before gamma^d). */
+double oracle_bias_exact(double sigma_o, double sigma_e, int A, int d) {
+  double ad1 = pow((double)A, (double)(d - 1)), ad = pow((double)A, (double)d);
+  return sigma_e * oracle_B_n(ad - ad1) - sigma_o * oracle_B_n(ad1);
+}
+
 /* --------------------------------------------------------------- the DFS */
 typedef struct {
   const oracle_model *m;
@@ -465,7 +603,7 @@ static int dfs(dfs_ctx *c, int t, double R, double *best, long *leaf) {
   for (int a = 0; a < m->A; ++a) {
     double r, v;
     long lf;
-    if (env_step(m, s, a, &c->buf[t + 1], &r)) return -1;
+    if (env_step(m, s, a, &c->buf[t + 1], &r, c->mode)) return -1;
     if (dfs(c, t + 1, acc_reward(c->mode, c->g, t, r, R), &v, &lf)) return -1;
     if (v > bv) { bv = v; bl = (long)a * span + lf; }
   }
@@ -477,7 +615,7 @@ static int dfs(dfs_ctx *c, int t, double R, double *best, long *leaf) {
 /* BCTS terms at one root: pi_o, delta_o, delta_e, B (Prop. 1, Eq. 5).
  * delta_a = r(s0,a) + gamma max Q(s1^a, .) - Q(s0, a) with depth-0/1 samples. */
 static int bcts_terms(const oracle_model *m, const ostate *root, int d, int mode, const double *g,
-                      double *terms, double *q0) {
+                      double *terms, double *q0, int corr) {
   const int A = m->A;
   ostate *s1 = (ostate *)malloc(sizeof(ostate));
   double q1[MAXA], delta[MAXA];
@@ -485,7 +623,7 @@ static int bcts_terms(const oracle_model *m, const ostate *root, int d, int mode
   int pio = argmax_low(q0, A);
   for (int a = 0; a < A && !rc; ++a) {
     double r;
-    rc = env_step(m, root, a, s1, &r);
+    rc = env_step(m, root, a, s1, &r, mode);
     if (!rc) rc = qrow(m, s1, mode, q1);
     if (rc) break;
     double R1 = acc_reward(mode, g, 0, r, 0.0);
@@ -500,7 +638,8 @@ static int bcts_terms(const oracle_model *m, const ostate *root, int d, int mode
   terms[0] = pio;
   terms[1] = dob;
   terms[2] = de;
-  terms[3] = oracle_penalty_eq5(de, dob, A, d);
+  /* corr == 2: Lemma 2's exact gap with sigma = delta / sqrt(2) (Prop. 1); else Eq. 5 */
+  terms[3] = corr == 2 ? oracle_bias_exact(dob / sqrt(2.0), de / sqrt(2.0), A, d) : oracle_penalty_eq5(de, dob, A, d);
   return 0;
 }
 
@@ -545,7 +684,7 @@ int oracle_search(const oracle_model *m, const void *roots, long n_roots, int de
       from_record(m, (const uint8_t *)roots + r * rb, &c.buf[0]);
       double rr, v = 0.0;
       long lf = 0;
-      int rc = env_step(m, &c.buf[0], a0, &c.buf[1], &rr);
+      int rc = env_step(m, &c.buf[0], a0, &c.buf[1], &rr, mode);
       if (!rc) rc = dfs(&c, 1, acc_reward(mode, g, 0, rr, 0.0), &v, &lf);
       long span = 1;
       for (int k = 1; k < depth; ++k) span *= A;
@@ -569,7 +708,7 @@ int oracle_search(const oracle_model *m, const void *roots, long n_roots, int de
       for (int a = 0; a < A; ++a) { vr[a] = q0[a]; q[a] = q0[a]; bl[r * A + a] = 0; }
       terms[0] = argmax_low(q0, A);
     } else {
-      if (corr && bcts_terms(m, root, depth, mode, g, terms, q0)) { err = 1; break; }
+      if (corr && bcts_terms(m, root, depth, mode, g, terms, q0, corr)) { err = 1; break; }
       apply_correction(A, depth, mode, g, beta, corr, vr, terms, q);
     }
     actions[r] = argmax_low(q, A);
@@ -600,7 +739,7 @@ int oracle_node(const oracle_model *m, const void *root_rec, int level, int64_t 
     for (int k = t + 1; k < level; ++k) div *= A;
     int act = (int)((index / div) % A);
     double r;
-    rc = env_step(m, a, act, b, &r);
+    rc = env_step(m, a, act, b, &r, mode);
     R = acc_reward(mode, g, t, r, R);
     ostate *tmp = a; a = b; b = tmp;
   }
@@ -643,7 +782,7 @@ int oracle_search_bruteforce(const oracle_model *m, const void *roots, long n_ro
     }
     if (rc) break;
     from_record(m, rr, root);
-    if (corr) rc = bcts_terms(m, root, depth, mode, g, terms, q0);
+    if (corr) rc = bcts_terms(m, root, depth, mode, g, terms, q0, corr);
     if (rc) break;
     apply_correction(A, depth, mode, g, beta, corr, van, terms, qq);
     actions[r] = argmax_low(qq, A);
@@ -677,7 +816,7 @@ int oracle_terms(const oracle_model *m, const void *roots, long n_roots, int dep
   int rc = 0;
   for (long r = 0; r < n_roots && !rc; ++r) {
     from_record(m, (const uint8_t *)roots + r * rb, root);
-    rc = bcts_terms(m, root, depth, mode, g, terms_out + 4 * r, q0_out + (long)m->A * r);
+    rc = bcts_terms(m, root, depth, mode, g, terms_out + 4 * r, q0_out + (long)m->A * r, 1);
   }
   free(root);
   return rc;
@@ -705,8 +844,8 @@ int oracle_search_subtrees(const oracle_model *m, const void *root_rec, int dept
     from_record(m, (const uint8_t *)root_rec, &c.buf[0]);
     double r0, r1, v = 0.0;
     long lf = 0;
-    int rc = env_step(m, &c.buf[0], (int)(t / A), mid, &r0);
-    if (!rc) rc = env_step(m, mid, (int)(t % A), &c.buf[2], &r1);
+    int rc = env_step(m, &c.buf[0], (int)(t / A), mid, &r0, mode);
+    if (!rc) rc = env_step(m, mid, (int)(t % A), &c.buf[2], &r1, mode);
     if (!rc) rc = dfs(&c, 2, acc_reward(mode, g, 1, r1, acc_reward(mode, g, 0, r0, 0.0)), &v, &lf);
     out[t - t_begin] = v;
     if (rc) {

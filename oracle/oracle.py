@@ -14,7 +14,7 @@ LIB_PATH = os.path.join(_HERE, "liboracle.so")
 _lock = threading.Lock()
 _lib = None
 
-ENV_TABULAR, ENV_INT_HASH, ENV_ATARI_HASH = 1, 2, 3
+ENV_TABULAR, ENV_INT_HASH, ENV_ATARI_HASH, ENV_DNN = 1, 2, 3, 4
 NET_TABLE, NET_MLP2_F32, NET_NATURE_BF16, NET_RAINBOW_BF16 = 1, 2, 3, 4
 
 
@@ -61,6 +61,13 @@ def _load():
             lib.oracle_search_subtrees.argtypes = [P, P, I, D, I, I, L, L, P]
             lib.oracle_leaf_total.restype = I
             lib.oracle_leaf_total.argtypes = [P, P, I, C.c_int64, D, I, C.POINTER(D)]
+            for fn in ("oracle_inv_norm_cdf", "oracle_B_n"):
+                getattr(lib, fn).restype = D
+                getattr(lib, fn).argtypes = [D]
+            lib.oracle_bias_exact.restype = D
+            lib.oracle_bias_exact.argtypes = [D, D, I, I]
+            lib.oracle_set_env_weights.restype = I
+            lib.oracle_set_env_weights.argtypes = [P, P, L]
             lib.oracle_max_threads.restype = I
             _lib = lib
     return _lib
@@ -78,6 +85,19 @@ def penalty_eq5(delta_e: float, delta_o: float, A: int, d: int) -> float:
     return _load().oracle_penalty_eq5(float(delta_e), float(delta_o), int(A), int(d))
 
 
+def inv_norm_cdf(p: float) -> float:
+    return _load().oracle_inv_norm_cdf(float(p))
+
+
+def B_n(n: float) -> float:
+    return _load().oracle_B_n(float(n))
+
+
+def bias_exact(sigma_o: float, sigma_e: float, A: int, d: int) -> float:
+    """Lemma 2 exact gap B_e - B_o."""
+    return _load().oracle_bias_exact(float(sigma_o), float(sigma_e), int(A), int(d))
+
+
 def bias_gap_eq4(sigma_o: float, sigma_e: float, A: int, d: int) -> float:
     return _load().oracle_bias_gap_eq4(float(sigma_o), float(sigma_e), int(A), int(d))
 
@@ -86,7 +106,7 @@ class Oracle:
     """One model (env + value net). Modes: 0 = fp64 reference, 1 = fp32 mirror."""
 
     def __init__(self, env: int, A: int, net: int, tab=None, weights=None,
-                 mlp_in=64, mlp_hidden=256, atoms=51, v_min=-10.0, v_max=10.0):
+                 mlp_in=64, mlp_hidden=256, atoms=51, v_min=-10.0, v_max=10.0, env_weights=None):
         lib = _load()
         self.env, self.A, self.net = env, A, net
         nS = 0
@@ -103,13 +123,19 @@ class Oracle:
                                     v_min, v_max)
         if not self._h:
             raise ValueError("oracle_create rejected the model")
+        if env_weights is not None:
+            ew = np.ascontiguousarray(env_weights, np.float32)
+            self._keep = self._keep + (ew,)
+            if lib.oracle_set_env_weights(self._h, _ptr(ew), ew.size):
+                raise ValueError("oracle_set_env_weights rejected the blob")
         self.record_bytes = lib.oracle_record_bytes(self._h)
 
     @classmethod
     def from_config(cls, cfg, tab=None):
-        from synth.inputs import make_weights  # input generator only
-        w = None if cfg.net == NET_TABLE else make_weights(cfg.net, cfg.A, cfg.wseed)[0]
-        return cls(cfg.env, cfg.A, cfg.net, tab=tab, weights=w)
+        from synth.inputs import make_weights, make_env_weights  # input generators only
+        w = None if cfg.net == NET_TABLE else make_weights(cfg.net, cfg.A, cfg.wseed, **cfg.net_kw())[0]
+        ew = make_env_weights(cfg) if cfg.env == ENV_DNN else None
+        return cls(cfg.env, cfg.A, cfg.net, tab=tab, weights=w, env_weights=ew, **cfg.net_kw())
 
     def close(self):
         if getattr(self, "_h", None):

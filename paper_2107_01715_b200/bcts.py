@@ -13,13 +13,13 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libbcts.so")
 
-ENV_TABULAR, ENV_INT_HASH, ENV_ATARI_HASH = 1, 2, 3
+ENV_TABULAR, ENV_INT_HASH, ENV_ATARI_HASH, ENV_DNN = 1, 2, 3, 4
 NET_TABLE, NET_MLP2_F32, NET_NATURE_BF16, NET_RAINBOW_BF16 = 1, 2, 3, 4
 F_CLAMP_PENALTY, F_SIMT_NET, F_MATERIALIZE_LEAVES = 0x1, 0x2, 0x4
-ABI_VERSION = 1
+ABI_VERSION = 2
 STATUS = {0: "BCTS_OK", 1: "BCTS_ERR_INVALID_ARG", 2: "BCTS_ERR_UNSUPPORTED", 3: "BCTS_ERR_OUT_OF_MEMORY",
           4: "BCTS_ERR_BUDGET", 5: "BCTS_ERR_CUDA", 7: "BCTS_ERR_NUMERIC"}
-RECORD_BYTES = {ENV_TABULAR: 4, ENV_INT_HASH: 64, ENV_ATARI_HASH: 28240}
+RECORD_BYTES = {ENV_TABULAR: 4, ENV_INT_HASH: 64, ENV_ATARI_HASH: 28240, ENV_DNN: 400}
 
 # every symbol include/bcts.h declares (checked by tests/test_abi.py)
 EXPORTS = ["bcts_create", "bcts_destroy", "bcts_abi_version", "bcts_root_record_bytes", "bcts_status_string",
@@ -41,7 +41,7 @@ class Config(C.Structure):
                 ("net", C.c_int32), ("weights", C.c_void_p), ("weights_count", C.c_int64),
                 ("mlp_in", C.c_int32), ("mlp_hidden", C.c_int32), ("atoms", C.c_int32),
                 ("v_min", C.c_float), ("v_max", C.c_float), ("workspace_bytes_max", C.c_int64),
-                ("flags", C.c_uint32)]
+                ("flags", C.c_uint32), ("env_weights", C.c_void_p), ("env_weights_count", C.c_int64)]
 
 
 class KernelProfile(C.Structure):
@@ -134,7 +134,7 @@ class Handle:
 
     def __init__(self, env: int, A: int, net: int, *, weights=None, tab=None, device: int = 0, stream=None,
                  mlp_in: int = 64, mlp_hidden: int = 256, atoms: int = 51, v_min: float = -10.0,
-                 v_max: float = 10.0, workspace_bytes_max: int = 0, flags: int = 0):
+                 v_max: float = 10.0, workspace_bytes_max: int = 0, flags: int = 0, env_weights=None):
         import torch
         self.env, self.A, self.net, self.device = env, A, net, device
         if stream is None:
@@ -157,6 +157,10 @@ class Handle:
             w = np.ascontiguousarray(weights, np.float32)
             keep.append(w)
             cfg.weights, cfg.weights_count = _p(w).value, w.size
+        if env_weights is not None:
+            ew = np.ascontiguousarray(env_weights, np.float32)
+            keep.append(ew)
+            cfg.env_weights, cfg.env_weights_count = _p(ew).value, ew.size
         cfg.mlp_in, cfg.mlp_hidden, cfg.atoms = mlp_in, mlp_hidden, atoms
         cfg.v_min, cfg.v_max = v_min, v_max
         cfg.workspace_bytes_max = workspace_bytes_max
@@ -170,9 +174,12 @@ class Handle:
 
     @classmethod
     def from_config(cls, cfg, tab=None, **kw):
-        from synth.inputs import make_weights  # input generator only
-        w = None if cfg.net == NET_TABLE else make_weights(cfg.net, cfg.A, cfg.wseed)[0]
-        return cls(cfg.env, cfg.A, cfg.net, weights=w, tab=tab, **kw)
+        from synth.inputs import make_weights, make_env_weights  # input generators only
+        nk = cfg.net_kw()
+        w = None if cfg.net == NET_TABLE else make_weights(cfg.net, cfg.A, cfg.wseed, **nk)[0]
+        if cfg.env == ENV_DNN:
+            kw.setdefault("env_weights", make_env_weights(cfg))
+        return cls(cfg.env, cfg.A, cfg.net, weights=w, tab=tab, **{**nk, **kw})
 
     def close(self):
         if getattr(self, "_h", None):

@@ -56,6 +56,13 @@ void launch_segmax(const float *totals, int64_t n, int64_t leaf_begin, int64_t l
   if (prof) prof->end(st);
 }
 
+// B(n) of App. A.2 with the CUDA math library's inverse normal CDF.
+__device__ double B_of_n(double n) {
+  const double gem = 0.57721566490153286;   // Euler-Mascheroni
+  if (n <= 1.0) return 0.0;
+  return gem * normcdfinv(1.0 - 1.0 / (2.718281828459045 * n)) + (1.0 - gem) * normcdfinv(1.0 - 1.0 / n);
+}
+
 // One thread per root.
 __global__ void k_finalize(FinalizeArgs f) {
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -88,9 +95,13 @@ __global__ void k_finalize(FinalizeArgs f) {
         else sum += fabs((double)delta);
       }
       const double de = sum / (double)(A - 1);
-      // Eq. 5 (natural log, R5)
-      double B = sqrt(log((double)A)) * (de * sqrt((double)f.d) - dob * sqrt((double)(f.d - 1))) -
-                 (de - dob) / sqrt(8.0);
+      double B;
+      if (f.corr == 2) {   // Lemma 2 exact gap B_e - B_o with sigma = delta / sqrt(2)
+        const double ad1 = pow((double)A, (double)(f.d - 1)), ad = ad1 * (double)A;
+        B = (de / sqrt(2.0)) * B_of_n(ad - ad1) - (dob / sqrt(2.0)) * B_of_n(ad1);
+      } else {             // Eq. 5 (natural log, R5)
+        B = sqrt(log((double)A)) * (de * sqrt((double)f.d) - dob * sqrt((double)(f.d - 1))) - (de - dob) / sqrt(8.0);
+      }
       if (f.clamp && B < 0.0) B = 0.0;
       terms[1] = (float)dob;
       terms[2] = (float)de;

@@ -20,6 +20,8 @@ struct bcts_handle_t {
   int env = 0, A = 0, nS = 0;
   uint32_t flags = 0;
   int32_t *d_next = nullptr;
+  float *d_envw = nullptr;   // DNN env image (dnn_repack)
+  EnvModel em;
   float *d_rew = nullptr;
   Net net;
   int64_t ws_max = 0;
@@ -41,10 +43,10 @@ namespace {
 const int64_t kDefaultWorkspace = 16LL << 30;
 
 int64_t state_bytes(int env) {
-  return env == BCTS_ENV_TABULAR ? 4 : env == BCTS_ENV_INT_HASH ? 64 : kFrameBytes;
+  return env == BCTS_ENV_TABULAR ? 4 : env == BCTS_ENV_INT_HASH ? 64 : env == BCTS_ENV_DNN ? 4 * kDnnS : kFrameBytes;
 }
 int64_t record_bytes(int env) {
-  return env == BCTS_ENV_TABULAR ? 4 : env == BCTS_ENV_INT_HASH ? 64 : kAtariRecord;
+  return env == BCTS_ENV_TABULAR ? 4 : env == BCTS_ENV_INT_HASH ? 64 : env == BCTS_ENV_DNN ? 4 * kDnnS : kAtariRecord;
 }
 int64_t node_bytes(int env) { return state_bytes(env) + (env == BCTS_ENV_ATARI_HASH ? 8 : 0) + 4; }
 size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
@@ -257,7 +259,7 @@ bcts_status run_shard(bcts_handle h, const void *roots, int32_t d, float gamma, 
     NodeView prev = root_view(h->env, roots, lo[0]);
     for (int k = 1; k <= dm; ++k) {
       const LevelBuf &b = ((dm - k) % 2 == 0) ? big : small;
-      launch_expand(h->env, prev, lo[k - 1], lo[k], hi[k], A, g[k - 1], h->d_next, h->d_rew, out_of(h->env, b),
+      launch_expand(h->env, prev, lo[k - 1], lo[k], hi[k], A, g[k - 1], h->em, out_of(h->env, b),
                     h->st, &h->prof);
       prev = view_of(h->env, b);
       trans += hi[k] - lo[k];
@@ -302,7 +304,7 @@ bcts_status run_prologue(bcts_handle h, const void *roots, int64_t n, float gamm
   for (int64_t r0 = 0; r0 < n; r0 += per) {
     const int64_t r1e = std::min(n, r0 + per);
     const int64_t cnt = (r1e - r0) * A;
-    launch_expand(h->env, root_view(h->env, roots, r0), r0, r0 * A, r1e * A, A, g[0], h->d_next, h->d_rew,
+    launch_expand(h->env, root_view(h->env, roots, r0), r0, r0 * A, r1e * A, A, g[0], h->em,
                   out_of(h->env, b), h->st, &h->prof);
     nl = net_eval(h->net, view_of(h->env, b), cnt, MODE_ROWMAX, 0.0f, m1 + r0 * A, h->st);
     cudaMemcpyAsync(r1 + r0 * A, b.cum, (size_t)cnt * 4, cudaMemcpyDeviceToDevice, h->st);
@@ -376,6 +378,7 @@ void bcts_destroy(bcts_handle h) {
   if (h->st) cudaStreamSynchronize(h->st);
   net_free(h->net);
   cudaFree(h->d_next);
+  cudaFree(h->d_envw);
   cudaFree(h->d_rew);
   cudaFree(h->ws);
   cudaFree(h->e2e_roots);
@@ -390,10 +393,12 @@ bcts_status bcts_create(const bcts_config *cfg, bcts_handle *out) {
   *out = nullptr;
   if (cfg->abi_version != BCTS_ABI_VERSION) return BCTS_ERR_INVALID_ARG;
   if (cfg->num_actions < 2 || cfg->num_actions > kMaxA) return BCTS_ERR_INVALID_ARG;
-  const bool env_ok = cfg->env == BCTS_ENV_TABULAR || cfg->env == BCTS_ENV_INT_HASH || cfg->env == BCTS_ENV_ATARI_HASH;
+  const bool env_ok = cfg->env == BCTS_ENV_TABULAR || cfg->env == BCTS_ENV_INT_HASH ||
+                      cfg->env == BCTS_ENV_ATARI_HASH || cfg->env == BCTS_ENV_DNN;
   if (!env_ok) return BCTS_ERR_INVALID_ARG;
   const bool pair_ok = (cfg->env == BCTS_ENV_TABULAR && cfg->net == BCTS_NET_TABLE) ||
                        (cfg->env == BCTS_ENV_INT_HASH && cfg->net == BCTS_NET_MLP2_F32) ||
+                       (cfg->env == BCTS_ENV_DNN && cfg->net == BCTS_NET_MLP2_F32) ||
                        (cfg->env == BCTS_ENV_ATARI_HASH &&
                         (cfg->net == BCTS_NET_NATURE_BF16 || cfg->net == BCTS_NET_RAINBOW_BF16));
   if (!pair_ok) return BCTS_ERR_UNSUPPORTED;
@@ -402,6 +407,9 @@ bcts_status bcts_create(const bcts_config *cfg, bcts_handle *out) {
     for (int64_t i = 0; i < (int64_t)cfg->num_states * cfg->num_actions; ++i)
       if (cfg->tab_next[i] < 0 || cfg->tab_next[i] >= cfg->num_states) return BCTS_ERR_INVALID_ARG;
   }
+  if (cfg->env == BCTS_ENV_DNN &&
+      (!cfg->env_weights || cfg->env_weights_count != dnn_env_weights_count(cfg->num_actions)))
+    return BCTS_ERR_INVALID_ARG;
   bcts_handle h = new (std::nothrow) bcts_handle_t();
   if (!h) return BCTS_ERR_OUT_OF_MEMORY;
   h->dev = cfg->device;
@@ -427,6 +435,19 @@ bcts_status bcts_create(const bcts_config *cfg, bcts_handle *out) {
       bcts_destroy(h);
       return BCTS_ERR_CUDA;
     }
+    h->em.tab_next = h->d_next;
+    h->em.tab_rew = h->d_rew;
+  }
+  if (cfg->env == BCTS_ENV_DNN) {
+    std::vector<float> img((size_t)kDnnImg + (size_t)kDnnS * cfg->num_actions);
+    dnn_repack(cfg->env_weights, cfg->num_actions, img.data());
+    if (cudaMalloc(&h->d_envw, img.size() * 4) != cudaSuccess ||
+        cudaMemcpy(h->d_envw, img.data(), img.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+      cudaGetLastError();
+      bcts_destroy(h);
+      return BCTS_ERR_CUDA;
+    }
+    h->em.dnn = h->d_envw;
   }
   std::string err;
   if (net_build(h->net, *cfg, err)) {
@@ -480,7 +501,7 @@ bcts_status bcts_finalize(bcts_handle h, const void *roots, int64_t n_roots, int
   bcts_status s = validate(h, roots, n_roots, depth, A, gamma);
   if (s) return s;
   if (!isfinite(beta) || beta < 0.0f) return fail(h, BCTS_ERR_INVALID_ARG, "beta must be finite and >= 0");
-  if (correction_on != 0 && correction_on != 1) return fail(h, BCTS_ERR_INVALID_ARG, "correction_on not 0/1");
+  if (correction_on < 0 || correction_on > 2) return fail(h, BCTS_ERR_INVALID_ARG, "correction_on not in {0,1,2}");
   if (n_roots == 0) return BCTS_OK;
   if (!actions_out || !root_q_out || (depth >= 1 && !keys))
     return fail(h, BCTS_ERR_INVALID_ARG, "NULL required pointer");
@@ -499,7 +520,7 @@ bcts_status bcts_search_ex(bcts_handle h, const void *roots, int64_t n_roots, in
   bcts_status s = validate(h, roots, n_roots, depth, A, gamma);
   if (s) return s;
   if (!isfinite(beta) || beta < 0.0f) return fail(h, BCTS_ERR_INVALID_ARG, "beta must be finite and >= 0");
-  if (correction_on != 0 && correction_on != 1) return fail(h, BCTS_ERR_INVALID_ARG, "correction_on not 0/1");
+  if (correction_on < 0 || correction_on > 2) return fail(h, BCTS_ERR_INVALID_ARG, "correction_on not in {0,1,2}");
   if (n_roots > 0 && (!actions_out || !root_q_out)) return fail(h, BCTS_ERR_INVALID_ARG, "NULL output pointer");
   if (stats) memset(stats, 0, sizeof(*stats));
   if (n_roots == 0) return BCTS_OK;
@@ -606,7 +627,7 @@ bcts_status bcts_expand(bcts_handle h, const void *roots, int64_t n_roots, int32
   int64_t n_prev = n_roots;
   for (int k = 1; k <= level; ++k) {
     const LevelBuf &b = ((level - k) % 2 == 0) ? big : small;
-    launch_expand(env, prev, 0, 0, n_prev * A, A, g[k - 1], h->d_next, h->d_rew, out_of(env, b), h->st);
+    launch_expand(env, prev, 0, 0, n_prev * A, A, g[k - 1], h->em, out_of(env, b), h->st);
     prev = view_of(env, b);
     n_prev *= A;
     h->launches += 1;
@@ -642,8 +663,9 @@ bcts_status bcts_profile_enable(bcts_handle h, int32_t on) {
 
 int32_t bcts_profile_read(bcts_handle h, bcts_kernel_profile *out, int32_t max) {
   static const char *names[KC_COUNT] = {"expand_atari", "expand_int", "expand_tabular", "conv1", "conv2", "conv3",
-                                        "fc_hidden", "fc_out", "head", "mlp", "table", "segmax", "finalize", "other"};
-  static const int units[KC_COUNT] = {0, 0, 0, 1, 1, 1, 1, 1, 0, 1, 0, 0, 0, 0};
+                                        "fc_hidden", "fc_out", "head", "mlp", "table", "segmax", "finalize", "other",
+                                        "expand_dnn"};
+  static const int units[KC_COUNT] = {0, 0, 0, 1, 1, 1, 1, 1, 0, 1, 0, 0, 0, 0, 1};
   if (!h || !out || max <= 0) return 0;
   cudaSetDevice(h->dev);
   cudaStreamSynchronize(h->st);

@@ -13,7 +13,7 @@ namespace bcts {
 // DESIGN.md §5) so bench.py can report achieved = work / duration.
 enum KernelClass {
   KC_EXPAND_ATARI = 0, KC_EXPAND_INT, KC_EXPAND_TAB, KC_CONV1, KC_CONV2, KC_CONV3, KC_FC_H, KC_FC_OUT, KC_HEAD,
-  KC_MLP, KC_TABLE, KC_SEGMAX, KC_FINALIZE, KC_OTHER, KC_COUNT
+  KC_MLP, KC_TABLE, KC_SEGMAX, KC_FINALIZE, KC_OTHER, KC_EXPAND_DNN, KC_COUNT
 };
 struct Profiler {
   bool on = false;
@@ -73,9 +73,20 @@ struct Profiler {
 // Expand parents (global level-k indices starting at p_first, view `par`) into
 // the children with global level-(k+1) indices [c_begin, c_end):
 // child c has parent c / A and action c % A (R1); R' = fmaf(gk, r, R).
+// Device-resident forward-model parameters (set at bcts_create).
+struct EnvModel {
+  const int32_t *tab_next = nullptr;  // TABULAR [nS*A]
+  const float *tab_rew = nullptr;     // TABULAR [nS*A]
+  const float *dnn = nullptr;         // DNN: smem image (kDnnImg floats) followed by W1A [A][100]
+};
+constexpr int kDnnS = 100;                         // DNN state width
+constexpr int kDnnImg = 3 * 10000 + 10400 + 404;   // W1T|W2T|W3T|W4T[100][104]|b1|b2|b3|b4[104] floats
+int64_t dnn_env_weights_count(int A);              // canonical blob size: 40,501 + 100*A
+// canonical blob (include/bcts.h) -> device image (host side; out has kDnnImg + 100*A floats)
+void dnn_repack(const float *blob, int A, float *out);
+
 void launch_expand(int env, const NodeView &par, int64_t p_first, int64_t c_begin, int64_t c_end, int A,
-                   float gk, const int32_t *tab_next, const float *tab_rew, const NodeOut &out,
-                   cudaStream_t st, Profiler *prof = nullptr);
+                   float gk, const EnvModel &em, const NodeOut &out, cudaStream_t st, Profiler *prof = nullptr);
 
 // s2d bf16 frames for the conv1 tensor-core layer (expand.cu)
 // planar != 0: write the chunk-planar layout (plane = bytes per 8-channel plane,
@@ -160,6 +171,7 @@ struct Net {
   // MLP2
   const float *l1w = nullptr, *l1b = nullptr, *l2w = nullptr, *l2b = nullptr;
   int in = 0, hid = 0;
+  int feat_f32 = 0;               // DNN env: features are the fp32 state itself
   // conv nets
   Layer c1, c2, c3, fc_h, z_v, z_a, fc2;
   int atoms = 51;

@@ -31,21 +31,26 @@ __global__ void k_table(const int32_t *__restrict__ ids, int64_t stride_bytes, c
 }
 
 // ------------------------------------------------------------------ MLP2
-// One warp per state. x_j = byte j of the state / 256 (exact); hidden unit u:
+// One warp per state. x_j = byte j of the state / 256 (exact; INT_HASH) or the
+// j-th fp32 state component (DNN env, feat_f32); hidden unit u:
 // acc = b1[u]; acc = fmaf(W1[u][i], x_i, acc) for i = 0..in-1; h = acc > 0 ? acc : 0.
 // Output a: acc = b2[a]; acc = fmaf(W2[a][u], h_u, acc) for u = 0..hid-1.
 constexpr int kMlpWarps = 4;
 __global__ void __launch_bounds__(32 * kMlpWarps)
     k_mlp(const uint8_t *__restrict__ states, int64_t stride_bytes, const float *__restrict__ w1,
           const float *__restrict__ b1, const float *__restrict__ w2, const float *__restrict__ b2, int IN, int H,
-          int A, int64_t n, int mode, float gd, const float *__restrict__ cum, float *__restrict__ out) {
-  __shared__ float xs[kMlpWarps][64];
+          int A, int64_t n, int mode, float gd, const float *__restrict__ cum, float *__restrict__ out,
+          int feat_f32) {
+  __shared__ float xs[kMlpWarps][128];
   __shared__ float hs[kMlpWarps][1024];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int64_t i = (int64_t)blockIdx.x * kMlpWarps + warp;
   if (i >= n) return;
   const uint8_t *s = states + i * stride_bytes;
-  for (int j = lane; j < IN; j += 32) xs[warp][j] = (float)s[j] / 256.0f;
+  if (feat_f32)
+    for (int j = lane; j < IN; j += 32) xs[warp][j] = ((const float *)s)[j];
+  else
+    for (int j = lane; j < IN; j += 32) xs[warp][j] = (float)s[j] / 256.0f;
   __syncwarp();
   for (int u = lane; u < H; u += 32) {
     float acc = b1[u];
@@ -338,7 +343,12 @@ int net_build(Net &net, const bcts_config &cfg, std::string &err) {
   const float *w = cfg.weights;
   if (cfg.net == BCTS_NET_MLP2_F32) {
     const int I = cfg.mlp_in, H = cfg.mlp_hidden;
-    if (I != 64 || H < 1 || H > 1024) { err = "MLP2 needs mlp_in == 64 and 1 <= mlp_hidden <= 1024"; return -1; }
+    const int want_in = cfg.env == BCTS_ENV_DNN ? kDnnS : 64;
+    if (I != want_in || H < 1 || H > 1024) {
+      err = "MLP2 needs mlp_in == 64 (INT_HASH) / 100 (DNN) and 1 <= mlp_hidden <= 1024";
+      return -1;
+    }
+    net.feat_f32 = cfg.env == BCTS_ENV_DNN;
     const int64_t need = (int64_t)H * I + H + (int64_t)A * H + A;
     if (cfg.weights_count != need) { err = "weights_count mismatch for MLP2"; return -1; }
     void *p[4];
@@ -696,7 +706,8 @@ int net_eval(Net &net, const NodeView &v, int64_t n, int mode, float gd, float *
   if (net.kind == BCTS_NET_MLP2_F32) {
     if (net.prof) net.prof->begin(KC_MLP, 2.0 * (double)n * ((double)net.in * net.hid + (double)net.hid * A), st);
     k_mlp<<<(unsigned)((n + kMlpWarps - 1) / kMlpWarps), 32 * kMlpWarps, 0, st>>>(
-        v.state, v.state_stride, net.l1w, net.l1b, net.l2w, net.l2b, net.in, net.hid, A, n, mode, gd, v.cum, out);
+        v.state, v.state_stride, net.l1w, net.l1b, net.l2w, net.l2b, net.in, net.hid, A, n, mode, gd, v.cum, out,
+        net.feat_f32);
     if (net.prof) net.prof->end(st);
     return 1;
   }

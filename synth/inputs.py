@@ -21,7 +21,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 __all__ = [
-    "MASK64", "mix64", "ENV_TABULAR", "ENV_INT_HASH", "ENV_ATARI_HASH",
+    "MASK64", "mix64", "ENV_TABULAR", "ENV_INT_HASH", "ENV_ATARI_HASH", "ENV_DNN", "DNN_STATE",
+    "dnn_roots", "make_env_weights",
     "NET_TABLE", "NET_MLP2_F32", "NET_NATURE_BF16", "NET_RAINBOW_BF16",
     "ATARI_WORDS", "ATARI_RECORD_BYTES", "INT_RECORD_BYTES",
     "atari_roots", "int_roots", "tabular_roots", "weight_specs", "make_weights",
@@ -29,7 +30,8 @@ __all__ = [
 ]
 
 MASK64 = (1 << 64) - 1
-ENV_TABULAR, ENV_INT_HASH, ENV_ATARI_HASH = 1, 2, 3
+ENV_TABULAR, ENV_INT_HASH, ENV_ATARI_HASH, ENV_DNN = 1, 2, 3, 4
+DNN_STATE = 100
 NET_TABLE, NET_MLP2_F32, NET_NATURE_BF16, NET_RAINBOW_BF16 = 1, 2, 3, 4
 
 ATARI_H = ATARI_W = 84
@@ -82,6 +84,15 @@ def int_roots(n: int, seed: int) -> np.ndarray:
     return (h & np.uint64(0xFFFFFFFF)).astype(np.uint32)
 
 
+def dnn_roots(n: int, seed: int) -> np.ndarray:
+    """n DNN-env root states, float32 [n, 100]: uniform in [-1, 1) from mix64(seed ^ mix64((r<<8)|j))."""
+    r = np.arange(n, dtype=np.uint64)[:, None]
+    j = np.arange(DNN_STATE, dtype=np.uint64)[None, :]
+    h = mix64(np.uint64(seed & MASK64) ^ mix64((r << np.uint64(8)) | j))
+    u = (h >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
+    return (2.0 * u - 1.0).astype(np.float32)
+
+
 def tabular_roots(ids) -> np.ndarray:
     return np.asarray(ids, dtype=np.int32)
 
@@ -104,6 +115,30 @@ def weight_specs(net: int, A: int, mlp_in: int = 64, mlp_hidden: int = 256, atom
                         ("fc_z_v.w", (atoms, 512), 512), ("fc_z_v.b", (atoms,), 512),
                         ("fc_z_a.w", (A * atoms, 512), 512), ("fc_z_a.b", (A * atoms,), 512)]
     raise ValueError(f"no weights for net kind {net}")
+
+
+def env_weight_specs(A: int):
+    """Random-DNN forward model: 3 hidden layers of width 100 over [state(100); onehot(a)],
+    linear output 101 = (next state, reward) (R27)."""
+    S = DNN_STATE
+    return [("g1.w", (S, S + A), S + A), ("g1.b", (S,), S + A), ("g2.w", (S, S), S), ("g2.b", (S,), S),
+            ("g3.w", (S, S), S), ("g3.b", (S,), S), ("g4.w", (S + 1, S), S), ("g4.b", (S + 1,), S)]
+
+
+def _blob(specs, wseed, scale_first=None):
+    parts = []
+    for t, (name, shape, fan_in) in enumerate(specs):
+        cnt = int(np.prod(shape))
+        e = np.arange(cnt, dtype=np.uint64)
+        h = mix64(np.uint64(wseed & MASK64) ^ mix64((np.uint64(t) << np.uint64(40)) | e))
+        u = (h >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
+        parts.append(((2.0 * u - 1.0) / math.sqrt(fan_in)).astype(np.float32))
+    return np.concatenate(parts)
+
+
+def make_env_weights(cfg) -> np.ndarray:
+    """Canonical fp32 blob of the random-DNN forward model (same element recipe as make_weights)."""
+    return _blob(env_weight_specs(cfg.A), cfg.extra.get("env_wseed", cfg.wseed + 7))
 
 
 def make_weights(net: int, A: int, wseed: int, **kw) -> tuple[np.ndarray, dict]:
@@ -206,12 +241,18 @@ class Config:
             return atari_roots(n, self.seed)
         if self.env == ENV_INT_HASH:
             return int_roots(n, self.seed)
+        if self.env == ENV_DNN:
+            return dnn_roots(n, self.seed)
         return tabular_roots([0] * n)
+
+    def net_kw(self) -> dict:
+        """Net shape arguments beyond the defaults (the DNN env's MLP reads 100 float features)."""
+        return {"mlp_in": DNN_STATE} if self.env == ENV_DNN else {}
 
     def weights(self):
         if self.net == NET_TABLE:
             return None, {}
-        return make_weights(self.net, self.A, self.wseed)
+        return make_weights(self.net, self.A, self.wseed, **self.net_kw())
 
 
 CONFIGS = {
@@ -225,6 +266,12 @@ CONFIGS = {
                  correction=(1,), note="Rainbow A=6 bf16, d=5, 1024 roots"),
     "C5": Config("C5", ENV_ATARI_HASH, NET_RAINBOW_BF16, 18, 4, 1, 0.99, 1.0, seed=5, wseed=105,
                  correction=(1,), note="Rainbow A=18 bf16, d=4, 1 root (headline)"),
+    # NEXT-1: the paper's second runtime workload, a random DNN as learned forward model,
+    # Fig. 4 right: A in {2, 10}; leaf value = MLP2 100-256-A fp32
+    "D2": Config("D2", ENV_DNN, NET_MLP2_F32, 2, 8, 64, 0.99, 1.0, seed=21, wseed=121,
+                 note="random-DNN forward model, A=2"),
+    "D10": Config("D10", ENV_DNN, NET_MLP2_F32, 10, 4, 64, 0.99, 1.0, seed=22, wseed=122,
+                  note="random-DNN forward model, A=10"),
 }
 
 

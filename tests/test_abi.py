@@ -37,24 +37,35 @@ def test_exports_every_declared_symbol(L):
     lib = L.lib()
     for s in syms:
         assert hasattr(lib, s)
-    assert lib.bcts_abi_version() == 1
+    ver = int(re.search(r"#define BCTS_ABI_VERSION (\d+)", open(os.path.join(ROOT, "include", "bcts.h")).read())[1])
+    assert lib.bcts_abi_version() == ver == L.bcts.ABI_VERSION
+
+
+@pytest.mark.parametrize("struct", ["Config", "Stats", "KernelProfile"])
+def test_ctypes_structs_match_c_layout(L, struct, tmp_path):
+    """The binding's ctypes mirrors of bcts_config / bcts_stats / bcts_kernel_profile have the C
+    compiler's size and field offsets (gcc on include/bcts.h)."""
+    import ctypes
+    import subprocess
+    cname = {"Config": "bcts_config", "Stats": "bcts_stats", "KernelProfile": "bcts_kernel_profile"}[struct]
+    py = getattr(L.bcts, struct)
+    lines = [f'printf("size %zu\\n", sizeof({cname}));']
+    lines += [f'printf("{f} %zu\\n", offsetof({cname}, {f}));' for f, _ in py._fields_]
+    src = tmp_path / "layout.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "bcts.h"\nint main(void) {\n'
+                   + "\n".join(lines) + "\nreturn 0; }\n")
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = dict(l.split() for l in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split("\n") if l)
+    assert int(got["size"]) == ctypes.sizeof(py)
+    for f, _ in py._fields_:
+        assert int(got[f]) == getattr(py, f).offset, f
 
 
 def test_status_strings(L):
     lib = L.lib()
     assert lib.bcts_status_string(0) == b"BCTS_OK"
     assert lib.bcts_status_string(4) == b"BCTS_ERR_BUDGET"
-
-
-def test_config_struct_layout(L):
-    """ctypes mirror of bcts_config has the C layout (natural alignment, 8-byte pointers)."""
-    C = L.bcts.Config
-    offs = {n: getattr(C, n).offset for n, _ in C._fields_}
-    assert offs["cuda_stream"] == 8 and offs["env"] == 16 and offs["tab_next"] == 32
-    assert offs["net"] == 56 and offs["weights"] == 64 and offs["weights_count"] == 72
-    assert offs["workspace_bytes_max"] == 104 and offs["flags"] == 112
-    import ctypes
-    assert ctypes.sizeof(C) == 120
 
 
 def f32(x):
@@ -98,11 +109,16 @@ def test_create_rejects_bad_config_without_gpu(L):
     h = ctypes.c_void_p()
     cfg.abi_version = 99
     assert lib.bcts_create(ctypes.byref(cfg), ctypes.byref(h)) == 1
-    cfg.abi_version = 1
+    cfg.abi_version = L.bcts.ABI_VERSION
     cfg.num_actions = 1                                        # A >= 2
     assert lib.bcts_create(ctypes.byref(cfg), ctypes.byref(h)) == 1
     cfg.num_actions, cfg.env, cfg.net = 4, 2, 1                # INT_HASH + TABLE: unsupported pair
     assert lib.bcts_create(ctypes.byref(cfg), ctypes.byref(h)) == 2
+    cfg.env, cfg.net, cfg.mlp_in, cfg.mlp_hidden = 4, 2, 100, 256   # DNN without env weights
+    assert lib.bcts_create(ctypes.byref(cfg), ctypes.byref(h)) == 1
+    ew = np.zeros(40501 + 100 * 4 - 1, np.float32)                # one float short
+    cfg.env_weights, cfg.env_weights_count = ew.ctypes.data, ew.size
+    assert lib.bcts_create(ctypes.byref(cfg), ctypes.byref(h)) == 1
     assert not h.value
     assert lib.bcts_search(None, None, 0, 1, 2, 0.9, 1.0, 1, None, None) == 1
 

@@ -317,7 +317,7 @@ def test_errors_leave_outputs_untouched():
     for gamma in (0.0, 1.0, float("nan")):
         assert P.lib().bcts_search(h._h, P.bcts._p(roots), 2, 2, 4, gamma, 1.0, 1, P.bcts._p(act), P.bcts._p(q)) == 1
     assert P.lib().bcts_search(h._h, P.bcts._p(roots), 2, 2, 4, 0.9, -1.0, 1, P.bcts._p(act), P.bcts._p(q)) == 1
-    assert P.lib().bcts_search(h._h, P.bcts._p(roots), 2, 2, 4, 0.9, 1.0, 2, P.bcts._p(act), P.bcts._p(q)) == 1
+    assert P.lib().bcts_search(h._h, P.bcts._p(roots), 2, 2, 4, 0.9, 1.0, 3, P.bcts._p(act), P.bcts._p(q)) == 1
     assert P.lib().bcts_search(h._h, P.bcts._p(roots), 0, 2, 4, 0.9, 1.0, 1, None, None) == 0
     torch.cuda.synchronize()
     assert (act.cpu() == -7).all() and (q.cpu() == 3.5).all()
@@ -339,3 +339,71 @@ def test_e2e_host_matches_device():
     h.search_host(pin, 2, 2, cfg.gamma, 1.0, 1, act, q)
     np.testing.assert_array_equal(act.numpy(), g["actions"])
     np.testing.assert_array_equal(q.numpy(), g["root_q"])
+
+
+@pytest.mark.parametrize("cname,n,d", [("C2", 16, 3), ("C5", 2, 2)])
+def test_exact_bias_correction(cname, n, d):
+    """correction_on = 2: Lemma 2's exact gap (App. A.2) instead of Eq. 5 -- GPU (normcdfinv) vs oracle."""
+    cfg = config(cname)
+    h = handle(cname)
+    o = Oracle.from_config(cfg)
+    roots = cfg.roots(n)
+    g = run(h, roots, d, cfg.gamma, 1.0, 2)
+    r = o.search(roots, d, float(np.float32(cfg.gamma)), 1.0, 2, mode=0, threads=THREADS)
+    tol = RTOL_F32 if cname == "C2" else RTOL_BF16
+    assert rel_err(g["root_q"], r["root_q"]).max() <= tol
+    np.testing.assert_array_equal(g["terms"][:, 0], r["terms"][:, 0])
+    assert (np.abs(g["terms"][:, 3] - r["terms"][:, 3]) <= tol * np.maximum(1.0, np.abs(r["terms"][:, 3]))).all()
+    frac, _, _ = action_agreement(g["actions"], r["root_q"], tol)
+    assert frac == 1.0
+
+
+# ------------------------------------------------- NEXT-1: random-DNN forward model
+def dnn_cfg(name):
+    """D2 / D10 (synth CONFIGS) and D3: A = 3, so 64-child tiles split sibling groups."""
+    import dataclasses
+    if name == "D3":
+        return dataclasses.replace(config("D10"), name="D3", A=3, seed=23, wseed=123)
+    return config(name)
+
+
+@pytest.mark.parametrize("cname,n,levels", [("D2", 5, 7), ("D3", 3, 4), ("D10", 2, 2)])
+def test_dnn_level_states_bit_exact(cname, n, levels):
+    """k_expand_dnn: every node's 100 fp32 state values and R bit-exact vs the oracle's fp32 mirror
+    (ragged 64-child tiles, sibling groups split across tiles for A = 3)."""
+    cfg = dnn_cfg(cname)
+    h = handle(cfg)
+    o = Oracle.from_config(cfg)
+    roots = cfg.roots(n)
+    g = float(np.float32(cfg.gamma))
+    for level in range(levels + 1):
+        st, cum = h.expand(dev(roots), n, level, np.float32(cfg.gamma))
+        st, cum = st.cpu().numpy(), cum.cpu().numpy()
+        per = cfg.A ** level
+        idx = range(n * per) if n * per <= 700 else np.random.default_rng(level).choice(n * per, 700, replace=False)
+        for j in idx:
+            r, i = divmod(int(j), per)
+            rec, R = o.node(roots[r], level, i, g, mode=1)
+            assert st[j].tobytes() == rec.tobytes(), (level, r, i)
+            assert cum[j] == np.float32(R), (level, r, i)
+
+
+@pytest.mark.parametrize("cname,n,d", [("D2", 64, 8), ("D3", 7, 5), ("D10", 16, 4), ("D10", 3, 1)])
+@pytest.mark.parametrize("corr", [0, 1, 2])
+def test_dnn_search_vs_oracle(cname, n, d, corr):
+    """Search on the DNN forward model + MLP2 100-256-A leaf net, fp32: vanilla Q and best leaf
+    bit-exact vs the fp32 mirror; root Q within 1e-5 of the fp64 oracle; actions equal."""
+    cfg = dnn_cfg(cname)
+    h = handle(cfg)
+    o = Oracle.from_config(cfg)
+    roots = cfg.roots(n)
+    gamma = float(np.float32(cfg.gamma))
+    gr = run(h, roots, d, cfg.gamma, 1.0, corr)
+    m = o.search(roots, d, gamma, 1.0, corr, mode=1, threads=THREADS)
+    r = o.search(roots, d, gamma, 1.0, corr, mode=0, threads=THREADS)
+    np.testing.assert_array_equal(gr["vanilla_q"], m["vanilla_q"].astype(np.float32))
+    np.testing.assert_array_equal(gr["best_leaf"], m["best_leaf"])
+    assert rel_err(gr["root_q"], r["root_q"]).max() <= RTOL_F32
+    frac, _, _ = action_agreement(gr["actions"], r["root_q"], RTOL_F32)
+    assert frac == 1.0
+    assert gr["stats"]["leaves"] == n * cfg.A ** d

@@ -415,3 +415,139 @@ def test_env_golden_vectors_frozen():
             for a, h, rw in zip(s["actions"], s["sha256"], s["rewards"]):
                 rec, r = o.step(rec, a)
                 assert hashlib.sha256(rec.tobytes()).hexdigest() == h and r == rw
+
+
+# ------------------------------------------------------------ NEXT-2: Lemma 2 exact biases
+def test_inv_norm_cdf_vs_scipy_and_roundtrip():
+    """Phi^-1 (App. A.1) against scipy.stats.norm.ppf and Phi(Phi^-1(p)) = p via math.erfc."""
+    from scipy.stats import norm
+    from oracle import inv_norm_cdf
+    rng = np.random.default_rng(8)
+    ps = np.concatenate([rng.uniform(1e-12, 1 - 1e-12, 2000), [0.5, 0.975, 1e-10, 1 - 1e-10, 0.02425, 0.97575]])
+    for p in ps:
+        z = inv_norm_cdf(p)
+        assert abs(z - norm.ppf(p)) <= 1e-9 * max(1.0, abs(z))
+        assert abs(0.5 * math.erfc(-z / math.sqrt(2)) - p) <= 1e-12 * max(p, 1e-3)
+    assert abs(inv_norm_cdf(0.975) - 1.959964) < 1e-6          # S:279 example
+    assert inv_norm_cdf(0.5) == 0.0 or abs(inv_norm_cdf(0.5)) < 1e-15
+
+
+def test_lemma2_special_cases_and_ordering():
+    """B_o = 0 at d=1; B_e = 0 at d=1, A=2; 0 <= B_o < B_e for sigma_o < sigma_e (Lemma 2)."""
+    from oracle import B_n, bias_exact
+    assert B_n(1) == 0.0
+    for A in (2, 3, 4, 6, 18):
+        assert bias_exact(1.0, 0.0, A, 1) == 0.0                   # B_o(d=1) = 0 -> gap = -B_o = 0 at sigma_e = 0
+    assert bias_exact(0.3, 2.0, 2, 1) == 0.0                       # both single-element maxima at d=1, A=2
+    for A in (2, 3, 4, 18):
+        for d in range(1, 9):
+            n_o, n_e = A ** (d - 1), A ** d - A ** (d - 1)
+            bo, be = 0.7 * B_n(n_o), 1.3 * B_n(n_e)
+            assert 0.0 <= bo < be or (A == 2 and d == 1)
+    # B(n) is increasing (it is composed of two increasing functions, P:612)
+    vals = [B_n(n) for n in (2, 3, 10, 100, 1e4, 1e6)]
+    assert all(x < y for x, y in zip(vals, vals[1:]))
+
+
+def test_lemma2_vs_library_formula_and_eq4_gap():
+    """Exact gap via scipy's ppf in the App. A.2 formula; the Eq. 4 approximation's relative error at
+    A=3, sigma_o=1, sigma_e=4 (App. A.6 setup) shrinks with d (+113%, +24%, +13%, +8%)."""
+    from scipy.stats import norm
+    from oracle import bias_exact, bias_gap_eq4
+    gem = 0.5772156649015329
+
+    def Bn(n):
+        return 0.0 if n == 1 else gem * norm.ppf(1 - 1 / (math.e * n)) + (1 - gem) * norm.ppf(1 - 1 / n)
+
+    for A in (2, 3, 18):
+        for d in (1, 2, 3, 4, 5):
+            ref = 4.0 * Bn(A ** d - A ** (d - 1)) - 1.0 * Bn(A ** (d - 1))
+            assert abs(bias_exact(1.0, 4.0, A, d) - ref) <= 1e-9 * max(1.0, abs(ref))
+    errs = [bias_gap_eq4(1, 4, 3, d) / bias_exact(1, 4, 3, d) - 1 for d in range(1, 7)]
+    np.testing.assert_allclose(errs[:4], [1.13, 0.24, 0.13, 0.08], atol=0.01)
+    assert all(a > b > 0 for a, b in zip(errs, errs[1:]))
+
+
+def test_exact_bias_worked_examples():
+    """W1: exact gap 0 (d=1, A=2); W2: 0.3675 -> BCTS-exact keeps vanilla's choice."""
+    o = tab_oracle(worked_w1())
+    r = o.search(ROOT0, 1, 0.5, 1.0, 2)
+    assert r["terms"][0, 3] == 0.0
+    np.testing.assert_array_equal(r["root_q"], r["vanilla_q"])
+    o2 = tab_oracle(worked_w2())
+    r2 = o2.search(ROOT0, 2, 0.5, 1.0, 2)
+    assert abs(r2["terms"][0, 3] - 0.3675225) < 1e-6
+    np.testing.assert_allclose(r2["root_q"][0], [1.25, 2.0 - 0.25 * 0.3675225285], atol=1e-9)
+
+
+# ------------------------------------------------------------ NEXT-1: random-DNN forward model
+def _dnn_torch(cfg):
+    """The paper's DNN forward model as a stock torch.nn stack in fp64: three hidden
+    layers of width 100 over [state(100); onehot(a)], ReLU, linear head 101 = (next state, reward)."""
+    import torch
+    from synth.inputs import make_env_weights, env_weight_specs
+    blob = make_env_weights(cfg).astype(np.float64)
+    specs = env_weight_specs(cfg.A)
+    off, ts = 0, []
+    for _, shape, _ in specs:
+        n = int(np.prod(shape))
+        ts.append(torch.from_numpy(blob[off:off + n].reshape(shape)))
+        off += n
+    layers = []
+    for L in range(4):
+        lin = torch.nn.Linear(ts[2 * L].shape[1], ts[2 * L].shape[0]).double()
+        with torch.no_grad():
+            lin.weight.copy_(ts[2 * L])
+            lin.bias.copy_(ts[2 * L + 1])
+        layers += [lin, torch.nn.ReLU()] if L < 3 else [lin]
+    return torch.nn.Sequential(*layers)
+
+
+@pytest.mark.parametrize("cname", ["D2", "D10"])
+def test_dnn_step_matches_torch_sequential(cname):
+    import torch
+    cfg = config(cname)
+    o = Oracle.from_config(cfg)
+    net = _dnn_torch(cfg)
+    roots = cfg.roots(5)
+    for r in range(5):
+        for a in range(cfg.A):
+            x = torch.cat([torch.from_numpy(roots[r].astype(np.float64)),
+                           torch.nn.functional.one_hot(torch.tensor(a), cfg.A).double()])
+            ref = net(x).detach().numpy()
+            rec, rew = o.step(roots[r], a)                  # fp32 mirror
+            np.testing.assert_allclose(rec.view(np.float32), ref[:100], rtol=0, atol=2e-6)
+            assert abs(rew - ref[100]) <= 2e-6
+            rec0, R0 = o.node(roots[r], 1, a, cfg.gamma, mode=0)   # fp64 chain, state rounded to fp32
+            np.testing.assert_allclose(rec0.view(np.float32), ref[:100].astype(np.float32), rtol=1e-6, atol=1e-7)
+            assert abs(R0 - ref[100]) <= 1e-12
+
+
+def test_dnn_mlp_leaf_value_matches_torch():
+    """Leaf value Q-hat on the DNN env: MLP2 100-256-A over the raw fp32 state features (R27)."""
+    import torch
+    cfg = config("D10")
+    o = Oracle.from_config(cfg)
+    _, v = cfg.weights()
+    s = cfg.roots(3)
+    x = torch.from_numpy(s.astype(np.float64))
+    h = torch.relu(x @ torch.from_numpy(v["l1.w"].astype(np.float64)).T + torch.from_numpy(v["l1.b"].astype(np.float64)))
+    q = (h @ torch.from_numpy(v["l2.w"].astype(np.float64)).T + torch.from_numpy(v["l2.b"].astype(np.float64))).numpy()
+    for r in range(3):
+        np.testing.assert_allclose(o.qrow(s[r], mode=0), q[r], rtol=0, atol=1e-12)
+        np.testing.assert_allclose(o.qrow(s[r], mode=1), q[r], rtol=0, atol=5e-6)
+
+
+@pytest.mark.parametrize("cname,d", [("D2", 5), ("D10", 2)])
+def test_dnn_bruteforce_equals_dfs_and_mirror_close(cname, d):
+    cfg = config(cname)
+    o = Oracle.from_config(cfg)
+    roots = cfg.roots(3)
+    for mode in (0, 1):
+        a = o.search(roots, d, cfg.gamma, 1.0, 1, mode=mode, threads=4)
+        b = o.search(roots, d, cfg.gamma, 1.0, 1, mode=mode, brute=True)
+        for k in ("actions", "root_q", "vanilla_q", "best_leaf"):
+            np.testing.assert_array_equal(a[k], b[k])
+    f64 = o.search(roots, d, cfg.gamma, 1.0, 1, mode=0)
+    f32 = o.search(roots, d, cfg.gamma, 1.0, 1, mode=1)
+    assert np.abs(f64["vanilla_q"] - f32["vanilla_q"]).max() < 1e-4
