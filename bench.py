@@ -39,9 +39,18 @@ def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
-                "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]), "source": "measured"}
-    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+        out = {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
+               "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]), "source": "measured",
+               "sm_max_mhz": d.get("sm_max_mhz", 1965.0)}
+    else:
+        out = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback",
+               "sm_max_mhz": 1965.0}
+    # fp32 FMA (ALU) peak, derived: 148 SMs x 4 SMSPs x 32 FFMA lanes x 2 FLOP x max SM clock
+    out["fp32_tflops"] = 148 * 128 * 2 * out["sm_max_mhz"] * 1e6 / 1e12
+    return out
+
+
+FP32_CLASSES = {"mlp", "expand_dnn"}      # fixed-order fmaf kernels: ALU-bound, fp32 peak
 
 
 class ClockSampler:
@@ -111,6 +120,26 @@ def dist_setup(args):
     return world, rank, local
 
 
+def metric_of(cfg):
+    if (cfg.A, cfg.depth) == (18, 4):
+        return METRIC
+    return f"tree nodes expanded+evaluated/sec and root decisions/sec at depth {cfg.depth}, A={cfg.A}"
+
+
+def dtype_of(cfg):
+    return "bf16" if cfg.net in (3, 4) else "f32"
+
+
+def workload_of(cfg, n):
+    base = f"{cfg.name}: Batch-BFS+BCTS, A={cfg.A}, depth={cfg.depth}, {n} root(s), "
+    if cfg.net in (3, 4):
+        return base + f"{'Rainbow' if cfg.net == 4 else 'Nature'}-shaped bf16 Q-net (random init), correction on"
+    if cfg.env == 4:
+        return base + ("random-DNN forward model (3x100 hidden, P:340-341) + MLP2 100-256-A fp32 leaf net "
+                       "(random init), correction on")
+    return base + "hash env + MLP2/table leaf values, correction on"
+
+
 # ------------------------------------------------------------------ CPU oracle leg
 def oracle_sample(cfg, seconds_target=12.0, threads=None):
     """Time the oracle (as it stands) on a bounded sample of the same workload:
@@ -121,6 +150,20 @@ def oracle_sample(cfg, seconds_target=12.0, threads=None):
     root = cfg.roots(1)
     A, d = cfg.A, cfg.depth
     exp, ev = nodes_per_root(A, d, 1)
+    if d < 2 or exp + ev <= 200_000:
+        # small trees: whole searches of batches of roots (one root per thread)
+        roots = cfg.roots(max(threads, 1))
+        done, elapsed = 0, 0.0
+        while elapsed < seconds_target and done < 256 * threads:
+            t = time.perf_counter()
+            o.search(roots, d, cfg.gamma, cfg.beta, 1, mode=0, threads=threads)
+            elapsed += time.perf_counter() - t
+            done += roots.shape[0]
+        nodes = (exp + ev) * done
+        return {"value": nodes / elapsed, "unit": "nodes/s", "cores": threads, "kind": "oracle",
+                "decisions_per_s": done / elapsed,
+                "sample": f"{done} whole depth-{d} searches ({cfg.name}: A={A}), plain-C DFS, {threads} threads, "
+                          f"{elapsed:.1f} s"}
     per_task_nodes = (exp + A ** d) / (A * A)      # subtree share of the tree's expansions + leaf evaluations
     done_tasks, elapsed, t0 = 0, 0.0, 0
     wave = threads
@@ -158,12 +201,12 @@ def run_reference(args, cfg, world, rank):
             times.append(dt)
     step = sum(times) / len(times)
     value = per_task * ntask / step
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "nodes/s", "n_gpus": args.gpus,
+    line = {"impl": "reference", "metric": metric_of(cfg), "value": value, "unit": "nodes/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "decisions_per_s": value / (exp + ev),
-            "config": {"workload": f"{cfg.name}: Batch-BFS+BCTS, A={A}, depth={d}, {cfg.n_roots} root(s), "
-                                   f"Rainbow-shaped Q-net; each step = {ntask} depth-2 subtrees (bounded sample)",
+            "decisions_per_s": value / (exp + ev), "metric_note": metric_of(cfg),
+            "config": {"workload": workload_of(cfg, cfg.n_roots) + f"; each step = {ntask} depth-2 subtrees "
+                                   "(bounded sample)",
                        "roots": cfg.n_roots, "depth": d, "A": A},
             "cpu_baseline": {"value": value, "unit": "nodes/s", "cores": threads, "kind": "oracle",
                              "sample": f"{ntask} of {A * A} depth-2 subtrees per step, plain-C DFS (fp64, bf16-emulated net)"},
@@ -281,16 +324,18 @@ def main():
         long_run = step_ms * args.steps > 1000.0
         if v["unit"] == "byte":
             peak, unit, bound = peaks["hbm_gbs"], "GB/s", "hbm"
+            psrc = peaks["source"] + " burst"
+        elif args.simt or name in FP32_CLASSES:
+            peak, unit, bound = peaks["fp32_tflops"], "TFLOP/s", "alu"
+            psrc = f"derived: 148 SMs x 128 FP32 FMA lanes x 2 x {peaks['sm_max_mhz']:.0f} MHz"
         else:
             peak = peaks["bf16_tflops_sustained"] if long_run else peaks["bf16_tflops"]
             unit, bound = "TFLOP/s", "tensor"
-            if args.simt:
-                bound = "alu"
+            psrc = peaks["source"] + (" sustained" if long_run else " burst")
         ach = kernels[name]["achieved"]
         roofline = {"kernel": name, "bound": bound, "achieved": ach, "peak": peak, "unit": unit,
                     "frac": ach / peak, "traffic": None,
-                    "work_per_launch": v["work"] / max(v["launches"], 1),
-                    "peak_source": peaks["source"] + (" sustained" if long_run and bound == "tensor" else " burst")}
+                    "work_per_launch": v["work"] / max(v["launches"], 1), "peak_source": psrc}
         tr = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tr):
             tj = json.load(open(tr))
@@ -336,13 +381,11 @@ def main():
         cpu = oracle_sample(cfg)
 
     if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": "nodes/s", "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        line = {"metric": metric_of(cfg), "value": value, "unit": "nodes/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": dtype_of(cfg), "data": "synthetic",
                 "decisions_per_s": n / (step_ms / 1e3),
-                "config": {"workload": f"{cfg.name}: Batch-BFS+BCTS, A={A}, depth={d}, {n} root(s), "
-                                       f"{'Rainbow' if cfg.net == 4 else 'Nature' if cfg.net == 3 else 'other'}"
-                                       f"-shaped bf16 Q-net (random init), correction on",
+                "config": {"workload": workload_of(cfg, n),
                            "roots": n, "depth": d, "A": A, "nodes_per_decision": exp + ev,
                            "parallelism": f"leaf-range shards x{world}" if world > 1 else "single GPU",
                            "l2": "flushed before every timed step (256 MiB write, untimed)" if flush is not None

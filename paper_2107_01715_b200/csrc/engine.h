@@ -87,6 +87,12 @@ void dnn_repack(const float *blob, int A, float *out);
 
 void launch_expand(int env, const NodeView &par, int64_t p_first, int64_t c_begin, int64_t c_end, int A,
                    float gk, const EnvModel &em, const NodeOut &out, cudaStream_t st, Profiler *prof = nullptr);
+// ffma_tiles.cu: fixed-order fp32 FMA kernels (DNN forward model, tiled MLP2)
+void launch_expand_dnn(const NodeView &par, int64_t p_first, int64_t c_begin, int64_t c_end, int A, float gk,
+                       const float *img, const NodeOut &out, cudaStream_t st, Profiler *prof);
+int mlp_image_floats(int I, int H, int A);
+void mlp_repack(const float *w1, const float *b1, const float *w2, const float *b2, int I, int H, int A, float *out);
+bool mlp_tiled_ok(int I, int H, int A);
 
 // s2d bf16 frames for the conv1 tensor-core layer (expand.cu)
 // planar != 0: write the chunk-planar layout (plane = bytes per 8-channel plane,
@@ -163,6 +169,9 @@ constexpr uint32_t kPlane3 = 152 * 16, kIn3Bytes = 8 * kPlane3;      // act2: 9x
 // Net output modes.
 enum { MODE_ROWS = 0, MODE_ROWMAX = 1, MODE_TOTAL = 2 };
 
+void launch_mlp_tiled(const NodeView &v, int64_t n, const float *img, int I, int H, int A, int mode, float gd,
+                      float *out, int feat_f32, cudaStream_t st);
+
 struct Net {
   int kind = 0, A = 0;
   // TABLE
@@ -172,6 +181,7 @@ struct Net {
   const float *l1w = nullptr, *l1b = nullptr, *l2w = nullptr, *l2b = nullptr;
   int in = 0, hid = 0;
   int feat_f32 = 0;               // DNN env: features are the fp32 state itself
+  const float *mlp_img = nullptr; // tiled-MLP smem image (mlp_repack), null = warp-per-state kernel
   // conv nets
   Layer c1, c2, c3, fc_h, z_v, z_a, fc2;
   int atoms = 51;

@@ -143,196 +143,13 @@ __global__ void __launch_bounds__(kExpandThreads) k_expand_atari(NodeView par, i
   }
 }
 
-// -------------------------------------------------------------------- DNN
-// Random-DNN learned forward model of the runtime study (DESIGN.md
-// R27): x = [s(100); onehot(a)] -> 3 x (Linear 100 + ReLU) -> Linear 101 =
-// (s', r). fp32; every output is ONE fmaf chain from the bias over the inputs
-// in index order -- the oracle's fp32 mirror, bit for bit. Sibling sharing:
-// the state part of layer 1, pre[u] = chain over s only, is computed once per
-// parent; child a then finishes the chain with the one-hot tail, where
-// fmaf(w, 0, acc) = acc and fmaf(w, 1, acc) = acc + w (a signed zero can
-// differ, and ReLU maps both zeros to +0).
-//
-// Persistent CTAs (one per SM, 1 CTA/SM at 214 KB smem): the 163 KB
-// transposed weight image lands in shared memory with ONE bulk copy, then each
-// CTA loops over tiles of 64 children. A thread owns a 4-unit x 8-child
-// register tile: per input i it reads one float4 of weights (WT[i][4u..4u+3])
-// and two float4 of activations (X[i][8c..8c+7]) for 32 FMAs.
-constexpr int kDnnTile = 64, kDnnThreads = 256;
-constexpr int kDnnOff2 = 10000, kDnnOff3 = 20000, kDnnOff4 = 30000, kDnnOffB = 40400;
-constexpr size_t kDnnSmem = (size_t)kDnnImg * 4 + 2 * (size_t)kDnnS * kDnnTile * 4;
-
-int64_t dnn_env_weights_count(int A) { return 40501 + 100LL * A; }
-
-void dnn_repack(const float *blob, int A, float *out) {
-  const int S = kDnnS, I1 = S + A;
-  const float *g1w = blob, *g1b = g1w + S * I1, *g2w = g1b + S, *g2b = g2w + S * S, *g3w = g2b + S,
-              *g3b = g3w + S * S, *g4w = g3b + S, *g4b = g4w + (S + 1) * S;
-  memset(out, 0, ((size_t)kDnnImg + (size_t)S * A) * 4);
-  for (int u = 0; u < S; ++u)
-    for (int i = 0; i < S; ++i) {
-      out[i * S + u] = g1w[u * I1 + i];
-      out[kDnnOff2 + i * S + u] = g2w[u * S + i];
-      out[kDnnOff3 + i * S + u] = g3w[u * S + i];
-    }
-  for (int u = 0; u <= S; ++u)
-    for (int i = 0; i < S; ++i) out[kDnnOff4 + i * 104 + u] = g4w[u * S + i];
-  for (int u = 0; u < S; ++u) {
-    out[kDnnOffB + u] = g1b[u];
-    out[kDnnOffB + 100 + u] = g2b[u];
-    out[kDnnOffB + 200 + u] = g3b[u];
-  }
-  for (int u = 0; u <= S; ++u) out[kDnnOffB + 300 + u] = g4b[u];
-  for (int a = 0; a < A; ++a)
-    for (int u = 0; u < S; ++u) out[kDnnImg + a * S + u] = g1w[u * I1 + S + a];
-}
-
-// acc[c][j] = chain_i fmaf(WT[i][4ug + j], X[i][8cg + c], b[4ug + j]) over i in [0, nin)
-__device__ __forceinline__ void dnn_tile(const float *__restrict__ WT, int ldw, const float *__restrict__ b,
-                                         const float *__restrict__ X, int nin, int ug, int cg, float (&acc)[8][4]) {
-  const float4 bb = *(const float4 *)(b + 4 * ug);
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    acc[c][0] = bb.x; acc[c][1] = bb.y; acc[c][2] = bb.z; acc[c][3] = bb.w;
-  }
-#pragma unroll 4
-  for (int i = 0; i < nin; ++i) {
-    const float4 w = *(const float4 *)(WT + i * ldw + 4 * ug);
-    const float4 x0 = *(const float4 *)(X + i * kDnnTile + 8 * cg);
-    const float4 x1 = *(const float4 *)(X + i * kDnnTile + 8 * cg + 4);
-    const float xs[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      acc[c][0] = fmaf(w.x, xs[c], acc[c][0]);
-      acc[c][1] = fmaf(w.y, xs[c], acc[c][1]);
-      acc[c][2] = fmaf(w.z, xs[c], acc[c][2]);
-      acc[c][3] = fmaf(w.w, xs[c], acc[c][3]);
-    }
-  }
-}
-
-// hidden layer: Y[u][c] = relu(chain) for u < 100, c < 8*n_cg
-__device__ __forceinline__ void dnn_hidden(const float *WT, const float *b, const float *X, float *Y, int n_cg) {
-  for (int task = threadIdx.x; task < 25 * n_cg; task += kDnnThreads) {
-    const int cg = task % n_cg, ug = task / n_cg;
-    float acc[8][4];
-    dnn_tile(WT, kDnnS, b, X, kDnnS, ug, cg, acc);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      float *y = Y + (4 * ug + j) * kDnnTile + 8 * cg;
-      *(float4 *)y = make_float4(fmaxf(acc[0][j], 0.f), fmaxf(acc[1][j], 0.f), fmaxf(acc[2][j], 0.f),
-                                 fmaxf(acc[3][j], 0.f));
-      *(float4 *)(y + 4) = make_float4(fmaxf(acc[4][j], 0.f), fmaxf(acc[5][j], 0.f), fmaxf(acc[6][j], 0.f),
-                                       fmaxf(acc[7][j], 0.f));
-    }
-  }
-}
-
-__global__ void __launch_bounds__(kDnnThreads, 1)
-    k_expand_dnn(NodeView par, int64_t p_first, int64_t c_begin, int64_t c_end, int A, float gk,
-                 const float *__restrict__ img, NodeOut out) {
-  extern __shared__ __align__(128) float dsm[];
-  float *W = dsm, *Bs = dsm + kDnnOffB;
-  float *bufA = dsm + kDnnImg, *bufB = bufA + kDnnS * kDnnTile;
-  __shared__ __align__(8) uint64_t bar;
-  const float *W1A = img + kDnnImg;
-  if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
-    mbar_expect_tx(&bar, kDnnImg * 4);
-    bulk_g2s(dsm, img, kDnnImg * 4, &bar);
-  }
-  __syncthreads();
-  mbar_wait(&bar, 0);
-  const int64_t n = c_end - c_begin, ntiles = (n + kDnnTile - 1) / kDnnTile;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int64_t c0 = c_begin + t * kDnnTile;
-    const int nc = (int)min((int64_t)kDnnTile, c_end - c0);
-    const int64_t p0 = c0 / A;
-    const int np = (int)((c0 + nc - 1) / A - p0 + 1);   // <= 64/A + 2 <= 34
-    // 0: parent states -> bufA[i][p] (columns past np are never read back)
-    for (int e = threadIdx.x; e < np * kDnnS; e += kDnnThreads) {
-      const int p = e / kDnnS, i = e - p * kDnnS;
-      bufA[i * kDnnTile + p] = ((const float *)(par.state + (p0 + p - p_first) * par.state_stride))[i];
-    }
-    __syncthreads();
-    // 1: pre[u][p] = b1[u] + chain over the 100 state inputs, once per parent -> bufB
-    {
-      const int n_cg = (np + 7) / 8;
-      for (int task = threadIdx.x; task < 25 * n_cg; task += kDnnThreads) {
-        const int cg = task % n_cg, ug = task / n_cg;
-        float acc[8][4];
-        dnn_tile(W, kDnnS, Bs, bufA, kDnnS, ug, cg, acc);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          float *y = bufB + (4 * ug + j) * kDnnTile + 8 * cg;
-          *(float4 *)y = make_float4(acc[0][j], acc[1][j], acc[2][j], acc[3][j]);
-          *(float4 *)(y + 4) = make_float4(acc[4][j], acc[5][j], acc[6][j], acc[7][j]);
-        }
-      }
-    }
-    __syncthreads();
-    // 2: h1[u][c] = relu(pre[u][parent(c)] + W1[u][100 + a(c)]) -> bufA (children past nc: zeros)
-    for (int e = threadIdx.x; e < kDnnS * kDnnTile; e += kDnnThreads) {
-      const int u = e / kDnnTile, c = e % kDnnTile;
-      float h = 0.0f;
-      if (c < nc) {
-        const int64_t cc = c0 + c, p = cc / A;
-        const int a = (int)(cc - p * A);
-        h = fmaxf(__fadd_rn(bufB[u * kDnnTile + (int)(p - p0)], __ldg(W1A + a * kDnnS + u)), 0.0f);
-      }
-      bufA[u * kDnnTile + c] = h;
-    }
-    __syncthreads();
-    const int n_cg = (nc + 7) / 8;
-    dnn_hidden(W + kDnnOff2, Bs + 100, bufA, bufB, n_cg);   // 3: layer 2
-    __syncthreads();
-    dnn_hidden(W + kDnnOff3, Bs + 200, bufB, bufA, n_cg);   // 4: layer 3
-    __syncthreads();
-    // 5: layer 4 (101 outputs, no ReLU): s' -> out.state, r -> out.cum
-    for (int task = threadIdx.x; task < 26 * n_cg; task += kDnnThreads) {
-      const int cg = task % n_cg, ug = task / n_cg;
-      float acc[8][4];
-      dnn_tile(W + kDnnOff4, 104, Bs + 300, bufA, kDnnS, ug, cg, acc);
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const int cl = 8 * cg + c;
-        if (cl >= nc) break;
-        const int64_t ci = c0 + cl - c_begin;
-        if (ug < 25) {
-          *(float4 *)((float *)(out.state + ci * out.state_stride) + 4 * ug) =
-              make_float4(acc[c][0], acc[c][1], acc[c][2], acc[c][3]);
-        } else {
-          const int64_t p = (c0 + cl) / A;
-          const float R = par.cum ? par.cum[p - p_first] : 0.0f;
-          out.cum[ci] = fmaf(gk, acc[c][0], R);
-        }
-      }
-    }
-    __syncthreads();   // bufA/bufB reuse by the next tile
-  }
-}
-
 void launch_expand(int env, const NodeView &par, int64_t p_first, int64_t c_begin, int64_t c_end, int A, float gk,
                    const EnvModel &em, const NodeOut &out, cudaStream_t st, Profiler *prof) {
   const int64_t n = c_end - c_begin;
   if (n <= 0) return;
   const int64_t nparents = (c_end - 1) / A - c_begin / A + 1;
   if (env == BCTS_ENV_DNN) {
-    // algorithmic FLOPs: per child 2*(100*100 + 2*100*100 + 101*100) (layers 2-4 + layer-1 tail),
-    // per parent 2*100*100 (the shared state part of layer 1)
-    if (prof) prof->begin(KC_EXPAND_DNN, 2.0 * (30100.0 * (double)n + 10000.0 * (double)nparents), st);
-    static int attr = 0, sms = 0;
-    if (!attr) {
-      cudaFuncSetAttribute(k_expand_dnn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDnnSmem);
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      attr = 1;
-    }
-    const int64_t ntiles = (n + kDnnTile - 1) / kDnnTile;
-    const unsigned grid = (unsigned)std::min<int64_t>(ntiles, sms > 0 ? sms : 148);
-    k_expand_dnn<<<grid, kDnnThreads, kDnnSmem, st>>>(par, p_first, c_begin, c_end, A, gk, em.dnn, out);
-    if (prof) prof->end(st);
+    launch_expand_dnn(par, p_first, c_begin, c_end, A, gk, em.dnn, out, st, prof);
     return;
   }
   // algorithmic bytes: every child node written once + every parent node read once

@@ -360,6 +360,15 @@ int net_build(Net &net, const bcts_config &cfg, std::string &err) {
     net.l1w = (const float *)p[0]; net.l1b = (const float *)p[1];
     net.l2w = (const float *)p[2]; net.l2b = (const float *)p[3];
     net.in = I; net.hid = H;
+    if (mlp_tiled_ok(I, H, A)) {
+      std::vector<float> img((size_t)mlp_image_floats(I, H, A));
+      const float *c = cfg.weights;
+      mlp_repack(c, c + (size_t)H * I, c + (size_t)H * I + H, c + (size_t)H * I + H + (size_t)A * H, I, H, A,
+                 img.data());
+      void *d;
+      if (upload(net, img.data(), img.size() * sizeof(float), &d) != cudaSuccess) { err = "upload MLP image"; return -1; }
+      net.mlp_img = (const float *)d;
+    }
     return 0;
   }
   const bool rainbow = cfg.net == BCTS_NET_RAINBOW_BF16;
@@ -705,6 +714,11 @@ int net_eval(Net &net, const NodeView &v, int64_t n, int mode, float gd, float *
   }
   if (net.kind == BCTS_NET_MLP2_F32) {
     if (net.prof) net.prof->begin(KC_MLP, 2.0 * (double)n * ((double)net.in * net.hid + (double)net.hid * A), st);
+    if (net.mlp_img) {
+      launch_mlp_tiled(v, n, net.mlp_img, net.in, net.hid, A, mode, gd, out, net.feat_f32, st);
+      if (net.prof) net.prof->end(st);
+      return 1;
+    }
     k_mlp<<<(unsigned)((n + kMlpWarps - 1) / kMlpWarps), 32 * kMlpWarps, 0, st>>>(
         v.state, v.state_stride, net.l1w, net.l1b, net.l2w, net.l2b, net.in, net.hid, A, n, mode, gd, v.cum, out,
         net.feat_f32);
