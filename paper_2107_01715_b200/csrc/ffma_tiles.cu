@@ -48,42 +48,77 @@ __device__ __forceinline__ void load_image(float *dst, const float *src, uint32_
       : "memory");
 }
 
-// acc[c][j] = fmaf chain over i = 0..nin-1 of WT[i][4ug + j] * X[i][8cg + c], from b[4ug + j]
-template <int LDX>
+// Column layout of an activation row X[i][0..T) (node index within the tile):
+// CPT = 8 tiles use a PERMUTED layout -- logical node 8cg + 4j + k sits at
+// column j*(T/2) + 4cg + k -- so that the 8 node groups a warp reads with one
+// LDS.128 are 8 consecutive float4 (one conflict-free wavefront) instead of 8
+// float4 32 bytes apart (2-way bank conflicts). Other CPT: plain, CPT*cg + c.
+template <int T, int CPT>
+__device__ __forceinline__ int xcol(int c) {
+  if constexpr (CPT == 8) return ((c >> 2) & 1) * (T / 2) + (c >> 3) * 4 + (c & 3);
+  else return c;
+}
+
+// acc[c][j] = fmaf chain over i = 0..nin-1 of WT[i][4ug + j] * X[i][node CPT*cg + c], from b[4ug + j].
+// The operands of step i+1 are loaded before the 4*CPT FFMAs of step i (register double buffer).
+template <int T, int CPT>
 __device__ __forceinline__ void ffma_tile(const float *__restrict__ WT, int ldw, const float *__restrict__ b,
-                                          const float *__restrict__ X, int nin, int ug, int cg, float (&acc)[8][4]) {
+                                          const float *__restrict__ X, int nin, int ug, int cg,
+                                          float (&acc)[CPT][4]) {
+  static_assert(CPT == 8 || CPT == 2, "tile shapes: 4x8 (permuted columns) or 4x2 (plain)");
   const float4 bb = *(const float4 *)(b + 4 * ug);
 #pragma unroll
-  for (int c = 0; c < 8; ++c) {
+  for (int c = 0; c < CPT; ++c) {
     acc[c][0] = bb.x; acc[c][1] = bb.y; acc[c][2] = bb.z; acc[c][3] = bb.w;
   }
-  const float *w = WT + 4 * ug, *x = X + 8 * cg;
-#pragma unroll 4
-  for (int i = 0; i < nin; ++i) {
-    const float4 wv = *(const float4 *)(w + i * ldw);
-    const float4 x0 = *(const float4 *)(x + i * LDX);
-    const float4 x1 = *(const float4 *)(x + i * LDX + 4);
-    const float xs[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      acc[c][0] = fmaf(wv.x, xs[c], acc[c][0]);
-      acc[c][1] = fmaf(wv.y, xs[c], acc[c][1]);
-      acc[c][2] = fmaf(wv.z, xs[c], acc[c][2]);
-      acc[c][3] = fmaf(wv.w, xs[c], acc[c][3]);
+  const float *w = WT + 4 * ug;
+  const float *x = X + (CPT == 8 ? 4 * cg : CPT * cg);
+  float4 wv = *(const float4 *)w;
+  float xv[CPT];
+  auto ldx = [&](const float *p, float (&v)[CPT]) {
+    if constexpr (CPT == 8) {
+      const float4 a = *(const float4 *)p, b2 = *(const float4 *)(p + T / 2);
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b2.x; v[5] = b2.y; v[6] = b2.z; v[7] = b2.w;
+    } else {
+      const float2 a = *(const float2 *)p;
+      v[0] = a.x; v[1] = a.y;
     }
+  };
+  ldx(x, xv);
+#pragma unroll 2
+  for (int i = 0; i < nin; ++i) {
+    const int nx = i + 1 < nin ? i + 1 : i;
+    const float4 wn = *(const float4 *)(w + nx * ldw);
+    float xn[CPT];
+    ldx(x + nx * T, xn);
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      acc[c][0] = fmaf(wv.x, xv[c], acc[c][0]);
+      acc[c][1] = fmaf(wv.y, xv[c], acc[c][1]);
+      acc[c][2] = fmaf(wv.z, xv[c], acc[c][2]);
+      acc[c][3] = fmaf(wv.w, xv[c], acc[c][3]);
+    }
+    wv = wn;
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) xv[c] = xn[c];
   }
 }
 
-template <int LDX>
-__device__ __forceinline__ void store_tile(float *Y, int ug, int cg, const float (&acc)[8][4], bool relu) {
+// Y[4ug + j][node CPT*cg + c] = (relu) acc[c][j], in the xcol layout
+template <int T, int CPT>
+__device__ __forceinline__ void store_tile(float *Y, int ug, int cg, const float (&acc)[CPT][4], bool relu) {
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    float v[8];
+    float v[CPT];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) v[c] = relu ? fmaxf(acc[c][j], 0.0f) : acc[c][j];
-    float *y = Y + (4 * ug + j) * LDX + 8 * cg;
-    *(float4 *)y = make_float4(v[0], v[1], v[2], v[3]);
-    *(float4 *)(y + 4) = make_float4(v[4], v[5], v[6], v[7]);
+    for (int c = 0; c < CPT; ++c) v[c] = relu ? fmaxf(acc[c][j], 0.0f) : acc[c][j];
+    float *y = Y + (4 * ug + j) * T;
+    if constexpr (CPT == 8) {
+      *(float4 *)(y + 4 * cg) = make_float4(v[0], v[1], v[2], v[3]);
+      *(float4 *)(y + T / 2 + 4 * cg) = make_float4(v[4], v[5], v[6], v[7]);
+    } else {
+      *(float2 *)(y + 2 * cg) = make_float2(v[0], v[1]);
+    }
   }
 }
 
@@ -99,9 +134,16 @@ __device__ __forceinline__ void store_tile(float *Y, int ug, int cg, const float
 // Device image (floats): W1T[100][100] | W2T | W3T | W4T[100][104] |
 // b1[100] b2[100] b3[100] b4[104]  (kDnnImg, one bulk copy), then W1A[A][100]
 // (the one-hot columns, read through L1).
-constexpr int kDnnTile = 64, kDnnThreads = 256;
+// Tiles: 10 groups of CPT children x 25 groups of 4 units = 250 tasks on
+// warps 0-7 (warp 8 computes the reward unit); T = 10*CPT children per tile. CPT = 8 (T = 80, the largest tile
+// whose two [100][T] activation buffers fit beside the 163 KB image) for big
+// levels; CPT = 2 (T = 20, 4x shorter per-tile latency, 4x more CTAs) for
+// levels too small to fill the GPU with 80-child tiles.
+constexpr int kDnnThreads = 288, kDnnCg = 10;   // warps 0-7: 250 tile tasks; warp 8: reward unit
+constexpr int kDnnPf = 4;                         // parent float4 prefetched per thread (<= 42 parents)
 constexpr int kDnnOff2 = 10000, kDnnOff3 = 20000, kDnnOff4 = 30000, kDnnOffB = 40400;
-constexpr size_t kDnnSmem = (size_t)kDnnImg * 4 + 2 * (size_t)kDnnS * kDnnTile * 4;
+template <int CPT>
+constexpr size_t dnn_smem() { return (size_t)kDnnImg * 4 + 2 * (size_t)kDnnS * (kDnnCg * CPT) * 4; }
 
 int64_t dnn_env_weights_count(int A) { return 40501 + 100LL * A; }
 
@@ -129,83 +171,129 @@ void dnn_repack(const float *blob, int A, float *out) {
 }
 
 namespace {
-// hidden layer: Y[u][c] = relu(chain) for u < 100, c < 8*n_cg
-__device__ __forceinline__ void dnn_hidden(const float *WT, const float *b, const float *X, float *Y, int n_cg) {
-  for (int task = threadIdx.x; task < 25 * n_cg; task += kDnnThreads) {
-    const int cg = task % n_cg, ug = task / n_cg;
-    float acc[8][4];
-    ffma_tile<kDnnTile>(WT, kDnnS, b, X, kDnnS, ug, cg, acc);
-    store_tile<kDnnTile>(Y, ug, cg, acc, true);
+// Task -> (unit group ug < 25, node group cg < 10). CPT = 8: tasks 0..199 are
+// warps of 8 node groups x 4 unit groups (cg 0..7; 3 wavefronts per step),
+// tasks 200..249 cover cg 8, 9 as 2 x 16 blocks. CPT = 2: cg = task % 10.
+template <int CPT>
+__device__ __forceinline__ void dnn_task(int task, int &ug, int &cg) {
+  if constexpr (CPT == 8) {
+    if (task < 200) { cg = task & 7; ug = task >> 3; }
+    else { cg = 8 + ((task - 200) & 1); ug = (task - 200) >> 1; }
+  } else {
+    cg = task % kDnnCg; ug = task / kDnnCg;
   }
 }
 
+// hidden layer: Y[u][c] = relu(chain) for u < 100, all T columns
+template <int T, int CPT>
+__device__ __forceinline__ void dnn_hidden(const float *WT, const float *b, const float *X, float *Y) {
+  const int task = threadIdx.x;
+  if (task < 25 * kDnnCg) {
+    int ug, cg;
+    dnn_task<CPT>(task, ug, cg);
+    float acc[CPT][4];
+    ffma_tile<T, CPT>(WT, kDnnS, b, X, kDnnS, ug, cg, acc);
+    store_tile<T, CPT>(Y, ug, cg, acc, true);
+  }
+}
+
+template <int CPT>
 __global__ void __launch_bounds__(kDnnThreads, 1)
     k_expand_dnn(NodeView par, int64_t p_first, int64_t c_begin, int64_t c_end, int A, float gk,
                  const float *__restrict__ img, NodeOut out) {
+  constexpr int T = kDnnCg * CPT;
   extern __shared__ __align__(128) float dsm[];
   float *W = dsm, *Bs = dsm + kDnnOffB;
-  float *bufA = dsm + kDnnImg, *bufB = bufA + kDnnS * kDnnTile;
+  float *bufA = dsm + kDnnImg, *bufB = bufA + kDnnS * T;
   __shared__ __align__(8) uint64_t bar;
   const float *W1A = img + kDnnImg;
   load_image(dsm, img, kDnnImg * 4, &bar);
-  const int64_t n = c_end - c_begin, ntiles = (n + kDnnTile - 1) / kDnnTile;
+  const int64_t n = c_end - c_begin, ntiles = (n + T - 1) / T;
+  // parent states of a tile, 25 float4 each, fetched into registers one tile ahead
+  float4 pf[kDnnPf];
+  auto fetch = [&](int64_t tt) {
+    if (tt >= ntiles) return;
+    const int64_t cb = c_begin + tt * T, pb = cb / A;
+    const int npp = (int)((cb + min((int64_t)T, c_end - cb) - 1) / A - pb + 1);
+#pragma unroll
+    for (int k = 0; k < kDnnPf; ++k) {
+      const int e = threadIdx.x + k * kDnnThreads;
+      if (e < npp * 25) {
+        const int p = e / 25, q = e - p * 25;
+        pf[k] = __ldg((const float4 *)(par.state + (pb + p - p_first) * par.state_stride) + q);
+      }
+    }
+  };
+  fetch(blockIdx.x);
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int64_t c0 = c_begin + t * kDnnTile;
-    const int nc = (int)min((int64_t)kDnnTile, c_end - c0);
+    const int64_t c0 = c_begin + t * T;
+    const int nc = (int)min((int64_t)T, c_end - c0);
     const int64_t p0 = c0 / A;
-    const int np = (int)((c0 + nc - 1) / A - p0 + 1);   // <= 64/A + 2 <= 34
-    // 0: parent states -> bufA[i][p] (columns past np are never read back)
-    for (int e = threadIdx.x; e < np * kDnnS; e += kDnnThreads) {
-      const int p = e / kDnnS, i = e - p * kDnnS;
-      bufA[i * kDnnTile + p] = ((const float *)(par.state + (p0 + p - p_first) * par.state_stride))[i];
+    const int np = (int)((c0 + nc - 1) / A - p0 + 1);   // <= T/A + 2 <= 42 (A >= 2)
+    // 0: parent states (prefetched) -> bufA[i][p] (columns past np are never read back)
+#pragma unroll
+    for (int k = 0; k < kDnnPf; ++k) {
+      const int e = threadIdx.x + k * kDnnThreads;
+      if (e < np * 25) {
+        const int p = e / 25, q = e - p * 25;
+        bufA[(4 * q + 0) * T + p] = pf[k].x;
+        bufA[(4 * q + 1) * T + p] = pf[k].y;
+        bufA[(4 * q + 2) * T + p] = pf[k].z;
+        bufA[(4 * q + 3) * T + p] = pf[k].w;
+      }
     }
     __syncthreads();
-    // 1: pre[u][p] = b1[u] + chain over the 100 state inputs, once per parent -> bufB
+    fetch(t + gridDim.x);
+    // 1: pre[u][p] = b1[u] + chain over the 100 state inputs, once per parent -> bufB (4x2 tiles)
     {
-      const int n_cg = (np + 7) / 8;
-      for (int task = threadIdx.x; task < 25 * n_cg; task += kDnnThreads) {
-        const int cg = task % n_cg, ug = task / n_cg;
-        float acc[8][4];
-        ffma_tile<kDnnTile>(W, kDnnS, Bs, bufA, kDnnS, ug, cg, acc);
-        store_tile<kDnnTile>(bufB, ug, cg, acc, false);
+      const int n_pg = (np + 1) / 2;
+      for (int task = threadIdx.x; task < 25 * n_pg; task += kDnnThreads) {
+        const int pg = task % n_pg, ug = task / n_pg;
+        float acc[2][4];
+        ffma_tile<T, 2>(W, kDnnS, Bs, bufA, kDnnS, ug, pg, acc);
+        store_tile<T, 2>(bufB, ug, pg, acc, false);
       }
     }
     __syncthreads();
     // 2: h1[u][c] = relu(pre[u][parent(c)] + W1[u][100 + a(c)]) -> bufA (children past nc: zeros)
-    for (int e = threadIdx.x; e < kDnnS * kDnnTile; e += kDnnThreads) {
-      const int u = e / kDnnTile, c = e % kDnnTile;
+#pragma unroll 4
+    for (int e = threadIdx.x; e < kDnnS * T; e += kDnnThreads) {
+      const int u = e / T, c = e % T;
       float h = 0.0f;
       if (c < nc) {
         const int64_t cc = c0 + c, p = cc / A;
         const int a = (int)(cc - p * A);
-        h = fmaxf(__fadd_rn(bufB[u * kDnnTile + (int)(p - p0)], __ldg(W1A + a * kDnnS + u)), 0.0f);
+        h = fmaxf(__fadd_rn(bufB[u * T + (int)(p - p0)], __ldg(W1A + a * kDnnS + u)), 0.0f);
       }
-      bufA[u * kDnnTile + c] = h;
+      bufA[u * T + xcol<T, CPT>(c)] = h;
     }
     __syncthreads();
-    const int n_cg = (nc + 7) / 8;
-    dnn_hidden(W + kDnnOff2, Bs + 100, bufA, bufB, n_cg);   // 3: layer 2
+    dnn_hidden<T, CPT>(W + kDnnOff2, Bs + 100, bufA, bufB);   // 3: layer 2
     __syncthreads();
-    dnn_hidden(W + kDnnOff3, Bs + 200, bufB, bufA, n_cg);   // 4: layer 3
+    dnn_hidden<T, CPT>(W + kDnnOff3, Bs + 200, bufB, bufA);   // 4: layer 3
     __syncthreads();
-    // 5: layer 4 (101 outputs, no ReLU): s' -> out.state, r -> out.cum
-    for (int task = threadIdx.x; task < 26 * n_cg; task += kDnnThreads) {
-      const int cg = task % n_cg, ug = task / n_cg;
-      float acc[8][4];
-      ffma_tile<kDnnTile>(W + kDnnOff4, 104, Bs + 300, bufA, kDnnS, ug, cg, acc);
+    // 5: layer 4 (no ReLU): units 0..99 = s' -> out.state (250 tile tasks); unit 100 = r -> out.cum,
+    //    one child chain per lane of warp 8
+    const int task = threadIdx.x;
+    if (task < 25 * kDnnCg) {
+      int ug, cg;
+      dnn_task<CPT>(task, ug, cg);
+      float acc[CPT][4];
+      ffma_tile<T, CPT>(W + kDnnOff4, 104, Bs + 300, bufA, kDnnS, ug, cg, acc);
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const int cl = 8 * cg + c;
-        if (cl >= nc) break;
-        const int64_t ci = c0 + cl - c_begin;
-        if (ug < 25) {
-          *(float4 *)((float *)(out.state + ci * out.state_stride) + 4 * ug) =
+      for (int c = 0; c < CPT; ++c) {
+        const int cl = CPT * cg + c;
+        if (cl < nc)
+          *(float4 *)((float *)(out.state + (c0 + cl - c_begin) * out.state_stride) + 4 * ug) =
               make_float4(acc[c][0], acc[c][1], acc[c][2], acc[c][3]);
-        } else {
-          const int64_t p = (c0 + cl) / A;
-          const float R = par.cum ? par.cum[p - p_first] : 0.0f;
-          out.cum[ci] = fmaf(gk, acc[c][0], R);
-        }
+      }
+    } else if (task >= 256) {
+      for (int cl = task - 256; cl < nc; cl += 32) {
+        const float *x = bufA + xcol<T, CPT>(cl);
+        float r = Bs[400];
+        for (int i = 0; i < kDnnS; ++i) r = fmaf(W[kDnnOff4 + i * 104 + 100], x[i * T], r);
+        const int64_t p = (c0 + cl) / A;
+        out.cum[c0 + cl - c_begin] = fmaf(gk, r, par.cum ? par.cum[p - p_first] : 0.0f);
       }
     }
     __syncthreads();   // bufA/bufB reuse by the next tile
@@ -234,12 +322,19 @@ void launch_expand_dnn(const NodeView &par, int64_t p_first, int64_t c_begin, in
   if (prof) prof->begin(KC_EXPAND_DNN, 2.0 * (30100.0 * (double)n + 10000.0 * (double)nparents), st);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_expand_dnn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDnnSmem);
+    cudaFuncSetAttribute(k_expand_dnn<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dnn_smem<8>());
+    cudaFuncSetAttribute(k_expand_dnn<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dnn_smem<2>());
     attr = true;
   }
-  const int64_t ntiles = (n + kDnnTile - 1) / kDnnTile;
-  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, sm_count());
-  k_expand_dnn<<<grid, kDnnThreads, kDnnSmem, st>>>(par, p_first, c_begin, c_end, A, gk, img, out);
+  const int sms = sm_count();
+  const int64_t tiles80 = (n + 79) / 80;
+  if (tiles80 >= 2 * sms) {
+    const unsigned grid = (unsigned)std::min<int64_t>(tiles80, sms);
+    k_expand_dnn<8><<<grid, kDnnThreads, dnn_smem<8>(), st>>>(par, p_first, c_begin, c_end, A, gk, img, out);
+  } else {
+    const unsigned grid = (unsigned)std::min<int64_t>((n + 19) / 20, sms);
+    k_expand_dnn<2><<<grid, kDnnThreads, dnn_smem<2>(), st>>>(par, p_first, c_begin, c_end, A, gk, img, out);
+  }
   if (prof) prof->end(st);
 }
 
@@ -290,28 +385,51 @@ __global__ void __launch_bounds__(kMlpThreads, 1)
   load_image(msm, img, (uint32_t)nimg * 4, &bar);
   const int64_t ntiles = (n + T - 1) / T;
   const int n_ug = H / 4, n_ag = A4 / 4;
+  // features of a tile in 16-byte chunks (4 fp32 or 16 u8 features), fetched into
+  // registers one tile ahead so the HBM latency hides under the previous tile's math
+  constexpr int KF = (T * 32 + kMlpThreads - 1) / kMlpThreads;   // chunks per thread (I <= 128)
+  const int nq = feat_f32 ? I / 4 : I / 16;
+  uint4 pf[KF];
+  auto fetch = [&](int64_t tt) {
+    if (tt >= ntiles) return;
+    const int ntt = (int)min((int64_t)T, n - tt * T);
+#pragma unroll
+    for (int k = 0; k < KF; ++k) {
+      const int e = threadIdx.x + k * kMlpThreads;
+      if (e < ntt * nq) {
+        const int c = e / nq, q = e - c * nq;
+        pf[k] = __ldg((const uint4 *)(states + (tt * T + c) * stride) + q);
+      }
+    }
+  };
+  fetch(blockIdx.x);
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int64_t first = t * T;
     const int nt = (int)min((int64_t)T, n - first);
-    // features -> X[i][c]
-    if (feat_f32) {
-      for (int e = threadIdx.x; e < nt * I; e += kMlpThreads) {
-        const int c = e / I, i = e - c * I;
-        X[i * T + c] = ((const float *)(states + (first + c) * stride))[i];
-      }
-    } else {
-      for (int e = threadIdx.x; e < nt * I; e += kMlpThreads) {
-        const int c = e / I, i = e - c * I;
-        X[i * T + c] = (float)states[(first + c) * stride + i] / 256.0f;
+    // features (prefetched) -> X[i][xcol(c)]
+#pragma unroll
+    for (int k = 0; k < KF; ++k) {
+      const int e = threadIdx.x + k * kMlpThreads;
+      if (e < nt * nq) {
+        const int c = e / nq, q = e - c * nq, col = xcol<T, 8>(c);
+        const uint32_t w[4] = {pf[k].x, pf[k].y, pf[k].z, pf[k].w};
+        if (feat_f32) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) X[(4 * q + j) * T + col] = __uint_as_float(w[j]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) X[(16 * q + j) * T + col] = (float)((w[j / 4] >> (8 * (j % 4))) & 0xFFu) / 256.0f;
+        }
       }
     }
     __syncthreads();
+    fetch(t + gridDim.x);
     // layer 1: Hs[u][c] = relu(b1[u] + chain_i W1[u][i] x_i)
     for (int task = threadIdx.x; task < n_ug * (T / 8); task += kMlpThreads) {
       const int cg = task % (T / 8), ug = task / (T / 8);
       float acc[8][4];
-      ffma_tile<T>(W1T, H, b1, X, I, ug, cg, acc);
-      store_tile<T>(Hs, ug, cg, acc, true);
+      ffma_tile<T, 8>(W1T, H, b1, X, I, ug, cg, acc);
+      store_tile<T, 8>(Hs, ug, cg, acc, true);
     }
     __syncthreads();
     // layer 2: Q[c][a] = b2[a] + chain_u W2[a][u] h_u
@@ -321,9 +439,10 @@ __global__ void __launch_bounds__(kMlpThreads, 1)
       const float4 bb = *(const float4 *)(b2 + 4 * ag);
       float q0 = bb.x, q1 = bb.y, q2 = bb.z, q3 = bb.w;
       const float *w = W2T + 4 * ag;
+      const float *hc = Hs + xcol<T, 8>(c);
 #pragma unroll 8
       for (int u = 0; u < H; ++u) {
-        const float h = Hs[u * T + c];
+        const float h = hc[u * T];
         const float4 wv = *(const float4 *)(w + u * A4);
         q0 = fmaf(wv.x, h, q0);
         q1 = fmaf(wv.y, h, q1);
@@ -351,7 +470,8 @@ __global__ void __launch_bounds__(kMlpThreads, 1)
 }  // namespace
 
 bool mlp_tiled_ok(int I, int H, int A) {
-  return H % 4 == 0 && I <= 128 && mlp_smem<32>(I, H, A) <= kMlpSmemMax;
+  // I is 64 (INT_HASH bytes, 4 x 16-byte chunks) or 100 (DNN floats, 25 chunks): net_build checks it
+  return H % 4 == 0 && I % 4 == 0 && I <= 128 && mlp_smem<32>(I, H, A) <= kMlpSmemMax;
 }
 
 void launch_mlp_tiled(const NodeView &v, int64_t n, const float *img, int I, int H, int A, int mode, float gd,
