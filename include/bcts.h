@@ -196,6 +196,22 @@ bcts_status bcts_finalize(bcts_handle h, const void *roots, int64_t n_roots, int
                           int32_t *actions_out, float *root_q_out, float *vanilla_q_out,
                           float *terms_out, int64_t *best_leaf_out, bcts_stats *stats);
 
+/* bcts_pv_targets: the propagated-value (PV) training target of App. B.3
+ * ("use the cumulative reward and value computed during the TS")
+ * and the principal variation behind it, for the actions a TS policy took.
+ * For root r with executed action a_r = actions[r] (device int32 [n], each in
+ * [0, A)): target_out[r] = vanilla_q[r*A + a_r] (Eq. 1's depth-d value of a_r,
+ * uncorrected: the best R_d + gamma^d max_a Q over a_r's subtree; DESIGN.md
+ * R29) and path_out[r*depth + t] = the t-th action of the lowest best leaf
+ * best_leaf[r*A + a_r] (base-A digit t, most significant first; path[0] ==
+ * a_r). vanilla_q / best_leaf are bcts_search_ex's outputs for the same
+ * roots and depth (device). All pointers device; outputs caller-owned.
+ * Errors: INVALID_ARG (null pointers, n < 0, depth < 1 or > 12). An action
+ * outside [0, A) yields target NaN and path -1 for that root. Enqueued. */
+bcts_status bcts_pv_targets(bcts_handle h, int64_t n_roots, int32_t depth, const int32_t *actions,
+                            const float *vanilla_q, const int64_t *best_leaf, float *target_out,
+                            int32_t *path_out);
+
 /* ---- inspection entry points (same kernels as the search) -------------
  * bcts_expand: expand n_roots roots to level `level` (Alg. 1 loop body,
  * P:318-321) and write the n_roots*A^level level-`level` states as root

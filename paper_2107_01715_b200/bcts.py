@@ -25,7 +25,8 @@ RECORD_BYTES = {ENV_TABULAR: 4, ENV_INT_HASH: 64, ENV_ATARI_HASH: 28240, ENV_DNN
 EXPORTS = ["bcts_create", "bcts_destroy", "bcts_abi_version", "bcts_root_record_bytes", "bcts_status_string",
            "bcts_last_error", "bcts_search", "bcts_search_ex", "bcts_search_host", "bcts_keys_init",
            "bcts_search_shard", "bcts_finalize", "bcts_expand", "bcts_q_rows", "bcts_pack_key",
-           "bcts_key_value", "bcts_key_leaf", "bcts_shard_range", "bcts_profile_enable", "bcts_profile_read"]
+           "bcts_key_value", "bcts_key_leaf", "bcts_shard_range", "bcts_profile_enable", "bcts_profile_read",
+           "bcts_pv_targets"]
 
 
 class BctsError(RuntimeError):
@@ -89,6 +90,7 @@ def lib():
             "bcts_shard_range": ([I64, I32, I32, I32, I32, C.POINTER(I64), C.POINTER(I64)], I32),
             "bcts_profile_enable": ([P, I32], I32),
             "bcts_profile_read": ([P, C.POINTER(KernelProfile), I32], I32),
+            "bcts_pv_targets": ([P, I64, I32, P, P, P, P, P], I32),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -267,6 +269,16 @@ class Handle:
         k = lib().bcts_profile_read(self._h, buf, 32)
         return {buf[i].name.decode(): {"launches": buf[i].launches, "ms": buf[i].ms, "work": buf[i].work,
                                        "unit": "flop" if buf[i].unit else "byte"} for i in range(k)}
+
+    def pv_targets(self, actions, vanilla_q, best_leaf, n, depth):
+        """PV training target (App. B.3) of the executed actions + the best-leaf action path."""
+        import torch
+        dev = torch.device("cuda", self.device)
+        target = torch.empty(n, dtype=torch.float32, device=dev)
+        path = torch.empty(n, depth, dtype=torch.int32, device=dev)
+        self._check(lib().bcts_pv_targets(self._h, n, depth, _p(actions), _p(vanilla_q), _p(best_leaf), _p(target),
+                                          _p(path)), "bcts_pv_targets")
+        return target, path
 
     def q_rows(self, states, n):
         import torch

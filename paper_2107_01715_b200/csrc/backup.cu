@@ -132,4 +132,31 @@ void launch_finalize(const FinalizeArgs &a, cudaStream_t st, Profiler *prof) {
   if (prof) prof->end(st);
 }
 
+// PV target (App. B.3; R29): gather the executed action's Eq. 1
+// value and decode its best leaf into base-A digits (one thread per root).
+__global__ void k_pv_targets(int64_t n, int A, int d, const int32_t *__restrict__ actions,
+                             const float *__restrict__ vanilla, const int64_t *__restrict__ best_leaf,
+                             float *__restrict__ target, int32_t *__restrict__ path) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int a = actions[r];
+  if (a < 0 || a >= A) {
+    target[r] = __int_as_float(0x7fc00000);
+    for (int t = 0; t < d; ++t) path[r * d + t] = -1;
+    return;
+  }
+  target[r] = vanilla[r * A + a];
+  int64_t leaf = best_leaf[r * A + a];
+  for (int t = d - 1; t >= 0; --t) {
+    path[r * d + t] = (int32_t)(leaf % A);
+    leaf /= A;
+  }
+}
+
+void launch_pv_targets(int64_t n, int A, int d, const int32_t *actions, const float *vanilla,
+                       const int64_t *best_leaf, float *target, int32_t *path, cudaStream_t st) {
+  if (n <= 0) return;
+  k_pv_targets<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(n, A, d, actions, vanilla, best_leaf, target, path);
+}
+
 }  // namespace bcts

@@ -652,6 +652,18 @@ bcts_status bcts_q_rows(bcts_handle h, const void *states, int64_t n, float *q_o
   return cuda_check(h, "q_rows");
 }
 
+bcts_status bcts_pv_targets(bcts_handle h, int64_t n_roots, int32_t depth, const int32_t *actions,
+                            const float *vanilla_q, const int64_t *best_leaf, float *target_out,
+                            int32_t *path_out) {
+  if (!h || n_roots < 0 || depth < 1 || depth > kMaxDepth) return BCTS_ERR_INVALID_ARG;
+  if (n_roots == 0) return BCTS_OK;
+  if (!actions || !vanilla_q || !best_leaf || !target_out || !path_out) return BCTS_ERR_INVALID_ARG;
+  cudaSetDevice(h->dev);
+  launch_pv_targets(n_roots, h->A, depth, actions, vanilla_q, best_leaf, target_out, path_out, h->st);
+  h->launches += 1;
+  return cuda_check(h, "pv_targets");
+}
+
 bcts_status bcts_profile_enable(bcts_handle h, int32_t on) {
   if (!h) return BCTS_ERR_INVALID_ARG;
   cudaSetDevice(h->dev);

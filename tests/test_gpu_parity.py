@@ -407,3 +407,47 @@ def test_dnn_search_vs_oracle(cname, n, d, corr):
     frac, _, _ = action_agreement(gr["actions"], r["root_q"], RTOL_F32)
     assert frac == 1.0
     assert gr["stats"]["leaves"] == n * cfg.A ** d
+
+
+# ------------------------------------------------- NEXT-3: propagated-value (PV) target
+@pytest.mark.parametrize("cname,n,d", [("C2", 16, 3), ("D10", 4, 3), ("C5", 1, 2)])
+def test_pv_targets_replay(cname, n, d):
+    """App. B.3 (R29): target = Eq. 1 value of the executed action; the returned path starts with
+    that action, and replaying it through the oracle's forward model reaches exactly that value."""
+    cfg = dnn_cfg(cname) if cname.startswith("D") else config(cname)
+    h = handle(cfg)
+    o = Oracle.from_config(cfg)
+    roots = cfg.roots(n)
+    gamma = float(np.float32(cfg.gamma))
+    out = h.search(dev(roots), n, d, cfg.gamma, 1.0, 1, extra=True)
+    tgt, path = h.pv_targets(out["actions"], out["vanilla_q"], out["best_leaf"], n, d)
+    torch.cuda.synchronize()
+    tgt, path = tgt.cpu().numpy(), path.cpu().numpy()
+    act = out["actions"].cpu().numpy()
+    van = out["vanilla_q"].cpu().numpy()
+    np.testing.assert_array_equal(path[:, 0], act)
+    np.testing.assert_array_equal(tgt, van[np.arange(n), act])
+    bf16 = cfg.net in (3, 4)
+    for r in range(n):
+        leaf = 0
+        for t in range(d):
+            leaf = leaf * cfg.A + int(path[r, t])
+        if bf16:   # bf16 net: the replayed leaf's fp64-oracle total within the bf16 tolerance
+            tot = o.leaf_total(roots[r], d, leaf, gamma, mode=0)
+            assert abs(tot - tgt[r]) <= RTOL_BF16 * max(abs(tot), 1e-6)
+        else:      # fp32 paths: bit-exact vs the fp32 mirror's R_d + gamma^d max Q of that leaf
+            assert np.float32(o.leaf_total(roots[r], d, leaf, gamma, mode=1)) == tgt[r], r
+
+
+def test_pv_targets_bad_action_and_args():
+    h = handle("C2")
+    n, d = 2, 2
+    act = torch.tensor([1, 7], dtype=torch.int32, device=DEV)
+    van = torch.zeros(n * 4, dtype=torch.float32, device=DEV)
+    bl = torch.tensor([0, 5, 0, 0, 0, 0, 0, 0], dtype=torch.int64, device=DEV)
+    tgt, path = h.pv_targets(act, van, bl, n, d)
+    torch.cuda.synchronize()
+    assert np.isnan(tgt[1].item()) and (path[1].cpu().numpy() == -1).all()
+    np.testing.assert_array_equal(path[0].cpu().numpy(), [1, 1])
+    with pytest.raises(P.BctsError):
+        h.pv_targets(act, van, bl, n, 0)
