@@ -10,6 +10,8 @@
 
 #include <vector>
 
+#include <cuda_fp16.h>
+
 #include "engine.h"
 
 namespace bcts {
@@ -398,9 +400,15 @@ int net_build(Net &net, const bcts_config &cfg, std::string &err) {
     // channel order (c, dy, dx) inside an s2d pixel:
     //   W_shared[o][tap*48 + c*16 + dy*4 + dx] = W[o][c][4ty+dy][4tx+dx]   (c = 0..2)
     //   W_new[o][tap*16 + dy*4 + dx]           = W[o][3][4ty+dy][4tx+dx]
+    // This path runs its MMAs in fp16 (kind::f16, f16 operands): frame bytes are
+    // exact in fp16 and convert with one PRMT + one HADD2 per pair. The weights are
+    // the bf16 weights of R15 scaled by 2^14: fp16(bf16(w) * 2^14) is EXACT (8
+    // significant bits, scaled into fp16's normal range), every product and fp32
+    // partial sum is then exactly 2^14 x the bf16 one, and the epilogue's 2^-14
+    // undoes it -- the same accumulator as a bf16 MMA, with cheaper conversions.
     {
-      auto sw_image = [](const std::vector<__nv_bfloat16> &wl, int Nr, int K) {
-        std::vector<__nv_bfloat16> img((size_t)Nr * K);
+      auto sw_image = [](const std::vector<__half> &wl, int Nr, int K) {
+        std::vector<__half> img((size_t)Nr * K);
         uint8_t *dst = (uint8_t *)img.data();
         for (int n = 0; n < Nr; ++n)
           for (int kb = 0; kb < K / 64; ++kb)
@@ -409,7 +417,8 @@ int net_build(Net &net, const bcts_config &cfg, std::string &err) {
                      (const uint8_t *)(wl.data() + (size_t)n * K + kb * 64) + j * 16, 16);
         return img;
       };
-      std::vector<__nv_bfloat16> wsh((size_t)32 * 192), wnw((size_t)32 * 64);
+      auto f16s = [](float x) { return __float2half_rn(__bfloat162float(__float2bfloat16_rn(x)) * 16384.0f); };
+      std::vector<__half> wsh((size_t)32 * 192), wnw((size_t)32 * 64);
       for (int o = 0; o < 32; ++o)
         for (int tap = 0; tap < 4; ++tap) {
           const int ty = tap >> 1, tx = tap & 1;
@@ -417,12 +426,11 @@ int net_build(Net &net, const bcts_config &cfg, std::string &err) {
             for (int dx = 0; dx < 4; ++dx) {
               for (int c = 0; c < 3; ++c)
                 wsh[(size_t)o * 192 + tap * 48 + c * 16 + dy * 4 + dx] =
-                    __float2bfloat16_rn(w[((o * 4 + c) * 8 + 4 * ty + dy) * 8 + 4 * tx + dx]);
-              wnw[(size_t)o * 64 + tap * 16 + dy * 4 + dx] =
-                  __float2bfloat16_rn(w[((o * 4 + 3) * 8 + 4 * ty + dy) * 8 + 4 * tx + dx]);
+                    f16s(w[((o * 4 + c) * 8 + 4 * ty + dy) * 8 + 4 * tx + dx]);
+              wnw[(size_t)o * 64 + tap * 16 + dy * 4 + dx] = f16s(w[((o * 4 + 3) * 8 + 4 * ty + dy) * 8 + 4 * tx + dx]);
             }
         }
-      std::vector<__nv_bfloat16> a = sw_image(wsh, 32, 192), b = sw_image(wnw, 32, 64);
+      std::vector<__half> a = sw_image(wsh, 32, 192), b = sw_image(wnw, 32, 64);
       void *da = nullptr, *db = nullptr;
       if (upload(net, a.data(), a.size() * 2, &da) != cudaSuccess || upload(net, b.data(), b.size() * 2, &db) != cudaSuccess) {
         err = "upload factorised conv1 weights";

@@ -42,10 +42,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
       "{\n"
       ".reg .pred P1;\n"
       "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
       "@!P1 bra WAIT_%=;\n"
       "}\n" ::"r"(saddr(b)),
-      "r"(parity)
+      "r"(parity), "r"(0x989680u)   // suspend-time hint: a waiting warp sleeps instead of spinning
       : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint64_t *bar) {
@@ -86,6 +86,10 @@ __device__ __forceinline__ uint64_t desc_sw128(uint32_t addr) {
   d |= (uint64_t)1 << 46;
   d |= (uint64_t)2 << 61;
   return d;
+}
+// kind::f16 with fp16 A and B (a_format = b_format = 0), fp32 accumulate
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+  return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
@@ -175,7 +179,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint8_t *__restrict__ in, int64_t n_img, uint8_t *__restrict__ out) {
   constexpr int N = G::N;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const bool tron = g_trace != nullptr && P.out_mode == g_trace_sel && blockIdx.x == 0;   // debug trace, read once
+  // 1024-byte aligned base, derived from smem_raw by an OFFSET so the compiler keeps the
+  // shared address space (a uintptr_t round trip turns every access into a generic LD/ST)
+  uint8_t *smem = smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u);
   uint8_t *sW = smem;                                   // K/64 blocks of [N x 128 B], SW128
   const int nkb = P.K / 64;
   uint8_t *sIn0 = smem + (size_t)nkb * N * 128;         // two input-image buffers
@@ -219,7 +226,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int64_t img = blockIdx.x; img < n_img; img += gridDim.x, ++i) {
         const uint32_t b = i & 1u, ph = (i >> 1) & 1u;
         mbar_wait(&in_empty[b], ph ^ 1u);
-        if (g_trace && P.out_mode == g_trace_sel && blockIdx.x == 0 && i < 64) g_trace[i * 4 + 0] = gtime();
+        if (tron && i < 64) g_trace[i * 4 + 0] = gtime();
         // only the valid rows of each 64-channel row block cross memory (the
         // windows of garbage outputs read stale smem rows, which is harmless)
         const uint32_t blk = P.plane * 8u, valid = (uint32_t)P.in_rows * 128u;
@@ -242,7 +249,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int64_t img = blockIdx.x; img < n_img; img += gridDim.x, ++i) {
       const uint32_t b = i & 1u, ph = (i >> 1) & 1u;
       mbar_wait(&in_full[b], ph);
-      if (g_trace && P.out_mode == g_trace_sel && blockIdx.x == 0 && i < 64 && elected) g_trace[i * 4 + 1] = gtime();
+      if (tron && i < 64 && elected) g_trace[i * 4 + 1] = gtime();
       mbar_wait(&tempty[b], ph ^ 1u);
       tc_fence_after();
       const uint32_t a_base = saddr(sIn0 + b * in_stride);
@@ -265,7 +272,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mma_pred(d0 + (uint32_t)(mt * N), adesc0 + (a_off >> 4), wdesc + (w_off >> 4), idesc,
                      (tap | kk) != 0, elected);
           }
-      if (g_trace && P.out_mode == g_trace_sel && blockIdx.x == 0 && i < 64 && elected) g_trace[i * 4 + 2] = gtime();
+      if (tron && i < 64 && elected) g_trace[i * 4 + 2] = gtime();
       commit_pred(&in_empty[b], elected);   // input buffer free once these MMAs retire
       commit_pred(&tfull[b], elected);      // accumulators of this image complete
       __syncwarp();
@@ -331,7 +338,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      if (g_trace && P.out_mode == g_trace_sel && blockIdx.x == 0 && i < 64 && r == 0 && c0 == 0)
+      if (tron && i < 64 && r == 0 && c0 == 0)
         g_trace[i * 4 + 3] = gtime();
     }
   }
@@ -377,7 +384,10 @@ __global__ void __launch_bounds__(kThreadsF, 1)
   using G = G1;
   constexpr int N = G::N;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const bool tron = g_trace != nullptr && g_trace_sel == 9 && blockIdx.x == 0;
+  // 1024-byte aligned base, derived from smem_raw by an OFFSET so the compiler keeps the
+  // shared address space (a uintptr_t round trip turns every access into a generic LD/ST)
+  uint8_t *smem = smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u);
   constexpr int nkb = 256 / 64;
   uint8_t *sW = smem;                                           // 16 KB SW128 weights
   uint8_t *sIn0 = smem + nkb * N * 128;                         // 2 x SW128 s2d child images
@@ -444,7 +454,7 @@ __global__ void __launch_bounds__(kThreadsF, 1)
             mma_pred(d0 + (uint32_t)(mt * N), adesc0 + (a_off >> 4), wdesc + (w_off >> 4), idesc, (tap | kk) != 0,
                      elected);
           }
-      if (g_trace && g_trace_sel == 9 && blockIdx.x == 0 && i < 64 && elected) g_trace[i * 4 + 2] = gtime();
+      if (tron && i < 64 && elected) g_trace[i * 4 + 2] = gtime();
       commit_pred(&in_empty[b], elected);
       commit_pred(&tfull[b], elected);
       __syncwarp();
@@ -492,7 +502,7 @@ __global__ void __launch_bounds__(kThreadsF, 1)
           *(uint4 *)(oimg + act_off(2, P.out_plane, row, sub * 4 + ((c0 + 8 * h2) >> 3))) =
               make_uint4(pk[4 * h2], pk[4 * h2 + 1], pk[4 * h2 + 2], pk[4 * h2 + 3]);
       }
-      if (g_trace && g_trace_sel == 9 && blockIdx.x == 0 && i < 64 && r == 0 && c0 == 0) g_trace[i * 4 + 3] = gtime();
+      if (tron && i < 64 && r == 0 && c0 == 0) g_trace[i * 4 + 3] = gtime();
     }
   } else {
     // ---------------------------------------------- converters (8 warps)
@@ -529,7 +539,7 @@ __global__ void __launch_bounds__(kThreadsF, 1)
       }
       const uint32_t b = i & 1u, ph = (i >> 1) & 1u;
       mbar_wait(&in_empty[b], ph ^ 1u);
-      const bool tr = g_trace && g_trace_sel == 9 && blockIdx.x == 0 && i < 64 && t == 0;
+      const bool tr = tron && i < 64 && t == 0;
       if (tr) g_trace[i * 4 + 0] = gtime();
       uint8_t *dimg = sIn0 + b * in_stride;
       for (int task = t; task < 441 * 4; task += kConvThreads) {
@@ -572,9 +582,22 @@ __global__ void __launch_bounds__(kThreadsF, 1)
 // order inside an s2d(4) pixel (c, dy, dx): plane j of the shared image holds
 // frame c = j/2 at dy in {2(j%2), 2(j%2)+1}; the new image has 2 planes (dy pairs).
 //   warp 0: MMA issuer   warps 1-8: epilogue   warps 9-16: converters
-constexpr int kSibThreads = 480;                    // warp 0 MMA, 1-8 epilogue, 9-14 converters
-constexpr int kSibConv = 192;
-__device__ __forceinline__ void sib_bar() { asm volatile("bar.sync 1, 192;" ::: "memory"); }
+constexpr int kSibThreads = 512;                    // warp 0 MMA, 1-8 epilogue, 9-15 converters
+constexpr int kSibConv = 224;
+__device__ __forceinline__ void sib_bar() { asm volatile("bar.sync 1, 224;" ::: "memory"); }   // 7 converter warps
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 2, 256;" ::: "memory"); }   // 8 epilogue warps
+constexpr int kStageBlk = 100 * 128;   // one act1 row block: 10x10 rows x 128 B
+// Two bytes -> fp16x2, exactly: PRMT builds halves 0x64bb (= 1024 + b), HADD2 subtracts 1024.
+__device__ __forceinline__ uint32_t h2_minus1024(uint32_t u) {
+  uint32_t r;
+  asm("add.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(u), "r"(0xE400E400u));
+  return r;
+}
+// bytes (i, i+1) of w -> fp16x2 (i = 0 or 2)
+__device__ __forceinline__ uint32_t u8pair_f16x2(uint32_t w, uint32_t sel) {
+  return h2_minus1024(__byte_perm(w, 0x64646464u, sel));
+}
+constexpr float kSibScale = 6.103515625e-05f;   // 2^-14: undoes the fp16 weight scaling (qnet.cu)
 constexpr uint32_t kSibPlane = 536 * 16;            // rows 0..535 x 16 B
 constexpr uint32_t kSharedBytes = 6 * kSibPlane;    // 51,456
 constexpr uint32_t kNewBytes = 2 * kSibPlane;       // 17,152
@@ -586,13 +609,17 @@ __global__ void __launch_bounds__(kSibThreads, 1)
                 float gk, uint8_t *__restrict__ out, float *__restrict__ cum_out) {
   constexpr int N = 32;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const bool tron = g_trace != nullptr && g_trace_sel == 10 && blockIdx.x == 0;
+  // 1024-byte aligned base, derived from smem_raw by an OFFSET so the compiler keeps the
+  // shared address space (a uintptr_t round trip turns every access into a generic LD/ST)
+  uint8_t *smem = smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u);
   uint8_t *sWsh = smem;                              // 3 k-blocks x [32 x 128 B] SW128 (K = 192)
   uint8_t *sWnw = sWsh + 3 * N * 128;                // 1 k-block (K = 64)
   uint8_t *sSh = sWnw + N * 128;                     // 2 x shared image
   uint8_t *sNw = sSh + 2 * kSharedBytes;             // kNewRing x new image
   uint32_t *sNew3 = (uint32_t *)(sNw + kNewRing * kNewBytes);   // 2 x parent newest-frame bytes (7056 B)
   uint64_t *sNoise = (uint64_t *)((uint8_t *)sNew3 + 2 * 7056);   // 882 noise words of the current child
+  uint8_t *sStage = (uint8_t *)sNoise + 882 * 8;     // one child's act1 (2 x 100 rows x 128 B, global layout)
   __shared__ __align__(8) uint64_t sh_full[2], sh_empty[2], p_full[2], p_empty[2];
   __shared__ __align__(8) uint64_t n_full[kNewRing], n_empty[kNewRing], c_full[2], c_empty[2], wbar;
   __shared__ uint32_t tmem_slot;
@@ -633,7 +660,7 @@ __global__ void __launch_bounds__(kSibThreads, 1)
 
   if (warp == 0) {
     // ---------------------------------------------- MMA issuer (whole warp, elected lane issues)
-    constexpr uint32_t idesc = idesc_bf16(128, N);
+    constexpr uint32_t idesc = idesc_f16(128, N);   // fp16 operands (see qnet.cu: exact 2^14-scaled weights)
     const uint32_t elected = elect_one();
     mbar_wait(&wbar, 0);
     const uint64_t wsh = desc_sw128(saddr(sWsh)), wnw = desc_sw128(saddr(sWnw));
@@ -681,7 +708,7 @@ __global__ void __launch_bounds__(kSibThreads, 1)
           mma_pred(tmem + 256 + cb * 128 + (uint32_t)(mt * N), desc_planar(a, kSibPlane), wnw + (w_off >> 4), idesc,
                    tap != 0, elected);
         }
-      if (g_trace && g_trace_sel == 10 && blockIdx.x == 0 && j < 64 && elected) g_trace[j * 4 + 2] = gtime();
+      if (tron && j < 64 && elected) g_trace[j * 4 + 3] = clock64();   // trace (cycles): MMAs issued
       commit_pred(&n_empty[nb], elected);
       commit_pred(&c_full[cb], elected);
       __syncwarp();
@@ -711,12 +738,20 @@ __global__ void __launch_bounds__(kSibThreads, 1)
         for (int mt = 0; mt < 4; ++mt) tmem_wait16(vp[mt]);
         tc_fence_before();
         mbar_arrive(&p_empty[sb]);   // the next parent's P may be accumulated now
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+          for (int e = 0; e < 16; ++e)   // Pb = P * 2^-14 + bias, once per parent
+            vp[mt][e] = __float_as_uint(fmaf(__uint_as_float(vp[mt][e]), kSibScale, sbias[c0 + e]));
         cur_p = p;
       }
       const uint32_t cb = j & 1u, cph = (j >> 1) & 1u;
       mbar_wait(&c_full[cb], cph);
       tc_fence_after();
       uint8_t *oimg = out + img * (int64_t)P.out_img_bytes;
+      // the staging buffer is free once the previous child's bulk store has read it
+      if (threadIdx.x == 32) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      epi_bar();
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {   // two tiles at a time (register budget)
         uint32_t vc[2][16];
@@ -737,26 +772,49 @@ __global__ void __launch_bounds__(kSibThreads, 1)
           if (oy >= 20 || ox >= 20) continue;
           uint32_t pk[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const float x = (__uint_as_float(vp[mt][2 * e]) + __uint_as_float(vc[u][2 * e])) + sbias[c0 + 2 * e];
-            const float y =
-                (__uint_as_float(vp[mt][2 * e + 1]) + __uint_as_float(vc[u][2 * e + 1])) + sbias[c0 + 2 * e + 1];
-            __nv_bfloat162 hh = __floats2bfloat162_rn(x > 0.0f ? x : 0.0f, y > 0.0f ? y : 0.0f);
+          for (int e = 0; e < 8; ++e) {   // relu(C * 2^-14 + Pb) -> bf16 (ReLU on the packed pair)
+            const float x = fmaf(__uint_as_float(vc[u][2 * e]), kSibScale, __uint_as_float(vp[mt][2 * e]));
+            const float y = fmaf(__uint_as_float(vc[u][2 * e + 1]), kSibScale, __uint_as_float(vp[mt][2 * e + 1]));
+            __nv_bfloat162 hh = __hmax2(__floats2bfloat162_rn(x, y), __float2bfloat162_rn(0.0f));
             pk[e] = *(uint32_t *)&hh;
           }
           const int sub = ((oy & 1) << 1) | (ox & 1);
           const int row = (oy >> 1) * P.out_w + (ox >> 1);
 #pragma unroll
-          for (int h2 = 0; h2 < 2; ++h2)
-            *(uint4 *)(oimg + act_off(2, P.out_plane, row, sub * 4 + ((c0 + 8 * h2) >> 3))) =
+          for (int h2 = 0; h2 < 2; ++h2) {   // into the staging image, in act1's global SW128 layout
+            const int chunk = sub * 4 + ((c0 + 8 * h2) >> 3);
+            *(uint4 *)(sStage + (chunk >> 3) * kStageBlk + row * 128 + (((chunk & 7) ^ (row & 7)) << 4)) =
                 make_uint4(pk[4 * h2], pk[4 * h2 + 1], pk[4 * h2 + 2], pk[4 * h2 + 3]);
+          }
         }
       }
-      if (g_trace && g_trace_sel == 10 && blockIdx.x == 0 && j < 64 && r == 0 && c0 == 0) g_trace[j * 4 + 3] = gtime();
+      // whole image staged: the TMA engine writes the two row blocks to global (async)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      epi_bar();
+      if (threadIdx.x == 32) {
+        for (int q = 0; q < 2; ++q)
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(oimg + q * P.out_plane * 8u),
+                       "r"(saddr(sStage) + q * kStageBlk), "r"(kStageBlk)
+                       : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
     }
   } else {
-    // ---------------------------------------------- converters (8 warps)
-    const int t = threadIdx.x - 288;   // 0..191
+    // ---------------------------------------------- converters (7 warps)
+    const int t = threadIdx.x - 288;   // 0..223
+    // this thread's new-frame tasks, fixed for every child: 4-pixel quad index of the
+    // (dy = 2*dyp) row and the destination offset in the new image
+    constexpr int kTasks = (441 * 2 + kSibConv - 1) / kSibConv;
+    int tq[kTasks];
+    uint32_t tdst[kTasks];
+#pragma unroll
+    for (int it = 0; it < kTasks; ++it) {
+      const int task = min(t + it * kSibConv, 441 * 2 - 1);
+      const int dyp = task >= 441, pix = task - 441 * dyp;   // plane-major: conflict-free STS
+      const int Y = pix / 21, X = pix - Y * 21;
+      tq[it] = ((4 * Y + 2 * dyp) * 84 + 4 * X) >> 2;
+      tdst[it] = (uint32_t)dyp * kSibPlane + (uint32_t)pix * 16u;
+    }
     int64_t cur_p = -1;
     uint32_t k = 0, j = 0;
     uint64_t pkey = 0;
@@ -778,18 +836,17 @@ __global__ void __launch_bounds__(kSibThreads, 1)
         for (int it = 0; it < (441 * 2 + kSibConv - 1) / kSibConv; ++it) {
           const int task = t + it * kSibConv;
           if (task >= 441 * 2) break;
-          const int pix = task >> 1, dyp = task & 1;
+          const int dyp = task >= 441, pix = task - 441 * dyp;   // plane-major: conflict-free STS
           const int Y = pix / 21, X = pix - Y * 21;
           const int pa = (4 * Y + 2 * dyp) * 84 + 4 * X;           // dy = 2*dyp, 2*dyp+1 (4 pixels each)
           const uint4 x = __ldg((const uint4 *)pf + (pa >> 2));
           const uint4 y = __ldg((const uint4 *)pf + ((pa + 84) >> 2));
-          // child frame c = parent frame c+1 (bytes 1..3), 8 values per plane row: (dy0: dx0..3, dy1: dx0..3)
+          // child frame c = parent frame c+1 (bytes 1..3), 8 fp16 per plane row: (dy0: dx0..3, dy1: dx0..3)
 #pragma unroll
           for (int cc = 0; cc < 3; ++cc) {
-            const uint32_t sel = 0x7540u + (uint32_t)(cc + 1);
-            auto cv = [&](uint32_t w) { return __float_as_uint(__uint_as_float(__byte_perm(w, 0x4B000000u, sel)) - 8388608.0f); };
-            const uint4 v = make_uint4(__byte_perm(cv(x.x), cv(x.y), 0x7632u), __byte_perm(cv(x.z), cv(x.w), 0x7632u),
-                                       __byte_perm(cv(y.x), cv(y.y), 0x7632u), __byte_perm(cv(y.z), cv(y.w), 0x7632u));
+            const uint32_t b = (uint32_t)(cc + 1), s2 = b | ((b + 4) << 8);   // byte b of u and of v
+            auto hp = [&](uint32_t u, uint32_t v) { return h2_minus1024(__byte_perm(__byte_perm(u, v, s2), 0x6464u, 0x5140u)); };
+            const uint4 v = make_uint4(hp(x.x, x.y), hp(x.z, x.w), hp(y.x, y.y), hp(y.z, y.w));
             *(uint4 *)(sh + (size_t)(2 * cc + dyp) * kSibPlane + (size_t)pix * 16) = v;
           }
           n3[pa >> 2] = __byte_perm(__byte_perm(x.x, x.y, 0x0073u), __byte_perm(x.z, x.w, 0x0073u), 0x5410u);
@@ -801,6 +858,7 @@ __global__ void __launch_bounds__(kSibThreads, 1)
         cur_p = p;
       }
       const uint32_t sb = k & 1u;
+      if (tron && j < 64 && t == 0) g_trace[j * 4 + 0] = clock64();   // trace (cycles): child start
       const uint64_t k2 = mix64d(pkey ^ (0x9E3779B97F4A7C15ull * (uint64_t)(a + 1)));   // child key
       if (t == 0) {
         const uint32_t tt = (uint32_t)(k2 >> 61);
@@ -817,29 +875,26 @@ __global__ void __launch_bounds__(kSibThreads, 1)
       }
       mbar_wait(&n_empty[nb], nph ^ 1u);
       sib_bar();   // noise table complete
-      const bool tr = g_trace && g_trace_sel == 10 && blockIdx.x == 0 && j < 64 && t == 0;
-      if (tr) g_trace[j * 4 + 0] = gtime();
+      const bool tr = tron && j < 64 && t == 0;
+      if (tr) g_trace[j * 4 + 1] = clock64();   // conversion start
       uint8_t *nw = sNw + nb * kNewBytes;
       const uint32_t *n3 = sNew3 + sb * (7056 / 4);
+      const uint32_t *nz = (const uint32_t *)sNoise;   // quad q's noise bytes = word q (little endian)
 #pragma unroll
-      for (int it = 0; it < (441 * 2 + kSibConv - 1) / kSibConv; ++it) {
-        const int task = t + it * kSibConv;
-        if (task >= 441 * 2) break;
-        const int pix = task >> 1, dyp = task & 1;
-        const int Y = pix / 21, X = pix - Y * 21;
-        const int pa = (4 * Y + 2 * dyp) * 84 + 4 * X;
-        const int pb = pa + 84;
-        const uint32_t na = (uint32_t)(sNoise[pa >> 3] >> (8 * (pa & 7)));
-        const uint32_t nbz = (uint32_t)(sNoise[pb >> 3] >> (8 * (pb & 7)));
-        const uint32_t ba = n3[pa >> 2] ^ na, bb = n3[pb >> 2] ^ nbz;   // child newest-frame bytes
-        const uint4 v = make_uint4(u8pair_bf16x2(ba, 0), u8pair_bf16x2(ba, 2), u8pair_bf16x2(bb, 0), u8pair_bf16x2(bb, 2));
-        *(uint4 *)(nw + (size_t)dyp * kSibPlane + (size_t)pix * 16) = v;
+      for (int it = 0; it < kTasks; ++it) {
+        if (t + it * kSibConv >= 441 * 2) break;
+        const int qa = tq[it], qb = qa + 21;          // rows dy and dy + 1 (84 pixels = 21 quads apart)
+        const uint32_t ba = n3[qa] ^ nz[qa], bb = n3[qb] ^ nz[qb];   // child newest-frame bytes
+        const uint4 v = make_uint4(u8pair_f16x2(ba, 0x4140u), u8pair_f16x2(ba, 0x4342u), u8pair_f16x2(bb, 0x4140u),
+                                   u8pair_f16x2(bb, 0x4342u));
+        *(uint4 *)(nw + tdst[it]) = v;
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(&n_full[nb]);
-      if (tr) g_trace[j * 4 + 1] = gtime();
+      if (tr) g_trace[j * 4 + 2] = clock64();   // conversion end (n_full arrived)
     }
   }
+  if (threadIdx.x == 32) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   __syncthreads();
   if (warp == 0) {
     tc_fence_after();
@@ -896,7 +951,8 @@ void launch_conv1_sib(const ConvSW &P, const Layer &L, const uint8_t *wsh, const
                       int64_t p_first, int64_t c_begin, int64_t n_img, int A, float gk, void *out, float *cum_out,
                       cudaStream_t st) {
   if (n_img <= 0) return;
-  constexpr int smem = 4 * 32 * 128 + 2 * (int)kSharedBytes + kNewRing * (int)kNewBytes + 2 * 7056 + 882 * 8 + 1024;
+  constexpr int smem = 4 * 32 * 128 + 2 * (int)kSharedBytes + kNewRing * (int)kNewBytes + 2 * 7056 + 882 * 8 +
+                       2 * (int)kStageBlk + 1024;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_conv1_sib, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

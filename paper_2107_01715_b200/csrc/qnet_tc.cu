@@ -134,7 +134,9 @@ __global__ void __launch_bounds__(kThreads2, 1) k_layer_tc(Layer L, const void *
                                                            void *__restrict__ out, int n_m, int n_n) {
   using C = Cfg<BN, U8, BRES>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  // 1024-byte aligned base, derived from smem_raw by an OFFSET so the compiler keeps the
+  // shared address space (a uintptr_t round trip turns every access into a generic LD/ST)
+  uint8_t *smem = smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u);
   uint8_t *sB_res = smem + C::STAGES * C::STAGE;   // resident weights (BRES)
   __shared__ __align__(8) uint64_t full[C::STAGES], empty[C::STAGES], tfull[2], tempty[2];
   __shared__ uint32_t tmem_slot;

@@ -20,6 +20,14 @@ else:
 lib.bcts_debug_conv_trace(None, -1)
 t = buf.cpu().numpy().reshape(64, 4).astype(np.float64)
 t0 = t[0, 0]
+if layer == 10:
+    print("k_conv1_sib trace in SM cycles: child start (converter), conversion start, conversion end, MMAs issued")
+    for i in range(64):
+        if t[i, 0] == 0: break
+        prev = t[i - 1, 0] if i else t0
+        print(f"{i:3d} period {t[i,0]-prev:7.0f}  k2+noise+bars {t[i,1]-t[i,0]:6.0f}  convert {t[i,2]-t[i,1]:6.0f}  "
+              f"->mma {t[i,3]-t[i,2]:7.0f}")
+    sys.exit(0)
 print("img  t0 t1 t2 t3 [copy_issued/conv_start, input_ready/conv_done, mma_issued, epi_done]   (us from first copy; layer out_mode %d, last sub-batch)" % layer + "")
 for i in range(64):
     if t[i, 0] == 0: break
