@@ -618,8 +618,7 @@ __global__ void __launch_bounds__(kSibThreads, 1)
   uint8_t *sSh = sWnw + N * 128;                     // 2 x shared image
   uint8_t *sNw = sSh + 2 * kSharedBytes;             // kNewRing x new image
   uint32_t *sNew3 = (uint32_t *)(sNw + kNewRing * kNewBytes);   // 2 x parent newest-frame bytes (7056 B)
-  uint64_t *sNoise = (uint64_t *)((uint8_t *)sNew3 + 2 * 7056);   // 882 noise words of the current child
-  uint8_t *sStage = (uint8_t *)sNoise + 882 * 8;     // one child's act1 (2 x 100 rows x 128 B, global layout)
+  uint8_t *sStage = (uint8_t *)sNew3 + 2 * 7056;    // one child's act1 (2 x 100 rows x 128 B, global layout)
   __shared__ __align__(8) uint64_t sh_full[2], sh_empty[2], p_full[2], p_empty[2];
   __shared__ __align__(8) uint64_t n_full[kNewRing], n_empty[kNewRing], c_full[2], c_empty[2], wbar;
   __shared__ uint32_t tmem_slot;
@@ -866,25 +865,21 @@ __global__ void __launch_bounds__(kSibThreads, 1)
         cum_out[img] = fmaf(gk, rw, pcum);   // R_d = fmaf(g[d-1], r, R_{d-1})
       }
       const uint32_t nb = j % kNewRing, nph = (j / kNewRing) & 1u;
-      // the child's 882 noise words (one mix64 per 8-pixel group; each is shared by two tasks)
-      sib_bar();   // previous child's tasks are done reading sNoise
-#pragma unroll
-      for (int it = 0; it < (882 + kSibConv - 1) / kSibConv; ++it) {
-        const int g = t + it * kSibConv;
-        if (g < 882) sNoise[g] = mix64d(k2 + (uint64_t)g);
-      }
       mbar_wait(&n_empty[nb], nph ^ 1u);
-      sib_bar();   // noise table complete
       const bool tr = tron && j < 64 && t == 0;
       if (tr) g_trace[j * 4 + 1] = clock64();   // conversion start
       uint8_t *nw = sNw + nb * kNewBytes;
       const uint32_t *n3 = sNew3 + sb * (7056 / 4);
-      const uint32_t *nz = (const uint32_t *)sNoise;   // quad q's noise bytes = word q (little endian)
+      // Each task hashes its own noise: quad q (pixels 4q..4q+3) takes the 32-bit half q&1 of
+      // mix64(k2 + q/2) (8-pixel groups, ENV_SPEC). No shared noise table, no converter barrier:
+      // every task is independent, so the mix64 chains of all tasks overlap.
 #pragma unroll
       for (int it = 0; it < kTasks; ++it) {
         if (t + it * kSibConv >= 441 * 2) break;
         const int qa = tq[it], qb = qa + 21;          // rows dy and dy + 1 (84 pixels = 21 quads apart)
-        const uint32_t ba = n3[qa] ^ nz[qa], bb = n3[qb] ^ nz[qb];   // child newest-frame bytes
+        const uint32_t na = (uint32_t)(mix64d(k2 + (uint64_t)(qa >> 1)) >> ((qa & 1) * 32));
+        const uint32_t nbq = (uint32_t)(mix64d(k2 + (uint64_t)(qb >> 1)) >> ((qb & 1) * 32));
+        const uint32_t ba = n3[qa] ^ na, bb = n3[qb] ^ nbq;   // child newest-frame bytes
         const uint4 v = make_uint4(u8pair_f16x2(ba, 0x4140u), u8pair_f16x2(ba, 0x4342u), u8pair_f16x2(bb, 0x4140u),
                                    u8pair_f16x2(bb, 0x4342u));
         *(uint4 *)(nw + tdst[it]) = v;
@@ -951,7 +946,7 @@ void launch_conv1_sib(const ConvSW &P, const Layer &L, const uint8_t *wsh, const
                       int64_t p_first, int64_t c_begin, int64_t n_img, int A, float gk, void *out, float *cum_out,
                       cudaStream_t st) {
   if (n_img <= 0) return;
-  constexpr int smem = 4 * 32 * 128 + 2 * (int)kSharedBytes + kNewRing * (int)kNewBytes + 2 * 7056 + 882 * 8 +
+  constexpr int smem = 4 * 32 * 128 + 2 * (int)kSharedBytes + kNewRing * (int)kNewBytes + 2 * 7056 +
                        2 * (int)kStageBlk + 1024;
   static bool attr = false;
   if (!attr) {
