@@ -128,6 +128,18 @@ struct TmaPlan {
   alignas(64) uint8_t mapB[128];
 };
 bool tma_plan(TmaPlan &P, const Layer &L, const void *in, int64_t cap_img);
+// Fused Rainbow head (qnet_tma.cu, k_zhead): z_v + z_a + dueling C51 + max_a in one kernel.
+struct HeadPlan {
+  bool ok = false;
+  alignas(64) uint8_t mapAv[128];
+  alignas(64) uint8_t mapAa[128];
+  alignas(64) uint8_t mapBv[128];
+  alignas(64) uint8_t mapBa[128];
+};
+bool head_plan(HeadPlan &H, const __nv_bfloat16 *hid, int64_t cap, const __nv_bfloat16 *wv64, const __nv_bfloat16 *wa64,
+               int A);
+void launch_zhead(const HeadPlan &H, const float *bias_v, const float *bias_a64, int A, int atoms, int64_t M,
+                  float vmin, float dz, int mode, float gd, const float *cum, float *out, cudaStream_t st);
 void launch_layer_tma(const TmaPlan &P, const Layer &L, int64_t n_img, void *out, cudaStream_t st);
 
 // Shifted-window conv layer (qnet_conv.cu): stride-1 conv over a per-image
@@ -186,6 +198,9 @@ struct Net {
   Layer c1, c2, c3, fc_h, z_v, z_a, fc2;
   int atoms = 51;
   float vmin = -10.f, vmax = 10.f;
+  const __nv_bfloat16 *wa64 = nullptr;   // fused head: z_a weights, 64 rows per action
+  const float *ba64 = nullptr;
+  HeadPlan head;
   // scratch: trunk sub-batches of `batch` images (conv activations stay
   // L2-resident), fc layers over `fc_batch` images at a time
   int64_t batch = 0, fc_batch = 0;

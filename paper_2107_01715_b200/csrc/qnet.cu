@@ -512,6 +512,24 @@ int net_build(Net &net, const bcts_config &cfg, std::string &err) {
     Z.H = Z.W = 1; Z.C = 512; Z.K = 512; Z.relu_bf16 = 0; Z.out_ld = Na; Z.in_img_stride = 1024; Z.in_col_off = 512;
     if (make_layer(net, Z, repack(A * atoms, Na, 1, 1, 512, [](int o, int, int, int c) { return o * 512 + c; }, w),
                    w + A * atoms * 512, A * atoms, Na, err)) return -1;
+    if (atoms <= 64) {   // fused-head copy of z_a: action a owns rows a*64 .. a*64+atoms-1 (zero pad)
+      std::vector<__nv_bfloat16> wa64((size_t)A * 64 * 512, __float2bfloat16_rn(0.0f));
+      std::vector<float> ba64((size_t)A * 64, 0.0f);
+      for (int a = 0; a < A; ++a)
+        for (int t = 0; t < atoms; ++t) {
+          for (int c = 0; c < 512; ++c)
+            wa64[((size_t)a * 64 + t) * 512 + c] = __float2bfloat16_rn(w[((size_t)a * atoms + t) * 512 + c]);
+          ba64[(size_t)a * 64 + t] = w[(size_t)A * atoms * 512 + a * atoms + t];
+        }
+      void *dw = nullptr, *db = nullptr;
+      if (upload(net, wa64.data(), wa64.size() * 2, &dw) != cudaSuccess ||
+          upload(net, ba64.data(), ba64.size() * 4, &db) != cudaSuccess) {
+        err = "upload fused-head weights";
+        return -1;
+      }
+      net.wa64 = (const __nv_bfloat16 *)dw;
+      net.ba64 = (const float *)db;
+    }
     w += (int64_t)A * atoms * 512 + A * atoms;
     net.ld_zv = Nv;
     net.ld_za = Na;
@@ -589,6 +607,8 @@ int net_build(Net &net, const bcts_config &cfg, std::string &err) {
   if (rainbow) {
     tma_plan(net.p_z_v, net.z_v, net.hid_act, FB);
     tma_plan(net.p_z_a, net.z_a, net.hid_act, FB);
+    if (net.wa64 && net.atoms == 51 && !getenv("BCTS_NO_FUSED_HEAD"))
+      head_plan(net.head, net.hid_act, FB, net.z_v.Wt, net.wa64, A);
   } else {
     tma_plan(net.p_fc2, net.fc2, net.hid_act, FB);
   }
@@ -681,6 +701,12 @@ static int eval_conv(Net &net, const NodeView *par, const NodeView *img, int64_t
                                                                gd, cum, o);
       if (net.prof) net.prof->end(st);
       launches += 2;
+    } else if (net.tc && net.head.ok) {   // z_v + z_a + dueling C51 head + max_a fused (k_zhead)
+      const float dz = (net.vmax - net.vmin) / (float)(net.atoms - 1);
+      if (net.prof) net.prof->begin(KC_FC_OUT, 2.0 * (double)nf * 512.0 * (double)(net.atoms + A * net.atoms), st);
+      launch_zhead(net.head, net.z_v.bias, net.ba64, A, net.atoms, nf, net.vmin, dz, mode, gd, cum, o, st);
+      if (net.prof) net.prof->end(st);
+      launches += 1;
     } else {
       run_layer(net, KC_FC_OUT, net.z_v, net.hid_act, nf, net.zv, st, &net.p_z_v);
       run_layer(net, KC_FC_OUT, net.z_a, net.hid_act, nf, net.za, st, &net.p_z_a);

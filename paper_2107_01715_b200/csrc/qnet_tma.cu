@@ -287,6 +287,218 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// =============================================================== fused Rainbow head
+// z_v, z_a and the dueling C51 head in ONE kernel (the 4-byte logits never reach
+// HBM). Per 128-leaf tile:
+//   job v            : z_v = h_v W_v^T (N = 64, 51 atoms) -> registers (+ bias)
+//   pass 1, chunk c  : z_a for actions 4c..4c+3 (64 TMEM columns per action: 51 atoms
+//                      + zero pad) -> running sum over actions per atom
+//   pass 2, chunk c  : z_a again -> logits = (v - mean_a) + z_a -> softmax
+//                      expectation per action -> max_a -> fmaf(g_d, max, R_d)
+// The fp32 arithmetic and its order are those of the separate z GEMM epilogues +
+// k_head_rainbow (acc + bias, sum over a in order, v - s/A, max, expf, num/den).
+// h_a (128 KB) stays resident in SMEM for both passes; h_v and the weight k-blocks
+// stream through a 3-stage ring. TMEM: two 256-column accumulators (job parity).
+constexpr int kHeadStages = 3, kHeadSlot = 32768, kHeadA = 8 * 16384;
+constexpr int kHeadSmem = kHeadA + kHeadStages * kHeadSlot + 1024;
+
+__device__ __forceinline__ void tmem_ld32_nw(uint32_t taddr, uint32_t *r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// 64 columns (one action or z_v) of this thread's TMEM lane
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t (&r)[64]) {
+  tmem_ld32_nw(taddr, r);
+  tmem_ld32_nw(taddr + 32, r + 32);
+  tmem_wait_ld();
+}
+
+template <int ATOMS>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_zhead(const __grid_constant__ CUtensorMap mapAv, const __grid_constant__ CUtensorMap mapAa,
+            const __grid_constant__ CUtensorMap mapBv, const __grid_constant__ CUtensorMap mapBa,
+            const float *__restrict__ bias_v, const float *__restrict__ bias_a64, int A, int64_t M, float vmin,
+            float dz, int mode, float gd, const float *__restrict__ cum, float *__restrict__ out) {
+  static_assert(ATOMS <= 64, "one action per 64 TMEM columns");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u);
+  uint8_t *sA = smem, *sRing = smem + kHeadA;
+  __shared__ __align__(8) uint64_t full[kHeadStages], empty[kHeadStages], tfull[2], tempty[2], a_full, a_empty;
+  __shared__ uint32_t tmem_slot;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
+  const int n_m = (int)((M + kBM - 1) / kBM);
+  const int nch = (A + 3) / 4;                       // z_a chunks of 4 actions (256 columns)
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kHeadStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 128);
+    }
+    mbar_init(&a_full, 1);
+    mbar_init(&a_empty, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(&tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {   // ------------------------------------------------ TMA producer
+      uint32_t it = 0, tl = 0;
+      for (int tile = blockIdx.x; tile < n_m; tile += gridDim.x, ++tl) {
+        const int m0 = tile * kBM;
+        for (int kb = 0; kb < 8; ++kb, ++it) {     // job v: h_v and W_v k-blocks through the ring
+          const int st = it % kHeadStages;
+          mbar_wait(&empty[st], ((it / kHeadStages) & 1u) ^ 1u);
+          const uint32_t slot = saddr(sRing + st * kHeadSlot);
+          mbar_expect_tx(&full[st], 16384 + 8192);
+          tma_2d(slot, &mapAv, kb * 64, m0, &full[st]);
+          tma_2d(slot + 16384, &mapBv, kb * 64, 0, &full[st]);
+        }
+        mbar_wait(&a_empty, (tl & 1u) ^ 1u);      // previous tile's z_a MMAs are done with sA
+        mbar_expect_tx(&a_full, kHeadA);
+        for (int kb = 0; kb < 8; ++kb) tma_2d(saddr(sA + kb * 16384), &mapAa, kb * 64, m0, &a_full);
+        for (int job = 0; job < 2 * nch; ++job) {
+          const int c = job % nch;
+          for (int kb = 0; kb < 8; ++kb, ++it) {
+            const int st = it % kHeadStages;
+            mbar_wait(&empty[st], ((it / kHeadStages) & 1u) ^ 1u);
+            mbar_expect_tx(&full[st], kHeadSlot);
+            tma_2d(saddr(sRing + st * kHeadSlot), &mapBa, kb * 64, c * 256, &full[st]);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {   // ------------------------------------------ MMA issuer
+    const uint32_t elected = elect_one();
+    uint32_t it = 0, job = 0, tl = 0;
+    for (int tile = blockIdx.x; tile < n_m; tile += gridDim.x, ++tl) {
+      for (int j = 0; j <= 2 * nch; ++j, ++job) {
+        const uint32_t b = job & 1u;
+        mbar_wait(&tempty[b], ((job >> 1) & 1u) ^ 1u);
+        tc_fence_after();
+        if (j == 1) {
+          mbar_wait(&a_full, tl & 1u);
+          tc_fence_after();
+        }
+        const int c = (j - 1) % nch;
+        const int nt = j == 0 ? 64 : (c < nch - 1 ? 256 : (A - 4 * c) * 64);
+        const uint32_t idesc = idesc_bf16(kBM, nt);
+        for (int kb = 0; kb < 8; ++kb, ++it) {
+          const int st = it % kHeadStages;
+          mbar_wait(&full[st], (it / kHeadStages) & 1u);
+          tc_fence_after();
+          const uint32_t slot = saddr(sRing + st * kHeadSlot);
+          const uint64_t ad = sdesc<64>(j == 0 ? slot : saddr(sA + kb * 16384));
+          const uint64_t bd = sdesc<64>(j == 0 ? slot + 16384 : slot);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            mma_pred(tmem + b * 256, ad + (uint64_t)(2 * kk), bd + (uint64_t)(2 * kk), idesc, (kb | kk) != 0, elected);
+          commit_pred(&empty[st], elected);
+        }
+        commit_pred(&tfull[b], elected);
+        __syncwarp();
+      }
+      commit_pred(&a_empty, elected);   // sA free once this tile's MMAs have completed
+      __syncwarp();
+    }
+  } else {   // ---------------------------------------------------------- epilogue (128 threads = rows)
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const uint32_t lanes = (uint32_t)(q * 32) << 16;
+    uint32_t job = 0;
+    for (int tile = blockIdx.x; tile < n_m; tile += gridDim.x) {
+      const int64_t m = (int64_t)tile * kBM + r;
+      float v[ATOMS], sm[ATOMS];
+      uint32_t x[64];
+      {   // job v
+        const uint32_t b = job & 1u;
+        mbar_wait(&tfull[b], (job >> 1) & 1u);
+        tc_fence_after();
+        tmem_ld64(tmem + b * 256 + lanes, x);
+        tc_fence_before();
+        mbar_arrive(&tempty[b]);
+        ++job;
+#pragma unroll
+        for (int t = 0; t < ATOMS; ++t) {
+          v[t] = __uint_as_float(x[t]) + __ldg(bias_v + t);
+          sm[t] = 0.0f;
+        }
+      }
+      for (int c = 0; c < nch; ++c, ++job) {   // pass 1: sum over actions, in action order
+        const uint32_t b = job & 1u;
+        mbar_wait(&tfull[b], (job >> 1) & 1u);
+        tc_fence_after();
+        const int na = min(4, A - 4 * c);
+        for (int s = 0; s < na; ++s) {
+          tmem_ld64(tmem + b * 256 + lanes + (uint32_t)(s * 64), x);
+          const float *bb = bias_a64 + (4 * c + s) * 64;
+#pragma unroll
+          for (int t = 0; t < ATOMS; ++t) sm[t] += __uint_as_float(x[t]) + __ldg(bb + t);
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[b]);
+      }
+#pragma unroll
+      for (int t = 0; t < ATOMS; ++t) v[t] = v[t] - sm[t] / (float)A;   // v_t - mean_a adv[a][t]
+      float best = -INFINITY;
+      for (int c = 0; c < nch; ++c, ++job) {   // pass 2: softmax expectation per action
+        const uint32_t b = job & 1u;
+        mbar_wait(&tfull[b], (job >> 1) & 1u);
+        tc_fence_after();
+        const int na = min(4, A - 4 * c);
+        for (int s = 0; s < na; ++s) {
+          tmem_ld64(tmem + b * 256 + lanes + (uint32_t)(s * 64), x);
+          const int a = 4 * c + s;
+          const float *bb = bias_a64 + a * 64;
+          float lg[ATOMS];
+          float mx = -INFINITY;
+#pragma unroll
+          for (int t = 0; t < ATOMS; ++t) {
+            lg[t] = v[t] + (__uint_as_float(x[t]) + __ldg(bb + t));
+            mx = fmaxf(mx, lg[t]);
+          }
+          float den = 0.0f, num = 0.0f;
+#pragma unroll
+          for (int t = 0; t < ATOMS; ++t) {
+            const float ex = expf(lg[t] - mx);
+            den += ex;
+            num += (vmin + (float)t * dz) * ex;
+          }
+          const float qa = num / den;
+          if (mode == MODE_ROWS && m < M) out[m * A + a] = qa;
+          best = fmaxf(best, qa);
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[b]);
+      }
+      if (mode != MODE_ROWS && m < M) out[m] = mode == MODE_ROWMAX ? best : fmaf(gd, best, cum ? cum[m] : 0.0f);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
 // ------------------------------------------------------------- host side
 PFN_cuTensorMapEncodeTiled_v12000 g_encode_tiled = nullptr;
 PFN_cuTensorMapEncodeIm2col_v12000 g_encode_im2col = nullptr;
@@ -384,6 +596,43 @@ bool tma_plan(TmaPlan &P, const Layer &L, const void *in, int64_t cap_img) {
   if (r != CUDA_SUCCESS) return false;
   P.ok = true;
   return true;
+}
+
+// Fused Rainbow head (k_zhead): maps over the hidden activations (h_v = columns
+// 0..511, h_a = 512..1023 of [cap][1024] bf16) and the head weights.
+bool head_plan(HeadPlan &H, const __nv_bfloat16 *hid, int64_t cap, const __nv_bfloat16 *wv64,
+               const __nv_bfloat16 *wa64, int A) {
+  H.ok = false;
+  if (!load_driver()) return false;
+  auto enc = [](void *map, const void *base, uint64_t cols, uint64_t rows, uint64_t ld_elems, uint32_t box_rows) {
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ld_elems * 2};
+    cuuint32_t box[2] = {64u, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    return g_encode_tiled((CUtensorMap *)map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), dims,
+                          strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  };
+  if (!enc(H.mapAv, hid, 512, (uint64_t)cap, 1024, 128) || !enc(H.mapAa, hid + 512, 512, (uint64_t)cap, 1024, 128) ||
+      !enc(H.mapBv, wv64, 512, 64, 512, 64) || !enc(H.mapBa, wa64, 512, (uint64_t)A * 64, 512, 256))
+    return false;
+  H.ok = true;
+  return true;
+}
+
+void launch_zhead(const HeadPlan &H, const float *bias_v, const float *bias_a64, int A, int atoms, int64_t M,
+                  float vmin, float dz, int mode, float gd, const float *cum, float *out, cudaStream_t st) {
+  if (M <= 0 || atoms != 51) return;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_zhead<51>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHeadSmem);
+    attr = true;
+  }
+  const int n_m = (int)((M + kBM - 1) / kBM);
+  const int grid = std::min(n_m, num_sms());
+  k_zhead<51><<<grid, kThreads, kHeadSmem, st>>>(*(const CUtensorMap *)H.mapAv, *(const CUtensorMap *)H.mapAa,
+                                                 *(const CUtensorMap *)H.mapBv, *(const CUtensorMap *)H.mapBa, bias_v,
+                                                 bias_a64, A, M, vmin, dz, mode, gd, cum, out);
 }
 
 void launch_layer_tma(const TmaPlan &P, const Layer &L, int64_t n_img, void *out, cudaStream_t st) {
