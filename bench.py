@@ -338,10 +338,14 @@ def main():
                     "work_per_launch": v["work"] / max(v["launches"], 1), "peak_source": psrc}
         tr = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tr):
-            tj = json.load(open(tr))
-            if tj.get("kernel") == name and tj.get("config") == cfg.name:
-                roofline["traffic"] = tj.get("dram_bytes_per_launch")
-                roofline["traffic_source"] = tj.get("source")
+            # one ncu --set full capture of this kernel (cold cache, a full launch), scaled to the
+            # average timed launch by algorithmic work; unit = bytes per launch like `achieved`
+            ent = json.load(open(tr)).get(cfg.name, {}).get(name)
+            if ent:
+                per_launch = v["work"] / max(v["launches"], 1)
+                roofline["traffic"] = ent["dram_bytes_per_launch"] * per_launch / ent["work_per_launch"]
+                roofline["traffic_unit"] = "bytes/launch (DRAM read+write)"
+                roofline["traffic_source"] = ent["source"]
 
     # ---- end to end: host roots in (pinned), host outputs out, through the public API
     e2e = None

@@ -168,6 +168,7 @@ __device__ __forceinline__ unsigned long long gtime() {
   return t;
 }
 
+constexpr int kConvInBufs = 3;   // k_conv_sw input ring (G1: 16 KB + 3 x 68 KB fits the 227 KB SMEM)
 // Compile-time trunk geometry (stride-1 convs after space-to-depth).
 struct G1 { static constexpr int N = 32, CIN = 64, KH = 2, KW = 2, W_IN = 21, N_MT = 4; static constexpr uint32_t BPLANE = kPlane1 * 8; };
 struct G2 { static constexpr int N = 64, CIN = 128, KH = 2, KW = 2, W_IN = 10, N_MT = 1; static constexpr uint32_t BPLANE = kPlane2 * 8; };
@@ -187,7 +188,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nkb = P.K / 64;
   uint8_t *sIn0 = smem + (size_t)nkb * N * 128;         // two input-image buffers
   const uint32_t in_stride = (P.in_img_bytes + 1023u) & ~1023u;
-  __shared__ __align__(8) uint64_t in_full[2], in_empty[2], tfull[2], tempty[2];
+  constexpr int NB = kConvInBufs;                       // input-image ring depth (hides the HBM fetch)
+  __shared__ __align__(8) uint64_t in_full[NB], in_empty[NB], tfull[2], tempty[2];
   __shared__ uint32_t tmem_slot;
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
   const uint32_t tcols_img = (uint32_t)(P.n_mt * N);
@@ -198,9 +200,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ __align__(8) uint64_t wbar;
   if (threadIdx.x < N) sbias[threadIdx.x] = bias[threadIdx.x];
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NB; ++i) {
       mbar_init(&in_full[i], 1);
       mbar_init(&in_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 256);
     }
@@ -224,7 +228,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       uint32_t i = 0;
       for (int64_t img = blockIdx.x; img < n_img; img += gridDim.x, ++i) {
-        const uint32_t b = i & 1u, ph = (i >> 1) & 1u;
+        const uint32_t b = i % NB, ph = (i / NB) & 1u;
         mbar_wait(&in_empty[b], ph ^ 1u);
         if (tron && i < 64) g_trace[i * 4 + 0] = gtime();
         // only the valid rows of each 64-channel row block cross memory (the
@@ -247,12 +251,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t wdesc = desc_sw128(saddr(sW));
     uint32_t i = 0;
     for (int64_t img = blockIdx.x; img < n_img; img += gridDim.x, ++i) {
-      const uint32_t b = i & 1u, ph = (i >> 1) & 1u;
-      mbar_wait(&in_full[b], ph);
+      const uint32_t bi = i % NB, phi = (i / NB) & 1u;     // input ring slot
+      const uint32_t b = i & 1u, ph = (i >> 1) & 1u;         // TMEM accumulator buffer
+      mbar_wait(&in_full[bi], phi);
       if (tron && i < 64 && elected) g_trace[i * 4 + 1] = gtime();
       mbar_wait(&tempty[b], ph ^ 1u);
       tc_fence_after();
-      const uint32_t a_base = saddr(sIn0 + b * in_stride);
+      const uint32_t a_base = saddr(sIn0 + bi * in_stride);
       const uint64_t adesc0 = desc_sw128_win(a_base, false);
       const uint32_t d0 = tmem + b * tcols_img;
 #pragma unroll
@@ -273,7 +278,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                      (tap | kk) != 0, elected);
           }
       if (tron && i < 64 && elected) g_trace[i * 4 + 2] = gtime();
-      commit_pred(&in_empty[b], elected);   // input buffer free once these MMAs retire
+      commit_pred(&in_empty[bi], elected);  // input buffer free once these MMAs retire
       commit_pred(&tfull[b], elected);      // accumulators of this image complete
       __syncwarp();
     }
@@ -911,7 +916,7 @@ int num_sms() {
 template <class G>
 void launch_n(const ConvSW &P, const Layer &L, const void *in, int64_t n_img, void *out, cudaStream_t st) {
   constexpr int N = G::N;
-  const int smem = (P.K / 64) * N * 128 + 2 * (int)((P.in_img_bytes + 1023u) & ~1023u) + 1024;
+  const int smem = (P.K / 64) * N * 128 + kConvInBufs * (int)((P.in_img_bytes + 1023u) & ~1023u) + 1024;
   static int attr_for = 0;
   if (attr_for < smem) {
     cudaFuncSetAttribute(k_conv_sw<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

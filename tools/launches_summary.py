@@ -9,8 +9,8 @@ agg = collections.defaultdict(lambda: [0, 0.0])
 for r in rows[start + 1:]:
     if len(r) <= val:
         continue
-    name = r[kn].split("(")[0].replace("void ", "").strip()
-    name = name.split("<unnamed>::")[-1]
+    name = r[kn].replace("void ", "").replace("bcts::<unnamed>::", "").replace("bcts::", "")
+    name = name.split("(")[0].strip()
     agg[name][0] += 1
     agg[name][1] += float(r[val].replace(",", "")) * scale.get(r[unit], 1.0)
 tot = sum(v[1] for v in agg.values())
