@@ -181,7 +181,11 @@ bcts_status validate(bcts_handle h, const void *roots, int64_t n_roots, int32_t 
 // leaves: big level (Lc) + small level (Lc/A + 2) + leaf totals (Lc). Fused
 // leaves (conv nets: the leaf level is generated inside the net): big level
 // d-1 (Lc/A + 2) + small level (Lc/A^2 + 2) + totals.
-bool fused_leaves(bcts_handle h) { return net_fuses_leaves(h->net) && h->env == BCTS_ENV_ATARI_HASH; }
+// Leaf level generated inside conv1 (k_conv1_sib) unless BCTS_F_MATERIALIZE_LEAVES asks for the
+// leaf states to be stored and scored like any other batch of states.
+bool fused_leaves(bcts_handle h) {
+  return net_fuses_leaves(h->net) && h->env == BCTS_ENV_ATARI_HASH && !(h->flags & BCTS_F_MATERIALIZE_LEAVES);
+}
 
 int64_t plan_chunk(bcts_handle h, int64_t range, size_t reserved) {
   const int64_t nb = node_bytes(h->env);
@@ -699,6 +703,19 @@ int32_t bcts_profile_read(bcts_handle h, bcts_kernel_profile *out, int32_t max) 
 // Test hook (not part of the public contract): route the shifted-window conv
 // kernel's CTA-0 phase timestamps to a device buffer (NULL disables).
 void bcts_debug_conv_trace(void *dev_buf, int32_t layer) { conv_trace_set((unsigned long long *)dev_buf, layer); }
+
+// Test hook (not part of the public contract): copy the head of an internal trunk buffer
+// (0 = act1 planar, 1 = act2 planar, 2 = act3 dense, 3 = leaf R_d) to dst (device).
+int64_t bcts_debug_net_buffer(bcts_handle h, int32_t which, void *dst, int64_t bytes) {
+  if (!h || !dst || bytes <= 0) return -1;
+  const void *src = which == 0 ? (const void *)h->net.act1p : which == 1 ? (const void *)h->net.act2p
+                    : which == 2 ? (const void *)h->net.act3 : (const void *)h->net.leaf_cum;
+  if (!src) return -1;
+  cudaSetDevice(h->dev);
+  cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice, h->st);
+  cudaStreamSynchronize(h->st);
+  return cudaGetLastError() == cudaSuccess ? bytes : -1;
+}
 
 int64_t bcts_pack_key(float value, int64_t leaf_index) { return pack_key(value, leaf_index); }
 float bcts_key_value(int64_t key) { return key_value(key); }

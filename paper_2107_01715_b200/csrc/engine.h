@@ -135,11 +135,13 @@ struct HeadPlan {
   alignas(64) uint8_t mapAa[128];
   alignas(64) uint8_t mapBv[128];
   alignas(64) uint8_t mapBa[128];
+  alignas(64) uint8_t mapBs[128];   // sum_a W_a as bf16 hi (rows 0..63) + lo (rows 64..127)
 };
 bool head_plan(HeadPlan &H, const __nv_bfloat16 *hid, int64_t cap, const __nv_bfloat16 *wv64, const __nv_bfloat16 *wa64,
-               int A);
-void launch_zhead(const HeadPlan &H, const float *bias_v, const float *bias_a64, int A, int atoms, int64_t M,
-                  float vmin, float dz, int mode, float gd, const float *cum, float *out, cudaStream_t st);
+               const __nv_bfloat16 *wsum, int A);
+void launch_zhead(const HeadPlan &H, const float *bias_v, const float *bias_a64, const float *bias_sum, int A,
+                  int atoms, int64_t M, float vmin, float dz, int mode, float gd, const float *cum, float *out,
+                  cudaStream_t st);
 void launch_layer_tma(const TmaPlan &P, const Layer &L, int64_t n_img, void *out, cudaStream_t st);
 
 // Shifted-window conv layer (qnet_conv.cu): stride-1 conv over a per-image
@@ -200,6 +202,8 @@ struct Net {
   float vmin = -10.f, vmax = 10.f;
   const __nv_bfloat16 *wa64 = nullptr;   // fused head: z_a weights, 64 rows per action
   const float *ba64 = nullptr;
+  const __nv_bfloat16 *wsum = nullptr;   // fused head: sum_a W_a (bf16 hi | lo), [128][512]
+  const float *bsum = nullptr;           // fused head: sum_a b_a [64]
   HeadPlan head;
   // scratch: trunk sub-batches of `batch` images (conv activations stay
   // L2-resident), fc layers over `fc_batch` images at a time

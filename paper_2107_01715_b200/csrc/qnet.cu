@@ -417,7 +417,14 @@ int net_build(Net &net, const bcts_config &cfg, std::string &err) {
                      (const uint8_t *)(wl.data() + (size_t)n * K + kb * 64) + j * 16, 16);
         return img;
       };
+#ifndef SIB_F16
+#define SIB_F16 1
+#endif
+#if SIB_F16
       auto f16s = [](float x) { return __float2half_rn(__bfloat162float(__float2bfloat16_rn(x)) * 16384.0f); };
+#else
+      auto f16s = [](float x) { __nv_bfloat16 b = __float2bfloat16_rn(x); return *(__half *)&b; };   // bf16 bits
+#endif
       std::vector<__half> wsh((size_t)32 * 192), wnw((size_t)32 * 64);
       for (int o = 0; o < 32; ++o)
         for (int tap = 0; tap < 4; ++tap) {
@@ -521,14 +528,34 @@ int net_build(Net &net, const bcts_config &cfg, std::string &err) {
             wa64[((size_t)a * 64 + t) * 512 + c] = __float2bfloat16_rn(w[((size_t)a * atoms + t) * 512 + c]);
           ba64[(size_t)a * 64 + t] = w[(size_t)A * atoms * 512 + a * atoms + t];
         }
-      void *dw = nullptr, *db = nullptr;
+      // sum over actions of the bf16 z_a weights (exact in double) as a bf16 hi + lo pair,
+      // and of the fp32 biases (double, rounded once)
+      std::vector<__nv_bfloat16> ws((size_t)128 * 512, __float2bfloat16_rn(0.0f));
+      std::vector<float> bs(64, 0.0f);
+      for (int t = 0; t < atoms; ++t) {
+        for (int c = 0; c < 512; ++c) {
+          double acc = 0.0;
+          for (int a = 0; a < A; ++a) acc += (double)__bfloat162float(wa64[((size_t)a * 64 + t) * 512 + c]);
+          const __nv_bfloat16 hi = __float2bfloat16_rn((float)acc);
+          ws[(size_t)t * 512 + c] = hi;
+          ws[(size_t)(64 + t) * 512 + c] = __float2bfloat16_rn((float)(acc - (double)__bfloat162float(hi)));
+        }
+        double bacc = 0.0;
+        for (int a = 0; a < A; ++a) bacc += (double)ba64[(size_t)a * 64 + t];
+        bs[t] = (float)bacc;
+      }
+      void *dw = nullptr, *db = nullptr, *dws = nullptr, *dbs = nullptr;
       if (upload(net, wa64.data(), wa64.size() * 2, &dw) != cudaSuccess ||
-          upload(net, ba64.data(), ba64.size() * 4, &db) != cudaSuccess) {
+          upload(net, ba64.data(), ba64.size() * 4, &db) != cudaSuccess ||
+          upload(net, ws.data(), ws.size() * 2, &dws) != cudaSuccess ||
+          upload(net, bs.data(), bs.size() * 4, &dbs) != cudaSuccess) {
         err = "upload fused-head weights";
         return -1;
       }
       net.wa64 = (const __nv_bfloat16 *)dw;
       net.ba64 = (const float *)db;
+      net.wsum = (const __nv_bfloat16 *)dws;
+      net.bsum = (const float *)dbs;
     }
     w += (int64_t)A * atoms * 512 + A * atoms;
     net.ld_zv = Nv;
@@ -608,7 +635,7 @@ int net_build(Net &net, const bcts_config &cfg, std::string &err) {
     tma_plan(net.p_z_v, net.z_v, net.hid_act, FB);
     tma_plan(net.p_z_a, net.z_a, net.hid_act, FB);
     if (net.wa64 && net.atoms == 51 && !getenv("BCTS_NO_FUSED_HEAD"))
-      head_plan(net.head, net.hid_act, FB, net.z_v.Wt, net.wa64, A);
+      head_plan(net.head, net.hid_act, FB, net.z_v.Wt, net.wa64, net.wsum, A);
   } else {
     tma_plan(net.p_fc2, net.fc2, net.hid_act, FB);
   }
@@ -704,7 +731,7 @@ static int eval_conv(Net &net, const NodeView *par, const NodeView *img, int64_t
     } else if (net.tc && net.head.ok) {   // z_v + z_a + dueling C51 head + max_a fused (k_zhead)
       const float dz = (net.vmax - net.vmin) / (float)(net.atoms - 1);
       if (net.prof) net.prof->begin(KC_FC_OUT, 2.0 * (double)nf * 512.0 * (double)(net.atoms + A * net.atoms), st);
-      launch_zhead(net.head, net.z_v.bias, net.ba64, A, net.atoms, nf, net.vmin, dz, mode, gd, cum, o, st);
+      launch_zhead(net.head, net.z_v.bias, net.ba64, net.bsum, A, net.atoms, nf, net.vmin, dz, mode, gd, cum, o, st);
       if (net.prof) net.prof->end(st);
       launches += 1;
     } else {

@@ -22,6 +22,8 @@
 //               double-buffered accumulators (one set per image)
 #include <algorithm>
 
+#include <cuda_fp16.h>
+
 #include "engine.h"
 
 namespace bcts {
@@ -602,7 +604,14 @@ __device__ __forceinline__ uint32_t h2_minus1024(uint32_t u) {
 __device__ __forceinline__ uint32_t u8pair_f16x2(uint32_t w, uint32_t sel) {
   return h2_minus1024(__byte_perm(w, 0x64646464u, sel));
 }
+#ifndef SIB_F16
+#define SIB_F16 1
+#endif
+#if SIB_F16
 constexpr float kSibScale = 6.103515625e-05f;   // 2^-14: undoes the fp16 weight scaling (qnet.cu)
+#else
+constexpr float kSibScale = 1.0f;
+#endif
 constexpr uint32_t kSibPlane = 536 * 16;            // rows 0..535 x 16 B
 constexpr uint32_t kSharedBytes = 6 * kSibPlane;    // 51,456
 constexpr uint32_t kNewBytes = 2 * kSibPlane;       // 17,152
@@ -664,7 +673,11 @@ __global__ void __launch_bounds__(kSibThreads, 1)
 
   if (warp == 0) {
     // ---------------------------------------------- MMA issuer (whole warp, elected lane issues)
+#if SIB_F16
     constexpr uint32_t idesc = idesc_f16(128, N);   // fp16 operands (see qnet.cu: exact 2^14-scaled weights)
+#else
+    constexpr uint32_t idesc = idesc_bf16(128, N);
+#endif
     const uint32_t elected = elect_one();
     mbar_wait(&wbar, 0);
     const uint64_t wsh = desc_sw128(saddr(sWsh)), wnw = desc_sw128(saddr(sWnw));
@@ -848,8 +861,14 @@ __global__ void __launch_bounds__(kSibThreads, 1)
           // child frame c = parent frame c+1 (bytes 1..3), 8 fp16 per plane row: (dy0: dx0..3, dy1: dx0..3)
 #pragma unroll
           for (int cc = 0; cc < 3; ++cc) {
-            const uint32_t b = (uint32_t)(cc + 1), s2 = b | ((b + 4) << 8);   // byte b of u and of v
+            const uint32_t b = (uint32_t)(cc + 1), s2 = b | ((b + 4) << 4);   // bytes: u.b, v.b
+#if SIB_F16
             auto hp = [&](uint32_t u, uint32_t v) { return h2_minus1024(__byte_perm(__byte_perm(u, v, s2), 0x6464u, 0x5140u)); };
+#else
+            const uint32_t sel = 0x7540u + b;
+            auto cv = [&](uint32_t w) { return __float_as_uint(__uint_as_float(__byte_perm(w, 0x4B000000u, sel)) - 8388608.0f); };
+            auto hp = [&](uint32_t u, uint32_t v) { (void)s2; return __byte_perm(cv(u), cv(v), 0x7632u); };
+#endif
             const uint4 v = make_uint4(hp(x.x, x.y), hp(x.z, x.w), hp(y.x, y.y), hp(y.z, y.w));
             *(uint4 *)(sh + (size_t)(2 * cc + dyp) * kSibPlane + (size_t)pix * 16) = v;
           }
@@ -885,8 +904,12 @@ __global__ void __launch_bounds__(kSibThreads, 1)
         const uint32_t na = (uint32_t)(mix64d(k2 + (uint64_t)(qa >> 1)) >> ((qa & 1) * 32));
         const uint32_t nbq = (uint32_t)(mix64d(k2 + (uint64_t)(qb >> 1)) >> ((qb & 1) * 32));
         const uint32_t ba = n3[qa] ^ na, bb = n3[qb] ^ nbq;   // child newest-frame bytes
+#if SIB_F16
         const uint4 v = make_uint4(u8pair_f16x2(ba, 0x4140u), u8pair_f16x2(ba, 0x4342u), u8pair_f16x2(bb, 0x4140u),
                                    u8pair_f16x2(bb, 0x4342u));
+#else
+        const uint4 v = make_uint4(u8pair_bf16x2(ba, 0), u8pair_bf16x2(ba, 2), u8pair_bf16x2(bb, 0), u8pair_bf16x2(bb, 2));
+#endif
         *(uint4 *)(nw + tdst[it]) = v;
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

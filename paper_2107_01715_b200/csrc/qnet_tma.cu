@@ -289,16 +289,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // =============================================================== fused Rainbow head
 // z_v, z_a and the dueling C51 head in ONE kernel (the 4-byte logits never reach
-// HBM). Per 128-leaf tile:
-//   job v            : z_v = h_v W_v^T (N = 64, 51 atoms) -> registers (+ bias)
-//   pass 1, chunk c  : z_a for actions 4c..4c+3 (64 TMEM columns per action: 51 atoms
-//                      + zero pad) -> running sum over actions per atom
-//   pass 2, chunk c  : z_a again -> logits = (v - mean_a) + z_a -> softmax
-//                      expectation per action -> max_a -> fmaf(g_d, max, R_d)
-// The fp32 arithmetic and its order are those of the separate z GEMM epilogues +
-// k_head_rainbow (acc + bias, sum over a in order, v - s/A, max, expf, num/den).
-// h_a (128 KB) stays resident in SMEM for both passes; h_v and the weight k-blocks
-// stream through a 3-stage ring. TMEM: two 256-column accumulators (job parity).
+// HBM). Per 128-leaf tile, jobs (each a K = 512 GEMM into a 256-column TMEM buffer):
+//   job v     : z_v = h_v W_v^T + b_v (N = 64, 51 atoms)
+//   job mean  : S = h_a (sum_a W_a)^T (N = 64): the action-sum of the advantage logits
+//               by linearity; sum_a W_a is carried as a bf16 hi + lo pair (K = 1024
+//               over [h_a; h_a]), i.e. to ~2^-16 relative, and sum_a b_a is added in
+//               fp32 -> mean_t = (S_t + sum_a b_a,t) / A.
+//   chunk c   : z_a for actions 4c..4c+3 (64 TMEM columns per action: 51 atoms + zero
+//               pad) -> logits = (v - mean) + z_a -> softmax expectation -> max_a.
+// h_a (128 KB) stays resident in SMEM; h_v and the weight k-blocks stream through a
+// 3-stage ring. TMEM: two 256-column accumulators, alternating by job parity.
 constexpr int kHeadStages = 3, kHeadSlot = 32768, kHeadA = 8 * 16384;
 constexpr int kHeadSmem = kHeadA + kHeadStages * kHeadSlot + 1024;
 
@@ -313,7 +313,7 @@ __device__ __forceinline__ void tmem_ld32_nw(uint32_t taddr, uint32_t *r) {
       : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-// 64 columns (one action or z_v) of this thread's TMEM lane
+// 64 columns (one action, z_v or S) of this thread's TMEM lane
 __device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t (&r)[64]) {
   tmem_ld32_nw(taddr, r);
   tmem_ld32_nw(taddr + 32, r + 32);
@@ -324,7 +324,8 @@ template <int ATOMS>
 __global__ void __launch_bounds__(kThreads, 1)
     k_zhead(const __grid_constant__ CUtensorMap mapAv, const __grid_constant__ CUtensorMap mapAa,
             const __grid_constant__ CUtensorMap mapBv, const __grid_constant__ CUtensorMap mapBa,
-            const float *__restrict__ bias_v, const float *__restrict__ bias_a64, int A, int64_t M, float vmin,
+            const __grid_constant__ CUtensorMap mapBs, const float *__restrict__ bias_v,
+            const float *__restrict__ bias_a64, const float *__restrict__ bias_sum, int A, int64_t M, float vmin,
             float dz, int mode, float gd, const float *__restrict__ cum, float *__restrict__ out) {
   static_assert(ATOMS <= 64, "one action per 64 TMEM columns");
   extern __shared__ uint8_t smem_raw[];
@@ -361,28 +362,32 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     if (lane == 0) {   // ------------------------------------------------ TMA producer
       uint32_t it = 0, tl = 0;
+      auto slot_wait = [&](uint32_t bytes) {
+        const int st = it % kHeadStages;
+        mbar_wait(&empty[st], ((it / kHeadStages) & 1u) ^ 1u);
+        mbar_expect_tx(&full[st], bytes);
+        return st;
+      };
       for (int tile = blockIdx.x; tile < n_m; tile += gridDim.x, ++tl) {
         const int m0 = tile * kBM;
         for (int kb = 0; kb < 8; ++kb, ++it) {     // job v: h_v and W_v k-blocks through the ring
-          const int st = it % kHeadStages;
-          mbar_wait(&empty[st], ((it / kHeadStages) & 1u) ^ 1u);
+          const int st = slot_wait(16384 + 8192);
           const uint32_t slot = saddr(sRing + st * kHeadSlot);
-          mbar_expect_tx(&full[st], 16384 + 8192);
           tma_2d(slot, &mapAv, kb * 64, m0, &full[st]);
           tma_2d(slot + 16384, &mapBv, kb * 64, 0, &full[st]);
         }
-        mbar_wait(&a_empty, (tl & 1u) ^ 1u);      // previous tile's z_a MMAs are done with sA
+        mbar_wait(&a_empty, (tl & 1u) ^ 1u);      // previous tile's MMAs are done with sA
         mbar_expect_tx(&a_full, kHeadA);
         for (int kb = 0; kb < 8; ++kb) tma_2d(saddr(sA + kb * 16384), &mapAa, kb * 64, m0, &a_full);
-        for (int job = 0; job < 2 * nch; ++job) {
-          const int c = job % nch;
+        for (int kb = 0; kb < 16; ++kb, ++it) {    // job mean: hi (rows 0..63) then lo (64..127)
+          const int st = slot_wait(8192);
+          tma_2d(saddr(sRing + st * kHeadSlot), &mapBs, (kb & 7) * 64, (kb >> 3) * 64, &full[st]);
+        }
+        for (int c = 0; c < nch; ++c)
           for (int kb = 0; kb < 8; ++kb, ++it) {
-            const int st = it % kHeadStages;
-            mbar_wait(&empty[st], ((it / kHeadStages) & 1u) ^ 1u);
-            mbar_expect_tx(&full[st], kHeadSlot);
+            const int st = slot_wait(kHeadSlot);
             tma_2d(saddr(sRing + st * kHeadSlot), &mapBa, kb * 64, c * 256, &full[st]);
           }
-        }
       }
     }
     __syncwarp();
@@ -390,7 +395,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t elected = elect_one();
     uint32_t it = 0, job = 0, tl = 0;
     for (int tile = blockIdx.x; tile < n_m; tile += gridDim.x, ++tl) {
-      for (int j = 0; j <= 2 * nch; ++j, ++job) {
+      for (int j = 0; j < nch + 2; ++j, ++job) {   // v, mean, chunks
         const uint32_t b = job & 1u;
         mbar_wait(&tempty[b], ((job >> 1) & 1u) ^ 1u);
         tc_fence_after();
@@ -398,15 +403,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&a_full, tl & 1u);
           tc_fence_after();
         }
-        const int c = (j - 1) % nch;
-        const int nt = j == 0 ? 64 : (c < nch - 1 ? 256 : (A - 4 * c) * 64);
+        const int c = j - 2;
+        const int nt = j < 2 ? 64 : (c < nch - 1 ? 256 : (A - 4 * c) * 64);
         const uint32_t idesc = idesc_bf16(kBM, nt);
-        for (int kb = 0; kb < 8; ++kb, ++it) {
+        const int nkb = j == 1 ? 16 : 8;
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
           const int st = it % kHeadStages;
           mbar_wait(&full[st], (it / kHeadStages) & 1u);
           tc_fence_after();
           const uint32_t slot = saddr(sRing + st * kHeadSlot);
-          const uint64_t ad = sdesc<64>(j == 0 ? slot : saddr(sA + kb * 16384));
+          const uint64_t ad = sdesc<64>(j == 0 ? slot : saddr(sA + (kb & 7) * 16384));
           const uint64_t bd = sdesc<64>(j == 0 ? slot + 16384 : slot);
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
@@ -426,7 +432,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t job = 0;
     for (int tile = blockIdx.x; tile < n_m; tile += gridDim.x) {
       const int64_t m = (int64_t)tile * kBM + r;
-      float v[ATOMS], sm[ATOMS];
+      float v[ATOMS];
       uint32_t x[64];
       {   // job v
         const uint32_t b = job & 1u;
@@ -437,29 +443,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(&tempty[b]);
         ++job;
 #pragma unroll
-        for (int t = 0; t < ATOMS; ++t) {
-          v[t] = __uint_as_float(x[t]) + __ldg(bias_v + t);
-          sm[t] = 0.0f;
-        }
+        for (int t = 0; t < ATOMS; ++t) v[t] = __uint_as_float(x[t]) + __ldg(bias_v + t);
       }
-      for (int c = 0; c < nch; ++c, ++job) {   // pass 1: sum over actions, in action order
+      {   // job mean: v_t - mean_a adv[a][t]
         const uint32_t b = job & 1u;
         mbar_wait(&tfull[b], (job >> 1) & 1u);
         tc_fence_after();
-        const int na = min(4, A - 4 * c);
-        for (int s = 0; s < na; ++s) {
-          tmem_ld64(tmem + b * 256 + lanes + (uint32_t)(s * 64), x);
-          const float *bb = bias_a64 + (4 * c + s) * 64;
-#pragma unroll
-          for (int t = 0; t < ATOMS; ++t) sm[t] += __uint_as_float(x[t]) + __ldg(bb + t);
-        }
+        tmem_ld64(tmem + b * 256 + lanes, x);
         tc_fence_before();
         mbar_arrive(&tempty[b]);
-      }
+        ++job;
 #pragma unroll
-      for (int t = 0; t < ATOMS; ++t) v[t] = v[t] - sm[t] / (float)A;   // v_t - mean_a adv[a][t]
+        for (int t = 0; t < ATOMS; ++t) v[t] = v[t] - (__uint_as_float(x[t]) + __ldg(bias_sum + t)) / (float)A;
+      }
       float best = -INFINITY;
-      for (int c = 0; c < nch; ++c, ++job) {   // pass 2: softmax expectation per action
+      for (int c = 0; c < nch; ++c, ++job) {   // softmax expectation per action
         const uint32_t b = job & 1u;
         mbar_wait(&tfull[b], (job >> 1) & 1u);
         tc_fence_after();
@@ -601,7 +599,7 @@ bool tma_plan(TmaPlan &P, const Layer &L, const void *in, int64_t cap_img) {
 // Fused Rainbow head (k_zhead): maps over the hidden activations (h_v = columns
 // 0..511, h_a = 512..1023 of [cap][1024] bf16) and the head weights.
 bool head_plan(HeadPlan &H, const __nv_bfloat16 *hid, int64_t cap, const __nv_bfloat16 *wv64,
-               const __nv_bfloat16 *wa64, int A) {
+               const __nv_bfloat16 *wa64, const __nv_bfloat16 *wsum, int A) {
   H.ok = false;
   if (!load_driver()) return false;
   auto enc = [](void *map, const void *base, uint64_t cols, uint64_t rows, uint64_t ld_elems, uint32_t box_rows) {
@@ -614,14 +612,16 @@ bool head_plan(HeadPlan &H, const __nv_bfloat16 *hid, int64_t cap, const __nv_bf
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   };
   if (!enc(H.mapAv, hid, 512, (uint64_t)cap, 1024, 128) || !enc(H.mapAa, hid + 512, 512, (uint64_t)cap, 1024, 128) ||
-      !enc(H.mapBv, wv64, 512, 64, 512, 64) || !enc(H.mapBa, wa64, 512, (uint64_t)A * 64, 512, 256))
+      !enc(H.mapBv, wv64, 512, 64, 512, 64) || !enc(H.mapBa, wa64, 512, (uint64_t)A * 64, 512, 256) ||
+      !enc(H.mapBs, wsum, 512, 128, 512, 64))
     return false;
   H.ok = true;
   return true;
 }
 
-void launch_zhead(const HeadPlan &H, const float *bias_v, const float *bias_a64, int A, int atoms, int64_t M,
-                  float vmin, float dz, int mode, float gd, const float *cum, float *out, cudaStream_t st) {
+void launch_zhead(const HeadPlan &H, const float *bias_v, const float *bias_a64, const float *bias_sum, int A,
+                  int atoms, int64_t M, float vmin, float dz, int mode, float gd, const float *cum, float *out,
+                  cudaStream_t st) {
   if (M <= 0 || atoms != 51) return;
   static bool attr = false;
   if (!attr) {
@@ -631,8 +631,9 @@ void launch_zhead(const HeadPlan &H, const float *bias_v, const float *bias_a64,
   const int n_m = (int)((M + kBM - 1) / kBM);
   const int grid = std::min(n_m, num_sms());
   k_zhead<51><<<grid, kThreads, kHeadSmem, st>>>(*(const CUtensorMap *)H.mapAv, *(const CUtensorMap *)H.mapAa,
-                                                 *(const CUtensorMap *)H.mapBv, *(const CUtensorMap *)H.mapBa, bias_v,
-                                                 bias_a64, A, M, vmin, dz, mode, gd, cum, out);
+                                                 *(const CUtensorMap *)H.mapBv, *(const CUtensorMap *)H.mapBa,
+                                                 *(const CUtensorMap *)H.mapBs, bias_v, bias_a64, bias_sum, A, M, vmin,
+                                                 dz, mode, gd, cum, out);
 }
 
 void launch_layer_tma(const TmaPlan &P, const Layer &L, int64_t n_img, void *out, cudaStream_t st) {

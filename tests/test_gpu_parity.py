@@ -27,6 +27,7 @@ from synth.inputs import (ENV_ATARI_HASH, NET_NATURE_BF16, NET_RAINBOW_BF16, Con
 THREADS = os.cpu_count() or 1
 DEV = torch.device("cuda", 0)
 RTOL_F32, RTOL_BF16 = 1e-5, 2e-2
+RTOL_BF16_SEARCH = 1e-3   # root Q of whole searches: observed <= 2e-5 (bf16 RNE flips); a broken trunk shows ~2e-3+ because random-init Q is flat across leaves
 
 
 def dev(a):
@@ -135,7 +136,7 @@ def bf16_compare(g, r, what):
     frac, exact, near = action_agreement(g["actions"], r["root_q"], RTOL_BF16)
     print(f"{what}: max rel err root_q {err.max():.2e} vanilla {verr.max():.2e}; actions {frac:.4f} "
           f"(exact {exact}, near-ties {near})")
-    assert err.max() <= RTOL_BF16 and verr.max() <= RTOL_BF16
+    assert err.max() <= RTOL_BF16_SEARCH and verr.max() <= RTOL_BF16_SEARCH
     assert frac >= 0.999
 
 
@@ -451,3 +452,22 @@ def test_pv_targets_bad_action_and_args():
     np.testing.assert_array_equal(path[0].cpu().numpy(), [1, 1])
     with pytest.raises(P.BctsError):
         h.pv_targets(act, van, bl, n, 0)
+
+
+# ------------------------------------------------- fused leaf level vs materialised leaves
+@pytest.mark.parametrize("cname,n,d", [("C3", 3, 2), ("C5", 1, 2), ("C5", 1, 3), ("C4", 2, 3)])
+def test_fused_leaves_match_materialized(cname, n, d):
+    """k_conv1_sib (leaf expansion fused into conv1, sibling-factorised, fp16 operands with exact
+    2^14-scaled weights) vs BCTS_F_MATERIALIZE_LEAVES (leaf states stored, standard conv1): the same
+    bf16 net on the same leaves, so results agree up to fp32 accumulation order / bf16 RNE flips.
+    Strict on purpose: random-init Q values are nearly flat across leaves, so a relative-to-max|Q|
+    tolerance alone cannot tell a broken trunk from rounding (best-leaf agreement can)."""
+    cfg = config(cname)
+    ha = handle(cname)
+    hb = handle(cname, flags=P.F_MATERIALIZE_LEAVES)
+    roots = cfg.roots(n)
+    a = run(ha, roots, d, cfg.gamma, 1.0, 0)
+    b = run(hb, roots, d, cfg.gamma, 1.0, 0)
+    scale = np.abs(b["vanilla_q"]).max(axis=1, keepdims=True)
+    assert (np.abs(a["vanilla_q"] - b["vanilla_q"]) <= 1e-4 * scale).all()
+    assert (a["best_leaf"] == b["best_leaf"]).mean() >= 0.9
