@@ -8,6 +8,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <vector>
 
 #include <cuda_fp16.h>
@@ -564,8 +565,10 @@ int net_build(Net &net, const bcts_config &cfg, std::string &err) {
   // scratch: trunk sub-batches of 1024 images (s2d frames, act1, act2 stay
   // L2-resident: ~94 MB), fc layers over 16384 images at a time (enough M
   // tiles to fill 148 SMs)
-  net.batch = 16384;
-  net.fc_batch = 16384;
+  // Buffer capacity = one full wave of 128-row M tiles (148 x 128): eval_conv splits a call
+  // into equal batches of at most this size (rounded to 128 rows), so no batch is a thin tail.
+  net.batch = 148 * 128;
+  net.fc_batch = 148 * 128;
   if (const char *e = getenv("BCTS_TRUNK_BATCH")) net.batch = atoll(e) > 0 ? atoll(e) : net.batch;
   const int64_t B = net.batch, FB = net.fc_batch;
   const bool simt = (cfg.flags & BCTS_F_SIMT_NET) != 0;   // dense NHWC trunk buffers only for the SIMT path
@@ -668,8 +671,11 @@ static int eval_conv(Net &net, const NodeView *par, const NodeView *img, int64_t
   const int A = net.A;
   const bool rainbow = net.kind == BCTS_NET_RAINBOW_BF16;
   int launches = 0;
-  for (int64_t f0 = 0; f0 < n; f0 += net.fc_batch) {
-    const int64_t nf = n - f0 < net.fc_batch ? n - f0 : net.fc_batch;
+  // balanced batches: ceil(n / capacity) of them, equal sizes rounded up to 128 rows
+  const int64_t nbat = (n + net.fc_batch - 1) / net.fc_batch;
+  const int64_t step = std::min<int64_t>(net.fc_batch, ((n + nbat - 1) / nbat + 127) / 128 * 128);
+  for (int64_t f0 = 0; f0 < n; f0 += step) {
+    const int64_t nf = n - f0 < step ? n - f0 : step;
     for (int64_t b0 = 0; b0 < nf; b0 += net.batch) {
       const int64_t nb = nf - b0 < net.batch ? nf - b0 : net.batch;
       const bool sw = net.tc && net.sw;
