@@ -3,13 +3,44 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
+
+#include <utility>
 
 #include <string>
 
 #include "bcts.h"
 
 namespace bcts {
+
+// ------------------------------------------------ programmatic dependent launch
+// Trunk kernels are launched with programmatic stream serialization: a kernel may be
+// scheduled while its stream predecessor drains, runs its prologue (barriers, TMEM,
+// weight bulk copies -- nothing the predecessor writes), then pdl_wait()s for the
+// predecessor's completion before touching its outputs. pdl_trigger() lets the next
+// kernel be scheduled as this one's CTAs retire. BCTS_NO_PDL=1 disables it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+inline bool pdl_enabled() {
+  static const int on = getenv("BCTS_NO_PDL") ? 0 : 1;
+  return on != 0;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 constexpr int kImg = 84;
 constexpr int kPix = kImg * kImg;             // 7056 packed pixel words per frame stack

@@ -225,6 +225,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
+  pdl_wait();      // inputs are the previous layer's outputs (PDL)
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -669,6 +671,8 @@ __global__ void __launch_bounds__(kSibThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_slot;   // cols [0,256): P[2] (4 tiles x 32 each); [256,512): C[2]
+  pdl_wait();
+  pdl_trigger();
   const int64_t pfirst_cta = (c_begin + i0) / A;
 
   if (warp == 0) {
@@ -946,7 +950,8 @@ void launch_n(const ConvSW &P, const Layer &L, const void *in, int64_t n_img, vo
     attr_for = smem;
   }
   const int grid = (int)std::min<int64_t>(n_img, num_sms());
-  k_conv_sw<G><<<grid, kThreads, smem, st>>>(P, P.wsw, L.bias, (const uint8_t *)in, n_img, (uint8_t *)out);
+  launch_pdl(k_conv_sw<G>, dim3(grid), dim3(kThreads), smem, st, P, P.wsw, L.bias, (const uint8_t *)in, n_img,
+             (uint8_t *)out);
 }
 
 }  // namespace
@@ -982,8 +987,8 @@ void launch_conv1_sib(const ConvSW &P, const Layer &L, const uint8_t *wsh, const
     attr = true;
   }
   const int grid = (int)std::min<int64_t>(n_img, num_sms());
-  k_conv1_sib<<<grid, kSibThreads, smem, st>>>(P, wsh, wnw, L.bias, par, p_first, c_begin, n_img, A, gk,
-                                             (uint8_t *)out, cum_out);
+  launch_pdl(k_conv1_sib, dim3(grid), dim3(kSibThreads), (size_t)smem, st, P, wsh, wnw, L.bias, par, p_first, c_begin,
+             n_img, A, gk, (uint8_t *)out, cum_out);
 }
 
 void launch_conv_sw(const ConvSW &P, const Layer &L, const void *in, int64_t n_img, void *out, cudaStream_t st) {

@@ -174,6 +174,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
+  pdl_wait();      // A operand = the previous kernel's output (PDL)
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -358,6 +360,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
+  pdl_wait();      // A operand = the previous kernel's output (PDL)
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {   // ------------------------------------------------ TMA producer
@@ -536,8 +540,8 @@ void launch_gemm(const TmaPlan &P, const Layer &L, int64_t M, void *out, cudaStr
   const int n_m = (int)((M + kBM - 1) / kBM), n_n = (L.Npad + BN - 1) / BN;
   const int grid = (int)std::min<int64_t>((int64_t)n_m * n_n, num_sms());
   TmaGeom G{P.im2col, L.OH, L.OW, L.S, L.KW, L.C};
-  k_gemm_tma<BN, KB><<<grid, kThreads, C::SMEM, st>>>(*(const CUtensorMap *)P.mapA, *(const CUtensorMap *)P.mapB,
-                                                     L, G, M, out, n_m, n_n);
+  launch_pdl(k_gemm_tma<BN, KB>, dim3(grid), dim3(kThreads), (size_t)C::SMEM, st, *(const CUtensorMap *)P.mapA,
+             *(const CUtensorMap *)P.mapB, L, G, M, out, n_m, n_n);
 }
 
 }  // namespace
@@ -630,10 +634,9 @@ void launch_zhead(const HeadPlan &H, const float *bias_v, const float *bias_a64,
   }
   const int n_m = (int)((M + kBM - 1) / kBM);
   const int grid = std::min(n_m, num_sms());
-  k_zhead<51><<<grid, kThreads, kHeadSmem, st>>>(*(const CUtensorMap *)H.mapAv, *(const CUtensorMap *)H.mapAa,
-                                                 *(const CUtensorMap *)H.mapBv, *(const CUtensorMap *)H.mapBa,
-                                                 *(const CUtensorMap *)H.mapBs, bias_v, bias_a64, bias_sum, A, M, vmin,
-                                                 dz, mode, gd, cum, out);
+  launch_pdl(k_zhead<51>, dim3(grid), dim3(kThreads), (size_t)kHeadSmem, st, *(const CUtensorMap *)H.mapAv,
+             *(const CUtensorMap *)H.mapAa, *(const CUtensorMap *)H.mapBv, *(const CUtensorMap *)H.mapBa,
+             *(const CUtensorMap *)H.mapBs, bias_v, bias_a64, bias_sum, A, M, vmin, dz, mode, gd, cum, out);
 }
 
 void launch_layer_tma(const TmaPlan &P, const Layer &L, int64_t n_img, void *out, cudaStream_t st) {
