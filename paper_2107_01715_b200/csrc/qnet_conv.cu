@@ -89,6 +89,12 @@ __device__ __forceinline__ uint64_t desc_sw128(uint32_t addr) {
   d |= (uint64_t)2 << 61;
   return d;
 }
+// (lo, hi) -> bf16x2 with ReLU folded into the conversion (one F2FP.RELU instead of F2FP + max)
+__device__ __forceinline__ uint32_t bf16x2_relu(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
 // kind::f16 with fp16 A and B (a_format = b_format = 0), fp32 accumulate
 __host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
   return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
@@ -325,8 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int e = 0; e < 8; ++e) {
             const float x = __uint_as_float(v[mt][h][2 * e]) + bias_r[h * 16 + 2 * e];
             const float y = __uint_as_float(v[mt][h][2 * e + 1]) + bias_r[h * 16 + 2 * e + 1];
-            __nv_bfloat162 hh = __floats2bfloat162_rn(x > 0.0f ? x : 0.0f, y > 0.0f ? y : 0.0f);
-            pk[e] = *(uint32_t *)&hh;
+            pk[e] = bf16x2_relu(x, y);
           }
 #pragma unroll
           for (int hh2 = 0; hh2 < 2; ++hh2) {
@@ -796,8 +801,7 @@ __global__ void __launch_bounds__(kSibThreads, 1)
           for (int e = 0; e < 8; ++e) {   // relu(C * 2^-14 + Pb) -> bf16 (ReLU on the packed pair)
             const float x = fmaf(__uint_as_float(vc[u][2 * e]), kSibScale, __uint_as_float(vp[mt][2 * e]));
             const float y = fmaf(__uint_as_float(vc[u][2 * e + 1]), kSibScale, __uint_as_float(vp[mt][2 * e + 1]));
-            __nv_bfloat162 hh = __hmax2(__floats2bfloat162_rn(x, y), __float2bfloat162_rn(0.0f));
-            pk[e] = *(uint32_t *)&hh;
+            pk[e] = bf16x2_relu(x, y);
           }
           const int sub = ((oy & 1) << 1) | (ox & 1);
           const int row = (oy >> 1) * P.out_w + (ox >> 1);
@@ -823,18 +827,19 @@ __global__ void __launch_bounds__(kSibThreads, 1)
   } else {
     // ---------------------------------------------- converters (7 warps)
     const int t = threadIdx.x - 288;   // 0..223
-    // this thread's new-frame tasks, fixed for every child: 4-pixel quad index of the
-    // (dy = 2*dyp) row and the destination offset in the new image
-    constexpr int kTasks = (441 * 2 + kSibConv - 1) / kSibConv;
-    int tq[kTasks];
-    uint32_t tdst[kTasks];
+    // this thread's new-frame tasks, fixed for every child: task = one 8-pixel noise group g
+    // (frame quads 2g, 2g+1: one mix64 serves both, ENV_SPEC) and the destinations of its two
+    // quads in the new image (plane dy/2, s2d pixel, 8-byte half dy%2)
+    constexpr int kTasks = (882 + kSibConv - 1) / kSibConv;
+    uint32_t tdst[kTasks][2];
 #pragma unroll
     for (int it = 0; it < kTasks; ++it) {
-      const int task = min(t + it * kSibConv, 441 * 2 - 1);
-      const int dyp = task >= 441, pix = task - 441 * dyp;   // plane-major: conflict-free STS
-      const int Y = pix / 21, X = pix - Y * 21;
-      tq[it] = ((4 * Y + 2 * dyp) * 84 + 4 * X) >> 2;
-      tdst[it] = (uint32_t)dyp * kSibPlane + (uint32_t)pix * 16u;
+      const int g = min(t + it * kSibConv, 881);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int q = 2 * g + h, y = q / 21, X = q - 21 * y;
+        tdst[it][h] = (uint32_t)(y & 3) / 2u * kSibPlane + (uint32_t)((y >> 2) * 21 + X) * 16u + (uint32_t)(y & 1) * 8u;
+      }
     }
     int64_t cur_p = -1;
     uint32_t k = 0, j = 0;
@@ -898,23 +903,21 @@ __global__ void __launch_bounds__(kSibThreads, 1)
       if (tr) g_trace[j * 4 + 1] = clock64();   // conversion start
       uint8_t *nw = sNw + nb * kNewBytes;
       const uint32_t *n3 = sNew3 + sb * (7056 / 4);
-      // Each task hashes its own noise: quad q (pixels 4q..4q+3) takes the 32-bit half q&1 of
-      // mix64(k2 + q/2) (8-pixel groups, ENV_SPEC). No shared noise table, no converter barrier:
-      // every task is independent, so the mix64 chains of all tasks overlap.
+      // noise group g: h = mix64(k2 + g) covers pixels 8g..8g+7 = quads 2g (low word) and 2g+1
 #pragma unroll
       for (int it = 0; it < kTasks; ++it) {
-        if (t + it * kSibConv >= 441 * 2) break;
-        const int qa = tq[it], qb = qa + 21;          // rows dy and dy + 1 (84 pixels = 21 quads apart)
-        const uint32_t na = (uint32_t)(mix64d(k2 + (uint64_t)(qa >> 1)) >> ((qa & 1) * 32));
-        const uint32_t nbq = (uint32_t)(mix64d(k2 + (uint64_t)(qb >> 1)) >> ((qb & 1) * 32));
-        const uint32_t ba = n3[qa] ^ na, bb = n3[qb] ^ nbq;   // child newest-frame bytes
+        const int g = t + it * kSibConv;
+        if (g >= 882) break;
+        const uint64_t h = mix64d(k2 + (uint64_t)g);
+        const uint2 pn = *(const uint2 *)(n3 + 2 * g);   // parent newest-frame bytes of both quads
+        const uint32_t b0 = pn.x ^ (uint32_t)h, b1 = pn.y ^ (uint32_t)(h >> 32);
 #if SIB_F16
-        const uint4 v = make_uint4(u8pair_f16x2(ba, 0x4140u), u8pair_f16x2(ba, 0x4342u), u8pair_f16x2(bb, 0x4140u),
-                                   u8pair_f16x2(bb, 0x4342u));
+        *(uint2 *)(nw + tdst[it][0]) = make_uint2(u8pair_f16x2(b0, 0x4140u), u8pair_f16x2(b0, 0x4342u));
+        *(uint2 *)(nw + tdst[it][1]) = make_uint2(u8pair_f16x2(b1, 0x4140u), u8pair_f16x2(b1, 0x4342u));
 #else
-        const uint4 v = make_uint4(u8pair_bf16x2(ba, 0), u8pair_bf16x2(ba, 2), u8pair_bf16x2(bb, 0), u8pair_bf16x2(bb, 2));
+        *(uint2 *)(nw + tdst[it][0]) = make_uint2(u8pair_bf16x2(b0, 0), u8pair_bf16x2(b0, 2));
+        *(uint2 *)(nw + tdst[it][1]) = make_uint2(u8pair_bf16x2(b1, 0), u8pair_bf16x2(b1, 2));
 #endif
-        *(uint4 *)(nw + tdst[it]) = v;
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(&n_full[nb]);
