@@ -622,7 +622,7 @@ constexpr float kSibScale = 1.0f;
 constexpr uint32_t kSibPlane = 536 * 16;            // rows 0..535 x 16 B
 constexpr uint32_t kSharedBytes = 6 * kSibPlane;    // 51,456
 constexpr uint32_t kNewBytes = 2 * kSibPlane;       // 17,152
-constexpr int kNewRing = 3;
+constexpr int kNewRing = 2;
 
 __global__ void __launch_bounds__(kSibThreads, 1)
     k_conv1_sib(ConvSW P, const uint8_t *__restrict__ Wsh, const uint8_t *__restrict__ Wnw,
@@ -639,7 +639,7 @@ __global__ void __launch_bounds__(kSibThreads, 1)
   uint8_t *sSh = sWnw + N * 128;                     // 2 x shared image
   uint8_t *sNw = sSh + 2 * kSharedBytes;             // kNewRing x new image
   uint32_t *sNew3 = (uint32_t *)(sNw + kNewRing * kNewBytes);   // 2 x parent newest-frame bytes (7056 B)
-  uint8_t *sStage = (uint8_t *)sNew3 + 2 * 7056;    // one child's act1 (2 x 100 rows x 128 B, global layout)
+  uint8_t *sStage0 = (uint8_t *)sNew3 + 2 * 7056;   // 2 x one child's act1 (2 x 100 rows x 128 B, global layout)
   __shared__ __align__(8) uint64_t sh_full[2], sh_empty[2], p_full[2], p_empty[2];
   __shared__ __align__(8) uint64_t n_full[kNewRing], n_empty[kNewRing], c_full[2], c_empty[2], wbar;
   __shared__ uint32_t tmem_slot;
@@ -749,6 +749,22 @@ __global__ void __launch_bounds__(kSibThreads, 1)
     const int c0 = ((warp - 1) >> 2) * HALF;
     const int r = q4 * 32 + lane;
     const uint32_t lanes = (uint32_t)(q4 * 32) << 16;
+    // staging offsets of this thread's 16-byte chunks, fixed for every child: output row
+    // q = mt*128 + r is pixel (q / 21, q % 21) of the full-width conv1 output; act1 is its
+    // s2d(2) image (row (oy/2)*10 + ox/2, sub-pixel (oy&1, ox&1)) in SW128 row blocks.
+    // ~0u marks the discarded full-width columns / padding rows.
+    uint32_t soff[4][2];
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+      const int q = mt * 128 + r, oy = q / 21, ox = q - oy * 21;
+      const int sub = ((oy & 1) << 1) | (ox & 1), row = (oy >> 1) * 10 + (ox >> 1);
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int chunk = sub * 4 + ((c0 + 8 * h2) >> 3);
+        soff[mt][h2] = (oy >= 20 || ox >= 20) ? ~0u
+                       : (uint32_t)((chunk >> 3) * kStageBlk + row * 128 + (((chunk & 7) ^ (row & 7)) << 4));
+      }
+    }
     uint32_t vp[4][16];
     int64_t cur_p = -1;
     uint32_t j = 0;
@@ -775,8 +791,9 @@ __global__ void __launch_bounds__(kSibThreads, 1)
       mbar_wait(&c_full[cb], cph);
       tc_fence_after();
       uint8_t *oimg = out + img * (int64_t)P.out_img_bytes;
-      // the staging buffer is free once the previous child's bulk store has read it
-      if (threadIdx.x == 32) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      // staging buffer j&1 is free once the bulk store of child j-2 has read it (<= 1 group pending)
+      uint8_t *sStage = sStage0 + (j & 1u) * (2 * kStageBlk);
+      if (threadIdx.x == 32) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
       epi_bar();
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {   // two tiles at a time (register budget)
@@ -793,9 +810,7 @@ __global__ void __launch_bounds__(kSibThreads, 1)
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
           const int mt = 2 * hf + u;
-          const int q = mt * 128 + r;
-          const int oy = q / 21, ox = q - oy * 21;
-          if (oy >= 20 || ox >= 20) continue;
+          if (soff[mt][0] == ~0u) continue;
           uint32_t pk[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) {   // relu(C * 2^-14 + Pb) -> bf16 (ReLU on the packed pair)
@@ -803,14 +818,9 @@ __global__ void __launch_bounds__(kSibThreads, 1)
             const float y = fmaf(__uint_as_float(vc[u][2 * e + 1]), kSibScale, __uint_as_float(vp[mt][2 * e + 1]));
             pk[e] = bf16x2_relu(x, y);
           }
-          const int sub = ((oy & 1) << 1) | (ox & 1);
-          const int row = (oy >> 1) * P.out_w + (ox >> 1);
 #pragma unroll
-          for (int h2 = 0; h2 < 2; ++h2) {   // into the staging image, in act1's global SW128 layout
-            const int chunk = sub * 4 + ((c0 + 8 * h2) >> 3);
-            *(uint4 *)(sStage + (chunk >> 3) * kStageBlk + row * 128 + (((chunk & 7) ^ (row & 7)) << 4)) =
-                make_uint4(pk[4 * h2], pk[4 * h2 + 1], pk[4 * h2 + 2], pk[4 * h2 + 3]);
-          }
+          for (int h2 = 0; h2 < 2; ++h2)   // into the staging image, in act1's global SW128 layout
+            *(uint4 *)(sStage + soff[mt][h2]) = make_uint4(pk[4 * h2], pk[4 * h2 + 1], pk[4 * h2 + 2], pk[4 * h2 + 3]);
         }
       }
       // whole image staged: the TMA engine writes the two row blocks to global (async)
@@ -983,7 +993,7 @@ void launch_conv1_sib(const ConvSW &P, const Layer &L, const uint8_t *wsh, const
                       cudaStream_t st) {
   if (n_img <= 0) return;
   constexpr int smem = 4 * 32 * 128 + 2 * (int)kSharedBytes + kNewRing * (int)kNewBytes + 2 * 7056 +
-                       2 * (int)kStageBlk + 1024;
+                       4 * (int)kStageBlk + 1024;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_conv1_sib, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
