@@ -99,14 +99,23 @@ __global__ void k_expand_int(NodeView par, int64_t p_first, int64_t c_begin, int
 constexpr int kExpandThreads = 256;
 constexpr int kGroups = kPix / 8;  // 882 groups of 8 pixel words (32 B)
 
+// split: CTAs per parent (each takes a contiguous slice of the parent's A children), so a
+// small level still spreads over every SM and no SM drains a long tail of whole parents.
 __global__ void __launch_bounds__(kExpandThreads) k_expand_atari(NodeView par, int64_t p_first, int64_t c_begin,
-                                                                   int64_t c_end, int A, float gk, NodeOut out) {
+                                                                   int64_t c_end, int A, float gk, NodeOut out,
+                                                                   int split) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint4 *sframe = (uint4 *)smem_raw;  // 1764 x 16 B
   __shared__ __align__(8) uint64_t bar;
-  const int64_t p = c_begin / A + blockIdx.x;
-  const int a_lo = (int)(max(c_begin, p * A) - p * A);
-  const int a_hi = (int)(min(c_end, (p + 1) * A) - p * A);
+  const unsigned us = (unsigned)split;
+  const int64_t p = c_begin / A + (int64_t)(blockIdx.x / us);
+  const int per = (A + split - 1) / split, s0 = (int)(blockIdx.x % us) * per;
+  const int64_t cfirst = p * (int64_t)A;                               // child index of action 0
+  const int64_t lo64 = c_begin > cfirst ? c_begin - cfirst : 0;        // this level call's children
+  const int64_t hi64 = c_end < cfirst + A ? c_end - cfirst : (int64_t)A;
+  const int a_lo = (int)(lo64 > (int64_t)s0 ? lo64 : (int64_t)s0);
+  const int a_hi = (int)(hi64 < (int64_t)(s0 + per) ? hi64 : (int64_t)(s0 + per));
+  if (a_lo >= a_hi) return;
   const int64_t pl = p - p_first;
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
@@ -168,8 +177,10 @@ void launch_expand(int env, const NodeView &par, int64_t p_first, int64_t c_begi
       cudaFuncSetAttribute(k_expand_atari, cudaFuncAttributeMaxDynamicSharedMemorySize, kFrameBytes);
       attr = true;
     }
-    k_expand_atari<<<(unsigned)nparents, kExpandThreads, kFrameBytes, st>>>(par, p_first, c_begin, c_end, A, gk,
-                                                                             out);
+    // about 4 CTAs per SM (8 fit by SMEM), at most one child per CTA
+    int split = (int)std::max<int64_t>(1, std::min<int64_t>(A, (4 * 148 + nparents - 1) / nparents));
+    k_expand_atari<<<(unsigned)(nparents * split), kExpandThreads, kFrameBytes, st>>>(par, p_first, c_begin, c_end, A, gk,
+                                                                             out, split);
   }
   if (prof) prof->end(st);
 }
