@@ -289,6 +289,161 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ============================================== fc GEMM with B multicast over a CTA pair
+// out[m][n] = act(A[m][:] . W[n][:] + b[n]) for the fc layers (2-D TMA A), persistent over
+// pair-tiles (M-tiles 2pm, 2pm+1) x (N-tile nt): the two CTAs of a cluster take the two
+// M-tiles and the SAME N-tile, so each weight k-block is fetched from L2 once and
+// TMA-multicast into both CTAs' shared memory (the fc GEMMs are L2-bandwidth bound on
+// re-reading W for every M-tile). MMAs stay cta_group::1. Slot reuse needs both CTAs'
+// consumers: each MMA commit is multicast to the empty barrier of both CTAs (count 2).
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_2d_mc(uint32_t dst, const CUtensorMap *map, int x, int y, uint64_t *bar,
+                                          uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(map), "r"(x), "r"(y), "r"(saddr(bar)), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void commit_mc_pred(uint64_t *bar, uint16_t mask, uint32_t issue) {
+  asm volatile(
+      "{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\n"
+      "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n}\n" ::
+          "r"(saddr(bar)),
+      "h"(mask), "r"(issue)
+      : "memory");
+}
+
+template <int BN, int KB>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_gemm_mc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, Layer L,
+              int64_t M, void *__restrict__ out, int n_pm, int n_n) {
+  using C = TmaCfg<BN, KB>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u);
+  __shared__ __align__(8) uint64_t full[C::STAGES], empty[C::STAGES], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_slot;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_rank();
+  const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int nk = L.K / KB;
+  const int n_tiles = n_pm * n_n;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 2);   // both CTAs' MMAs must release a slot (B lands in both)
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(&tmem_slot)),
+                 "r"(C::TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();          // barriers of both CTAs initialised before any multicast
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+  pdl_wait();
+  pdl_trigger();
+
+  if (warp == 0) {
+    if (lane == 0) {   // ------------------------------------------------ producer
+      uint32_t it = 0;
+      for (int tile = cl; tile < n_tiles; tile += ncl) {
+        const int pm = tile / n_n, nt = tile - pm * n_n;
+        const int m0 = (2 * pm + (int)rank) * kBM;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % C::STAGES;
+          mbar_wait(&empty[s], ((it / C::STAGES) & 1u) ^ 1u);
+          const uint32_t sa = saddr(smem + s * C::STAGE);
+          mbar_expect_tx(&full[s], C::STAGE);             // own A + the multicast B
+          tma_2d(sa, &mapA, kb * KB, m0, &full[s]);
+          if (rank == 0) tma_2d_mc(sa + C::A_BYTES, &mapB, kb * KB, nt * BN, &full[s], (uint16_t)3);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {   // ------------------------------------------ MMA issuer
+    const uint32_t elected = elect_one();
+    uint32_t it = 0, acc_it = 0;
+    for (int tile = cl; tile < n_tiles; tile += ncl, ++acc_it) {
+      const int nt = tile % n_n;
+      const int ntn = min(BN, L.Npad - nt * BN);
+      const uint32_t idesc = idesc_bf16(kBM, ntn);
+      const uint32_t a = acc_it & 1u, aph = (acc_it >> 1) & 1u;
+      mbar_wait(&tempty[a], aph ^ 1u);
+      tc_fence_after();
+      const uint32_t d = tmem + a * BN;
+      for (int kb = 0; kb < nk; ++kb, ++it) {
+        const int s = it % C::STAGES;
+        mbar_wait(&full[s], (it / C::STAGES) & 1u);
+        tc_fence_after();
+        const uint32_t a0 = saddr(smem + s * C::STAGE), b0 = a0 + C::A_BYTES;
+        const uint64_t ad = sdesc<KB>(a0), bd = sdesc<KB>(b0);
+#pragma unroll
+        for (int kk = 0; kk < KB / 16; ++kk)
+          mma_pred(d, ad + (uint64_t)(2 * kk), bd + (uint64_t)(2 * kk), idesc, (kb | kk) != 0, elected);
+        commit_mc_pred(&empty[s], (uint16_t)3, elected);   // release the slot in both CTAs
+      }
+      commit_pred(&tfull[a], elected);
+      __syncwarp();
+    }
+  } else {   // ---------------------------------------------------------- epilogue
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    uint32_t acc_it = 0;
+    for (int tile = cl; tile < n_tiles; tile += ncl, ++acc_it) {
+      const int pm = tile / n_n, nt = tile - pm * n_n;
+      const int64_t m = (int64_t)(2 * pm + (int)rank) * kBM + r;
+      const int n0 = nt * BN;
+      const int ntn = min(BN, L.Npad - n0);
+      const uint32_t a = acc_it & 1u, aph = (acc_it >> 1) & 1u;
+      mbar_wait(&tfull[a], aph);
+      tc_fence_after();
+      const uint32_t trow = tmem + a * BN + ((uint32_t)(q * 32) << 16);
+      for (int c = 0; c < ntn; c += 16) {
+        uint32_t v[16];
+        tmem_ld16(trow + (uint32_t)c, v);
+        if (m >= M) continue;
+        const float *bias = L.bias + n0 + c;
+        uint32_t pk[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float x = __uint_as_float(v[2 * i]) + __ldg(bias + 2 * i);
+          const float y = __uint_as_float(v[2 * i + 1]) + __ldg(bias + 2 * i + 1);
+          __nv_bfloat162 hh = __floats2bfloat162_rn(x > 0.0f ? x : 0.0f, y > 0.0f ? y : 0.0f);
+          pk[i] = *(uint32_t *)&hh;
+        }
+        uint4 *dst = (uint4 *)((__nv_bfloat16 *)out + m * L.out_ld + n0 + c);
+        dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[a]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TCOLS));
+  }
+  cluster_sync_all();          // no CTA leaves while its peer may still multicast into it
+}
+
 // =============================================================== fused Rainbow head
 // z_v, z_a and the dueling C51 head in ONE kernel (the 4-byte logits never reach
 // HBM). Per 128-leaf tile, jobs (each a K = 512 GEMM into a 256-column TMEM buffer):
@@ -529,8 +684,41 @@ int num_sms() {
   return n;
 }
 
+// fc layer with ReLU + bf16 output (fc_hidden): the B-multicast pair kernel
+template <int BN, int KB>
+bool launch_gemm_mc(const TmaPlan &P, const Layer &L, int64_t M, void *out, cudaStream_t st) {
+  using C = TmaCfg<BN, KB>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_gemm_mc<BN, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    attr = true;
+  }
+  const int n_m = (int)((M + kBM - 1) / kBM), n_pm = (n_m + 1) / 2, n_n = (L.Npad + BN - 1) / BN;
+  const int n_cl = std::min(n_pm * n_n, num_sms() / 2);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * n_cl);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[2];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = 2;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, k_gemm_mc<BN, KB>, *(const CUtensorMap *)P.mapA, *(const CUtensorMap *)P.mapB, L, M,
+                            out, n_pm, n_n) == cudaSuccess;
+}
+
 template <int BN, int KB>
 void launch_gemm(const TmaPlan &P, const Layer &L, int64_t M, void *out, cudaStream_t st) {
+  static const bool mc = !getenv("BCTS_NO_MULTICAST");
+  if (mc && !P.im2col && L.relu_bf16 && BN == 256 && L.Npad % BN == 0 && launch_gemm_mc<BN, KB>(P, L, M, out, st))
+    return;
+  cudaGetLastError();
   using C = TmaCfg<BN, KB>;
   static bool attr = false;
   if (!attr) {
