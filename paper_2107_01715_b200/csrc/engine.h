@@ -129,6 +129,13 @@ struct TmaPlan {
 };
 bool tma_plan(TmaPlan &P, const Layer &L, const void *in, int64_t cap_img);
 // Fused Rainbow head (qnet_tma.cu, k_zhead): z_v + z_a + dueling C51 + max_a in one kernel.
+// The head biases travel as a __grid_constant__ kernel parameter: every lane of a warp reads
+// the same (action, atom) bias, so they are broadcast constant-bank loads (no L1 latency).
+struct HeadBias {
+  float v[64];         // z_v bias (atoms)
+  float sum[64];       // sum over actions of the z_a bias
+  float a64[64 * 64];  // z_a bias, 64 slots per action
+};
 struct HeadPlan {
   bool ok = false;
   alignas(64) uint8_t mapAv[128];
@@ -136,12 +143,12 @@ struct HeadPlan {
   alignas(64) uint8_t mapBv[128];
   alignas(64) uint8_t mapBa[128];
   alignas(64) uint8_t mapBs[128];   // sum_a W_a as bf16 hi (rows 0..63) + lo (rows 64..127)
+  HeadBias bias;
 };
 bool head_plan(HeadPlan &H, const __nv_bfloat16 *hid, int64_t cap, const __nv_bfloat16 *wv64, const __nv_bfloat16 *wa64,
                const __nv_bfloat16 *wsum, int A);
-void launch_zhead(const HeadPlan &H, const float *bias_v, const float *bias_a64, const float *bias_sum, int A,
-                  int atoms, int64_t M, float vmin, float dz, int mode, float gd, const float *cum, float *out,
-                  cudaStream_t st);
+void launch_zhead(const HeadPlan &H, int A, int atoms, int64_t M, float vmin, float dz, int mode, float gd,
+                  const float *cum, float *out, cudaStream_t st);
 void launch_layer_tma(const TmaPlan &P, const Layer &L, int64_t n_img, void *out, cudaStream_t st);
 
 // Shifted-window conv layer (qnet_conv.cu): stride-1 conv over a per-image

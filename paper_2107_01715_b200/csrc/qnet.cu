@@ -514,6 +514,8 @@ int net_build(Net &net, const bcts_config &cfg, std::string &err) {
     V.H = V.W = 1; V.C = 512; V.K = 512; V.relu_bf16 = 0; V.out_ld = Nv; V.in_img_stride = 1024; V.in_col_off = 0;
     if (make_layer(net, V, repack(atoms, Nv, 1, 1, 512, [](int o, int, int, int c) { return o * 512 + c; }, w),
                    w + atoms * 512, atoms, Nv, err)) return -1;
+    if (atoms <= 64)
+      for (int t = 0; t < atoms; ++t) net.head.bias.v[t] = w[atoms * 512 + t];
     w += atoms * 512 + atoms;
     Layer &Z = net.z_a;
     const int Na = round_up(A * atoms, 16);
@@ -557,6 +559,10 @@ int net_build(Net &net, const bcts_config &cfg, std::string &err) {
       net.ba64 = (const float *)db;
       net.wsum = (const __nv_bfloat16 *)dws;
       net.bsum = (const float *)dbs;
+      if (A <= 64) {
+        for (int t = 0; t < 64; ++t) net.head.bias.sum[t] = bs[t];
+        for (size_t e = 0; e < ba64.size(); ++e) net.head.bias.a64[e] = ba64[e];
+      }
     }
     w += (int64_t)A * atoms * 512 + A * atoms;
     net.ld_zv = Nv;
@@ -637,7 +643,7 @@ int net_build(Net &net, const bcts_config &cfg, std::string &err) {
   if (rainbow) {
     tma_plan(net.p_z_v, net.z_v, net.hid_act, FB);
     tma_plan(net.p_z_a, net.z_a, net.hid_act, FB);
-    if (net.wa64 && net.atoms == 51 && !getenv("BCTS_NO_FUSED_HEAD"))
+    if (net.wa64 && net.atoms == 51 && A <= 64 && !getenv("BCTS_NO_FUSED_HEAD"))
       head_plan(net.head, net.hid_act, FB, net.z_v.Wt, net.wa64, net.wsum, A);
   } else {
     tma_plan(net.p_fc2, net.fc2, net.hid_act, FB);
@@ -737,7 +743,7 @@ static int eval_conv(Net &net, const NodeView *par, const NodeView *img, int64_t
     } else if (net.tc && net.head.ok) {   // z_v + z_a + dueling C51 head + max_a fused (k_zhead)
       const float dz = (net.vmax - net.vmin) / (float)(net.atoms - 1);
       if (net.prof) net.prof->begin(KC_FC_OUT, 2.0 * (double)nf * 512.0 * (double)(net.atoms + A * net.atoms), st);
-      launch_zhead(net.head, net.z_v.bias, net.ba64, net.bsum, A, net.atoms, nf, net.vmin, dz, mode, gd, cum, o, st);
+      launch_zhead(net.head, A, net.atoms, nf, net.vmin, dz, mode, gd, cum, o, st);
       if (net.prof) net.prof->end(st);
       launches += 1;
     } else {

@@ -481,8 +481,7 @@ template <int ATOMS>
 __global__ void __launch_bounds__(kThreads, 1)
     k_zhead(const __grid_constant__ CUtensorMap mapAv, const __grid_constant__ CUtensorMap mapAa,
             const __grid_constant__ CUtensorMap mapBv, const __grid_constant__ CUtensorMap mapBa,
-            const __grid_constant__ CUtensorMap mapBs, const float *__restrict__ bias_v,
-            const float *__restrict__ bias_a64, const float *__restrict__ bias_sum, int A, int64_t M, float vmin,
+            const __grid_constant__ CUtensorMap mapBs, const __grid_constant__ HeadBias hb, int A, int64_t M, float vmin,
             float dz, int mode, float gd, const float *__restrict__ cum, float *__restrict__ out) {
   static_assert(ATOMS <= 64, "one action per 64 TMEM columns");
   extern __shared__ uint8_t smem_raw[];
@@ -602,7 +601,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(&tempty[b]);
         ++job;
 #pragma unroll
-        for (int t = 0; t < ATOMS; ++t) v[t] = __uint_as_float(x[t]) + __ldg(bias_v + t);
+        for (int t = 0; t < ATOMS; ++t) v[t] = __uint_as_float(x[t]) + hb.v[t];
       }
       {   // job mean: v_t - mean_a adv[a][t]
         const uint32_t b = job & 1u;
@@ -613,7 +612,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(&tempty[b]);
         ++job;
 #pragma unroll
-        for (int t = 0; t < ATOMS; ++t) v[t] = v[t] - (__uint_as_float(x[t]) + __ldg(bias_sum + t)) / (float)A;
+        for (int t = 0; t < ATOMS; ++t) v[t] = v[t] - (__uint_as_float(x[t]) + hb.sum[t]) / (float)A;
       }
       float best = -INFINITY;
       for (int c = 0; c < nch; ++c, ++job) {   // softmax expectation per action
@@ -624,12 +623,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int s = 0; s < na; ++s) {
           tmem_ld64(tmem + b * 256 + lanes + (uint32_t)(s * 64), x);
           const int a = 4 * c + s;
-          const float *bb = bias_a64 + a * 64;
           float lg[ATOMS];
           float mx = -INFINITY;
 #pragma unroll
           for (int t = 0; t < ATOMS; ++t) {
-            lg[t] = v[t] + (__uint_as_float(x[t]) + __ldg(bb + t));
+            lg[t] = v[t] + (__uint_as_float(x[t]) + hb.a64[a * 64 + t]);
             mx = fmaxf(mx, lg[t]);
           }
           float den = 0.0f, num = 0.0f;
@@ -811,9 +809,8 @@ bool head_plan(HeadPlan &H, const __nv_bfloat16 *hid, int64_t cap, const __nv_bf
   return true;
 }
 
-void launch_zhead(const HeadPlan &H, const float *bias_v, const float *bias_a64, const float *bias_sum, int A,
-                  int atoms, int64_t M, float vmin, float dz, int mode, float gd, const float *cum, float *out,
-                  cudaStream_t st) {
+void launch_zhead(const HeadPlan &H, int A, int atoms, int64_t M, float vmin, float dz, int mode, float gd,
+                  const float *cum, float *out, cudaStream_t st) {
   if (M <= 0 || atoms != 51) return;
   static bool attr = false;
   if (!attr) {
@@ -824,7 +821,7 @@ void launch_zhead(const HeadPlan &H, const float *bias_v, const float *bias_a64,
   const int grid = std::min(n_m, num_sms());
   launch_pdl(k_zhead<51>, dim3(grid), dim3(kThreads), (size_t)kHeadSmem, st, *(const CUtensorMap *)H.mapAv,
              *(const CUtensorMap *)H.mapAa, *(const CUtensorMap *)H.mapBv, *(const CUtensorMap *)H.mapBa,
-             *(const CUtensorMap *)H.mapBs, bias_v, bias_a64, bias_sum, A, M, vmin, dz, mode, gd, cum, out);
+             *(const CUtensorMap *)H.mapBs, H.bias, A, M, vmin, dz, mode, gd, cum, out);
 }
 
 void launch_layer_tma(const TmaPlan &P, const Layer &L, int64_t n_img, void *out, cudaStream_t st) {
