@@ -457,6 +457,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // h_a (128 KB) stays resident in SMEM; h_v and the weight k-blocks stream through a
 // 3-stage ring. TMEM: two 256-column accumulators, alternating by job parity.
 constexpr int kHeadStages = 3, kHeadSlot = 32768, kHeadA = 8 * 16384;
+constexpr int kHeadThreads = 320;   // warp 0 TMA, warp 1 MMA, warps 2-9 epilogue (2 groups)
 constexpr int kHeadSmem = kHeadA + kHeadStages * kHeadSlot + 1024;
 
 __device__ __forceinline__ void tmem_ld32_nw(uint32_t taddr, uint32_t *r) {
@@ -478,7 +479,7 @@ __device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t (&r)[64]) {
 }
 
 template <int ATOMS>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kHeadThreads, 1)
     k_zhead(const __grid_constant__ CUtensorMap mapAv, const __grid_constant__ CUtensorMap mapAa,
             const __grid_constant__ CUtensorMap mapBv, const __grid_constant__ CUtensorMap mapBa,
             const __grid_constant__ CUtensorMap mapBs, const __grid_constant__ HeadBias hb, int A, int64_t M, float vmin,
@@ -489,6 +490,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t *sA = smem, *sRing = smem + kHeadA;
   __shared__ __align__(8) uint64_t full[kHeadStages], empty[kHeadStages], tfull[2], tempty[2], a_full, a_empty;
   __shared__ uint32_t tmem_slot;
+  __shared__ float s_best[2][kBM];                   // group 1's max_a, per tile parity
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
   const int n_m = (int)((M + kBM - 1) / kBM);
   const int nch = (A + 3) / 4;                       // z_a chunks of 4 actions (256 columns)
@@ -499,7 +501,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 128);
+      mbar_init(&tempty[i], 256);
     }
     mbar_init(&a_full, 1);
     mbar_init(&a_empty, 1);
@@ -583,12 +585,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       commit_pred(&a_empty, elected);   // sA free once this tile's MMAs have completed
       __syncwarp();
     }
-  } else {   // ---------------------------------------------------------- epilogue (128 threads = rows)
-    const int q = warp & 3;
+  } else {   // ------------------------------- epilogue: 2 groups x 4 warps (lane quarter q = rows)
+    // Both groups read v and the action mean; the softmax work is split by action parity
+    // (group g takes actions 4c + s with s % 2 == g) and max_a is combined through SMEM.
+    const int q = warp & 3, grp = (warp - 2) >> 2;
     const int r = q * 32 + lane;
     const uint32_t lanes = (uint32_t)(q * 32) << 16;
-    uint32_t job = 0;
-    for (int tile = blockIdx.x; tile < n_m; tile += gridDim.x) {
+    uint32_t job = 0, tl = 0;
+    for (int tile = blockIdx.x; tile < n_m; tile += gridDim.x, ++tl) {
       const int64_t m = (int64_t)tile * kBM + r;
       float v[ATOMS];
       uint32_t x[64];
@@ -620,20 +624,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&tfull[b], (job >> 1) & 1u);
         tc_fence_after();
         const int na = min(4, A - 4 * c);
-        for (int s = 0; s < na; ++s) {
+        for (int s = grp; s < na; s += 2) {
           tmem_ld64(tmem + b * 256 + lanes + (uint32_t)(s * 64), x);
           const int a = 4 * c + s;
-          float lg[ATOMS];
           float mx = -INFINITY;
 #pragma unroll
           for (int t = 0; t < ATOMS; ++t) {
-            lg[t] = v[t] + (__uint_as_float(x[t]) + hb.a64[a * 64 + t]);
-            mx = fmaxf(mx, lg[t]);
+            x[t] = __float_as_uint(v[t] + (__uint_as_float(x[t]) + hb.a64[a * 64 + t]));   // logit
+            mx = fmaxf(mx, __uint_as_float(x[t]));
           }
           float den = 0.0f, num = 0.0f;
 #pragma unroll
           for (int t = 0; t < ATOMS; ++t) {
-            const float ex = expf(lg[t] - mx);
+            const float ex = expf(__uint_as_float(x[t]) - mx);
             den += ex;
             num += (vmin + (float)t * dz) * ex;
           }
@@ -644,7 +647,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         mbar_arrive(&tempty[b]);
       }
-      if (mode != MODE_ROWS && m < M) out[m] = mode == MODE_ROWMAX ? best : fmaf(gd, best, cum ? cum[m] : 0.0f);
+      if (mode != MODE_ROWS) {   // max_a over both groups (max is order-independent)
+        if (grp == 1) s_best[tl & 1u][r] = best;
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (grp == 0 && m < M) {
+          best = fmaxf(best, s_best[tl & 1u][r]);
+          out[m] = mode == MODE_ROWMAX ? best : fmaf(gd, best, cum ? cum[m] : 0.0f);
+        }
+      }
     }
   }
   __syncthreads();
@@ -819,7 +829,7 @@ void launch_zhead(const HeadPlan &H, int A, int atoms, int64_t M, float vmin, fl
   }
   const int n_m = (int)((M + kBM - 1) / kBM);
   const int grid = std::min(n_m, num_sms());
-  launch_pdl(k_zhead<51>, dim3(grid), dim3(kThreads), (size_t)kHeadSmem, st, *(const CUtensorMap *)H.mapAv,
+  launch_pdl(k_zhead<51>, dim3(grid), dim3(kHeadThreads), (size_t)kHeadSmem, st, *(const CUtensorMap *)H.mapAv,
              *(const CUtensorMap *)H.mapAa, *(const CUtensorMap *)H.mapBv, *(const CUtensorMap *)H.mapBa,
              *(const CUtensorMap *)H.mapBs, H.bias, A, M, vmin, dz, mode, gd, cum, out);
 }
