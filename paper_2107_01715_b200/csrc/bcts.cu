@@ -680,8 +680,8 @@ bcts_status bcts_profile_enable(bcts_handle h, int32_t on) {
 int32_t bcts_profile_read(bcts_handle h, bcts_kernel_profile *out, int32_t max) {
   static const char *names[KC_COUNT] = {"expand_atari", "expand_int", "expand_tabular", "conv1", "conv2", "conv3",
                                         "fc_hidden", "fc_out", "head", "mlp", "table", "segmax", "finalize", "other",
-                                        "expand_dnn"};
-  static const int units[KC_COUNT] = {0, 0, 0, 1, 1, 1, 1, 1, 0, 1, 0, 0, 0, 0, 1};
+                                        "expand_dnn", "conv2+conv3"};
+  static const int units[KC_COUNT] = {0, 0, 0, 1, 1, 1, 1, 1, 0, 1, 0, 0, 0, 0, 1, 1};
   if (!h || !out || max <= 0) return 0;
   cudaSetDevice(h->dev);
   cudaStreamSynchronize(h->st);

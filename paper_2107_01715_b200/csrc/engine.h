@@ -13,7 +13,7 @@ namespace bcts {
 // DESIGN.md §5) so bench.py can report achieved = work / duration.
 enum KernelClass {
   KC_EXPAND_ATARI = 0, KC_EXPAND_INT, KC_EXPAND_TAB, KC_CONV1, KC_CONV2, KC_CONV3, KC_FC_H, KC_FC_OUT, KC_HEAD,
-  KC_MLP, KC_TABLE, KC_SEGMAX, KC_FINALIZE, KC_OTHER, KC_EXPAND_DNN, KC_COUNT
+  KC_MLP, KC_TABLE, KC_SEGMAX, KC_FINALIZE, KC_OTHER, KC_EXPAND_DNN, KC_CONV23, KC_COUNT
 };
 struct Profiler {
   bool on = false;
@@ -164,6 +164,9 @@ struct ConvSW {
   int in_rows = 0;                             // valid input rows per 64-channel block
 };
 void launch_conv_sw(const ConvSW &P, const Layer &L, const void *in, int64_t n_img, void *out, cudaStream_t st);
+// conv2 + conv3 in one kernel (act2 stays in SMEM): act1 planar in, dense act3 out
+void launch_conv23(const ConvSW &P2, const Layer &L2, const ConvSW &P3, const Layer &L3, const void *in, int64_t n_img,
+                   void *out, cudaStream_t st);
 void conv_trace_set(unsigned long long *p, int sel);
 // conv1, sibling-factorised (shared frames once per parent + new frame per child)
 void launch_conv1_sib(const ConvSW &P, const Layer &L, const uint8_t *wsh, const uint8_t *wnw, const NodeView &par,

@@ -670,6 +670,10 @@ static void run_layer(const Net &net, int cls, const Layer &L, const void *in, i
 // Conv-net evaluation over n images that come either from a view of frame
 // stacks (`img`, images [0, n)) or are the children [c_begin, c_begin + n) of
 // the parents in `par` (fused last-level expansion). Trunk in L2-sized
+static bool c23_enabled() {
+  static const bool on = !getenv("BCTS_NO_CONV23");
+  return on;
+}
 // sub-batches: frames -> s2d bf16 -> conv1 -> conv2 -> conv3 (act3 of the fc
 // batch); then fc_hidden, the output layer(s) and the head.
 static int eval_conv(Net &net, const NodeView *par, const NodeView *img, int64_t p_first, int64_t c_begin, float gk,
@@ -694,13 +698,20 @@ static int eval_conv(Net &net, const NodeView *par, const NodeView *img, int64_t
         launch_conv1_sib(net.sw1, net.c1, net.w1_shared, net.w1_new, *par, p_first, c_begin + f0 + b0, nb, A, gk,
                          net.act1p, net.leaf_cum + b0, st);
         if (net.prof) net.prof->end(st);
-        if (net.prof) net.prof->begin(KC_CONV2, fl * 81 * 64 * 512, st);
-        launch_conv_sw(net.sw2, net.c2s, net.act1p, nb, net.act2p, st);
-        if (net.prof) net.prof->end(st);
-        if (net.prof) net.prof->begin(KC_CONV3, fl * 49 * 64 * 576, st);
-        launch_conv_sw(net.sw3, net.c3, net.act2p, nb, net.act3 + b0 * 3136, st);
-        if (net.prof) net.prof->end(st);
-        launches += 3;
+        if (c23_enabled()) {   // conv2 + conv3 fused: act2 never leaves the SM
+          if (net.prof) net.prof->begin(KC_CONV23, fl * (81 * 64 * 512 + 49 * 64 * 576), st);
+          launch_conv23(net.sw2, net.c2s, net.sw3, net.c3, net.act1p, nb, net.act3 + b0 * 3136, st);
+          if (net.prof) net.prof->end(st);
+          launches += 2;
+        } else {
+          if (net.prof) net.prof->begin(KC_CONV2, fl * 81 * 64 * 512, st);
+          launch_conv_sw(net.sw2, net.c2s, net.act1p, nb, net.act2p, st);
+          if (net.prof) net.prof->end(st);
+          if (net.prof) net.prof->begin(KC_CONV3, fl * 49 * 64 * 576, st);
+          launch_conv_sw(net.sw3, net.c3, net.act2p, nb, net.act3 + b0 * 3136, st);
+          if (net.prof) net.prof->end(st);
+          launches += 3;
+        }
         continue;
       }
       if (par) {

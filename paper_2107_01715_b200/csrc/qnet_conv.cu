@@ -1090,6 +1090,228 @@ __global__ void __launch_bounds__(kC3tThreads, 1)
   }
 }
 
+// ------------------------------------------------ conv2 + conv3 fused (act2 stays on-chip)
+// Per image: conv2 (2x2/1 over act1's s2d(2) 10x10x128 -> 9x9x64; A = full-width image rows,
+// M = 128, B = weights, N = 64) then conv3 (3x3/1 over act2 9x9x64 -> 7x7x64, transposed:
+// A = weights M = 64, B = act2 row window N = 64). act2 is written by the conv2 epilogue
+// straight into a double-buffered SMEM image in conv3's SW128 layout and never touches
+// HBM (the separate kernels wrote and re-read 2 x 10 KB per leaf). The MMA warp alternates
+// conv2(i) and conv3(i-1) so the tensor core has work while either epilogue runs.
+// act1 lands in a compact ring (planes of 104 rows instead of act1's 144-row global planes).
+// Warps: 0 producer, 1 MMA, 2-9 conv2 epilogue (lane quarter x 32-channel half),
+// 10-13 conv3 epilogue (lane quarter; lanes 0-15 carry a channel).
+constexpr int kC23Threads = 448;
+constexpr uint32_t kC23Plane = 104 * 128;                 // compact act1 row block (rows 0..103)
+constexpr uint32_t kC23In = 2 * kC23Plane;                // 26,624 per act1 image
+constexpr uint32_t kC23A2 = 11 * 1024;                    // act2 image: 84 rows x 128 B, 1 KB aligned
+constexpr int kC23Smem = 8 * 64 * 128 + 9 * 64 * 128 + 2 * (int)kC23In + 2 * (int)kC23A2 + 2 * kC3tOutBytes + 1024;
+
+__global__ void __launch_bounds__(kC23Threads, 1)
+    k_conv23(ConvSW P2, ConvSW P3, const uint8_t *__restrict__ W2, const float *__restrict__ bias2,
+             const uint8_t *__restrict__ W3, const float *__restrict__ bias3, const uint8_t *__restrict__ in,
+             int64_t n_img, uint8_t *__restrict__ out) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u);
+  uint8_t *sW2 = smem;                                  // conv2 B: 8 k-blocks x [64 x 128 B]
+  uint8_t *sW3 = sW2 + 8 * 64 * 128;                    // conv3 A: 9 k-blocks x [64 x 128 B]
+  uint8_t *sIn = sW3 + 9 * 64 * 128;                    // 2 x act1 (compact planes)
+  uint8_t *sA2 = sIn + 2 * kC23In;                      // 2 x act2
+  uint8_t *sO3 = sA2 + 2 * kC23A2;                      // 2 x act3 staging [49][64] bf16
+  __shared__ __align__(8) uint64_t in_full[2], in_empty[2], t2full[2], t2empty[2], a2full[2], a2empty[2], t3full[2],
+      t3empty[2], wbar;
+  __shared__ uint32_t tmem_slot;
+  __shared__ float sb2[64], sb3[64];
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
+  if (threadIdx.x < 64) {
+    sb2[threadIdx.x] = bias2[threadIdx.x];
+    sb3[threadIdx.x] = bias3[threadIdx.x];
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&in_full[i], 1);
+      mbar_init(&in_empty[i], 1);
+      mbar_init(&t2full[i], 1);
+      mbar_init(&t2empty[i], 256);
+      mbar_init(&a2full[i], 256);
+      mbar_init(&a2empty[i], 1);
+      mbar_init(&t3full[i], 1);
+      mbar_init(&t3empty[i], 128);
+    }
+    mbar_init(&wbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(&wbar, (8u + 9u) * 64 * 128);
+    bulk_g2s(saddr(sW2), W2, 8u * 64 * 128, &wbar);
+    bulk_g2s(saddr(sW3), W3, 9u * 64 * 128, &wbar);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(&tmem_slot)),
+                 "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;   // cols [0,128): T2[2] (64 each); [128,256): T3[2]
+  pdl_wait();
+  pdl_trigger();
+  const int n_my = n_img > blockIdx.x ? (int)((n_img - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+
+  if (warp == 0) {
+    if (lane == 0) {   // ------------------------------------------------ producer (act1)
+      for (int li = 0; li < n_my; ++li) {
+        const int64_t img = blockIdx.x + (int64_t)li * gridDim.x;
+        const uint32_t b = li & 1, ph = (li >> 1) & 1u;
+        mbar_wait(&in_empty[b], ph ^ 1u);
+        mbar_expect_tx(&in_full[b], 2u * 12800u);
+        for (uint32_t q = 0; q < 2; ++q)
+          bulk_g2s(saddr(sIn + b * kC23In) + q * kC23Plane, in + img * (int64_t)P2.in_img_bytes + q * (P2.plane * 8u),
+                   12800u, &in_full[b]);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {   // ------------------------------------------ MMA issuer
+    constexpr uint32_t idesc2 = idesc_bf16(128, 64), idesc3 = idesc_bf16(64, 64);
+    const uint32_t elected = elect_one();
+    mbar_wait(&wbar, 0);
+    const uint64_t w2desc = desc_sw128(saddr(sW2)), w3desc = desc_sw128(saddr(sW3));
+    auto conv3 = [&](int jj) {
+      const uint32_t b = jj & 1, ph = (jj >> 1) & 1u;
+      mbar_wait(&a2full[b], ph);
+      mbar_wait(&t3empty[b], ph ^ 1u);
+      tc_fence_after();
+      const uint64_t xdesc = desc_sw128_win(saddr(sA2 + b * kC23A2), false);
+#pragma unroll
+      for (int tap = 0; tap < 9; ++tap)
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const uint32_t w_off = (uint32_t)tap * (64 * 128) + (uint32_t)(kk * 32);
+          const uint32_t x_off = (uint32_t)((tap / 3) * 9 + (tap % 3)) * 128u + (uint32_t)(kk * 32);
+          mma_pred(tmem + 128 + b * 64, w3desc + (w_off >> 4), xdesc + (x_off >> 4), idesc3, (tap | kk) != 0, elected);
+        }
+      commit_pred(&a2empty[b], elected);
+      commit_pred(&t3full[b], elected);
+    };
+    for (int li = 0; li < n_my; ++li) {
+      {   // conv2(li): 4 taps x 8 K-steps
+        const uint32_t b = li & 1, ph = (li >> 1) & 1u;
+        mbar_wait(&in_full[b], ph);
+        mbar_wait(&t2empty[b], ph ^ 1u);
+        tc_fence_after();
+        const uint64_t adesc0 = desc_sw128_win(saddr(sIn + b * kC23In), false);
+#pragma unroll
+        for (int tap = 0; tap < 4; ++tap)
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint32_t a_off = (uint32_t)(kk >> 2) * kC23Plane + (uint32_t)((tap >> 1) * 10 + (tap & 1)) * 128u +
+                                   (uint32_t)((kk & 3) * 32);
+            const int k = tap * 128 + 16 * kk;
+            const uint32_t w_off = (uint32_t)(k >> 6) * (64 * 128) + (uint32_t)((k & 63) * 2);
+            mma_pred(tmem + b * 64, adesc0 + (a_off >> 4), w2desc + (w_off >> 4), idesc2, (tap | kk) != 0, elected);
+          }
+        commit_pred(&in_empty[b], elected);
+        commit_pred(&t2full[b], elected);
+      }
+      if (li >= 1) conv3(li - 1);
+      __syncwarp();
+    }
+    if (n_my >= 1) conv3(n_my - 1);
+    __syncwarp();
+  } else if (warp < 10) {   // --------------------------- conv2 epilogue -> act2 in SMEM (SW128)
+    const int q4 = warp & 3, c0 = ((warp - 2) >> 2) * 32;
+    const int r = q4 * 32 + lane;                       // full-width output row: oy = r / 10, ox = r % 10
+    const int oy = r / 10, ox = r - oy * 10;
+    const bool valid = oy < 9 && ox < 9;
+    const int row = oy * 9 + ox;                        // act2 row
+    float bias_r[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) bias_r[c] = sb2[c0 + c];
+    for (int li = 0; li < n_my; ++li) {
+      const uint32_t b = li & 1, ph = (li >> 1) & 1u;
+      mbar_wait(&t2full[b], ph);
+      tc_fence_after();
+      uint32_t v[2][16];
+      const uint32_t tb = tmem + b * 64 + ((uint32_t)(q4 * 32) << 16) + (uint32_t)c0;
+      tmem_ld16_nw(tb, v[0]);
+      tmem_ld16_nw(tb + 16, v[1]);
+      tmem_wait16(v[0]);
+      tmem_wait16(v[1]);
+      tc_fence_before();
+      mbar_arrive(&t2empty[b]);
+      mbar_wait(&a2empty[b], ph ^ 1u);                  // conv3 of image li-2 is done with sA2[b]
+      if (valid) {
+        uint8_t *dst = sA2 + b * kC23A2 + row * 128;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint32_t pk[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            pk[e] = bf16x2_relu(__uint_as_float(v[h][2 * e]) + bias_r[h * 16 + 2 * e],
+                                __uint_as_float(v[h][2 * e + 1]) + bias_r[h * 16 + 2 * e + 1]);
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const int chunk = (c0 + h * 16 + 8 * h2) >> 3;
+            *(uint4 *)(dst + (((chunk & 7) ^ (row & 7)) << 4)) =
+                make_uint4(pk[4 * h2], pk[4 * h2 + 1], pk[4 * h2 + 2], pk[4 * h2 + 3]);
+          }
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&a2full[b]);
+    }
+  } else {   // --------------------------------------------------- conv3 epilogue -> act3 (dense)
+    const int q = warp & 3;
+    const int c = 16 * q + (lane & 15);
+    const float bc = sb3[c];
+    const uint32_t taddr0 = tmem + 128 + ((uint32_t)(q * 32) << 16);
+    const bool lead = threadIdx.x == 32 * 10;
+    for (int li = 0; li < n_my; ++li) {
+      const int64_t img = blockIdx.x + (int64_t)li * gridDim.x;
+      const uint32_t b = li & 1, ph = (li >> 1) & 1u;
+      mbar_wait(&t3full[b], ph);
+      tc_fence_after();
+      uint32_t v[64];
+      tmem_ld16_nw(taddr0 + b * 64 + 0, *(uint32_t(*)[16])(v + 0));
+      tmem_ld16_nw(taddr0 + b * 64 + 16, *(uint32_t(*)[16])(v + 16));
+      tmem_ld16_nw(taddr0 + b * 64 + 32, *(uint32_t(*)[16])(v + 32));
+      tmem_ld16_nw(taddr0 + b * 64 + 48, *(uint32_t(*)[16])(v + 48));
+      tmem_wait16(*(uint32_t(*)[16])(v + 0));
+      tmem_wait16(*(uint32_t(*)[16])(v + 16));
+      tmem_wait16(*(uint32_t(*)[16])(v + 32));
+      tmem_wait16(*(uint32_t(*)[16])(v + 48));
+      tc_fence_before();
+      mbar_arrive(&t3empty[b]);
+      uint8_t *so = sO3 + b * kC3tOutBytes;
+      if (lead) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (lane < 16) {
+#pragma unroll
+        for (int n = 0; n < 63; ++n) {
+          const int oy = n / 9, ox = n % 9;
+          if (oy < 7 && ox < 7) {
+            uint16_t h;
+            asm("cvt.rn.relu.bf16.f32 %0, %1;" : "=h"(h) : "f"(__uint_as_float(v[n]) + bc));
+            *(uint16_t *)(so + ((oy * 7 + ox) * 64 + c) * 2) = h;
+          }
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (lead) {
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + img * (int64_t)P3.out_img_bytes),
+                     "r"(saddr(so)), "r"(kC3tOutBytes)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    }
+    if (lead) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+  }
+}
+
 int num_sms() {
   static int n = 0;
   if (!n) {
@@ -1162,6 +1384,19 @@ void launch_conv3t(const ConvSW &P, const Layer &L, const void *in, int64_t n_im
   const int grid = (int)std::min<int64_t>(n_img, num_sms());
   launch_pdl(k_conv3t, dim3(grid), dim3(kC3tThreads), (size_t)smem, st, P, P.wsw, L.bias, (const uint8_t *)in, n_img,
              (uint8_t *)out);
+}
+
+void launch_conv23(const ConvSW &P2, const Layer &L2, const ConvSW &P3, const Layer &L3, const void *in, int64_t n_img,
+                   void *out, cudaStream_t st) {
+  if (n_img <= 0) return;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_conv23, cudaFuncAttributeMaxDynamicSharedMemorySize, kC23Smem);
+    attr = true;
+  }
+  const int grid = (int)std::min<int64_t>(n_img, num_sms());
+  launch_pdl(k_conv23, dim3(grid), dim3(kC23Threads), (size_t)kC23Smem, st, P2, P3, P2.wsw, L2.bias, P3.wsw, L3.bias,
+             (const uint8_t *)in, n_img, (uint8_t *)out);
 }
 
 void launch_conv_sw(const ConvSW &P, const Layer &L, const void *in, int64_t n_img, void *out, cudaStream_t st) {
