@@ -126,6 +126,8 @@ struct TmaPlan {
   int im2col = 0, kb = 64, bn = 64;
   alignas(64) uint8_t mapA[128];
   alignas(64) uint8_t mapB[128];
+  bool ok2sm = false;               // mapB2: B with 128-row boxes (2-SM MMA, half an N tile per CTA)
+  alignas(64) uint8_t mapB2[128];
 };
 bool tma_plan(TmaPlan &P, const Layer &L, const void *in, int64_t cap_img);
 // Fused Rainbow head (qnet_tma.cu, k_zhead): z_v + z_a + dueling C51 + max_a in one kernel.

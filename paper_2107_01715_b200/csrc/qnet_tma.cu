@@ -444,6 +444,177 @@ __global__ void __launch_bounds__(kThreads, 1)
   cluster_sync_all();          // no CTA leaves while its peer may still multicast into it
 }
 
+// =========================================== fc GEMM on a CTA pair with the 2-SM MMA
+// tcgen05.mma.cta_group::2, M = 256 (128 rows per CTA) x N = 256 (B split along N: CTA r holds
+// weight rows nt*256 + 128r .. +127), issued by the leader (cluster rank 0); each CTA's TMEM
+// receives its own 128 rows x all 256 columns (semantics checked in tools/mma2sm_test.cu).
+// Per SM a k-block brings A 16 KB + B 16 KB instead of 16 + 32 KB: the fc GEMM is bound by
+// per-SM operand ingest, which this halves for B. Cross-CTA signalling: both CTAs' TMA loads
+// (the .cta_group::2 form) complete on the LEADER's full barrier, armed by the leader with both
+// halves' bytes; the leader's commits multicast to both CTAs' empty / tfull barriers; the
+// peer's epilogue threads arrive remotely on the leader's tempty barrier. (A first version that
+// forwarded the peer's fills through its idle MMA warp ran 2.5x slower: that hop sat on the
+// critical path of every stage.)
+constexpr int k2smStages = 6, k2smStage = 32768;
+constexpr int k2smSmem = k2smStages * k2smStage + 1024;
+__device__ __forceinline__ uint32_t mapa_rank0(uint32_t local_saddr) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(local_saddr));
+  return r;
+}
+// 2-D TMA load into this CTA's smem whose completion is counted on a barrier of the CTA pair
+// (here: the leader's), the .cta_group::2 form (SASS UTMALDG.2D.2CTA)
+__device__ __forceinline__ void tma_2d_2cta(uint32_t dst, const CUtensorMap *map, int x, int y, uint32_t bar_cluster) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(map), "r"(x), "r"(y), "r"(bar_cluster)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_gemm_2sm(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, Layer L,
+               int64_t M, void *__restrict__ out, int n_pm, int n_n) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u);
+  __shared__ __align__(8) uint64_t full[k2smStages], empty[k2smStages], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_slot;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_rank();
+  const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int nk = L.K / 64;
+  const int n_tiles = n_pm * n_n;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < k2smStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 256);   // both CTAs' epilogue threads (leader's barrier is the one used)
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(&tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+  pdl_wait();
+  pdl_trigger();
+
+  if (warp == 0) {
+    if (lane == 0) {   // -------------------- producer: own halves, completing on the LEADER's barrier
+      uint32_t it = 0;
+      const uint32_t full0 = mapa_rank0(saddr(&full[0]));
+      for (int tile = cl; tile < n_tiles; tile += ncl) {
+        const int pm = tile / n_n, nt = tile - pm * n_n;
+        const int m0 = pm * 256 + (int)rank * kBM, n0 = nt * 256 + (int)rank * 128;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % k2smStages;
+          mbar_wait(&empty[s], ((it / k2smStages) & 1u) ^ 1u);
+          const uint32_t sa = saddr(smem + s * k2smStage);
+          if (rank == 0) mbar_expect_tx(&full[s], 2 * k2smStage);   // both CTAs' bytes land on this barrier
+          tma_2d_2cta(sa, &mapA, kb * 64, m0, full0 + (uint32_t)s * 8u);
+          tma_2d_2cta(sa + 16384, &mapB, kb * 64, n0, full0 + (uint32_t)s * 8u);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (rank == 0) {   // --------------------------------------------- MMA issuer (leader)
+      const uint32_t elected = elect_one();
+      const uint32_t idesc = idesc_bf16(256, 256);
+      uint32_t it = 0, acc_it = 0;
+      for (int tile = cl; tile < n_tiles; tile += ncl, ++acc_it) {
+        const uint32_t a = acc_it & 1u, aph = (acc_it >> 1) & 1u;
+        mbar_wait(&tempty[a], aph ^ 1u);
+        tc_fence_after();
+        const uint32_t d = tmem + a * 256;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % k2smStages;
+          const uint32_t ph = (it / k2smStages) & 1u;
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t a0 = saddr(smem + s * k2smStage), b0 = a0 + 16384;
+          const uint64_t ad = sdesc<64>(a0), bd = sdesc<64>(b0);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            asm volatile(
+                "{\n.reg .pred p, q;\nsetp.ne.b32 p, %4, 0;\nsetp.ne.b32 q, %5, 0;\n"
+                "@q tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+                "l"(ad + (uint64_t)(2 * kk)), "l"(bd + (uint64_t)(2 * kk)), "r"(idesc), "r"((kb | kk) != 0 ? 1u : 0u),
+                "r"(elected));
+          }
+          asm volatile(
+              "{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\n"
+              "@q tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n}\n" ::
+                  "r"(saddr(&empty[s])),
+              "h"((uint16_t)3), "r"(elected)
+              : "memory");
+        }
+        asm volatile(
+            "{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\n"
+            "@q tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n}\n" ::
+                "r"(saddr(&tfull[a])),
+            "h"((uint16_t)3), "r"(elected)
+            : "memory");
+        __syncwarp();
+      }
+    }
+    __syncwarp();
+  } else {   // ---------------------------------------------------------- epilogue (own 128 rows)
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const uint32_t tempty0 = mapa_rank0(saddr(&tempty[0]));
+    uint32_t acc_it = 0;
+    for (int tile = cl; tile < n_tiles; tile += ncl, ++acc_it) {
+      const int pm = tile / n_n, nt = tile - pm * n_n;
+      const int64_t m = (int64_t)pm * 256 + (int64_t)rank * kBM + r;
+      const int n0 = nt * 256;
+      const uint32_t a = acc_it & 1u, aph = (acc_it >> 1) & 1u;
+      mbar_wait(&tfull[a], aph);
+      tc_fence_after();
+      const uint32_t trow = tmem + a * 256 + ((uint32_t)(q * 32) << 16);
+      for (int c = 0; c < 256; c += 16) {
+        uint32_t v[16];
+        tmem_ld16(trow + (uint32_t)c, v);
+        if (m >= M) continue;
+        const float *bias = L.bias + n0 + c;
+        uint32_t pk[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float x = __uint_as_float(v[2 * i]) + __ldg(bias + 2 * i);
+          const float y = __uint_as_float(v[2 * i + 1]) + __ldg(bias + 2 * i + 1);
+          __nv_bfloat162 hh = __floats2bfloat162_rn(x > 0.0f ? x : 0.0f, y > 0.0f ? y : 0.0f);
+          pk[i] = *(uint32_t *)&hh;
+        }
+        uint4 *dst = (uint4 *)((__nv_bfloat16 *)out + m * L.out_ld + n0 + c);
+        dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      }
+      tc_fence_before();
+      mbar_arrive_remote(tempty0 + a * 8u);   // the leader's accumulator may be reused
+    }
+  }
+  __syncthreads();
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
 // =============================================================== fused Rainbow head
 // z_v, z_a and the dueling C51 head in ONE kernel (the 4-byte logits never reach
 // HBM). Per 128-leaf tile, jobs (each a K = 512 GEMM into a 256-column TMEM buffer):
@@ -721,8 +892,41 @@ bool launch_gemm_mc(const TmaPlan &P, const Layer &L, int64_t M, void *out, cuda
                             out, n_pm, n_n) == cudaSuccess;
 }
 
+// fc layer (ReLU + bf16) on CTA pairs with the 2-SM MMA; needs B tensor map boxes of 128 rows
+bool launch_gemm_2sm(const TmaPlan &P, const Layer &L, int64_t M, void *out, cudaStream_t st) {
+  if (!P.ok2sm) return false;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_gemm_2sm, cudaFuncAttributeMaxDynamicSharedMemorySize, k2smSmem);
+    attr = true;
+  }
+  const int n_m = (int)((M + kBM - 1) / kBM), n_pm = (n_m + 1) / 2, n_n = L.Npad / 256;
+  const int n_cl = std::min(n_pm * n_n, num_sms() / 2);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * n_cl);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = k2smSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[2];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = 2;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, k_gemm_2sm, *(const CUtensorMap *)P.mapA, *(const CUtensorMap *)P.mapB2, L, M, out,
+                            n_pm, n_n) == cudaSuccess;
+}
+
 template <int BN, int KB>
 void launch_gemm(const TmaPlan &P, const Layer &L, int64_t M, void *out, cudaStream_t st) {
+  static const bool two_sm = !getenv("BCTS_NO_2SM");
+  if (two_sm && !P.im2col && L.relu_bf16 && BN == 256 && KB == 64 && L.Npad % 256 == 0 &&
+      launch_gemm_2sm(P, L, M, out, st))
+    return;
+  cudaGetLastError();
   static const bool mc = !getenv("BCTS_NO_MULTICAST");
   if (mc && !P.im2col && L.relu_bf16 && BN == 256 && L.Npad % BN == 0 && launch_gemm_mc<BN, KB>(P, L, M, out, st))
     return;
@@ -790,6 +994,14 @@ bool tma_plan(TmaPlan &P, const Layer &L, const void *in, int64_t cap_img) {
     r = g_encode_tiled(mb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<__nv_bfloat16 *>(L.Wt), dims, strides, box,
                        estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    P.ok2sm = false;
+    if (r == CUDA_SUCCESS && !conv && KB == 64 && L.Npad % 256 == 0) {   // 2-SM GEMM: half-tile B boxes
+      cuuint32_t box2[2] = {(cuuint32_t)KB, 128u};
+      P.ok2sm = g_encode_tiled((CUtensorMap *)P.mapB2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                               const_cast<__nv_bfloat16 *>(L.Wt), dims, strides, box2, estr,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
   }
   if (r != CUDA_SUCCESS) return false;
   P.ok = true;
