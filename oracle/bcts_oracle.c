@@ -877,3 +877,170 @@ int oracle_leaf_total(const oracle_model *m, const void *root_rec, int depth, in
   free(s);
   return rc;
 }
+
+/* ------------------------------------------------ early pruning (NEXT-4) */
+/* Early pruning with an index array of unpruned states ("future work";
+ * DESIGN.md R30-R33). Alg. 1 run level by level over explicit node
+ * lists; every node carries its implicit index f in the UNPRUNED tree below its
+ * root (base-A digits = the action path, R1), so the root action of a node is
+ * its leading digit and the best leaf is traced through f ("These indices
+ * are then used for tracing the optimal action at the root"). After level k is
+ * expanded, for k in [first, d-1], one rule thins it within each group
+ * (root, root action a_0) = f / A^(k-1):
+ *   rule 1 (BOUND, exact; R31): with one-step rewards in [r_lo, r_hi] and leaf
+ *     values max_a Q in [q_lo, q_hi], every leaf below node i totals within
+ *     [R_i + L_k, R_i + U_k], L_k = sum_{j=k}^{d-1} g[j] r_lo + g[d] q_lo (U_k with
+ *     the _hi ends). Node i is pruned iff R_i + U_k + s_i < max over its group of
+ *     (R_j + L_k - s_j), s = 2^-16 (|R| + S_k) a rounding margin, S_k the same
+ *     sum over max(|lo|, |hi|). Such a node holds no leaf that can reach its
+ *     group's max, so the search result is unchanged (only work is saved).
+ *   rule 2 (BEAM; R32): keep the `beam` nodes of each group with the highest
+ *     depth-k estimate v_i = R_i + g[k] max_a Q(s_i, a) (the "estimated value
+ *     over all the tree nodes" of P:299), ties to the lower f.
+ * Leaves (level d) are never pruned. survivors[k] (nullable) = nodes kept at
+ * level k summed over roots (survivors[0] = n_roots, survivors[d] = leaves scored). Other outputs as
+ * oracle_search. The bound arithmetic is plain double, the discounts g[j]
+ * rounded to fp32 in mode 1 (the values the search itself uses). */
+typedef struct {
+  ostate s;
+  double R;
+  int64_t f;
+} pnode;
+
+static void prune_bounds(const double *g, int k, int d, double r_lo, double r_hi, double q_lo, double q_hi,
+                         double *L, double *U, double *S) {
+  double l = 0.0, u = 0.0, sa = 0.0;
+  const double ra = fabs(r_lo) > fabs(r_hi) ? fabs(r_lo) : fabs(r_hi);
+  const double qa = fabs(q_lo) > fabs(q_hi) ? fabs(q_lo) : fabs(q_hi);
+  for (int j = k; j < d; ++j) {
+    l = l + g[j] * r_lo;
+    u = u + g[j] * r_hi;
+    sa = sa + g[j] * ra;
+  }
+  *L = l + g[d] * q_lo;
+  *U = u + g[d] * q_hi;
+  *S = sa + g[d] * qa;
+}
+
+int oracle_search_pruned(const oracle_model *m, const void *roots, long n_roots, int depth, double gamma,
+                         double beta, int corr, int mode, int rule, int first, long beam, double r_lo,
+                         double r_hi, double q_lo, double q_hi, int32_t *actions, double *root_q,
+                         double *vanilla_q, double *terms_out, int64_t *best_leaf, int64_t *survivors) {
+  const int A = m->A;
+  if (depth < 1 || depth > MAXD || n_roots < 0 || rule < 0 || rule > 2) return -1;
+  if (rule == 2 && beam < 1) return -1;
+  if (rule == 1 && !(r_lo <= r_hi && q_lo <= q_hi)) return -1;
+  if (first < 1) first = 1;
+  const long rb = oracle_record_bytes(m);
+  double g[MAXD + 1], gu[MAXD + 1];
+  discounts(gamma, depth, g);
+  for (int k = 0; k <= depth; ++k) gu[k] = mode ? (double)(float)g[k] : g[k];
+  if (survivors) {
+    for (int k = 0; k <= depth; ++k) survivors[k] = 0;
+    survivors[0] = n_roots;
+  }
+  int64_t span = 1;                       /* A^(d-1) leaves per root action */
+  for (int k = 1; k < depth; ++k) span *= A;
+  int rc = 0;
+  for (long r = 0; r < n_roots && !rc; ++r) {
+    pnode *cur = (pnode *)malloc(sizeof(pnode));
+    long ncur = 1;
+    from_record(m, (const uint8_t *)roots + r * rb, &cur[0].s);
+    cur[0].R = 0.0;
+    cur[0].f = 0;
+    double van[MAXA], q[MAXA];
+    int64_t bl[MAXA];
+    for (int a = 0; a < A; ++a) { van[a] = -INFINITY; bl[a] = 0; }
+    for (int k = 1; k <= depth && !rc; ++k) {
+      if (k == depth) {                   /* leaves: R_d + g[d] max_a Q, max per root action */
+        ostate *leaf = (ostate *)malloc(sizeof(ostate));
+        if (survivors) survivors[depth] += ncur * A;
+        for (long i = 0; i < ncur && !rc; ++i)
+          for (int a = 0; a < A && !rc; ++a) {
+            double rr;
+            rc = env_step(m, &cur[i].s, a, leaf, &rr, mode);
+            if (!rc) rc = qrow(m, leaf, mode, q);
+            if (rc) break;
+            const double tot = leaf_total(mode, g, depth, rowmax(q, A), acc_reward(mode, g, k - 1, rr, cur[i].R));
+            const int64_t f = cur[i].f * A + a;
+            const int a0 = (int)(f / span);
+            if (tot > van[a0] || (tot == van[a0] && f < bl[a0])) { van[a0] = tot; bl[a0] = f; }
+          }
+        free(leaf);
+        break;
+      }
+      /* expand: children of node i in action order (Alg. 1) */
+      pnode *nxt = (pnode *)malloc(sizeof(pnode) * (size_t)(ncur * A));
+      long nn = 0;
+      for (long i = 0; i < ncur && !rc; ++i)
+        for (int a = 0; a < A && !rc; ++a) {
+          double rr;
+          rc = env_step(m, &cur[i].s, a, &nxt[nn].s, &rr, mode);
+          nxt[nn].R = acc_reward(mode, g, k - 1, rr, cur[i].R);
+          nxt[nn].f = cur[i].f * A + a;
+          ++nn;
+        }
+      free(cur);
+      cur = nxt;
+      ncur = nn;
+      if (rc) break;
+      if (rule != 0 && k >= first && k <= depth - 1) {
+        int64_t gsz = 1;                  /* A^(k-1) level-k nodes per root action */
+        for (int j = 1; j < k; ++j) gsz *= A;
+        char *keep = (char *)calloc((size_t)ncur, 1);
+        if (rule == 1) {
+          double L, U, S, best[MAXA];
+          prune_bounds(gu, k, depth, r_lo, r_hi, q_lo, q_hi, &L, &U, &S);
+          for (int a = 0; a < A; ++a) best[a] = -INFINITY;
+          for (long i = 0; i < ncur; ++i) {
+            const double s = ldexp(fabs(cur[i].R) + S, -16);
+            const double lb = (cur[i].R + L) - s;
+            const int a0 = (int)(cur[i].f / gsz);
+            if (lb > best[a0]) best[a0] = lb;
+          }
+          for (long i = 0; i < ncur; ++i) {
+            const double s = ldexp(fabs(cur[i].R) + S, -16);
+            const double ub = (cur[i].R + U) + s;
+            keep[i] = !(ub < best[cur[i].f / gsz]);
+          }
+        } else {
+          double *v = (double *)malloc(sizeof(double) * (size_t)ncur);
+          for (long i = 0; i < ncur && !rc; ++i) {
+            rc = qrow(m, &cur[i].s, mode, q);
+            v[i] = leaf_total(mode, g, k, rowmax(q, A), cur[i].R);   /* depth-k estimate */
+          }
+          for (long i = 0; i < ncur; ++i) {   /* rank within the group: better = higher v, then lower f */
+            long rank = 0;
+            for (long j = 0; j < ncur; ++j)
+              if (j != i && cur[j].f / gsz == cur[i].f / gsz &&
+                  (v[j] > v[i] || (v[j] == v[i] && cur[j].f < cur[i].f)))
+                ++rank;
+            keep[i] = rank < beam;
+          }
+          free(v);
+        }
+        long w = 0;
+        for (long i = 0; i < ncur; ++i)
+          if (keep[i]) cur[w++] = cur[i];
+        ncur = w;
+        free(keep);
+      }
+      if (survivors) survivors[k] += ncur;
+    }
+    free(cur);
+    if (rc) break;
+    ostate *root = (ostate *)malloc(sizeof(ostate));
+    from_record(m, (const uint8_t *)roots + r * rb, root);
+    double q0[MAXA], terms[4] = {0, 0, 0, 0}, qq[MAXA];
+    if (corr) rc = bcts_terms(m, root, depth, mode, g, terms, q0, corr);
+    free(root);
+    if (rc) break;
+    apply_correction(A, depth, mode, g, beta, corr, van, terms, qq);
+    actions[r] = argmax_low(qq, A);
+    for (int a = 0; a < A; ++a) root_q[r * A + a] = qq[a];
+    if (vanilla_q) for (int a = 0; a < A; ++a) vanilla_q[r * A + a] = van[a];
+    if (terms_out) for (int k = 0; k < 4; ++k) terms_out[r * 4 + k] = terms[k];
+    if (best_leaf) for (int a = 0; a < A; ++a) best_leaf[r * A + a] = bl[a];
+  }
+  return rc ? -1 : 0;
+}

@@ -69,6 +69,9 @@ def _load():
             lib.oracle_set_env_weights.restype = I
             lib.oracle_set_env_weights.argtypes = [P, P, L]
             lib.oracle_max_threads.restype = I
+            lib.oracle_search_pruned.restype = I
+            lib.oracle_search_pruned.argtypes = [P, P, L, I, D, D, I, I, I, I, L, D, D, D, D,
+                                                 P, P, P, P, P, P]
             _lib = lib
     return _lib
 
@@ -192,6 +195,27 @@ class Oracle:
             raise ValueError("oracle search failed (domain error)")
         return {"actions": act, "root_q": rq.reshape(n, A), "vanilla_q": van.reshape(n, A),
                 "terms": terms.reshape(n, 4), "best_leaf": bl.reshape(n, A)}
+
+    def search_pruned(self, roots, depth: int, gamma: float, rule: int, first: int = 1, beam: int = 1,
+                      r_lo: float = 0.0, r_hi: float = 0.0, q_lo: float = 0.0, q_hi: float = 0.0,
+                      beta: float = 1.0, correction: int = 1, mode: int = 0) -> dict:
+        """Early-pruned search (rule 0 none, 1 BOUND, 2 BEAM; see bcts_oracle.c)."""
+        recs = self._records(roots)
+        n = recs.shape[0]
+        A = self.A
+        act = np.zeros(n, np.int32)
+        rq = np.zeros(n * A, np.float64)
+        van = np.zeros(n * A, np.float64)
+        terms = np.zeros(n * 4, np.float64)
+        bl = np.zeros(n * A, np.int64)
+        surv = np.zeros(depth + 1, np.int64)
+        rc = _load().oracle_search_pruned(self._h, _ptr(recs), n, depth, gamma, beta, correction, mode, rule,
+                                          first, beam, r_lo, r_hi, q_lo, q_hi, _ptr(act), _ptr(rq), _ptr(van),
+                                          _ptr(terms), _ptr(bl), _ptr(surv))
+        if rc:
+            raise ValueError("oracle_search_pruned failed")
+        return {"actions": act, "root_q": rq.reshape(n, A), "vanilla_q": van.reshape(n, A),
+                "terms": terms.reshape(n, 4), "best_leaf": bl.reshape(n, A), "survivors": surv}
 
     def leaf_total(self, root_rec, depth: int, index: int, gamma: float, mode: int = 0) -> float:
         rec = self._records(root_rec)[0]
