@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define BCTS_ABI_VERSION 2   /* 2: env_weights fields + BCTS_ENV_DNN */
+#define BCTS_ABI_VERSION 3   /* 2: env_weights fields + BCTS_ENV_DNN; 3: bcts_search_pruned */
 
 typedef struct bcts_handle_t *bcts_handle;
 
@@ -211,6 +211,50 @@ bcts_status bcts_finalize(bcts_handle h, const void *roots, int64_t n_roots, int
 bcts_status bcts_pv_targets(bcts_handle h, int64_t n_roots, int32_t depth, const int32_t *actions,
                             const float *vanilla_q, const int64_t *best_leaf, float *target_out,
                             int32_t *path_out);
+
+/* ---- early pruning (NEXT-4; "future work"; R30-R33) ----
+ * "Efficient pruning can be done by maintaining an index array of
+ * unpruned states which are updated with each pruning step. These indices are
+ * then used for tracing the optimal action at the root." bcts_search_pruned
+ * runs Alg. 1 level by level; after expanding level k, for k in
+ * [first_level, depth-1], a rule thins the level inside each group
+ * (root, root action) and the survivors are compacted (stream compaction of
+ * their states + the index array: each node's index f in the UNPRUNED tree,
+ * whose base-A digits are its action path). Leaves are never pruned.
+ *   BCTS_PRUNE_BOUND (exact, R31): with every one-step reward in [r_lo, r_hi]
+ *     and every leaf value max_a Q_hat in [q_lo, q_hi], node i at level k is
+ *     dropped iff R_i + U_k + s_i < max over its group of (R_j + L_k - s_j),
+ *     L_k = sum_{j=k}^{d-1} gamma^j r_lo + gamma^d q_lo (U_k: the _hi ends),
+ *     s = 2^-16 (|R| + S_k) a rounding margin. Outputs are then bit-identical
+ *     to bcts_search_ex when the bounds hold (C51 nets: q in [v_min, v_max]).
+ *   BCTS_PRUNE_BEAM (approximate, R32): keep the `beam` nodes of each group
+ *     with the highest depth-k estimate fmaf(gamma^k, max_a Q_hat(s, a), R),
+ *     ties to the lower f; costs one Q_hat evaluation per node of each
+ *     pruned level.
+ * Outputs as bcts_search_ex (best_leaf keeps its unpruned meaning).
+ * survivors_out: HOST int64 [depth+1] (nullable): nodes kept per level over
+ * all roots (survivors[0] = n_roots, survivors[depth] = leaves scored).
+ * Synchronizes the stream once per pruned level (the survivor count sizes the
+ * next level). Roots are processed in chunks sized for the worst case
+ * (BOUND: no pruning) within workspace_bytes_max.
+ * Errors: INVALID_ARG (null prune, unknown rule, beam < 1 for BEAM, r_lo >
+ * r_hi or q_lo > q_hi or non-finite bounds for BOUND, depth < 1, plus those of
+ * bcts_search_ex), BUDGET, CUDA. */
+#define BCTS_PRUNE_NONE 0
+#define BCTS_PRUNE_BOUND 1
+#define BCTS_PRUNE_BEAM 2
+typedef struct {
+  int32_t rule;         /* BCTS_PRUNE_* */
+  int32_t first_level;  /* first level pruned (values < 1 read as 1) */
+  int64_t beam;         /* BEAM: nodes kept per (root, root action) group and level */
+  float r_lo, r_hi;     /* BOUND: one-step reward bounds */
+  float q_lo, q_hi;     /* BOUND: leaf-value (max_a Q_hat) bounds */
+} bcts_prune;
+bcts_status bcts_search_pruned(bcts_handle h, const void *roots, int64_t n_roots, int32_t depth, int32_t A,
+                               float gamma, float beta, int32_t correction_on, const bcts_prune *prune,
+                               int32_t *actions_out, float *root_q_out, float *vanilla_q_out,
+                               float *terms_out, int64_t *best_leaf_out, int64_t *survivors_out,
+                               bcts_stats *stats);
 
 /* ---- inspection entry points (same kernels as the search) -------------
  * bcts_expand: expand n_roots roots to level `level` (Alg. 1 loop body,

@@ -16,7 +16,8 @@ LIB_PATH = os.path.join(_HERE, "libbcts.so")
 ENV_TABULAR, ENV_INT_HASH, ENV_ATARI_HASH, ENV_DNN = 1, 2, 3, 4
 NET_TABLE, NET_MLP2_F32, NET_NATURE_BF16, NET_RAINBOW_BF16 = 1, 2, 3, 4
 F_CLAMP_PENALTY, F_SIMT_NET, F_MATERIALIZE_LEAVES = 0x1, 0x2, 0x4
-ABI_VERSION = 2
+ABI_VERSION = 3
+PRUNE_NONE, PRUNE_BOUND, PRUNE_BEAM = 0, 1, 2
 STATUS = {0: "BCTS_OK", 1: "BCTS_ERR_INVALID_ARG", 2: "BCTS_ERR_UNSUPPORTED", 3: "BCTS_ERR_OUT_OF_MEMORY",
           4: "BCTS_ERR_BUDGET", 5: "BCTS_ERR_CUDA", 7: "BCTS_ERR_NUMERIC"}
 RECORD_BYTES = {ENV_TABULAR: 4, ENV_INT_HASH: 64, ENV_ATARI_HASH: 28240, ENV_DNN: 400}
@@ -26,7 +27,7 @@ EXPORTS = ["bcts_create", "bcts_destroy", "bcts_abi_version", "bcts_root_record_
            "bcts_last_error", "bcts_search", "bcts_search_ex", "bcts_search_host", "bcts_keys_init",
            "bcts_search_shard", "bcts_finalize", "bcts_expand", "bcts_q_rows", "bcts_pack_key",
            "bcts_key_value", "bcts_key_leaf", "bcts_shard_range", "bcts_profile_enable", "bcts_profile_read",
-           "bcts_pv_targets"]
+           "bcts_pv_targets", "bcts_search_pruned"]
 
 
 class BctsError(RuntimeError):
@@ -48,6 +49,11 @@ class Config(C.Structure):
 class KernelProfile(C.Structure):
     _fields_ = [("name", C.c_char * 32), ("launches", C.c_int64), ("ms", C.c_double), ("work", C.c_double),
                 ("unit", C.c_int32)]
+
+
+class Prune(C.Structure):
+    _fields_ = [("rule", C.c_int32), ("first_level", C.c_int32), ("beam", C.c_int64), ("r_lo", C.c_float),
+                ("r_hi", C.c_float), ("q_lo", C.c_float), ("q_hi", C.c_float)]
 
 
 class Stats(C.Structure):
@@ -91,6 +97,8 @@ def lib():
             "bcts_profile_enable": ([P, I32], I32),
             "bcts_profile_read": ([P, C.POINTER(KernelProfile), I32], I32),
             "bcts_pv_targets": ([P, I64, I32, P, P, P, P, P], I32),
+            "bcts_search_pruned": ([P, P, I64, I32, I32, F, F, I32, C.POINTER(Prune), P, P, P, P, P, P,
+                                    C.POINTER(Stats)], I32),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -219,6 +227,23 @@ class Handle:
                                  _p(out["actions"]), _p(out["root_q"]), _p(out.get("vanilla_q")),
                                  _p(out.get("terms")), _p(out.get("best_leaf")), C.byref(st))
         self._check(s, "bcts_search_ex")
+        out["stats"] = st.as_dict()
+        return out
+
+    def search_pruned(self, roots, n_roots: int, depth: int, gamma: float, rule: int, first_level: int = 1,
+                      beam: int = 1, r_lo: float = 0.0, r_hi: float = 0.0, q_lo: float = 0.0, q_hi: float = 0.0,
+                      beta: float = 1.0, correction: int = 1):
+        """Early-pruned search (NEXT-4, include/bcts.h bcts_search_pruned). Returns device outputs
+        (actions, root_q, vanilla_q, terms, best_leaf), 'survivors' (numpy [depth+1]) and 'stats'."""
+        out = self._outputs(n_roots, True)
+        pr = Prune(rule, first_level, beam, r_lo, r_hi, q_lo, q_hi)
+        surv = np.zeros(depth + 1, np.int64)
+        st = Stats()
+        s = lib().bcts_search_pruned(self._h, _p(roots), n_roots, depth, self.A, gamma, beta, correction,
+                                     C.byref(pr), _p(out["actions"]), _p(out["root_q"]), _p(out["vanilla_q"]),
+                                     _p(out["terms"]), _p(out["best_leaf"]), _p(surv), C.byref(st))
+        self._check(s, "bcts_search_pruned")
+        out["survivors"] = surv
         out["stats"] = st.as_dict()
         return out
 

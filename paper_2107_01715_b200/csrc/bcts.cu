@@ -352,6 +352,173 @@ bcts_status finalize_impl(bcts_handle h, const void *roots, int64_t n, int32_t d
   return cuda_check(h, "finalize");
 }
 
+// ------------------------------------------------------------ early pruning
+// NEXT-4 (R30-R33). Per-root worst-case level sizes: E[k] nodes after expanding
+// level k, K[k] after its rule (BOUND: nothing pruned in the worst case; BEAM: min(beam, E/A)
+// per root action). Levels 1..dm are materialised (dm = d-1 when the net generates the leaves).
+struct PruneShape {
+  int64_t E[kMaxDepth + 1], K[kMaxDepth + 1];
+  int64_t capE = 0, leaves = 0;
+};
+bool prune_level(const bcts_prune &p, int k, int d) { return p.rule != BCTS_PRUNE_NONE && k >= p.first_level && k <= d - 1; }
+PruneShape prune_shape(const bcts_prune &p, int A, int d, int dm) {
+  PruneShape s;
+  s.K[0] = s.E[0] = 1;
+  for (int k = 1; k <= d; ++k) {
+    s.E[k] = s.K[k - 1] * A;
+    s.K[k] = s.E[k];
+    if (prune_level(p, k, d) && p.rule == BCTS_PRUNE_BEAM) s.K[k] = A * std::min<int64_t>(p.beam, s.E[k] / A);
+    if (k <= dm) s.capE = std::max(s.capE, s.E[k]);
+  }
+  s.leaves = s.E[d];
+  return s;
+}
+// Bytes per root of one chunk: level buffers X, Y (capE each), f arrays (max(capE, leaves) each),
+// flags + selection + scores (capE), totals (leaves), group maxima (A).
+size_t pruned_bytes_per_root(bcts_handle h, const PruneShape &s) {
+  const int64_t capF = std::max(s.capE, s.leaves);
+  return (size_t)(2 * s.capE * node_bytes(h->env) + 2 * capF * 8 + s.capE * (1 + 8 + 4) + s.leaves * 4 + h->A * 8);
+}
+// L_k, U_k, S_k of R31 in the oracle's operation order (plain double, x86-64 host: no FMA).
+void prune_bounds(const float *g, int k, int d, const bcts_prune &p, double *L, double *U, double *S) {
+  double l = 0.0, u = 0.0, sa = 0.0;
+  const double ra = std::max(fabs((double)p.r_lo), fabs((double)p.r_hi));
+  const double qa = std::max(fabs((double)p.q_lo), fabs((double)p.q_hi));
+  for (int j = k; j < d; ++j) {
+    volatile double t1 = (double)g[j] * (double)p.r_lo, t2 = (double)g[j] * (double)p.r_hi, t3 = (double)g[j] * ra;
+    l = l + t1;
+    u = u + t2;
+    sa = sa + t3;
+  }
+  volatile double t1 = (double)g[d] * (double)p.q_lo, t2 = (double)g[d] * (double)p.q_hi, t3 = (double)g[d] * qa;
+  *L = l + t1;
+  *U = u + t2;
+  *S = sa + t3;
+}
+
+bcts_status run_pruned(bcts_handle h, const void *roots, int64_t n, int32_t d, float gamma, const bcts_prune &p,
+                       int64_t *keys, size_t reserved, int64_t *surv, bcts_stats *stats) {
+  const int A = h->A;
+  const bool fused = fused_leaves(h);
+  const int dm = fused ? d - 1 : d;
+  const PruneShape sh = prune_shape(p, A, d, dm);
+  float g[kMaxDepth + 1];
+  discounts(gamma, d, g);
+  int64_t pw[kMaxDepth + 1];
+  pw[0] = 1;
+  for (int k = 1; k <= d; ++k) pw[k] = pw[k - 1] * A;
+  const size_t per_root = pruned_bytes_per_root(h, sh);
+  const int64_t budget = h->ws_max - (int64_t)reserved - (8 << 20);
+  int64_t per = budget > 0 ? (int64_t)((double)budget / (double)per_root) : 0;
+  per = std::min<int64_t>(per, n);
+  if (per < 1) return fail(h, BCTS_ERR_BUDGET, "workspace budget too small for one root of the pruned search");
+  const int64_t capE = sh.capE * per, capF = std::max(sh.capE, sh.leaves) * per, capL = sh.leaves * per;
+  Carver c(h->ws + reserved);
+  LevelBuf X = c.level(h->env, std::max<int64_t>(capE, 1)), Y = c.level(h->env, std::max<int64_t>(capE, 1));
+  int64_t *fX = (int64_t *)c.take((size_t)capF * 8), *fY = (int64_t *)c.take((size_t)capF * 8);
+  uint8_t *keep = (uint8_t *)c.take((size_t)capE);
+  int64_t *sel = (int64_t *)c.take((size_t)capE * 8);
+  float *score = (float *)c.take((size_t)capE * 4);
+  float *totals = (float *)c.take((size_t)capL * 4);
+  unsigned long long *gmax = (unsigned long long *)c.take((size_t)per * A * 8);
+  int64_t *d_count = (int64_t *)c.take(8);
+  const size_t tbytes = compact_temp_bytes(std::max<int64_t>(capE, 1));
+  void *temp = c.take(tbytes);
+  if (reserved + c.off > h->ws_size) return fail(h, BCTS_ERR_BUDGET, "workspace not sized for the pruned search");
+  const int64_t sb = state_bytes(h->env);
+  int64_t trans = 0, evaluated = 0, leaves = 0, chunks = 0, lvl_launch = 0;
+  bcts_status s = BCTS_OK;
+  for (int64_t r0 = 0; r0 < n; r0 += per) {
+    const int64_t nr = std::min(per, n - r0);
+    // current level: view + index array; starts at the chunk's roots (f = global root index)
+    NodeView cur = root_view(h->env, roots, r0);
+    int64_t ncur = nr;
+    int64_t *fcur = fY;
+    launch_prune_iota(fcur, r0, nr, h->st);
+    int inbuf = -1;   // -1: roots, 0: X, 1: Y
+    h->launches += 1;
+    for (int k = 1; k <= dm; ++k) {
+      LevelBuf &dst = inbuf == 0 ? Y : X;
+      int64_t *fdst = inbuf == 0 ? fY : fX;
+      if (fdst == fcur) fdst = (fcur == fX) ? fY : fX;
+      const int64_t ne = ncur * A;
+      launch_expand(h->env, cur, 0, 0, ne, A, g[k - 1], h->em, out_of(h->env, dst), h->st, &h->prof);
+      launch_child_index(fcur, ne, A, fdst, h->st);
+      h->launches += 2;
+      trans += ne;
+      ++lvl_launch;
+      NodeView exp = view_of(h->env, dst);
+      if (!prune_level(p, k, d)) {
+        cur = exp;
+        fcur = fdst;
+        ncur = ne;
+        inbuf = (&dst == &X) ? 0 : 1;
+        continue;
+      }
+      if (p.rule == BCTS_PRUNE_BOUND) {
+        BoundRule b;
+        prune_bounds(g, k, d, p, &b.L, &b.U, &b.S);
+        b.gsz = pw[k - 1];
+        b.g0 = r0 * A;
+        b.groups = nr * A;
+        launch_bound_keep(exp.cum, fdst, ne, b, gmax, keep, h->st, &h->prof);
+        h->launches += 2;
+      } else {
+        const int nl = net_eval(h->net, exp, ne, MODE_ROWMAX, 0.0f, score, h->st);
+        if (nl < 0) return fail(h, BCTS_ERR_CUDA, "net_eval (beam scores)");
+        evaluated += ne;
+        // every group of this level holds the same number of nodes: ne / (nr * A)
+        launch_beam_keep(score, exp.cum, g[k], ne, ne / (nr * A), p.beam, keep, h->st, &h->prof);
+        h->launches += nl + 1;
+      }
+      launch_compact(keep, ne, sel, d_count, temp, tbytes, h->st);
+      int64_t kept = 0;
+      cudaMemcpyAsync(&kept, d_count, 8, cudaMemcpyDeviceToHost, h->st);
+      if (cudaStreamSynchronize(h->st) != cudaSuccess || (s = cuda_check(h, "prune compaction"))) return s ? s : BCTS_ERR_CUDA;
+      if (kept < 1 || kept > ne) return fail(h, BCTS_ERR_NUMERIC, "prune: survivor count out of range");
+      // survivors go to the other buffer (the parents' buffer is free once they are expanded)
+      LevelBuf &cmp = (&dst == &X) ? Y : X;
+      int64_t *fcmp = (fdst == fX) ? fY : fX;
+      launch_gather_level(sb, exp, fdst, sel, kept, out_of(h->env, cmp), fcmp, h->st, &h->prof);
+      h->launches += 3;
+      cur = view_of(h->env, cmp);
+      fcur = fcmp;
+      ncur = kept;
+      inbuf = (&cmp == &X) ? 0 : 1;
+      if (surv) surv[k] += kept;
+    }
+    // leaves
+    const int64_t nleaf = fused ? ncur * A : ncur;
+    int64_t *fleaf = fcur;
+    int nl;
+    if (fused) {
+      fleaf = (fcur == fX) ? fY : fX;
+      launch_child_index(fcur, nleaf, A, fleaf, h->st);
+      nl = net_eval_children(h->net, cur, 0, 0, nleaf, A, g[d - 1], MODE_TOTAL, g[d], totals, h->st);
+      trans += nleaf;
+      h->launches += 1;
+    } else {
+      nl = net_eval(h->net, cur, nleaf, MODE_TOTAL, g[d], totals, h->st);
+    }
+    if (nl < 0) return fail(h, BCTS_ERR_CUDA, "net_eval (leaves)");
+    launch_segmax_f(totals, fleaf, nleaf, pw[d], pw[d - 1], keys, h->st, &h->prof);
+    h->launches += nl + 1;
+    evaluated += nleaf;
+    leaves += nleaf;
+    ++chunks;
+    if ((s = cuda_check(h, "pruned chunk"))) return s;
+  }
+  if (stats) {
+    stats->transitions += trans;
+    stats->leaves += leaves;
+    stats->evaluated += evaluated;
+    stats->chunks += chunks;
+    stats->level_launches += lvl_launch;
+  }
+  if (surv) surv[d] = leaves;
+  return BCTS_OK;
+}
+
 }  // namespace
 
 // =================================================================== C ABI
@@ -555,6 +722,64 @@ bcts_status bcts_search_ex(bcts_handle h, const void *roots, int64_t n_roots, in
   return s;
 }
 
+bcts_status bcts_search_pruned(bcts_handle h, const void *roots, int64_t n_roots, int32_t depth, int32_t A,
+                               float gamma, float beta, int32_t correction_on, const bcts_prune *prune,
+                               int32_t *actions_out, float *root_q_out, float *vanilla_q_out, float *terms_out,
+                               int64_t *best_leaf_out, int64_t *survivors_out, bcts_stats *stats) {
+  bcts_status s = validate(h, roots, n_roots, depth, A, gamma);
+  if (s) return s;
+  if (!prune) return fail(h, BCTS_ERR_INVALID_ARG, "prune is NULL");
+  if (depth < 1) return fail(h, BCTS_ERR_INVALID_ARG, "pruned search needs depth >= 1");
+  bcts_prune p = *prune;
+  if (p.rule < BCTS_PRUNE_NONE || p.rule > BCTS_PRUNE_BEAM) return fail(h, BCTS_ERR_INVALID_ARG, "unknown prune rule");
+  if (p.rule == BCTS_PRUNE_BEAM && p.beam < 1) return fail(h, BCTS_ERR_INVALID_ARG, "beam must be >= 1");
+  if (p.rule == BCTS_PRUNE_BOUND &&
+      (!isfinite(p.r_lo) || !isfinite(p.r_hi) || !isfinite(p.q_lo) || !isfinite(p.q_hi) || p.r_lo > p.r_hi ||
+       p.q_lo > p.q_hi))
+    return fail(h, BCTS_ERR_INVALID_ARG, "BOUND needs finite r_lo <= r_hi and q_lo <= q_hi");
+  if (p.first_level < 1) p.first_level = 1;
+  if (!isfinite(beta) || beta < 0.0f) return fail(h, BCTS_ERR_INVALID_ARG, "beta must be finite and >= 0");
+  if (correction_on < 0 || correction_on > 2) return fail(h, BCTS_ERR_INVALID_ARG, "correction_on not in {0,1,2}");
+  if (n_roots > 0 && (!actions_out || !root_q_out)) return fail(h, BCTS_ERR_INVALID_ARG, "NULL output pointer");
+  if (stats) memset(stats, 0, sizeof(*stats));
+  if (survivors_out) {
+    for (int k = 0; k <= depth; ++k) survivors_out[k] = 0;
+    survivors_out[0] = n_roots;
+  }
+  if (n_roots == 0) return BCTS_OK;
+  cudaSetDevice(h->dev);
+  const int64_t l0 = h->launches;
+  const size_t kbytes = align_up((size_t)n_roots * A * 8);
+  const bool fused = fused_leaves(h);
+  const PruneShape sh = prune_shape(p, A, depth, fused ? depth - 1 : depth);
+  const size_t per_root = pruned_bytes_per_root(h, sh);
+  const int64_t budget = h->ws_max - (int64_t)kbytes - (8 << 20);
+  const int64_t per = budget > 0 ? std::min<int64_t>(n_roots, (int64_t)((double)budget / (double)per_root)) : 0;
+  if (per < 1) return fail(h, BCTS_ERR_BUDGET, "workspace budget too small for one root of the pruned search");
+  const size_t need = std::max(finalize_ws(h, n_roots, kbytes),
+                               (size_t)per * per_root + compact_temp_bytes(sh.capE * per) + (4 << 20));
+  if ((s = ensure_ws(h, kbytes + need))) return s;
+  int64_t *keys = (int64_t *)h->ws;
+  launch_keys_init(keys, n_roots * A, h->st);
+  h->launches += 1;
+  // pruned levels accumulate their survivors over the root chunks; unpruned levels are A x the level above
+  int64_t surv[kMaxDepth + 1] = {0};
+  s = run_pruned(h, roots, n_roots, depth, gamma, p, keys, kbytes, surv, stats);
+  if (s) return s;
+  if (survivors_out) {
+    int64_t cnt = n_roots;
+    for (int k = 1; k < depth; ++k) {
+      cnt = prune_level(p, k, depth) ? surv[k] : cnt * A;
+      survivors_out[k] = cnt;
+    }
+    survivors_out[depth] = surv[depth];
+  }
+  Outs o{actions_out, root_q_out, vanilla_q_out, terms_out, best_leaf_out};
+  s = finalize_impl(h, roots, n_roots, depth, gamma, beta, correction_on, keys, o, kbytes, stats);
+  if (stats) stats->kernel_launches = h->launches - l0;
+  return s;
+}
+
 bcts_status bcts_search(bcts_handle h, const void *roots, int64_t n_roots, int32_t depth, int32_t A, float gamma,
                         float beta, int32_t correction_on, int32_t *actions_out, float *root_q_out) {
   return bcts_search_ex(h, roots, n_roots, depth, A, gamma, beta, correction_on, actions_out, root_q_out, nullptr,
@@ -680,8 +905,8 @@ bcts_status bcts_profile_enable(bcts_handle h, int32_t on) {
 int32_t bcts_profile_read(bcts_handle h, bcts_kernel_profile *out, int32_t max) {
   static const char *names[KC_COUNT] = {"expand_atari", "expand_int", "expand_tabular", "conv1", "conv2", "conv3",
                                         "fc_hidden", "fc_out", "head", "mlp", "table", "segmax", "finalize", "other",
-                                        "expand_dnn", "conv2+conv3"};
-  static const int units[KC_COUNT] = {0, 0, 0, 1, 1, 1, 1, 1, 0, 1, 0, 0, 0, 0, 1, 1};
+                                        "expand_dnn", "conv2+conv3", "prune"};
+  static const int units[KC_COUNT] = {0, 0, 0, 1, 1, 1, 1, 1, 0, 1, 0, 0, 0, 0, 1, 1, 0};
   if (!h || !out || max <= 0) return 0;
   cudaSetDevice(h->dev);
   cudaStreamSynchronize(h->st);

@@ -13,7 +13,7 @@ namespace bcts {
 // DESIGN.md §5) so bench.py can report achieved = work / duration.
 enum KernelClass {
   KC_EXPAND_ATARI = 0, KC_EXPAND_INT, KC_EXPAND_TAB, KC_CONV1, KC_CONV2, KC_CONV3, KC_FC_H, KC_FC_OUT, KC_HEAD,
-  KC_MLP, KC_TABLE, KC_SEGMAX, KC_FINALIZE, KC_OTHER, KC_EXPAND_DNN, KC_CONV23, KC_COUNT
+  KC_MLP, KC_TABLE, KC_SEGMAX, KC_FINALIZE, KC_OTHER, KC_EXPAND_DNN, KC_CONV23, KC_PRUNE, KC_COUNT
 };
 struct Profiler {
   bool on = false;
@@ -275,5 +275,26 @@ struct FinalizeArgs {
 void launch_finalize(const FinalizeArgs &a, cudaStream_t st, Profiler *prof = nullptr);
 void launch_pv_targets(int64_t n, int A, int d, const int32_t *actions, const float *vanilla,
                        const int64_t *best_leaf, float *target, int32_t *path, cudaStream_t st);
+
+// ------------------------------------------------- early pruning (prune.cu, NEXT-4)
+// f = index of a node in the unpruned tree (global over the call's roots): the index array.
+void launch_prune_iota(int64_t *f, int64_t first, int64_t n, cudaStream_t st);
+void launch_child_index(const int64_t *pf, int64_t n_child, int A, int64_t *cf, cudaStream_t st);
+struct BoundRule {            // R31; L, U, S computed on the host in the oracle's order
+  double L = 0, U = 0, S = 0;
+  int64_t gsz = 1;            // level-k nodes per (root, root action) group in the unpruned tree: A^(k-1)
+  int64_t g0 = 0, groups = 0; // first group of the chunk, groups in the chunk
+};
+void launch_bound_keep(const float *cum, const int64_t *f, int64_t n, const BoundRule &b, unsigned long long *gmax,
+                       uint8_t *keep, cudaStream_t st, Profiler *prof);
+void launch_beam_keep(const float *m, const float *cum, float gk, int64_t n, int64_t G, int64_t beam, uint8_t *keep,
+                      cudaStream_t st, Profiler *prof);
+size_t compact_temp_bytes(int64_t n);
+void launch_compact(const uint8_t *keep, int64_t n, int64_t *sel, int64_t *d_count, void *temp, size_t temp_bytes,
+                    cudaStream_t st);
+void launch_gather_level(int64_t state_bytes, const NodeView &src, const int64_t *f, const int64_t *sel, int64_t n_out,
+                         const NodeOut &dst, int64_t *f_out, cudaStream_t st, Profiler *prof);
+void launch_segmax_f(const float *totals, const int64_t *f, int64_t n, int64_t lpr, int64_t seg, int64_t *keys,
+                     cudaStream_t st, Profiler *prof);
 
 }  // namespace bcts

@@ -727,12 +727,19 @@ static int eval_conv(Net &net, const NodeView *par, const NodeView *img, int64_t
         if (net.prof) net.prof->begin(KC_CONV1, fl * 400 * 32 * 256, st);
         launch_conv_sw(net.sw1, net.c1, net.in1p, nb, net.act1p, st);
         if (net.prof) net.prof->end(st);
-        if (net.prof) net.prof->begin(KC_CONV2, fl * 81 * 64 * 512, st);
-        launch_conv_sw(net.sw2, net.c2s, net.act1p, nb, net.act2p, st);
-        if (net.prof) net.prof->end(st);
-        if (net.prof) net.prof->begin(KC_CONV3, fl * 49 * 64 * 576, st);
-        launch_conv_sw(net.sw3, net.c3, net.act2p, nb, net.act3 + b0 * 3136, st);
-        if (net.prof) net.prof->end(st);
+        if (c23_enabled()) {
+          if (net.prof) net.prof->begin(KC_CONV23, fl * (81 * 64 * 512 + 49 * 64 * 576), st);
+          launch_conv23(net.sw2, net.c2s, net.sw3, net.c3, net.act1p, nb, net.act3 + b0 * 3136, st);
+          if (net.prof) net.prof->end(st);
+          launches -= 1;
+        } else {
+          if (net.prof) net.prof->begin(KC_CONV2, fl * 81 * 64 * 512, st);
+          launch_conv_sw(net.sw2, net.c2s, net.act1p, nb, net.act2p, st);
+          if (net.prof) net.prof->end(st);
+          if (net.prof) net.prof->begin(KC_CONV3, fl * 49 * 64 * 576, st);
+          launch_conv_sw(net.sw3, net.c3, net.act2p, nb, net.act3 + b0 * 3136, st);
+          if (net.prof) net.prof->end(st);
+        }
       } else {
         run_layer(net, KC_CONV1, net.c1, net.s2d, nb, net.act1, st, &net.p_c1);
         run_layer(net, KC_CONV2, net.c2, net.act1, nb, net.act2, st, &net.p_c2);

@@ -41,13 +41,14 @@ def test_exports_every_declared_symbol(L):
     assert lib.bcts_abi_version() == ver == L.bcts.ABI_VERSION
 
 
-@pytest.mark.parametrize("struct", ["Config", "Stats", "KernelProfile"])
+@pytest.mark.parametrize("struct", ["Config", "Stats", "KernelProfile", "Prune"])
 def test_ctypes_structs_match_c_layout(L, struct, tmp_path):
     """The binding's ctypes mirrors of bcts_config / bcts_stats / bcts_kernel_profile have the C
     compiler's size and field offsets (gcc on include/bcts.h)."""
     import ctypes
     import subprocess
-    cname = {"Config": "bcts_config", "Stats": "bcts_stats", "KernelProfile": "bcts_kernel_profile"}[struct]
+    cname = {"Config": "bcts_config", "Stats": "bcts_stats", "KernelProfile": "bcts_kernel_profile",
+             "Prune": "bcts_prune"}[struct]
     py = getattr(L.bcts, struct)
     lines = [f'printf("size %zu\\n", sizeof({cname}));']
     lines += [f'printf("{f} %zu\\n", offsetof({cname}, {f}));' for f, _ in py._fields_]
