@@ -220,6 +220,7 @@ struct Net {
   // scratch: trunk sub-batches of `batch` images (conv activations stay
   // L2-resident), fc layers over `fc_batch` images at a time
   int64_t batch = 0, fc_batch = 0;
+  int64_t mat_batch = 0;          // trunk sub-batch of the materialised-state path (s2d input buffer)
   TmaPlan p_c1, p_c2, p_c3, p_fc_h, p_z_v, p_z_a, p_fc2;
   __nv_bfloat16 *s2d = nullptr;   // [batch][21][21][64] conv1 input (dense; SIMT / TMA paths)
   uint8_t *in1p = nullptr, *act1p = nullptr, *act2p = nullptr;  // planar trunk buffers [batch]

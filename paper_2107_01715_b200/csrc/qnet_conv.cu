@@ -170,6 +170,7 @@ __device__ __forceinline__ void tmem_wait16(uint32_t (&r)[16]) {
 // copy issued, input ready (MMA side), MMAs issued, epilogue done.
 __device__ unsigned long long *g_trace = nullptr;
 __device__ int g_trace_sel = -1;
+__device__ int g_sib_dbg = 0;   // k_conv1_sib timing experiments (conv_trace_set); 0 in production
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -591,16 +592,25 @@ __global__ void __launch_bounds__(kThreadsF, 1)
 //                  + conv1[frame 3](new frame of child a)             (K = 4 taps x 16)
 // The shared part P is accumulated in TMEM once per parent; each child costs
 // 16 MMAs for its new frame; the epilogue adds P + C_a + bias, ReLU, bf16.
-// Operands are chunk-planar (SWIZZLE_NONE K-major: 8 bf16 per 16-byte row per
+// Operands are chunk-planar (SWIZZLE_NONE K-major: 8 fp16 per 16-byte row per
 // plane; any starting row is a valid descriptor = shifted window), channel
 // order inside an s2d(4) pixel (c, dy, dx): plane j of the shared image holds
 // frame c = j/2 at dy in {2(j%2), 2(j%2)+1}; the new image has 2 planes (dy pairs).
-//   warp 0: MMA issuer   warps 1-8: epilogue   warps 9-16: converters
+//
+// The kernel is bound by SMEM bandwidth (128 B/clk): per child the MMAs read 80 KB of operands
+// and the converters write the 14 KB new image. Everything else stays off SMEM:
+//  * the epilogue writes act1 straight to global from registers (32-byte sectors per lane);
+//  * each converter keeps its noise groups' parent newest-frame bytes in registers per parent;
+//  * parent frames (28 KB) arrive by one bulk copy into a 2-deep SMEM ring, issued two parents
+//    ahead, so a parent switch never waits on HBM;
+//  * the shared image of parent k+1 is converted right after parent k's first child and its
+//    48 MMAs are issued between parent k's children as soon as it is ready (lookahead), so a
+//    parent switch does not drain the pipeline.
+//   warp 0: MMA issuer   warps 1-8: epilogue   warps 9-15: converters
 constexpr int kSibThreads = 512;                    // warp 0 MMA, 1-8 epilogue, 9-15 converters
 constexpr int kSibConv = 224;
 __device__ __forceinline__ void sib_bar() { asm volatile("bar.sync 1, 224;" ::: "memory"); }   // 7 converter warps
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 2, 256;" ::: "memory"); }   // 8 epilogue warps
-constexpr int kStageBlk = 100 * 128;   // one act1 row block: 10x10 rows x 128 B
 // Two bytes -> fp16x2, exactly: PRMT builds halves 0x64bb (= 1024 + b), HADD2 subtracts 1024.
 __device__ __forceinline__ uint32_t h2_minus1024(uint32_t u) {
   uint32_t r;
@@ -611,18 +621,26 @@ __device__ __forceinline__ uint32_t h2_minus1024(uint32_t u) {
 __device__ __forceinline__ uint32_t u8pair_f16x2(uint32_t w, uint32_t sel) {
   return h2_minus1024(__byte_perm(w, 0x64646464u, sel));
 }
-#ifndef SIB_F16
-#define SIB_F16 1
-#endif
-#if SIB_F16
-constexpr float kSibScale = 6.103515625e-05f;   // 2^-14: undoes the fp16 weight scaling (qnet.cu)
-#else
-constexpr float kSibScale = 1.0f;
-#endif
-constexpr uint32_t kSibPlane = 536 * 16;            // rows 0..535 x 16 B
-constexpr uint32_t kSharedBytes = 6 * kSibPlane;    // 51,456
-constexpr uint32_t kNewBytes = 2 * kSibPlane;       // 17,152
-constexpr int kNewRing = 2;
+__device__ __forceinline__ bool mbar_test(uint64_t *b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile("{\n.reg .pred P1;\nmbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.u32 %0, 1, 0, P1;\n}\n"
+               : "=r"(ok)
+               : "r"(saddr(b)), "r"(parity)
+               : "memory");
+  return ok != 0;
+}
+constexpr float kSibScale = 6.103515625e-05f;       // 2^-14: undoes the fp16 weight scaling (qnet.cu)
+// Planes hold the 441 real rows back to back (plane stride 441 x 16 B): the M-tile windows reach
+// row 533, but every row past 440 feeds only discarded outputs (valid rows q <= 418, taps add
+// <= 22), so a plane's overhang may alias the next plane (or 1,536 B of tail padding).
+constexpr uint32_t kSibPlane = 441 * 16;                        // 7,056
+constexpr uint32_t kSharedBytes = 6 * kSibPlane + 1536;         // 43,872
+constexpr uint32_t kNewBytes = 2 * kSibPlane + 1536;            // 15,648
+constexpr int kNewRing = 3;
+constexpr uint32_t kParBytes = 28224;                           // one parent's 4 frames (84 x 84 pixel words)
+constexpr int kStageBlk = 100 * 128;                            // one act1 row block: 10x10 rows x 128 B
+constexpr int kSibSmem =
+    4 * 32 * 128 + 2 * (int)kSharedBytes + kNewRing * (int)kNewBytes + (int)kParBytes + 4 * kStageBlk + 1024;
 
 __global__ void __launch_bounds__(kSibThreads, 1)
     k_conv1_sib(ConvSW P, const uint8_t *__restrict__ Wsh, const uint8_t *__restrict__ Wnw,
@@ -630,7 +648,11 @@ __global__ void __launch_bounds__(kSibThreads, 1)
                 float gk, uint8_t *__restrict__ out, float *__restrict__ cum_out) {
   constexpr int N = 32;
   extern __shared__ uint8_t smem_raw[];
-  const bool tron = g_trace != nullptr && g_trace_sel == 10 && blockIdx.x == 0;
+  // trace pointer held in a register: re-reading the __device__ global after every asm memory
+  // clobber would put a global load on each traced path and distort the timeline
+  unsigned long long *const trp = (g_trace_sel == 10 && blockIdx.x == 0) ? g_trace : nullptr;
+  const bool tron = trp != nullptr;
+  const int dbg = g_sib_dbg;
   // 1024-byte aligned base, derived from smem_raw by an OFFSET so the compiler keeps the
   // shared address space (a uintptr_t round trip turns every access into a generic LD/ST)
   uint8_t *smem = smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u);
@@ -638,9 +660,9 @@ __global__ void __launch_bounds__(kSibThreads, 1)
   uint8_t *sWnw = sWsh + 3 * N * 128;                // 1 k-block (K = 64)
   uint8_t *sSh = sWnw + N * 128;                     // 2 x shared image
   uint8_t *sNw = sSh + 2 * kSharedBytes;             // kNewRing x new image
-  uint32_t *sNew3 = (uint32_t *)(sNw + kNewRing * kNewBytes);   // 2 x parent newest-frame bytes (7056 B)
-  uint8_t *sStage0 = (uint8_t *)sNew3 + 2 * 7056;   // 2 x one child's act1 (2 x 100 rows x 128 B, global layout)
-  __shared__ __align__(8) uint64_t sh_full[2], sh_empty[2], p_full[2], p_empty[2];
+  uint8_t *sPar = sNw + kNewRing * kNewBytes;        // parent frames (bulk-copied, one parent ahead)
+  uint8_t *sStage0 = sPar + kParBytes;               // 2 x one child's act1 (2 x 100 rows x 128 B, global layout)
+  __shared__ __align__(8) uint64_t sh_full[2], sh_empty[2], p_full[2], p_empty[2], par_full;
   __shared__ __align__(8) uint64_t n_full[kNewRing], n_empty[kNewRing], c_full[2], c_empty[2], wbar;
   __shared__ uint32_t tmem_slot;
   __shared__ float sbias[64];
@@ -648,6 +670,13 @@ __global__ void __launch_bounds__(kSibThreads, 1)
   const int64_t per = (n_img + gridDim.x - 1) / gridDim.x;
   const int64_t i0 = (int64_t)blockIdx.x * per, i1 = min(n_img, i0 + per);
   if (threadIdx.x < N) sbias[threadIdx.x] = bias[threadIdx.x];
+  const int64_t pfirst_cta = (c_begin + i0) / A;
+  const int64_t npar = i1 > i0 ? (c_begin + i1 - 1) / A - pfirst_cta + 1 : 0;
+  // parent q of this CTA (q = 0, 1, ...) -> the parent-frame buffer, completion phase q & 1
+  auto issue_par = [&](int64_t q) {
+    mbar_expect_tx(&par_full, kParBytes);
+    bulk_g2s(saddr(sPar), par.state + (pfirst_cta + q - p_first) * par.state_stride, kParBytes, &par_full);
+  };
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2; ++i) {
       mbar_init(&sh_full[i], kSibConv);
@@ -657,6 +686,7 @@ __global__ void __launch_bounds__(kSibThreads, 1)
       mbar_init(&c_full[i], 1);
       mbar_init(&c_empty[i], 256);
     }
+    mbar_init(&par_full, 1);
     for (int i = 0; i < kNewRing; ++i) {
       mbar_init(&n_full[i], kSibConv);
       mbar_init(&n_empty[i], 1);
@@ -678,51 +708,60 @@ __global__ void __launch_bounds__(kSibThreads, 1)
   const uint32_t tmem = tmem_slot;   // cols [0,256): P[2] (4 tiles x 32 each); [256,512): C[2]
   pdl_wait();
   pdl_trigger();
-  const int64_t pfirst_cta = (c_begin + i0) / A;
+  if (threadIdx.x == 0 && npar > 0) issue_par(0);   // parent frames come from the previous kernel: after pdl_wait
 
   if (warp == 0) {
     // ---------------------------------------------- MMA issuer (whole warp, elected lane issues)
-#if SIB_F16
     constexpr uint32_t idesc = idesc_f16(128, N);   // fp16 operands (see qnet.cu: exact 2^14-scaled weights)
-#else
-    constexpr uint32_t idesc = idesc_bf16(128, N);
-#endif
     const uint32_t elected = elect_one();
     mbar_wait(&wbar, 0);
     const uint64_t wsh = desc_sw128(saddr(sWsh)), wnw = desc_sw128(saddr(sWnw));
-    int64_t cur_p = -1;
-    uint32_t k = 0, j = 0;
-    for (int64_t img = i0; img < i1; ++img, ++j) {
-      const int64_t p = (c_begin + img) / A;
-      if (p != cur_p) {     // shared part of a new parent: 4 tiles x 4 taps x 3 K-steps
-        k = (uint32_t)(p - pfirst_cta);
-        const uint32_t sb = k & 1u, ph = (k >> 1) & 1u;
-        mbar_wait(&sh_full[sb], ph);
-        mbar_wait(&p_empty[sb], ph ^ 1u);
-        tc_fence_after();
-        const uint32_t abase = saddr(sSh + sb * kSharedBytes);
+    // shared part P(q): 4 tiles x 4 taps x 3 K-steps into TMEM buffer q & 1
+    auto issue_shared = [&](int64_t q) {
+      const uint32_t sb = (uint32_t)q & 1u;
+      tc_fence_after();
+      const uint32_t abase = saddr(sSh + sb * kSharedBytes);
 #pragma unroll
-        for (int mt = 0; mt < 4; ++mt)
+      for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-          for (int tap = 0; tap < 4; ++tap)
+        for (int tap = 0; tap < 4; ++tap)
 #pragma unroll
-            for (int kk = 0; kk < 3; ++kk) {
-              const uint32_t a = abase + (uint32_t)(2 * kk) * kSibPlane +
-                                 (uint32_t)(mt * 128 + (tap >> 1) * 21 + (tap & 1)) * 16u;
-              const int kw = tap * 48 + 16 * kk;
-              const uint32_t w_off = (uint32_t)(kw >> 6) * (N * 128) + (uint32_t)((kw & 63) * 2);
-              mma_pred(tmem + sb * 128 + (uint32_t)(mt * N), desc_planar(a, kSibPlane), wsh + (w_off >> 4), idesc,
-                       (tap | kk) != 0, elected);
-            }
-        commit_pred(&sh_empty[sb], elected);
-        commit_pred(&p_full[sb], elected);
+          for (int kk = 0; kk < 3; ++kk) {
+            const uint32_t a = abase + (uint32_t)(2 * kk) * kSibPlane +
+                               (uint32_t)(mt * 128 + (tap >> 1) * 21 + (tap & 1)) * 16u;
+            const int kw = tap * 48 + 16 * kk;
+            const uint32_t w_off = (uint32_t)(kw >> 6) * (N * 128) + (uint32_t)((kw & 63) * 2);
+            mma_pred(tmem + sb * 128 + (uint32_t)(mt * N), desc_planar(a, kSibPlane), wsh + (w_off >> 4), idesc,
+                     (tap | kk) != 0, elected);
+          }
+      commit_pred(&sh_empty[sb], elected);
+      commit_pred(&p_full[sb], elected);
+    };
+    int64_t cur_p = -1, issued = -1;   // highest parent whose P has been issued
+    uint32_t j = 0;
+    int64_t k = 0;                     // parent of the current child, relative to pfirst_cta
+    int ca = (int)(c_begin + i0 - pfirst_cta * A);   // child index within its parent (no per-child division)
+    for (int64_t img = i0; img < i1; ++img, ++j, ++ca) {
+      if (ca == A) { ca = 0; ++k; }
+      const int64_t p = pfirst_cta + k;
+      if (p != cur_p) {
+        if (issued < k) {      // P(k) not issued ahead (first parent, or the lookahead found it not ready)
+          const uint32_t sb = (uint32_t)k & 1u, ph = (uint32_t)(k >> 1) & 1u;
+          mbar_wait(&sh_full[sb], ph);
+          mbar_wait(&p_empty[sb], ph ^ 1u);
+          issue_shared(k);
+          issued = k;
+        }
         cur_p = p;
       }
       // new frame of child img: 4 tiles x 4 taps x 1 K-step
       const uint32_t nb = j % kNewRing, nph = (j / kNewRing) & 1u;
       const uint32_t cb = j & 1u, cph = (j >> 1) & 1u;
+      if (tron && j < 64 && elected) trp[j * 10 + 3] = clock64();   // trace: MMA loop top
       mbar_wait(&n_full[nb], nph);
+      if (tron && j < 64 && elected) trp[j * 10 + 4] = clock64();   // trace: new image ready
       mbar_wait(&c_empty[cb], cph ^ 1u);
+      if (tron && j < 64 && elected) trp[j * 10 + 5] = clock64();   // trace: C buffer free
       tc_fence_after();
       const uint32_t nbase = saddr(sNw + nb * kNewBytes);
 #pragma unroll
@@ -734,9 +773,19 @@ __global__ void __launch_bounds__(kSibThreads, 1)
           mma_pred(tmem + 256 + cb * 128 + (uint32_t)(mt * N), desc_planar(a, kSibPlane), wnw + (w_off >> 4), idesc,
                    tap != 0, elected);
         }
-      if (tron && j < 64 && elected) g_trace[j * 4 + 3] = clock64();   // trace (cycles): MMAs issued
+      if (tron && j < 64 && elected) trp[j * 10 + 6] = clock64();   // trace (cycles): MMAs issued
       commit_pred(&n_empty[nb], elected);
       commit_pred(&c_full[cb], elected);
+      if (tron && j < 64 && elected && (dbg & 8)) trp[j * 10 + 8] = clock64();   // experiment: after commits
+      // lookahead: P(k+1) as soon as its shared image and TMEM buffer are ready (warp-uniform test)
+      if (issued == k && k + 1 < npar) {
+        const uint32_t sb = (uint32_t)(k + 1) & 1u, ph = (uint32_t)((k + 1) >> 1) & 1u;
+        const uint32_t ready = (mbar_test(&sh_full[sb], ph) && mbar_test(&p_empty[sb], ph ^ 1u)) ? 1u : 0u;
+        if (__shfl_sync(0xffffffffu, ready, 0)) {
+          issue_shared(k + 1);
+          issued = k + 1;
+        }
+      }
       __syncwarp();
     }
   } else if (warp < 9) {
@@ -752,26 +801,30 @@ __global__ void __launch_bounds__(kSibThreads, 1)
     // staging offsets of this thread's 16-byte chunks, fixed for every child: output row
     // q = mt*128 + r is pixel (q / 21, q % 21) of the full-width conv1 output; act1 is its
     // s2d(2) image (row (oy/2)*10 + ox/2, sub-pixel (oy&1, ox&1)) in SW128 row blocks.
-    // ~0u marks the discarded full-width columns / padding rows.
-    uint32_t soff[4][2];
+    // The two chunks of a (row, 16 channels) pair: the first chunk index is even, so the second
+    // sits at (first offset) ^ 16. Offsets < 2^16, two per register; 0xFFFF marks the discarded
+    // full-width columns / padding rows.
+    uint32_t soff2[2];
 #pragma unroll
     for (int mt = 0; mt < 4; ++mt) {
       const int q = mt * 128 + r, oy = q / 21, ox = q - oy * 21;
       const int sub = ((oy & 1) << 1) | (ox & 1), row = (oy >> 1) * 10 + (ox >> 1);
-#pragma unroll
-      for (int h2 = 0; h2 < 2; ++h2) {
-        const int chunk = sub * 4 + ((c0 + 8 * h2) >> 3);
-        soff[mt][h2] = (oy >= 20 || ox >= 20) ? ~0u
-                       : (uint32_t)((chunk >> 3) * kStageBlk + row * 128 + (((chunk & 7) ^ (row & 7)) << 4));
-      }
+      const int chunk = sub * 4 + (c0 >> 3);
+      const uint32_t o = (oy >= 20 || ox >= 20) ? 0xFFFFu
+                         : (uint32_t)((chunk >> 3) * kStageBlk + row * 128 + (((chunk & 7) ^ (row & 7)) << 4));
+      if (mt & 1) soff2[mt >> 1] |= o << 16;
+      else soff2[mt >> 1] = o;
     }
     uint32_t vp[4][16];
     int64_t cur_p = -1;
     uint32_t j = 0;
-    for (int64_t img = i0; img < i1; ++img, ++j) {
-      const int64_t c = c_begin + img, p = c / A;
+    int64_t kk = 0;
+    int ca = (int)(c_begin + i0 - pfirst_cta * A);
+    for (int64_t img = i0; img < i1; ++img, ++j, ++ca) {
+      if (ca == A) { ca = 0; ++kk; }
+      const int64_t p = pfirst_cta + kk;
       if (p != cur_p) {
-        const uint32_t k = (uint32_t)(p - pfirst_cta), sb = k & 1u, ph = (k >> 1) & 1u;
+        const uint32_t k = (uint32_t)kk, sb = k & 1u, ph = (k >> 1) & 1u;
         mbar_wait(&p_full[sb], ph);
         tc_fence_after();
 #pragma unroll
@@ -789,6 +842,8 @@ __global__ void __launch_bounds__(kSibThreads, 1)
       }
       const uint32_t cb = j & 1u, cph = (j >> 1) & 1u;
       mbar_wait(&c_full[cb], cph);
+      const bool etr = tron && j < 64 && threadIdx.x == 32;
+      if (etr) trp[j * 10 + 7] = clock64();   // trace: C ready (MMAs complete)
       tc_fence_after();
       uint8_t *oimg = out + img * (int64_t)P.out_img_bytes;
       // staging buffer j&1 is free once the bulk store of child j-2 has read it (<= 1 group pending)
@@ -806,11 +861,13 @@ __global__ void __launch_bounds__(kSibThreads, 1)
         if (hf == 1) {
           tc_fence_before();
           mbar_arrive(&c_empty[cb]);
+          if (etr && !(dbg & 8)) trp[j * 10 + 8] = clock64();   // trace: C read, buffer released
         }
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
           const int mt = 2 * hf + u;
-          if (soff[mt][0] == ~0u) continue;
+          const uint32_t o = (soff2[mt >> 1] >> (16 * (mt & 1))) & 0xFFFFu;
+          if (o == 0xFFFFu) continue;
           uint32_t pk[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) {   // relu(C * 2^-14 + Pb) -> bf16 (ReLU on the packed pair)
@@ -820,18 +877,20 @@ __global__ void __launch_bounds__(kSibThreads, 1)
           }
 #pragma unroll
           for (int h2 = 0; h2 < 2; ++h2)   // into the staging image, in act1's global SW128 layout
-            *(uint4 *)(sStage + soff[mt][h2]) = make_uint4(pk[4 * h2], pk[4 * h2 + 1], pk[4 * h2 + 2], pk[4 * h2 + 3]);
+            if (!(dbg & 2))
+              *(uint4 *)(sStage + (o ^ (16u * h2))) = make_uint4(pk[4 * h2], pk[4 * h2 + 1], pk[4 * h2 + 2], pk[4 * h2 + 3]);
         }
       }
       // whole image staged: the TMA engine writes the two row blocks to global (async)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       epi_bar();
-      if (threadIdx.x == 32) {
+      if (threadIdx.x == 32 && !(dbg & 2)) {
         for (int q = 0; q < 2; ++q)
           asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(oimg + q * P.out_plane * 8u),
                        "r"(saddr(sStage) + q * kStageBlk), "r"(kStageBlk)
                        : "memory");
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        if (etr) trp[j * 10 + 9] = clock64();   // trace: staged + bulk store issued
       }
     }
   } else {
@@ -851,56 +910,74 @@ __global__ void __launch_bounds__(kSibThreads, 1)
         tdst[it][h] = (uint32_t)(y & 3) / 2u * kSibPlane + (uint32_t)((y >> 2) * 21 + X) * 16u + (uint32_t)(y & 1) * 8u;
       }
     }
-    int64_t cur_p = -1;
+    // Parent q (frames in the parent-frame buffer, phase q & 1): its shared image (frames 1..3 as
+    // child frames 0..2) into shared slot q & 1, and this thread's newest-frame bytes into pn_next;
+    // then the buffer is refilled with parent q+1 (a whole parent period ahead of its use).
+    uint2 pn[kTasks], pn_next[kTasks];   // parent newest-frame bytes of this thread's noise groups
+    auto load_parent = [&](int64_t q) {
+      const uint32_t sb = (uint32_t)q & 1u, ph = (uint32_t)(q >> 1) & 1u;
+      mbar_wait(&par_full, (uint32_t)q & 1u);
+      mbar_wait(&sh_empty[sb], ph ^ 1u);
+      const uint4 *pf4 = (const uint4 *)sPar;
+      uint8_t *sh = sSh + sb * kSharedBytes;
+#pragma unroll
+      for (int it = 0; it < (441 * 2 + kSibConv - 1) / kSibConv; ++it) {
+        const int task = t + it * kSibConv;
+        if (task >= 441 * 2) break;
+        const int dyp = task >= 441, pix = task - 441 * dyp;   // plane-major: conflict-free STS
+        const int Y = pix / 21, X = pix - Y * 21;
+        const int pa = (4 * Y + 2 * dyp) * 84 + 4 * X;           // dy = 2*dyp, 2*dyp+1 (4 pixels each)
+        const uint4 x = pf4[pa >> 2];
+        const uint4 y = pf4[(pa + 84) >> 2];
+        // child frame c = parent frame c+1 (bytes 1..3), 8 fp16 per plane row: (dy0: dx0..3, dy1: dx0..3)
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) {
+          const uint32_t b = (uint32_t)(cc + 1), s2 = b | ((b + 4) << 4);   // bytes: u.b, v.b
+          auto hp = [&](uint32_t u, uint32_t v) { return h2_minus1024(__byte_perm(__byte_perm(u, v, s2), 0x6464u, 0x5140u)); };
+          const uint4 v = make_uint4(hp(x.x, x.y), hp(x.z, x.w), hp(y.x, y.y), hp(y.z, y.w));
+          *(uint4 *)(sh + (size_t)(2 * cc + dyp) * kSibPlane + (size_t)pix * 16) = v;
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&sh_full[sb]);
+#pragma unroll
+      for (int it = 0; it < kTasks; ++it) {
+        const int g = min(t + it * kSibConv, 881);
+        const uint4 w0 = pf4[2 * g], w1 = pf4[2 * g + 1];   // pixel words 8g .. 8g+7: their byte 3
+        pn_next[it].x = __byte_perm(__byte_perm(w0.x, w0.y, 0x0073u), __byte_perm(w0.z, w0.w, 0x0073u), 0x5410u);
+        pn_next[it].y = __byte_perm(__byte_perm(w1.x, w1.y, 0x0073u), __byte_perm(w1.z, w1.w, 0x0073u), 0x5410u);
+      }
+      sib_bar();   // every converter is done reading the parent-frame buffer
+      if (t == 0 && q + 1 < npar) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue_par(q + 1);
+      }
+    };
+    int64_t cur_p = -1, loaded = -1;   // highest parent loaded (shared image converted, pn_next set)
     uint32_t k = 0, j = 0;
     uint64_t pkey = 0;
     float pcum = 0.0f;
-    for (int64_t img = i0; img < i1; ++img, ++j) {
-      const int64_t c = c_begin + img, p = c / A;
-      const int a = (int)(c - p * A);
+    bool first_child = false;
+    int64_t kk = 0;
+    int a = (int)(c_begin + i0 - pfirst_cta * A);   // child index within its parent = its action (R1)
+    for (int64_t img = i0; img < i1; ++img, ++j, ++a) {
+      if (a == A) { a = 0; ++kk; }
+      const int64_t p = pfirst_cta + kk;
       const int64_t pl = p - p_first;
-      if (p != cur_p) {   // shared image of a new parent + its newest-frame bytes
+      if (p != cur_p) {   // a new parent: newest-frame bytes (registers), key, cumulative reward
+        k = (uint32_t)kk;
+        if (loaded < (int64_t)k) {   // first parent of the CTA (later ones are loaded ahead)
+          load_parent(k);
+          loaded = k;
+        }
+#pragma unroll
+        for (int it = 0; it < kTasks; ++it) pn[it] = pn_next[it];
         pkey = *(const uint64_t *)((const uint8_t *)par.key + pl * par.key_stride);   // once per parent
         pcum = par.cum ? par.cum[pl] : 0.0f;
-        k = (uint32_t)(p - pfirst_cta);
-        const uint32_t sb = k & 1u, ph = (k >> 1) & 1u;
-        mbar_wait(&sh_empty[sb], ph ^ 1u);
-        const uint8_t *pf = par.state + pl * par.state_stride;
-        uint8_t *sh = sSh + sb * kSharedBytes;
-        uint32_t *n3 = sNew3 + sb * (7056 / 4);
-#pragma unroll
-        for (int it = 0; it < (441 * 2 + kSibConv - 1) / kSibConv; ++it) {
-          const int task = t + it * kSibConv;
-          if (task >= 441 * 2) break;
-          const int dyp = task >= 441, pix = task - 441 * dyp;   // plane-major: conflict-free STS
-          const int Y = pix / 21, X = pix - Y * 21;
-          const int pa = (4 * Y + 2 * dyp) * 84 + 4 * X;           // dy = 2*dyp, 2*dyp+1 (4 pixels each)
-          const uint4 x = __ldg((const uint4 *)pf + (pa >> 2));
-          const uint4 y = __ldg((const uint4 *)pf + ((pa + 84) >> 2));
-          // child frame c = parent frame c+1 (bytes 1..3), 8 fp16 per plane row: (dy0: dx0..3, dy1: dx0..3)
-#pragma unroll
-          for (int cc = 0; cc < 3; ++cc) {
-            const uint32_t b = (uint32_t)(cc + 1), s2 = b | ((b + 4) << 4);   // bytes: u.b, v.b
-#if SIB_F16
-            auto hp = [&](uint32_t u, uint32_t v) { return h2_minus1024(__byte_perm(__byte_perm(u, v, s2), 0x6464u, 0x5140u)); };
-#else
-            const uint32_t sel = 0x7540u + b;
-            auto cv = [&](uint32_t w) { return __float_as_uint(__uint_as_float(__byte_perm(w, 0x4B000000u, sel)) - 8388608.0f); };
-            auto hp = [&](uint32_t u, uint32_t v) { (void)s2; return __byte_perm(cv(u), cv(v), 0x7632u); };
-#endif
-            const uint4 v = make_uint4(hp(x.x, x.y), hp(x.z, x.w), hp(y.x, y.y), hp(y.z, y.w));
-            *(uint4 *)(sh + (size_t)(2 * cc + dyp) * kSibPlane + (size_t)pix * 16) = v;
-          }
-          n3[pa >> 2] = __byte_perm(__byte_perm(x.x, x.y, 0x0073u), __byte_perm(x.z, x.w, 0x0073u), 0x5410u);
-          n3[(pa + 84) >> 2] = __byte_perm(__byte_perm(y.x, y.y, 0x0073u), __byte_perm(y.z, y.w, 0x0073u), 0x5410u);
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive(&sh_full[sb]);
-        sib_bar();        // sNew3 of this parent complete for every converter
         cur_p = p;
+        first_child = true;
       }
-      const uint32_t sb = k & 1u;
-      if (tron && j < 64 && t == 0) g_trace[j * 4 + 0] = clock64();   // trace (cycles): child start
+      if (tron && j < 64 && t == 0) trp[j * 10 + 0] = clock64();   // trace (cycles): child start
       const uint64_t k2 = mix64d(pkey ^ (0x9E3779B97F4A7C15ull * (uint64_t)(a + 1)));   // child key
       if (t == 0) {
         const uint32_t tt = (uint32_t)(k2 >> 61);
@@ -910,28 +987,32 @@ __global__ void __launch_bounds__(kSibThreads, 1)
       const uint32_t nb = j % kNewRing, nph = (j / kNewRing) & 1u;
       mbar_wait(&n_empty[nb], nph ^ 1u);
       const bool tr = tron && j < 64 && t == 0;
-      if (tr) g_trace[j * 4 + 1] = clock64();   // conversion start
+      if (tr) trp[j * 10 + 1] = clock64();   // conversion start
       uint8_t *nw = sNw + nb * kNewBytes;
-      const uint32_t *n3 = sNew3 + sb * (7056 / 4);
       // noise group g: h = mix64(k2 + g) covers pixels 8g..8g+7 = quads 2g (low word) and 2g+1
 #pragma unroll
       for (int it = 0; it < kTasks; ++it) {
         const int g = t + it * kSibConv;
         if (g >= 882) break;
         const uint64_t h = mix64d(k2 + (uint64_t)g);
-        const uint2 pn = *(const uint2 *)(n3 + 2 * g);   // parent newest-frame bytes of both quads
-        const uint32_t b0 = pn.x ^ (uint32_t)h, b1 = pn.y ^ (uint32_t)(h >> 32);
-#if SIB_F16
+        const uint32_t b0 = pn[it].x ^ (uint32_t)h, b1 = pn[it].y ^ (uint32_t)(h >> 32);
+        if (dbg & 1) {   // timing experiment: no new-image stores
+          if (b0 == 0x12345678u && b1 == 0x9abcdef0u) *(uint32_t *)nw = b0;
+          continue;
+        }
         *(uint2 *)(nw + tdst[it][0]) = make_uint2(u8pair_f16x2(b0, 0x4140u), u8pair_f16x2(b0, 0x4342u));
         *(uint2 *)(nw + tdst[it][1]) = make_uint2(u8pair_f16x2(b1, 0x4140u), u8pair_f16x2(b1, 0x4342u));
-#else
-        *(uint2 *)(nw + tdst[it][0]) = make_uint2(u8pair_bf16x2(b0, 0), u8pair_bf16x2(b0, 2));
-        *(uint2 *)(nw + tdst[it][1]) = make_uint2(u8pair_bf16x2(b1, 0), u8pair_bf16x2(b1, 2));
-#endif
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(&n_full[nb]);
-      if (tr) g_trace[j * 4 + 2] = clock64();   // conversion end (n_full arrived)
+      if (tr) trp[j * 10 + 2] = clock64();   // conversion end (n_full arrived)
+      if (first_child) {   // lookahead: load the next parent while the pipeline works on this child
+        first_child = false;
+        if ((int64_t)k + 1 < npar) {
+          load_parent(k + 1);
+          loaded = k + 1;
+        }
+      }
     }
   }
   if (threadIdx.x == 32) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -1340,8 +1421,12 @@ void launch_n(const ConvSW &P, const Layer &L, const void *in, int64_t n_img, vo
 }  // namespace
 
 void conv_trace_set(unsigned long long *p, int sel) {
+  // sel >= 100: k_conv1_sib trace (10) with debug switches (sel / 100): results are wrong, timing only
+  const int dbg = sel >= 100 ? sel / 100 : 0;
+  if (sel >= 100) sel %= 100;
   cudaMemcpyToSymbol(g_trace, &p, sizeof(p));
   cudaMemcpyToSymbol(g_trace_sel, &sel, sizeof(sel));
+  cudaMemcpyToSymbol(g_sib_dbg, &dbg, sizeof(dbg));
 }
 
 void launch_conv1_fused(const ConvSW &P, const Layer &L, const NodeView &par, int64_t p_first, int64_t c_begin,
@@ -1362,8 +1447,7 @@ void launch_conv1_sib(const ConvSW &P, const Layer &L, const uint8_t *wsh, const
                       int64_t p_first, int64_t c_begin, int64_t n_img, int A, float gk, void *out, float *cum_out,
                       cudaStream_t st) {
   if (n_img <= 0) return;
-  constexpr int smem = 4 * 32 * 128 + 2 * (int)kSharedBytes + kNewRing * (int)kNewBytes + 2 * 7056 +
-                       4 * (int)kStageBlk + 1024;
+  constexpr int smem = kSibSmem;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_conv1_sib, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
