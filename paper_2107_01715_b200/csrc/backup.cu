@@ -56,6 +56,19 @@ void launch_segmax(const float *totals, int64_t n, int64_t leaf_begin, int64_t l
   if (prof) prof->end(st);
 }
 
+// out[i] = max_a rows[i*A + a] (the level-1 maxima of the prologue, from full rows).
+__global__ void k_rowmax(const float *__restrict__ rows, int64_t n, int A, float *__restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float m = rows[i * A];
+  for (int a = 1; a < A; ++a) m = fmaxf(m, rows[i * A + a]);
+  out[i] = m;
+}
+
+void launch_rowmax(const float *rows, int64_t n, int A, float *out, cudaStream_t st) {
+  if (n > 0) k_rowmax<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(rows, n, A, out);
+}
+
 // B(n) of App. A.2 with the CUDA math library's inverse normal CDF.
 __device__ double B_of_n(double n) {
   const double gem = 0.57721566490153286;   // Euler-Mascheroni

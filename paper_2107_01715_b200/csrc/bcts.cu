@@ -218,17 +218,28 @@ size_t shard_ws(bcts_handle h, int64_t range, size_t reserved) {
   const int64_t lc = plan_chunk(h, range, reserved);
   return lc < h->A ? 0 : chunk_bytes(h, lc);
 }
-// Roots per prologue step and the workspace the finalize phase needs.
+// Roots per prologue step and the workspace the finalize phase needs. A prologue step holds
+// the step's roots and their A children as one batch of states ([roots | children]) plus the
+// Q rows of that batch: one net evaluation serves Q_hat(s0, .) and max_a Q_hat(s1, a).
+size_t prologue_root_bytes(bcts_handle h) {
+  return (size_t)((h->A + 1) * node_bytes(h->env) + (int64_t)(h->A + 1) * h->A * 4);
+}
 int64_t prologue_per(bcts_handle h, int64_t n, size_t reserved) {
-  int64_t per = std::max<int64_t>(1, plan_chunk(h, n * h->A, reserved) / h->A);
-  return std::min(per, n);
+  const int64_t budget = h->ws_max - (int64_t)reserved - (2 << 20);
+  int64_t per = budget > 0 ? (int64_t)((double)budget / (double)prologue_root_bytes(h)) : 1;
+  return std::min(std::max<int64_t>(per, 1), n);
+}
+size_t prologue_ws(bcts_handle h, int64_t per) {
+  Carver c(nullptr);
+  c.level(h->env, per * (h->A + 1));
+  c.take((size_t)per * (h->A + 1) * h->A * 4);
+  return c.off;
 }
 size_t finalize_ws(bcts_handle h, int64_t n, size_t reserved) {
   Carver c(nullptr);
-  c.take((size_t)n * h->A * 4 * 3);
+  for (int k = 0; k < 3; ++k) c.take((size_t)n * h->A * 4);   // q0, m1, r1 as finalize_impl carves them
   const size_t base = c.off;
-  c.level(h->env, prologue_per(h, n, reserved + base) * h->A);
-  return c.off;
+  return base + prologue_ws(h, prologue_per(h, n, reserved + base));
 }
 
 // Leaf-range search: expand the ancestors of leaves [L0, L1), score the leaves,
@@ -293,28 +304,45 @@ bcts_status run_shard(bcts_handle h, const void *roots, int32_t d, float gamma, 
 
 // Depth-0/1 quantities for the BCTS terms (Prop. 1; R7):
 // q0 = Q_hat(s0, .), m1[a] = max Q_hat(s1^a, .), r1[a] = R_1 of child a.
+// With the level-1 terms needed, each step copies its roots' states next to their expanded
+// children and evaluates the batch [roots | children] once in full-row mode (one set of net
+// launches instead of two; the prologue's batches are tiny, so its cost is launch latency).
 bcts_status run_prologue(bcts_handle h, const void *roots, int64_t n, float gamma, bool need_level1, float *q0,
                          float *m1, float *r1, size_t reserved, bcts_stats *stats) {
   const int A = h->A;
-  int nl = net_eval(h->net, root_view(h->env, roots, 0), n, MODE_ROWS, 0.0f, q0, h->st);
-  h->launches += nl;
-  if (stats) stats->evaluated += n;
-  if (!need_level1) return cuda_check(h, "prologue");
+  if (!need_level1) {
+    const int nl = net_eval(h->net, root_view(h->env, roots, 0), n, MODE_ROWS, 0.0f, q0, h->st);
+    h->launches += nl;
+    if (stats) stats->evaluated += n;
+    return cuda_check(h, "prologue");
+  }
   float g[2];
   discounts(gamma, 1, g);
   const int64_t per = prologue_per(h, n, reserved);
   Carver cc(h->ws + reserved);
-  LevelBuf b = cc.level(h->env, per * A);
+  LevelBuf b = cc.level(h->env, per * (A + 1));
+  float *rows = (float *)cc.take((size_t)per * (A + 1) * A * 4);
+  const int64_t sb = state_bytes(h->env), rb = record_bytes(h->env);
+  const NodeView rv = root_view(h->env, roots, 0);
   for (int64_t r0 = 0; r0 < n; r0 += per) {
     const int64_t r1e = std::min(n, r0 + per);
-    const int64_t cnt = (r1e - r0) * A;
-    launch_expand(h->env, root_view(h->env, roots, r0), r0, r0 * A, r1e * A, A, g[0], h->em,
-                  out_of(h->env, b), h->st, &h->prof);
-    nl = net_eval(h->net, view_of(h->env, b), cnt, MODE_ROWMAX, 0.0f, m1 + r0 * A, h->st);
-    cudaMemcpyAsync(r1 + r0 * A, b.cum, (size_t)cnt * 4, cudaMemcpyDeviceToDevice, h->st);
-    h->launches += 1 + nl;
+    const int64_t nr = r1e - r0, cnt = nr * A;
+    // slots [0, nr): the roots' states; slots [nr, nr + cnt): their children (Alg. 1 body)
+    cudaMemcpy2DAsync(b.state, (size_t)sb, rv.state + r0 * rb, (size_t)rb, (size_t)sb, (size_t)nr,
+                      cudaMemcpyDeviceToDevice, h->st);
+    NodeOut co = out_of(h->env, b);
+    co.state += nr * sb;
+    if (co.key) co.key += nr;
+    co.cum += nr;
+    launch_expand(h->env, root_view(h->env, roots, r0), r0, r0 * A, r1e * A, A, g[0], h->em, co, h->st, &h->prof);
+    const int nl = net_eval(h->net, view_of(h->env, b), nr + cnt, MODE_ROWS, 0.0f, rows, h->st);
+    if (nl < 0) return fail(h, BCTS_ERR_CUDA, "net_eval (prologue)");
+    cudaMemcpyAsync(q0 + r0 * A, rows, (size_t)nr * A * 4, cudaMemcpyDeviceToDevice, h->st);
+    launch_rowmax(rows + nr * A, cnt, A, m1 + r0 * A, h->st);
+    cudaMemcpyAsync(r1 + r0 * A, b.cum + nr, (size_t)cnt * 4, cudaMemcpyDeviceToDevice, h->st);
+    h->launches += 2 + nl;
     if (stats) {
-      stats->evaluated += cnt;
+      stats->evaluated += nr + cnt;
       stats->transitions += cnt;
     }
   }

@@ -274,6 +274,7 @@ struct FinalizeArgs {
   int64_t *best_leaf = nullptr;
 };
 void launch_finalize(const FinalizeArgs &a, cudaStream_t st, Profiler *prof = nullptr);
+void launch_rowmax(const float *rows, int64_t n, int A, float *out, cudaStream_t st);
 void launch_pv_targets(int64_t n, int A, int d, const int32_t *actions, const float *vanilla,
                        const int64_t *best_leaf, float *target, int32_t *path, cudaStream_t st);
 
