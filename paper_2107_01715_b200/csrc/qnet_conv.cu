@@ -1179,13 +1179,32 @@ __global__ void __launch_bounds__(kC3tThreads, 1)
 // HBM (the separate kernels wrote and re-read 2 x 10 KB per leaf). The MMA warp alternates
 // conv2(i) and conv3(i-1) so the tensor core has work while either epilogue runs.
 // act1 lands in a compact ring (planes of 104 rows instead of act1's 144-row global planes).
-// Warps: 0 producer, 1 MMA, 2-9 conv2 epilogue (lane quarter x 32-channel half),
-// 10-13 conv3 epilogue (lane quarter; lanes 0-15 carry a channel).
-constexpr int kC23Threads = 448;
+// The kernel is bound by the tensor core's SMEM operand reads (ncu: the tc SMEM data pipe at
+// 85% with every operand in SMEM), so conv3's A operand -- the weights, the same for every
+// image -- lives in TMEM (tcgen05.mma A-from-TMEM; M = 64 rows at lane (m/16)*32 + m%16,
+// measured in tools/mma_ts_test.cu), loaded once per CTA with tcgen05.st by the conv3-epilogue
+// warps: conv3 then reads only its 2 KB act2 window per MMA from SMEM (336 -> 264 KB per image).
+// TMEM: T2[2] cols 0..127, T3 (single: conv3(i) is issued after conv2(i+1), long after the
+// epilogue read T3 of image i-1) cols 128..191, W3 cols 192..479.
+// Warps: 0 producer, 1 conv2 MMA issuer, 2-9 conv2 epilogue (lane quarter x 32-channel half),
+// 10-13 conv3 epilogue (lane quarter; lanes 0-15 carry a channel) + the W3 -> TMEM load,
+// 14 conv3 MMA issuer. Two issuing warps: while one waits on its barriers the other keeps the
+// tensor pipe's queue filled (one warp alternating conv2(i) / conv3(i-1) left ~300 idle
+// cycles per image at the hand-offs, traced with selector 11).
+constexpr int kC23Threads = 480;
 constexpr uint32_t kC23Plane = 104 * 128;                 // compact act1 row block (rows 0..103)
 constexpr uint32_t kC23In = 2 * kC23Plane;                // 26,624 per act1 image
 constexpr uint32_t kC23A2 = 11 * 1024;                    // act2 image: 84 rows x 128 B, 1 KB aligned
-constexpr int kC23Smem = 8 * 64 * 128 + 9 * 64 * 128 + 2 * (int)kC23In + 2 * (int)kC23A2 + 2 * kC3tOutBytes + 1024;
+constexpr int kC23InBufs = 3;                             // act1 ring depth (the SMEM W3 copy is gone)
+constexpr int kC23Smem = 8 * 64 * 128 + kC23InBufs * (int)kC23In + 2 * (int)kC23A2 + 2 * kC3tOutBytes + 1024;
+constexpr uint32_t kC23W3Col = 192;                       // TMEM column of W3 (288 columns)
+__device__ __forceinline__ void mma_ts_pred(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc,
+                                            uint32_t issue) {
+  asm volatile(
+      "{\n.reg .pred p, q;\nsetp.ne.b32 p, %4, 0;\nsetp.ne.b32 q, %5, 0;\n"
+      "@q tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc), "r"(issue));
+}
 
 __global__ void __launch_bounds__(kC23Threads, 1)
     k_conv23(ConvSW P2, ConvSW P3, const uint8_t *__restrict__ W2, const float *__restrict__ bias2,
@@ -1194,45 +1213,48 @@ __global__ void __launch_bounds__(kC23Threads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u);
   uint8_t *sW2 = smem;                                  // conv2 B: 8 k-blocks x [64 x 128 B]
-  uint8_t *sW3 = sW2 + 8 * 64 * 128;                    // conv3 A: 9 k-blocks x [64 x 128 B]
-  uint8_t *sIn = sW3 + 9 * 64 * 128;                    // 2 x act1 (compact planes)
-  uint8_t *sA2 = sIn + 2 * kC23In;                      // 2 x act2
+  uint8_t *sIn = sW2 + 8 * 64 * 128;                    // kC23InBufs x act1 (compact planes)
+  uint8_t *sA2 = sIn + kC23InBufs * kC23In;             // 2 x act2
   uint8_t *sO3 = sA2 + 2 * kC23A2;                      // 2 x act3 staging [49][64] bf16
-  __shared__ __align__(8) uint64_t in_full[2], in_empty[2], t2full[2], t2empty[2], a2full[2], a2empty[2], t3full[2],
-      t3empty[2], wbar;
+  __shared__ __align__(8) uint64_t in_full[kC23InBufs], in_empty[kC23InBufs], t2full[2], t2empty[2], a2full[2],
+      a2empty[2], t3full, t3empty, w3ready, wbar;
   __shared__ uint32_t tmem_slot;
   __shared__ float sb2[64], sb3[64];
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
+  // debug timeline (BCTS trace selector 11, CTA 0): [img][8] clock64 stamps, pointer held in a register
+  unsigned long long *const trp = (g_trace_sel == 11 && blockIdx.x == 0) ? g_trace : nullptr;
   if (threadIdx.x < 64) {
     sb2[threadIdx.x] = bias2[threadIdx.x];
     sb3[threadIdx.x] = bias3[threadIdx.x];
   }
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kC23InBufs; ++i) {
       mbar_init(&in_full[i], 1);
       mbar_init(&in_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&t2full[i], 1);
       mbar_init(&t2empty[i], 256);
       mbar_init(&a2full[i], 256);
       mbar_init(&a2empty[i], 1);
-      mbar_init(&t3full[i], 1);
-      mbar_init(&t3empty[i], 128);
     }
+    mbar_init(&t3full, 1);
+    mbar_init(&t3empty, 128);
+    mbar_init(&w3ready, 128);
     mbar_init(&wbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    mbar_expect_tx(&wbar, (8u + 9u) * 64 * 128);
+    mbar_expect_tx(&wbar, 8u * 64 * 128);
     bulk_g2s(saddr(sW2), W2, 8u * 64 * 128, &wbar);
-    bulk_g2s(saddr(sW3), W3, 9u * 64 * 128, &wbar);
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(&tmem_slot)),
-                 "r"(256));
+                 "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = tmem_slot;   // cols [0,128): T2[2] (64 each); [128,256): T3[2]
+  const uint32_t tmem = tmem_slot;   // cols [0,128): T2[2]; [128,192): T3; [192,480): W3
   pdl_wait();
   pdl_trigger();
   const int n_my = n_img > blockIdx.x ? (int)((n_img - 1 - blockIdx.x) / gridDim.x + 1) : 0;
@@ -1241,7 +1263,7 @@ __global__ void __launch_bounds__(kC23Threads, 1)
     if (lane == 0) {   // ------------------------------------------------ producer (act1)
       for (int li = 0; li < n_my; ++li) {
         const int64_t img = blockIdx.x + (int64_t)li * gridDim.x;
-        const uint32_t b = li & 1, ph = (li >> 1) & 1u;
+        const uint32_t b = li % kC23InBufs, ph = (li / kC23InBufs) & 1u;
         mbar_wait(&in_empty[b], ph ^ 1u);
         mbar_expect_tx(&in_full[b], 2u * 12800u);
         for (uint32_t q = 0; q < 2; ++q)
@@ -1250,35 +1272,50 @@ __global__ void __launch_bounds__(kC23Threads, 1)
       }
     }
     __syncwarp();
-  } else if (warp == 1) {   // ------------------------------------------ MMA issuer
-    constexpr uint32_t idesc2 = idesc_bf16(128, 64), idesc3 = idesc_bf16(64, 64);
+  } else if (warp == 14) {   // ------------------------------------------ conv3 MMA issuer
+    constexpr uint32_t idesc3 = idesc_bf16(64, 64);
     const uint32_t elected = elect_one();
-    mbar_wait(&wbar, 0);
-    const uint64_t w2desc = desc_sw128(saddr(sW2)), w3desc = desc_sw128(saddr(sW3));
     auto conv3 = [&](int jj) {
+      if (jj == 0) mbar_wait(&w3ready, 0);   // W3 in TMEM (tcgen05.st by the conv3-epilogue warps)
       const uint32_t b = jj & 1, ph = (jj >> 1) & 1u;
+      if (trp && jj < 64 && elected) trp[jj * 8 + 4] = clock64();   // conv3: waits begin
       mbar_wait(&a2full[b], ph);
-      mbar_wait(&t3empty[b], ph ^ 1u);
+      if (trp && jj < 64 && elected) trp[jj * 8 + 5] = clock64();   // act2 ready
+      mbar_wait(&t3empty, (jj & 1u) ^ 1u);
       tc_fence_after();
       const uint64_t xdesc = desc_sw128_win(saddr(sA2 + b * kC23A2), false);
 #pragma unroll
       for (int tap = 0; tap < 9; ++tap)
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          const uint32_t w_off = (uint32_t)tap * (64 * 128) + (uint32_t)(kk * 32);
+        for (int kk = 0; kk < 4; ++kk) {   // A: W3 columns (tap * 64 + kk * 16) / 2 of the TMEM copy
           const uint32_t x_off = (uint32_t)((tap / 3) * 9 + (tap % 3)) * 128u + (uint32_t)(kk * 32);
-          mma_pred(tmem + 128 + b * 64, w3desc + (w_off >> 4), xdesc + (x_off >> 4), idesc3, (tap | kk) != 0, elected);
+          mma_ts_pred(tmem + 128, tmem + kC23W3Col + (uint32_t)(tap * 32 + kk * 8), xdesc + (x_off >> 4), idesc3,
+                      (tap | kk) != 0, elected);
         }
       commit_pred(&a2empty[b], elected);
-      commit_pred(&t3full[b], elected);
+      commit_pred(&t3full, elected);
+      if (trp && jj < 64 && elected) trp[jj * 8 + 6] = clock64();   // conv3 issued
     };
+    for (int jj = 0; jj < n_my; ++jj) {
+      conv3(jj);
+      __syncwarp();
+    }
+  } else if (warp == 1) {   // ------------------------------------------ conv2 MMA issuer
+    constexpr uint32_t idesc2 = idesc_bf16(128, 64);
+    const uint32_t elected = elect_one();
+    mbar_wait(&wbar, 0);
+    const uint64_t w2desc = desc_sw128(saddr(sW2));
     for (int li = 0; li < n_my; ++li) {
       {   // conv2(li): 4 taps x 8 K-steps
         const uint32_t b = li & 1, ph = (li >> 1) & 1u;
-        mbar_wait(&in_full[b], ph);
+        const uint32_t bi = li % kC23InBufs, phi = (li / kC23InBufs) & 1u;
+        if (trp && li < 64 && elected) trp[li * 8 + 0] = clock64();   // conv2: waits begin
+        mbar_wait(&in_full[bi], phi);
+        if (trp && li < 64 && elected) trp[li * 8 + 1] = clock64();   // act1 landed
         mbar_wait(&t2empty[b], ph ^ 1u);
+        if (trp && li < 64 && elected) trp[li * 8 + 2] = clock64();   // T2 free
         tc_fence_after();
-        const uint64_t adesc0 = desc_sw128_win(saddr(sIn + b * kC23In), false);
+        const uint64_t adesc0 = desc_sw128_win(saddr(sIn + bi * kC23In), false);
 #pragma unroll
         for (int tap = 0; tap < 4; ++tap)
 #pragma unroll
@@ -1289,14 +1326,12 @@ __global__ void __launch_bounds__(kC23Threads, 1)
             const uint32_t w_off = (uint32_t)(k >> 6) * (64 * 128) + (uint32_t)((k & 63) * 2);
             mma_pred(tmem + b * 64, adesc0 + (a_off >> 4), w2desc + (w_off >> 4), idesc2, (tap | kk) != 0, elected);
           }
-        commit_pred(&in_empty[b], elected);
+        commit_pred(&in_empty[bi], elected);
         commit_pred(&t2full[b], elected);
+        if (trp && li < 64 && elected) trp[li * 8 + 3] = clock64();   // conv2 issued
       }
-      if (li >= 1) conv3(li - 1);
       __syncwarp();
     }
-    if (n_my >= 1) conv3(n_my - 1);
-    __syncwarp();
   } else if (warp < 10) {   // --------------------------- conv2 epilogue -> act2 in SMEM (SW128)
     const int q4 = warp & 3, c0 = ((warp - 2) >> 2) * 32;
     const int r = q4 * 32 + lane;                       // full-width output row: oy = r / 10, ox = r % 10
@@ -1309,6 +1344,7 @@ __global__ void __launch_bounds__(kC23Threads, 1)
     for (int li = 0; li < n_my; ++li) {
       const uint32_t b = li & 1, ph = (li >> 1) & 1u;
       mbar_wait(&t2full[b], ph);
+      if (trp && li < 64 && threadIdx.x == 64) trp[li * 8 + 7] = clock64();   // conv2 done (epilogue starts)
       tc_fence_after();
       uint32_t v[2][16];
       const uint32_t tb = tmem + b * 64 + ((uint32_t)(q4 * 32) << 16) + (uint32_t)c0;
@@ -1339,28 +1375,58 @@ __global__ void __launch_bounds__(kC23Threads, 1)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(&a2full[b]);
     }
-  } else {   // --------------------------------------------------- conv3 epilogue -> act3 (dense)
+  } else {   // ------------------------------------------- conv3 epilogue -> act3 (dense), warps 10-13
     const int q = warp & 3;
     const int c = 16 * q + (lane & 15);
     const float bc = sb3[c];
     const uint32_t taddr0 = tmem + 128 + ((uint32_t)(q * 32) << 16);
     const bool lead = threadIdx.x == 32 * 10;
+    {   // W3 -> TMEM: output channel m = 16q + l (lanes l < 16 of quarter q), K = (tap, cin) in
+        // bf16 pairs per column; source = the SW128 weight image in global memory
+      uint32_t r[32];
+#pragma unroll 1
+      for (int tap = 0; tap < 9; ++tap) {
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {   // 8-channel chunk ch of this tap: 4 columns
+          uint4 v4 = make_uint4(0, 0, 0, 0);
+          if (lane < 16) {
+            const int m = 16 * q + lane;
+            v4 = __ldg((const uint4 *)(W3 + (size_t)tap * (64 * 128) + (size_t)m * 128 + (((ch ^ (m & 7)) & 7) << 4)));
+          }
+          r[4 * ch] = v4.x;
+          r[4 * ch + 1] = v4.y;
+          r[4 * ch + 2] = v4.z;
+          r[4 * ch + 3] = v4.w;
+        }
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+            "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(
+                tmem + ((uint32_t)(q * 32) << 16) + kC23W3Col + (uint32_t)(tap * 32)),
+            "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+            "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+            "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+            "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      mbar_arrive(&w3ready);
+    }
     for (int li = 0; li < n_my; ++li) {
       const int64_t img = blockIdx.x + (int64_t)li * gridDim.x;
-      const uint32_t b = li & 1, ph = (li >> 1) & 1u;
-      mbar_wait(&t3full[b], ph);
+      const uint32_t b = li & 1;
+      mbar_wait(&t3full, li & 1u);
       tc_fence_after();
       uint32_t v[64];
-      tmem_ld16_nw(taddr0 + b * 64 + 0, *(uint32_t(*)[16])(v + 0));
-      tmem_ld16_nw(taddr0 + b * 64 + 16, *(uint32_t(*)[16])(v + 16));
-      tmem_ld16_nw(taddr0 + b * 64 + 32, *(uint32_t(*)[16])(v + 32));
-      tmem_ld16_nw(taddr0 + b * 64 + 48, *(uint32_t(*)[16])(v + 48));
+      tmem_ld16_nw(taddr0 + 0, *(uint32_t(*)[16])(v + 0));
+      tmem_ld16_nw(taddr0 + 16, *(uint32_t(*)[16])(v + 16));
+      tmem_ld16_nw(taddr0 + 32, *(uint32_t(*)[16])(v + 32));
+      tmem_ld16_nw(taddr0 + 48, *(uint32_t(*)[16])(v + 48));
       tmem_wait16(*(uint32_t(*)[16])(v + 0));
       tmem_wait16(*(uint32_t(*)[16])(v + 16));
       tmem_wait16(*(uint32_t(*)[16])(v + 32));
       tmem_wait16(*(uint32_t(*)[16])(v + 48));
       tc_fence_before();
-      mbar_arrive(&t3empty[b]);
+      mbar_arrive(&t3empty);
       uint8_t *so = sO3 + b * kC3tOutBytes;
       if (lead) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
       asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -1389,7 +1455,7 @@ __global__ void __launch_bounds__(kC23Threads, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
   }
 }
 
