@@ -130,20 +130,18 @@ __global__ void __launch_bounds__(kExpandThreads) k_expand_atari(NodeView par, i
     const uint64_t k2 = atari_child_key(key, a);
     const int64_t ci = p * A + a - c_begin;
     uint4 *dst = (uint4 *)(out.state + ci * out.state_stride);
-    for (int g = threadIdx.x; g < kGroups; g += kExpandThreads) {
-      const uint64_t h = mix64(k2 + (uint64_t)g);
-      const uint32_t lo = (uint32_t)h, hi = (uint32_t)(h >> 32);
-      uint4 v0 = sframe[2 * g], v1 = sframe[2 * g + 1];
-      v0.x = (v0.x >> 8) | ((v0.x ^ (lo << 24)) & 0xFF000000u);
-      v0.y = (v0.y >> 8) | ((v0.y ^ ((lo >> 8) << 24)) & 0xFF000000u);
-      v0.z = (v0.z >> 8) | ((v0.z ^ ((lo >> 16) << 24)) & 0xFF000000u);
-      v0.w = (v0.w >> 8) | ((v0.w ^ (lo & 0xFF000000u)) & 0xFF000000u);
-      v1.x = (v1.x >> 8) | ((v1.x ^ (hi << 24)) & 0xFF000000u);
-      v1.y = (v1.y >> 8) | ((v1.y ^ ((hi >> 8) << 24)) & 0xFF000000u);
-      v1.z = (v1.z >> 8) | ((v1.z ^ ((hi >> 16) << 24)) & 0xFF000000u);
-      v1.w = (v1.w >> 8) | ((v1.w ^ (hi & 0xFF000000u)) & 0xFF000000u);
-      st_v4(dst + 2 * g, v0);
-      st_v4(dst + 2 * g + 1, v1);
+    // one 16-byte chunk (4 pixel words) per thread: a warp stores 512 contiguous bytes per
+    // instruction (tools/expand_bench.cu: 1.7x the bandwidth of two stores 16 B apart); both
+    // threads of an 8-pixel group hash it and each keeps its half of the 8 noise bytes
+#pragma unroll 4
+    for (int j = threadIdx.x; j < 2 * kGroups; j += kExpandThreads) {
+      const uint32_t nz = (uint32_t)(mix64(k2 + (uint64_t)(j >> 1)) >> (32 * (j & 1)));
+      uint4 v = sframe[j];
+      v.x = (v.x >> 8) | ((v.x ^ (nz << 24)) & 0xFF000000u);
+      v.y = (v.y >> 8) | ((v.y ^ ((nz >> 8) << 24)) & 0xFF000000u);
+      v.z = (v.z >> 8) | ((v.z ^ ((nz >> 16) << 24)) & 0xFF000000u);
+      v.w = (v.w >> 8) | ((v.w ^ (nz & 0xFF000000u)) & 0xFF000000u);
+      st_v4(dst + j, v);
     }
     if (threadIdx.x == 0) {
       out.key[ci] = k2;
@@ -177,8 +175,10 @@ void launch_expand(int env, const NodeView &par, int64_t p_first, int64_t c_begi
       cudaFuncSetAttribute(k_expand_atari, cudaFuncAttributeMaxDynamicSharedMemorySize, kFrameBytes);
       attr = true;
     }
-    // about 4 CTAs per SM (8 fit by SMEM), at most one child per CTA
-    int split = (int)std::max<int64_t>(1, std::min<int64_t>(A, (4 * 148 + nparents - 1) / nparents));
+    // about 6 CTAs per SM (8 fit by SMEM) and at most ~6 children per CTA (measured best at the
+    // C5 level-3 and C3 level-2 shapes, tools/expand_bench.cu)
+    const int64_t want = std::max<int64_t>((6 * 148 + nparents - 1) / nparents, (A + 5) / 6);
+    int split = (int)std::max<int64_t>(1, std::min<int64_t>(A, want));
     k_expand_atari<<<(unsigned)(nparents * split), kExpandThreads, kFrameBytes, st>>>(par, p_first, c_begin, c_end, A, gk,
                                                                              out, split);
   }
