@@ -319,6 +319,13 @@ def main():
         kernels[name] = {"launches_per_step": v["launches"] / args.steps, "ms_per_launch": per_launch_ms,
                          "share": v["ms"] / step_kernel_ms if step_kernel_ms else 0.0,
                          "achieved": ach, "unit": "GB/s" if v["unit"] == "byte" else "TFLOP/s"}
+        if v.get("big_launches") and v["big_launches"] < v["launches"] and v["big_ms"] > 0:
+            # the class's largest launches alone (e.g. the deepest expanded level, the full batches)
+            kernels[name]["largest"] = {
+                "launches_per_step": v["big_launches"] / args.steps,
+                "ms_per_launch": v["big_ms"] / v["big_launches"],
+                "achieved": v["big_work"] * v["big_launches"] / (v["big_ms"] / 1e3)
+                / (1e9 if v["unit"] == "byte" else 1e12)}
     if dom:
         name, v = dom
         long_run = step_ms * args.steps > 1000.0

@@ -280,6 +280,11 @@ typedef struct {
   double ms;    /* summed event durations */
   double work;  /* summed algorithmic bytes (unit 0) or FLOPs (unit 1) */
   int32_t unit;
+  /* the class's LARGEST launches (maximal work per launch, e.g. the deepest expanded level):
+   * how many there were, their summed durations and the work of one */
+  int64_t big_launches;
+  double big_ms;
+  double big_work;
 } bcts_kernel_profile;
 bcts_status bcts_profile_enable(bcts_handle h, int32_t on);
 int32_t bcts_profile_read(bcts_handle h, bcts_kernel_profile *out, int32_t max);

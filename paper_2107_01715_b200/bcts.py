@@ -48,7 +48,7 @@ class Config(C.Structure):
 
 class KernelProfile(C.Structure):
     _fields_ = [("name", C.c_char * 32), ("launches", C.c_int64), ("ms", C.c_double), ("work", C.c_double),
-                ("unit", C.c_int32)]
+                ("unit", C.c_int32), ("big_launches", C.c_int64), ("big_ms", C.c_double), ("big_work", C.c_double)]
 
 
 class Prune(C.Structure):
@@ -293,7 +293,9 @@ class Handle:
         buf = (KernelProfile * 32)()
         k = lib().bcts_profile_read(self._h, buf, 32)
         return {buf[i].name.decode(): {"launches": buf[i].launches, "ms": buf[i].ms, "work": buf[i].work,
-                                       "unit": "flop" if buf[i].unit else "byte"} for i in range(k)}
+                                       "unit": "flop" if buf[i].unit else "byte",
+                                       "big_launches": buf[i].big_launches, "big_ms": buf[i].big_ms,
+                                       "big_work": buf[i].big_work} for i in range(k)}
 
     def pv_targets(self, actions, vanilla_q, best_leaf, n, depth):
         """PV training target (App. B.3) of the executed actions + the best-leaf action path."""

@@ -281,14 +281,22 @@ bcts_status run_shard(bcts_handle h, const void *roots, int32_t d, float gamma, 
       ++lvl_launch;
     }
     int nl;
+    bool folded = false;   // backup fused into the head's epilogue (Rainbow tcgen05 head)
     if (fused) {   // leaf level generated inside the net (s2d frames, L2-resident)
-      nl = net_eval_children(h->net, prev, lo[d - 1], L, Le, A, g[d - 1], MODE_TOTAL, g[d], totals, h->st);
+      KeyFold kf;
+      kf.keys = keys;
+      kf.leaf0 = L;
+      kf.lpr = pw[d];
+      kf.seg = pw[d - 1];
+      kf.A = A;
+      nl = net_eval_children(h->net, prev, lo[d - 1], L, Le, A, g[d - 1], MODE_TOTAL, g[d], totals, h->st, &kf,
+                             &folded);
       trans += Le - L;
     } else {
       nl = net_eval(h->net, prev, Le - L, MODE_TOTAL, g[d], totals, h->st);
     }
-    launch_segmax(totals, Le - L, L, pw[d], pw[d - 1], A, keys, h->st, &h->prof);
-    h->launches += dm + nl + 1;
+    if (!folded) launch_segmax(totals, Le - L, L, pw[d], pw[d - 1], A, keys, h->st, &h->prof);
+    h->launches += dm + nl + (folded ? 0 : 1);
     ++nchunks;
     if ((s = cuda_check(h, "shard chunk"))) return s;
   }
@@ -948,6 +956,9 @@ int32_t bcts_profile_read(bcts_handle h, bcts_kernel_profile *out, int32_t max) 
     out[k].ms = h->prof.ms[c];
     out[k].work = h->prof.work[c];
     out[k].unit = units[c];
+    out[k].big_launches = h->prof.big_n[c];
+    out[k].big_ms = h->prof.big_ms[c];
+    out[k].big_work = h->prof.big_work[c];
     ++k;
   }
   return k;

@@ -26,6 +26,8 @@ struct Profiler {
   std::vector<cudaEvent_t> pool;
   double ms[KC_COUNT] = {}, work[KC_COUNT] = {};
   int64_t launches[KC_COUNT] = {};
+  double big_work[KC_COUNT] = {}, big_ms[KC_COUNT] = {};   // the class's largest launches
+  int64_t big_n[KC_COUNT] = {};
   cudaEvent_t get() {
     if (!pool.empty()) {
       cudaEvent_t e = pool.back();
@@ -54,6 +56,8 @@ struct Profiler {
       ms[r.cls] += t;
       work[r.cls] += r.work;
       launches[r.cls] += 1;
+      if (r.work > big_work[r.cls]) big_work[r.cls] = r.work, big_ms[r.cls] = 0.0, big_n[r.cls] = 0;
+      if (r.work == big_work[r.cls]) big_ms[r.cls] += t, big_n[r.cls] += 1;
       pool.push_back(r.a);
       pool.push_back(r.b);
     }
@@ -61,7 +65,7 @@ struct Profiler {
   }
   void reset() {
     collect();
-    for (int i = 0; i < KC_COUNT; ++i) ms[i] = work[i] = 0, launches[i] = 0;
+    for (int i = 0; i < KC_COUNT; ++i) ms[i] = work[i] = big_work[i] = big_ms[i] = 0, launches[i] = big_n[i] = 0;
   }
   ~Profiler() {
     for (auto &r : pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
@@ -128,7 +132,11 @@ struct TmaPlan {
   alignas(64) uint8_t mapB[128];
   bool ok2sm = false;               // mapB2: B with 128-row boxes (2-SM MMA, half an N tile per CTA)
   alignas(64) uint8_t mapB2[128];
+  bool ok_small = false;            // mapAs / mapBs: 32-row boxes for fc batches of <= kSmallM rows
+  alignas(64) uint8_t mapAs[128];
+  alignas(64) uint8_t mapBs[128];
 };
+constexpr int kSmallM = 32;
 bool tma_plan(TmaPlan &P, const Layer &L, const void *in, int64_t cap_img);
 // Fused Rainbow head (qnet_tma.cu, k_zhead): z_v + z_a + dueling C51 + max_a in one kernel.
 // The head biases travel as a __grid_constant__ kernel parameter: every lane of a warp reads
@@ -149,8 +157,17 @@ struct HeadPlan {
 };
 bool head_plan(HeadPlan &H, const __nv_bfloat16 *hid, int64_t cap, const __nv_bfloat16 *wv64, const __nv_bfloat16 *wa64,
                const __nv_bfloat16 *wsum, int A);
+// Backup fused into a MODE_TOTAL head epilogue (K3a): leaf row m of the batch is
+// global leaf leaf0 + m of root (leaf / lpr), root action (leaf % lpr) / seg; its packed key
+// (total, leaf % lpr) is max-folded into keys[root * A + action] (warp max, one atomicMax per
+// warp-uniform segment). keys == nullptr: totals only.
+struct KeyFold {
+  int64_t *keys = nullptr;
+  int64_t leaf0 = 0, lpr = 1, seg = 1;
+  int A = 0;
+};
 void launch_zhead(const HeadPlan &H, int A, int atoms, int64_t M, float vmin, float dz, int mode, float gd,
-                  const float *cum, float *out, cudaStream_t st);
+                  const float *cum, float *out, cudaStream_t st, KeyFold kf = KeyFold());
 void launch_layer_tma(const TmaPlan &P, const Layer &L, int64_t n_img, void *out, cudaStream_t st);
 
 // Shifted-window conv layer (qnet_conv.cu): stride-1 conv over a per-image
@@ -245,8 +262,11 @@ int net_eval(Net &net, const NodeView &v, int64_t n, int mode, float gd, float *
 // `par` (global level indices from p_first), generating each child's frames on
 // the fly (fused last-level expansion, gk = g[d-1]); out[i] per MODE.
 bool net_fuses_leaves(const Net &net);
+// kf (nullable): fold the totals into packed keys inside the head when it supports it
+// (*folded set to true); otherwise the caller runs the backup kernel.
 int net_eval_children(Net &net, const NodeView &par, int64_t p_first, int64_t c_begin, int64_t c_end, int A,
-                      float gk, int mode, float gd, float *out, cudaStream_t st);
+                      float gk, int mode, float gd, float *out, cudaStream_t st, const KeyFold *kf = nullptr,
+                      bool *folded = nullptr);
 int net_build(Net &net, const bcts_config &cfg, std::string &err);  // 0 ok
 void net_free(Net &net);
 

@@ -682,7 +682,7 @@ static bool c23_enabled() {
 // sub-batches: frames -> s2d bf16 -> conv1 -> conv2 -> conv3 (act3 of the fc
 // batch); then fc_hidden, the output layer(s) and the head.
 static int eval_conv(Net &net, const NodeView *par, const NodeView *img, int64_t p_first, int64_t c_begin, float gk,
-                     int64_t n, int mode, float gd, float *out, cudaStream_t st) {
+                     int64_t n, int mode, float gd, float *out, cudaStream_t st, const KeyFold *kf = nullptr) {
   const int A = net.A;
   const bool rainbow = net.kind == BCTS_NET_RAINBOW_BF16;
   int launches = 0;
@@ -768,7 +768,12 @@ static int eval_conv(Net &net, const NodeView *par, const NodeView *img, int64_t
     } else if (net.tc && net.head.ok) {   // z_v + z_a + dueling C51 head + max_a fused (k_zhead)
       const float dz = (net.vmax - net.vmin) / (float)(net.atoms - 1);
       if (net.prof) net.prof->begin(KC_FC_OUT, 2.0 * (double)nf * 512.0 * (double)(net.atoms + A * net.atoms), st);
-      launch_zhead(net.head, A, net.atoms, nf, net.vmin, dz, mode, gd, cum, o, st);
+      KeyFold kb;
+      if (kf) {
+        kb = *kf;
+        kb.leaf0 += f0;
+      }
+      launch_zhead(net.head, A, net.atoms, nf, net.vmin, dz, mode, gd, cum, o, st, kb);
       if (net.prof) net.prof->end(st);
       launches += 1;
     } else {
@@ -795,9 +800,13 @@ bool net_fuses_leaves(const Net &net) {
 }
 
 int net_eval_children(Net &net, const NodeView &par, int64_t p_first, int64_t c_begin, int64_t c_end, int A,
-                      float gk, int mode, float gd, float *out, cudaStream_t st) {
+                      float gk, int mode, float gd, float *out, cudaStream_t st, const KeyFold *kf, bool *folded) {
   (void)A;
-  return eval_conv(net, &par, nullptr, p_first, c_begin, gk, c_end - c_begin, mode, gd, out, st);
+  static const bool fold_ok = !getenv("BCTS_NO_HEAD_BACKUP");
+  const bool fold = kf && kf->keys && fold_ok && mode == MODE_TOTAL && net.kind == BCTS_NET_RAINBOW_BF16 && net.tc &&
+                    net.head.ok;
+  if (folded) *folded = fold;
+  return eval_conv(net, &par, nullptr, p_first, c_begin, gk, c_end - c_begin, mode, gd, out, st, fold ? kf : nullptr);
 }
 
 int net_eval(Net &net, const NodeView &v, int64_t n, int mode, float gd, float *out, cudaStream_t st) {

@@ -140,7 +140,10 @@ struct TmaGeom {
 template <int BN, int KB>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_tma(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, Layer L,
-               TmaGeom G, int64_t M, void *__restrict__ out, int n_m, int n_n) {
+               TmaGeom G, int64_t M, void *__restrict__ out, int n_m, int n_n, uint32_t a_bytes) {
+  // a_bytes: bytes of A one k-block brings (C::A_BYTES; less for the small-M maps, whose
+  // 32-row boxes fill only the first rows of the 128-row tile -- the other rows' outputs
+  // are never stored, and every output row depends only on its own A row)
   using C = TmaCfg<BN, KB>;
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte aligned base, derived from smem_raw by an OFFSET so the compiler keeps the
@@ -196,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t ph = (it / C::STAGES) & 1u;
           mbar_wait(&empty[s], ph ^ 1u);
           const uint32_t sa = saddr(smem + s * C::STAGE);
-          mbar_expect_tx(&full[s], C::STAGE);
+          mbar_expect_tx(&full[s], a_bytes + C::B_BYTES);
           if (G.im2col) {
             const int k0 = kb * KB;
             const int kwc = G.KW * G.C;
@@ -654,7 +657,10 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
     k_zhead(const __grid_constant__ CUtensorMap mapAv, const __grid_constant__ CUtensorMap mapAa,
             const __grid_constant__ CUtensorMap mapBv, const __grid_constant__ CUtensorMap mapBa,
             const __grid_constant__ CUtensorMap mapBs, const __grid_constant__ HeadBias hb, int A, int64_t M, float vmin,
-            float dz, int mode, float gd, const float *__restrict__ cum, float *__restrict__ out) {
+            float dz, int mode, float gd, const float *__restrict__ cum, float *__restrict__ out, int ns,
+            const KeyFold kf) {
+  // ns: work items per 128-row tile, each taking a contiguous slice of the action chunks
+  // (MODE_ROWS only: tiny batches spread their z_a weight stream over ns CTAs; ns = 1 otherwise)
   static_assert(ATOMS <= 64, "one action per 64 TMEM columns");
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u);
@@ -665,6 +671,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
   const int n_m = (int)((M + kBM - 1) / kBM);
   const int nch = (A + 3) / 4;                       // z_a chunks of 4 actions (256 columns)
+  const int cpc = (nch + ns - 1) / ns, n_work = n_m * ns;
   if (threadIdx.x == 0) {
     for (int i = 0; i < kHeadStages; ++i) {
       mbar_init(&full[i], 1);
@@ -699,7 +706,8 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
         mbar_expect_tx(&full[st], bytes);
         return st;
       };
-      for (int tile = blockIdx.x; tile < n_m; tile += gridDim.x, ++tl) {
+      for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++tl) {
+        const int tile = w / ns, c_lo = (w - tile * ns) * cpc, c_hi = min(nch, c_lo + cpc);
         const int m0 = tile * kBM;
         for (int kb = 0; kb < 8; ++kb, ++it) {     // job v: h_v and W_v k-blocks through the ring
           const int st = slot_wait(16384 + 8192);
@@ -714,7 +722,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
           const int st = slot_wait(8192);
           tma_2d(saddr(sRing + st * kHeadSlot), &mapBs, (kb & 7) * 64, (kb >> 3) * 64, &full[st]);
         }
-        for (int c = 0; c < nch; ++c)
+        for (int c = c_lo; c < c_hi; ++c)
           for (int kb = 0; kb < 8; ++kb, ++it) {
             const int st = slot_wait(kHeadSlot);
             tma_2d(saddr(sRing + st * kHeadSlot), &mapBa, kb * 64, c * 256, &full[st]);
@@ -725,8 +733,10 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
   } else if (warp == 1) {   // ------------------------------------------ MMA issuer
     const uint32_t elected = elect_one();
     uint32_t it = 0, job = 0, tl = 0;
-    for (int tile = blockIdx.x; tile < n_m; tile += gridDim.x, ++tl) {
-      for (int j = 0; j < nch + 2; ++j, ++job) {   // v, mean, chunks
+    for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++tl) {
+      const int tile = w / ns, c_lo = (w - tile * ns) * cpc, c_hi = min(nch, c_lo + cpc);
+      (void)tile;
+      for (int j = 0; j < c_hi - c_lo + 2; ++j, ++job) {   // v, mean, chunks
         const uint32_t b = job & 1u;
         mbar_wait(&tempty[b], ((job >> 1) & 1u) ^ 1u);
         tc_fence_after();
@@ -734,7 +744,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
           mbar_wait(&a_full, tl & 1u);
           tc_fence_after();
         }
-        const int c = j - 2;
+        const int c = c_lo + j - 2;
         const int nt = j < 2 ? 64 : (c < nch - 1 ? 256 : (A - 4 * c) * 64);
         const uint32_t idesc = idesc_bf16(kBM, nt);
         const int nkb = j == 1 ? 16 : 8;
@@ -763,7 +773,8 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
     const int r = q * 32 + lane;
     const uint32_t lanes = (uint32_t)(q * 32) << 16;
     uint32_t job = 0, tl = 0;
-    for (int tile = blockIdx.x; tile < n_m; tile += gridDim.x, ++tl) {
+    for (int w = blockIdx.x; w < n_work; w += gridDim.x, ++tl) {
+      const int tile = w / ns, c_lo = (w - tile * ns) * cpc, c_hi = min(nch, c_lo + cpc);
       const int64_t m = (int64_t)tile * kBM + r;
       float v[ATOMS];
       uint32_t x[64];
@@ -790,7 +801,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
         for (int t = 0; t < ATOMS; ++t) v[t] = v[t] - (__uint_as_float(x[t]) + hb.sum[t]) / (float)A;
       }
       float best = -INFINITY;
-      for (int c = 0; c < nch; ++c, ++job) {   // softmax expectation per action
+      for (int c = c_lo; c < c_hi; ++c, ++job) {   // softmax expectation per action
         const uint32_t b = job & 1u;
         mbar_wait(&tfull[b], (job >> 1) & 1u);
         tc_fence_after();
@@ -821,9 +832,31 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
       if (mode != MODE_ROWS) {   // max_a over both groups (max is order-independent)
         if (grp == 1) s_best[tl & 1u][r] = best;
         asm volatile("bar.sync 1, 256;" ::: "memory");
-        if (grp == 0 && m < M) {
-          best = fmaxf(best, s_best[tl & 1u][r]);
-          out[m] = mode == MODE_ROWMAX ? best : fmaf(gd, best, cum ? cum[m] : 0.0f);
+        if (grp == 0) {
+          int64_t key = kKeyEmpty, slot = -1;
+          if (m < M) {
+            best = fmaxf(best, s_best[tl & 1u][r]);
+            const float tot = mode == MODE_ROWMAX ? best : fmaf(gd, best, cum ? cum[m] : 0.0f);
+            out[m] = tot;
+            if (kf.keys) {   // fused backup (same fold as k_segmax)
+              const int64_t L = kf.leaf0 + m, root = L / kf.lpr, within = L - root * kf.lpr;
+              slot = root * kf.A + within / kf.seg;
+              key = pack_key(tot, within);
+            }
+          }
+          if (kf.keys) {
+            const int64_t s0 = __shfl_sync(0xffffffffu, slot, 0);
+            if (__all_sync(0xffffffffu, slot == s0 || slot < 0)) {
+#pragma unroll
+              for (int o = 16; o > 0; o >>= 1) {
+                const int64_t other = __shfl_xor_sync(0xffffffffu, key, o);
+                key = other > key ? other : key;
+              }
+              if (lane == 0 && s0 >= 0) atomicMax((long long *)&kf.keys[s0], (long long)key);
+            } else if (slot >= 0) {
+              atomicMax((long long *)&kf.keys[slot], (long long)key);
+            }
+          }
         }
       }
     }
@@ -920,8 +953,14 @@ bool launch_gemm_2sm(const TmaPlan &P, const Layer &L, int64_t M, void *out, cud
                             n_pm, n_n) == cudaSuccess;
 }
 
+void launch_gemm_small(const TmaPlan &P, const Layer &L, int64_t M, void *out, cudaStream_t st);
+
 template <int BN, int KB>
 void launch_gemm(const TmaPlan &P, const Layer &L, int64_t M, void *out, cudaStream_t st) {
+  if (P.ok_small && M <= kSmallM && KB == 64 && !P.im2col) {
+    launch_gemm_small(P, L, M, out, st);
+    return;
+  }
   static const bool two_sm = !getenv("BCTS_NO_2SM");
   if (two_sm && !P.im2col && L.relu_bf16 && BN == 256 && KB == 64 && L.Npad % 256 == 0 &&
       launch_gemm_2sm(P, L, M, out, st))
@@ -941,7 +980,24 @@ void launch_gemm(const TmaPlan &P, const Layer &L, int64_t M, void *out, cudaStr
   const int grid = (int)std::min<int64_t>((int64_t)n_m * n_n, num_sms());
   TmaGeom G{P.im2col, L.OH, L.OW, L.S, L.KW, L.C};
   launch_pdl(k_gemm_tma<BN, KB>, dim3(grid), dim3(kThreads), (size_t)C::SMEM, st, *(const CUtensorMap *)P.mapA,
-             *(const CUtensorMap *)P.mapB, L, G, M, out, n_m, n_n);
+             *(const CUtensorMap *)P.mapB, L, G, M, out, n_m, n_n, (uint32_t)C::A_BYTES);
+}
+
+// Tiny fc batches (M <= 32 rows: the prologue's [roots | level-1 children] at one root) are
+// latency-bound streams of the weights: 32-column N tiles put them on Npad/32 SMs and 32-row
+// A boxes stop every CTA from fetching 128 rows of A (~4 KB + 4 KB per k-block and CTA).
+void launch_gemm_small(const TmaPlan &P, const Layer &L, int64_t M, void *out, cudaStream_t st) {
+  using C = TmaCfg<32, 64>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_gemm_tma<32, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    attr = true;
+  }
+  const int n_n = L.Npad / 32;
+  const int grid = std::min(n_n, num_sms());
+  TmaGeom G{0, L.OH, L.OW, L.S, L.KW, L.C};
+  launch_pdl(k_gemm_tma<32, 64>, dim3(grid), dim3(kThreads), (size_t)C::SMEM, st, *(const CUtensorMap *)P.mapAs,
+             *(const CUtensorMap *)P.mapBs, L, G, M, out, 1, n_n, (uint32_t)(kSmallM * 64 * 2));
 }
 
 }  // namespace
@@ -994,6 +1050,21 @@ bool tma_plan(TmaPlan &P, const Layer &L, const void *in, int64_t cap_img) {
     r = g_encode_tiled(mb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<__nv_bfloat16 *>(L.Wt), dims, strides, box,
                        estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    P.ok_small = false;
+    if (r == CUDA_SUCCESS && !conv && KB == 64 && L.Npad % 32 == 0 && !getenv("BCTS_NO_SMALL_M")) {
+      // small-M maps: 32-row A boxes (kSmallM) and 32-row B boxes (N tiles of 32)
+      cuuint64_t adims[2] = {(cuuint64_t)L.K, (cuuint64_t)cap_img};
+      cuuint64_t astr[1] = {(cuuint64_t)L.in_img_stride * 2};
+      cuuint32_t abox[2] = {64u, (cuuint32_t)kSmallM}, bbox[2] = {64u, 32u};
+      P.ok_small = g_encode_tiled((CUtensorMap *)P.mapAs, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                                  const_cast<__nv_bfloat16 *>((const __nv_bfloat16 *)in) + L.in_col_off, adims, astr,
+                                  abox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS &&
+                   g_encode_tiled((CUtensorMap *)P.mapBs, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                                  const_cast<__nv_bfloat16 *>(L.Wt), dims, strides, bbox, estr,
+                                  CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
     P.ok2sm = false;
     if (r == CUDA_SUCCESS && !conv && KB == 64 && L.Npad % 256 == 0) {   // 2-SM GEMM: half-tile B boxes
       cuuint32_t box2[2] = {(cuuint32_t)KB, 128u};
@@ -1032,18 +1103,20 @@ bool head_plan(HeadPlan &H, const __nv_bfloat16 *hid, int64_t cap, const __nv_bf
 }
 
 void launch_zhead(const HeadPlan &H, int A, int atoms, int64_t M, float vmin, float dz, int mode, float gd,
-                  const float *cum, float *out, cudaStream_t st) {
+                  const float *cum, float *out, cudaStream_t st, KeyFold kf) {
   if (M <= 0 || atoms != 51) return;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_zhead<51>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHeadSmem);
     attr = true;
   }
-  const int n_m = (int)((M + kBM - 1) / kBM);
-  const int grid = std::min(n_m, num_sms());
+  const int n_m = (int)((M + kBM - 1) / kBM), nch = (A + 3) / 4;
+  // full-row batches smaller than the GPU: split each tile's action chunks over several CTAs
+  const int ns = mode == MODE_ROWS ? std::max(1, std::min(nch, num_sms() / n_m)) : 1;
+  const int grid = std::min(n_m * ns, num_sms());
   launch_pdl(k_zhead<51>, dim3(grid), dim3(kHeadThreads), (size_t)kHeadSmem, st, *(const CUtensorMap *)H.mapAv,
              *(const CUtensorMap *)H.mapAa, *(const CUtensorMap *)H.mapBv, *(const CUtensorMap *)H.mapBa,
-             *(const CUtensorMap *)H.mapBs, H.bias, A, M, vmin, dz, mode, gd, cum, out);
+             *(const CUtensorMap *)H.mapBs, H.bias, A, M, vmin, dz, mode, gd, cum, out, ns, kf);
 }
 
 void launch_layer_tma(const TmaPlan &P, const Layer &L, int64_t n_img, void *out, cudaStream_t st) {
