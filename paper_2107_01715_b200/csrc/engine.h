@@ -145,6 +145,7 @@ struct HeadBias {
   float v[64];         // z_v bias (atoms)
   float sum[64];       // sum over actions of the z_a bias
   float a64[64 * 64];  // z_a bias, 64 slots per action
+  float z[64];         // C51 support z_t = v_min + t dz (fp32, as fmaf(t, dz, v_min))
 };
 struct HeadPlan {
   bool ok = false;

@@ -514,8 +514,11 @@ int net_build(Net &net, const bcts_config &cfg, std::string &err) {
     V.H = V.W = 1; V.C = 512; V.K = 512; V.relu_bf16 = 0; V.out_ld = Nv; V.in_img_stride = 1024; V.in_col_off = 0;
     if (make_layer(net, V, repack(atoms, Nv, 1, 1, 512, [](int o, int, int, int c) { return o * 512 + c; }, w),
                    w + atoms * 512, atoms, Nv, err)) return -1;
-    if (atoms <= 64)
+    if (atoms <= 64) {
       for (int t = 0; t < atoms; ++t) net.head.bias.v[t] = w[atoms * 512 + t];
+      for (int t = 0; t < 64; ++t)   // the kernel's former in-loop support value, fmaf(t, dz, v_min)
+        net.head.bias.z[t] = std::fmaf((float)t, (net.vmax - net.vmin) / (float)(atoms - 1), net.vmin);
+    }
     w += atoms * 512 + atoms;
     Layer &Z = net.z_a;
     const int Na = round_up(A * atoms, 16);

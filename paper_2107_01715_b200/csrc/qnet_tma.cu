@@ -652,6 +652,11 @@ __device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t (&r)[64]) {
   tmem_wait_ld();
 }
 
+// Timing experiments only (env BCTS_HEAD_DBG; 0 in production, results are wrong otherwise):
+// bit 0 no softmax, bit 1 no TMEM loads, bit 2 no MMAs, bits 4-5 ring stages in use (1-3).
+// Measured (C5, 52K-leaf launch): everything off but the TMA ring still takes ~70 us of ~80, and
+// T(stages) = 37 + 102 / stages us -- the ring (3 x 32 KB beside the 128 KB resident h_a) bounds it.
+__device__ int g_head_dbg = 0;
 template <int ATOMS>
 __global__ void __launch_bounds__(kHeadThreads, 1)
     k_zhead(const __grid_constant__ CUtensorMap mapAv, const __grid_constant__ CUtensorMap mapAa,
@@ -672,6 +677,8 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
   const int n_m = (int)((M + kBM - 1) / kBM);
   const int nch = (A + 3) / 4;                       // z_a chunks of 4 actions (256 columns)
   const int cpc = (nch + ns - 1) / ns, n_work = n_m * ns;
+  const int dbg = g_head_dbg;
+  const int nst = ((dbg >> 4) & 3) ? ((dbg >> 4) & 3) : kHeadStages;   // ring stages in use (experiments)
   if (threadIdx.x == 0) {
     for (int i = 0; i < kHeadStages; ++i) {
       mbar_init(&full[i], 1);
@@ -701,8 +708,8 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
     if (lane == 0) {   // ------------------------------------------------ TMA producer
       uint32_t it = 0, tl = 0;
       auto slot_wait = [&](uint32_t bytes) {
-        const int st = it % kHeadStages;
-        mbar_wait(&empty[st], ((it / kHeadStages) & 1u) ^ 1u);
+        const int st = it % nst;
+        mbar_wait(&empty[st], ((it / nst) & 1u) ^ 1u);
         mbar_expect_tx(&full[st], bytes);
         return st;
       };
@@ -749,15 +756,16 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
         const uint32_t idesc = idesc_bf16(kBM, nt);
         const int nkb = j == 1 ? 16 : 8;
         for (int kb = 0; kb < nkb; ++kb, ++it) {
-          const int st = it % kHeadStages;
-          mbar_wait(&full[st], (it / kHeadStages) & 1u);
+          const int st = it % nst;
+          mbar_wait(&full[st], (it / nst) & 1u);
           tc_fence_after();
           const uint32_t slot = saddr(sRing + st * kHeadSlot);
           const uint64_t ad = sdesc<64>(j == 0 ? slot : saddr(sA + (kb & 7) * 16384));
           const uint64_t bd = sdesc<64>(j == 0 ? slot + 16384 : slot);
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
-            mma_pred(tmem + b * 256, ad + (uint64_t)(2 * kk), bd + (uint64_t)(2 * kk), idesc, (kb | kk) != 0, elected);
+            mma_pred(tmem + b * 256, ad + (uint64_t)(2 * kk), bd + (uint64_t)(2 * kk), idesc, (kb | kk) != 0,
+                     (dbg & 4) ? 0u : elected);
           commit_pred(&empty[st], elected);
         }
         commit_pred(&tfull[b], elected);
@@ -807,7 +815,12 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
         tc_fence_after();
         const int na = min(4, A - 4 * c);
         for (int s = grp; s < na; s += 2) {
+          if (dbg & 2) continue;
           tmem_ld64(tmem + b * 256 + lanes + (uint32_t)(s * 64), x);
+          if (dbg & 1) {
+            best = fmaxf(best, __uint_as_float(x[0]));
+            continue;
+          }
           const int a = 4 * c + s;
           float mx = -INFINITY;
 #pragma unroll
@@ -815,12 +828,16 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
             x[t] = __float_as_uint(v[t] + (__uint_as_float(x[t]) + hb.a64[a * 64 + t]));   // logit
             mx = fmaxf(mx, __uint_as_float(x[t]));
           }
+          // exp(l - max) = 2^(l log2e - max log2e): one FFMA + MUFU.EX2 per atom (expf's range
+          // reduction is ~5 more instructions; the epilogue's issue rate bounds this kernel)
+          const float mxs = mx * 1.4426950408889634f;
           float den = 0.0f, num = 0.0f;
 #pragma unroll
           for (int t = 0; t < ATOMS; ++t) {
-            const float ex = expf(__uint_as_float(x[t]) - mx);
+            float ex;
+            asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(ex) : "f"(fmaf(__uint_as_float(x[t]), 1.4426950408889634f, -mxs)));
             den += ex;
-            num += (vmin + (float)t * dz) * ex;
+            num = fmaf(hb.z[t], ex, num);   // support z_t = v_min + t dz (constant bank)
           }
           const float qa = num / den;
           if (mode == MODE_ROWS && m < M) out[m * A + a] = qa;
@@ -1098,6 +1115,7 @@ bool head_plan(HeadPlan &H, const __nv_bfloat16 *hid, int64_t cap, const __nv_bf
       !enc(H.mapBv, wv64, 512, 64, 512, 64) || !enc(H.mapBa, wa64, 512, (uint64_t)A * 64, 512, 256) ||
       !enc(H.mapBs, wsum, 512, 128, 512, 64))
     return false;
+
   H.ok = true;
   return true;
 }
@@ -1111,6 +1129,14 @@ void launch_zhead(const HeadPlan &H, int A, int atoms, int64_t M, float vmin, fl
     attr = true;
   }
   const int n_m = (int)((M + kBM - 1) / kBM), nch = (A + 3) / 4;
+  static bool dbg_set = false;
+  if (!dbg_set) {
+    dbg_set = true;
+    if (const char *e = getenv("BCTS_HEAD_DBG")) {
+      const int d = atoi(e);
+      cudaMemcpyToSymbol(g_head_dbg, &d, sizeof(d));
+    }
+  }
   // full-row batches smaller than the GPU: split each tile's action chunks over several CTAs
   const int ns = mode == MODE_ROWS ? std::max(1, std::min(nch, num_sms() / n_m)) : 1;
   const int grid = std::min(n_m * ns, num_sms());
