@@ -103,7 +103,15 @@ __global__ void k_finalize(FinalizeArgs f) {
       // delta_a = fmaf(g1, max_a' Q(s1^a, a'), R1_a) - Q(s0, a)   (Prop. 1; R7)
       double dob = 0.0, sum = 0.0;
       for (int a = 0; a < A; ++a) {
-        const float delta = fmaf(f.g1, f.m1[r * A + a], f.r1[r * A + a]) - f.q0[r * A + a];
+        float m1 = 0.0f;
+        if (f.rows1) {   // max_a' Q_hat(s_1^a, a') from the prologue's rows (fmaxf is exact)
+          const float *row = f.rows1 + (r * A + a) * A;
+          m1 = row[0];
+          for (int b = 1; b < A; ++b) m1 = fmaxf(m1, row[b]);
+        } else {
+          m1 = f.m1[r * A + a];
+        }
+        const float delta = fmaf(f.g1, m1, f.r1[r * A + a]) - f.q0[r * A + a];
         if (a == pio) dob = fabs((double)delta);
         else sum += fabs((double)delta);
       }

@@ -315,8 +315,12 @@ bcts_status run_shard(bcts_handle h, const void *roots, int32_t d, float gamma, 
 // With the level-1 terms needed, each step copies its roots' states next to their expanded
 // children and evaluates the batch [roots | children] once in full-row mode (one set of net
 // launches instead of two; the prologue's batches are tiny, so its cost is launch latency).
+// When every root fits in one prologue step the finalize kernel reads the batch's rows and R_1
+// in place (*direct set: q0 -> the root rows, *rows1 -> the level-1 rows, r1 -> R_1), which saves
+// two copies and the row-max kernel; otherwise they are gathered into q0 / m1 / r1 per step.
 bcts_status run_prologue(bcts_handle h, const void *roots, int64_t n, float gamma, bool need_level1, float *q0,
-                         float *m1, float *r1, size_t reserved, bcts_stats *stats) {
+                         float *m1, float *r1, size_t reserved, bcts_stats *stats, const float **dq0 = nullptr,
+                         const float **drows1 = nullptr, const float **dr1 = nullptr) {
   const int A = h->A;
   if (!need_level1) {
     const int nl = net_eval(h->net, root_view(h->env, roots, 0), n, MODE_ROWS, 0.0f, q0, h->st);
@@ -345,10 +349,17 @@ bcts_status run_prologue(bcts_handle h, const void *roots, int64_t n, float gamm
     launch_expand(h->env, root_view(h->env, roots, r0), r0, r0 * A, r1e * A, A, g[0], h->em, co, h->st, &h->prof);
     const int nl = net_eval(h->net, view_of(h->env, b), nr + cnt, MODE_ROWS, 0.0f, rows, h->st);
     if (nl < 0) return fail(h, BCTS_ERR_CUDA, "net_eval (prologue)");
-    cudaMemcpyAsync(q0 + r0 * A, rows, (size_t)nr * A * 4, cudaMemcpyDeviceToDevice, h->st);
-    launch_rowmax(rows + nr * A, cnt, A, m1 + r0 * A, h->st);
-    cudaMemcpyAsync(r1 + r0 * A, b.cum + nr, (size_t)cnt * 4, cudaMemcpyDeviceToDevice, h->st);
-    h->launches += 2 + nl;
+    if (nr == n && dq0 && drows1 && dr1) {   // one step: finalize reads the rows in place
+      *dq0 = rows;
+      *drows1 = rows + nr * A;
+      *dr1 = b.cum + nr;
+      h->launches += 1 + nl;
+    } else {
+      cudaMemcpyAsync(q0 + r0 * A, rows, (size_t)nr * A * 4, cudaMemcpyDeviceToDevice, h->st);
+      launch_rowmax(rows + nr * A, cnt, A, m1 + r0 * A, h->st);
+      cudaMemcpyAsync(r1 + r0 * A, b.cum + nr, (size_t)cnt * 4, cudaMemcpyDeviceToDevice, h->st);
+      h->launches += 2 + nl;
+    }
     if (stats) {
       stats->evaluated += nr + cnt;
       stats->transitions += cnt;
@@ -372,8 +383,9 @@ bcts_status finalize_impl(bcts_handle h, const void *roots, int64_t n, int32_t d
   float *q0 = (float *)cc.take((size_t)n * A * 4);
   float *m1 = (float *)cc.take((size_t)n * A * 4);
   float *r1 = (float *)cc.take((size_t)n * A * 4);
+  const float *dq0 = nullptr, *drows1 = nullptr, *dr1 = nullptr;
   if (need_q0) {
-    s = run_prologue(h, roots, n, gamma, corr && d >= 1, q0, m1, r1, reserved + cc.off, stats);
+    s = run_prologue(h, roots, n, gamma, corr && d >= 1, q0, m1, r1, reserved + cc.off, stats, &dq0, &drows1, &dr1);
     if (s) return s;
   }
   float g[kMaxDepth + 1];
@@ -382,6 +394,7 @@ bcts_status finalize_impl(bcts_handle h, const void *roots, int64_t n, int32_t d
   f.n = n; f.A = A; f.d = d; f.corr = corr; f.clamp = (h->flags & BCTS_F_CLAMP_PENALTY) ? 1 : 0;
   f.beta = beta; f.g1 = d >= 1 ? g[1] : 0.0f; f.gd = g[d];
   f.keys = keys; f.q0 = q0; f.m1 = m1; f.r1 = r1;
+  if (drows1) f.q0 = dq0, f.m1 = nullptr, f.rows1 = drows1, f.r1 = dr1;
   f.actions = o.actions; f.root_q = o.root_q; f.vanilla = o.vanilla; f.terms = o.terms; f.best_leaf = o.best_leaf;
   launch_finalize(f, h->st, &h->prof);
   h->launches += 1;

@@ -288,7 +288,8 @@ struct FinalizeArgs {
   float beta = 0.f, g1 = 0.f, gd = 0.f;
   const int64_t *keys = nullptr;  // [n*A] (d >= 1)
   const float *q0 = nullptr;      // [n*A] root rows (corr or d == 0)
-  const float *m1 = nullptr;      // [n*A] max_a Q_hat(s_1^a, .) (corr, d >= 1)
+  const float *m1 = nullptr;      // [n*A] max_a Q_hat(s_1^a, .) (corr, d >= 1), or:
+  const float *rows1 = nullptr;   // [n*A][A] the level-1 Q rows themselves (m1 taken as their row max)
   const float *r1 = nullptr;      // [n*A] R_1 of the root's children (corr, d >= 1)
   int32_t *actions = nullptr;
   float *root_q = nullptr, *vanilla = nullptr, *terms = nullptr;
