@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define BCTS_ABI_VERSION 3   /* 2: env_weights fields + BCTS_ENV_DNN; 3: bcts_search_pruned */
+#define BCTS_ABI_VERSION 4   /* 2: env_weights fields + BCTS_ENV_DNN; 3: bcts_search_pruned; 4: bcts_kernel_profile largest-launch fields */
 
 typedef struct bcts_handle_t *bcts_handle;
 
@@ -92,6 +92,9 @@ typedef enum {
 #define BCTS_F_SIMT_NET 0x2u      /* use the SIMT reference net (no tensor cores) */
 #define BCTS_F_MATERIALIZE_LEAVES 0x4u /* store the leaf level (else leaf frames are
                                         * generated inside the net's A-operand producer) */
+#define BCTS_F_SEPARATE_BACKUP 0x8u /* run the segmented-max backup (Alg. 1) as its own kernel
+                                     * instead of inside the Rainbow head's epilogue; same result bit
+                                     * for bit (the max over packed keys is order-independent) */
 
 typedef struct {
   uint32_t abi_version;     /* must be BCTS_ABI_VERSION */

@@ -289,8 +289,8 @@ bcts_status run_shard(bcts_handle h, const void *roots, int32_t d, float gamma, 
       kf.lpr = pw[d];
       kf.seg = pw[d - 1];
       kf.A = A;
-      nl = net_eval_children(h->net, prev, lo[d - 1], L, Le, A, g[d - 1], MODE_TOTAL, g[d], totals, h->st, &kf,
-                             &folded);
+      nl = net_eval_children(h->net, prev, lo[d - 1], L, Le, A, g[d - 1], MODE_TOTAL, g[d], totals, h->st,
+                             (h->flags & BCTS_F_SEPARATE_BACKUP) ? nullptr : &kf, &folded);
       trans += Le - L;
     } else {
       nl = net_eval(h->net, prev, Le - L, MODE_TOTAL, g[d], totals, h->st);

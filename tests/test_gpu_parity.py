@@ -455,6 +455,20 @@ def test_pv_targets_bad_action_and_args():
 
 
 # ------------------------------------------------- fused leaf level vs materialised leaves
+@pytest.mark.parametrize("cname,n,d", [("C5", 1, 3), ("C4", 3, 4)])
+def test_head_backup_bit_identical(cname, n, d):
+    """The backup folded into the Rainbow head's epilogue (Alg. 1: warp max + atomicMax on
+    packed (total, leaf) keys) equals the separate k_segmax pass bit for bit: both fold the same
+    leaf totals and the max over packed keys is exact and order-independent (R4)."""
+    cfg = config(cname)
+    roots = cfg.roots(n)
+    a = run(handle(cname), roots, d, cfg.gamma, 1.0, 1)
+    b = run(handle(cname, flags=P.F_SEPARATE_BACKUP), roots, d, cfg.gamma, 1.0, 1)
+    for k in ("actions", "root_q", "vanilla_q", "terms", "best_leaf"):
+        np.testing.assert_array_equal(a[k], b[k])
+    assert a["stats"]["kernel_launches"] < b["stats"]["kernel_launches"]
+
+
 @pytest.mark.parametrize("cname,n,d", [("C3", 3, 2), ("C5", 1, 2), ("C5", 1, 3), ("C4", 2, 3)])
 def test_fused_leaves_match_materialized(cname, n, d):
     """k_conv1_sib (leaf expansion fused into conv1, sibling-factorised, fp16 operands with exact
