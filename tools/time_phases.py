@@ -21,6 +21,7 @@ ap.add_argument("--config", default="C5")
 ap.add_argument("--depth", type=int, default=0)
 ap.add_argument("--roots", type=int, default=0)
 ap.add_argument("--iters", type=int, default=20)
+ap.add_argument("--world", type=int, default=1, help="time rank 0's share of a world-size-W partition")
 a = ap.parse_args()
 cfg = config(a.config)
 n = a.roots or cfg.n_roots
@@ -31,6 +32,7 @@ roots = torch.from_numpy(cfg.roots(n).view(np.uint8).copy()).to(dev)
 keys = torch.empty(n * cfg.A, dtype=torch.int64, device=dev)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 L = n * cfg.A ** d
+b, e = P.shard_range(n, d, cfg.A, 0, a.world)
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
 tot = np.zeros(2)
 for it in range(a.iters + 3):
@@ -38,7 +40,7 @@ for it in range(a.iters + 3):
     torch.cuda.synchronize()
     ev[0].record()
     h.keys_init(keys)
-    h.search_shard(roots, n, d, cfg.gamma, 0, L, keys)
+    h.search_shard(roots, n, d, cfg.gamma, b, e, keys)
     ev[1].record()
     h.finalize(roots, n, d, cfg.gamma, cfg.beta, 1, keys, extra=False)
     ev[2].record()
@@ -46,5 +48,5 @@ for it in range(a.iters + 3):
     if it >= 3:
         tot += [ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])]
 tot /= a.iters
-print(f"{a.config} n={n} d={d}: shard {tot[0]:.3f} ms, finalize (prologue + Eq. 3/5) {tot[1]:.3f} ms, "
+print(f"{a.config} n={n} d={d} rank 0 of {a.world} (leaves [{b}, {e})): shard {tot[0]:.3f} ms, finalize (prologue + Eq. 3/5) {tot[1]:.3f} ms, "
       f"total {tot.sum():.3f} ms")
