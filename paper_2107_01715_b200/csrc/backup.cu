@@ -76,42 +76,57 @@ __device__ double B_of_n(double n) {
   return gem * normcdfinv(1.0 - 1.0 / (2.718281828459045 * n)) + (1.0 - gem) * normcdfinv(1.0 - 1.0 / n);
 }
 
-// One thread per root.
+// One warp per root, lane a (and a + 32) owns action a: the loads and the level-1 row maxima run
+// in parallel across the lanes; the order-sensitive double sum of |delta_a| (R6: increasing a) and
+// the Eq. 5 arithmetic run on lane 0 in exactly the sequential order of the single-thread form.
 __global__ void k_finalize(FinalizeArgs f) {
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= f.n) return;
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x % 32;
+  if (r >= f.n) return;   // warp-uniform
   const int A = f.A;
-  float van[kMaxA], q[kMaxA];
-  float terms[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int a = 0; a < A; ++a) {
+  float van[2], q0v[2], dl[2];
+  for (int h = 0; h < 2; ++h) {
+    const int a = lane + 32 * h;
+    van[h] = q0v[h] = dl[h] = 0.0f;
+    if (a >= A) continue;
     if (f.d == 0) {
-      van[a] = f.q0[r * A + a];
+      van[h] = f.q0[r * A + a];
       if (f.best_leaf) f.best_leaf[r * A + a] = 0;
     } else {
       const int64_t k = f.keys[r * A + a];
-      van[a] = key_value(k);
+      van[h] = key_value(k);
       if (f.best_leaf) f.best_leaf[r * A + a] = key_leaf(k);
     }
-    q[a] = van[a];
-  }
-  if (f.d == 0 || f.corr) {
-    int pio = 0;                           // pi_o = lowest argmax of Q_hat(s0, .) (R23)
-    for (int a = 1; a < A; ++a)
-      if (f.q0[r * A + a] > f.q0[r * A + pio]) pio = a;
-    terms[0] = (float)pio;
-    if (f.d >= 1) {
-      // delta_a = fmaf(g1, max_a' Q(s1^a, a'), R1_a) - Q(s0, a)   (Prop. 1; R7)
-      double dob = 0.0, sum = 0.0;
-      for (int a = 0; a < A; ++a) {
-        float m1 = 0.0f;
-        if (f.rows1) {   // max_a' Q_hat(s_1^a, a') from the prologue's rows (fmaxf is exact)
+    if (f.d == 0 || f.corr) {
+      q0v[h] = f.q0[r * A + a];
+      if (f.d >= 1) {   // delta_a = fmaf(g1, max_a' Q(s1^a, a'), R1_a) - Q(s0, a)   (Prop. 1; R7)
+        float m1;
+        if (f.rows1) {  // max over the level-1 row (fmaxf is exact)
           const float *row = f.rows1 + (r * A + a) * A;
           m1 = row[0];
           for (int b = 1; b < A; ++b) m1 = fmaxf(m1, row[b]);
         } else {
           m1 = f.m1[r * A + a];
         }
-        const float delta = fmaf(f.g1, m1, f.r1[r * A + a]) - f.q0[r * A + a];
+        dl[h] = fmaf(f.g1, m1, f.r1[r * A + a]) - q0v[h];
+      }
+    }
+  }
+  float terms[4] = {0.f, 0.f, 0.f, 0.f};
+  double pen = 0.0;
+  int pio = 0;
+  if (f.d == 0 || f.corr) {
+    // pi_o = lowest argmax of Q_hat(s0, .) (R23), gathered in increasing a on every lane
+    float best = -INFINITY;
+    for (int a = 0; a < A; ++a) {
+      const float v = __shfl_sync(0xffffffffu, q0v[a >> 5], a & 31);
+      if (a == 0 || v > best) best = v, pio = a;
+    }
+    terms[0] = (float)pio;
+    if (f.d >= 1) {
+      double dob = 0.0, sum = 0.0;
+      for (int a = 0; a < A; ++a) {
+        const float delta = __shfl_sync(0xffffffffu, dl[a >> 5], a & 31);
         if (a == pio) dob = fabs((double)delta);
         else sum += fabs((double)delta);
       }
@@ -127,29 +142,36 @@ __global__ void k_finalize(FinalizeArgs f) {
       terms[1] = (float)dob;
       terms[2] = (float)de;
       terms[3] = (float)B;
-      if (f.beta != 0.0f) {                 // Eq. 3: subtract beta*g_d*B from a != pi_o (R9, R12)
-        const double pen = (double)f.beta * (double)f.gd * B;
-        for (int a = 0; a < A; ++a)
-          if (a != pio) q[a] = (float)((double)van[a] - pen);
-      }
+      if (f.beta != 0.0f) pen = (double)f.beta * (double)f.gd * B;   // Eq. 3 (R9, R12)
     }
   }
-  int best = 0;
-  for (int a = 1; a < A; ++a)
-    if (q[a] > q[best]) best = a;          // lowest index attaining the max (R4)
-  f.actions[r] = best;
-  for (int a = 0; a < A; ++a) {
-    f.root_q[r * A + a] = q[a];
-    if (f.vanilla) f.vanilla[r * A + a] = van[a];
+  float q[2];
+  for (int h = 0; h < 2; ++h) {
+    const int a = lane + 32 * h;
+    q[h] = (pen != 0.0 && a != pio) ? (float)((double)van[h] - pen) : van[h];
+    if (a < A) {
+      f.root_q[r * A + a] = q[h];
+      if (f.vanilla) f.vanilla[r * A + a] = van[h];
+    }
   }
-  if (f.terms)
-    for (int k = 0; k < 4; ++k) f.terms[r * 4 + k] = terms[k];
+  // lowest index attaining the max of q (R4), gathered in increasing a
+  int best = 0;
+  float bq = 0.0f;
+  for (int a = 0; a < A; ++a) {
+    const float v = __shfl_sync(0xffffffffu, q[a >> 5], a & 31);
+    if (a == 0 || v > bq) bq = v, best = a;
+  }
+  if (lane == 0) {
+    f.actions[r] = best;
+    if (f.terms)
+      for (int k = 0; k < 4; ++k) f.terms[r * 4 + k] = terms[k];
+  }
 }
 
 void launch_finalize(const FinalizeArgs &a, cudaStream_t st, Profiler *prof) {
   if (a.n <= 0) return;
   if (prof) prof->begin(KC_FINALIZE, (double)a.n * a.A * 28.0, st);
-  k_finalize<<<(unsigned)((a.n + 127) / 128), 128, 0, st>>>(a);
+  k_finalize<<<(unsigned)((a.n + 3) / 4), 128, 0, st>>>(a);   // one warp per root
   if (prof) prof->end(st);
 }
 

@@ -245,7 +245,7 @@ size_t finalize_ws(bcts_handle h, int64_t n, size_t reserved) {
 // Leaf-range search: expand the ancestors of leaves [L0, L1), score the leaves,
 // fold the totals into keys (K1 -> K2 -> K3a per chunk).
 bcts_status run_shard(bcts_handle h, const void *roots, int32_t d, float gamma, int64_t L0, int64_t L1,
-                      int64_t *keys, size_t reserved, bcts_stats *stats) {
+                      int64_t *keys, size_t reserved, bcts_stats *stats, PrologueFold *pf = nullptr) {
   const int A = h->A;
   if (L1 <= L0 || d < 1) return BCTS_OK;
   float g[kMaxDepth + 1];
@@ -290,7 +290,7 @@ bcts_status run_shard(bcts_handle h, const void *roots, int32_t d, float gamma, 
       kf.seg = pw[d - 1];
       kf.A = A;
       nl = net_eval_children(h->net, prev, lo[d - 1], L, Le, A, g[d - 1], MODE_TOTAL, g[d], totals, h->st,
-                             (h->flags & BCTS_F_SEPARATE_BACKUP) ? nullptr : &kf, &folded);
+                             (h->flags & BCTS_F_SEPARATE_BACKUP) ? nullptr : &kf, &folded, pf);
       trans += Le - L;
     } else {
       nl = net_eval(h->net, prev, Le - L, MODE_TOTAL, g[d], totals, h->st);
@@ -374,8 +374,11 @@ struct Outs {
   int64_t *best_leaf;
 };
 
+// pre (nullable): the prologue was already evaluated (folded into a leaf batch, PrologueFold):
+// pre->rows_out holds the Q rows of [roots | level-1 children] and pre->view.cum their R.
 bcts_status finalize_impl(bcts_handle h, const void *roots, int64_t n, int32_t d, float gamma, float beta,
-                          int32_t corr, const int64_t *keys, const Outs &o, size_t reserved, bcts_stats *stats) {
+                          int32_t corr, const int64_t *keys, const Outs &o, size_t reserved, bcts_stats *stats,
+                          const PrologueFold *pre = nullptr) {
   const int A = h->A;
   const bool need_q0 = corr || d == 0;
   bcts_status s = BCTS_OK;
@@ -384,7 +387,15 @@ bcts_status finalize_impl(bcts_handle h, const void *roots, int64_t n, int32_t d
   float *m1 = (float *)cc.take((size_t)n * A * 4);
   float *r1 = (float *)cc.take((size_t)n * A * 4);
   const float *dq0 = nullptr, *drows1 = nullptr, *dr1 = nullptr;
-  if (need_q0) {
+  if (pre && pre->done && corr && d >= 1) {
+    dq0 = pre->rows_out;
+    drows1 = pre->rows_out + n * A;
+    dr1 = pre->view.cum + n;
+    if (stats) {
+      stats->evaluated += n * (A + 1);
+      stats->transitions += n * A;
+    }
+  } else if (need_q0) {
     s = run_prologue(h, roots, n, gamma, corr && d >= 1, q0, m1, r1, reserved + cc.off, stats, &dq0, &drows1, &dr1);
     if (s) return s;
   }
@@ -750,7 +761,20 @@ bcts_status bcts_search_ex(bcts_handle h, const void *roots, int64_t n_roots, in
   ipow_ok(A, depth, lpr);
   // keys live at the front of the workspace; the shard and finalize phases
   // reuse the space after them (stream-ordered). Size everything up front.
-  const size_t kbytes = align_up((size_t)n_roots * A * 8);
+  const size_t kbytes0 = align_up((size_t)n_roots * A * 8);
+  // With the level-1 terms needed and a conv net generating the leaves, the prologue's states
+  // [roots | level-1 children] are expanded up front into a region after the keys and evaluated
+  // inside a leaf batch (PrologueFold; finalize then only reads their rows).
+  const bool try_fold = depth >= 1 && correction_on && fused_leaves(h) && h->net.kind == BCTS_NET_RAINBOW_BF16 &&
+                        n_roots * (A + 1) <= (int64_t)4096 && !getenv("BCTS_NO_PROLOGUE_FOLD");
+  size_t pbytes = 0;
+  if (try_fold) {
+    Carver pc(nullptr);
+    pc.level(h->env, n_roots * (A + 1));
+    pc.take((size_t)n_roots * (A + 1) * A * 4);
+    pbytes = align_up(pc.off);
+  }
+  const size_t kbytes = kbytes0 + pbytes;
   size_t need = finalize_ws(h, n_roots, kbytes);
   if (depth >= 1) {
     const size_t sw = shard_ws(h, n_roots * lpr, kbytes);
@@ -759,14 +783,35 @@ bcts_status bcts_search_ex(bcts_handle h, const void *roots, int64_t n_roots, in
   }
   if ((s = ensure_ws(h, kbytes + need))) return s;
   int64_t *keys = (int64_t *)h->ws;
+  PrologueFold pf;
+  if (try_fold) {   // slots [0, n): the roots' states; [n, n + nA): their children (Alg. 1 body)
+    Carver pc(h->ws + kbytes0);
+    LevelBuf b = pc.level(h->env, n_roots * (A + 1));
+    pf.rows_out = (float *)pc.take((size_t)n_roots * (A + 1) * A * 4);
+    float g1[2];
+    discounts(gamma, 1, g1);
+    const int64_t sb = state_bytes(h->env), rb = record_bytes(h->env);
+    const NodeView rv = root_view(h->env, roots, 0);
+    cudaMemcpy2DAsync(b.state, (size_t)sb, rv.state, (size_t)rb, (size_t)sb, (size_t)n_roots,
+                      cudaMemcpyDeviceToDevice, h->st);
+    NodeOut co = out_of(h->env, b);
+    co.state += n_roots * sb;
+    if (co.key) co.key += n_roots;
+    co.cum += n_roots;
+    launch_expand(h->env, rv, 0, 0, n_roots * A, A, g1[0], h->em, co, h->st, &h->prof);
+    h->launches += 1;
+    pf.view = view_of(h->env, b);
+    pf.ne = n_roots * (A + 1);
+  }
   if (depth >= 1) {
     launch_keys_init(keys, n_roots * A, h->st);
     h->launches += 1;
-    s = run_shard(h, roots, depth, gamma, 0, n_roots * lpr, keys, kbytes, stats);
+    s = run_shard(h, roots, depth, gamma, 0, n_roots * lpr, keys, kbytes, stats, try_fold ? &pf : nullptr);
     if (s) return s;
   }
   Outs o{actions_out, root_q_out, vanilla_q_out, terms_out, best_leaf_out};
-  s = finalize_impl(h, roots, n_roots, depth, gamma, beta, correction_on, keys, o, kbytes, stats);
+  s = finalize_impl(h, roots, n_roots, depth, gamma, beta, correction_on, keys, o, kbytes, stats,
+                    try_fold ? &pf : nullptr);
   if (stats) stats->kernel_launches = h->launches - l0;
   return s;
 }

@@ -167,8 +167,11 @@ struct KeyFold {
   int64_t leaf0 = 0, lpr = 1, seg = 1;
   int A = 0;
 };
+// rows_out != NULL: rows [mrow0, M) are full-row rows (Q_hat(s, .) -> rows_out[(m - mrow0) * A + a]);
+// only rows below mrow0 produce totals / keys.
 void launch_zhead(const HeadPlan &H, int A, int atoms, int64_t M, float vmin, float dz, int mode, float gd,
-                  const float *cum, float *out, cudaStream_t st, KeyFold kf = KeyFold());
+                  const float *cum, float *out, cudaStream_t st, KeyFold kf = KeyFold(), int64_t mrow0 = 0,
+                  float *rows_out = nullptr);
 void launch_layer_tma(const TmaPlan &P, const Layer &L, int64_t n_img, void *out, cudaStream_t st);
 
 // Shifted-window conv layer (qnet_conv.cu): stride-1 conv over a per-image
@@ -265,9 +268,19 @@ int net_eval(Net &net, const NodeView &v, int64_t n, int mode, float gd, float *
 bool net_fuses_leaves(const Net &net);
 // kf (nullable): fold the totals into packed keys inside the head when it supports it
 // (*folded set to true); otherwise the caller runs the backup kernel.
+// pf (nullable): the finalize prologue's materialised states [roots | level-1 children] ride along
+// in the last leaf batch that has room for them (conv1 on the explicit states, then the batch's
+// conv2+conv3 / fc / head launches); their Q rows land in pf->rows_out and pf->done is set. The
+// prologue's own four launches (its latency-bound tiny batch) disappear from the step.
+struct PrologueFold {
+  NodeView view;
+  int64_t ne = 0;
+  float *rows_out = nullptr;
+  bool done = false;
+};
 int net_eval_children(Net &net, const NodeView &par, int64_t p_first, int64_t c_begin, int64_t c_end, int A,
                       float gk, int mode, float gd, float *out, cudaStream_t st, const KeyFold *kf = nullptr,
-                      bool *folded = nullptr);
+                      bool *folded = nullptr, PrologueFold *pf = nullptr);
 int net_build(Net &net, const bcts_config &cfg, std::string &err);  // 0 ok
 void net_free(Net &net);
 

@@ -685,7 +685,8 @@ static bool c23_enabled() {
 // sub-batches: frames -> s2d bf16 -> conv1 -> conv2 -> conv3 (act3 of the fc
 // batch); then fc_hidden, the output layer(s) and the head.
 static int eval_conv(Net &net, const NodeView *par, const NodeView *img, int64_t p_first, int64_t c_begin, float gk,
-                     int64_t n, int mode, float gd, float *out, cudaStream_t st, const KeyFold *kf = nullptr) {
+                     int64_t n, int mode, float gd, float *out, cudaStream_t st, const KeyFold *kf = nullptr,
+                     PrologueFold *pf = nullptr) {
   const int A = net.A;
   const bool rainbow = net.kind == BCTS_NET_RAINBOW_BF16;
   int launches = 0;
@@ -696,6 +697,12 @@ static int eval_conv(Net &net, const NodeView *par, const NodeView *img, int64_t
     const int64_t nf = n - f0 < step ? n - f0 : step;
     const bool fused_leaf = par && net.tc && net.sw;
     const int64_t tb = fused_leaf ? (c23_enabled() ? net.batch : net.mat_batch) : net.mat_batch;
+    // the prologue's states ride along in this (last) batch when it has room (PrologueFold)
+    const int64_t ne = (pf && !pf->done && f0 + nf >= n && fused_leaf && c23_enabled() && mode == MODE_TOTAL &&
+                        net.kind == BCTS_NET_RAINBOW_BF16 && net.head.ok && nf <= tb && nf + pf->ne <= net.batch &&
+                        nf + pf->ne <= net.fc_batch && pf->ne <= net.mat_batch)
+                           ? pf->ne
+                           : 0;
     for (int64_t b0 = 0; b0 < nf; b0 += tb) {
       const int64_t nb = nf - b0 < tb ? nf - b0 : tb;
       const bool sw = net.tc && net.sw;
@@ -708,9 +715,19 @@ static int eval_conv(Net &net, const NodeView *par, const NodeView *img, int64_t
         launch_conv1_sib(net.sw1, net.c1, net.w1_shared, net.w1_new, *par, p_first, c_begin + f0 + b0, nb, A, gk,
                          net.act1p, net.leaf_cum + b0, st);
         if (net.prof) net.prof->end(st);
+        if (ne) {   // conv1 of the prologue's explicit states, appended after the batch's act1 images
+          if (net.prof) net.prof->begin(KC_OTHER, (double)ne * (kFrameBytes + 2.0 * 28224), st);
+          launch_s2d_convert(pf->view, 0, ne, net.in1p, kPlane1, st, net.sw1.layout);
+          if (net.prof) net.prof->end(st);
+          if (net.prof) net.prof->begin(KC_CONV1, 2.0 * (double)ne * 400 * 32 * 256, st);
+          launch_conv_sw(net.sw1, net.c1, net.in1p, ne, (uint8_t *)net.act1p + nb * (int64_t)kIn2Bytes, st);
+          if (net.prof) net.prof->end(st);
+          launches += 2;
+        }
         if (c23_enabled()) {   // conv2 + conv3 fused: act2 never leaves the SM
-          if (net.prof) net.prof->begin(KC_CONV23, fl * (81 * 64 * 512 + 49 * 64 * 576), st);
-          launch_conv23(net.sw2, net.c2s, net.sw3, net.c3, net.act1p, nb, net.act3 + b0 * 3136, st);
+          const double fl2 = 2.0 * (double)(nb + ne);
+          if (net.prof) net.prof->begin(KC_CONV23, fl2 * (81 * 64 * 512 + 49 * 64 * 576), st);
+          launch_conv23(net.sw2, net.c2s, net.sw3, net.c3, net.act1p, nb + ne, net.act3 + b0 * 3136, st);
           if (net.prof) net.prof->end(st);
           launches += 2;
         } else {
@@ -757,7 +774,7 @@ static int eval_conv(Net &net, const NodeView *par, const NodeView *img, int64_t
       }
       launches += 4;
     }
-    run_layer(net, KC_FC_H, net.fc_h, net.act3, nf, net.hid_act, st, &net.p_fc_h);
+    run_layer(net, KC_FC_H, net.fc_h, net.act3, nf + ne, net.hid_act, st, &net.p_fc_h);
     launches += 1;
     float *o = out + (mode == MODE_ROWS ? f0 * A : f0);
     const float *cum = par ? net.leaf_cum : (img->cum ? img->cum + f0 : nullptr);
@@ -770,13 +787,15 @@ static int eval_conv(Net &net, const NodeView *par, const NodeView *img, int64_t
       launches += 2;
     } else if (net.tc && net.head.ok) {   // z_v + z_a + dueling C51 head + max_a fused (k_zhead)
       const float dz = (net.vmax - net.vmin) / (float)(net.atoms - 1);
-      if (net.prof) net.prof->begin(KC_FC_OUT, 2.0 * (double)nf * 512.0 * (double)(net.atoms + A * net.atoms), st);
+      if (net.prof) net.prof->begin(KC_FC_OUT, 2.0 * (double)(nf + ne) * 512.0 * (double)(net.atoms + A * net.atoms), st);
       KeyFold kb;
       if (kf) {
         kb = *kf;
         kb.leaf0 += f0;
       }
-      launch_zhead(net.head, A, net.atoms, nf, net.vmin, dz, mode, gd, cum, o, st, kb);
+      launch_zhead(net.head, A, net.atoms, nf + ne, net.vmin, dz, mode, gd, cum, o, st, kb, nf,
+                   ne ? pf->rows_out : nullptr);
+      if (ne) pf->done = true;
       if (net.prof) net.prof->end(st);
       launches += 1;
     } else {
@@ -803,13 +822,15 @@ bool net_fuses_leaves(const Net &net) {
 }
 
 int net_eval_children(Net &net, const NodeView &par, int64_t p_first, int64_t c_begin, int64_t c_end, int A,
-                      float gk, int mode, float gd, float *out, cudaStream_t st, const KeyFold *kf, bool *folded) {
+                      float gk, int mode, float gd, float *out, cudaStream_t st, const KeyFold *kf, bool *folded,
+                      PrologueFold *pf) {
   (void)A;
   static const bool fold_ok = !getenv("BCTS_NO_HEAD_BACKUP");
   const bool fold = kf && kf->keys && fold_ok && mode == MODE_TOTAL && net.kind == BCTS_NET_RAINBOW_BF16 && net.tc &&
                     net.head.ok;
   if (folded) *folded = fold;
-  return eval_conv(net, &par, nullptr, p_first, c_begin, gk, c_end - c_begin, mode, gd, out, st, fold ? kf : nullptr);
+  return eval_conv(net, &par, nullptr, p_first, c_begin, gk, c_end - c_begin, mode, gd, out, st, fold ? kf : nullptr,
+                   pf);
 }
 
 int net_eval(Net &net, const NodeView &v, int64_t n, int mode, float gd, float *out, cudaStream_t st) {

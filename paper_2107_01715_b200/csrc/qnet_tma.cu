@@ -663,7 +663,9 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
             const __grid_constant__ CUtensorMap mapBv, const __grid_constant__ CUtensorMap mapBa,
             const __grid_constant__ CUtensorMap mapBs, const __grid_constant__ HeadBias hb, int A, int64_t M, float vmin,
             float dz, int mode, float gd, const float *__restrict__ cum, float *__restrict__ out, int ns,
-            const KeyFold kf) {
+            const KeyFold kf, int64_t mrow0, float *__restrict__ rows_out) {
+  // rows m >= mrow0 (MODE_TOTAL / ROWMAX batches only) are full-row rows appended to the batch
+  // (the finalize prologue's [roots | level-1 children]): Q rows -> rows_out
   // ns: work items per 128-row tile, each taking a contiguous slice of the action chunks
   // (MODE_ROWS only: tiny batches spread their z_a weight stream over ns CTAs; ns = 1 otherwise)
   static_assert(ATOMS <= 64, "one action per 64 TMEM columns");
@@ -841,6 +843,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
           }
           const float qa = num / den;
           if (mode == MODE_ROWS && m < M) out[m * A + a] = qa;
+          else if (m >= mrow0 && m < M) rows_out[(m - mrow0) * A + a] = qa;
           best = fmaxf(best, qa);
         }
         tc_fence_before();
@@ -851,7 +854,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
         asm volatile("bar.sync 1, 256;" ::: "memory");
         if (grp == 0) {
           int64_t key = kKeyEmpty, slot = -1;
-          if (m < M) {
+          if (m < M && m < mrow0) {
             best = fmaxf(best, s_best[tl & 1u][r]);
             const float tot = mode == MODE_ROWMAX ? best : fmaf(gd, best, cum ? cum[m] : 0.0f);
             out[m] = tot;
@@ -1121,7 +1124,7 @@ bool head_plan(HeadPlan &H, const __nv_bfloat16 *hid, int64_t cap, const __nv_bf
 }
 
 void launch_zhead(const HeadPlan &H, int A, int atoms, int64_t M, float vmin, float dz, int mode, float gd,
-                  const float *cum, float *out, cudaStream_t st, KeyFold kf) {
+                  const float *cum, float *out, cudaStream_t st, KeyFold kf, int64_t mrow0, float *rows_out) {
   if (M <= 0 || atoms != 51) return;
   static bool attr = false;
   if (!attr) {
@@ -1142,7 +1145,8 @@ void launch_zhead(const HeadPlan &H, int A, int atoms, int64_t M, float vmin, fl
   const int grid = std::min(n_m * ns, num_sms());
   launch_pdl(k_zhead<51>, dim3(grid), dim3(kHeadThreads), (size_t)kHeadSmem, st, *(const CUtensorMap *)H.mapAv,
              *(const CUtensorMap *)H.mapAa, *(const CUtensorMap *)H.mapBv, *(const CUtensorMap *)H.mapBa,
-             *(const CUtensorMap *)H.mapBs, H.bias, A, M, vmin, dz, mode, gd, cum, out, ns, kf);
+             *(const CUtensorMap *)H.mapBs, H.bias, A, M, vmin, dz, mode, gd, cum, out, ns, kf,
+             rows_out ? mrow0 : INT64_MAX, rows_out);
 }
 
 void launch_layer_tma(const TmaPlan &P, const Layer &L, int64_t n_img, void *out, cudaStream_t st) {
