@@ -189,7 +189,12 @@ bcts_status bcts_search_host(bcts_handle h, const void *roots_host, int64_t n_ro
  * int64 max, so shards combine with any max all-reduce (ncclMax over
  * ncclInt64, torch.distributed ReduceOp.MAX). bcts_finalize turns the
  * reduced keys into the outputs of bcts_search_ex, evaluating the depth-0/1
- * Bellman terms itself (the same on every rank). */
+ * Bellman terms itself (the same on every rank). With a Rainbow conv net and
+ * n_roots * (A + 1) <= 4096, bcts_search_shard also evaluates those depth-0/1
+ * rows inside its last leaf batch and keeps them in handle-owned memory for the
+ * next bcts_finalize with the same roots pointer, n_roots, depth and gamma (the
+ * roots' contents must not change in between); any other finalize evaluates
+ * them itself. Results are identical either way. */
 bcts_status bcts_keys_init(bcts_handle h, int64_t *keys, int64_t count);
 bcts_status bcts_search_shard(bcts_handle h, const void *roots, int64_t n_roots, int32_t depth, int32_t A,
                               float gamma, int64_t leaf_begin, int64_t leaf_end, int64_t *keys_out,

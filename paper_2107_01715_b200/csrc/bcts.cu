@@ -36,6 +36,16 @@ struct bcts_handle_t {
   std::string err;
   int64_t launches = 0;
   Profiler prof;
+  // prologue folded into a bcts_search_shard leaf batch, kept for the bcts_finalize that follows
+  // (identified by roots pointer, n_roots, depth, gamma); pbuf holds its states and rows
+  uint8_t *pbuf = nullptr;
+  size_t pbuf_size = 0;
+  PrologueFold pfs;
+  bool pfs_valid = false;
+  const void *pfs_roots = nullptr;
+  int64_t pfs_n = 0;
+  int32_t pfs_d = 0;
+  float pfs_gamma = 0.f;
 };
 
 namespace {
@@ -374,6 +384,42 @@ struct Outs {
   int64_t *best_leaf;
 };
 
+// Prologue fold (PrologueFold): bytes of the region holding [roots | level-1 children] states and
+// their Q rows, and the front end that fills the states (root copy + level-1 expansion, Alg. 1
+// body) -- the rows are produced later inside a leaf batch.
+bool fold_wanted(bcts_handle h, int64_t n, int32_t d) {
+  return d >= 1 && fused_leaves(h) && h->net.kind == BCTS_NET_RAINBOW_BF16 && n * (h->A + 1) <= (int64_t)4096 &&
+         !getenv("BCTS_NO_PROLOGUE_FOLD");
+}
+size_t fold_bytes(bcts_handle h, int64_t n) {
+  Carver pc(nullptr);
+  pc.level(h->env, n * (h->A + 1));
+  pc.take((size_t)n * (h->A + 1) * h->A * 4);
+  return align_up(pc.off);
+}
+PrologueFold fold_front(bcts_handle h, const void *roots, int64_t n, float gamma, uint8_t *region) {
+  const int A = h->A;
+  PrologueFold pf;
+  Carver pc(region);
+  LevelBuf b = pc.level(h->env, n * (A + 1));
+  pf.rows_out = (float *)pc.take((size_t)n * (A + 1) * A * 4);
+  float g1[2];
+  discounts(gamma, 1, g1);
+  const int64_t sb = state_bytes(h->env), rb = record_bytes(h->env);
+  const NodeView rv = root_view(h->env, roots, 0);
+  // slots [0, n): the roots' states; [n, n + nA): their children
+  cudaMemcpy2DAsync(b.state, (size_t)sb, rv.state, (size_t)rb, (size_t)sb, (size_t)n, cudaMemcpyDeviceToDevice, h->st);
+  NodeOut co = out_of(h->env, b);
+  co.state += n * sb;
+  if (co.key) co.key += n;
+  co.cum += n;
+  launch_expand(h->env, rv, 0, 0, n * A, A, g1[0], h->em, co, h->st, &h->prof);
+  h->launches += 1;
+  pf.view = view_of(h->env, b);
+  pf.ne = n * (A + 1);
+  return pf;
+}
+
 // pre (nullable): the prologue was already evaluated (folded into a leaf batch, PrologueFold):
 // pre->rows_out holds the Q rows of [roots | level-1 children] and pre->view.cum their R.
 bcts_status finalize_impl(bcts_handle h, const void *roots, int64_t n, int32_t d, float gamma, float beta,
@@ -608,6 +654,7 @@ void bcts_destroy(bcts_handle h) {
   cudaSetDevice(h->dev);
   if (h->st) cudaStreamSynchronize(h->st);
   net_free(h->net);
+  cudaFree(h->pbuf);
   cudaFree(h->d_next);
   cudaFree(h->d_envw);
   cudaFree(h->d_rew);
@@ -720,7 +767,31 @@ bcts_status bcts_search_shard(bcts_handle h, const void *roots, int64_t n_roots,
     if (!need) return fail(h, BCTS_ERR_BUDGET, "workspace budget too small for one chunk of leaves");
     if ((s = ensure_ws(h, need))) return s;
   }
-  s = run_shard(h, roots, depth, gamma, leaf_begin, leaf_end, keys_out, 0, stats);
+  // the finalize prologue rides along in this shard's last leaf batch; bcts_finalize picks it up
+  h->pfs_valid = false;
+  PrologueFold *pf = nullptr;
+  if (leaf_end > leaf_begin && fold_wanted(h, n_roots, depth)) {
+    const size_t pb = fold_bytes(h, n_roots);
+    if (pb > h->pbuf_size) {
+      cudaFree(h->pbuf);
+      h->pbuf = nullptr;
+      h->pbuf_size = 0;
+      if (cudaMalloc(&h->pbuf, pb) == cudaSuccess) h->pbuf_size = pb;
+      cudaGetLastError();
+    }
+    if (h->pbuf) {
+      h->pfs = fold_front(h, roots, n_roots, gamma, h->pbuf);
+      pf = &h->pfs;
+    }
+  }
+  s = run_shard(h, roots, depth, gamma, leaf_begin, leaf_end, keys_out, 0, stats, pf);
+  if (!s && pf && pf->done) {
+    h->pfs_valid = true;
+    h->pfs_roots = roots;
+    h->pfs_n = n_roots;
+    h->pfs_d = depth;
+    h->pfs_gamma = gamma;
+  }
   if (stats) stats->kernel_launches = h->launches - l0;
   return s;
 }
@@ -740,7 +811,10 @@ bcts_status bcts_finalize(bcts_handle h, const void *roots, int64_t n_roots, int
   const int64_t l0 = h->launches;
   Outs o{actions_out, root_q_out, vanilla_q_out, terms_out, best_leaf_out};
   if ((s = ensure_ws(h, finalize_ws(h, n_roots, 0)))) return s;
-  s = finalize_impl(h, roots, n_roots, depth, gamma, beta, correction_on, keys, o, 0, stats);
+  const bool pre = h->pfs_valid && h->pfs_roots == roots && h->pfs_n == n_roots && h->pfs_d == depth &&
+                   h->pfs_gamma == gamma;
+  h->pfs_valid = false;
+  s = finalize_impl(h, roots, n_roots, depth, gamma, beta, correction_on, keys, o, 0, stats, pre ? &h->pfs : nullptr);
   if (stats) stats->kernel_launches += h->launches - l0;
   return s;
 }
@@ -765,15 +839,8 @@ bcts_status bcts_search_ex(bcts_handle h, const void *roots, int64_t n_roots, in
   // With the level-1 terms needed and a conv net generating the leaves, the prologue's states
   // [roots | level-1 children] are expanded up front into a region after the keys and evaluated
   // inside a leaf batch (PrologueFold; finalize then only reads their rows).
-  const bool try_fold = depth >= 1 && correction_on && fused_leaves(h) && h->net.kind == BCTS_NET_RAINBOW_BF16 &&
-                        n_roots * (A + 1) <= (int64_t)4096 && !getenv("BCTS_NO_PROLOGUE_FOLD");
-  size_t pbytes = 0;
-  if (try_fold) {
-    Carver pc(nullptr);
-    pc.level(h->env, n_roots * (A + 1));
-    pc.take((size_t)n_roots * (A + 1) * A * 4);
-    pbytes = align_up(pc.off);
-  }
+  const bool try_fold = correction_on && fold_wanted(h, n_roots, depth);
+  const size_t pbytes = try_fold ? fold_bytes(h, n_roots) : 0;
   const size_t kbytes = kbytes0 + pbytes;
   size_t need = finalize_ws(h, n_roots, kbytes);
   if (depth >= 1) {
@@ -784,25 +851,7 @@ bcts_status bcts_search_ex(bcts_handle h, const void *roots, int64_t n_roots, in
   if ((s = ensure_ws(h, kbytes + need))) return s;
   int64_t *keys = (int64_t *)h->ws;
   PrologueFold pf;
-  if (try_fold) {   // slots [0, n): the roots' states; [n, n + nA): their children (Alg. 1 body)
-    Carver pc(h->ws + kbytes0);
-    LevelBuf b = pc.level(h->env, n_roots * (A + 1));
-    pf.rows_out = (float *)pc.take((size_t)n_roots * (A + 1) * A * 4);
-    float g1[2];
-    discounts(gamma, 1, g1);
-    const int64_t sb = state_bytes(h->env), rb = record_bytes(h->env);
-    const NodeView rv = root_view(h->env, roots, 0);
-    cudaMemcpy2DAsync(b.state, (size_t)sb, rv.state, (size_t)rb, (size_t)sb, (size_t)n_roots,
-                      cudaMemcpyDeviceToDevice, h->st);
-    NodeOut co = out_of(h->env, b);
-    co.state += n_roots * sb;
-    if (co.key) co.key += n_roots;
-    co.cum += n_roots;
-    launch_expand(h->env, rv, 0, 0, n_roots * A, A, g1[0], h->em, co, h->st, &h->prof);
-    h->launches += 1;
-    pf.view = view_of(h->env, b);
-    pf.ne = n_roots * (A + 1);
-  }
+  if (try_fold) pf = fold_front(h, roots, n_roots, gamma, h->ws + kbytes0);
   if (depth >= 1) {
     launch_keys_init(keys, n_roots * A, h->st);
     h->launches += 1;
