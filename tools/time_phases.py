@@ -22,6 +22,7 @@ ap.add_argument("--depth", type=int, default=0)
 ap.add_argument("--roots", type=int, default=0)
 ap.add_argument("--iters", type=int, default=20)
 ap.add_argument("--world", type=int, default=1, help="time rank 0's share of a world-size-W partition")
+ap.add_argument("--profile", action="store_true", help="also print the per-kernel-class breakdown")
 a = ap.parse_args()
 cfg = config(a.config)
 n = a.roots or cfg.n_roots
@@ -48,5 +49,15 @@ for it in range(a.iters + 3):
     if it >= 3:
         tot += [ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])]
 tot /= a.iters
+if a.profile:   # per kernel class (event pairs on the handle's stream), one more pass of iters
+    h.profile(True)
+    for it in range(a.iters):
+        h.keys_init(keys)
+        h.search_shard(roots, n, d, cfg.gamma, b, e, keys)
+        h.finalize(roots, n, d, cfg.gamma, cfg.beta, 1, keys, extra=False)
+    torch.cuda.synchronize()
+    for k, v in sorted(h.profile_read().items(), key=lambda kv: -kv[1]["ms"]):
+        print(f"  {k:14s} {v['ms'] / a.iters * 1e3:8.1f} us/step  {v['launches'] / a.iters:5.1f} launches/step")
+    h.profile(False)
 print(f"{a.config} n={n} d={d} rank 0 of {a.world} (leaves [{b}, {e})): shard {tot[0]:.3f} ms, finalize (prologue + Eq. 3/5) {tot[1]:.3f} ms, "
       f"total {tot.sum():.3f} ms")
