@@ -174,7 +174,12 @@ bcts_status bcts_search_ex(bcts_handle h, const void *roots, int64_t n_roots, in
 
 /* End-to-end convenience: HOST roots in, HOST outputs out. Copies the roots
  * host->device, runs bcts_search_ex and copies actions/root_q device->host,
- * then synchronizes the stream. Same errors as bcts_search. */
+ * then synchronizes the stream. Same errors as bcts_search. When all three
+ * host buffers are page-locked (cudaHostAlloc / torch pin_memory) the call
+ * after an eager one with the same pointers and arguments replays a CUDA graph
+ * of the whole sequence (captured on a private stream, launched on the
+ * handle's); the buffers' CURRENT contents are copied in on every call.
+ * BCTS_NO_GRAPH=1 in the environment disables the graph. */
 bcts_status bcts_search_host(bcts_handle h, const void *roots_host, int64_t n_roots, int32_t depth,
                              int32_t A, float gamma, float beta, int32_t correction_on,
                              int32_t *actions_host, float *root_q_host);

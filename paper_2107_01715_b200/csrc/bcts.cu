@@ -46,6 +46,23 @@ struct bcts_handle_t {
   int64_t pfs_n = 0;
   int32_t pfs_d = 0;
   float pfs_gamma = 0.f;
+  // bcts_search_host replays a CUDA graph of [H2D, search, D2H] captured for its last arguments
+  struct GraphKey {
+    const void *rh = nullptr;
+    void *ah = nullptr, *qh = nullptr;
+    int64_t n = 0;
+    int32_t d = 0, A = 0, corr = 0;
+    float gamma = 0.f, beta = 0.f;
+    uint8_t *ws = nullptr;
+    size_t wss = 0;
+    bool operator==(const GraphKey &o) const {
+      return rh == o.rh && ah == o.ah && qh == o.qh && n == o.n && d == o.d && A == o.A && corr == o.corr &&
+             gamma == o.gamma && beta == o.beta && ws == o.ws && wss == o.wss;
+    }
+  } gkey;
+  cudaGraphExec_t gexec = nullptr;
+  bool gvalid = false;
+  cudaStream_t gst = nullptr;
 };
 
 namespace {
@@ -655,6 +672,8 @@ void bcts_destroy(bcts_handle h) {
   if (h->st) cudaStreamSynchronize(h->st);
   net_free(h->net);
   cudaFree(h->pbuf);
+  if (h->gexec) cudaGraphExecDestroy(h->gexec);
+  if (h->gst) cudaStreamDestroy(h->gst);
   cudaFree(h->d_next);
   cudaFree(h->d_envw);
   cudaFree(h->d_rew);
@@ -959,14 +978,66 @@ bcts_status bcts_search_host(bcts_handle h, const void *roots_host, int64_t n_ro
     }
     h->e2e_out = (size_t)n_roots * A;
   }
-  if (cudaMemcpyAsync(h->e2e_roots, roots_host, rb, cudaMemcpyHostToDevice, h->st) != cudaSuccess)
-    return cuda_check(h, "e2e H2D");
-  bcts_status s = bcts_search(h, h->e2e_roots, n_roots, depth, A, gamma, beta, correction_on, h->e2e_act, h->e2e_q);
+  // One call = H2D of the roots, the search, D2H of the outputs. With page-locked host buffers the
+  // sequence is captured once as a CUDA graph (after an eager run with the same arguments, so every
+  // buffer exists) and replayed: one launch instead of ~20 kernel / copy enqueues from the host.
+  auto pinned = [](const void *p) {
+    cudaPointerAttributes a;
+    const bool ok = cudaPointerGetAttributes(&a, p) == cudaSuccess && a.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    return ok;
+  };
+  const bool can_graph = !h->prof.on && !getenv("BCTS_NO_GRAPH") && pinned(roots_host) && pinned(actions_host) &&
+                         pinned(root_q_host);
+  bcts_handle_t::GraphKey key;
+  key.rh = roots_host, key.ah = actions_host, key.qh = root_q_host, key.n = n_roots, key.d = depth, key.A = A;
+  key.corr = correction_on, key.gamma = gamma, key.beta = beta, key.ws = h->ws, key.wss = h->ws_size;
+  if (can_graph && h->gvalid && key == h->gkey) {
+    if (cudaGraphLaunch(h->gexec, h->st) == cudaSuccess && cudaStreamSynchronize(h->st) == cudaSuccess)
+      return cuda_check(h, "e2e graph");
+    cudaGetLastError();
+    h->gvalid = false;
+  }
+  auto enqueue = [&]() -> bcts_status {
+    if (cudaMemcpyAsync(h->e2e_roots, roots_host, rb, cudaMemcpyHostToDevice, h->st) != cudaSuccess)
+      return cuda_check(h, "e2e H2D");
+    bcts_status s2 = bcts_search(h, h->e2e_roots, n_roots, depth, A, gamma, beta, correction_on, h->e2e_act, h->e2e_q);
+    if (s2) return s2;
+    cudaMemcpyAsync(actions_host, h->e2e_act, (size_t)n_roots * 4, cudaMemcpyDeviceToHost, h->st);
+    cudaMemcpyAsync(root_q_host, h->e2e_q, (size_t)n_roots * A * 4, cudaMemcpyDeviceToHost, h->st);
+    return BCTS_OK;
+  };
+  bcts_status s = enqueue();
   if (s) return s;
-  cudaMemcpyAsync(actions_host, h->e2e_act, (size_t)n_roots * 4, cudaMemcpyDeviceToHost, h->st);
-  cudaMemcpyAsync(root_q_host, h->e2e_q, (size_t)n_roots * A * 4, cudaMemcpyDeviceToHost, h->st);
   if (cudaStreamSynchronize(h->st) != cudaSuccess) return cuda_check(h, "e2e sync");
-  return cuda_check(h, "e2e D2H");
+  if ((s = cuda_check(h, "e2e D2H"))) return s;
+  if (can_graph) {   // capture the same sequence on a private stream for the next call
+    h->gvalid = false;
+    if (!h->gst) cudaStreamCreateWithFlags(&h->gst, cudaStreamNonBlocking);
+    key.ws = h->ws, key.wss = h->ws_size;
+    cudaStream_t saved = h->st;
+    h->st = h->gst;
+    cudaGraph_t g = nullptr;
+    bool ok = h->gst && cudaStreamBeginCapture(h->gst, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    if (ok) {
+      const bcts_status sc = enqueue();
+      ok = cudaStreamEndCapture(h->gst, &g) == cudaSuccess && sc == BCTS_OK && g;
+    }
+    h->st = saved;
+    h->err.clear();
+    if (ok && h->ws == key.ws && h->ws_size == key.wss) {
+      cudaGraphExec_t ex = nullptr;
+      if (cudaGraphInstantiate(&ex, g, 0) == cudaSuccess) {
+        if (h->gexec) cudaGraphExecDestroy(h->gexec);
+        h->gexec = ex;
+        h->gkey = key;
+        h->gvalid = true;
+      }
+    }
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+  }
+  return BCTS_OK;
 }
 
 bcts_status bcts_expand(bcts_handle h, const void *roots, int64_t n_roots, int32_t level, int32_t A, float gamma,

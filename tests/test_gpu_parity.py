@@ -342,6 +342,24 @@ def test_e2e_host_matches_device():
     np.testing.assert_array_equal(q.numpy(), g["root_q"])
 
 
+def test_e2e_graph_replay_reads_new_inputs():
+    """bcts_search_host replays a CUDA graph captured after its first call with the same page-locked
+    buffers: every replay must copy the buffer's CURRENT roots in and the new outputs out."""
+    cfg = config("C5")
+    h = P.Handle.from_config(cfg)
+    pin = torch.zeros(2, P.RECORD_BYTES[P.ENV_ATARI_HASH], dtype=torch.uint8).pin_memory()
+    act = torch.zeros(2, dtype=torch.int32).pin_memory()
+    q = torch.zeros(2, cfg.A, dtype=torch.float32).pin_memory()
+    for seed in (21, 22, 23, 24):   # call 1 eager (+ capture), calls 2-4 graph replays
+        roots = atari_roots(2, seed)
+        g = run(h, roots, 3, cfg.gamma, 1.0, 1)
+        pin.copy_(torch.from_numpy(roots.view(np.uint8).reshape(2, -1)))
+        h.search_host(pin, 2, 3, cfg.gamma, 1.0, 1, act, q)
+        np.testing.assert_array_equal(act.numpy(), g["actions"])
+        np.testing.assert_array_equal(q.numpy(), g["root_q"])
+    h.close()
+
+
 @pytest.mark.parametrize("cname,n,d", [("C2", 16, 3), ("C5", 2, 2)])
 def test_exact_bias_correction(cname, n, d):
     """correction_on = 2: Lemma 2's exact gap (App. A.2) instead of Eq. 5 -- GPU (normcdfinv) vs oracle."""
