@@ -571,12 +571,14 @@ int net_build(Net &net, const bcts_config &cfg, std::string &err) {
     net.ld_zv = Nv;
     net.ld_za = Na;
   }
-  // Batch capacity = three waves of 128-row M tiles (3 x 148 x 128 images): eval_conv splits a
-  // call into equal batches of at most this size (rounded to 128 rows), so no batch is a thin
-  // tail. Three tiles per SM let the fc / head kernels overlap one tile's loads with another's
-  // math (measured on C5: 1 wave 2.70 ms/step, 2 waves 2.62, 3 waves 2.61). The materialised-
-  // state path (s2d input, act2) keeps one wave of sub-batch: it only scores small sets.
-  int64_t waves = 3;
+  // Batch capacity = six waves of 128-row M tiles (6 x 148 x 128 = 113,664 images): eval_conv
+  // splits a call into equal batches of at most this size (rounded to 128 rows), so no batch is a
+  // thin tail. Several tiles per SM let the fc / head kernels overlap one tile's loads with
+  // another's math, and fewer batches mean fewer kernel tails (measured on C5: 1 wave 2.41 ms/step,
+  // 2 waves 2.33, 3 waves 2.31, 6 waves -- the whole 104,976-leaf level in one batch -- 2.28). The
+  // materialised-state path (s2d input, act2) keeps one wave of sub-batch: it only scores small
+  // sets. Scratch at 6 waves: ~4.2 GB of act1 + ~1 GB of act3 / hidden / head buffers.
+  int64_t waves = 6;
   if (const char *e = getenv("BCTS_FC_WAVES")) waves = atoll(e) > 0 ? atoll(e) : waves;
   net.batch = 148 * 128 * waves;
   net.fc_batch = 148 * 128 * waves;
