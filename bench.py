@@ -54,33 +54,55 @@ FP32_CLASSES = {"mlp", "expand_dnn"}      # fixed-order fmaf kernels: ALU-bound,
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region.
+
+    nvidia-smi needs ~0.1-0.3 s before its first sample, longer than a default timed region, so the
+    sampler is started (and its first line awaited) before the warm-up; a reader thread timestamps
+    every line and mark()/unmark() bracket the timed region. The summary uses the samples taken
+    inside it (plus the one just before, so a short region still has one)."""
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, device):
-        self.device, self.proc = device, None
+        self.device, self.proc, self.stamped, self.t0, self.t1 = device, None, [], None, None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            if line.strip():
+                self.stamped.append((time.monotonic(), line))
 
     def __enter__(self):
+        import threading
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+            deadline = time.monotonic() + 3.0
+            while not self.stamped and time.monotonic() < deadline:
+                time.sleep(0.01)
         except OSError:
             self.proc = None
         return self
 
+    def mark(self):
+        self.t0 = time.monotonic()
+
+    def unmark(self):
+        self.t1 = time.monotonic() + 0.03   # one more sampling period
+
     def __exit__(self, *a):
-        self.lines = []
         if self.proc:
             self.proc.terminate()
             try:
-                out, _ = self.proc.communicate(timeout=5)
+                self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
-                out, _ = self.proc.communicate()
-            self.lines = [l for l in out.splitlines() if l.strip()]
+        t0 = self.t0 if self.t0 is not None else float("-inf")
+        t1 = self.t1 if self.t1 is not None else float("inf")
+        before = [l for t, l in self.stamped if t < t0][-1:]
+        self.lines = before + [l for t, l in self.stamped if t0 <= t <= t1]
 
     def summary(self):
         if not getattr(self, "lines", None):
@@ -270,6 +292,7 @@ def main():
             import torch.distributed as dist
             dist.barrier()
 
+    clk = ClockSampler(local).__enter__()   # started before the warm-up (see ClockSampler)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -279,15 +302,17 @@ def main():
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        for i in range(args.steps):
-            if flush is not None:
-                flush.fill_(i & 0xFF)
-            evs[i][0].record()
-            step()
-            evs[i][1].record()
-        torch.cuda.synchronize()
-        barrier()
+    clk.mark()
+    for i in range(args.steps):
+        if flush is not None:
+            flush.fill_(i & 0xFF)
+        evs[i][0].record()
+        step()
+        evs[i][1].record()
+    torch.cuda.synchronize()
+    clk.unmark()
+    clk.__exit__(None, None, None)
+    barrier()
     # ---- profiled repeat of the timed region: per-kernel-class CUDA events on the launching stream
     h.profile(True)
     for i in range(args.steps):

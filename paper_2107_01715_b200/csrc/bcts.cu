@@ -992,6 +992,10 @@ bcts_status bcts_search_host(bcts_handle h, const void *roots_host, int64_t n_ro
   bcts_handle_t::GraphKey key;
   key.rh = roots_host, key.ah = actions_host, key.qh = root_q_host, key.n = n_roots, key.d = depth, key.A = A;
   key.corr = correction_on, key.gamma = gamma, key.beta = beta, key.ws = h->ws, key.wss = h->ws_size;
+  static const bool gdbg = getenv("BCTS_GRAPH_DEBUG") != nullptr;
+  if (gdbg)
+    fprintf(stderr, "search_host: can_graph=%d valid=%d match=%d ws=%p/%zu\n", (int)can_graph, (int)h->gvalid,
+            (int)(key == h->gkey), (void *)h->ws, h->ws_size);
   if (can_graph && h->gvalid && key == h->gkey) {
     if (cudaGraphLaunch(h->gexec, h->st) == cudaSuccess && cudaStreamSynchronize(h->st) == cudaSuccess)
       return cuda_check(h, "e2e graph");
@@ -1035,6 +1039,7 @@ bcts_status bcts_search_host(bcts_handle h, const void *roots_host, int64_t n_ro
       }
     }
     if (g) cudaGraphDestroy(g);
+    if (gdbg) fprintf(stderr, "search_host: captured ok=%d valid=%d\n", (int)ok, (int)h->gvalid);
     cudaGetLastError();
   }
   return BCTS_OK;
