@@ -154,6 +154,24 @@ def test_conv_nets_small_trees(cname, n, d):
             np.testing.assert_array_equal(g["terms"][:, 0], r["terms"][:, 0])
 
 
+@pytest.mark.parametrize("net,A,n,d", [(NET_RAINBOW_BF16, 7, 2, 2), (NET_RAINBOW_BF16, 2, 3, 3),
+                                        (NET_RAINBOW_BF16, 33, 1, 1), (NET_NATURE_BF16, 5, 2, 2)])
+def test_conv_nets_unusual_action_counts(net, A, n, d):
+    """Action counts that are not multiples of the head's 4-action chunks or of the expansion's
+    CTA split (A = 7, 5), the minimum A = 2, and A > 32 (two lanes per action in the finalize warp),
+    against the oracle."""
+    cfg = Config(f"A{A}", ENV_ATARI_HASH, net, A, d, n, 0.99, 1.0, seed=40 + A, wseed=140 + A)
+    h = handle(cfg)
+    o = Oracle.from_config(cfg)
+    roots = cfg.roots()
+    for corr in (0, 1):
+        g = run(h, roots, d, cfg.gamma, cfg.beta, corr)
+        r = o.search(roots, d, float(np.float32(cfg.gamma)), cfg.beta, corr, mode=0, threads=THREADS)
+        bf16_compare(g, r, f"{cfg.name} net={net} n={n} d={d} corr={corr}")
+        if corr:
+            np.testing.assert_array_equal(g["terms"][:, 0], r["terms"][:, 0])
+
+
 @pytest.mark.parametrize("cname", ["C3", "C5"])
 def test_q_rows_vs_oracle(cname):
     """Leaf value net, full rows: GPU bf16 tensor-core net vs the bf16-emulating fp64 oracle."""
