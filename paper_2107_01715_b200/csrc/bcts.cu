@@ -299,13 +299,26 @@ bcts_status run_shard(bcts_handle h, const void *roots, int32_t d, float gamma, 
       hi[k] = (Le - 1) / pw[d - k] + 1;
     }
     NodeView prev = root_view(h->env, roots, lo[0]);
+    int64_t vbase = lo[0];   // global level index of prev's element 0
+    int expanded = 0;
     for (int k = 1; k <= dm; ++k) {
+      if (k == 1 && pf && pf->ne) {   // level 1 = the prologue front end's children (slots n .. n + nA)
+        const int64_t nr = pf->ne / (A + 1);
+        prev = pf->view;
+        prev.state += nr * prev.state_stride;
+        if (prev.key) prev.key = (const uint64_t *)((const uint8_t *)prev.key + nr * prev.key_stride);
+        prev.cum += nr;
+        vbase = 0;
+        trans += hi[1] - lo[1];
+        continue;
+      }
       const LevelBuf &b = ((dm - k) % 2 == 0) ? big : small;
-      launch_expand(h->env, prev, lo[k - 1], lo[k], hi[k], A, g[k - 1], h->em, out_of(h->env, b),
-                    h->st, &h->prof);
+      launch_expand(h->env, prev, vbase, lo[k], hi[k], A, g[k - 1], h->em, out_of(h->env, b), h->st, &h->prof);
       prev = view_of(h->env, b);
+      vbase = lo[k];
       trans += hi[k] - lo[k];
       ++lvl_launch;
+      ++expanded;
     }
     int nl;
     bool folded = false;   // backup fused into the head's epilogue (Rainbow tcgen05 head)
@@ -316,14 +329,14 @@ bcts_status run_shard(bcts_handle h, const void *roots, int32_t d, float gamma, 
       kf.lpr = pw[d];
       kf.seg = pw[d - 1];
       kf.A = A;
-      nl = net_eval_children(h->net, prev, lo[d - 1], L, Le, A, g[d - 1], MODE_TOTAL, g[d], totals, h->st,
+      nl = net_eval_children(h->net, prev, vbase, L, Le, A, g[d - 1], MODE_TOTAL, g[d], totals, h->st,
                              (h->flags & BCTS_F_SEPARATE_BACKUP) ? nullptr : &kf, &folded, pf);
       trans += Le - L;
     } else {
       nl = net_eval(h->net, prev, Le - L, MODE_TOTAL, g[d], totals, h->st);
     }
     if (!folded) launch_segmax(totals, Le - L, L, pw[d], pw[d - 1], A, keys, h->st, &h->prof);
-    h->launches += dm + nl + (folded ? 0 : 1);
+    h->launches += expanded + nl + (folded ? 0 : 1);
     ++nchunks;
     if ((s = cuda_check(h, "shard chunk"))) return s;
   }
@@ -454,10 +467,7 @@ bcts_status finalize_impl(bcts_handle h, const void *roots, int64_t n, int32_t d
     dq0 = pre->rows_out;
     drows1 = pre->rows_out + n * A;
     dr1 = pre->view.cum + n;
-    if (stats) {
-      stats->evaluated += n * (A + 1);
-      stats->transitions += n * A;
-    }
+    if (stats) stats->evaluated += n * (A + 1);   // (their level-1 transitions are the shard's)
   } else if (need_q0) {
     s = run_prologue(h, roots, n, gamma, corr && d >= 1, q0, m1, r1, reserved + cc.off, stats, &dq0, &drows1, &dr1);
     if (s) return s;
