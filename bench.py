@@ -142,6 +142,12 @@ def dist_setup(args):
     return world, rank, local
 
 
+def tab_of(cfg):
+    """The C1 tabular MDP (SPEC chain-grid) for TABULAR configs, else None."""
+    from synth.inputs import ENV_TABULAR, chain_c1
+    return chain_c1() if cfg.env == ENV_TABULAR else None
+
+
 def metric_of(cfg):
     if (cfg.A, cfg.depth) == (18, 4):
         return METRIC
@@ -168,7 +174,7 @@ def oracle_sample(cfg, seconds_target=12.0, threads=None):
     whole depth-2 subtrees of the first root, run across the host cores."""
     from oracle import Oracle
     threads = threads or os.cpu_count() or 1
-    o = Oracle.from_config(cfg)
+    o = Oracle.from_config(cfg, tab=tab_of(cfg))
     root = cfg.roots(1)
     A, d = cfg.A, cfg.depth
     exp, ev = nodes_per_root(A, d, 1)
@@ -208,7 +214,7 @@ def run_reference(args, cfg, world, rank):
         return 0
     from oracle import Oracle
     threads = os.cpu_count() or 1
-    o = Oracle.from_config(cfg)
+    o = Oracle.from_config(cfg, tab=tab_of(cfg))
     root = cfg.roots(1)
     A, d = cfg.A, cfg.depth
     exp, ev = nodes_per_root(A, d, 1)
@@ -268,7 +274,7 @@ def main():
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     flags = P.F_SIMT_NET if args.simt else 0
-    h = P.Handle.from_config(cfg, device=local, flags=flags)
+    h = P.Handle.from_config(cfg, tab=tab_of(cfg), device=local, flags=flags)
     n, d, A, corr = cfg.n_roots, cfg.depth, cfg.A, 1
     roots_np = cfg.roots()
     roots = torch.from_numpy(roots_np.view(np.uint8).reshape(n, -1).copy()).to(dev)
