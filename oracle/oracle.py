@@ -135,8 +135,8 @@ class Oracle:
 
     @classmethod
     def from_config(cls, cfg, tab=None):
-        from synth.inputs import make_weights, make_env_weights  # input generators only
-        w = None if cfg.net == NET_TABLE else make_weights(cfg.net, cfg.A, cfg.wseed, **cfg.net_kw())[0]
+        from synth.inputs import make_env_weights  # input generators only
+        w = cfg.weights()[0]
         ew = make_env_weights(cfg) if cfg.env == ENV_DNN else None
         return cls(cfg.env, cfg.A, cfg.net, tab=tab, weights=w, env_weights=ew, **cfg.net_kw())
 

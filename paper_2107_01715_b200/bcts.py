@@ -184,9 +184,9 @@ class Handle:
 
     @classmethod
     def from_config(cls, cfg, tab=None, **kw):
-        from synth.inputs import make_weights, make_env_weights  # input generators only
+        from synth.inputs import make_env_weights  # input generators only
         nk = cfg.net_kw()
-        w = None if cfg.net == NET_TABLE else make_weights(cfg.net, cfg.A, cfg.wseed, **nk)[0]
+        w = cfg.weights()[0]
         if cfg.env == ENV_DNN:
             kw.setdefault("env_weights", make_env_weights(cfg))
         return cls(cfg.env, cfg.A, cfg.net, weights=w, tab=tab, **{**nk, **kw})

@@ -141,12 +141,19 @@ def make_env_weights(cfg) -> np.ndarray:
     return _blob(env_weight_specs(cfg.A), cfg.extra.get("env_wseed", cfg.wseed + 7))
 
 
-def make_weights(net: int, A: int, wseed: int, **kw) -> tuple[np.ndarray, dict]:
+HEAD_TENSORS = ("fc2.w", "fc_z_v.w", "fc_z_a.w")   # the output layers (Nature fc2; Rainbow z_v, z_a)
+
+
+def make_weights(net: int, A: int, wseed: int, head_scale: float = 1.0, **kw) -> tuple[np.ndarray, dict]:
     """Canonical fp32 weight blob (concatenation in weight_specs order) + views.
 
     Element e of tensor t: u = (mix64(wseed ^ mix64((t<<40)|e)) >> 11) * 2^-53,
     value = (2u-1)/sqrt(fan_in)  (PyTorch's default Linear/Conv bound);
     conv1.w is additionally scaled by 1/255 (input /255 folded in, R15).
+    head_scale (test-only "spread" weights): the output layers' weights
+    (HEAD_TENSORS) are multiplied by it. Random-init Q-hat is nearly flat across leaves
+    (max |Q| ~ 0.05, leaf-to-leaf spread ~ 0.004); x64 spreads it (~1.5 / ~0.25) so a
+    parity test at the search tolerance can tell a broken trunk from rounding.
     """
     specs = weight_specs(net, A, **kw)
     parts, views = [], {}
@@ -158,6 +165,8 @@ def make_weights(net: int, A: int, wseed: int, **kw) -> tuple[np.ndarray, dict]:
         v = (2.0 * u - 1.0) / math.sqrt(fan_in)
         if name == "conv1.w":
             v = v / 255.0
+        if head_scale != 1.0 and name in HEAD_TENSORS:
+            v = v * head_scale
         parts.append(v.astype(np.float32))
     blob = np.concatenate(parts) if parts else np.zeros(0, np.float32)
     off = 0
@@ -250,9 +259,11 @@ class Config:
         return {"mlp_in": DNN_STATE} if self.env == ENV_DNN else {}
 
     def weights(self):
+        """The value net's canonical weight blob and views (None for the table net)."""
         if self.net == NET_TABLE:
             return None, {}
-        return make_weights(self.net, self.A, self.wseed, **self.net_kw())
+        return make_weights(self.net, self.A, self.wseed, head_scale=self.extra.get("head_scale", 1.0),
+                            **self.net_kw())
 
 
 CONFIGS = {
@@ -273,6 +284,14 @@ CONFIGS = {
     "D10": Config("D10", ENV_DNN, NET_MLP2_F32, 10, 4, 64, 0.99, 1.0, seed=22, wseed=122,
                   note="random-DNN forward model, A=10"),
 }
+
+
+# test-only "spread" variants (head_scale, see make_weights): same envs / roots, output layers x64
+for _n in ("C3", "C4", "C5"):
+    _c = CONFIGS[_n]
+    CONFIGS[_n + "S"] = Config(_n + "S", _c.env, _c.net, _c.A, _c.depth, _c.n_roots, _c.gamma, _c.beta, _c.seed,
+                               _c.wseed, _c.correction, _c.note + "; output layers x64 (spread Q-hat, tests only)",
+                               {"head_scale": 64.0})
 
 
 def config(name: str) -> Config:

@@ -551,3 +551,24 @@ def test_dnn_bruteforce_equals_dfs_and_mirror_close(cname, d):
     f64 = o.search(roots, d, cfg.gamma, 1.0, 1, mode=0)
     f32 = o.search(roots, d, cfg.gamma, 1.0, 1, mode=1)
     assert np.abs(f64["vanilla_q"] - f32["vanilla_q"]).max() < 1e-4
+
+
+def test_int_hash_mlp2_leaf_value_matches_torch():
+    """C2 leaf value: MLP2 64-256-4 over x_j = (byte j of the 64-byte INT_HASH state) / 256 (SURVEY §8d,
+    little-endian bytes of the 16 u32 words), pinned to torch.nn.functional.linear in float64 (a library
+    routine). Covers roots and level-2 states so the feature map is exercised on stepped states too."""
+    import torch
+    F = torch.nn.functional
+    cfg = config("C2")
+    o = Oracle.from_config(cfg)
+    _, v = cfg.weights()
+    W = {k: torch.from_numpy(x.astype(np.float64)) for k, x in v.items()}
+    states = list(cfg.roots(4))
+    for i in (0, 5, 15):
+        rec, _ = o.node(cfg.roots(1)[0], 2, i, float(np.float32(cfg.gamma)), mode=1)
+        states.append(rec.view(np.uint32))
+    for s in states:
+        x = torch.from_numpy(np.ascontiguousarray(s).view(np.uint8).astype(np.float64)) / 256.0
+        q = F.linear(F.relu(F.linear(x, W["l1.w"], W["l1.b"])), W["l2.w"], W["l2.b"]).numpy()
+        np.testing.assert_allclose(o.qrow(s, mode=0), q, rtol=0, atol=1e-12)
+        np.testing.assert_allclose(o.qrow(s, mode=1), q, rtol=0, atol=5e-6)
