@@ -182,6 +182,7 @@ struct ConvSW {
   uint32_t out_img_bytes = 0, out_plane = 0;   // output layout of the next layer
   int out_w = 0, out_mode = 0;                 // 0: s2d(2) planar, 1: planar, 2: dense [row][N]
   const uint8_t *wsw = nullptr;                // weights pre-swizzled as their SW128 smem image
+  const uint8_t *wpair = nullptr;              // conv2 only: tap-pair image for k_conv23 (qnet.cu)
   int layout = 0;                              // activation layout (see act_off)
   uint32_t copy_chunks = 1;                    // (unused) bulk copies per input image
   int in_rows = 0;                             // valid input rows per 64-channel block

@@ -640,6 +640,23 @@ int net_build(Net &net, const bcts_config &cfg, std::string &err) {
       void *d = nullptr;
       if (upload(net, img.data(), img.size() * 2, &d) != cudaSuccess) { err = "upload swizzled weights"; return -1; }
       cs[t]->wsw = (const uint8_t *)d;
+      if (t == 1) {   // conv2 tap pairs for k_conv23: k-block (pr, kb) = [128 rows x 128 B], row n < 64 =
+                      // tap (pr, 0) channel n, row n >= 64 = tap (pr, 1) channel n - 64; K = s2d channels
+                      // kb*64 .. kb*64+63 of that tap (k = tap*128 + c2 in hw)
+        std::vector<__nv_bfloat16> pimg((size_t)4 * 128 * 64);
+        uint8_t *pd = (uint8_t *)pimg.data();
+        for (int pr = 0; pr < 2; ++pr)
+          for (int kb = 0; kb < 2; ++kb)
+            for (int n = 0; n < 128; ++n) {
+              const int tap = pr * 2 + (n >> 6), o = n & 63;
+              for (int j = 0; j < 8; ++j)
+                memcpy(pd + (size_t)(pr * 2 + kb) * 128 * 128 + (n / 8) * 1024 + (n % 8) * 128 + ((j ^ (n % 8)) * 16),
+                       (const uint8_t *)(hw.data() + (size_t)o * K + tap * 128 + kb * 64) + j * 16, 16);
+            }
+        void *dp = nullptr;
+        if (upload(net, pimg.data(), pimg.size() * 2, &dp) != cudaSuccess) { err = "upload paired conv2 weights"; return -1; }
+        cs[t]->wpair = (const uint8_t *)dp;
+      }
     }
   }
   // TMA plans (tensor maps over the fixed scratch buffers; fall back to the

@@ -1172,32 +1172,43 @@ __global__ void __launch_bounds__(kC3tThreads, 1)
 }
 
 // ------------------------------------------------ conv2 + conv3 fused (act2 stays on-chip)
-// Per image: conv2 (2x2/1 over act1's s2d(2) 10x10x128 -> 9x9x64; A = full-width image rows,
-// M = 128, B = weights, N = 64) then conv3 (3x3/1 over act2 9x9x64 -> 7x7x64, transposed:
-// A = weights M = 64, B = act2 row window N = 64). act2 is written by the conv2 epilogue
-// straight into a double-buffered SMEM image in conv3's SW128 layout and never touches
-// HBM (the separate kernels wrote and re-read 2 x 10 KB per leaf). The MMA warp alternates
-// conv2(i) and conv3(i-1) so the tensor core has work while either epilogue runs.
+// Per image: conv2 (2x2/1 over act1's s2d(2) 10x10x128 -> 9x9x64) then conv3 (3x3/1 over act2
+// 9x9x64 -> 7x7x64). act2 goes from the conv2 epilogue straight into a double-buffered SMEM
+// image in conv3's SW128 layout and never touches HBM.
+//
+// TAP PAIRS. Both convs are written as sums over filter taps t of shifted windows,
+//   out[q] = sum_t W_t . in[q + s_t]                       (q = full-width output row)
+// and the kernel is bound by the SMEM bytes its MMAs read. One MMA now serves TWO taps that
+// differ by one column (s_b = s_a + 1) and read the SAME window:
+//  * conv2 (A = image rows, M = 128; B = weights): B = [W_a | W_b] (N = 128) over the window at
+//    s_a gives D_L[m] = W_a.in[m + s_a] (a term of out[m]) and D_R[m] = W_b.in[m + s_a] (a term of
+//    out[m - 1]); pairs (0,0|0,1) and (1,0|1,1) keep that offset, so out[q] = D_L[q] + D_R[q + 1]
+//    -- a one-lane shuffle in the epilogue (rows 31 / 63 take row 32 / 64 from the next lane
+//    quarter through SMEM). 16 MMAs of 4 + 4 KB instead of 32 of 4 + 2 KB: 128 instead of 192 KB
+//    of operand reads per image, and the tensor time is unchanged (1,024 cycles).
+//  * conv3 (transposed: A = weights from TMEM, B = act2 window N = 64 image rows): A = [W_a ; W_b]
+//    stacked along M = 128 (lanes 0-63 tap a, lanes 64-127 tap b) over the window at s_a; groups
+//    (ty,0|ty,1) for ty = 0..2 and (ty,2|zero), so D_lo[n] is a term of out[n] and D_hi[n] a term
+//    of out[n - 1]: out[n] = D_lo[n] + D_hi[n + 1]. The upper-half lanes hand their rows to the
+//    lower half through SMEM. 24 M = 128 MMAs (32 cycles each) replace 36 M = 64 MMAs that cost
+//    the same per instruction: 768 instead of 1,152 tensor cycles per image, 48 instead of 72 KB
+//    of B reads. The sums are the same products in another fp32 order (R17/R18).
 // act1 lands in a compact ring (planes of 104 rows instead of act1's 144-row global planes).
-// The kernel is bound by the tensor core's SMEM operand reads (ncu: the tc SMEM data pipe at
-// 85% with every operand in SMEM), so conv3's A operand -- the weights, the same for every
-// image -- lives in TMEM (tcgen05.mma A-from-TMEM; M = 64 rows at lane (m/16)*32 + m%16,
-// measured in tools/mma_ts_test.cu), loaded once per CTA with tcgen05.st by the conv3-epilogue
-// warps: conv3 then reads only its 2 KB act2 window per MMA from SMEM (336 -> 264 KB per image).
-// TMEM: T2[2] cols 0..127, T3 (single: conv3(i) is issued after conv2(i+1), long after the
-// epilogue read T3 of image i-1) cols 128..191, W3 cols 192..479.
+// TMEM: T2[2] cols 0..255 (N = 128 each), T3 (single: conv3(i) is issued after conv2(i+1), long
+// after the epilogue read T3 of image i-1) cols 256..319, W3 (6 groups x 32 cols) 320..511.
 // Warps: 0 producer, 1 conv2 MMA issuer, 2-9 conv2 epilogue (lane quarter x 32-channel half),
-// 10-13 conv3 epilogue (lane quarter; lanes 0-15 carry a channel) + the W3 -> TMEM load,
-// 14 conv3 MMA issuer. Two issuing warps: while one waits on its barriers the other keeps the
-// tensor pipe's queue filled (one warp alternating conv2(i) / conv3(i-1) left ~300 idle
-// cycles per image at the hand-offs, traced with selector 11).
+// 10-13 conv3 epilogue (lane quarter) + the W3 -> TMEM load, 14 conv3 MMA issuer. Two issuing
+// warps: while one waits on its barriers the other keeps the tensor pipe's queue filled.
 constexpr int kC23Threads = 480;
 constexpr uint32_t kC23Plane = 104 * 128;                 // compact act1 row block (rows 0..103)
 constexpr uint32_t kC23In = 2 * kC23Plane;                // 26,624 per act1 image
 constexpr uint32_t kC23A2 = 11 * 1024;                    // act2 image: 84 rows x 128 B, 1 KB aligned
-constexpr int kC23InBufs = 3;                             // act1 ring depth (the SMEM W3 copy is gone)
-constexpr int kC23Smem = 8 * 64 * 128 + kC23InBufs * (int)kC23In + 2 * (int)kC23A2 + 2 * kC3tOutBytes + 1024;
-constexpr uint32_t kC23W3Col = 192;                       // TMEM column of W3 (288 columns)
+constexpr int kC23InBufs = 3;                             // act1 ring depth
+constexpr int kX3Ld = 68;                                 // conv3 hand-off row stride (floats): conflict-free
+constexpr int kC23Smem = 4 * 128 * 128 + kC23InBufs * (int)kC23In + 2 * (int)kC23A2 + 2 * kC3tOutBytes +
+                         64 * kX3Ld * 4 + 2 * 2 * 4 * 32 * 4 + 1024;
+constexpr uint32_t kC23T3Col = 256;
+constexpr uint32_t kC23W3Col = 320;                       // TMEM column of W3 (6 groups x 32 columns)
 __device__ __forceinline__ void mma_ts_pred(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc,
                                             uint32_t issue) {
   asm volatile(
@@ -1205,28 +1216,37 @@ __device__ __forceinline__ void mma_ts_pred(uint32_t d, uint32_t a_tmem, uint64_
       "@q tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
       "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc), "r"(issue));
 }
+// conv3 tap groups: lower-half tap (ty, tx) with window offset s = 9 ty + tx; the upper half
+// holds tap (ty, tx + 1) for groups 0-2 and zeros for groups 3-5
+__host__ __device__ constexpr int c3_lo_ty(int g) { return g < 3 ? g : g - 3; }
+__host__ __device__ constexpr int c3_lo_tx(int g) { return g < 3 ? 0 : 2; }
 
 __global__ void __launch_bounds__(kC23Threads, 1)
-    k_conv23(ConvSW P2, ConvSW P3, const uint8_t *__restrict__ W2, const float *__restrict__ bias2,
+    k_conv23(ConvSW P2, ConvSW P3, const uint8_t *__restrict__ W2p, const float *__restrict__ bias2,
              const uint8_t *__restrict__ W3, const float *__restrict__ bias3, const uint8_t *__restrict__ in,
              int64_t n_img, uint8_t *__restrict__ out) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u);
-  uint8_t *sW2 = smem;                                  // conv2 B: 8 k-blocks x [64 x 128 B]
-  uint8_t *sIn = sW2 + 8 * 64 * 128;                    // kC23InBufs x act1 (compact planes)
+  uint8_t *sW2 = smem;                                  // conv2 B: 4 k-blocks (pair, 64-channel half) x [128 x 128 B]
+  uint8_t *sIn = sW2 + 4 * 128 * 128;                   // kC23InBufs x act1 (compact planes)
   uint8_t *sA2 = sIn + kC23InBufs * kC23In;             // 2 x act2
   uint8_t *sO3 = sA2 + 2 * kC23A2;                      // 2 x act3 staging [49][64] bf16
+  float *sX3 = (float *)(sO3 + 2 * kC3tOutBytes);       // conv3 upper-half rows [64][kX3Ld]
+  float *sX2 = sX3 + 64 * kX3Ld;                        // conv2 row hand-off [2 buf][2 half][4 quarter][32]
   __shared__ __align__(8) uint64_t in_full[kC23InBufs], in_empty[kC23InBufs], t2full[2], t2empty[2], a2full[2],
       a2empty[2], t3full, t3empty, w3ready, wbar;
   __shared__ uint32_t tmem_slot;
   __shared__ float sb2[64], sb3[64];
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
-  // debug timeline (BCTS trace selector 11, CTA 0): [img][8] clock64 stamps, pointer held in a register
-  unsigned long long *const trp = (g_trace_sel == 11 && blockIdx.x == 0) ? g_trace : nullptr;
   if (threadIdx.x < 64) {
     sb2[threadIdx.x] = bias2[threadIdx.x];
     sb3[threadIdx.x] = bias3[threadIdx.x];
   }
+  // act2 rows 81..87 are never written by the conv2 epilogue, but the zero-weight upper half of
+  // conv3's groups 3-5 reads rows up to 81 for a kept output (0 x NaN = NaN): zero them once
+  for (int i = threadIdx.x; i < 2 * 7 * 8; i += blockDim.x)
+    *(uint4 *)(sA2 + (i / 56) * kC23A2 + (81 + (i % 56) / 8) * 128 + (i % 8) * 16) = make_uint4(0, 0, 0, 0);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (threadIdx.x == 0) {
     for (int i = 0; i < kC23InBufs; ++i) {
       mbar_init(&in_full[i], 1);
@@ -1243,8 +1263,8 @@ __global__ void __launch_bounds__(kC23Threads, 1)
     mbar_init(&w3ready, 128);
     mbar_init(&wbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    mbar_expect_tx(&wbar, 8u * 64 * 128);
-    bulk_g2s(saddr(sW2), W2, 8u * 64 * 128, &wbar);
+    mbar_expect_tx(&wbar, 4u * 128 * 128);
+    bulk_g2s(saddr(sW2), W2p, 4u * 128 * 128, &wbar);
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(&tmem_slot)),
@@ -1254,7 +1274,7 @@ __global__ void __launch_bounds__(kC23Threads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = tmem_slot;   // cols [0,128): T2[2]; [128,192): T3; [192,480): W3
+  const uint32_t tmem = tmem_slot;
   pdl_wait();
   pdl_trigger();
   const int n_my = n_img > blockIdx.x ? (int)((n_img - 1 - blockIdx.x) / gridDim.x + 1) : 0;
@@ -1273,67 +1293,53 @@ __global__ void __launch_bounds__(kC23Threads, 1)
     }
     __syncwarp();
   } else if (warp == 14) {   // ------------------------------------------ conv3 MMA issuer
-    constexpr uint32_t idesc3 = idesc_bf16(64, 64);
+    constexpr uint32_t idesc3 = idesc_bf16(128, 64);
     const uint32_t elected = elect_one();
-    auto conv3 = [&](int jj) {
+    for (int jj = 0; jj < n_my; ++jj) {
       if (jj == 0) mbar_wait(&w3ready, 0);   // W3 in TMEM (tcgen05.st by the conv3-epilogue warps)
       const uint32_t b = jj & 1, ph = (jj >> 1) & 1u;
-      if (trp && jj < 64 && elected) trp[jj * 8 + 4] = clock64();   // conv3: waits begin
       mbar_wait(&a2full[b], ph);
-      if (trp && jj < 64 && elected) trp[jj * 8 + 5] = clock64();   // act2 ready
       mbar_wait(&t3empty, (jj & 1u) ^ 1u);
       tc_fence_after();
       const uint64_t xdesc = desc_sw128_win(saddr(sA2 + b * kC23A2), false);
 #pragma unroll
-      for (int tap = 0; tap < 9; ++tap)
+      for (int g = 0; g < 6; ++g)
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {   // A: W3 columns (tap * 64 + kk * 16) / 2 of the TMEM copy
-          const uint32_t x_off = (uint32_t)((tap / 3) * 9 + (tap % 3)) * 128u + (uint32_t)(kk * 32);
-          mma_ts_pred(tmem + 128, tmem + kC23W3Col + (uint32_t)(tap * 32 + kk * 8), xdesc + (x_off >> 4), idesc3,
-                      (tap | kk) != 0, elected);
+        for (int kk = 0; kk < 4; ++kk) {   // A: group g's K-step kk = W3 columns g * 32 + kk * 8
+          const uint32_t x_off = (uint32_t)(c3_lo_ty(g) * 9 + c3_lo_tx(g)) * 128u + (uint32_t)(kk * 32);
+          mma_ts_pred(tmem + kC23T3Col, tmem + kC23W3Col + (uint32_t)(g * 32 + kk * 8), xdesc + (x_off >> 4), idesc3,
+                      (g | kk) != 0, elected);
         }
       commit_pred(&a2empty[b], elected);
       commit_pred(&t3full, elected);
-      if (trp && jj < 64 && elected) trp[jj * 8 + 6] = clock64();   // conv3 issued
-    };
-    for (int jj = 0; jj < n_my; ++jj) {
-      conv3(jj);
       __syncwarp();
     }
   } else if (warp == 1) {   // ------------------------------------------ conv2 MMA issuer
-    constexpr uint32_t idesc2 = idesc_bf16(128, 64);
+    constexpr uint32_t idesc2 = idesc_bf16(128, 128);
     const uint32_t elected = elect_one();
     mbar_wait(&wbar, 0);
     const uint64_t w2desc = desc_sw128(saddr(sW2));
     for (int li = 0; li < n_my; ++li) {
-      {   // conv2(li): 4 taps x 8 K-steps
-        const uint32_t b = li & 1, ph = (li >> 1) & 1u;
-        const uint32_t bi = li % kC23InBufs, phi = (li / kC23InBufs) & 1u;
-        if (trp && li < 64 && elected) trp[li * 8 + 0] = clock64();   // conv2: waits begin
-        mbar_wait(&in_full[bi], phi);
-        if (trp && li < 64 && elected) trp[li * 8 + 1] = clock64();   // act1 landed
-        mbar_wait(&t2empty[b], ph ^ 1u);
-        if (trp && li < 64 && elected) trp[li * 8 + 2] = clock64();   // T2 free
-        tc_fence_after();
-        const uint64_t adesc0 = desc_sw128_win(saddr(sIn + bi * kC23In), false);
+      const uint32_t b = li & 1, ph = (li >> 1) & 1u;
+      const uint32_t bi = li % kC23InBufs, phi = (li / kC23InBufs) & 1u;
+      mbar_wait(&in_full[bi], phi);
+      mbar_wait(&t2empty[b], ph ^ 1u);
+      tc_fence_after();
+      const uint64_t adesc0 = desc_sw128_win(saddr(sIn + bi * kC23In), false);
 #pragma unroll
-        for (int tap = 0; tap < 4; ++tap)
+      for (int pr = 0; pr < 2; ++pr)   // tap pair (pr, 0 | pr, 1): window offset 10 pr
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            const uint32_t a_off = (uint32_t)(kk >> 2) * kC23Plane + (uint32_t)((tap >> 1) * 10 + (tap & 1)) * 128u +
-                                   (uint32_t)((kk & 3) * 32);
-            const int k = tap * 128 + 16 * kk;
-            const uint32_t w_off = (uint32_t)(k >> 6) * (64 * 128) + (uint32_t)((k & 63) * 2);
-            mma_pred(tmem + b * 64, adesc0 + (a_off >> 4), w2desc + (w_off >> 4), idesc2, (tap | kk) != 0, elected);
-          }
-        commit_pred(&in_empty[bi], elected);
-        commit_pred(&t2full[b], elected);
-        if (trp && li < 64 && elected) trp[li * 8 + 3] = clock64();   // conv2 issued
-      }
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t a_off = (uint32_t)(kk >> 2) * kC23Plane + (uint32_t)(pr * 10) * 128u + (uint32_t)((kk & 3) * 32);
+          const uint32_t w_off = (uint32_t)(pr * 2 + (kk >> 2)) * (128 * 128) + (uint32_t)((kk & 3) * 32);
+          mma_pred(tmem + b * 128, adesc0 + (a_off >> 4), w2desc + (w_off >> 4), idesc2, (pr | kk) != 0, elected);
+        }
+      commit_pred(&in_empty[bi], elected);
+      commit_pred(&t2full[b], elected);
       __syncwarp();
     }
   } else if (warp < 10) {   // --------------------------- conv2 epilogue -> act2 in SMEM (SW128)
-    const int q4 = warp & 3, c0 = ((warp - 2) >> 2) * 32;
+    const int q4 = warp & 3, hf = (warp - 2) >> 2, c0 = hf * 32;
     const int r = q4 * 32 + lane;                       // full-width output row: oy = r / 10, ox = r % 10
     const int oy = r / 10, ox = r - oy * 10;
     const bool valid = oy < 9 && ox < 9;
@@ -1344,16 +1350,35 @@ __global__ void __launch_bounds__(kC23Threads, 1)
     for (int li = 0; li < n_my; ++li) {
       const uint32_t b = li & 1, ph = (li >> 1) & 1u;
       mbar_wait(&t2full[b], ph);
-      if (trp && li < 64 && threadIdx.x == 64) trp[li * 8 + 7] = clock64();   // conv2 done (epilogue starts)
       tc_fence_after();
-      uint32_t v[2][16];
-      const uint32_t tb = tmem + b * 64 + ((uint32_t)(q4 * 32) << 16) + (uint32_t)c0;
+      uint32_t v[4][16];   // [0..1]: D_L (this row), [2..3]: D_R (this row)
+      const uint32_t tb = tmem + b * 128 + ((uint32_t)(q4 * 32) << 16) + (uint32_t)c0;
       tmem_ld16_nw(tb, v[0]);
       tmem_ld16_nw(tb + 16, v[1]);
+      tmem_ld16_nw(tb + 64, v[2]);
+      tmem_ld16_nw(tb + 80, v[3]);
       tmem_wait16(v[0]);
       tmem_wait16(v[1]);
+      tmem_wait16(v[2]);
+      tmem_wait16(v[3]);
       tc_fence_before();
       mbar_arrive(&t2empty[b]);
+      // D_R of row r + 1: the next lane, or (lane 31) lane 0 of the next quarter via SMEM
+      float *xw = sX2 + ((b * 2 + hf) * 4 + q4) * 32;
+      if (lane == 0) {
+#pragma unroll
+        for (int c = 0; c < 32; c += 4)
+          *(float4 *)(xw + c) = make_float4(__uint_as_float(v[2 + c / 16][c % 16]), __uint_as_float(v[2 + c / 16][c % 16 + 1]),
+                                            __uint_as_float(v[2 + c / 16][c % 16 + 2]), __uint_as_float(v[2 + c / 16][c % 16 + 3]));
+      }
+      asm volatile("bar.sync 3, 256;" ::: "memory");   // the 8 conv2-epilogue warps
+      const float *xr = xw + 32;                        // quarter q4 + 1 (only read when q4 < 3)
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        float nx = __shfl_down_sync(0xffffffffu, __uint_as_float(v[2 + c / 16][c % 16]), 1);
+        if (lane == 31) nx = q4 < 3 ? xr[c] : 0.0f;
+        v[c / 16][c % 16] = __float_as_uint(__uint_as_float(v[c / 16][c % 16]) + nx);
+      }
       mbar_wait(&a2empty[b], ph ^ 1u);                  // conv3 of image li-2 is done with sA2[b]
       if (valid) {
         uint8_t *dst = sA2 + b * kC23A2 + row * 128;
@@ -1376,23 +1401,25 @@ __global__ void __launch_bounds__(kC23Threads, 1)
       mbar_arrive(&a2full[b]);
     }
   } else {   // ------------------------------------------- conv3 epilogue -> act3 (dense), warps 10-13
-    const int q = warp & 3;
-    const int c = 16 * q + (lane & 15);
+    const int q = warp & 3;                 // TMEM lane quarter; q < 2: tap a (lower half), q >= 2: tap b
+    const bool upper = q >= 2;
+    const int c = 32 * (q & 1) + lane;      // output channel of this lane
     const float bc = sb3[c];
-    const uint32_t taddr0 = tmem + 128 + ((uint32_t)(q * 32) << 16);
+    const uint32_t taddr0 = tmem + kC23T3Col + ((uint32_t)(q * 32) << 16);
     const bool lead = threadIdx.x == 32 * 10;
-    {   // W3 -> TMEM: output channel m = 16q + l (lanes l < 16 of quarter q), K = (tap, cin) in
-        // bf16 pairs per column; source = the SW128 weight image in global memory
+    {   // W3 -> TMEM: lane m = 64 h + c holds output channel c of group g's tap (upper half:
+        // tap (ty, tx + 1) for g < 3, zero for g >= 3); K = cin in bf16 pairs per column; source =
+        // the SW128 weight image in global memory ([tap][64 rows][128 B])
       uint32_t r[32];
 #pragma unroll 1
-      for (int tap = 0; tap < 9; ++tap) {
+      for (int g = 0; g < 6; ++g) {
+        const int ty = c3_lo_ty(g), tx = c3_lo_tx(g) + (upper ? 1 : 0);
+        const bool zero = upper && g >= 3;
+        const int tap = ty * 3 + tx;
 #pragma unroll
-        for (int ch = 0; ch < 8; ++ch) {   // 8-channel chunk ch of this tap: 4 columns
+        for (int ch = 0; ch < 8; ++ch) {   // 8-channel chunk ch: 4 columns
           uint4 v4 = make_uint4(0, 0, 0, 0);
-          if (lane < 16) {
-            const int m = 16 * q + lane;
-            v4 = __ldg((const uint4 *)(W3 + (size_t)tap * (64 * 128) + (size_t)m * 128 + (((ch ^ (m & 7)) & 7) << 4)));
-          }
+          if (!zero) v4 = __ldg((const uint4 *)(W3 + (size_t)tap * (64 * 128) + (size_t)c * 128 + (((ch ^ (c & 7)) & 7) << 4)));
           r[4 * ch] = v4.x;
           r[4 * ch + 1] = v4.y;
           r[4 * ch + 2] = v4.z;
@@ -1401,7 +1428,7 @@ __global__ void __launch_bounds__(kC23Threads, 1)
         asm volatile(
             "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
             "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(
-                tmem + ((uint32_t)(q * 32) << 16) + kC23W3Col + (uint32_t)(tap * 32)),
+                tmem + ((uint32_t)(q * 32) << 16) + kC23W3Col + (uint32_t)(g * 32)),
             "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
             "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
             "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
@@ -1411,6 +1438,7 @@ __global__ void __launch_bounds__(kC23Threads, 1)
       tc_fence_before();
       mbar_arrive(&w3ready);
     }
+    float *xrow = sX3 + c * kX3Ld;
     for (int li = 0; li < n_my; ++li) {
       const int64_t img = blockIdx.x + (int64_t)li * gridDim.x;
       const uint32_t b = li & 1;
@@ -1427,17 +1455,31 @@ __global__ void __launch_bounds__(kC23Threads, 1)
       tmem_wait16(*(uint32_t(*)[16])(v + 48));
       tc_fence_before();
       mbar_arrive(&t3empty);
+      if (upper) {   // hand D_hi[c][1..62] to the lower half (row stride 68 floats: conflict-free float4)
+#pragma unroll
+        for (int n = 0; n < 64; n += 4)
+          *(float4 *)(xrow + n) = make_float4(__uint_as_float(v[n]), __uint_as_float(v[n + 1]), __uint_as_float(v[n + 2]),
+                                             __uint_as_float(v[n + 3]));
+      }
       uint8_t *so = sO3 + b * kC3tOutBytes;
       if (lead) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (lane < 16) {
+      if (!upper) {
 #pragma unroll
-        for (int n = 0; n < 63; ++n) {
-          const int oy = n / 9, ox = n % 9;
-          if (oy < 7 && ox < 7) {
-            uint16_t h;
-            asm("cvt.rn.relu.bf16.f32 %0, %1;" : "=h"(h) : "f"(__uint_as_float(v[n]) + bc));
-            *(uint16_t *)(so + ((oy * 7 + ox) * 64 + c) * 2) = h;
+        for (int n4 = 0; n4 < 64; n4 += 4) {
+          const float4 hi = *(const float4 *)(xrow + n4);
+          const float h4[4] = {hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int n = n4 + e - 1;   // D_hi[n + 1] is a term of out[n]
+            if (n >= 0 && n < 63) {
+              const int oy = n / 9, ox = n % 9;
+              if (oy < 7 && ox < 7) {
+                uint16_t h;
+                asm("cvt.rn.relu.bf16.f32 %0, %1;" : "=h"(h) : "f"(__uint_as_float(v[n]) + h4[e] + bc));
+                *(uint16_t *)(so + ((oy * 7 + ox) * 64 + c) * 2) = h;
+              }
+            }
           }
         }
       }
@@ -1545,7 +1587,7 @@ void launch_conv23(const ConvSW &P2, const Layer &L2, const ConvSW &P3, const La
     attr = true;
   }
   const int grid = (int)std::min<int64_t>(n_img, num_sms());
-  launch_pdl(k_conv23, dim3(grid), dim3(kC23Threads), (size_t)kC23Smem, st, P2, P3, P2.wsw, L2.bias, P3.wsw, L3.bias,
+  launch_pdl(k_conv23, dim3(grid), dim3(kC23Threads), (size_t)kC23Smem, st, P2, P3, P2.wpair, L2.bias, P3.wsw, L3.bias,
              (const uint8_t *)in, n_img, (uint8_t *)out);
 }
 
