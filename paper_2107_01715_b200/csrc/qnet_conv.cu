@@ -1194,8 +1194,9 @@ __global__ void __launch_bounds__(kC3tThreads, 1)
 //    the same per instruction: 768 instead of 1,152 tensor cycles per image, 48 instead of 72 KB
 //    of B reads. The sums are the same products in another fp32 order (R17/R18).
 // act1 lands in a compact ring (planes of 104 rows instead of act1's 144-row global planes).
-// TMEM: T2[2] cols 0..255 (N = 128 each), T3 (single: conv3(i) is issued after conv2(i+1), long
-// after the epilogue read T3 of image i-1) cols 256..319, W3 (6 groups x 32 cols) 320..511.
+// TMEM: T2 cols 0..127 (single: its epilogue releases it right after tcgen05.ld, while conv3(i-1)
+// keeps the tensor pipe busy), T3[2] cols 128..255 (double: the conv3 epilogue's hand-off and
+// staging take longer than one image's conv3 MMAs), W3 (6 groups x 32 cols) 256..447.
 // Warps: 0 producer, 1 conv2 MMA issuer, 2-9 conv2 epilogue (lane quarter x 32-channel half),
 // 10-13 conv3 epilogue (lane quarter) + the W3 -> TMEM load, 14 conv3 MMA issuer. Two issuing
 // warps: while one waits on its barriers the other keeps the tensor pipe's queue filled.
@@ -1207,8 +1208,8 @@ constexpr int kC23InBufs = 3;                             // act1 ring depth
 constexpr int kX3Ld = 68;                                 // conv3 hand-off row stride (floats): conflict-free
 constexpr int kC23Smem = 4 * 128 * 128 + kC23InBufs * (int)kC23In + 2 * (int)kC23A2 + 2 * kC3tOutBytes +
                          64 * kX3Ld * 4 + 2 * 2 * 4 * 32 * 4 + 1024;
-constexpr uint32_t kC23T3Col = 256;
-constexpr uint32_t kC23W3Col = 320;                       // TMEM column of W3 (6 groups x 32 columns)
+constexpr uint32_t kC23T3Col = 128;                       // T3[2]: columns 128..255
+constexpr uint32_t kC23W3Col = 256;                       // TMEM column of W3 (6 groups x 32 columns)
 __device__ __forceinline__ void mma_ts_pred(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc,
                                             uint32_t issue) {
   asm volatile(
@@ -1233,8 +1234,8 @@ __global__ void __launch_bounds__(kC23Threads, 1)
   uint8_t *sO3 = sA2 + 2 * kC23A2;                      // 2 x act3 staging [49][64] bf16
   float *sX3 = (float *)(sO3 + 2 * kC3tOutBytes);       // conv3 upper-half rows [64][kX3Ld]
   float *sX2 = sX3 + 64 * kX3Ld;                        // conv2 row hand-off [2 buf][2 half][4 quarter][32]
-  __shared__ __align__(8) uint64_t in_full[kC23InBufs], in_empty[kC23InBufs], t2full[2], t2empty[2], a2full[2],
-      a2empty[2], t3full, t3empty, w3ready, wbar;
+  __shared__ __align__(8) uint64_t in_full[kC23InBufs], in_empty[kC23InBufs], t2full, t2empty, a2full[2],
+      a2empty[2], t3full[2], t3empty[2], w3ready, wbar;
   __shared__ uint32_t tmem_slot;
   __shared__ float sb2[64], sb3[64];
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
@@ -1253,13 +1254,13 @@ __global__ void __launch_bounds__(kC23Threads, 1)
       mbar_init(&in_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&t2full[i], 1);
-      mbar_init(&t2empty[i], 256);
       mbar_init(&a2full[i], 256);
       mbar_init(&a2empty[i], 1);
+      mbar_init(&t3full[i], 1);
+      mbar_init(&t3empty[i], 128);
     }
-    mbar_init(&t3full, 1);
-    mbar_init(&t3empty, 128);
+    mbar_init(&t2full, 1);
+    mbar_init(&t2empty, 256);
     mbar_init(&w3ready, 128);
     mbar_init(&wbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1299,7 +1300,7 @@ __global__ void __launch_bounds__(kC23Threads, 1)
       if (jj == 0) mbar_wait(&w3ready, 0);   // W3 in TMEM (tcgen05.st by the conv3-epilogue warps)
       const uint32_t b = jj & 1, ph = (jj >> 1) & 1u;
       mbar_wait(&a2full[b], ph);
-      mbar_wait(&t3empty, (jj & 1u) ^ 1u);
+      mbar_wait(&t3empty[b], ph ^ 1u);
       tc_fence_after();
       const uint64_t xdesc = desc_sw128_win(saddr(sA2 + b * kC23A2), false);
 #pragma unroll
@@ -1307,11 +1308,11 @@ __global__ void __launch_bounds__(kC23Threads, 1)
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {   // A: group g's K-step kk = W3 columns g * 32 + kk * 8
           const uint32_t x_off = (uint32_t)(c3_lo_ty(g) * 9 + c3_lo_tx(g)) * 128u + (uint32_t)(kk * 32);
-          mma_ts_pred(tmem + kC23T3Col, tmem + kC23W3Col + (uint32_t)(g * 32 + kk * 8), xdesc + (x_off >> 4), idesc3,
+          mma_ts_pred(tmem + kC23T3Col + b * 64, tmem + kC23W3Col + (uint32_t)(g * 32 + kk * 8), xdesc + (x_off >> 4), idesc3,
                       (g | kk) != 0, elected);
         }
       commit_pred(&a2empty[b], elected);
-      commit_pred(&t3full, elected);
+      commit_pred(&t3full[b], elected);
       __syncwarp();
     }
   } else if (warp == 1) {   // ------------------------------------------ conv2 MMA issuer
@@ -1323,7 +1324,7 @@ __global__ void __launch_bounds__(kC23Threads, 1)
       const uint32_t b = li & 1, ph = (li >> 1) & 1u;
       const uint32_t bi = li % kC23InBufs, phi = (li / kC23InBufs) & 1u;
       mbar_wait(&in_full[bi], phi);
-      mbar_wait(&t2empty[b], ph ^ 1u);
+      mbar_wait(&t2empty, (li & 1u) ^ 1u);
       tc_fence_after();
       const uint64_t adesc0 = desc_sw128_win(saddr(sIn + bi * kC23In), false);
 #pragma unroll
@@ -1332,10 +1333,10 @@ __global__ void __launch_bounds__(kC23Threads, 1)
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t a_off = (uint32_t)(kk >> 2) * kC23Plane + (uint32_t)(pr * 10) * 128u + (uint32_t)((kk & 3) * 32);
           const uint32_t w_off = (uint32_t)(pr * 2 + (kk >> 2)) * (128 * 128) + (uint32_t)((kk & 3) * 32);
-          mma_pred(tmem + b * 128, adesc0 + (a_off >> 4), w2desc + (w_off >> 4), idesc2, (pr | kk) != 0, elected);
+          mma_pred(tmem, adesc0 + (a_off >> 4), w2desc + (w_off >> 4), idesc2, (pr | kk) != 0, elected);
         }
       commit_pred(&in_empty[bi], elected);
-      commit_pred(&t2full[b], elected);
+      commit_pred(&t2full, elected);
       __syncwarp();
     }
   } else if (warp < 10) {   // --------------------------- conv2 epilogue -> act2 in SMEM (SW128)
@@ -1349,10 +1350,10 @@ __global__ void __launch_bounds__(kC23Threads, 1)
     for (int c = 0; c < 32; ++c) bias_r[c] = sb2[c0 + c];
     for (int li = 0; li < n_my; ++li) {
       const uint32_t b = li & 1, ph = (li >> 1) & 1u;
-      mbar_wait(&t2full[b], ph);
+      mbar_wait(&t2full, li & 1u);
       tc_fence_after();
       uint32_t v[4][16];   // [0..1]: D_L (this row), [2..3]: D_R (this row)
-      const uint32_t tb = tmem + b * 128 + ((uint32_t)(q4 * 32) << 16) + (uint32_t)c0;
+      const uint32_t tb = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)c0;
       tmem_ld16_nw(tb, v[0]);
       tmem_ld16_nw(tb + 16, v[1]);
       tmem_ld16_nw(tb + 64, v[2]);
@@ -1362,7 +1363,7 @@ __global__ void __launch_bounds__(kC23Threads, 1)
       tmem_wait16(v[2]);
       tmem_wait16(v[3]);
       tc_fence_before();
-      mbar_arrive(&t2empty[b]);
+      mbar_arrive(&t2empty);
       // D_R of row r + 1: the next lane, or (lane 31) lane 0 of the next quarter via SMEM
       float *xw = sX2 + ((b * 2 + hf) * 4 + q4) * 32;
       if (lane == 0) {
@@ -1372,12 +1373,18 @@ __global__ void __launch_bounds__(kC23Threads, 1)
                                             __uint_as_float(v[2 + c / 16][c % 16 + 2]), __uint_as_float(v[2 + c / 16][c % 16 + 3]));
       }
       asm volatile("bar.sync 3, 256;" ::: "memory");   // the 8 conv2-epilogue warps
-      const float *xr = xw + 32;                        // quarter q4 + 1 (only read when q4 < 3)
 #pragma unroll
-      for (int c = 0; c < 32; ++c) {
-        float nx = __shfl_down_sync(0xffffffffu, __uint_as_float(v[2 + c / 16][c % 16]), 1);
-        if (lane == 31) nx = q4 < 3 ? xr[c] : 0.0f;
-        v[c / 16][c % 16] = __float_as_uint(__uint_as_float(v[c / 16][c % 16]) + nx);
+      for (int c4 = 0; c4 < 32; c4 += 4) {
+        float4 t = make_float4(0.f, 0.f, 0.f, 0.f);     // lane 31: quarter q4 + 1's row 0 (q4 < 3)
+        if (lane == 31 && q4 < 3) t = *(const float4 *)(xw + 32 + c4);
+        const float tn[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int c = c4 + e;
+          float nx = __shfl_down_sync(0xffffffffu, __uint_as_float(v[2 + c / 16][c % 16]), 1);
+          if (lane == 31) nx = tn[e];
+          v[c / 16][c % 16] = __float_as_uint(__uint_as_float(v[c / 16][c % 16]) + nx);
+        }
       }
       mbar_wait(&a2empty[b], ph ^ 1u);                  // conv3 of image li-2 is done with sA2[b]
       if (valid) {
@@ -1438,48 +1445,69 @@ __global__ void __launch_bounds__(kC23Threads, 1)
       tc_fence_before();
       mbar_arrive(&w3ready);
     }
+    // hand-off row of channel c: [0, 36) = D_hi columns 0..35 (written by the upper half),
+    // [36, 68) = D_lo columns 32..63 (written by the lower half). The lower half then finishes
+    // output rows n < 32 (it needs D_hi[1..32]), the upper half rows 32..62 (it needs D_lo[32..62]).
     float *xrow = sX3 + c * kX3Ld;
     for (int li = 0; li < n_my; ++li) {
       const int64_t img = blockIdx.x + (int64_t)li * gridDim.x;
-      const uint32_t b = li & 1;
-      mbar_wait(&t3full, li & 1u);
+      const uint32_t b = li & 1, ph = (li >> 1) & 1u;
+      mbar_wait(&t3full[b], ph);
       tc_fence_after();
       uint32_t v[64];
-      tmem_ld16_nw(taddr0 + 0, *(uint32_t(*)[16])(v + 0));
-      tmem_ld16_nw(taddr0 + 16, *(uint32_t(*)[16])(v + 16));
-      tmem_ld16_nw(taddr0 + 32, *(uint32_t(*)[16])(v + 32));
-      tmem_ld16_nw(taddr0 + 48, *(uint32_t(*)[16])(v + 48));
+      const uint32_t ta = taddr0 + b * 64;
+      tmem_ld16_nw(ta + 0, *(uint32_t(*)[16])(v + 0));
+      tmem_ld16_nw(ta + 16, *(uint32_t(*)[16])(v + 16));
+      tmem_ld16_nw(ta + 32, *(uint32_t(*)[16])(v + 32));
+      tmem_ld16_nw(ta + 48, *(uint32_t(*)[16])(v + 48));
       tmem_wait16(*(uint32_t(*)[16])(v + 0));
       tmem_wait16(*(uint32_t(*)[16])(v + 16));
       tmem_wait16(*(uint32_t(*)[16])(v + 32));
       tmem_wait16(*(uint32_t(*)[16])(v + 48));
       tc_fence_before();
-      mbar_arrive(&t3empty);
-      if (upper) {   // hand D_hi[c][1..62] to the lower half (row stride 68 floats: conflict-free float4)
+      mbar_arrive(&t3empty[b]);
+      if (upper) {
 #pragma unroll
-        for (int n = 0; n < 64; n += 4)
+        for (int n = 0; n < 36; n += 4)
           *(float4 *)(xrow + n) = make_float4(__uint_as_float(v[n]), __uint_as_float(v[n + 1]), __uint_as_float(v[n + 2]),
                                              __uint_as_float(v[n + 3]));
+      } else {
+#pragma unroll
+        for (int n = 32; n < 64; n += 4)
+          *(float4 *)(xrow + 4 + n) = make_float4(__uint_as_float(v[n]), __uint_as_float(v[n + 1]), __uint_as_float(v[n + 2]),
+                                                 __uint_as_float(v[n + 3]));
       }
       uint8_t *so = sO3 + b * kC3tOutBytes;
       if (lead) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (!upper) {
+      auto emit = [&](int n, float x) {   // out[n] = D_lo[n] + D_hi[n + 1] + bias (n valid)
+        const int oy = n / 9, ox = n % 9;
+        if (oy < 7 && ox < 7) {
+          uint16_t hv;
+          asm("cvt.rn.relu.bf16.f32 %0, %1;" : "=h"(hv) : "f"(x + bc));
+          *(uint16_t *)(so + ((oy * 7 + ox) * 64 + c) * 2) = hv;
+        }
+      };
+      if (!upper) {   // rows 0..31: own D_lo[n], the upper half's D_hi[n + 1]
 #pragma unroll
-        for (int n4 = 0; n4 < 64; n4 += 4) {
-          const float4 hi = *(const float4 *)(xrow + n4);
-          const float h4[4] = {hi.x, hi.y, hi.z, hi.w};
+        for (int n4 = 0; n4 < 36; n4 += 4) {
+          const float4 t = *(const float4 *)(xrow + n4);
+          const float h4[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const int n = n4 + e - 1;   // D_hi[n + 1] is a term of out[n]
-            if (n >= 0 && n < 63) {
-              const int oy = n / 9, ox = n % 9;
-              if (oy < 7 && ox < 7) {
-                uint16_t h;
-                asm("cvt.rn.relu.bf16.f32 %0, %1;" : "=h"(h) : "f"(__uint_as_float(v[n]) + h4[e] + bc));
-                *(uint16_t *)(so + ((oy * 7 + ox) * 64 + c) * 2) = h;
-              }
-            }
+            const int n = n4 + e - 1;
+            if (n >= 0 && n < 32) emit(n, __uint_as_float(v[n]) + h4[e]);
+          }
+        }
+      } else {        // rows 32..62: the lower half's D_lo[n], own D_hi[n + 1]
+#pragma unroll
+        for (int n4 = 32; n4 < 64; n4 += 4) {
+          const float4 t = *(const float4 *)(xrow + 4 + n4);
+          const float l4[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int n = n4 + e;
+            if (n < 63) emit(n, l4[e] + __uint_as_float(v[n + 1]));
           }
         }
       }
