@@ -1157,10 +1157,6 @@ int32_t bcts_profile_read(bcts_handle h, bcts_kernel_profile *out, int32_t max) 
   return k;
 }
 
-// Test hook (not part of the public contract): route the shifted-window conv
-// kernel's CTA-0 phase timestamps to a device buffer (NULL disables).
-void bcts_debug_conv_trace(void *dev_buf, int32_t layer) { conv_trace_set((unsigned long long *)dev_buf, layer); }
-
 // Test hook (not part of the public contract): copy the head of an internal trunk buffer
 // (0 = act1 planar, 1 = act2 planar, 2 = act3 dense, 3 = leaf R_d) to dst (device).
 int64_t bcts_debug_net_buffer(bcts_handle h, int32_t which, void *dst, int64_t bytes) {

@@ -191,14 +191,10 @@ void launch_conv_sw(const ConvSW &P, const Layer &L, const void *in, int64_t n_i
 // conv2 + conv3 in one kernel (act2 stays in SMEM): act1 planar in, dense act3 out
 void launch_conv23(const ConvSW &P2, const Layer &L2, const ConvSW &P3, const Layer &L3, const void *in, int64_t n_img,
                    void *out, cudaStream_t st);
-void conv_trace_set(unsigned long long *p, int sel);
 // conv1, sibling-factorised (shared frames once per parent + new frame per child)
 void launch_conv1_sib(const ConvSW &P, const Layer &L, const uint8_t *wsh, const uint8_t *wnw, const NodeView &par,
                       int64_t p_first, int64_t c_begin, int64_t n_img, int A, float gk, void *out, float *cum_out,
                       cudaStream_t st);
-// conv1 with the last-level expansion fused in (children [c_begin, c_begin+n) of `par`)
-void launch_conv1_fused(const ConvSW &P, const Layer &L, const NodeView &par, int64_t p_first, int64_t c_begin,
-                        int64_t n_img, int A, float gk, void *out, float *cum_out, cudaStream_t st);
 // Trunk activation layout (runtime, BCTS_CONV_LAYOUT): 0 = chunk-planar
 // SWIZZLE_NONE; 1 = SW128 row blocks, descriptor base_offset = row phase;
 // 2 = SW128 row blocks, base_offset 0. In the SW128 layouts

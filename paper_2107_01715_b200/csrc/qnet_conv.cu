@@ -95,6 +95,14 @@ __device__ __forceinline__ uint32_t bf16x2_relu(float lo, float hi) {
   asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
   return r;
 }
+// two independent fp32 FMAs in one FFMA2 (each rounded exactly as fmaf)
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(r)
+      : "l"(*(const uint64_t *)&a), "l"(*(const uint64_t *)&b), "l"(*(const uint64_t *)&c));
+  return *(const float2 *)&r;
+}
 // kind::f16 with fp16 A and B (a_format = b_format = 0), fp32 accumulate
 __host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
   return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
@@ -166,17 +174,6 @@ __device__ __forceinline__ void tmem_wait16(uint32_t (&r)[16]) {
                : "memory");
 }
 
-// Debug phase timestamps (CTA 0 only; BCTS_CONV_TRACE=1): [img][4] =
-// copy issued, input ready (MMA side), MMAs issued, epilogue done.
-__device__ unsigned long long *g_trace = nullptr;
-__device__ int g_trace_sel = -1;
-__device__ int g_sib_dbg = 0;   // k_conv1_sib timing experiments (conv_trace_set); 0 in production
-__device__ __forceinline__ unsigned long long gtime() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-
 constexpr int kConvInBufs = 3;   // k_conv_sw input ring (G1: 16 KB + 3 x 68 KB fits the 227 KB SMEM)
 // Compile-time trunk geometry (stride-1 convs after space-to-depth).
 struct G1 { static constexpr int N = 32, CIN = 64, KH = 2, KW = 2, W_IN = 21, N_MT = 4; static constexpr uint32_t BPLANE = kPlane1 * 8; };
@@ -189,7 +186,6 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint8_t *__restrict__ in, int64_t n_img, uint8_t *__restrict__ out) {
   constexpr int N = G::N;
   extern __shared__ uint8_t smem_raw[];
-  const bool tron = g_trace != nullptr && P.out_mode == g_trace_sel && blockIdx.x == 0;   // debug trace, read once
   // 1024-byte aligned base, derived from smem_raw by an OFFSET so the compiler keeps the
   // shared address space (a uintptr_t round trip turns every access into a generic LD/ST)
   uint8_t *smem = smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u);
@@ -241,7 +237,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int64_t img = blockIdx.x; img < n_img; img += gridDim.x, ++i) {
         const uint32_t b = i % NB, ph = (i / NB) & 1u;
         mbar_wait(&in_empty[b], ph ^ 1u);
-        if (tron && i < 64) g_trace[i * 4 + 0] = gtime();
         // only the valid rows of each 64-channel row block cross memory (the
         // windows of garbage outputs read stale smem rows, which is harmless)
         const uint32_t blk = P.plane * 8u, valid = (uint32_t)P.in_rows * 128u;
@@ -265,7 +260,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t bi = i % NB, phi = (i / NB) & 1u;     // input ring slot
       const uint32_t b = i & 1u, ph = (i >> 1) & 1u;         // TMEM accumulator buffer
       mbar_wait(&in_full[bi], phi);
-      if (tron && i < 64 && elected) g_trace[i * 4 + 1] = gtime();
       mbar_wait(&tempty[b], ph ^ 1u);
       tc_fence_after();
       const uint32_t a_base = saddr(sIn0 + bi * in_stride);
@@ -288,7 +282,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             mma_pred(d0 + (uint32_t)(mt * N), adesc0 + (a_off >> 4), wdesc + (w_off >> 4), idesc,
                      (tap | kk) != 0, elected);
           }
-      if (tron && i < 64 && elected) g_trace[i * 4 + 2] = gtime();
       commit_pred(&in_empty[bi], elected);  // input buffer free once these MMAs retire
       commit_pred(&tfull[b], elected);      // accumulators of this image complete
       __syncwarp();
@@ -353,8 +346,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      if (tron && i < 64 && r == 0 && c0 == 0)
-        g_trace[i * 4 + 3] = gtime();
     }
   }
   __syncthreads();
@@ -364,224 +355,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// ============================================================ conv1 + fused leaf expansion
-// The last tree level never exists outside shared memory: converter warps
-// build each child's conv1 input (space-to-depth(4) bf16, SW128 row layout)
-// in smem. Per parent (once per A children) they convert its frame stack to
-// dense bf16 s2d and keep its newest frame's bytes; a child then is the
-// parent's bf16 channels shifted by one frame (the ATARI_HASH step: frames
-// 1..3 move down, Alg. 1) plus one new bf16 per pixel,
-// bf16(parent_newest ^ noise). The child's R_d = fmaf(g[d-1], r, R_{d-1}) is
-// written too. MMA / epilogue as in k_conv_sw<G1>. Each CTA owns a contiguous
-// child range so consecutive children share the converted parent.
-//   warp 0: MMA issuer   warps 1-8: epilogue   warps 9-16: converters
-constexpr int kThreadsF = 544;
-constexpr int kConvThreads = 256;
-
+// splitmix64 finalizer (ENV_SPEC mix64; the ATARI_HASH step's noise and keys)
 __device__ __forceinline__ uint64_t mix64d(uint64_t z) {
   z ^= z >> 30; z *= 0xBF58476D1CE4E5B9ull;
   z ^= z >> 27; z *= 0x94D049BB133111EBull;
   z ^= z >> 31; return z;
-}
-// exact u8 -> bf16 bits in the upper half of the returned float bits
-__device__ __forceinline__ uint32_t u8_f32bits(uint32_t w, uint32_t i) {
-  return __float_as_uint(__uint_as_float(__byte_perm(w, 0x4B000000u, 0x7540u + i)) - 8388608.0f);
-}
-__device__ __forceinline__ uint32_t u8pair_bf16x2(uint32_t w, uint32_t i) {
-  return __byte_perm(u8_f32bits(w, i), u8_f32bits(w, i + 1), 0x7632u);
-}
-__device__ __forceinline__ void conv_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
-
-__global__ void __launch_bounds__(kThreadsF, 1)
-    k_conv1_fused(ConvSW P, const uint8_t *__restrict__ Wsw, const float *__restrict__ bias, NodeView par,
-                  int64_t p_first, int64_t c_begin, int64_t n_img, int A, float gk, uint8_t *__restrict__ out,
-                  float *__restrict__ cum_out) {
-  using G = G1;
-  constexpr int N = G::N;
-  extern __shared__ uint8_t smem_raw[];
-  const bool tron = g_trace != nullptr && g_trace_sel == 9 && blockIdx.x == 0;
-  // 1024-byte aligned base, derived from smem_raw by an OFFSET so the compiler keeps the
-  // shared address space (a uintptr_t round trip turns every access into a generic LD/ST)
-  uint8_t *smem = smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u);
-  constexpr int nkb = 256 / 64;
-  uint8_t *sW = smem;                                           // 16 KB SW128 weights
-  uint8_t *sIn0 = smem + nkb * N * 128;                         // 2 x SW128 s2d child images
-  constexpr uint32_t in_stride = (kIn1Bytes + 1023u) & ~1023u;
-  uint4 *sPar = (uint4 *)(sIn0 + 2 * in_stride);               // parent bf16 s2d, [pix*4 + dy] x 32 B
-  uint32_t *sNew = (uint32_t *)((uint8_t *)sPar + 441 * 4 * 32); // parent newest-frame bytes, 7056 B
-  __shared__ __align__(8) uint64_t in_full[2], in_empty[2], tfull[2], tempty[2], wbar;
-  __shared__ uint32_t tmem_slot;
-  __shared__ float sbias[64];
-  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
-  constexpr uint32_t tcols_img = G::N_MT * N;                   // 128
-  constexpr uint32_t tcols = 256;
-  const int64_t per = (n_img + gridDim.x - 1) / gridDim.x;
-  const int64_t i0 = (int64_t)blockIdx.x * per, i1 = min(n_img, i0 + per);
-  if (threadIdx.x < N) sbias[threadIdx.x] = bias[threadIdx.x];
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&in_full[i], kConvThreads);
-      mbar_init(&in_empty[i], 1);
-      mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 256);
-    }
-    mbar_init(&wbar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    mbar_expect_tx(&wbar, (uint32_t)(nkb * N * 128));
-    bulk_g2s(saddr(sW), Wsw, (uint32_t)(nkb * N * 128), &wbar);
-  }
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(&tmem_slot)),
-                 "r"(tcols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = tmem_slot;
-
-  if (warp == 0) {
-    // ---------------------------------------------- MMA issuer (identical to k_conv_sw<G1>)
-    constexpr uint32_t idesc = idesc_bf16(128, N);
-    constexpr int TAPS = G::KH * G::KW, KSTEPS = G::CIN / 16;
-    const uint32_t elected = elect_one();
-    mbar_wait(&wbar, 0);
-    const uint64_t wdesc = desc_sw128(saddr(sW));
-    uint32_t i = 0;
-    for (int64_t img = i0; img < i1; ++img, ++i) {
-      const uint32_t b = i & 1u, ph = (i >> 1) & 1u;
-      mbar_wait(&in_full[b], ph);
-      mbar_wait(&tempty[b], ph ^ 1u);
-      tc_fence_after();
-      const uint64_t adesc0 = desc_sw128_win(saddr(sIn0 + b * in_stride), false);
-      const uint32_t d0 = tmem + b * tcols_img;
-#pragma unroll
-      for (int mt = 0; mt < G::N_MT; ++mt)
-#pragma unroll
-        for (int tap = 0; tap < TAPS; ++tap)
-#pragma unroll
-          for (int kk = 0; kk < KSTEPS; ++kk) {
-            const uint32_t a_off = (uint32_t)(kk >> 2) * G::BPLANE +
-                                   (uint32_t)(mt * 128 + (tap / G::KW) * G::W_IN + (tap % G::KW)) * 128u +
-                                   (uint32_t)((kk & 3) * 32);
-            const int k = tap * G::CIN + 16 * kk;
-            const uint32_t w_off = (uint32_t)(k >> 6) * (N * 128) + (uint32_t)((k & 63) * 2);
-            mma_pred(d0 + (uint32_t)(mt * N), adesc0 + (a_off >> 4), wdesc + (w_off >> 4), idesc, (tap | kk) != 0,
-                     elected);
-          }
-      if (tron && i < 64 && elected) g_trace[i * 4 + 2] = gtime();
-      commit_pred(&in_empty[b], elected);
-      commit_pred(&tfull[b], elected);
-      __syncwarp();
-    }
-  } else if (warp < 9) {
-    // ---------------------------------------------- epilogue (8 warps) -> conv2's s2d(2) SW128 input
-    constexpr int HALF = N / 2;
-    const int q4 = warp & 3;
-    const int c0 = ((warp - 1) >> 2) * HALF;
-    const int r = q4 * 32 + lane;
-    float bias_r[HALF];
-#pragma unroll
-    for (int c = 0; c < HALF; ++c) bias_r[c] = sbias[c0 + c];
-    uint32_t i = 0;
-    for (int64_t img = i0; img < i1; ++img, ++i) {
-      const uint32_t b = i & 1u, ph = (i >> 1) & 1u;
-      mbar_wait(&tfull[b], ph);
-      tc_fence_after();
-      uint32_t v[G::N_MT][16];
-      const uint32_t tbase = tmem + b * tcols_img + ((uint32_t)(q4 * 32) << 16) + (uint32_t)c0;
-#pragma unroll
-      for (int mt = 0; mt < G::N_MT; ++mt) tmem_ld16_nw(tbase + (uint32_t)(mt * N), v[mt]);
-#pragma unroll
-      for (int mt = 0; mt < G::N_MT; ++mt) tmem_wait16(v[mt]);
-      tc_fence_before();
-      mbar_arrive(&tempty[b]);
-      uint8_t *oimg = out + img * (int64_t)P.out_img_bytes;
-#pragma unroll
-      for (int mt = 0; mt < G::N_MT; ++mt) {
-        const int q = mt * 128 + r;
-        const int oy = q / G::W_IN, ox = q - oy * G::W_IN;
-        if (oy >= 20 || ox >= 20) continue;
-        uint32_t pk[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float x = __uint_as_float(v[mt][2 * e]) + bias_r[2 * e];
-          const float y = __uint_as_float(v[mt][2 * e + 1]) + bias_r[2 * e + 1];
-          __nv_bfloat162 hh = __floats2bfloat162_rn(x > 0.0f ? x : 0.0f, y > 0.0f ? y : 0.0f);
-          pk[e] = *(uint32_t *)&hh;
-        }
-        const int sub = ((oy & 1) << 1) | (ox & 1);
-        const int row = (oy >> 1) * P.out_w + (ox >> 1);
-#pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2)
-          *(uint4 *)(oimg + act_off(2, P.out_plane, row, sub * 4 + ((c0 + 8 * h2) >> 3))) =
-              make_uint4(pk[4 * h2], pk[4 * h2 + 1], pk[4 * h2 + 2], pk[4 * h2 + 3]);
-      }
-      if (tron && i < 64 && r == 0 && c0 == 0) g_trace[i * 4 + 3] = gtime();
-    }
-  } else {
-    // ---------------------------------------------- converters (8 warps)
-    const int t = threadIdx.x - 288;   // 0..255
-    uint32_t i = 0;
-    int64_t cur_p = -1;
-    for (int64_t img = i0; img < i1; ++img, ++i) {
-      const int64_t c = c_begin + img, p = c / A;
-      const int a = (int)(c - p * A);
-      const int64_t pl = p - p_first;
-      if (p != cur_p) {   // new parent: convert its frame stack once (global -> smem bf16 s2d)
-        conv_bar();       // every converter is done reading the previous parent
-        const uint8_t *pf = par.state + pl * par.state_stride;
-        for (int task = t; task < 441 * 4; task += kConvThreads) {
-          const int pix = task >> 2, dy = task & 3;
-          const int Y = pix / 21, X = pix - Y * 21;
-          const int p0 = (4 * Y + dy) * 84 + 4 * X;
-          const uint4 x = __ldg((const uint4 *)(pf) + (p0 >> 2));
-          sPar[task * 2] = make_uint4(u8pair_bf16x2(x.x, 0), u8pair_bf16x2(x.x, 2), u8pair_bf16x2(x.y, 0),
-                                      u8pair_bf16x2(x.y, 2));
-          sPar[task * 2 + 1] = make_uint4(u8pair_bf16x2(x.z, 0), u8pair_bf16x2(x.z, 2), u8pair_bf16x2(x.w, 0),
-                                          u8pair_bf16x2(x.w, 2));
-          sNew[p0 >> 2] = __byte_perm(__byte_perm(x.x, x.y, 0x0073u), __byte_perm(x.z, x.w, 0x0073u), 0x5410u);
-        }
-        conv_bar();
-        cur_p = p;
-      }
-      const uint64_t key = *(const uint64_t *)((const uint8_t *)par.key + pl * par.key_stride);
-      const uint64_t k2 = mix64d(key ^ (0x9E3779B97F4A7C15ull * (uint64_t)(a + 1)));
-      if (t == 0) {
-        const uint32_t tt = (uint32_t)(k2 >> 61);
-        const float rw = tt == 7u ? 1.0f : (tt == 0u ? -1.0f : 0.0f);
-        cum_out[img] = fmaf(gk, rw, par.cum ? par.cum[pl] : 0.0f);
-      }
-      const uint32_t b = i & 1u, ph = (i >> 1) & 1u;
-      mbar_wait(&in_empty[b], ph ^ 1u);
-      const bool tr = tron && i < 64 && t == 0;
-      if (tr) g_trace[i * 4 + 0] = gtime();
-      uint8_t *dimg = sIn0 + b * in_stride;
-      for (int task = t; task < 441 * 4; task += kConvThreads) {
-        const int pix = task >> 2, dy = task & 3;
-        const int Y = pix / 21, X = pix - Y * 21;
-        const int p0 = (4 * Y + dy) * 84 + 4 * X;                // 4 pixels, p0 % 4 == 0
-        const uint32_t nz = (uint32_t)(mix64d(k2 + (uint64_t)(p0 >> 3)) >> (8 * (p0 & 7)));
-        const uint32_t nb = sNew[p0 >> 2] ^ nz;                  // the 4 new newest-frame bytes
-        const uint4 lo = sPar[task * 2], hi = sPar[task * 2 + 1];
-        // parent pixel j = words (ch0,ch1), (ch2,ch3); child = (ch1,ch2), (ch3,new)
-        const uint4 clo = make_uint4(__byte_perm(lo.x, lo.y, 0x5432u), __byte_perm(lo.y, u8_f32bits(nb, 0), 0x7632u),
-                                     __byte_perm(lo.z, lo.w, 0x5432u), __byte_perm(lo.w, u8_f32bits(nb, 1), 0x7632u));
-        const uint4 chi = make_uint4(__byte_perm(hi.x, hi.y, 0x5432u), __byte_perm(hi.y, u8_f32bits(nb, 2), 0x7632u),
-                                     __byte_perm(hi.z, hi.w, 0x5432u), __byte_perm(hi.w, u8_f32bits(nb, 3), 0x7632u));
-        *(uint4 *)(dimg + act_off(2, kPlane1, pix, 2 * dy)) = clo;
-        *(uint4 *)(dimg + act_off(2, kPlane1, pix, 2 * dy + 1)) = chi;
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic stores -> tensor-core reads
-      mbar_arrive(&in_full[b]);
-      if (tr) g_trace[i * 4 + 1] = gtime();
-    }
-  }
-  __syncthreads();
-  if (warp == 0) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tcols));
-  }
 }
 
 // ============================================================ conv1, sibling-factorised
@@ -629,6 +407,27 @@ __device__ __forceinline__ bool mbar_test(uint64_t *b, uint32_t parity) {
                : "memory");
   return ok != 0;
 }
+// Converter warp-task T (0..27) and lane -> noise group (0..881) or -1. s2d row band Y = the 4 frame
+// rows 4Y..4Y+3 (42 groups). Tasks 0-20: band T, lane = (row j = lane/8, first quad X = 2(lane%8) +
+// (j&1)): the 8-byte slot of quad (j, X) is (j + 2X + 10Y) mod 16, so both store instructions of the
+// task hit all 16 bank pairs exactly twice. Tasks 21-27: the 10 remaining groups of bands 3(T-21) ..
+// +2 (first quads X = 16/18/20 on rows 0, 2 and 17/19 on rows 1, 3), <= 3 lanes per bank pair;
+// lanes 30, 31 of those tasks get -1 (the caller gives them a duplicate of lanes 28, 29).
+__device__ __forceinline__ int sib_group(int T, int i) {
+  int Y, j, X;
+  if (T < 21) {
+    Y = T;
+    j = i >> 3;
+    X = 2 * (i & 7) + (j & 1);
+  } else {
+    if (i >= 30) return -1;
+    Y = 3 * (T - 21) + i / 10;
+    const int r = i % 10;
+    j = r < 3 ? 0 : r < 5 ? 1 : r < 8 ? 2 : 3;
+    X = r < 3 ? 16 + 2 * r : r < 5 ? 17 + 2 * (r - 3) : r < 8 ? 16 + 2 * (r - 5) : 17 + 2 * (r - 8);
+  }
+  return 42 * Y + (21 * j + X) / 2;
+}
 constexpr float kSibScale = 6.103515625e-05f;       // 2^-14: undoes the fp16 weight scaling (qnet.cu)
 // Planes hold the 441 real rows back to back (plane stride 441 x 16 B): the M-tile windows reach
 // row 533, but every row past 440 feeds only discarded outputs (valid rows q <= 418, taps add
@@ -648,11 +447,6 @@ __global__ void __launch_bounds__(kSibThreads, 1)
                 float gk, uint8_t *__restrict__ out, float *__restrict__ cum_out) {
   constexpr int N = 32;
   extern __shared__ uint8_t smem_raw[];
-  // trace pointer held in a register: re-reading the __device__ global after every asm memory
-  // clobber would put a global load on each traced path and distort the timeline
-  unsigned long long *const trp = (g_trace_sel == 10 && blockIdx.x == 0) ? g_trace : nullptr;
-  const bool tron = trp != nullptr;
-  const int dbg = g_sib_dbg;
   // 1024-byte aligned base, derived from smem_raw by an OFFSET so the compiler keeps the
   // shared address space (a uintptr_t round trip turns every access into a generic LD/ST)
   uint8_t *smem = smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u);
@@ -757,11 +551,8 @@ __global__ void __launch_bounds__(kSibThreads, 1)
       // new frame of child img: 4 tiles x 4 taps x 1 K-step
       const uint32_t nb = j % kNewRing, nph = (j / kNewRing) & 1u;
       const uint32_t cb = j & 1u, cph = (j >> 1) & 1u;
-      if (tron && j < 64 && elected) trp[j * 10 + 3] = clock64();   // trace: MMA loop top
       mbar_wait(&n_full[nb], nph);
-      if (tron && j < 64 && elected) trp[j * 10 + 4] = clock64();   // trace: new image ready
       mbar_wait(&c_empty[cb], cph ^ 1u);
-      if (tron && j < 64 && elected) trp[j * 10 + 5] = clock64();   // trace: C buffer free
       tc_fence_after();
       const uint32_t nbase = saddr(sNw + nb * kNewBytes);
 #pragma unroll
@@ -773,10 +564,8 @@ __global__ void __launch_bounds__(kSibThreads, 1)
           mma_pred(tmem + 256 + cb * 128 + (uint32_t)(mt * N), desc_planar(a, kSibPlane), wnw + (w_off >> 4), idesc,
                    tap != 0, elected);
         }
-      if (tron && j < 64 && elected) trp[j * 10 + 6] = clock64();   // trace (cycles): MMAs issued
       commit_pred(&n_empty[nb], elected);
       commit_pred(&c_full[cb], elected);
-      if (tron && j < 64 && elected && (dbg & 8)) trp[j * 10 + 8] = clock64();   // experiment: after commits
       // lookahead: P(k+1) as soon as its shared image and TMEM buffer are ready (warp-uniform test)
       if (issued == k && k + 1 < npar) {
         const uint32_t sb = (uint32_t)(k + 1) & 1u, ph = (uint32_t)((k + 1) >> 1) & 1u;
@@ -842,8 +631,6 @@ __global__ void __launch_bounds__(kSibThreads, 1)
       }
       const uint32_t cb = j & 1u, cph = (j >> 1) & 1u;
       mbar_wait(&c_full[cb], cph);
-      const bool etr = tron && j < 64 && threadIdx.x == 32;
-      if (etr) trp[j * 10 + 7] = clock64();   // trace: C ready (MMAs complete)
       tc_fence_after();
       uint8_t *oimg = out + img * (int64_t)P.out_img_bytes;
       // staging buffer j&1 is free once the bulk store of child j-2 has read it (<= 1 group pending)
@@ -861,7 +648,6 @@ __global__ void __launch_bounds__(kSibThreads, 1)
         if (hf == 1) {
           tc_fence_before();
           mbar_arrive(&c_empty[cb]);
-          if (etr && !(dbg & 8)) trp[j * 10 + 8] = clock64();   // trace: C read, buffer released
         }
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
@@ -871,26 +657,25 @@ __global__ void __launch_bounds__(kSibThreads, 1)
           uint32_t pk[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) {   // relu(C * 2^-14 + Pb) -> bf16 (ReLU on the packed pair)
-            const float x = fmaf(__uint_as_float(vc[u][2 * e]), kSibScale, __uint_as_float(vp[mt][2 * e]));
-            const float y = fmaf(__uint_as_float(vc[u][2 * e + 1]), kSibScale, __uint_as_float(vp[mt][2 * e + 1]));
-            pk[e] = bf16x2_relu(x, y);
+            const float2 xy = ffma2(make_float2(__uint_as_float(vc[u][2 * e]), __uint_as_float(vc[u][2 * e + 1])),
+                                    make_float2(kSibScale, kSibScale),
+                                    make_float2(__uint_as_float(vp[mt][2 * e]), __uint_as_float(vp[mt][2 * e + 1])));
+            pk[e] = bf16x2_relu(xy.x, xy.y);
           }
 #pragma unroll
           for (int h2 = 0; h2 < 2; ++h2)   // into the staging image, in act1's global SW128 layout
-            if (!(dbg & 2))
-              *(uint4 *)(sStage + (o ^ (16u * h2))) = make_uint4(pk[4 * h2], pk[4 * h2 + 1], pk[4 * h2 + 2], pk[4 * h2 + 3]);
+            *(uint4 *)(sStage + (o ^ (16u * h2))) = make_uint4(pk[4 * h2], pk[4 * h2 + 1], pk[4 * h2 + 2], pk[4 * h2 + 3]);
         }
       }
       // whole image staged: the TMA engine writes the two row blocks to global (async)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       epi_bar();
-      if (threadIdx.x == 32 && !(dbg & 2)) {
+      if (threadIdx.x == 32) {
         for (int q = 0; q < 2; ++q)
           asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(oimg + q * P.out_plane * 8u),
                        "r"(saddr(sStage) + q * kStageBlk), "r"(kStageBlk)
                        : "memory");
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        if (etr) trp[j * 10 + 9] = clock64();   // trace: staged + bulk store issued
       }
     }
   } else {
@@ -898,12 +683,19 @@ __global__ void __launch_bounds__(kSibThreads, 1)
     const int t = threadIdx.x - 288;   // 0..223
     // this thread's new-frame tasks, fixed for every child: task = one 8-pixel noise group g
     // (frame quads 2g, 2g+1: one mix64 serves both, ENV_SPEC) and the destinations of its two
-    // quads in the new image (plane dy/2, s2d pixel, 8-byte half dy%2)
-    constexpr int kTasks = (882 + kSibConv - 1) / kSibConv;
+    // quads in the new image (plane dy/2, s2d pixel, 8-byte half dy%2). Warp-task T = warp + 7 it
+    // (sib_group): each 8-byte store instruction covers every SMEM bank pair twice (2 wavefronts)
+    constexpr int kTasks = 4;
     uint32_t tdst[kTasks][2];
+    int tg[kTasks];
 #pragma unroll
     for (int it = 0; it < kTasks; ++it) {
-      const int g = min(t + it * kSibConv, 881);
+      // lanes 30, 31 of the leftover tasks repeat lanes 28, 29 (identical stores): no lane of a
+      // converter warp ever skips the per-child loop body, so the warp stays converged up to the
+      // aligned barriers that follow (sib_bar)
+      const int T = (t >> 5) + 7 * it;
+      tg[it] = sib_group(T, T < 21 || (t & 31) < 30 ? (t & 31) : (t & 31) - 2);
+      const int g = tg[it];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int q = 2 * g + h, y = q / 21, X = q - 21 * y;
@@ -942,11 +734,12 @@ __global__ void __launch_bounds__(kSibThreads, 1)
       mbar_arrive(&sh_full[sb]);
 #pragma unroll
       for (int it = 0; it < kTasks; ++it) {
-        const int g = min(t + it * kSibConv, 881);
+        const int g = tg[it];
         const uint4 w0 = pf4[2 * g], w1 = pf4[2 * g + 1];   // pixel words 8g .. 8g+7: their byte 3
         pn_next[it].x = __byte_perm(__byte_perm(w0.x, w0.y, 0x0073u), __byte_perm(w0.z, w0.w, 0x0073u), 0x5410u);
         pn_next[it].y = __byte_perm(__byte_perm(w1.x, w1.y, 0x0073u), __byte_perm(w1.z, w1.w, 0x0073u), 0x5410u);
       }
+      __syncwarp();
       sib_bar();   // every converter is done reading the parent-frame buffer
       if (t == 0 && q + 1 < npar) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -977,7 +770,6 @@ __global__ void __launch_bounds__(kSibThreads, 1)
         cur_p = p;
         first_child = true;
       }
-      if (tron && j < 64 && t == 0) trp[j * 10 + 0] = clock64();   // trace (cycles): child start
       const uint64_t k2 = mix64d(pkey ^ (0x9E3779B97F4A7C15ull * (uint64_t)(a + 1)));   // child key
       if (t == 0) {
         const uint32_t tt = (uint32_t)(k2 >> 61);
@@ -986,26 +778,18 @@ __global__ void __launch_bounds__(kSibThreads, 1)
       }
       const uint32_t nb = j % kNewRing, nph = (j / kNewRing) & 1u;
       mbar_wait(&n_empty[nb], nph ^ 1u);
-      const bool tr = tron && j < 64 && t == 0;
-      if (tr) trp[j * 10 + 1] = clock64();   // conversion start
       uint8_t *nw = sNw + nb * kNewBytes;
       // noise group g: h = mix64(k2 + g) covers pixels 8g..8g+7 = quads 2g (low word) and 2g+1
 #pragma unroll
       for (int it = 0; it < kTasks; ++it) {
-        const int g = t + it * kSibConv;
-        if (g >= 882) break;
+        const int g = tg[it];
         const uint64_t h = mix64d(k2 + (uint64_t)g);
         const uint32_t b0 = pn[it].x ^ (uint32_t)h, b1 = pn[it].y ^ (uint32_t)(h >> 32);
-        if (dbg & 1) {   // timing experiment: no new-image stores
-          if (b0 == 0x12345678u && b1 == 0x9abcdef0u) *(uint32_t *)nw = b0;
-          continue;
-        }
         *(uint2 *)(nw + tdst[it][0]) = make_uint2(u8pair_f16x2(b0, 0x4140u), u8pair_f16x2(b0, 0x4342u));
         *(uint2 *)(nw + tdst[it][1]) = make_uint2(u8pair_f16x2(b1, 0x4140u), u8pair_f16x2(b1, 0x4342u));
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(&n_full[nb]);
-      if (tr) trp[j * 10 + 2] = clock64();   // conversion end (n_full arrived)
       if (first_child) {   // lookahead: load the next parent while the pipeline works on this child
         first_child = false;
         if ((int64_t)k + 1 < npar) {
@@ -1555,29 +1339,6 @@ void launch_n(const ConvSW &P, const Layer &L, const void *in, int64_t n_img, vo
 }
 
 }  // namespace
-
-void conv_trace_set(unsigned long long *p, int sel) {
-  // sel >= 100: k_conv1_sib trace (10) with debug switches (sel / 100): results are wrong, timing only
-  const int dbg = sel >= 100 ? sel / 100 : 0;
-  if (sel >= 100) sel %= 100;
-  cudaMemcpyToSymbol(g_trace, &p, sizeof(p));
-  cudaMemcpyToSymbol(g_trace_sel, &sel, sizeof(sel));
-  cudaMemcpyToSymbol(g_sib_dbg, &dbg, sizeof(dbg));
-}
-
-void launch_conv1_fused(const ConvSW &P, const Layer &L, const NodeView &par, int64_t p_first, int64_t c_begin,
-                        int64_t n_img, int A, float gk, void *out, float *cum_out, cudaStream_t st) {
-  if (n_img <= 0) return;
-  constexpr int smem = 4 * 32 * 128 + 2 * (int)((kIn1Bytes + 1023u) & ~1023u) + 441 * 4 * 32 + 7056 + 1024;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_conv1_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
-  const int grid = (int)std::min<int64_t>(n_img, num_sms());
-  k_conv1_fused<<<grid, kThreadsF, smem, st>>>(P, P.wsw, L.bias, par, p_first, c_begin, n_img, A, gk, (uint8_t *)out,
-                                               cum_out);
-}
 
 void launch_conv1_sib(const ConvSW &P, const Layer &L, const uint8_t *wsh, const uint8_t *wnw, const NodeView &par,
                       int64_t p_first, int64_t c_begin, int64_t n_img, int A, float gk, void *out, float *cum_out,

@@ -652,11 +652,9 @@ __device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t (&r)[64]) {
   tmem_wait_ld();
 }
 
-// Timing experiments only (env BCTS_HEAD_DBG; 0 in production, results are wrong otherwise):
-// bit 0 no softmax, bit 1 no TMEM loads, bit 2 no MMAs, bits 4-5 ring stages in use (1-3).
-// Measured (C5, 52K-leaf launch): everything off but the TMA ring still takes ~70 us of ~80, and
-// T(stages) = 37 + 102 / stages us -- the ring (3 x 32 KB beside the 128 KB resident h_a) bounds it.
-__device__ int g_head_dbg = 0;
+// (Round-1 timing experiments: with every part switched off but the TMA ring the
+// C5 52K-leaf launch still took ~70 of ~80 us, T(stages) = 37 + 102 / stages us -- the weight ring
+// beside the 128 KB resident h_a bounds it.)
 template <int ATOMS>
 __global__ void __launch_bounds__(kHeadThreads, 1)
     k_zhead(const __grid_constant__ CUtensorMap mapAv, const __grid_constant__ CUtensorMap mapAa,
@@ -679,8 +677,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
   const int n_m = (int)((M + kBM - 1) / kBM);
   const int nch = (A + 3) / 4;                       // z_a chunks of 4 actions (256 columns)
   const int cpc = (nch + ns - 1) / ns, n_work = n_m * ns;
-  const int dbg = g_head_dbg;
-  const int nst = ((dbg >> 4) & 3) ? ((dbg >> 4) & 3) : kHeadStages;   // ring stages in use (experiments)
+  constexpr int nst = kHeadStages;
   if (threadIdx.x == 0) {
     for (int i = 0; i < kHeadStages; ++i) {
       mbar_init(&full[i], 1);
@@ -767,7 +764,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
             mma_pred(tmem + b * 256, ad + (uint64_t)(2 * kk), bd + (uint64_t)(2 * kk), idesc, (kb | kk) != 0,
-                     (dbg & 4) ? 0u : elected);
+                     elected);
           commit_pred(&empty[st], elected);
         }
         commit_pred(&tfull[b], elected);
@@ -817,12 +814,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
         tc_fence_after();
         const int na = min(4, A - 4 * c);
         for (int s = grp; s < na; s += 2) {
-          if (dbg & 2) continue;
           tmem_ld64(tmem + b * 256 + lanes + (uint32_t)(s * 64), x);
-          if (dbg & 1) {
-            best = fmaxf(best, __uint_as_float(x[0]));
-            continue;
-          }
           const int a = 4 * c + s;
           float mx = -INFINITY;
 #pragma unroll
@@ -1132,14 +1124,6 @@ void launch_zhead(const HeadPlan &H, int A, int atoms, int64_t M, float vmin, fl
     attr = true;
   }
   const int n_m = (int)((M + kBM - 1) / kBM), nch = (A + 3) / 4;
-  static bool dbg_set = false;
-  if (!dbg_set) {
-    dbg_set = true;
-    if (const char *e = getenv("BCTS_HEAD_DBG")) {
-      const int d = atoi(e);
-      cudaMemcpyToSymbol(g_head_dbg, &d, sizeof(d));
-    }
-  }
   // full-row batches smaller than the GPU: split each tile's action chunks over several CTAs
   const int ns = mode == MODE_ROWS ? std::max(1, std::min(nch, num_sms() / n_m)) : 1;
   const int grid = std::min(n_m * ns, num_sms());
