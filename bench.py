@@ -126,6 +126,18 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def self_launch(argv, gpus):
+    """`bench.py --gpus N` outside torchrun: re-run this script as N ranks (one process per GPU)
+    under torch.distributed.run on 127.0.0.1 and return its exit code."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *argv]
+    return subprocess.call(cmd)
+
+
 def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -257,6 +269,8 @@ def main():
     ap.add_argument("--no-flush", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(sys.argv[1:], args.gpus)
 
     from synth.inputs import config
     import dataclasses
@@ -270,24 +284,23 @@ def main():
     import numpy as np
     import torch
     import paper_2107_01715_b200 as P
-    from paper_2107_01715_b200.parallel import sharded_search
+    from paper_2107_01715_b200.parallel import world_handle
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     flags = P.F_SIMT_NET if args.simt else 0
-    h = P.Handle.from_config(cfg, tab=tab_of(cfg), device=local, flags=flags)
+    # world > 1: every rank's handle owns an NCCL communicator (id made on rank 0, broadcast); the
+    # search is then collective inside the library: each rank scores its leaf range and one
+    # ncclAllReduce(MAX) of the packed root keys runs on the handle's stream
+    h = world_handle(cfg, tab=tab_of(cfg), device=local, flags=flags)
     n, d, A, corr = cfg.n_roots, cfg.depth, cfg.A, 1
     roots_np = cfg.roots()
     roots = torch.from_numpy(roots_np.view(np.uint8).reshape(n, -1).copy()).to(dev)
     act = torch.empty(n, dtype=torch.int32, device=dev)
     q = torch.empty(n, A, dtype=torch.float32, device=dev)
-    keys = torch.empty(n * A, dtype=torch.int64, device=dev)
     launches_per_step = [0]
 
     def step():
-        if world == 1:
-            out = h.search(roots, n, d, cfg.gamma, cfg.beta, corr, out={"actions": act, "root_q": q})
-        else:
-            out = sharded_search(h, roots, n, d, cfg.gamma, cfg.beta, corr, keys=keys)
+        out = h.search(roots, n, d, cfg.gamma, cfg.beta, corr, out={"actions": act, "root_q": q})
         launches_per_step[0] = out["stats"]["kernel_launches"]
         return out
 
@@ -399,14 +412,7 @@ def main():
         torch.cuda.synchronize()
         barrier()
         t0 = time.perf_counter()
-        if world == 1:
-            h.search_host(pin_roots, n, d, cfg.gamma, cfg.beta, corr, pin_act, pin_q)
-        else:
-            droots = pin_roots.to(dev, non_blocking=True)
-            out = sharded_search(h, droots, n, d, cfg.gamma, cfg.beta, corr, keys=keys)
-            pin_act.copy_(out["actions"], non_blocking=True)
-            pin_q.copy_(out["root_q"], non_blocking=True)
-            torch.cuda.synchronize()
+        h.search_host(pin_roots, n, d, cfg.gamma, cfg.beta, corr, pin_act, pin_q)
         dt = time.perf_counter() - t0
         if i >= args.warmup:
             e2e_times.append(dt)
@@ -431,7 +437,9 @@ def main():
                 "decisions_per_s": n / (step_ms / 1e3),
                 "config": {"workload": workload_of(cfg, n),
                            "roots": n, "depth": d, "A": A, "nodes_per_decision": exp + ev,
-                           "parallelism": f"leaf-range shards x{world}" if world > 1 else "single GPU",
+                           "parallelism": (f"leaf-range shards x{world}, one NCCL max all-reduce of the "
+                                           f"{n * A} packed root keys inside the library") if world > 1
+                           else "single GPU",
                            "l2": "flushed before every timed step (256 MiB write, untimed)" if flush is not None
                            else "not flushed", "net_path": "simt" if args.simt else "tcgen05"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,

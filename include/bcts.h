@@ -45,7 +45,8 @@
 extern "C" {
 #endif
 
-#define BCTS_ABI_VERSION 4   /* 2: env_weights fields + BCTS_ENV_DNN; 3: bcts_search_pruned; 4: bcts_kernel_profile largest-launch fields */
+#define BCTS_ABI_VERSION 5   /* 2: env_weights fields + BCTS_ENV_DNN; 3: bcts_search_pruned; 4: bcts_kernel_profile largest-launch fields;
+                                5: NCCL (nccl_unique_id / rank / world, BCTS_ERR_NCCL), caller workspace, ms_* stats, flags 0x10-0x20 */
 
 typedef struct bcts_handle_t *bcts_handle;
 
@@ -56,6 +57,7 @@ typedef enum {
   BCTS_ERR_OUT_OF_MEMORY = 3, /* device allocation failed */
   BCTS_ERR_BUDGET = 4,        /* one root's per-call tree cannot fit the workspace, or A^d overflows */
   BCTS_ERR_CUDA = 5,          /* a CUDA runtime error (detail in bcts_last_error) */
+  BCTS_ERR_NCCL = 6,          /* an NCCL error, or the communicator is in an error state (detail in bcts_last_error) */
   BCTS_ERR_NUMERIC = 7        /* non-finite value met where the contract forbids it */
 } bcts_status;
 
@@ -95,6 +97,10 @@ typedef enum {
 #define BCTS_F_SEPARATE_BACKUP 0x8u /* run the segmented-max backup (Alg. 1) as its own kernel
                                      * instead of inside the Rainbow head's epilogue; same result bit
                                      * for bit (the max over packed keys is order-independent) */
+#define BCTS_F_NO_PROLOGUE_FOLD 0x10u /* evaluate the depth-0/1 rows of the BCTS terms (Prop. 1) in their
+                                       * own net launches instead of inside the last leaf batch; same
+                                       * result bit for bit */
+#define BCTS_F_NO_GRAPH 0x20u        /* never replay CUDA graphs (bcts_search_host, bcts_search_ex) */
 
 typedef struct {
   uint32_t abi_version;     /* must be BCTS_ABI_VERSION */
@@ -123,6 +129,15 @@ typedef struct {
    * those sizes); ignored for the other envs. */
   const float *env_weights;
   int64_t env_weights_count;
+  /* Multi-GPU (one process per GPU). world > 1: bcts_create is COLLECTIVE --
+   * every rank 0..world-1 calls it with the same 128-byte id from bcts_nccl_unique_id (made on one
+   * rank, shared by the caller, e.g. torch.distributed.broadcast) and its own rank; the handle owns
+   * an NCCL communicator on `device` and its searches are collective. world == 1 with a non-NULL id:
+   * a one-rank communicator (the collective path on one GPU, e.g. for tests). world <= 1 with a
+   * NULL id: no NCCL at all. INVALID_ARG if rank is outside [0, max(world, 1)) or world > 1 with a
+   * NULL id; NCCL if the communicator cannot be created. */
+  const void *nccl_unique_id;  /* HOST, 128 bytes (copied at create) */
+  int32_t rank, world;
 } bcts_config;
 
 typedef struct {
@@ -132,12 +147,44 @@ typedef struct {
   int64_t kernel_launches; /* kernels this call launched */
   int64_t chunks;          /* leaf chunks the call was split into */
   int64_t level_launches;  /* expansion-kernel launches */
+  /* Device time of the call by phase, in ms (CUDA events on the handle's stream). Filled only while
+   * profiling is on (bcts_profile_enable(h, 1)): the call then synchronizes its stream before it
+   * returns. 0 otherwise (calls stay asynchronous). expand = level expansion (Alg. 1),
+   * leaf = the value net (incl. the depth-0/1 rows), backup = segmented max + BCTS
+   * correction (Eq. 3/5), comm = the NCCL all-reduce (world > 1), total = the whole call. */
+  float ms_total, ms_expand, ms_leaf, ms_backup, ms_comm;
 } bcts_stats;
 
 /* Create a handle: validates cfg, copies tables, repacks weights into the
- * device layouts, creates the stream. Errors: INVALID_ARG (bad kinds, A<2,
- * A>64, wrong weights_count, null required pointers), CUDA, OUT_OF_MEMORY. */
+ * device layouts. Device scratch is NOT allocated here: the first call that
+ * needs it allocates it (library-owned), unless bcts_set_workspace gave the
+ * handle caller-owned memory first. Errors: INVALID_ARG (bad kinds, A<2,
+ * A>64, wrong weights_count, null required pointers, rank/world), CUDA,
+ * OUT_OF_MEMORY, NCCL (world > 1). */
 bcts_status bcts_create(const bcts_config *cfg, bcts_handle *out);
+
+/* 128-byte NCCL unique id for the multi-GPU handles of one job (host memory, caller-owned);
+ * call on ONE rank and give the same bytes to every rank's bcts_create. Needs no GPU.
+ * Errors: INVALID_ARG (NULL), NCCL (libnccl.so.2 not loadable, or ncclGetUniqueId failed). */
+bcts_status bcts_nccl_unique_id(void *out128);
+
+/* Device memory a bcts_search / bcts_search_ex / bcts_search_host call over n_roots roots at
+ * `depth` needs on this handle: the value net's scratch (conv nets: fixed, ~4-5 GB for the
+ * 6-wave leaf batches) + the tree workspace (level buffers, leaf totals, packed keys, the
+ * folded prologue; capped by workspace_bytes_max through chunking). *bytes is written.
+ * Errors: INVALID_ARG (NULL, n_roots < 0, depth outside [0, 12]), BUDGET (one chunk does not
+ * fit workspace_bytes_max). Host-only; enqueues nothing. */
+bcts_status bcts_workspace_size(bcts_handle h, int64_t n_roots, int32_t depth, size_t *bytes);
+
+/* Give the handle caller-owned device memory (e.g. a torch uint8 tensor on the handle's device):
+ * [dev_ptr, dev_ptr + bytes), 256-byte aligned. From now on the handle allocates no scratch or
+ * tree workspace of its own (it frees what it had); a later call that needs more than `bytes`
+ * fails with BUDGET (nothing enqueued) -- size it with bcts_workspace_size. dev_ptr == NULL
+ * returns to library-owned memory. The caller keeps the memory alive and untouched while the
+ * handle may use it (until bcts_destroy or the next bcts_set_workspace), and must not pass it
+ * to two handles whose calls can overlap. Synchronizes the handle's stream first.
+ * Errors: INVALID_ARG (misaligned, or bytes smaller than the net scratch), CUDA. */
+bcts_status bcts_set_workspace(bcts_handle h, void *dev_ptr, size_t bytes);
 
 /* NULL-safe. Frees device memory owned by the handle. */
 void bcts_destroy(bcts_handle h);
@@ -166,7 +213,15 @@ bcts_status bcts_search(bcts_handle h, const void *roots, int64_t n_roots, int32
  *   vanilla_q_out  float [n*A]  uncorrected d-step Q (Eq. 1)
  *   terms_out      float [n*4]  (pi_o, delta_o, delta_e, B) (zeros when not computed)
  *   best_leaf_out  int64 [n*A]  lowest leaf index (within the root) attaining vanilla_q
- *   stats          HOST bcts_stats* */
+ *   stats          HOST bcts_stats*
+ * Multi-GPU handles (world > 1): the call is COLLECTIVE -- every rank passes identical arguments
+ * and the full roots; rank r scores the leaf range bcts_shard_range(n, d, A, r, world), one
+ * ncclAllReduce(ncclInt64, ncclMax) of the n*A packed keys runs on the handle's stream, and every
+ * rank applies the identical correction: all ranks return the same outputs, bit for bit equal to
+ * the single-GPU search.
+ * CUDA graphs: unless BCTS_F_NO_GRAPH or profiling is on, a call whose arguments (pointers
+ * included) equal the previous call's replays a graph of that call's launches captured after it
+ * ran eagerly (one launch instead of ~10-20); the buffers' CURRENT contents are used. */
 bcts_status bcts_search_ex(bcts_handle h, const void *roots, int64_t n_roots, int32_t depth, int32_t A,
                            float gamma, float beta, int32_t correction_on, int32_t *actions_out,
                            float *root_q_out, float *vanilla_q_out, float *terms_out,
@@ -179,7 +234,7 @@ bcts_status bcts_search_ex(bcts_handle h, const void *roots, int64_t n_roots, in
  * after an eager one with the same pointers and arguments replays a CUDA graph
  * of the whole sequence (captured on a private stream, launched on the
  * handle's); the buffers' CURRENT contents are copied in on every call.
- * BCTS_NO_GRAPH=1 in the environment disables the graph. */
+ * BCTS_F_NO_GRAPH disables the graph. Collective when world > 1. */
 bcts_status bcts_search_host(bcts_handle h, const void *roots_host, int64_t n_roots, int32_t depth,
                              int32_t A, float gamma, float beta, int32_t correction_on,
                              int32_t *actions_host, float *root_q_host);

@@ -16,10 +16,11 @@ LIB_PATH = os.path.join(_HERE, "libbcts.so")
 ENV_TABULAR, ENV_INT_HASH, ENV_ATARI_HASH, ENV_DNN = 1, 2, 3, 4
 NET_TABLE, NET_MLP2_F32, NET_NATURE_BF16, NET_RAINBOW_BF16 = 1, 2, 3, 4
 F_CLAMP_PENALTY, F_SIMT_NET, F_MATERIALIZE_LEAVES, F_SEPARATE_BACKUP = 0x1, 0x2, 0x4, 0x8
-ABI_VERSION = 4
+F_NO_PROLOGUE_FOLD, F_NO_GRAPH = 0x10, 0x20
+ABI_VERSION = 5
 PRUNE_NONE, PRUNE_BOUND, PRUNE_BEAM = 0, 1, 2
 STATUS = {0: "BCTS_OK", 1: "BCTS_ERR_INVALID_ARG", 2: "BCTS_ERR_UNSUPPORTED", 3: "BCTS_ERR_OUT_OF_MEMORY",
-          4: "BCTS_ERR_BUDGET", 5: "BCTS_ERR_CUDA", 7: "BCTS_ERR_NUMERIC"}
+          4: "BCTS_ERR_BUDGET", 5: "BCTS_ERR_CUDA", 6: "BCTS_ERR_NCCL", 7: "BCTS_ERR_NUMERIC"}
 RECORD_BYTES = {ENV_TABULAR: 4, ENV_INT_HASH: 64, ENV_ATARI_HASH: 28240, ENV_DNN: 400}
 
 # every symbol include/bcts.h declares (checked by tests/test_abi.py)
@@ -27,7 +28,8 @@ EXPORTS = ["bcts_create", "bcts_destroy", "bcts_abi_version", "bcts_root_record_
            "bcts_last_error", "bcts_search", "bcts_search_ex", "bcts_search_host", "bcts_keys_init",
            "bcts_search_shard", "bcts_finalize", "bcts_expand", "bcts_q_rows", "bcts_pack_key",
            "bcts_key_value", "bcts_key_leaf", "bcts_shard_range", "bcts_profile_enable", "bcts_profile_read",
-           "bcts_pv_targets", "bcts_search_pruned"]
+           "bcts_pv_targets", "bcts_search_pruned", "bcts_nccl_unique_id", "bcts_workspace_size",
+           "bcts_set_workspace"]
 
 
 class BctsError(RuntimeError):
@@ -43,7 +45,8 @@ class Config(C.Structure):
                 ("net", C.c_int32), ("weights", C.c_void_p), ("weights_count", C.c_int64),
                 ("mlp_in", C.c_int32), ("mlp_hidden", C.c_int32), ("atoms", C.c_int32),
                 ("v_min", C.c_float), ("v_max", C.c_float), ("workspace_bytes_max", C.c_int64),
-                ("flags", C.c_uint32), ("env_weights", C.c_void_p), ("env_weights_count", C.c_int64)]
+                ("flags", C.c_uint32), ("env_weights", C.c_void_p), ("env_weights_count", C.c_int64),
+                ("nccl_unique_id", C.c_void_p), ("rank", C.c_int32), ("world", C.c_int32)]
 
 
 class KernelProfile(C.Structure):
@@ -58,7 +61,9 @@ class Prune(C.Structure):
 
 class Stats(C.Structure):
     _fields_ = [("transitions", C.c_int64), ("leaves", C.c_int64), ("evaluated", C.c_int64),
-                ("kernel_launches", C.c_int64), ("chunks", C.c_int64), ("level_launches", C.c_int64)]
+                ("kernel_launches", C.c_int64), ("chunks", C.c_int64), ("level_launches", C.c_int64),
+                ("ms_total", C.c_float), ("ms_expand", C.c_float), ("ms_leaf", C.c_float), ("ms_backup", C.c_float),
+                ("ms_comm", C.c_float)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -99,6 +104,9 @@ def lib():
             "bcts_pv_targets": ([P, I64, I32, P, P, P, P, P], I32),
             "bcts_search_pruned": ([P, P, I64, I32, I32, F, F, I32, C.POINTER(Prune), P, P, P, P, P, P,
                                     C.POINTER(Stats)], I32),
+            "bcts_nccl_unique_id": ([P], I32),
+            "bcts_workspace_size": ([P, I64, I32, C.POINTER(C.c_size_t)], I32),
+            "bcts_set_workspace": ([P, P, C.c_size_t], I32),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -131,6 +139,16 @@ def key_leaf(key: int) -> int:
     return lib().bcts_key_leaf(int(key))
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (bcts_nccl_unique_id; needs no GPU). Make it on one rank and give the
+    same bytes to every rank's Handle(..., nccl_id=..., rank=r, world=W)."""
+    buf = C.create_string_buffer(128)
+    s = lib().bcts_nccl_unique_id(buf)
+    if s:
+        raise BctsError(s, "bcts_nccl_unique_id")
+    return buf.raw
+
+
 def shard_range(n_roots: int, depth: int, A: int, rank: int, world: int) -> tuple[int, int]:
     b, e = C.c_int64(), C.c_int64()
     s = lib().bcts_shard_range(n_roots, depth, A, rank, world, C.byref(b), C.byref(e))
@@ -144,7 +162,8 @@ class Handle:
 
     def __init__(self, env: int, A: int, net: int, *, weights=None, tab=None, device: int = 0, stream=None,
                  mlp_in: int = 64, mlp_hidden: int = 256, atoms: int = 51, v_min: float = -10.0,
-                 v_max: float = 10.0, workspace_bytes_max: int = 0, flags: int = 0, env_weights=None):
+                 v_max: float = 10.0, workspace_bytes_max: int = 0, flags: int = 0, env_weights=None,
+                 nccl_id: bytes | None = None, rank: int = 0, world: int = 1):
         import torch
         self.env, self.A, self.net, self.device = env, A, net, device
         if stream is None:
@@ -175,6 +194,13 @@ class Handle:
         cfg.v_min, cfg.v_max = v_min, v_max
         cfg.workspace_bytes_max = workspace_bytes_max
         cfg.flags = flags
+        if nccl_id is not None:   # collective create: every rank passes the same id (bcts_nccl_unique_id)
+            idbuf = C.create_string_buffer(bytes(nccl_id), 128)
+            keep.append(idbuf)
+            cfg.nccl_unique_id = C.cast(idbuf, C.c_void_p).value
+        cfg.rank, cfg.world = rank, world
+        self.rank, self.world = rank, world
+        self._ws = None
         h = C.c_void_p()
         s = lib().bcts_create(C.byref(cfg), C.byref(h))
         if s:
@@ -306,6 +332,19 @@ class Handle:
         self._check(lib().bcts_pv_targets(self._h, n, depth, _p(actions), _p(vanilla_q), _p(best_leaf), _p(target),
                                           _p(path)), "bcts_pv_targets")
         return target, path
+
+    def workspace_size(self, n_roots: int, depth: int) -> int:
+        """Device bytes a search of n_roots roots at `depth` needs (net scratch + tree workspace)."""
+        b = C.c_size_t()
+        self._check(lib().bcts_workspace_size(self._h, n_roots, depth, C.byref(b)), "bcts_workspace_size")
+        return b.value
+
+    def set_workspace(self, buf):
+        """Caller-owned device memory (a torch uint8 tensor on this device, or None to return to
+        library-owned memory); the handle keeps a reference while it may use it."""
+        self._check(lib().bcts_set_workspace(self._h, _p(buf), 0 if buf is None else buf.numel() * buf.element_size()),
+                    "bcts_set_workspace")
+        self._ws = buf
 
     def q_rows(self, states, n):
         import torch

@@ -56,7 +56,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed")
     tmp = LIB + ".tmp"
     subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs,
-                    "-lcuda"], check=True)
+                    "-lcuda", "-ldl"], check=True)
     os.replace(tmp, LIB)
     return LIB
 

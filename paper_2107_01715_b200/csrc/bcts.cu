@@ -5,8 +5,11 @@
 #include <string.h>
 
 #include <algorithm>
+#include <mutex>
 #include <new>
+#include <set>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "engine.h"
@@ -25,8 +28,15 @@ struct bcts_handle_t {
   float *d_rew = nullptr;
   Net net;
   int64_t ws_max = 0;
-  uint8_t *ws = nullptr;
+  uint8_t *ws = nullptr;      // tree workspace (library-owned, or inside the caller's memory)
   size_t ws_size = 0;
+  bool ws_own = true;
+  uint8_t *scratch_own = nullptr;   // library-owned net scratch (when no caller memory)
+  uint8_t *ext = nullptr;           // caller-owned memory (bcts_set_workspace): [net scratch | tree ws]
+  size_t ext_bytes = 0;
+  // multi-GPU: the handle's NCCL communicator (world > 1)
+  void *comm = nullptr;
+  int rank = 0, world = 1;
   // end-to-end (host buffer) staging
   uint8_t *e2e_roots = nullptr;
   size_t e2e_roots_size = 0;
@@ -53,17 +63,65 @@ struct bcts_handle_t {
     int64_t n = 0;
     int32_t d = 0, A = 0, corr = 0;
     float gamma = 0.f, beta = 0.f;
-    uint8_t *ws = nullptr;
+    uint8_t *ws = nullptr, *scratch = nullptr;
     size_t wss = 0;
+    const void *dr = nullptr, *da = nullptr, *dq = nullptr;   // the device staging buffers the graph uses
     bool operator==(const GraphKey &o) const {
       return rh == o.rh && ah == o.ah && qh == o.qh && n == o.n && d == o.d && A == o.A && corr == o.corr &&
-             gamma == o.gamma && beta == o.beta && ws == o.ws && wss == o.wss;
+             gamma == o.gamma && beta == o.beta && ws == o.ws && wss == o.wss && scratch == o.scratch &&
+             dr == o.dr && da == o.da && dq == o.dq;
     }
   } gkey;
   cudaGraphExec_t gexec = nullptr;
   bool gvalid = false;
   cudaStream_t gst = nullptr;
+  // bcts_search_ex (device pointers) replays a graph of its last call's launches
+  struct DevKey {
+    const void *roots = nullptr;
+    void *o[5] = {};
+    int64_t n = 0;
+    int32_t d = 0, A = 0, corr = 0;
+    float gamma = 0.f, beta = 0.f;
+    uint8_t *ws = nullptr, *scratch = nullptr;
+    size_t wss = 0;
+    bool operator==(const DevKey &k) const {
+      for (int i = 0; i < 5; ++i)
+        if (o[i] != k.o[i]) return false;
+      return roots == k.roots && n == k.n && d == k.d && A == k.A && corr == k.corr && gamma == k.gamma &&
+             beta == k.beta && ws == k.ws && scratch == k.scratch && wss == k.wss;
+    }
+  } dkey;
+  cudaGraphExec_t dexec = nullptr;
+  bool dvalid = false;
+  bcts_stats dstats = {};
+  bool capturing = false;   // inside a capture of ours: no nested graph logic
 };
+
+namespace bcts {
+int sm_count_current() {
+  static int cache[64] = {};   // per device ordinal (a benign race: every writer stores the same value)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  int n = __atomic_load_n(&cache[dev], __ATOMIC_RELAXED);
+  if (!n) {
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    __atomic_store_n(&cache[dev], n, __ATOMIC_RELAXED);
+  }
+  return n;
+}
+cudaError_t smem_optin(const void *kernel, int bytes) {
+  static std::mutex mu;
+  static std::set<std::tuple<const void *, int, int>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count(std::make_tuple(kernel, dev, bytes))) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.insert(std::make_tuple(kernel, dev, bytes));
+  return e;
+}
+}  // namespace bcts
 
 namespace {
 
@@ -160,6 +218,10 @@ bcts_status cuda_check(bcts_handle h, const char *where) {
 
 bcts_status ensure_ws(bcts_handle h, size_t bytes) {
   if (bytes <= h->ws_size) return BCTS_OK;
+  if (!h->ws_own)
+    return fail(h, BCTS_ERR_BUDGET, "caller workspace too small: the tree workspace needs " + std::to_string(bytes) +
+                                        " bytes, " + std::to_string(h->ws_size) + " available (bcts_workspace_size)");
+  h->dvalid = h->gvalid = false;   // graphs bake the workspace address in
   if (h->ws) {
     cudaStreamSynchronize(h->st);
     cudaFree(h->ws);
@@ -171,6 +233,25 @@ bcts_status ensure_ws(bcts_handle h, size_t bytes) {
     return fail(h, BCTS_ERR_OUT_OF_MEMORY, "workspace cudaMalloc of " + std::to_string(bytes) + " bytes failed");
   }
   h->ws_size = bytes;
+  return BCTS_OK;
+}
+
+// The value net's scratch, bound on first use: inside the caller's memory (bcts_set_workspace) or
+// one library allocation.
+bcts_status ensure_net(bcts_handle h) {
+  if (h->net.scratch || !net_scratch_bytes(h->net)) return BCTS_OK;
+  std::string err;
+  uint8_t *base = h->ext;
+  if (!base) {
+    if (cudaMalloc(&h->scratch_own, net_scratch_bytes(h->net)) != cudaSuccess) {
+      cudaGetLastError();
+      h->scratch_own = nullptr;
+      return fail(h, BCTS_ERR_OUT_OF_MEMORY, "net scratch cudaMalloc of " + std::to_string(net_scratch_bytes(h->net)) +
+                                                 " bytes failed");
+    }
+    base = h->scratch_own;
+  }
+  if (net_bind_scratch(h->net, base, err)) return fail(h, BCTS_ERR_CUDA, err);
   return BCTS_OK;
 }
 
@@ -419,7 +500,7 @@ struct Outs {
 // body) -- the rows are produced later inside a leaf batch.
 bool fold_wanted(bcts_handle h, int64_t n, int32_t d) {
   return d >= 1 && fused_leaves(h) && h->net.kind == BCTS_NET_RAINBOW_BF16 && n * (h->A + 1) <= (int64_t)4096 &&
-         !getenv("BCTS_NO_PROLOGUE_FOLD");
+         !(h->flags & BCTS_F_NO_PROLOGUE_FOLD);
 }
 size_t fold_bytes(bcts_handle h, int64_t n) {
   Carver pc(nullptr);
@@ -652,6 +733,97 @@ bcts_status run_pruned(bcts_handle h, const void *roots, int64_t n, int32_t d, f
   return BCTS_OK;
 }
 
+// ------------------------------------------------------------ one search call
+// Workspace plan of a bcts_search_ex call: [keys | folded-prologue region | phase space], the leaf
+// range of this rank ([0, n A^d) on one GPU, bcts_shard_range's on rank r of a multi-GPU handle).
+struct SearchPlan {
+  int64_t lpr = 1, L0 = 0, L1 = 0;
+  size_t kbytes0 = 0, pbytes = 0, kbytes = 0, total = 0;
+  bool fold = false;
+};
+bcts_status plan_search(bcts_handle h, int64_t n, int32_t d, int32_t corr, SearchPlan &pl) {
+  ipow_ok(h->A, d, pl.lpr);
+  pl.L0 = 0;
+  pl.L1 = d >= 1 ? n * pl.lpr : 0;
+  if (h->world > 1 && d >= 1) bcts_shard_range(n, d, h->A, h->rank, h->world, &pl.L0, &pl.L1);
+  pl.kbytes0 = align_up((size_t)n * h->A * 8);
+  // with the level-1 terms needed and a conv net generating the leaves, the prologue's states
+  // [roots | level-1 children] are expanded up front into a region after the keys and evaluated
+  // inside this rank's last leaf batch (PrologueFold; finalize then only reads their rows)
+  pl.fold = corr && fold_wanted(h, n, d) && pl.L1 > pl.L0;
+  pl.pbytes = pl.fold ? fold_bytes(h, n) : 0;
+  pl.kbytes = pl.kbytes0 + pl.pbytes;
+  size_t need = finalize_ws(h, n, pl.kbytes);
+  if (pl.L1 > pl.L0) {
+    const size_t sw = shard_ws(h, pl.L1 - pl.L0, pl.kbytes);
+    if (!sw) return fail(h, BCTS_ERR_BUDGET, "workspace budget too small for one chunk of leaves");
+    need = std::max(need, sw);
+  }
+  pl.total = pl.kbytes + need;
+  return BCTS_OK;
+}
+
+// Enqueue one whole search on h->st (validated arguments, sized workspace): expansion + leaf net +
+// backup over this rank's leaf range, the max all-reduce of the keys on a multi-GPU handle, then
+// the BCTS terms and correction (identical on every rank).
+bcts_status search_body(bcts_handle h, const void *roots, int64_t n, int32_t d, float gamma, float beta, int32_t corr,
+                        const Outs &o, const SearchPlan &pl, bcts_stats *stats) {
+  bcts_status s = BCTS_OK;
+  int64_t *keys = (int64_t *)h->ws;
+  PrologueFold pf;
+  if (pl.fold) pf = fold_front(h, roots, n, gamma, h->ws + pl.kbytes0);
+  if (d >= 1) {
+    launch_keys_init(keys, n * h->A, h->st);
+    h->launches += 1;
+    s = run_shard(h, roots, d, gamma, pl.L0, pl.L1, keys, pl.kbytes, stats, pl.fold ? &pf : nullptr);
+    if (s) return s;
+    if (h->comm) {   // the one exchange: MAX over the ranks' packed (value, ~leaf) keys
+      std::string err;
+      h->prof.begin(KC_COMM, 8.0 * (double)n * h->A, h->st);
+      const bool ok = comm_allreduce_max_i64(h->comm, keys, n * h->A, h->st, err);
+      h->prof.end(h->st);
+      if (!ok) return fail(h, BCTS_ERR_NCCL, err);
+    }
+  }
+  return finalize_impl(h, roots, n, d, gamma, beta, corr, keys, o, pl.kbytes, stats, pl.fold ? &pf : nullptr);
+}
+
+// bcts_stats.ms_*: per-phase device time of one call while profiling is on (synchronizes)
+struct PhaseTimer {
+  bcts_handle h;
+  bool on;
+  cudaEvent_t a = nullptr, b = nullptr;
+  double before[KC_COUNT] = {};
+  PhaseTimer(bcts_handle hh, bcts_stats *stats) : h(hh), on(stats && hh->prof.on) {
+    if (!on) return;
+    cudaStreamSynchronize(h->st);
+    h->prof.collect();
+    for (int c = 0; c < KC_COUNT; ++c) before[c] = h->prof.ms[c];
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, h->st);
+  }
+  void finish(bcts_stats *st) {
+    if (!on) return;
+    cudaEventRecord(b, h->st);
+    cudaStreamSynchronize(h->st);
+    h->prof.collect();
+    float t = 0.f;
+    cudaEventElapsedTime(&t, a, b);
+    st->ms_total = t;
+    auto d = [&](int c) { return (float)(h->prof.ms[c] - before[c]); };
+    st->ms_expand = d(KC_EXPAND_ATARI) + d(KC_EXPAND_INT) + d(KC_EXPAND_TAB) + d(KC_EXPAND_DNN);
+    st->ms_leaf = d(KC_CONV1) + d(KC_CONV2) + d(KC_CONV3) + d(KC_CONV23) + d(KC_FC_H) + d(KC_FC_OUT) + d(KC_HEAD) +
+                  d(KC_MLP) + d(KC_TABLE) + d(KC_OTHER);
+    st->ms_backup = d(KC_SEGMAX) + d(KC_FINALIZE) + d(KC_PRUNE);
+    st->ms_comm = d(KC_COMM);
+  }
+  ~PhaseTimer() {
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+  }
+};
+
 }  // namespace
 
 // =================================================================== C ABI
@@ -667,6 +839,7 @@ const char *bcts_status_string(bcts_status s) {
     case BCTS_ERR_OUT_OF_MEMORY: return "BCTS_ERR_OUT_OF_MEMORY";
     case BCTS_ERR_BUDGET: return "BCTS_ERR_BUDGET";
     case BCTS_ERR_CUDA: return "BCTS_ERR_CUDA";
+    case BCTS_ERR_NCCL: return "BCTS_ERR_NCCL";
     case BCTS_ERR_NUMERIC: return "BCTS_ERR_NUMERIC";
   }
   return "BCTS_ERR_UNKNOWN";
@@ -680,14 +853,17 @@ void bcts_destroy(bcts_handle h) {
   if (!h) return;
   cudaSetDevice(h->dev);
   if (h->st) cudaStreamSynchronize(h->st);
+  comm_destroy(h->comm);
   net_free(h->net);
   cudaFree(h->pbuf);
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
+  if (h->dexec) cudaGraphExecDestroy(h->dexec);
   if (h->gst) cudaStreamDestroy(h->gst);
   cudaFree(h->d_next);
   cudaFree(h->d_envw);
   cudaFree(h->d_rew);
-  cudaFree(h->ws);
+  if (h->ws_own) cudaFree(h->ws);
+  cudaFree(h->scratch_own);
   cudaFree(h->e2e_roots);
   cudaFree(h->e2e_act);
   cudaFree(h->e2e_q);
@@ -717,6 +893,8 @@ bcts_status bcts_create(const bcts_config *cfg, bcts_handle *out) {
   if (cfg->env == BCTS_ENV_DNN &&
       (!cfg->env_weights || cfg->env_weights_count != dnn_env_weights_count(cfg->num_actions)))
     return BCTS_ERR_INVALID_ARG;
+  if (cfg->world > 1 && !cfg->nccl_unique_id) return BCTS_ERR_INVALID_ARG;
+  if (cfg->rank < 0 || cfg->rank >= std::max(cfg->world, 1)) return BCTS_ERR_INVALID_ARG;
   bcts_handle h = new (std::nothrow) bcts_handle_t();
   if (!h) return BCTS_ERR_OUT_OF_MEMORY;
   h->dev = cfg->device;
@@ -757,14 +935,24 @@ bcts_status bcts_create(const bcts_config *cfg, bcts_handle *out) {
     h->em.dnn = h->d_envw;
   }
   std::string err;
-  if (net_build(h->net, *cfg, err)) {
-    cudaGetLastError();
+  if (net_build(h->net, *cfg, err)) {   // weight validation and repacking (no scratch yet)
+    const bool cuda = cudaGetLastError() != cudaSuccess || err.find("cuda") != std::string::npos ||
+                      err.find("upload") != std::string::npos;
     bcts_destroy(h);
-    return BCTS_ERR_INVALID_ARG;
+    return cuda ? BCTS_ERR_CUDA : BCTS_ERR_INVALID_ARG;
   }
   h->net.tc = !(cfg->flags & BCTS_F_SIMT_NET);
   h->net.sw = true;
   h->net.prof = &h->prof;
+  if (cfg->world > 1 || cfg->nccl_unique_id) {   // collective: every rank creates its handle with the same id
+    h->rank = cfg->rank;
+    h->world = std::max(cfg->world, 1);
+    if (!comm_init(&h->comm, cfg->nccl_unique_id, cfg->rank, cfg->world, err)) {
+      h->comm = nullptr;
+      bcts_destroy(h);
+      return BCTS_ERR_NCCL;
+    }
+  }
   *out = h;
   return BCTS_OK;
 }
@@ -791,6 +979,7 @@ bcts_status bcts_search_shard(bcts_handle h, const void *roots, int64_t n_roots,
   cudaSetDevice(h->dev);
   if (stats) memset(stats, 0, sizeof(*stats));
   const int64_t l0 = h->launches;
+  if ((s = ensure_net(h))) return s;
   if (leaf_end > leaf_begin) {
     const size_t need = shard_ws(h, leaf_end - leaf_begin, 0);
     if (!need) return fail(h, BCTS_ERR_BUDGET, "workspace budget too small for one chunk of leaves");
@@ -839,6 +1028,7 @@ bcts_status bcts_finalize(bcts_handle h, const void *roots, int64_t n_roots, int
   cudaSetDevice(h->dev);
   const int64_t l0 = h->launches;
   Outs o{actions_out, root_q_out, vanilla_q_out, terms_out, best_leaf_out};
+  if ((s = ensure_net(h))) return s;
   if ((s = ensure_ws(h, finalize_ws(h, n_roots, 0)))) return s;
   const bool pre = h->pfs_valid && h->pfs_roots == roots && h->pfs_n == n_roots && h->pfs_d == depth &&
                    h->pfs_gamma == gamma;
@@ -860,38 +1050,112 @@ bcts_status bcts_search_ex(bcts_handle h, const void *roots, int64_t n_roots, in
   if (n_roots == 0) return BCTS_OK;
   cudaSetDevice(h->dev);
   const int64_t l0 = h->launches;
-  int64_t lpr;
-  ipow_ok(A, depth, lpr);
-  // keys live at the front of the workspace; the shard and finalize phases
-  // reuse the space after them (stream-ordered). Size everything up front.
-  const size_t kbytes0 = align_up((size_t)n_roots * A * 8);
-  // With the level-1 terms needed and a conv net generating the leaves, the prologue's states
-  // [roots | level-1 children] are expanded up front into a region after the keys and evaluated
-  // inside a leaf batch (PrologueFold; finalize then only reads their rows).
-  const bool try_fold = correction_on && fold_wanted(h, n_roots, depth);
-  const size_t pbytes = try_fold ? fold_bytes(h, n_roots) : 0;
-  const size_t kbytes = kbytes0 + pbytes;
-  size_t need = finalize_ws(h, n_roots, kbytes);
-  if (depth >= 1) {
-    const size_t sw = shard_ws(h, n_roots * lpr, kbytes);
-    if (!sw) return fail(h, BCTS_ERR_BUDGET, "workspace budget too small for one chunk of leaves");
-    need = std::max(need, sw);
+  SearchPlan pl;
+  if ((s = plan_search(h, n_roots, depth, correction_on, pl))) return s;
+  if ((s = ensure_net(h))) return s;
+  if ((s = ensure_ws(h, pl.total))) return s;
+  const Outs o{actions_out, root_q_out, vanilla_q_out, terms_out, best_leaf_out};
+  // graph replay of an identical previous call (device pointers and workspace included)
+  const bool graphable = !(h->flags & BCTS_F_NO_GRAPH) && !h->prof.on && !h->capturing && h->env != BCTS_ENV_TABULAR;
+  bcts_handle_t::DevKey key;
+  key.roots = roots, key.n = n_roots, key.d = depth, key.A = A, key.corr = correction_on;
+  key.gamma = gamma, key.beta = beta, key.ws = h->ws, key.wss = h->ws_size, key.scratch = h->net.scratch;
+  key.o[0] = actions_out, key.o[1] = root_q_out, key.o[2] = vanilla_q_out, key.o[3] = terms_out, key.o[4] = best_leaf_out;
+  if (graphable && h->dvalid && key == h->dkey) {
+    if (cudaGraphLaunch(h->dexec, h->st) == cudaSuccess) {
+      if (stats) *stats = h->dstats;
+      return cuda_check(h, "graph replay");
+    }
+    cudaGetLastError();
+    h->dvalid = false;
   }
-  if ((s = ensure_ws(h, kbytes + need))) return s;
-  int64_t *keys = (int64_t *)h->ws;
-  PrologueFold pf;
-  if (try_fold) pf = fold_front(h, roots, n_roots, gamma, h->ws + kbytes0);
-  if (depth >= 1) {
-    launch_keys_init(keys, n_roots * A, h->st);
-    h->launches += 1;
-    s = run_shard(h, roots, depth, gamma, 0, n_roots * lpr, keys, kbytes, stats, try_fold ? &pf : nullptr);
+  PhaseTimer pt(h, stats);
+  bcts_stats st_local;
+  memset(&st_local, 0, sizeof(st_local));
+  s = search_body(h, roots, n_roots, depth, gamma, beta, correction_on, o, pl, &st_local);
+  if (s) return s;
+  st_local.kernel_launches = h->launches - l0;
+  pt.finish(&st_local);
+  if (stats) *stats = st_local;
+  // the same arguments twice in a row: capture this sequence for the calls that follow
+  if (graphable && !h->dvalid && key == h->dkey) {
+    if (!h->gst) cudaStreamCreateWithFlags(&h->gst, cudaStreamNonBlocking);
+    cudaStream_t saved = h->st;
+    cudaGraph_t g = nullptr;
+    bool ok = h->gst && cudaStreamBeginCapture(h->gst, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    if (ok) {
+      h->st = h->gst;
+      h->capturing = true;
+      bcts_stats scratch_stats;
+      memset(&scratch_stats, 0, sizeof(scratch_stats));
+      const bcts_status sc = search_body(h, roots, n_roots, depth, gamma, beta, correction_on, o, pl, &scratch_stats);
+      h->capturing = false;
+      h->st = saved;
+      ok = cudaStreamEndCapture(h->gst, &g) == cudaSuccess && sc == BCTS_OK && g;
+    }
+    h->err.clear();
+    cudaGraphExec_t ex = nullptr;
+    if (ok && cudaGraphInstantiate(&ex, g, 0) == cudaSuccess) {
+      if (h->dexec) cudaGraphExecDestroy(h->dexec);
+      h->dexec = ex;
+      h->dvalid = true;
+      h->dstats = st_local;
+      h->dstats.ms_total = h->dstats.ms_expand = h->dstats.ms_leaf = h->dstats.ms_backup = h->dstats.ms_comm = 0.f;
+    }
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+  }
+  if (!(key == h->dkey)) h->dvalid = false;
+  h->dkey = key;
+  return BCTS_OK;
+}
+
+bcts_status bcts_nccl_unique_id(void *out128) {
+  if (!out128) return BCTS_ERR_INVALID_ARG;
+  std::string err;
+  return comm_unique_id(out128, err) ? BCTS_OK : BCTS_ERR_NCCL;
+}
+
+bcts_status bcts_workspace_size(bcts_handle h, int64_t n_roots, int32_t depth, size_t *bytes) {
+  if (!h || !bytes || n_roots < 0 || depth < 0 || depth > kMaxDepth) return BCTS_ERR_INVALID_ARG;
+  SearchPlan pl;
+  size_t tree = 0;
+  if (n_roots > 0) {
+    bcts_status s = plan_search(h, n_roots, depth, 1, pl);
+    if (s) return s;
+    tree = pl.total;
+  }
+  *bytes = align_up(net_scratch_bytes(h->net)) + tree;
+  return BCTS_OK;
+}
+
+bcts_status bcts_set_workspace(bcts_handle h, void *dev_ptr, size_t bytes) {
+  if (!h) return BCTS_ERR_INVALID_ARG;
+  if (dev_ptr && ((uintptr_t)dev_ptr % 256 != 0 || bytes < align_up(net_scratch_bytes(h->net))))
+    return fail(h, BCTS_ERR_INVALID_ARG, "caller workspace misaligned or smaller than the net scratch (" +
+                                             std::to_string(net_scratch_bytes(h->net)) + " bytes)");
+  cudaSetDevice(h->dev);
+  if (cudaStreamSynchronize(h->st) != cudaSuccess) return cuda_check(h, "set_workspace sync");
+  std::string err;
+  // drop the current memory (graphs bake its addresses in)
+  h->dvalid = h->gvalid = false;
+  if (h->ws_own) cudaFree(h->ws);
+  h->ws = nullptr;
+  h->ws_size = 0;
+  cudaFree(h->scratch_own);
+  h->scratch_own = nullptr;
+  net_bind_scratch(h->net, nullptr, err);
+  h->ext = (uint8_t *)dev_ptr;
+  h->ext_bytes = dev_ptr ? bytes : 0;
+  h->ws_own = dev_ptr == nullptr;
+  if (dev_ptr) {
+    const size_t ns = align_up(net_scratch_bytes(h->net));
+    h->ws = h->ext + ns;
+    h->ws_size = bytes - ns;
+    bcts_status s = ensure_net(h);
     if (s) return s;
   }
-  Outs o{actions_out, root_q_out, vanilla_q_out, terms_out, best_leaf_out};
-  s = finalize_impl(h, roots, n_roots, depth, gamma, beta, correction_on, keys, o, kbytes, stats,
-                    try_fold ? &pf : nullptr);
-  if (stats) stats->kernel_launches = h->launches - l0;
-  return s;
+  return cuda_check(h, "set_workspace");
 }
 
 bcts_status bcts_search_pruned(bcts_handle h, const void *roots, int64_t n_roots, int32_t depth, int32_t A,
@@ -930,6 +1194,7 @@ bcts_status bcts_search_pruned(bcts_handle h, const void *roots, int64_t n_roots
   if (per < 1) return fail(h, BCTS_ERR_BUDGET, "workspace budget too small for one root of the pruned search");
   const size_t need = std::max(finalize_ws(h, n_roots, kbytes),
                                (size_t)per * per_root + compact_temp_bytes(sh.capE * per) + (4 << 20));
+  if ((s = ensure_net(h))) return s;
   if ((s = ensure_ws(h, kbytes + need))) return s;
   int64_t *keys = (int64_t *)h->ws;
   launch_keys_init(keys, n_roots * A, h->st);
@@ -968,22 +1233,31 @@ bcts_status bcts_search_host(bcts_handle h, const void *roots_host, int64_t n_ro
   cudaSetDevice(h->dev);
   const size_t rb = (size_t)n_roots * record_bytes(h->env);
   if (rb > h->e2e_roots_size) {
+    h->gvalid = false;   // the graph copies into the old buffer
     cudaFree(h->e2e_roots);
     h->e2e_roots = nullptr;
+    h->e2e_roots_size = 0;
     if (cudaMalloc(&h->e2e_roots, rb) != cudaSuccess) {
       cudaGetLastError();
-      h->e2e_roots_size = 0;
+      h->e2e_roots = nullptr;
       return fail(h, BCTS_ERR_OUT_OF_MEMORY, "e2e roots buffer");
     }
     h->e2e_roots_size = rb;
   }
   if ((size_t)n_roots * A > h->e2e_out) {
+    h->gvalid = false;
     cudaFree(h->e2e_act);
     cudaFree(h->e2e_q);
+    h->e2e_act = nullptr;
+    h->e2e_q = nullptr;
+    h->e2e_out = 0;
     if (cudaMalloc(&h->e2e_act, (size_t)n_roots * 4) != cudaSuccess ||
         cudaMalloc(&h->e2e_q, (size_t)n_roots * A * 4) != cudaSuccess) {
       cudaGetLastError();
-      h->e2e_out = 0;
+      cudaFree(h->e2e_act);
+      cudaFree(h->e2e_q);
+      h->e2e_act = nullptr;
+      h->e2e_q = nullptr;
       return fail(h, BCTS_ERR_OUT_OF_MEMORY, "e2e output buffers");
     }
     h->e2e_out = (size_t)n_roots * A;
@@ -997,15 +1271,13 @@ bcts_status bcts_search_host(bcts_handle h, const void *roots_host, int64_t n_ro
     cudaGetLastError();
     return ok;
   };
-  const bool can_graph = !h->prof.on && !getenv("BCTS_NO_GRAPH") && pinned(roots_host) && pinned(actions_host) &&
-                         pinned(root_q_host);
+  // TABULAR checks its root ids on the host (a synchronizing copy), which a capture cannot hold
+  const bool can_graph = !h->prof.on && !(h->flags & BCTS_F_NO_GRAPH) && h->env != BCTS_ENV_TABULAR &&
+                         pinned(roots_host) && pinned(actions_host) && pinned(root_q_host);
   bcts_handle_t::GraphKey key;
   key.rh = roots_host, key.ah = actions_host, key.qh = root_q_host, key.n = n_roots, key.d = depth, key.A = A;
   key.corr = correction_on, key.gamma = gamma, key.beta = beta, key.ws = h->ws, key.wss = h->ws_size;
-  static const bool gdbg = getenv("BCTS_GRAPH_DEBUG") != nullptr;
-  if (gdbg)
-    fprintf(stderr, "search_host: can_graph=%d valid=%d match=%d ws=%p/%zu\n", (int)can_graph, (int)h->gvalid,
-            (int)(key == h->gkey), (void *)h->ws, h->ws_size);
+  key.dr = h->e2e_roots, key.da = h->e2e_act, key.dq = h->e2e_q, key.scratch = h->net.scratch;
   if (can_graph && h->gvalid && key == h->gkey) {
     if (cudaGraphLaunch(h->gexec, h->st) == cudaSuccess && cudaStreamSynchronize(h->st) == cudaSuccess)
       return cuda_check(h, "e2e graph");
@@ -1028,13 +1300,15 @@ bcts_status bcts_search_host(bcts_handle h, const void *roots_host, int64_t n_ro
   if (can_graph) {   // capture the same sequence on a private stream for the next call
     h->gvalid = false;
     if (!h->gst) cudaStreamCreateWithFlags(&h->gst, cudaStreamNonBlocking);
-    key.ws = h->ws, key.wss = h->ws_size;
+    key.ws = h->ws, key.wss = h->ws_size, key.scratch = h->net.scratch;
     cudaStream_t saved = h->st;
     h->st = h->gst;
     cudaGraph_t g = nullptr;
     bool ok = h->gst && cudaStreamBeginCapture(h->gst, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
     if (ok) {
+      h->capturing = true;
       const bcts_status sc = enqueue();
+      h->capturing = false;
       ok = cudaStreamEndCapture(h->gst, &g) == cudaSuccess && sc == BCTS_OK && g;
     }
     h->st = saved;
@@ -1049,7 +1323,6 @@ bcts_status bcts_search_host(bcts_handle h, const void *roots_host, int64_t n_ro
       }
     }
     if (g) cudaGraphDestroy(g);
-    if (gdbg) fprintf(stderr, "search_host: captured ok=%d valid=%d\n", (int)ok, (int)h->gvalid);
     cudaGetLastError();
   }
   return BCTS_OK;
@@ -1106,6 +1379,8 @@ bcts_status bcts_q_rows(bcts_handle h, const void *states, int64_t n, float *q_o
   if (!h || n < 0 || (n > 0 && (!states || !q_out))) return BCTS_ERR_INVALID_ARG;
   if (n == 0) return BCTS_OK;
   cudaSetDevice(h->dev);
+  bcts_status s = ensure_net(h);
+  if (s) return s;
   h->launches += net_eval(h->net, root_view(h->env, states, 0), n, MODE_ROWS, 0.0f, q_out, h->st);
   return cuda_check(h, "q_rows");
 }

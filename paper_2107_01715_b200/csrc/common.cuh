@@ -19,13 +19,16 @@ namespace bcts {
 // scheduled while its stream predecessor drains, runs its prologue (barriers, TMEM,
 // weight bulk copies -- nothing the predecessor writes), then pdl_wait()s for the
 // predecessor's completion before touching its outputs. pdl_trigger() lets the next
-// kernel be scheduled as this one's CTAs retire. BCTS_NO_PDL=1 disables it.
+// kernel be scheduled as this one's CTAs retire.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-inline bool pdl_enabled() {
-  static const int on = getenv("BCTS_NO_PDL") ? 0 : 1;
-  return on != 0;
-}
+inline bool pdl_enabled() { return true; }
+
+// Per-device launch configuration (defined in bcts.cu): the SM count of the current device, and
+// the dynamic-SMEM opt-in of a kernel on the current device (cudaFuncSetAttribute is per device:
+// every device a handle runs on gets it; thread-safe, once per (kernel, device, size)).
+int sm_count_current();
+cudaError_t smem_optin(const void *kernel, int bytes);
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                               Args &&...args) {

@@ -13,7 +13,7 @@ namespace bcts {
 // DESIGN.md §5) so bench.py can report achieved = work / duration.
 enum KernelClass {
   KC_EXPAND_ATARI = 0, KC_EXPAND_INT, KC_EXPAND_TAB, KC_CONV1, KC_CONV2, KC_CONV3, KC_FC_H, KC_FC_OUT, KC_HEAD,
-  KC_MLP, KC_TABLE, KC_SEGMAX, KC_FINALIZE, KC_OTHER, KC_EXPAND_DNN, KC_CONV23, KC_PRUNE, KC_COUNT
+  KC_MLP, KC_TABLE, KC_SEGMAX, KC_FINALIZE, KC_OTHER, KC_EXPAND_DNN, KC_CONV23, KC_PRUNE, KC_COMM, KC_COUNT
 };
 struct Profiler {
   bool on = false;
@@ -216,6 +216,7 @@ enum { MODE_ROWS = 0, MODE_ROWMAX = 1, MODE_TOTAL = 2 };
 void launch_mlp_tiled(const NodeView &v, int64_t n, const float *img, int I, int H, int A, int mode, float gd,
                       float *out, int feat_f32, cudaStream_t st);
 
+constexpr int kNetScratch = 11;
 struct Net {
   int kind = 0, A = 0;
   // TABLE
@@ -240,6 +241,11 @@ struct Net {
   int64_t batch = 0, fc_batch = 0;
   int64_t mat_batch = 0;          // trunk sub-batch of the materialised-state path (s2d input buffer)
   TmaPlan p_c1, p_c2, p_c3, p_fc_h, p_z_v, p_z_a, p_fc2;
+  // scratch buffers (net_bind_scratch): sizes fixed at build, memory bound later (library-owned
+  // or caller-provided via bcts_set_workspace)
+  size_t scratch_sz[kNetScratch] = {};
+  uint8_t *scratch = nullptr;
+  bool simt = false;
   __nv_bfloat16 *s2d = nullptr;   // [batch][21][21][64] conv1 input (dense; SIMT / TMA paths)
   uint8_t *in1p = nullptr, *act1p = nullptr, *act2p = nullptr;  // planar trunk buffers [batch]
   Layer c2s;                      // conv2 as 2x2 stride-1 over s2d(2) of act1 (shifted windows)
@@ -259,6 +265,16 @@ struct Net {
 // out[n] = max_a Q; MODE_TOTAL: out[n] = fmaf(gd, max_a Q, cum[i]).
 // Returns the number of kernels launched, or -1 on a CUDA error.
 int net_eval(Net &net, const NodeView &v, int64_t n, int mode, float gd, float *out, cudaStream_t st);
+// Scratch the conv nets need (0 for the table / MLP nets), and binding it: carve the buffers out
+// of `base` (256-byte aligned pieces) and re-encode the TMA tensor maps over them.
+size_t net_scratch_bytes(const Net &net);
+// NCCL (comm.cu): the multi-GPU handle's communicator; errors as text in err
+constexpr int kNcclIdBytes = 128;
+bool comm_unique_id(void *out128, std::string &err);
+bool comm_init(void **comm, const void *id128, int rank, int world, std::string &err);
+bool comm_allreduce_max_i64(void *comm, int64_t *buf, int64_t count, cudaStream_t st, std::string &err);
+void comm_destroy(void *comm);
+int net_bind_scratch(Net &net, uint8_t *base, std::string &err);
 // Conv nets only: evaluate the children [c_begin, c_end) of the parents in view
 // `par` (global level indices from p_first), generating each child's frames on
 // the fly (fused last-level expansion, gk = g[d-1]); out[i] per MODE.
@@ -282,8 +298,6 @@ int net_build(Net &net, const bcts_config &cfg, std::string &err);  // 0 ok
 void net_free(Net &net);
 
 // tcgen05 layer (qnet_tc.cu); returns false if the layer shape is unsupported.
-bool tc_supported(const Layer &L);
-void launch_layer_tc(const Layer &L, const void *in, int64_t n_img, void *out, cudaStream_t st);
 void launch_layer_simt(const Layer &L, const void *in, int64_t n_img, void *out, cudaStream_t st);
 
 // ---------------------------------------------------------------- K3 backup

@@ -170,11 +170,7 @@ void launch_expand(int env, const NodeView &par, int64_t p_first, int64_t c_begi
   } else if (env == BCTS_ENV_INT_HASH) {
     k_expand_int<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(par, p_first, c_begin, n, A, gk, out);
   } else {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_expand_atari, cudaFuncAttributeMaxDynamicSharedMemorySize, kFrameBytes);
-      attr = true;
-    }
+    smem_optin((const void *)k_expand_atari, kFrameBytes);
     // about 6 CTAs per SM (8 fit by SMEM) and at most ~6 children per CTA (measured best at the
     // C5 level-3 and C3 level-2 shapes, tools/expand_bench.cu)
     const int64_t want = std::max<int64_t>((6 * 148 + nparents - 1) / nparents, (A + 5) / 6);

@@ -300,16 +300,7 @@ __global__ void __launch_bounds__(kDnnThreads, 1)
   }
 }
 
-int sm_count() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
-  return sms;
-}
+int sm_count() { return sm_count_current(); }
 }  // namespace
 
 void launch_expand_dnn(const NodeView &par, int64_t p_first, int64_t c_begin, int64_t c_end, int A, float gk,
@@ -320,12 +311,8 @@ void launch_expand_dnn(const NodeView &par, int64_t p_first, int64_t c_begin, in
   // algorithmic FLOPs: per child 2*(100*100 + 100*100 + 101*100) (layers 2-4; the layer-1 tail is
   // one add), per parent 2*100*100 (the shared state part of layer 1)
   if (prof) prof->begin(KC_EXPAND_DNN, 2.0 * (30100.0 * (double)n + 10000.0 * (double)nparents), st);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_expand_dnn<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dnn_smem<8>());
-    cudaFuncSetAttribute(k_expand_dnn<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dnn_smem<2>());
-    attr = true;
-  }
+  smem_optin((const void *)k_expand_dnn<8>, (int)dnn_smem<8>());
+  smem_optin((const void *)k_expand_dnn<2>, (int)dnn_smem<2>());
   const int sms = sm_count();
   const int64_t tiles80 = (n + 79) / 80;
   if (tiles80 >= 2 * sms) {
@@ -478,22 +465,15 @@ void launch_mlp_tiled(const NodeView &v, int64_t n, const float *img, int I, int
                       float *out, int feat_f32, cudaStream_t st) {
   if (n <= 0) return;
   // the attribute is raised to what this launch needs (static smem counts against the same 227 KB)
-  static size_t attr64 = 0, attr32 = 0;
   if (mlp_smem<64>(I, H, A) <= kMlpSmemMax) {
     const size_t sm = mlp_smem<64>(I, H, A);
-    if (sm > attr64) {
-      cudaFuncSetAttribute(k_mlp_tiled<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      attr64 = sm;
-    }
+    smem_optin((const void *)k_mlp_tiled<64>, (int)sm);
     const unsigned grid = (unsigned)std::min<int64_t>((n + 63) / 64, sm_count());
     k_mlp_tiled<64><<<grid, kMlpThreads, sm, st>>>(v.state, v.state_stride, img, I, H, A, n, mode, gd, v.cum, out,
                                                    feat_f32);
   } else {
     const size_t sm = mlp_smem<32>(I, H, A);
-    if (sm > attr32) {
-      cudaFuncSetAttribute(k_mlp_tiled<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      attr32 = sm;
-    }
+    smem_optin((const void *)k_mlp_tiled<32>, (int)sm);
     const unsigned grid = (unsigned)std::min<int64_t>((n + 31) / 32, sm_count());
     k_mlp_tiled<32><<<grid, kMlpThreads, sm, st>>>(v.state, v.state_stride, img, I, H, A, n, mode, gd, v.cum, out,
                                                    feat_f32);

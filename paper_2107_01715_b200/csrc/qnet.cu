@@ -578,31 +578,20 @@ int net_build(Net &net, const bcts_config &cfg, std::string &err) {
   // 2 waves 2.33, 3 waves 2.31, 6 waves -- the whole 104,976-leaf level in one batch -- 2.28). The
   // materialised-state path (s2d input, act2) keeps one wave of sub-batch: it only scores small
   // sets. Scratch at 6 waves: ~4.2 GB of act1 + ~1 GB of act3 / hidden / head buffers.
-  int64_t waves = 6;
-  if (const char *e = getenv("BCTS_FC_WAVES")) waves = atoll(e) > 0 ? atoll(e) : waves;
+  const int64_t waves = 6;
   net.batch = 148 * 128 * waves;
   net.fc_batch = 148 * 128 * waves;
   net.mat_batch = 148 * 128;
-  if (const char *e = getenv("BCTS_TRUNK_BATCH")) net.batch = atoll(e) > 0 ? atoll(e) : net.batch;
-  if (net.mat_batch > net.batch) net.mat_batch = net.batch;
   const int64_t B = net.batch, FB = net.fc_batch, MB = net.mat_batch;
-  const int64_t B2 = getenv("BCTS_NO_CONV23") ? B : MB;   // act2 is materialised only without the conv2+conv3 fusion
   const bool simt = (cfg.flags & BCTS_F_SIMT_NET) != 0;   // dense NHWC trunk buffers only for the SIMT path
-  size_t bytes[11] = {simt ? (size_t)MB * 400 * 32 * 2 : 0, simt ? (size_t)MB * 81 * 64 * 2 : 0,
-                      (size_t)FB * 49 * 64 * 2, (size_t)FB * hidN * 2, (size_t)FB * (rainbow ? net.ld_zv : 16) * 4,
-                      (size_t)FB * net.ld_za * 4, simt ? (size_t)MB * 21 * 21 * 64 * 2 : 0, (size_t)FB * 4,
-                      (size_t)MB * kIn1Bytes, (size_t)B * kIn2Bytes, (size_t)B2 * kIn3Bytes};
-  void *p[11];
-  for (int t = 0; t < 11; ++t) {
-    p[t] = nullptr;
-    if (!bytes[t]) continue;
-    if (cudaMalloc(&p[t], bytes[t]) != cudaSuccess) { err = "cudaMalloc net scratch failed"; return -1; }
-    net.allocs.push_back(p[t]);
-  }
-  net.act1 = (__nv_bfloat16 *)p[0]; net.act2 = (__nv_bfloat16 *)p[1]; net.act3 = (__nv_bfloat16 *)p[2];
-  net.hid_act = (__nv_bfloat16 *)p[3]; net.zv = (float *)p[4]; net.za = (float *)p[5];
-  net.s2d = (__nv_bfloat16 *)p[6]; net.leaf_cum = (float *)p[7];
-  net.in1p = (uint8_t *)p[8]; net.act1p = (uint8_t *)p[9]; net.act2p = (uint8_t *)p[10];
+  net.simt = simt;
+  // scratch (device memory bound later by net_bind_scratch: library-owned or caller-provided)
+  const size_t bytes[kNetScratch] = {simt ? (size_t)MB * 400 * 32 * 2 : 0, simt ? (size_t)MB * 81 * 64 * 2 : 0,
+                                     (size_t)FB * 49 * 64 * 2, (size_t)FB * hidN * 2,
+                                     (size_t)FB * (rainbow ? net.ld_zv : 16) * 4, (size_t)FB * net.ld_za * 4,
+                                     simt ? (size_t)MB * 21 * 21 * 64 * 2 : 0, (size_t)FB * 4, (size_t)MB * kIn1Bytes,
+                                     (size_t)B * kIn2Bytes, (size_t)MB * kIn3Bytes};
+  for (int t = 0; t < kNetScratch; ++t) net.scratch_sz[t] = bytes[t];
   // shifted-window trunk geometry (qnet_conv.cu)
   {
     ConvSW &a = net.sw1;
@@ -619,9 +608,6 @@ int net_build(Net &net, const bcts_config &cfg, std::string &err) {
     c.out_mode = 2; c.out_plane = 0; c.out_w = 7; c.out_img_bytes = 3136 * 2;
     const int layout = 2;   // SW128 row blocks, address-based swizzle (the compiled MMA loop assumes it)
     a.layout = b.layout = c.layout = layout;
-    uint32_t chunks = 1;
-    if (const char *e = getenv("BCTS_COPY_CHUNKS")) chunks = (uint32_t)atoi(e) > 0 ? (uint32_t)atoi(e) : 1;
-    a.copy_chunks = b.copy_chunks = c.copy_chunks = chunks;
     // weights of each shifted-window layer as the exact SW128 shared-memory
     // image the kernel wants (K/64 blocks of [N rows x 128 B], 16-byte chunk
     // j of row n at (n/8)*1024 + (n%8)*128 + ((j ^ n%8) * 16)): one bulk copy
@@ -659,23 +645,49 @@ int net_build(Net &net, const bcts_config &cfg, std::string &err) {
       }
     }
   }
-  // TMA plans (tensor maps over the fixed scratch buffers; fall back to the
-  // thread-gather tcgen05 layer if the driver entry points are unavailable)
-  if (simt) {   // dense trunk (SIMT reference path only; kept for completeness of the TMA im2col path)
-    tma_plan(net.p_c1, net.c1, net.s2d, MB);
-    tma_plan(net.p_c2, net.c2, net.act1, MB);
-    tma_plan(net.p_c3, net.c3, net.act2, MB);
-  }
-  tma_plan(net.p_fc_h, net.fc_h, net.act3, FB);
-  if (rainbow) {
-    tma_plan(net.p_z_v, net.z_v, net.hid_act, FB);
-    tma_plan(net.p_z_a, net.z_a, net.hid_act, FB);
-    if (net.wa64 && net.atoms == 51 && A <= 64 && !getenv("BCTS_NO_FUSED_HEAD"))
-      head_plan(net.head, net.hid_act, FB, net.z_v.Wt, net.wa64, net.wsum, A);
-  } else {
-    tma_plan(net.p_fc2, net.fc2, net.hid_act, FB);
-  }
   cudaGetLastError();
+  return 0;
+}
+
+size_t net_scratch_bytes(const Net &net) {
+  size_t t = 0;
+  for (int i = 0; i < kNetScratch; ++i) t += (net.scratch_sz[i] + 255) / 256 * 256;
+  return t;
+}
+
+int net_bind_scratch(Net &net, uint8_t *base, std::string &err) {
+  void *p[kNetScratch];
+  size_t off = 0;
+  for (int t = 0; t < kNetScratch; ++t) {
+    p[t] = net.scratch_sz[t] && base ? base + off : nullptr;
+    off += (net.scratch_sz[t] + 255) / 256 * 256;
+  }
+  net.act1 = (__nv_bfloat16 *)p[0]; net.act2 = (__nv_bfloat16 *)p[1]; net.act3 = (__nv_bfloat16 *)p[2];
+  net.hid_act = (__nv_bfloat16 *)p[3]; net.zv = (float *)p[4]; net.za = (float *)p[5];
+  net.s2d = (__nv_bfloat16 *)p[6]; net.leaf_cum = (float *)p[7];
+  net.in1p = (uint8_t *)p[8]; net.act1p = (uint8_t *)p[9]; net.act2p = (uint8_t *)p[10];
+  net.scratch = base;
+  if (!base || (net.kind != BCTS_NET_NATURE_BF16 && net.kind != BCTS_NET_RAINBOW_BF16)) return 0;
+  // TMA plans: tensor maps over the scratch buffers (re-encoded whenever the scratch moves)
+  const int64_t FB = net.fc_batch, MB = net.mat_batch;
+  bool ok = true;
+  if (net.simt) {   // dense trunk (SIMT reference path)
+    ok &= tma_plan(net.p_c1, net.c1, net.s2d, MB);
+    ok &= tma_plan(net.p_c2, net.c2, net.act1, MB);
+    ok &= tma_plan(net.p_c3, net.c3, net.act2, MB);
+  }
+  ok &= tma_plan(net.p_fc_h, net.fc_h, net.act3, FB);
+  if (net.kind == BCTS_NET_RAINBOW_BF16) {
+    ok &= tma_plan(net.p_z_v, net.z_v, net.hid_act, FB);
+    ok &= tma_plan(net.p_z_a, net.z_a, net.hid_act, FB);
+    if (net.wa64 && net.atoms == 51 && net.A <= 64) ok &= head_plan(net.head, net.hid_act, FB, net.z_v.Wt, net.wa64, net.wsum, net.A);
+  } else {
+    ok &= tma_plan(net.p_fc2, net.fc2, net.hid_act, FB);
+  }
+  if (!ok) {
+    err = "TMA tensor-map encoding failed (driver entry point cuTensorMapEncodeTiled)";
+    return -1;
+  }
   return 0;
 }
 
@@ -689,18 +701,13 @@ static void run_layer(const Net &net, int cls, const Layer &L, const void *in, i
   // algorithmic FLOPs: 2 * M * N * K with the true (unpadded) N
   if (net.prof) net.prof->begin(cls, 2.0 * (double)(n_img * L.rows_per_img()) * L.N * L.K, st);
   if (net.tc && plan && plan->ok) launch_layer_tma(*plan, L, n_img, out, st);
-  else if (net.tc && tc_supported(L)) launch_layer_tc(L, in, n_img, out, st);
-  else launch_layer_simt(L, in, n_img, out, st);
+  else launch_layer_simt(L, in, n_img, out, st);   // BCTS_F_SIMT_NET (tensor-map plans are checked at bind)
   if (net.prof) net.prof->end(st);
 }
 
 // Conv-net evaluation over n images that come either from a view of frame
 // stacks (`img`, images [0, n)) or are the children [c_begin, c_begin + n) of
 // the parents in `par` (fused last-level expansion). Trunk in L2-sized
-static bool c23_enabled() {
-  static const bool on = !getenv("BCTS_NO_CONV23");
-  return on;
-}
 // sub-batches: frames -> s2d bf16 -> conv1 -> conv2 -> conv3 (act3 of the fc
 // batch); then fc_hidden, the output layer(s) and the head.
 static int eval_conv(Net &net, const NodeView *par, const NodeView *img, int64_t p_first, int64_t c_begin, float gk,
@@ -715,9 +722,9 @@ static int eval_conv(Net &net, const NodeView *par, const NodeView *img, int64_t
   for (int64_t f0 = 0; f0 < n; f0 += step) {
     const int64_t nf = n - f0 < step ? n - f0 : step;
     const bool fused_leaf = par && net.tc && net.sw;
-    const int64_t tb = fused_leaf ? (c23_enabled() ? net.batch : net.mat_batch) : net.mat_batch;
+    const int64_t tb = fused_leaf ? (net.batch) : net.mat_batch;
     // the prologue's states ride along in this (last) batch when it has room (PrologueFold)
-    const int64_t ne = (pf && !pf->done && f0 + nf >= n && fused_leaf && c23_enabled() && mode == MODE_TOTAL &&
+    const int64_t ne = (pf && !pf->done && f0 + nf >= n && fused_leaf && mode == MODE_TOTAL &&
                         net.kind == BCTS_NET_RAINBOW_BF16 && net.head.ok && nf <= tb && nf + pf->ne <= net.batch &&
                         nf + pf->ne <= net.fc_batch && pf->ne <= net.mat_batch)
                            ? pf->ne
@@ -743,20 +750,12 @@ static int eval_conv(Net &net, const NodeView *par, const NodeView *img, int64_t
           if (net.prof) net.prof->end(st);
           launches += 2;
         }
-        if (c23_enabled()) {   // conv2 + conv3 fused: act2 never leaves the SM
+        {   // conv2 + conv3 fused: act2 never leaves the SM
           const double fl2 = 2.0 * (double)(nb + ne);
           if (net.prof) net.prof->begin(KC_CONV23, fl2 * (81 * 64 * 512 + 49 * 64 * 576), st);
           launch_conv23(net.sw2, net.c2s, net.sw3, net.c3, net.act1p, nb + ne, net.act3 + b0 * 3136, st);
           if (net.prof) net.prof->end(st);
           launches += 2;
-        } else {
-          if (net.prof) net.prof->begin(KC_CONV2, fl * 81 * 64 * 512, st);
-          launch_conv_sw(net.sw2, net.c2s, net.act1p, nb, net.act2p, st);
-          if (net.prof) net.prof->end(st);
-          if (net.prof) net.prof->begin(KC_CONV3, fl * 49 * 64 * 576, st);
-          launch_conv_sw(net.sw3, net.c3, net.act2p, nb, net.act3 + b0 * 3136, st);
-          if (net.prof) net.prof->end(st);
-          launches += 3;
         }
         continue;
       }
@@ -773,19 +772,10 @@ static int eval_conv(Net &net, const NodeView *par, const NodeView *img, int64_t
         if (net.prof) net.prof->begin(KC_CONV1, fl * 400 * 32 * 256, st);
         launch_conv_sw(net.sw1, net.c1, net.in1p, nb, net.act1p, st);
         if (net.prof) net.prof->end(st);
-        if (c23_enabled()) {
-          if (net.prof) net.prof->begin(KC_CONV23, fl * (81 * 64 * 512 + 49 * 64 * 576), st);
-          launch_conv23(net.sw2, net.c2s, net.sw3, net.c3, net.act1p, nb, net.act3 + b0 * 3136, st);
-          if (net.prof) net.prof->end(st);
-          launches -= 1;
-        } else {
-          if (net.prof) net.prof->begin(KC_CONV2, fl * 81 * 64 * 512, st);
-          launch_conv_sw(net.sw2, net.c2s, net.act1p, nb, net.act2p, st);
-          if (net.prof) net.prof->end(st);
-          if (net.prof) net.prof->begin(KC_CONV3, fl * 49 * 64 * 576, st);
-          launch_conv_sw(net.sw3, net.c3, net.act2p, nb, net.act3 + b0 * 3136, st);
-          if (net.prof) net.prof->end(st);
-        }
+        if (net.prof) net.prof->begin(KC_CONV23, fl * (81 * 64 * 512 + 49 * 64 * 576), st);
+        launch_conv23(net.sw2, net.c2s, net.sw3, net.c3, net.act1p, nb, net.act3 + b0 * 3136, st);
+        if (net.prof) net.prof->end(st);
+        launches -= 1;
       } else {
         run_layer(net, KC_CONV1, net.c1, net.s2d, nb, net.act1, st, &net.p_c1);
         run_layer(net, KC_CONV2, net.c2, net.act1, nb, net.act2, st, &net.p_c2);
@@ -844,8 +834,7 @@ int net_eval_children(Net &net, const NodeView &par, int64_t p_first, int64_t c_
                       float gk, int mode, float gd, float *out, cudaStream_t st, const KeyFold *kf, bool *folded,
                       PrologueFold *pf) {
   (void)A;
-  static const bool fold_ok = !getenv("BCTS_NO_HEAD_BACKUP");
-  const bool fold = kf && kf->keys && fold_ok && mode == MODE_TOTAL && net.kind == BCTS_NET_RAINBOW_BF16 && net.tc &&
+  const bool fold = kf && kf->keys && mode == MODE_TOTAL && net.kind == BCTS_NET_RAINBOW_BF16 && net.tc &&
                     net.head.ok;
   if (folded) *folded = fold;
   return eval_conv(net, &par, nullptr, p_first, c_begin, gk, c_end - c_begin, mode, gd, out, st, fold ? kf : nullptr,

@@ -177,8 +177,6 @@ __device__ __forceinline__ void tmem_wait16(uint32_t (&r)[16]) {
 constexpr int kConvInBufs = 3;   // k_conv_sw input ring (G1: 16 KB + 3 x 68 KB fits the 227 KB SMEM)
 // Compile-time trunk geometry (stride-1 convs after space-to-depth).
 struct G1 { static constexpr int N = 32, CIN = 64, KH = 2, KW = 2, W_IN = 21, N_MT = 4; static constexpr uint32_t BPLANE = kPlane1 * 8; };
-struct G2 { static constexpr int N = 64, CIN = 128, KH = 2, KW = 2, W_IN = 10, N_MT = 1; static constexpr uint32_t BPLANE = kPlane2 * 8; };
-struct G3 { static constexpr int N = 64, CIN = 64, KH = 3, KW = 3, W_IN = 9, N_MT = 1; static constexpr uint32_t BPLANE = kPlane3 * 8; };
 
 template <class G>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -807,153 +805,7 @@ __global__ void __launch_bounds__(kSibThreads, 1)
   }
 }
 
-// ------------------------------------------------------------ conv3, transposed MMA
-// conv3 (3x3 / 1 over act2 9x9x64 -> 7x7x64) as D^T = W x X^T: the MMA's A operand is the
-// weight tile (M = 64 output channels, K-major SW128, SMEM-resident) and B is the shifted
-// window of image rows (N = 64 >= the 63 full-width output rows, K-major SW128). An M = 64
-// MMA costs the same as M = 128 (tensor floor max(M,128)*N/256 = 32 cycles at N = 64) and
-// reads 4 KB of SMEM instead of 6 KB, so the 49 useful rows per image take 36 x 32 cycles
-// instead of 36 x 48 with M = 128 image rows (38% of them useful). The M = 64 accumulator
-// lives in TMEM lanes 32q .. 32q+15 of each lane quarter q (channel 16q + l at lane 32q + l;
-// measured, tools/m64_layout.cu), columns = image rows.
-// Warps: 0 = bulk-copy producer (3-deep input ring), 1 = MMA, 2-5 = epilogue (one per lane
-// quarter; lanes 0-15 carry a channel): bias + ReLU + bf16 into a dense [49][64] staging
-// tile, written to act3 with one bulk copy per image.
-constexpr int kC3tThreads = 192;
-constexpr int kC3tOutBytes = 49 * 64 * 2;   // 6,272
-
-__global__ void __launch_bounds__(kC3tThreads, 1)
-    k_conv3t(ConvSW P, const uint8_t *__restrict__ Wsw, const float *__restrict__ bias,
-             const uint8_t *__restrict__ in, int64_t n_img, uint8_t *__restrict__ out) {
-  constexpr int NB = kConvInBufs;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u);
-  uint8_t *sW = smem;                                   // 9 k-blocks of [64 x 128 B], SW128 (A)
-  uint8_t *sIn0 = smem + 9 * 64 * 128;                  // NB input images (B windows)
-  const uint32_t in_stride = (P.in_img_bytes + 1023u) & ~1023u;
-  uint8_t *sOut0 = sIn0 + NB * in_stride;               // 2 x [49][64] bf16 staging
-  __shared__ __align__(8) uint64_t in_full[NB], in_empty[NB], tfull[2], tempty[2], wbar;
-  __shared__ uint32_t tmem_slot;
-  __shared__ float sbias[64];
-  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
-  if (threadIdx.x < 64) sbias[threadIdx.x] = bias[threadIdx.x];
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < NB; ++i) {
-      mbar_init(&in_full[i], 1);
-      mbar_init(&in_empty[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 128);
-    }
-    mbar_init(&wbar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    mbar_expect_tx(&wbar, 9u * 64 * 128);
-    bulk_g2s(saddr(sW), Wsw, 9u * 64 * 128, &wbar);
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(&tmem_slot)),
-                 "r"(128));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = tmem_slot;
-  pdl_wait();
-  pdl_trigger();
-
-  if (warp == 0) {
-    if (lane == 0) {   // ------------------------------------------------ producer
-      uint32_t i = 0;
-      const uint32_t blk = P.plane * 8u, valid = (uint32_t)P.in_rows * 128u;
-      for (int64_t img = blockIdx.x; img < n_img; img += gridDim.x, ++i) {
-        const uint32_t b = i % NB, ph = (i / NB) & 1u;
-        mbar_wait(&in_empty[b], ph ^ 1u);
-        mbar_expect_tx(&in_full[b], valid);   // one 64-channel row block (Cin = 64)
-        bulk_g2s(saddr(sIn0 + b * in_stride), in + img * (int64_t)P.in_img_bytes, valid, &in_full[b]);
-        (void)blk;
-      }
-    }
-    __syncwarp();
-  } else if (warp == 1) {   // ------------------------------------------ MMA issuer
-    constexpr uint32_t idesc = idesc_bf16(64, 64);
-    const uint32_t elected = elect_one();
-    mbar_wait(&wbar, 0);
-    const uint64_t wdesc = desc_sw128(saddr(sW));
-    uint32_t i = 0;
-    for (int64_t img = blockIdx.x; img < n_img; img += gridDim.x, ++i) {
-      const uint32_t bi = i % NB, phi = (i / NB) & 1u, b = i & 1u, ph = (i >> 1) & 1u;
-      mbar_wait(&in_full[bi], phi);
-      mbar_wait(&tempty[b], ph ^ 1u);
-      tc_fence_after();
-      const uint64_t xdesc = desc_sw128_win(saddr(sIn0 + bi * in_stride), false);
-#pragma unroll
-      for (int tap = 0; tap < 9; ++tap)
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          const uint32_t w_off = (uint32_t)tap * (64 * 128) + (uint32_t)(kk * 32);   // k = tap*64 + 16kk
-          const uint32_t x_off = (uint32_t)((tap / 3) * 9 + (tap % 3)) * 128u + (uint32_t)(kk * 32);
-          mma_pred(tmem + b * 64, wdesc + (w_off >> 4), xdesc + (x_off >> 4), idesc, (tap | kk) != 0, elected);
-        }
-      commit_pred(&in_empty[bi], elected);
-      commit_pred(&tfull[b], elected);
-      __syncwarp();
-    }
-  } else {   // -------------------------------------------------------- epilogue (lane quarter q)
-    const int q = warp & 3;
-    const int c = 16 * q + (lane & 15);                 // this lane's output channel (lanes 0-15)
-    const float bc = sbias[c];
-    const uint32_t taddr0 = tmem + ((uint32_t)(q * 32) << 16);
-    uint32_t i = 0;
-    for (int64_t img = blockIdx.x; img < n_img; img += gridDim.x, ++i) {
-      const uint32_t b = i & 1u, ph = (i >> 1) & 1u;
-      mbar_wait(&tfull[b], ph);
-      tc_fence_after();
-      uint32_t v[64];
-      tmem_ld16_nw(taddr0 + b * 64 + 0, *(uint32_t(*)[16])(v + 0));
-      tmem_ld16_nw(taddr0 + b * 64 + 16, *(uint32_t(*)[16])(v + 16));
-      tmem_ld16_nw(taddr0 + b * 64 + 32, *(uint32_t(*)[16])(v + 32));
-      tmem_ld16_nw(taddr0 + b * 64 + 48, *(uint32_t(*)[16])(v + 48));
-      // the wait ties all 64 loaded registers (repeated waits are free once the first retires)
-      tmem_wait16(*(uint32_t(*)[16])(v + 0));
-      tmem_wait16(*(uint32_t(*)[16])(v + 16));
-      tmem_wait16(*(uint32_t(*)[16])(v + 32));
-      tmem_wait16(*(uint32_t(*)[16])(v + 48));
-      tc_fence_before();
-      mbar_arrive(&tempty[b]);
-      uint8_t *so = sOut0 + b * kC3tOutBytes;
-      // staging buffer b is free once the bulk store of image i-2 has read it
-      if (threadIdx.x == 64) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (lane < 16) {
-#pragma unroll
-        for (int n = 0; n < 63; ++n) {
-          const int oy = n / 9, ox = n % 9;
-          if (oy < 7 && ox < 7) {
-            uint16_t h;
-            asm("cvt.rn.relu.bf16.f32 %0, %1;" : "=h"(h) : "f"(__uint_as_float(v[n]) + bc));
-            *(uint16_t *)(so + ((oy * 7 + ox) * 64 + c) * 2) = h;
-          }
-        }
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (threadIdx.x == 64) {
-        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + img * (int64_t)P.out_img_bytes),
-                     "r"(saddr(so)), "r"(kC3tOutBytes)
-                     : "memory");
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      }
-    }
-    if (threadIdx.x == 64) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-  }
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128));
-  }
-}
+constexpr int kC3tOutBytes = 49 * 64 * 2;   // dense act3 [49][64] bf16 of one image (6,272 B)
 
 // ------------------------------------------------ conv2 + conv3 fused (act2 stays on-chip)
 // Per image: conv2 (2x2/1 over act1's s2d(2) 10x10x128 -> 9x9x64) then conv3 (3x3/1 over act2
@@ -1313,26 +1165,13 @@ __global__ void __launch_bounds__(kC23Threads, 1)
   }
 }
 
-int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
+int num_sms() { return sm_count_current(); }
 
 template <class G>
 void launch_n(const ConvSW &P, const Layer &L, const void *in, int64_t n_img, void *out, cudaStream_t st) {
   constexpr int N = G::N;
   const int smem = (P.K / 64) * N * 128 + kConvInBufs * (int)((P.in_img_bytes + 1023u) & ~1023u) + 1024;
-  static int attr_for = 0;
-  if (attr_for < smem) {
-    cudaFuncSetAttribute(k_conv_sw<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr_for = smem;
-  }
+  smem_optin((const void *)k_conv_sw<G>, smem);
   const int grid = (int)std::min<int64_t>(n_img, num_sms());
   launch_pdl(k_conv_sw<G>, dim3(grid), dim3(kThreads), smem, st, P, P.wsw, L.bias, (const uint8_t *)in, n_img,
              (uint8_t *)out);
@@ -1345,36 +1184,16 @@ void launch_conv1_sib(const ConvSW &P, const Layer &L, const uint8_t *wsh, const
                       cudaStream_t st) {
   if (n_img <= 0) return;
   constexpr int smem = kSibSmem;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_conv1_sib, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  smem_optin((const void *)k_conv1_sib, smem);
   const int grid = (int)std::min<int64_t>(n_img, num_sms());
   launch_pdl(k_conv1_sib, dim3(grid), dim3(kSibThreads), (size_t)smem, st, P, wsh, wnw, L.bias, par, p_first, c_begin,
              n_img, A, gk, (uint8_t *)out, cum_out);
 }
 
-void launch_conv3t(const ConvSW &P, const Layer &L, const void *in, int64_t n_img, void *out, cudaStream_t st) {
-  const int smem = 9 * 64 * 128 + kConvInBufs * (int)((P.in_img_bytes + 1023u) & ~1023u) + 2 * kC3tOutBytes + 1024;
-  static int attr_for = 0;
-  if (attr_for < smem) {
-    cudaFuncSetAttribute(k_conv3t, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr_for = smem;
-  }
-  const int grid = (int)std::min<int64_t>(n_img, num_sms());
-  launch_pdl(k_conv3t, dim3(grid), dim3(kC3tThreads), (size_t)smem, st, P, P.wsw, L.bias, (const uint8_t *)in, n_img,
-             (uint8_t *)out);
-}
-
 void launch_conv23(const ConvSW &P2, const Layer &L2, const ConvSW &P3, const Layer &L3, const void *in, int64_t n_img,
                    void *out, cudaStream_t st) {
   if (n_img <= 0) return;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_conv23, cudaFuncAttributeMaxDynamicSharedMemorySize, kC23Smem);
-    attr = true;
-  }
+  smem_optin((const void *)k_conv23, kC23Smem);
   const int grid = (int)std::min<int64_t>(n_img, num_sms());
   launch_pdl(k_conv23, dim3(grid), dim3(kC23Threads), (size_t)kC23Smem, st, P2, P3, P2.wpair, L2.bias, P3.wsw, L3.bias,
              (const uint8_t *)in, n_img, (uint8_t *)out);
@@ -1382,16 +1201,9 @@ void launch_conv23(const ConvSW &P2, const Layer &L2, const ConvSW &P3, const La
 
 void launch_conv_sw(const ConvSW &P, const Layer &L, const void *in, int64_t n_img, void *out, cudaStream_t st) {
   if (n_img <= 0) return;
-  // conv3 writing the dense fc input: transposed (M = 64 channels) MMA form
-  static const bool c3t = !getenv("BCTS_NO_CONV3T");
-  if (c3t && P.N == 64 && P.Cin == 64 && P.out_mode == 2) {
-    launch_conv3t(P, L, in, n_img, out, st);
-    return;
-  }
-  // the MMA loop is compile-time unrolled per trunk layer (SW128 activations)
-  if (P.N == 32) launch_n<G1>(P, L, in, n_img, out, st);
-  else if (P.Cin == 128) launch_n<G2>(P, L, in, n_img, out, st);
-  else launch_n<G3>(P, L, in, n_img, out, st);
+  // conv1 over explicit states (the materialised path and the folded prologue rows); conv2 and
+  // conv3 always run fused in k_conv23
+  launch_n<G1>(P, L, in, n_img, out, st);
 }
 
 }  // namespace bcts

@@ -897,26 +897,13 @@ bool load_driver() {
   return true;
 }
 
-int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
+int num_sms() { return sm_count_current(); }
 
 // fc layer with ReLU + bf16 output (fc_hidden): the B-multicast pair kernel
 template <int BN, int KB>
 bool launch_gemm_mc(const TmaPlan &P, const Layer &L, int64_t M, void *out, cudaStream_t st) {
   using C = TmaCfg<BN, KB>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_gemm_mc<BN, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    attr = true;
-  }
+  smem_optin((const void *)k_gemm_mc<BN, KB>, C::SMEM);
   const int n_m = (int)((M + kBM - 1) / kBM), n_pm = (n_m + 1) / 2, n_n = (L.Npad + BN - 1) / BN;
   const int n_cl = std::min(n_pm * n_n, num_sms() / 2);
   cudaLaunchConfig_t cfg = {};
@@ -940,11 +927,7 @@ bool launch_gemm_mc(const TmaPlan &P, const Layer &L, int64_t M, void *out, cuda
 // fc layer (ReLU + bf16) on CTA pairs with the 2-SM MMA; needs B tensor map boxes of 128 rows
 bool launch_gemm_2sm(const TmaPlan &P, const Layer &L, int64_t M, void *out, cudaStream_t st) {
   if (!P.ok2sm) return false;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_gemm_2sm, cudaFuncAttributeMaxDynamicSharedMemorySize, k2smSmem);
-    attr = true;
-  }
+  smem_optin((const void *)k_gemm_2sm, k2smSmem);
   const int n_m = (int)((M + kBM - 1) / kBM), n_pm = (n_m + 1) / 2, n_n = L.Npad / 256;
   const int n_cl = std::min(n_pm * n_n, num_sms() / 2);
   cudaLaunchConfig_t cfg = {};
@@ -973,21 +956,19 @@ void launch_gemm(const TmaPlan &P, const Layer &L, int64_t M, void *out, cudaStr
     launch_gemm_small(P, L, M, out, st);
     return;
   }
-  static const bool two_sm = !getenv("BCTS_NO_2SM");
-  if (two_sm && !P.im2col && L.relu_bf16 && BN == 256 && KB == 64 && L.Npad % 256 == 0 &&
-      launch_gemm_2sm(P, L, M, out, st))
+  // one kernel per shape, chosen by eligibility (a failed launch stays pending for the caller's
+  // cuda_check; nothing falls back silently): CTA pairs for the wide fc_hidden, otherwise the
+  // cluster-multicast kernel for N-multiple-of-256 layers, otherwise the plain TMA GEMM
+  if (!P.im2col && L.relu_bf16 && BN == 256 && KB == 64 && L.Npad % 256 == 0) {
+    launch_gemm_2sm(P, L, M, out, st);
     return;
-  cudaGetLastError();
-  static const bool mc = !getenv("BCTS_NO_MULTICAST");
-  if (mc && !P.im2col && L.relu_bf16 && BN == 256 && L.Npad % BN == 0 && launch_gemm_mc<BN, KB>(P, L, M, out, st))
-    return;
-  cudaGetLastError();
-  using C = TmaCfg<BN, KB>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_gemm_tma<BN, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    attr = true;
   }
+  if (!P.im2col && L.relu_bf16 && BN == 256 && L.Npad % BN == 0) {
+    launch_gemm_mc<BN, KB>(P, L, M, out, st);
+    return;
+  }
+  using C = TmaCfg<BN, KB>;
+  smem_optin((const void *)k_gemm_tma<BN, KB>, C::SMEM);
   const int n_m = (int)((M + kBM - 1) / kBM), n_n = (L.Npad + BN - 1) / BN;
   const int grid = (int)std::min<int64_t>((int64_t)n_m * n_n, num_sms());
   TmaGeom G{P.im2col, L.OH, L.OW, L.S, L.KW, L.C};
@@ -1000,11 +981,7 @@ void launch_gemm(const TmaPlan &P, const Layer &L, int64_t M, void *out, cudaStr
 // A boxes stop every CTA from fetching 128 rows of A (~4 KB + 4 KB per k-block and CTA).
 void launch_gemm_small(const TmaPlan &P, const Layer &L, int64_t M, void *out, cudaStream_t st) {
   using C = TmaCfg<32, 64>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_gemm_tma<32, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    attr = true;
-  }
+  smem_optin((const void *)k_gemm_tma<32, 64>, C::SMEM);
   const int n_n = L.Npad / 32;
   const int grid = std::min(n_n, num_sms());
   TmaGeom G{0, L.OH, L.OW, L.S, L.KW, L.C};
@@ -1063,7 +1040,7 @@ bool tma_plan(TmaPlan &P, const Layer &L, const void *in, int64_t cap_img) {
                        estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     P.ok_small = false;
-    if (r == CUDA_SUCCESS && !conv && KB == 64 && L.Npad % 32 == 0 && !getenv("BCTS_NO_SMALL_M")) {
+    if (r == CUDA_SUCCESS && !conv && KB == 64 && L.Npad % 32 == 0) {
       // small-M maps: 32-row A boxes (kSmallM) and 32-row B boxes (N tiles of 32)
       cuuint64_t adims[2] = {(cuuint64_t)L.K, (cuuint64_t)cap_img};
       cuuint64_t astr[1] = {(cuuint64_t)L.in_img_stride * 2};
@@ -1118,11 +1095,7 @@ bool head_plan(HeadPlan &H, const __nv_bfloat16 *hid, int64_t cap, const __nv_bf
 void launch_zhead(const HeadPlan &H, int A, int atoms, int64_t M, float vmin, float dz, int mode, float gd,
                   const float *cum, float *out, cudaStream_t st, KeyFold kf, int64_t mrow0, float *rows_out) {
   if (M <= 0 || atoms != 51) return;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_zhead<51>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHeadSmem);
-    attr = true;
-  }
+  smem_optin((const void *)k_zhead<51>, kHeadSmem);
   const int n_m = (int)((M + kBM - 1) / kBM), nch = (A + 3) / 4;
   // full-row batches smaller than the GPU: split each tile's action chunks over several CTAs
   const int ns = mode == MODE_ROWS ? std::max(1, std::min(nch, num_sms() / n_m)) : 1;

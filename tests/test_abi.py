@@ -132,3 +132,51 @@ def test_no_cpu_fallback_in_product_path():
         for f in files:
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 assert not pat.search(open(os.path.join(dirpath, f)).read()), f
+
+
+def test_nccl_unique_id_without_gpu(L):
+    """bcts_nccl_unique_id needs no GPU (NCCL resolved at run time): 128 bytes, fresh per call."""
+    a, b = L.nccl_unique_id(), L.nccl_unique_id()
+    assert len(a) == len(b) == 128 and a != b
+    assert L.lib().bcts_nccl_unique_id(None) == 1
+
+
+def test_world_and_workspace_argument_checks_without_gpu(L):
+    """Argument checks that precede any CUDA call: rank/world of a multi-GPU config, NULL handles
+    of the workspace entry points."""
+    import ctypes
+    lib = L.lib()
+    cfg = L.bcts.Config()
+    cfg.abi_version = L.bcts.ABI_VERSION
+    cfg.env, cfg.net, cfg.num_actions, cfg.mlp_in, cfg.mlp_hidden = 2, 2, 4, 64, 256
+    h = ctypes.c_void_p()
+    cfg.world, cfg.rank = 2, 0                     # world > 1 needs the unique id
+    assert lib.bcts_create(ctypes.byref(cfg), ctypes.byref(h)) == 1
+    idbuf = ctypes.create_string_buffer(L.nccl_unique_id(), 128)
+    cfg.nccl_unique_id = ctypes.cast(idbuf, ctypes.c_void_p).value
+    cfg.rank = 2                                   # rank outside [0, world)
+    assert lib.bcts_create(ctypes.byref(cfg), ctypes.byref(h)) == 1
+    cfg.rank = -1
+    assert lib.bcts_create(ctypes.byref(cfg), ctypes.byref(h)) == 1
+    assert not h.value
+    size = ctypes.c_size_t()
+    assert lib.bcts_workspace_size(None, 1, 4, ctypes.byref(size)) == 1
+    assert lib.bcts_set_workspace(None, None, 0) == 1
+    assert lib.bcts_status_string(6) == b"BCTS_ERR_NCCL"
+
+
+def test_bench_self_launches_world2_reference_on_cpu():
+    """`bench.py --gpus 2 --impl reference` outside torchrun re-runs itself as 2 ranks (gloo on CPU for
+    the reference arm): rank 0 prints one JSON line with n_gpus 2, the other rank exits 0."""
+    import json
+    import subprocess
+    import sys
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_PORT")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--impl", "reference",
+                        "--config", "C2", "--steps", "1", "--warmup", "3"], capture_output=True, text=True,
+                       timeout=600, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
