@@ -386,9 +386,13 @@ def main():
             unit, bound = "TFLOP/s", "tensor"
             psrc = peaks["source"] + (" sustained" if long_run else " burst")
         ach = kernels[name]["achieved"]
+        # nominal denominators beside the measured ones: 2.25 PFLOP/s dense bf16,
+        # 8 TB/s HBM3e; the ALU peak is already the nominal unit count x clock
+        nominal = {"tensor": 2250.0, "hbm": 8000.0, "alu": peaks["fp32_tflops"]}[bound]
         roofline = {"kernel": name, "bound": bound, "achieved": ach, "peak": peak, "unit": unit,
                     "frac": ach / peak, "traffic": None,
-                    "work_per_launch": v["work"] / max(v["launches"], 1), "peak_source": psrc}
+                    "work_per_launch": v["work"] / max(v["launches"], 1), "peak_source": psrc,
+                    "peak_nominal": nominal, "frac_nominal": ach / nominal}
         tr = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tr):
             # one ncu --set full capture of this kernel (cold cache, a full launch), scaled to the
@@ -429,6 +433,10 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = oracle_sample(cfg)
+        # the canonical CPU baseline of SURVEY §8d: the same DFS on ONE thread (smaller sample)
+        one = oracle_sample(cfg, seconds_target=5.0, threads=1)
+        cpu["single_thread"] = {"value": one["value"], "unit": one["unit"], "cores": 1,
+                                "decisions_per_s": one["decisions_per_s"], "sample": one["sample"]}
 
     if rank == 0:
         line = {"metric": metric_of(cfg), "value": value, "unit": "nodes/s", "n_gpus": world,

@@ -6,40 +6,11 @@
 #include <algorithm>
 
 #include "engine.h"
+#include "ptx.cuh"
 
 namespace bcts {
 
-// ------------------------------------------------------------ PTX helpers
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-// 1-D bulk copy global -> shared (TMA engine, SASS UBLKCP), completes on mbar.
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
+// ------------------------------------------------------------ PTX helpers (the rest: ptx.cuh)
 __device__ __forceinline__ void st_v4(uint4 *p, const uint4 &v) {
   asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                : "memory");
@@ -119,13 +90,14 @@ __global__ void __launch_bounds__(kExpandThreads) k_expand_atari(NodeView par, i
   const int64_t pl = p - p_first;
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     mbar_expect_tx(&bar, kFrameBytes);
-    bulk_g2s(sframe, par.state + pl * par.state_stride, kFrameBytes, &bar);
+    bulk_g2s(saddr(sframe), par.state + pl * par.state_stride, kFrameBytes, &bar);   // one UBLKCP
   }
   const uint64_t key = *(const uint64_t *)((const uint8_t *)par.key + pl * par.key_stride);
   const float R = par.cum ? par.cum[pl] : 0.0f;
   __syncthreads();          // mbarrier init visible before anyone waits on it
-  mbar_wait(&bar, 0);
+  mbar_wait_spin(&bar, 0);
   for (int a = a_lo; a < a_hi; ++a) {
     const uint64_t k2 = atari_child_key(key, a);
     const int64_t ci = p * A + a - c_begin;

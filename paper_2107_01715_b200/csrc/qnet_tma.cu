@@ -17,33 +17,11 @@
 #include <algorithm>
 
 #include "engine.h"
+#include "ptx.cuh"
 
 namespace bcts {
 namespace {
 
-__device__ __forceinline__ uint32_t saddr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(b)), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(saddr(b)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
 __device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap *map, int x, int y, uint64_t *bar) {
   asm volatile(
@@ -75,47 +53,7 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t addr) {
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
-__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc));
-}
-__device__ __forceinline__ uint32_t elect_one() {
-  uint32_t e;
-  asm volatile("{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}\n" : "=r"(e));
-  return e;
-}
 // warp-uniform issue, elected lane predicated (see qnet_conv.cu / tools/mma_bench.cu)
-__device__ __forceinline__ void mma_pred(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc,
-                                         uint32_t issue) {
-  asm volatile(
-      "{\n.reg .pred p, q;\nsetp.ne.b32 p, %4, 0;\nsetp.ne.b32 q, %5, 0;\n"
-      "@q tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc), "r"(issue));
-}
-__device__ __forceinline__ void commit_pred(uint64_t *bar, uint32_t issue) {
-  asm volatile(
-      "{\n.reg .pred q;\nsetp.ne.b32 q, %1, 0;\n"
-      "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(saddr(bar)),
-      "r"(issue)
-      : "memory");
-}
-__device__ __forceinline__ void mma_commit(uint64_t *bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(saddr(bar))
-               : "memory");
-}
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
 
 constexpr int kBM = 128;
 constexpr int kThreads = 192;
@@ -197,7 +135,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % C::STAGES;
           const uint32_t ph = (it / C::STAGES) & 1u;
-          mbar_wait(&empty[s], ph ^ 1u);
+          mbar_wait_spin(&empty[s], ph ^ 1u);
           const uint32_t sa = saddr(smem + s * C::STAGE);
           mbar_expect_tx(&full[s], a_bytes + C::B_BYTES);
           if (G.im2col) {
@@ -223,13 +161,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int nt = min(BN, L.Npad - ntile * BN);
       const uint32_t idesc = idesc_bf16(kBM, nt);
       const uint32_t a = acc_it & 1u, aph = (acc_it >> 1) & 1u;
-      mbar_wait(&tempty[a], aph ^ 1u);
+      mbar_wait_spin(&tempty[a], aph ^ 1u);
       tc_fence_after();
       const uint32_t d = tmem + a * BN;
       for (int kb = 0; kb < nk; ++kb, ++it) {
         const int s = it % C::STAGES;
         const uint32_t ph = (it / C::STAGES) & 1u;
-        mbar_wait(&full[s], ph);
+        mbar_wait_spin(&full[s], ph);
         tc_fence_after();
         const uint32_t a0 = saddr(smem + s * C::STAGE), b0 = a0 + C::A_BYTES;
         const uint64_t ad = sdesc<KB>(a0), bd = sdesc<KB>(b0);
@@ -251,7 +189,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int n0 = ntile * BN;
       const int nt = min(BN, L.Npad - n0);
       const uint32_t a = acc_it & 1u, aph = (acc_it >> 1) & 1u;
-      mbar_wait(&tfull[a], aph);
+      mbar_wait_spin(&tfull[a], aph);
       tc_fence_after();
       const uint32_t trow = tmem + a * BN + ((uint32_t)(q * 32) << 16);
       for (int c = 0; c < nt; c += 16) {
@@ -371,7 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int m0 = (2 * pm + (int)rank) * kBM;
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % C::STAGES;
-          mbar_wait(&empty[s], ((it / C::STAGES) & 1u) ^ 1u);
+          mbar_wait_spin(&empty[s], ((it / C::STAGES) & 1u) ^ 1u);
           const uint32_t sa = saddr(smem + s * C::STAGE);
           mbar_expect_tx(&full[s], C::STAGE);             // own A + the multicast B
           tma_2d(sa, &mapA, kb * KB, m0, &full[s]);
@@ -388,12 +326,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int ntn = min(BN, L.Npad - nt * BN);
       const uint32_t idesc = idesc_bf16(kBM, ntn);
       const uint32_t a = acc_it & 1u, aph = (acc_it >> 1) & 1u;
-      mbar_wait(&tempty[a], aph ^ 1u);
+      mbar_wait_spin(&tempty[a], aph ^ 1u);
       tc_fence_after();
       const uint32_t d = tmem + a * BN;
       for (int kb = 0; kb < nk; ++kb, ++it) {
         const int s = it % C::STAGES;
-        mbar_wait(&full[s], (it / C::STAGES) & 1u);
+        mbar_wait_spin(&full[s], (it / C::STAGES) & 1u);
         tc_fence_after();
         const uint32_t a0 = saddr(smem + s * C::STAGE), b0 = a0 + C::A_BYTES;
         const uint64_t ad = sdesc<KB>(a0), bd = sdesc<KB>(b0);
@@ -415,7 +353,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int n0 = nt * BN;
       const int ntn = min(BN, L.Npad - n0);
       const uint32_t a = acc_it & 1u, aph = (acc_it >> 1) & 1u;
-      mbar_wait(&tfull[a], aph);
+      mbar_wait_spin(&tfull[a], aph);
       tc_fence_after();
       const uint32_t trow = tmem + a * BN + ((uint32_t)(q * 32) << 16);
       for (int c = 0; c < ntn; c += 16) {
@@ -524,7 +462,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int m0 = pm * 256 + (int)rank * kBM, n0 = nt * 256 + (int)rank * 128;
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % k2smStages;
-          mbar_wait(&empty[s], ((it / k2smStages) & 1u) ^ 1u);
+          mbar_wait_spin(&empty[s], ((it / k2smStages) & 1u) ^ 1u);
           const uint32_t sa = saddr(smem + s * k2smStage);
           if (rank == 0) mbar_expect_tx(&full[s], 2 * k2smStage);   // both CTAs' bytes land on this barrier
           tma_2d_2cta(sa, &mapA, kb * 64, m0, full0 + (uint32_t)s * 8u);
@@ -540,13 +478,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t it = 0, acc_it = 0;
       for (int tile = cl; tile < n_tiles; tile += ncl, ++acc_it) {
         const uint32_t a = acc_it & 1u, aph = (acc_it >> 1) & 1u;
-        mbar_wait(&tempty[a], aph ^ 1u);
+        mbar_wait_spin(&tempty[a], aph ^ 1u);
         tc_fence_after();
         const uint32_t d = tmem + a * 256;
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % k2smStages;
           const uint32_t ph = (it / k2smStages) & 1u;
-          mbar_wait(&full[s], ph);
+          mbar_wait_spin(&full[s], ph);
           tc_fence_after();
           const uint32_t a0 = saddr(smem + s * k2smStage), b0 = a0 + 16384;
           const uint64_t ad = sdesc<64>(a0), bd = sdesc<64>(b0);
@@ -585,7 +523,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t m = (int64_t)pm * 256 + (int64_t)rank * kBM + r;
       const int n0 = nt * 256;
       const uint32_t a = acc_it & 1u, aph = (acc_it >> 1) & 1u;
-      mbar_wait(&tfull[a], aph);
+      mbar_wait_spin(&tfull[a], aph);
       tc_fence_after();
       const uint32_t trow = tmem + a * 256 + ((uint32_t)(q * 32) << 16);
       for (int c = 0; c < 256; c += 16) {
@@ -708,7 +646,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
       uint32_t it = 0, tl = 0;
       auto slot_wait = [&](uint32_t bytes) {
         const int st = it % nst;
-        mbar_wait(&empty[st], ((it / nst) & 1u) ^ 1u);
+        mbar_wait_spin(&empty[st], ((it / nst) & 1u) ^ 1u);
         mbar_expect_tx(&full[st], bytes);
         return st;
       };
@@ -721,7 +659,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
           tma_2d(slot, &mapAv, kb * 64, m0, &full[st]);
           tma_2d(slot + 16384, &mapBv, kb * 64, 0, &full[st]);
         }
-        mbar_wait(&a_empty, (tl & 1u) ^ 1u);      // previous tile's MMAs are done with sA
+        mbar_wait_spin(&a_empty, (tl & 1u) ^ 1u);      // previous tile's MMAs are done with sA
         mbar_expect_tx(&a_full, kHeadA);
         for (int kb = 0; kb < 8; ++kb) tma_2d(saddr(sA + kb * 16384), &mapAa, kb * 64, m0, &a_full);
         for (int kb = 0; kb < 16; ++kb, ++it) {    // job mean: hi (rows 0..63) then lo (64..127)
@@ -744,10 +682,10 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
       (void)tile;
       for (int j = 0; j < c_hi - c_lo + 2; ++j, ++job) {   // v, mean, chunks
         const uint32_t b = job & 1u;
-        mbar_wait(&tempty[b], ((job >> 1) & 1u) ^ 1u);
+        mbar_wait_spin(&tempty[b], ((job >> 1) & 1u) ^ 1u);
         tc_fence_after();
         if (j == 1) {
-          mbar_wait(&a_full, tl & 1u);
+          mbar_wait_spin(&a_full, tl & 1u);
           tc_fence_after();
         }
         const int c = c_lo + j - 2;
@@ -756,7 +694,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
         const int nkb = j == 1 ? 16 : 8;
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const int st = it % nst;
-          mbar_wait(&full[st], (it / nst) & 1u);
+          mbar_wait_spin(&full[st], (it / nst) & 1u);
           tc_fence_after();
           const uint32_t slot = saddr(sRing + st * kHeadSlot);
           const uint64_t ad = sdesc<64>(j == 0 ? slot : saddr(sA + (kb & 7) * 16384));
@@ -787,7 +725,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
       uint32_t x[64];
       {   // job v
         const uint32_t b = job & 1u;
-        mbar_wait(&tfull[b], (job >> 1) & 1u);
+        mbar_wait_spin(&tfull[b], (job >> 1) & 1u);
         tc_fence_after();
         tmem_ld64(tmem + b * 256 + lanes, x);
         tc_fence_before();
@@ -798,7 +736,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
       }
       {   // job mean: v_t - mean_a adv[a][t]
         const uint32_t b = job & 1u;
-        mbar_wait(&tfull[b], (job >> 1) & 1u);
+        mbar_wait_spin(&tfull[b], (job >> 1) & 1u);
         tc_fence_after();
         tmem_ld64(tmem + b * 256 + lanes, x);
         tc_fence_before();
@@ -810,7 +748,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
       float best = -INFINITY;
       for (int c = c_lo; c < c_hi; ++c, ++job) {   // softmax expectation per action
         const uint32_t b = job & 1u;
-        mbar_wait(&tfull[b], (job >> 1) & 1u);
+        mbar_wait_spin(&tfull[b], (job >> 1) & 1u);
         tc_fence_after();
         const int na = min(4, A - 4 * c);
         for (int s = grp; s < na; s += 2) {
