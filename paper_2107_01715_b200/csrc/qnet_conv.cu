@@ -711,40 +711,43 @@ constexpr int kC3tOutBytes = 49 * 64 * 2;   // dense act3 [49][64] bf16 of one i
 // 9x9x64 -> 7x7x64). act2 goes from the conv2 epilogue straight into a double-buffered SMEM
 // image in conv3's SW128 layout and never touches HBM.
 //
-// TAP PAIRS. Both convs are written as sums over filter taps t of shifted windows,
+// TAP PAIRS, TRANSPOSED. Both convs are written as sums over filter taps t of shifted windows,
 //   out[q] = sum_t W_t . in[q + s_t]                       (q = full-width output row)
-// and the kernel is bound by the SMEM bytes its MMAs read. One MMA now serves TWO taps that
-// differ by one column (s_b = s_a + 1) and read the SAME window:
-//  * conv2 (A = image rows, M = 128; B = weights): B = [W_a | W_b] (N = 128) over the window at
-//    s_a gives D_L[m] = W_a.in[m + s_a] (a term of out[m]) and D_R[m] = W_b.in[m + s_a] (a term of
-//    out[m - 1]); pairs (0,0|0,1) and (1,0|1,1) keep that offset, so out[q] = D_L[q] + D_R[q + 1]
-//    -- a one-lane shuffle in the epilogue (rows 31 / 63 take row 32 / 64 from the next lane
-//    quarter through SMEM). 16 MMAs of 4 + 4 KB instead of 32 of 4 + 2 KB: 128 instead of 192 KB
-//    of operand reads per image, and the tensor time is unchanged (1,024 cycles).
-//  * conv3 (transposed: A = weights from TMEM, B = act2 window N = 64 image rows): A = [W_a ; W_b]
-//    stacked along M = 128 (lanes 0-63 tap a, lanes 64-127 tap b) over the window at s_a; groups
-//    (ty,0|ty,1) for ty = 0..2 and (ty,2|zero), so D_lo[n] is a term of out[n] and D_hi[n] a term
-//    of out[n - 1]: out[n] = D_lo[n] + D_hi[n + 1]. The upper-half lanes hand their rows to the
-//    lower half through SMEM. 24 M = 128 MMAs (32 cycles each) replace 36 M = 64 MMAs that cost
-//    the same per instruction: 768 instead of 1,152 tensor cycles per image, 48 instead of 72 KB
-//    of B reads. The sums are the same products in another fp32 order (R17/R18).
-// act1 lands in a compact ring (planes of 104 rows instead of act1's 144-row global planes).
-// TMEM: T2 cols 0..127 (single: its epilogue releases it right after tcgen05.ld, while conv3(i-1)
-// keeps the tensor pipe busy), T3[2] cols 128..255 (double: the conv3 epilogue's hand-off and
-// staging take longer than one image's conv3 MMAs), W3 (6 groups x 32 cols) 256..447.
-// Warps: 0 producer, 1 conv2 MMA issuer, 2-9 conv2 epilogue (lane quarter x 32-channel half),
-// 10-13 conv3 epilogue (lane quarter) + the W3 -> TMEM load, 14 conv3 MMA issuer. Two issuing
-// warps: while one waits on its barriers the other keeps the tensor pipe's queue filled.
+// and both run TRANSPOSED: A = the weights, resident in TMEM (lanes = output channels), B = the
+// act image window (N = full-width rows, K-major SW128 in SMEM), so an MMA reads only its
+// B window from SMEM. One M = 128 MMA serves TWO taps a, b that read the SAME window: A =
+// [W_a ; W_b] stacked along M (lanes 0-63 tap a, lanes 64-127 tap b) over the window at s_a gives
+// D_lo[n] = W_a.in[n + s_a] (a term of out[n]) and D_hi[n] = W_b.in[n + s_a] (a term of
+// out[n - (s_b - s_a)]); pairs are chosen with s_b = s_a + 1, so out[n] = D_lo[n] + D_hi[n + 1]:
+// the upper-half lanes hand their rows to the lower half (and back) through SMEM.
+//  * conv2 (2x2/1 over act1's s2d(2) 10x10x128): pairs (ty,0|ty,1), ty = 0, 1 (window s = 10 ty),
+//    N = 96 >= 90 full-width rows + 1, K = 128: 16 MMAs of 48 tensor cycles (768 per image, 84%
+//    of them algorithmic) reading 3 KB of B each (48 KB per image; the image-rows-as-M form
+//    needed 1,024 cycles and 128 KB).
+//  * conv3 (3x3/1 over act2 9x9x64): groups (ty,0|ty,1) for ty = 0..2 and (ty,2|zero), N = 64
+//    >= 63 rows: 24 MMAs of 32 cycles (768 per image), 2 KB of B each.
+// The sums are the same products in another fp32 order (R17/R18).
+// act1 lands in a compact ring (planes of 112 rows instead of act1's 144-row global planes; the
+// conv2 window at row 10 reaches row 105, rows >= 100 only feed discarded columns n >= 90).
+// TMEM (480 of 512 columns): T2 0..95 (single: its epilogue releases it right after tcgen05.ld
+// while conv3(i-1) keeps the tensor pipe busy), W2 96..223 (2 pairs x K = 128 as bf16 pairs),
+// T3 224..287 (single), W3 288..479 (6 groups x 32 columns).
+// Warps: 0 producer, 1 conv2 MMA issuer, 2-9 conv2 epilogue (lane quarter x part) + the W2 ->
+// TMEM load, 10-13 conv3 epilogue (lane quarter) + the W3 -> TMEM load, 14 conv3 MMA issuer. Two
+// issuing warps: while one waits on its barriers the other keeps the tensor pipe's queue filled.
 constexpr int kC23Threads = 480;
-constexpr uint32_t kC23Plane = 104 * 128;                 // compact act1 row block (rows 0..103)
-constexpr uint32_t kC23In = 2 * kC23Plane;                // 26,624 per act1 image
+constexpr uint32_t kC23Plane = 112 * 128;                 // compact act1 row block (rows 0..111)
+constexpr uint32_t kC23In = 2 * kC23Plane;                // 28,672 per act1 image
 constexpr uint32_t kC23A2 = 11 * 1024;                    // act2 image: 84 rows x 128 B, 1 KB aligned
-constexpr int kC23InBufs = 3;                             // act1 ring depth
+constexpr int kC23InBufs = 4;                             // act1 ring depth
 constexpr int kX3Ld = 68;                                 // conv3 hand-off row stride (floats): conflict-free
-constexpr int kC23Smem = 4 * 128 * 128 + kC23InBufs * (int)kC23In + 2 * (int)kC23A2 + 2 * kC3tOutBytes +
-                         64 * kX3Ld * 4 + 2 * 2 * 4 * 32 * 4 + 1024;
-constexpr uint32_t kC23T3Col = 128;                       // T3[2]: columns 128..255
-constexpr uint32_t kC23W3Col = 256;                       // TMEM column of W3 (6 groups x 32 columns)
+constexpr int kX2Ld = 100;                                // conv2 hand-off row stride (floats, = 4 mod 32)
+constexpr int kC23Smem = kC23InBufs * (int)kC23In + 2 * (int)kC23A2 + 2 * kC3tOutBytes + 64 * kX3Ld * 4 +
+                         2 * 64 * kX2Ld * 4 + 1024;
+constexpr uint32_t kC23T2Col = 0;                         // T2: columns 0..95
+constexpr uint32_t kC23W2Col = 96;                        // W2: pair pr at 96 + 64 pr, K-step kk at + 8 kk
+constexpr uint32_t kC23T3Col = 224;                       // T3: columns 224..287
+constexpr uint32_t kC23W3Col = 288;                       // W3: 6 groups x 32 columns
 // conv3 tap groups: lower-half tap (ty, tx) with window offset s = 9 ty + tx; the upper half
 // holds tap (ty, tx + 1) for groups 0-2 and zeros for groups 3-5
 __host__ __device__ constexpr int c3_lo_ty(int g) { return g < 3 ? g : g - 3; }
@@ -756,14 +759,13 @@ __global__ void __launch_bounds__(kC23Threads, 1)
              int64_t n_img, uint8_t *__restrict__ out) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u);
-  uint8_t *sW2 = smem;                                  // conv2 B: 4 k-blocks (pair, 64-channel half) x [128 x 128 B]
-  uint8_t *sIn = sW2 + 4 * 128 * 128;                   // kC23InBufs x act1 (compact planes)
+  uint8_t *sIn = smem;                                  // kC23InBufs x act1 (compact planes)
   uint8_t *sA2 = sIn + kC23InBufs * kC23In;             // 2 x act2
   uint8_t *sO3 = sA2 + 2 * kC23A2;                      // 2 x act3 staging [49][64] bf16
-  float *sX3 = (float *)(sO3 + 2 * kC3tOutBytes);       // conv3 upper-half rows [64][kX3Ld]
-  float *sX2 = sX3 + 64 * kX3Ld;                        // conv2 row hand-off [2 buf][2 half][4 quarter][32]
+  float *sX3 = (float *)(sO3 + 2 * kC3tOutBytes);       // conv3 hand-off rows [64][kX3Ld]
+  float *sX2 = sX3 + 64 * kX3Ld;                        // conv2 hand-off rows [2 buf][64][kX2Ld]
   __shared__ __align__(8) uint64_t in_full[kC23InBufs], in_empty[kC23InBufs], t2full, t2empty, a2full[2],
-      a2empty[2], t3full[2], t3empty[2], w3ready, wbar;
+      a2empty[2], t3full, t3empty, w2ready, w3ready;
   __shared__ uint32_t tmem_slot;
   __shared__ float sb2[64], sb3[64];
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
@@ -782,18 +784,16 @@ __global__ void __launch_bounds__(kC23Threads, 1)
       mbar_init(&in_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&a2full[i], 256);
+      mbar_init(&a2full[i], 128);
       mbar_init(&a2empty[i], 1);
-      mbar_init(&t3full[i], 1);
-      mbar_init(&t3empty[i], 128);
     }
+    mbar_init(&t3full, 1);
+    mbar_init(&t3empty, 128);
     mbar_init(&t2full, 1);
     mbar_init(&t2empty, 256);
+    mbar_init(&w2ready, 256);
     mbar_init(&w3ready, 128);
-    mbar_init(&wbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    mbar_expect_tx(&wbar, 4u * 128 * 128);
-    bulk_g2s(saddr(sW2), W2p, 4u * 128 * 128, &wbar);
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(&tmem_slot)),
@@ -813,7 +813,7 @@ __global__ void __launch_bounds__(kC23Threads, 1)
       for (int li = 0; li < n_my; ++li) {
         const int64_t img = blockIdx.x + (int64_t)li * gridDim.x;
         const uint32_t b = li % kC23InBufs, ph = (li / kC23InBufs) & 1u;
-        mbar_wait(&in_empty[b], ph ^ 1u);
+        mbar_wait_spin(&in_empty[b], ph ^ 1u);
         mbar_expect_tx(&in_full[b], 2u * 12800u);
         for (uint32_t q = 0; q < 2; ++q)
           bulk_g2s(saddr(sIn + b * kC23In) + q * kC23Plane, in + img * (int64_t)P2.in_img_bytes + q * (P2.plane * 8u),
@@ -825,10 +825,10 @@ __global__ void __launch_bounds__(kC23Threads, 1)
     constexpr uint32_t idesc3 = idesc_bf16(128, 64);
     const uint32_t elected = elect_one();
     for (int jj = 0; jj < n_my; ++jj) {
-      if (jj == 0) mbar_wait(&w3ready, 0);   // W3 in TMEM (tcgen05.st by the conv3-epilogue warps)
+      if (jj == 0) mbar_wait_spin(&w3ready, 0);   // W3 in TMEM (tcgen05.st by the conv3-epilogue warps)
       const uint32_t b = jj & 1, ph = (jj >> 1) & 1u;
-      mbar_wait(&a2full[b], ph);
-      mbar_wait(&t3empty[b], ph ^ 1u);
+      mbar_wait_spin(&a2full[b], ph);
+      mbar_wait_spin(&t3empty, (jj & 1u) ^ 1u);
       tc_fence_after();
       const uint64_t xdesc = desc_sw128_win(saddr(sA2 + b * kC23A2), false);
 #pragma unroll
@@ -836,104 +836,131 @@ __global__ void __launch_bounds__(kC23Threads, 1)
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {   // A: group g's K-step kk = W3 columns g * 32 + kk * 8
           const uint32_t x_off = (uint32_t)(c3_lo_ty(g) * 9 + c3_lo_tx(g)) * 128u + (uint32_t)(kk * 32);
-          mma_ts_pred(tmem + kC23T3Col + b * 64, tmem + kC23W3Col + (uint32_t)(g * 32 + kk * 8), xdesc + (x_off >> 4), idesc3,
+          mma_ts_pred(tmem + kC23T3Col, tmem + kC23W3Col + (uint32_t)(g * 32 + kk * 8), xdesc + (x_off >> 4), idesc3,
                       (g | kk) != 0, elected);
         }
       commit_pred(&a2empty[b], elected);
-      commit_pred(&t3full[b], elected);
+      commit_pred(&t3full, elected);
       __syncwarp();
     }
   } else if (warp == 1) {   // ------------------------------------------ conv2 MMA issuer
-    constexpr uint32_t idesc2 = idesc_bf16(128, 128);
+    constexpr uint32_t idesc2 = idesc_bf16(128, 96);
     const uint32_t elected = elect_one();
-    mbar_wait(&wbar, 0);
-    const uint64_t w2desc = desc_sw128(saddr(sW2));
+    mbar_wait_spin(&w2ready, 0);   // W2 in TMEM (tcgen05.st by the conv2-epilogue warps)
     for (int li = 0; li < n_my; ++li) {
-      const uint32_t b = li & 1, ph = (li >> 1) & 1u;
       const uint32_t bi = li % kC23InBufs, phi = (li / kC23InBufs) & 1u;
-      mbar_wait(&in_full[bi], phi);
-      mbar_wait(&t2empty, (li & 1u) ^ 1u);
+      mbar_wait_spin(&in_full[bi], phi);
+      mbar_wait_spin(&t2empty, (li & 1u) ^ 1u);
       tc_fence_after();
-      const uint64_t adesc0 = desc_sw128_win(saddr(sIn + bi * kC23In), false);
+      const uint64_t bdesc0 = desc_sw128_win(saddr(sIn + bi * kC23In), false);
 #pragma unroll
-      for (int pr = 0; pr < 2; ++pr)   // tap pair (pr, 0 | pr, 1): window offset 10 pr
+      for (int pr = 0; pr < 2; ++pr)   // tap pair (pr, 0 | pr, 1): window at row 10 pr
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t a_off = (uint32_t)(kk >> 2) * kC23Plane + (uint32_t)(pr * 10) * 128u + (uint32_t)((kk & 3) * 32);
-          const uint32_t w_off = (uint32_t)(pr * 2 + (kk >> 2)) * (128 * 128) + (uint32_t)((kk & 3) * 32);
-          mma_pred(tmem, adesc0 + (a_off >> 4), w2desc + (w_off >> 4), idesc2, (pr | kk) != 0, elected);
+        for (int kk = 0; kk < 8; ++kk) {   // K-step kk: s2d channels 16 kk .. 16 kk + 15
+          const uint32_t b_off = (uint32_t)(kk >> 2) * kC23Plane + (uint32_t)(pr * 10) * 128u + (uint32_t)((kk & 3) * 32);
+          mma_ts_pred(tmem + kC23T2Col, tmem + kC23W2Col + (uint32_t)(pr * 64 + kk * 8), bdesc0 + (b_off >> 4), idesc2,
+                      (pr | kk) != 0, elected);
         }
       commit_pred(&in_empty[bi], elected);
       commit_pred(&t2full, elected);
       __syncwarp();
     }
   } else if (warp < 10) {   // --------------------------- conv2 epilogue -> act2 in SMEM (SW128)
-    const int q4 = warp & 3, hf = (warp - 2) >> 2, c0 = hf * 32;
-    const int r = q4 * 32 + lane;                       // full-width output row: oy = r / 10, ox = r % 10
-    const int oy = r / 10, ox = r - oy * 10;
-    const bool valid = oy < 9 && ox < 9;
-    const int row = oy * 9 + ox;                        // act2 row
-    float bias_r[32];
+    // lane quarter q: lanes 32 q .. 32 q + 31 = output channel c of tap half (q >= 2); part = which
+    // 48 of T2's 96 columns this warp reads. Lower part 0 finishes rows 0..47 (needs D_hi[1..48]),
+    // upper part 1 rows 48..88 (needs D_lo[48..88]); the other two parts only hand their columns
+    // over: hand-off row of channel c (buffer li & 1): [0, 48) = D_hi[1..48], [48, 89) = D_lo[48..88].
+    const int q = warp & 3, part = (warp - 2) >> 2;
+    const bool upper = q >= 2;
+    const int c = 32 * (q & 1) + lane;
+    const float bc = sb2[c];
+    const uint32_t lanes = (uint32_t)(q * 32) << 16;
+    {   // W2 -> TMEM: lane m = 64 h + c holds output channel c of tap (pr, h), pr = part; K = the s2d
+        // channel in bf16 pairs per column; source = the tap-pair SW128 image (qnet.cu `wpair`)
+      const int m = q * 32 + lane;
+#pragma unroll 1
+      for (int kb = 0; kb < 2; ++kb) {
+        uint32_t r[32];
 #pragma unroll
-    for (int c = 0; c < 32; ++c) bias_r[c] = sb2[c0 + c];
+        for (int j = 0; j < 8; ++j) {
+          const uint4 v4 = __ldg((const uint4 *)(W2p + (size_t)(part * 2 + kb) * (128 * 128) + (size_t)m * 128 +
+                                                 (((j ^ (m & 7)) & 7) << 4)));
+          r[4 * j] = v4.x;
+          r[4 * j + 1] = v4.y;
+          r[4 * j + 2] = v4.z;
+          r[4 * j + 3] = v4.w;
+        }
+        tmem_st32(tmem + lanes + kC23W2Col + (uint32_t)(part * 64 + kb * 32), r);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&w2ready);
+    }
+    auto emit = [&](uint8_t *a2, int n, float x) {   // out2[n] + bias -> ReLU -> bf16 at act2 row (oy, ox)
+      const int oy = n / 10, ox = n % 10;
+      if (oy < 9 && ox < 9) {
+        const int row = oy * 9 + ox;
+        uint16_t hv;
+        asm("cvt.rn.relu.bf16.f32 %0, %1;" : "=h"(hv) : "f"(x + bc));
+        *(uint16_t *)(a2 + row * 128 + ((((c >> 3) ^ row) & 7) << 4) + (c & 7) * 2) = hv;
+      }
+    };
     for (int li = 0; li < n_my; ++li) {
       const uint32_t b = li & 1, ph = (li >> 1) & 1u;
-      mbar_wait(&t2full, li & 1u);
+      mbar_wait_spin(&t2full, li & 1u);
       tc_fence_after();
-      uint32_t v[4][16];   // [0..1]: D_L (this row), [2..3]: D_R (this row)
-      const uint32_t tb = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)c0;
-      tmem_ld16_nw(tb, v[0]);
-      tmem_ld16_nw(tb + 16, v[1]);
-      tmem_ld16_nw(tb + 64, v[2]);
-      tmem_ld16_nw(tb + 80, v[3]);
-      tmem_wait16(v[0]);
-      tmem_wait16(v[1]);
-      tmem_wait16(v[2]);
-      tmem_wait16(v[3]);
+      uint32_t v[48];
+      const uint32_t ta = tmem + lanes + kC23T2Col + (uint32_t)(part * 48);
+      tmem_ld16_nw(ta + 0, *(uint32_t(*)[16])(v + 0));
+      tmem_ld16_nw(ta + 16, *(uint32_t(*)[16])(v + 16));
+      tmem_ld16_nw(ta + 32, *(uint32_t(*)[16])(v + 32));
+      tmem_wait16(*(uint32_t(*)[16])(v + 0));
+      tmem_wait16(*(uint32_t(*)[16])(v + 16));
+      tmem_wait16(*(uint32_t(*)[16])(v + 32));
       tc_fence_before();
       mbar_arrive(&t2empty);
-      // D_R of row r + 1: the next lane, or (lane 31) lane 0 of the next quarter via SMEM
-      float *xw = sX2 + ((b * 2 + hf) * 4 + q4) * 32;
-      if (lane == 0) {
+      float *xrow = sX2 + (b * 64 + c) * kX2Ld;
+      const auto f = [&](int i) { return __uint_as_float(v[i]); };
+      if (upper && part == 0) {          // v = D_hi[0..47] -> xrow[j] = D_hi[j + 1], j < 47
 #pragma unroll
-        for (int c = 0; c < 32; c += 4)
-          *(float4 *)(xw + c) = make_float4(__uint_as_float(v[2 + c / 16][c % 16]), __uint_as_float(v[2 + c / 16][c % 16 + 1]),
-                                            __uint_as_float(v[2 + c / 16][c % 16 + 2]), __uint_as_float(v[2 + c / 16][c % 16 + 3]));
+        for (int j = 0; j < 44; j += 4) *(float4 *)(xrow + j) = make_float4(f(j + 1), f(j + 2), f(j + 3), f(j + 4));
+        xrow[44] = f(45);
+        xrow[45] = f(46);
+        xrow[46] = f(47);
+      } else if (upper) {                // v = D_hi[48..95]
+        xrow[47] = f(0);
+      } else if (part == 1) {            // v = D_lo[48..95] -> xrow[48..88]
+#pragma unroll
+        for (int j = 0; j < 40; j += 4) *(float4 *)(xrow + 48 + j) = make_float4(f(j), f(j + 1), f(j + 2), f(j + 3));
+        xrow[88] = f(40);
       }
       asm volatile("bar.sync 3, 256;" ::: "memory");   // the 8 conv2-epilogue warps
+      if (upper == (part == 1)) {        // the two finishing parts
+        mbar_wait_spin(&a2empty[b], ph ^ 1u);                 // conv3 of image li-2 is done with sA2[b]
+        uint8_t *a2 = sA2 + b * kC23A2;
+        if (!upper) {                    // rows 0..47: own D_lo[n] + D_hi[n + 1]
 #pragma unroll
-      for (int c4 = 0; c4 < 32; c4 += 4) {
-        float4 t = make_float4(0.f, 0.f, 0.f, 0.f);     // lane 31: quarter q4 + 1's row 0 (q4 < 3)
-        if (lane == 31 && q4 < 3) t = *(const float4 *)(xw + 32 + c4);
-        const float tn[4] = {t.x, t.y, t.z, t.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int c = c4 + e;
-          float nx = __shfl_down_sync(0xffffffffu, __uint_as_float(v[2 + c / 16][c % 16]), 1);
-          if (lane == 31) nx = tn[e];
-          v[c / 16][c % 16] = __float_as_uint(__uint_as_float(v[c / 16][c % 16]) + nx);
-        }
-      }
-      mbar_wait(&a2empty[b], ph ^ 1u);                  // conv3 of image li-2 is done with sA2[b]
-      if (valid) {
-        uint8_t *dst = sA2 + b * kC23A2 + row * 128;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          uint32_t pk[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e)
-            pk[e] = bf16x2_relu(__uint_as_float(v[h][2 * e]) + bias_r[h * 16 + 2 * e],
-                                __uint_as_float(v[h][2 * e + 1]) + bias_r[h * 16 + 2 * e + 1]);
-#pragma unroll
-          for (int h2 = 0; h2 < 2; ++h2) {
-            const int chunk = (c0 + h * 16 + 8 * h2) >> 3;
-            *(uint4 *)(dst + (((chunk & 7) ^ (row & 7)) << 4)) =
-                make_uint4(pk[4 * h2], pk[4 * h2 + 1], pk[4 * h2 + 2], pk[4 * h2 + 3]);
+          for (int n4 = 0; n4 < 48; n4 += 4) {
+            const float4 t = *(const float4 *)(xrow + n4);
+            emit(a2, n4, f(n4) + t.x);
+            emit(a2, n4 + 1, f(n4 + 1) + t.y);
+            emit(a2, n4 + 2, f(n4 + 2) + t.z);
+            emit(a2, n4 + 3, f(n4 + 3) + t.w);
           }
+        } else {                         // rows 48..88: D_lo[n] + own D_hi[n + 1] (= v[n - 47])
+#pragma unroll
+          for (int n4 = 48; n4 < 88; n4 += 4) {
+            const float4 t = *(const float4 *)(xrow + n4);
+            emit(a2, n4, t.x + f(n4 - 47));
+            emit(a2, n4 + 1, t.y + f(n4 - 46));
+            emit(a2, n4 + 2, t.z + f(n4 - 45));
+            emit(a2, n4 + 3, t.w + f(n4 - 44));
+          }
+          emit(a2, 88, xrow[88] + f(41));
         }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&a2full[b]);
       }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive(&a2full[b]);
     }
   } else {   // ------------------------------------------- conv3 epilogue -> act3 (dense), warps 10-13
     const int q = warp & 3;                 // TMEM lane quarter; q < 2: tap a (lower half), q >= 2: tap b
@@ -960,16 +987,9 @@ __global__ void __launch_bounds__(kC23Threads, 1)
           r[4 * ch + 2] = v4.z;
           r[4 * ch + 3] = v4.w;
         }
-        asm volatile(
-            "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
-            "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(
-                tmem + ((uint32_t)(q * 32) << 16) + kC23W3Col + (uint32_t)(g * 32)),
-            "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
-            "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
-            "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
-            "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
+        tmem_st32(tmem + ((uint32_t)(q * 32) << 16) + kC23W3Col + (uint32_t)(g * 32), r);
       }
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&w3ready);
     }
@@ -979,11 +999,11 @@ __global__ void __launch_bounds__(kC23Threads, 1)
     float *xrow = sX3 + c * kX3Ld;
     for (int li = 0; li < n_my; ++li) {
       const int64_t img = blockIdx.x + (int64_t)li * gridDim.x;
-      const uint32_t b = li & 1, ph = (li >> 1) & 1u;
-      mbar_wait(&t3full[b], ph);
+      const uint32_t b = li & 1;
+      mbar_wait_spin(&t3full, li & 1u);
       tc_fence_after();
       uint32_t v[64];
-      const uint32_t ta = taddr0 + b * 64;
+      const uint32_t ta = taddr0;
       tmem_ld16_nw(ta + 0, *(uint32_t(*)[16])(v + 0));
       tmem_ld16_nw(ta + 16, *(uint32_t(*)[16])(v + 16));
       tmem_ld16_nw(ta + 32, *(uint32_t(*)[16])(v + 32));
@@ -993,7 +1013,7 @@ __global__ void __launch_bounds__(kC23Threads, 1)
       tmem_wait16(*(uint32_t(*)[16])(v + 32));
       tmem_wait16(*(uint32_t(*)[16])(v + 48));
       tc_fence_before();
-      mbar_arrive(&t3empty[b]);
+      mbar_arrive(&t3empty);
       if (upper) {
 #pragma unroll
         for (int n = 0; n < 36; n += 4)
