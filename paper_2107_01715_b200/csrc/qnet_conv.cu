@@ -727,8 +727,9 @@ constexpr int kC3tOutBytes = 49 * 64 * 2;   // dense act3 [49][64] bf16 of one i
 //  * conv3 (3x3/1 over act2 9x9x64): groups (ty,0|ty,1) for ty = 0..2 and (ty,2|zero), N = 64
 //    >= 63 rows: 24 MMAs of 32 cycles (768 per image), 2 KB of B each.
 // The sums are the same products in another fp32 order (R17/R18).
-// act1 lands in a compact ring (planes of 112 rows instead of act1's 144-row global planes; the
-// conv2 window at row 10 reaches row 105, rows >= 100 only feed discarded columns n >= 90).
+// act1 lands in a compact 5-deep ring (planes of 104 rows instead of act1's 144-row global planes;
+// the conv2 window at row 10 reaches row 105, but rows >= 100 only feed discarded columns n >= 90,
+// so a window may run into the next plane or buffer).
 // TMEM (480 of 512 columns): T2 0..95 (single: its epilogue releases it right after tcgen05.ld
 // while conv3(i-1) keeps the tensor pipe busy), W2 96..223 (2 pairs x K = 128 as bf16 pairs),
 // T3 224..287 (single), W3 288..479 (6 groups x 32 columns).
@@ -736,14 +737,14 @@ constexpr int kC3tOutBytes = 49 * 64 * 2;   // dense act3 [49][64] bf16 of one i
 // TMEM load, 10-13 conv3 epilogue (lane quarter) + the W3 -> TMEM load, 14 conv3 MMA issuer. Two
 // issuing warps: while one waits on its barriers the other keeps the tensor pipe's queue filled.
 constexpr int kC23Threads = 480;
-constexpr uint32_t kC23Plane = 112 * 128;                 // compact act1 row block (rows 0..111)
-constexpr uint32_t kC23In = 2 * kC23Plane;                // 28,672 per act1 image
+constexpr uint32_t kC23Plane = 104 * 128;                 // compact act1 row block (rows 0..103)
+constexpr uint32_t kC23In = 2 * kC23Plane;                // 26,624 per act1 image
 constexpr uint32_t kC23A2 = 11 * 1024;                    // act2 image: 84 rows x 128 B, 1 KB aligned
-constexpr int kC23InBufs = 4;                             // act1 ring depth
+constexpr int kC23InBufs = 5;                             // act1 ring depth (HBM latency: 4 images in flight)
 constexpr int kX3Ld = 68;                                 // conv3 hand-off row stride (floats): conflict-free
-constexpr int kX2Ld = 100;                                // conv2 hand-off row stride (floats, = 4 mod 32)
+constexpr int kX2Ld = 92;                                 // conv2 hand-off row stride (floats, = 4 mod 8)
 constexpr int kC23Smem = kC23InBufs * (int)kC23In + 2 * (int)kC23A2 + 2 * kC3tOutBytes + 64 * kX3Ld * 4 +
-                         2 * 64 * kX2Ld * 4 + 1024;
+                         64 * kX2Ld * 4 + 1024;
 constexpr uint32_t kC23T2Col = 0;                         // T2: columns 0..95
 constexpr uint32_t kC23W2Col = 96;                        // W2: pair pr at 96 + 64 pr, K-step kk at + 8 kk
 constexpr uint32_t kC23T3Col = 224;                       // T3: columns 224..287
@@ -763,7 +764,7 @@ __global__ void __launch_bounds__(kC23Threads, 1)
   uint8_t *sA2 = sIn + kC23InBufs * kC23In;             // 2 x act2
   uint8_t *sO3 = sA2 + 2 * kC23A2;                      // 2 x act3 staging [49][64] bf16
   float *sX3 = (float *)(sO3 + 2 * kC3tOutBytes);       // conv3 hand-off rows [64][kX3Ld]
-  float *sX2 = sX3 + 64 * kX3Ld;                        // conv2 hand-off rows [2 buf][64][kX2Ld]
+  float *sX2 = sX3 + 64 * kX3Ld;                        // conv2 hand-off rows [64][kX2Ld]
   __shared__ __align__(8) uint64_t in_full[kC23InBufs], in_empty[kC23InBufs], t2full, t2empty, a2full[2],
       a2empty[2], t3full, t3empty, w2ready, w3ready;
   __shared__ uint32_t tmem_slot;
@@ -871,7 +872,7 @@ __global__ void __launch_bounds__(kC23Threads, 1)
     // upper part 1 rows 48..88 (needs D_lo[48..88]); the other two parts only hand their columns
     // over: hand-off row of channel c (buffer li & 1): [0, 48) = D_hi[1..48], [48, 89) = D_lo[48..88].
     const int q = warp & 3, part = (warp - 2) >> 2;
-    const bool upper = q >= 2;
+    const bool upper = q >= 2, reader_only = !upper && part == 0;
     const int c = 32 * (q & 1) + lane;
     const float bc = sb2[c];
     const uint32_t lanes = (uint32_t)(q * 32) << 16;
@@ -919,8 +920,11 @@ __global__ void __launch_bounds__(kC23Threads, 1)
       tmem_wait16(*(uint32_t(*)[16])(v + 32));
       tc_fence_before();
       mbar_arrive(&t2empty);
-      float *xrow = sX2 + (b * 64 + c) * kX2Ld;
+      float *xrow = sX2 + c * kX2Ld;
       const auto f = [&](int i) { return __uint_as_float(v[i]); };
+      // single hand-off buffer: the writers of image li wait (barrier 4) until lower part 0 has
+      // read image li-1's rows (it arrives without waiting); upper part 1 reads before it writes
+      if (!reader_only && li > 0) asm volatile("bar.sync 4, 256;" ::: "memory");
       if (upper && part == 0) {          // v = D_hi[0..47] -> xrow[j] = D_hi[j + 1], j < 47
 #pragma unroll
         for (int j = 0; j < 44; j += 4) *(float4 *)(xrow + j) = make_float4(f(j + 1), f(j + 2), f(j + 3), f(j + 4));
@@ -958,6 +962,7 @@ __global__ void __launch_bounds__(kC23Threads, 1)
           }
           emit(a2, 88, xrow[88] + f(41));
         }
+        if (reader_only && li + 1 < n_my) asm volatile("bar.arrive 4, 256;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive(&a2full[b]);
       }
