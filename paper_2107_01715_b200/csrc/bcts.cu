@@ -416,6 +416,7 @@ bcts_status run_shard(bcts_handle h, const void *roots, int32_t d, float gamma, 
     } else {
       nl = net_eval(h->net, prev, Le - L, MODE_TOTAL, g[d], totals, h->st);
     }
+    if (nl < 0) return fail(h, BCTS_ERR_CUDA, "net_eval (leaf chunk)");
     if (!folded) launch_segmax(totals, Le - L, L, pw[d], pw[d - 1], A, keys, h->st, &h->prof);
     h->launches += expanded + nl + (folded ? 0 : 1);
     ++nchunks;
@@ -1409,8 +1410,8 @@ bcts_status bcts_profile_enable(bcts_handle h, int32_t on) {
 int32_t bcts_profile_read(bcts_handle h, bcts_kernel_profile *out, int32_t max) {
   static const char *names[KC_COUNT] = {"expand_atari", "expand_int", "expand_tabular", "conv1", "conv2", "conv3",
                                         "fc_hidden", "fc_out", "head", "mlp", "table", "segmax", "finalize", "other",
-                                        "expand_dnn", "conv2+conv3", "prune"};
-  static const int units[KC_COUNT] = {0, 0, 0, 1, 1, 1, 1, 1, 0, 1, 0, 0, 0, 0, 1, 1, 0};
+                                        "expand_dnn", "conv2+conv3", "prune", "comm"};
+  static const int units[KC_COUNT] = {0, 0, 0, 1, 1, 1, 1, 1, 0, 1, 0, 0, 0, 0, 1, 1, 0, 0};
   if (!h || !out || max <= 0) return 0;
   cudaSetDevice(h->dev);
   cudaStreamSynchronize(h->st);
