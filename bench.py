@@ -266,6 +266,8 @@ def main():
     ap.add_argument("--roots", type=int, default=0, help="override n_roots (throughput variants)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--simt", action="store_true", help="SIMT reference net (no tensor cores)")
+    ap.add_argument("--tf32", action="store_true",
+                    help="BCTS_F_TF32: DNN forward model / MLP2 on tcgen05 kind::tf32 (within the tf32 tolerance)")
     ap.add_argument("--no-flush", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -287,7 +289,7 @@ def main():
     from paper_2107_01715_b200.parallel import world_handle
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    flags = P.F_SIMT_NET if args.simt else 0
+    flags = (P.F_SIMT_NET if args.simt else 0) | (P.F_TF32 if args.tf32 else 0)
     # world > 1: every rank's handle owns an NCCL communicator (id made on rank 0, broadcast); the
     # search is then collective inside the library: each rank scores its leaf range and one
     # ncclAllReduce(MAX) of the packed root keys runs on the handle's stream
@@ -378,17 +380,21 @@ def main():
         if v["unit"] == "byte":
             peak, unit, bound = peaks["hbm_gbs"], "GB/s", "hbm"
             psrc = peaks["source"] + " burst"
-        elif args.simt or name in FP32_CLASSES:
+        elif args.simt or (name in FP32_CLASSES and not args.tf32):
             peak, unit, bound = peaks["fp32_tflops"], "TFLOP/s", "alu"
             psrc = f"derived: 148 SMs x 128 FP32 FMA lanes x 2 x {peaks['sm_max_mhz']:.0f} MHz"
         else:
             peak = peaks["bf16_tflops_sustained"] if long_run else peaks["bf16_tflops"]
             unit, bound = "TFLOP/s", "tensor"
             psrc = peaks["source"] + (" sustained" if long_run else " burst")
+            if args.tf32 and name in FP32_CLASSES:   # kind::tf32 runs at half the bf16 rate (nominal ratio)
+                peak *= 0.5
+                psrc += " bf16 peak x 0.5 (tf32)"
         ach = kernels[name]["achieved"]
         # nominal denominators beside the measured ones: 2.25 PFLOP/s dense bf16,
         # 8 TB/s HBM3e; the ALU peak is already the nominal unit count x clock
-        nominal = {"tensor": 2250.0, "hbm": 8000.0, "alu": peaks["fp32_tflops"]}[bound]
+        nominal = {"tensor": 1125.0 if (args.tf32 and name in FP32_CLASSES) else 2250.0, "hbm": 8000.0,
+                   "alu": peaks["fp32_tflops"]}[bound]
         roofline = {"kernel": name, "bound": bound, "achieved": ach, "peak": peak, "unit": unit,
                     "frac": ach / peak, "traffic": None,
                     "work_per_launch": v["work"] / max(v["launches"], 1), "peak_source": psrc,
@@ -441,7 +447,7 @@ def main():
     if rank == 0:
         line = {"metric": metric_of(cfg), "value": value, "unit": "nodes/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": dtype_of(cfg), "data": "synthetic",
+                "scaling": "strong", "vs_baseline": None, "dtype": "tf32" if (args.tf32 and cfg.net not in (3, 4)) else dtype_of(cfg), "data": "synthetic",
                 "decisions_per_s": n / (step_ms / 1e3),
                 "config": {"workload": workload_of(cfg, n),
                            "roots": n, "depth": d, "A": A, "nodes_per_decision": exp + ev,
@@ -449,7 +455,7 @@ def main():
                                            f"{n * A} packed root keys inside the library") if world > 1
                            else "single GPU",
                            "l2": "flushed before every timed step (256 MiB write, untimed)" if flush is not None
-                           else "not flushed", "net_path": "simt" if args.simt else "tcgen05"},
+                           else "not flushed", "net_path": "simt" if args.simt else ("tcgen05 tf32" if args.tf32 else "tcgen05")},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches_per_step[0] * args.steps,
                 "clocks": clk.summary(), "kernels": kernels}

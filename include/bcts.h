@@ -101,6 +101,11 @@ typedef enum {
                                        * own net launches instead of inside the last leaf batch; same
                                        * result bit for bit */
 #define BCTS_F_NO_GRAPH 0x20u        /* never replay CUDA graphs (bcts_search_host, bcts_search_ex) */
+#define BCTS_F_TF32 0x40u /* NEXT-1 on the tensor cores: the DNN forward model (BCTS_ENV_DNN) and the MLP2
+                           * net run as tcgen05 kind::tf32 GEMMs (operands rounded to tf32, fp32
+                           * accumulation in the MMA's order). NOT bit-exact with the fp32 default:
+                           * within the tf32 tolerance of the fp64 oracle (R34). Other
+                           * envs / nets ignore it. */
 
 typedef struct {
   uint32_t abi_version;     /* must be BCTS_ABI_VERSION */

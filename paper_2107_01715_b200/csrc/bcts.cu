@@ -5,6 +5,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <map>
 #include <mutex>
 #include <new>
 #include <set>
@@ -24,6 +25,7 @@ struct bcts_handle_t {
   uint32_t flags = 0;
   int32_t *d_next = nullptr;
   float *d_envw = nullptr;   // DNN env image (dnn_repack)
+  float *d_envw_tc = nullptr;   // DNN env image of the tf32 tensor-core path (dnn_tc_repack)
   EnvModel em;
   float *d_rew = nullptr;
   Net net;
@@ -111,14 +113,17 @@ int sm_count_current() {
   return n;
 }
 cudaError_t smem_optin(const void *kernel, int bytes) {
+  // the attribute is an upper bound: keep the largest size any launch of (kernel, device) asked for
+  // (setting a smaller one after a larger one would break the larger launches)
   static std::mutex mu;
-  static std::set<std::tuple<const void *, int, int>> done;
+  static std::map<std::pair<const void *, int>, int> set_to;
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lock(mu);
-  if (done.count(std::make_tuple(kernel, dev, bytes))) return cudaSuccess;
+  int &cur = set_to[std::make_pair(kernel, dev)];
+  if (bytes <= cur) return cudaSuccess;
   const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (e == cudaSuccess) done.insert(std::make_tuple(kernel, dev, bytes));
+  if (e == cudaSuccess) cur = bytes;
   return e;
 }
 }  // namespace bcts
@@ -862,6 +867,7 @@ void bcts_destroy(bcts_handle h) {
   if (h->gst) cudaStreamDestroy(h->gst);
   cudaFree(h->d_next);
   cudaFree(h->d_envw);
+  cudaFree(h->d_envw_tc);
   cudaFree(h->d_rew);
   if (h->ws_own) cudaFree(h->ws);
   cudaFree(h->scratch_own);
@@ -934,6 +940,21 @@ bcts_status bcts_create(const bcts_config *cfg, bcts_handle *out) {
       return BCTS_ERR_CUDA;
     }
     h->em.dnn = h->d_envw;
+    if (cfg->flags & BCTS_F_TF32) {
+      if (!dnn_tc_ok(cfg->num_actions)) {
+        bcts_destroy(h);
+        return BCTS_ERR_INVALID_ARG;
+      }
+      std::vector<float> tc(dnn_tc_image_floats(cfg->num_actions));
+      dnn_tc_repack(cfg->env_weights, cfg->num_actions, tc.data());
+      if (cudaMalloc(&h->d_envw_tc, tc.size() * 4) != cudaSuccess ||
+          cudaMemcpy(h->d_envw_tc, tc.data(), tc.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaGetLastError();
+        bcts_destroy(h);
+        return BCTS_ERR_CUDA;
+      }
+      h->em.dnn_tc = h->d_envw_tc;
+    }
   }
   std::string err;
   if (net_build(h->net, *cfg, err)) {   // weight validation and repacking (no scratch yet)

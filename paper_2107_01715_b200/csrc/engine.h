@@ -82,6 +82,7 @@ struct EnvModel {
   const int32_t *tab_next = nullptr;  // TABULAR [nS*A]
   const float *tab_rew = nullptr;     // TABULAR [nS*A]
   const float *dnn = nullptr;         // DNN: smem image (kDnnImg floats) followed by W1A [A][100]
+  const float *dnn_tc = nullptr;      // DNN, BCTS_F_TF32: the k_dnn_tc image (tf32_tc.cu)
 };
 constexpr int kDnnS = 100;                         // DNN state width
 constexpr int kDnnImg = 3 * 10000 + 10400 + 404;   // W1T|W2T|W3T|W4T[100][104]|b1|b2|b3|b4[104] floats
@@ -94,6 +95,18 @@ void launch_expand(int env, const NodeView &par, int64_t p_first, int64_t c_begi
 // ffma_tiles.cu: fixed-order fp32 FMA kernels (DNN forward model, tiled MLP2)
 void launch_expand_dnn(const NodeView &par, int64_t p_first, int64_t c_begin, int64_t c_end, int A, float gk,
                        const float *img, const NodeOut &out, cudaStream_t st, Profiler *prof);
+// tf32_tc.cu: the same two nets on the tensor cores (kind::tf32, opt-in BCTS_F_TF32)
+size_t dnn_tc_image_floats(int A);
+void dnn_tc_repack(const float *blob, int A, float *out);
+bool dnn_tc_ok(int A);
+void launch_expand_dnn_tc(const NodeView &par, int64_t p_first, int64_t c_begin, int64_t c_end, int A, float gk,
+                          const float *img, const NodeOut &out, cudaStream_t st, Profiler *prof);
+size_t mlp_tc_image_bytes(int I, int H, int A);
+bool mlp_tc_ok(int I, int H, int A);
+void mlp_tc_repack(const float *w1, const float *b1, const float *w2, const float *b2, int I, int H, int A,
+                   uint8_t *out);
+void launch_mlp_tc(const NodeView &v, int64_t n, const uint8_t *img, int I, int H, int A, int mode, float gd,
+                   float *out, int feat_f32, cudaStream_t st);
 int mlp_image_floats(int I, int H, int A);
 void mlp_repack(const float *w1, const float *b1, const float *w2, const float *b2, int I, int H, int A, float *out);
 bool mlp_tiled_ok(int I, int H, int A);
@@ -227,6 +240,7 @@ struct Net {
   int in = 0, hid = 0;
   int feat_f32 = 0;               // DNN env: features are the fp32 state itself
   const float *mlp_img = nullptr; // tiled-MLP smem image (mlp_repack), null = warp-per-state kernel
+  const uint8_t *mlp_tc_img = nullptr;  // BCTS_F_TF32: the k_mlp_tc image (tf32_tc.cu)
   // conv nets
   Layer c1, c2, c3, fc_h, z_v, z_a, fc2;
   int atoms = 51;

@@ -372,6 +372,16 @@ int net_build(Net &net, const bcts_config &cfg, std::string &err) {
       if (upload(net, img.data(), img.size() * sizeof(float), &d) != cudaSuccess) { err = "upload MLP image"; return -1; }
       net.mlp_img = (const float *)d;
     }
+    if (cfg.flags & BCTS_F_TF32) {
+      if (!mlp_tc_ok(I, H, A)) { err = "BCTS_F_TF32: MLP2 needs mlp_hidden % 16 == 0, <= 256 and A <= 64"; return -1; }
+      std::vector<uint8_t> img(mlp_tc_image_bytes(I, H, A));
+      const float *c = cfg.weights;
+      mlp_tc_repack(c, c + (size_t)H * I, c + (size_t)H * I + H, c + (size_t)H * I + H + (size_t)A * H, I, H, A,
+                    img.data());
+      void *d;
+      if (upload(net, img.data(), img.size(), &d) != cudaSuccess) { err = "upload tf32 MLP image"; return -1; }
+      net.mlp_tc_img = (const uint8_t *)d;
+    }
     return 0;
   }
   const bool rainbow = cfg.net == BCTS_NET_RAINBOW_BF16;
@@ -853,6 +863,11 @@ int net_eval(Net &net, const NodeView &v, int64_t n, int mode, float gd, float *
   }
   if (net.kind == BCTS_NET_MLP2_F32) {
     if (net.prof) net.prof->begin(KC_MLP, 2.0 * (double)n * ((double)net.in * net.hid + (double)net.hid * A), st);
+    if (net.mlp_tc_img) {
+      launch_mlp_tc(v, n, net.mlp_tc_img, net.in, net.hid, A, mode, gd, out, net.feat_f32, st);
+      if (net.prof) net.prof->end(st);
+      return 1;
+    }
     if (net.mlp_img) {
       launch_mlp_tiled(v, n, net.mlp_img, net.in, net.hid, A, mode, gd, out, net.feat_f32, st);
       if (net.prof) net.prof->end(st);

@@ -1,0 +1,463 @@
+// tf32_tc.cu -- NEXT-1 on the tensor cores (opt-in, BCTS_F_TF32): the random-DNN forward model
+// (level expansion, Alg. 1 P:318-321 with the learned model of P:340-341, R27) and the
+// MLP2 leaf net as tcgen05 kind::tf32 GEMMs with TMEM-resident activations.
+//
+// The default fp32 kernels (ffma_tiles.cu) reproduce the oracle's fmaf chains bit for bit; this
+// path trades that for the tensor pipe: operands are rounded to tf32 (10-bit mantissa, round to
+// nearest, ties away) and accumulated in fp32 in the MMA's own order, so results are compared with
+// the fp64 oracle within the tolerance derived in DESIGN.md R34.
+//
+// Both kernels keep a 128-node tile's activations in TMEM as the A operand of the next layer:
+//   D (fp32, lanes = nodes, columns = units) --tcgen05.ld--> bias / ReLU / tf32 rounding in
+//   registers --tcgen05.st--> A columns (lanes = nodes, columns = inputs)
+// so no activation touches shared or global memory between layers. The weights of every layer
+// are resident in SMEM (one bulk copy per CTA) as K-major SWIZZLE_NONE tf32 images:
+//   byte(n, k) = (k / 4) * (Npad * 16) + n * 16 + (k % 4) * 4
+// (8-row x 16-byte core matrices; LBO = one 4-wide K chunk = Npad * 16 B, SBO = 128 B); an MMA
+// (K = 8) reads two chunks.
+#include <algorithm>
+#include <vector>
+
+#include "engine.h"
+#include "ptx.cuh"
+
+namespace bcts {
+namespace {
+
+constexpr int kTcThreadsDnn = 384;   // warp 0 MMA issuer; warps 4-7 / 8-11: epilogue of tile slot 0 / 1
+constexpr int kTcThreadsMlp = 256;   // warp 0 MMA issuer; warps 4-7: epilogue
+constexpr int kTcK = 104;            // DNN state width 100 padded to a multiple of 8 (tf32 MMA K)
+constexpr int kTcN = 112;            // DNN layer outputs (100, or 101 for the last) padded to 16
+constexpr uint32_t kTcPlane = kTcN * 16;                       // one 4-wide K chunk of a DNN layer
+constexpr uint32_t kTcLayerBytes = (kTcK / 4) * kTcPlane;      // 46,592 B per DNN layer image
+constexpr int kTcDnnFloats = (int)(4 * kTcLayerBytes / 4) + 4 * kTcN;   // 4 layers + biases [4][112]
+
+// K-major SWIZZLE_NONE descriptor: LBO = K-chunk stride, SBO = 8-row-group stride (128 B).
+__device__ __forceinline__ uint64_t desc_kmajor(uint32_t addr, uint32_t plane_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)((plane_bytes >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)(128 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  return d;
+}
+// kind::tf32: c_format F32, a_format = b_format = TF32 (2), K-major A and B
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+// D[tmem] (+)= A[tmem] x B[smem]^T, kind::tf32, issued by the elected lane of a converged warp
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc,
+                                            uint32_t issue) {
+  asm volatile(
+      "{\n.reg .pred p, q;\nsetp.ne.b32 p, %4, 0;\nsetp.ne.b32 q, %5, 0;\n"
+      "@q tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc), "r"(issue));
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+// fp32 -> tf32 (round to nearest, ties away from zero; low 13 bits cleared)
+__device__ __forceinline__ uint32_t tf32_bits(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+// one bulk copy per 32 KB piece (the whole image completes `bar`)
+__device__ __forceinline__ void load_weights(uint8_t *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  mbar_expect_tx(bar, bytes);
+  for (uint32_t o = 0; o < bytes; o += 32768u)
+    bulk_g2s(saddr(dst + o), (const uint8_t *)src + o, min(32768u, bytes - o), bar);
+}
+
+// ------------------------------------------------------------------ DNN forward model, one level
+// Tile = 128 children (child c: parent c / A, action c % A, R1). Per tile and slot s (two tiles
+// in flight, one per epilogue warpgroup): A0 = the parent's state (100 -> 104 columns, tf32) ->
+// L1 = relu(W1s.s + W1[:, 100 + a] + b1) -> L2, L3 = relu(W.h + b) -> L4 = W4.h + b4: units
+// 0..99 = s', unit 100 = r; R' = fmaf(gk, r, R). The action part of layer 1 is the one-hot column
+// W1[:, 100 + a], added in fp32 in the epilogue (exact: the one-hot product is the weight itself).
+// TMEM per slot s: A at columns 256 s .. +104, D at 256 s + 128 .. +112.
+__global__ void __launch_bounds__(kTcThreadsDnn, 1)
+    k_dnn_tc(NodeView par, int64_t p_first, int64_t c_begin, int64_t c_end, int A, float gk,
+             const float *__restrict__ img, NodeOut out) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = smem_raw + ((128u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 127u)) & 127u);
+  const float *sB = (const float *)(smem + 4 * kTcLayerBytes);   // biases [4][112]
+  const float *sW1A = sB + 4 * kTcN;                               // one-hot columns [A][100]
+  __shared__ __align__(8) uint64_t wbar, a_ready[2], d_full[2];
+  __shared__ uint32_t tmem_slot;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    mbar_init(&wbar, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&a_ready[s], 128);
+      mbar_init(&d_full[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    load_weights(smem, img, (uint32_t)(kTcDnnFloats + A * kDnnS) * 4u, &wbar);
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(&tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+  const int64_t n = c_end - c_begin, ntiles = (n + 127) / 128;
+
+  if (warp == 0) {   // ---------------------------------------------------------- MMA issuer
+    constexpr uint32_t idesc = idesc_tf32(128, kTcN);
+    const uint32_t elected = elect_one();
+    mbar_wait(&wbar, 0);
+    const uint32_t wbase = saddr(smem);
+    // tiles in pairs (slot 0: t, slot 1: t + grid), layers interleaved across the pair so one
+    // slot's MMAs run while the other slot's epilogue works. Each slot's barriers complete four
+    // times per tile, so the parity of layer L's wait is L & 1.
+    for (int64_t t0 = blockIdx.x; t0 < ntiles; t0 += 2 * (int64_t)gridDim.x) {
+      const int nslot = t0 + gridDim.x < ntiles ? 2 : 1;
+      for (int L = 0; L < 4; ++L)
+        for (int s = 0; s < nslot; ++s) {
+          mbar_wait(&a_ready[s], (uint32_t)L & 1u);
+          tc_fence_after();
+          const uint32_t tA = tmem + 256u * s, tD = tA + 128u;
+#pragma unroll
+          for (int kk = 0; kk < kTcK / 8; ++kk)
+            mma_tf32_ts(tD, tA + 8u * kk,
+                        desc_kmajor(wbase + (uint32_t)L * kTcLayerBytes + (uint32_t)(2 * kk) * kTcPlane, kTcPlane),
+                        idesc, kk != 0, elected);
+          commit_pred(&d_full[s], elected);
+          __syncwarp();
+        }
+    }
+  } else if (warp >= 4) {   // ------------------------------------------ epilogue, slot s
+    const int s = (warp - 4) >> 2, q = warp & 3, m = q * 32 + lane;
+    const uint32_t tA = tmem + ((uint32_t)(q * 32) << 16) + 256u * s, tD = tA + 128u;
+    for (int64_t t = blockIdx.x + (int64_t)s * gridDim.x; t < ntiles; t += 2 * (int64_t)gridDim.x) {
+      const int64_t c = c_begin + t * 128 + m;
+      const bool valid = c < c_end;
+      const int64_t p = valid ? c / A : c_begin / A;
+      const int a = valid ? (int)(c - p * A) : 0;
+      // A0: the parent's state, rounded to tf32; columns 100..103 and invalid rows are zero
+      {
+        const float4 *ps = (const float4 *)(par.state + (p - p_first) * par.state_stride);
+#pragma unroll
+        for (int j0 = 0; j0 < kTcK; j0 += 32) {
+          uint32_t r[32];
+#pragma unroll
+          for (int e = 0; e < 32; e += 4) {
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (valid && j0 + e < kDnnS) v = __ldg(ps + (j0 + e) / 4);
+            r[e] = tf32_bits(v.x);
+            r[e + 1] = tf32_bits(v.y);
+            r[e + 2] = tf32_bits(v.z);
+            r[e + 3] = tf32_bits(v.w);
+          }
+          if (j0 + 32 <= kTcK) {
+            tmem_st32(tA + (uint32_t)j0, r);
+          } else {
+            const uint32_t r8[8] = {r[0], r[1], r[2], r[3], r[4], r[5], r[6], r[7]};
+            tmem_st8(tA + (uint32_t)j0, r8);
+          }
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&a_ready[s]);
+      }
+      const float rpar = valid && par.cum ? par.cum[p - p_first] : 0.0f;
+      float *srow = (float *)(out.state + (valid ? c - c_begin : 0) * out.state_stride);
+      for (int L = 0; L < 4; ++L) {
+        mbar_wait(&d_full[s], (uint32_t)L & 1u);
+        tc_fence_after();
+        const float *b = sB + L * kTcN;
+#pragma unroll
+        for (int j0 = 0; j0 < kTcN; j0 += 16) {
+          uint32_t v[16];
+          tmem_ld16_nw(tD + (uint32_t)j0, v);
+          tmem_wait16(v);
+          if (L < 3) {   // hidden layer: relu(D + b (+ W1[:, 100 + a])) -> tf32 -> A columns j0..
+            uint32_t r[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const int u = j0 + e;
+              float x = 0.0f;
+              if (u < kDnnS) {
+                x = __uint_as_float(v[e]) + b[u];
+                if (L == 0) x += sW1A[a * kDnnS + u];
+                x = fmaxf(x, 0.0f);
+              }
+              r[e] = tf32_bits(x);
+            }
+            if (j0 + 16 <= kTcK) {
+              const uint32_t(&lo)[8] = *(const uint32_t(*)[8])r;
+              const uint32_t(&hi)[8] = *(const uint32_t(*)[8])(r + 8);
+              tmem_st8(tA + (uint32_t)j0, lo);
+              tmem_st8(tA + (uint32_t)j0 + 8u, hi);
+            } else if (j0 < kTcK) {
+              const uint32_t(&lo)[8] = *(const uint32_t(*)[8])r;
+              tmem_st8(tA + (uint32_t)j0, lo);
+            }
+          } else if (valid) {   // output layer: s' (units 0..99) and r (unit 100)
+#pragma unroll
+            for (int e = 0; e < 16; e += 4) {
+              const int u = j0 + e;
+              if (u < kDnnS)
+                *(float4 *)(srow + u) = make_float4(__uint_as_float(v[e]) + b[u], __uint_as_float(v[e + 1]) + b[u + 1],
+                                                    __uint_as_float(v[e + 2]) + b[u + 2],
+                                                    __uint_as_float(v[e + 3]) + b[u + 3]);
+            }
+            if (j0 <= kDnnS && kDnnS < j0 + 16)
+              out.cum[c - c_begin] = fmaf(gk, __uint_as_float(v[kDnnS - j0]) + b[kDnnS], rpar);
+          }
+        }
+        if (L < 3) {
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(&a_ready[s]);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+// ------------------------------------------------------------------ MLP2 leaf / row net
+// Q(x, .) = W2 relu(W1 x + b1) + b2 over 128-node tiles; x = 100 fp32 state values (DNN env) or
+// 64 state bytes / 256 (INT_HASH, exact in tf32). TMEM: A0 at column 0 (IK = I padded to 8),
+// D1 = A1 at column 128 (H units), D2 at column 384 (NA = A padded to 16). One tile at a time.
+struct MlpTcShape {
+  int I, IK, H, A, NA;
+  uint32_t w1_bytes, b1_off, w2_off, w2_bytes, b2_off, total;   // image layout (bytes)
+};
+__host__ __device__ inline MlpTcShape mlp_tc_shape(int I, int H, int A) {
+  MlpTcShape s;
+  s.I = I;
+  s.IK = (I + 7) / 8 * 8;
+  s.H = H;
+  s.A = A;
+  s.NA = (A + 15) / 16 * 16;
+  s.w1_bytes = (uint32_t)(s.IK / 4) * (uint32_t)H * 16u;
+  s.b1_off = s.w1_bytes;
+  s.w2_off = s.b1_off + (uint32_t)H * 4u;
+  s.w2_bytes = (uint32_t)(H / 4) * (uint32_t)s.NA * 16u;
+  s.b2_off = s.w2_off + s.w2_bytes;
+  s.total = s.b2_off + (uint32_t)s.NA * 4u;
+  return s;
+}
+
+__global__ void __launch_bounds__(kTcThreadsMlp, 1)
+    k_mlp_tc(const uint8_t *__restrict__ states, int64_t stride, const uint8_t *__restrict__ img, MlpTcShape sh,
+             int64_t n, int mode, float gd, const float *__restrict__ cum, float *__restrict__ out, int feat_f32) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = smem_raw + ((128u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 127u)) & 127u);
+  const float *sb1 = (const float *)(smem + sh.b1_off), *sb2 = (const float *)(smem + sh.b2_off);
+  __shared__ __align__(8) uint64_t wbar, a_ready, d_full;
+  __shared__ uint32_t tmem_slot;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    mbar_init(&wbar, 1);
+    mbar_init(&a_ready, 128);
+    mbar_init(&d_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    load_weights(smem, img, sh.total, &wbar);
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(&tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+  const int64_t ntiles = (n + 127) / 128;
+
+  if (warp == 0) {   // ---------------------------------------------------------- MMA issuer
+    const uint32_t elected = elect_one();
+    const uint32_t id1 = idesc_tf32(128, sh.H), id2 = idesc_tf32(128, sh.NA);
+    const uint32_t w1 = saddr(smem), w2 = saddr(smem + sh.w2_off);
+    const uint32_t p1 = (uint32_t)sh.H * 16u, p2 = (uint32_t)sh.NA * 16u;
+    mbar_wait(&wbar, 0);
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      mbar_wait(&a_ready, 0);   // two completions per tile: A0 (parity 0), A1 (parity 1)
+      tc_fence_after();
+      for (int kk = 0; kk < sh.IK / 8; ++kk)
+        mma_tf32_ts(tmem + 128u, tmem + 8u * kk, desc_kmajor(w1 + (uint32_t)(2 * kk) * p1, p1), id1, kk != 0, elected);
+      commit_pred(&d_full, elected);
+      __syncwarp();
+      mbar_wait(&a_ready, 1);
+      tc_fence_after();
+      for (int kk = 0; kk < sh.H / 8; ++kk)
+        mma_tf32_ts(tmem + 384u, tmem + 128u + 8u * kk, desc_kmajor(w2 + (uint32_t)(2 * kk) * p2, p2), id2, kk != 0,
+                    elected);
+      commit_pred(&d_full, elected);
+      __syncwarp();
+    }
+  } else if (warp >= 4) {   // ------------------------------------------------- epilogue
+    const int q = warp & 3, m = q * 32 + lane;
+    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int64_t node = t * 128 + m;
+      const bool valid = node < n;
+      const uint8_t *srow = states + (valid ? node : 0) * stride;
+      // A0: features -> tf32 (columns I..IK-1 and invalid rows zero)
+      for (int j0 = 0; j0 < sh.IK; j0 += 8) {
+        uint32_t r[8];
+        if (feat_f32) {
+          float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0;
+          if (valid && j0 < sh.I) v0 = __ldg((const float4 *)srow + j0 / 4);
+          if (valid && j0 + 4 < sh.I) v1 = __ldg((const float4 *)srow + j0 / 4 + 1);
+          r[0] = tf32_bits(v0.x); r[1] = tf32_bits(v0.y); r[2] = tf32_bits(v0.z); r[3] = tf32_bits(v0.w);
+          r[4] = tf32_bits(v1.x); r[5] = tf32_bits(v1.y); r[6] = tf32_bits(v1.z); r[7] = tf32_bits(v1.w);
+        } else {   // bytes / 256: exact in tf32
+          const uint2 w = valid && j0 < sh.I ? __ldg((const uint2 *)(srow + j0)) : make_uint2(0u, 0u);
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            r[e] = __float_as_uint((float)((((e < 4 ? w.x : w.y) >> (8 * (e & 3))) & 0xFFu)) * (1.0f / 256.0f));
+        }
+        tmem_st8(tl + (uint32_t)j0, r);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&a_ready);
+      // layer 1: relu(D1 + b1) -> tf32 -> A1 (the same columns)
+      mbar_wait(&d_full, 0);
+      tc_fence_after();
+      for (int j0 = 0; j0 < sh.H; j0 += 16) {
+        uint32_t v[16];
+        tmem_ld16_nw(tl + 128u + (uint32_t)j0, v);
+        tmem_wait16(v);
+        uint32_t lo[8], hi[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          lo[e] = tf32_bits(fmaxf(__uint_as_float(v[e]) + sb1[j0 + e], 0.0f));
+          hi[e] = tf32_bits(fmaxf(__uint_as_float(v[e + 8]) + sb1[j0 + e + 8], 0.0f));
+        }
+        tmem_st8(tl + 128u + (uint32_t)j0, lo);
+        tmem_st8(tl + 128u + (uint32_t)j0 + 8u, hi);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&a_ready);
+      // layer 2: Q = D2 + b2 -> rows / max / total
+      mbar_wait(&d_full, 1);
+      tc_fence_after();
+      float best = -INFINITY;
+      for (int j0 = 0; j0 < sh.NA; j0 += 16) {
+        uint32_t v[16];
+        tmem_ld16_nw(tl + 384u + (uint32_t)j0, v);
+        tmem_wait16(v);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const int a = j0 + e;
+          if (a < sh.A) {
+            const float qv = __uint_as_float(v[e]) + sb2[a];
+            best = fmaxf(best, qv);
+            if (valid && mode == MODE_ROWS) out[node * sh.A + a] = qv;
+          }
+        }
+      }
+      if (valid && mode != MODE_ROWS) out[node] = mode == MODE_ROWMAX ? best : fmaf(gd, best, cum ? cum[node] : 0.0f);
+      tc_fence_before();
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+// host: fp32 -> tf32, round to nearest with ties away from zero (= cvt.rna.tf32.f32)
+float tf32_round_host(float x) {
+  uint32_t u;
+  memcpy(&u, &x, 4);
+  if ((u & 0x7F800000u) != 0x7F800000u) u = (u + 0x1000u) & 0xFFFFE000u;
+  float r;
+  memcpy(&r, &u, 4);
+  return r;
+}
+// element (n, k) of a K-major SWIZZLE_NONE image with Npad rows
+inline size_t kmajor_index(int n, int k, int npad) { return (size_t)(k / 4) * npad * 4 + (size_t)n * 4 + (k % 4); }
+
+}  // namespace
+
+// canonical DNN blob (include/bcts.h: g1.w [100][100+A], g1.b, g2.w, g2.b, g3.w, g3.b, g4.w [101][100],
+// g4.b [101]) -> the k_dnn_tc image: 4 layer images (tf32-rounded), biases [4][112], W1A [A][100]
+size_t dnn_tc_image_floats(int A) { return (size_t)kTcDnnFloats + (size_t)kDnnS * A; }
+void dnn_tc_repack(const float *blob, int A, float *out) {
+  const int S = kDnnS, I1 = S + A;
+  memset(out, 0, dnn_tc_image_floats(A) * 4);
+  const float *g1w = blob, *g1b = g1w + (size_t)S * I1, *g2w = g1b + S, *g2b = g2w + S * S, *g3w = g2b + S,
+              *g3b = g3w + S * S, *g4w = g3b + S, *g4b = g4w + (S + 1) * S;
+  const float *W[4] = {g1w, g2w, g3w, g4w}, *B[4] = {g1b, g2b, g3b, g4b};
+  const int ld[4] = {I1, S, S, S}, nout[4] = {S, S, S, S + 1};
+  for (int L = 0; L < 4; ++L) {
+    float *img = out + (size_t)L * (kTcLayerBytes / 4);
+    for (int u = 0; u < nout[L]; ++u)
+      for (int i = 0; i < S; ++i) img[kmajor_index(u, i, kTcN)] = tf32_round_host(W[L][(size_t)u * ld[L] + i]);
+    for (int u = 0; u < nout[L]; ++u) out[4 * (kTcLayerBytes / 4) + L * kTcN + u] = B[L][u];
+  }
+  float *w1a = out + kTcDnnFloats;
+  for (int a = 0; a < A; ++a)
+    for (int u = 0; u < S; ++u) w1a[a * S + u] = g1w[(size_t)u * I1 + S + a];
+}
+
+static size_t dnn_tc_smem(int A) { return dnn_tc_image_floats(A) * 4 + 128; }
+
+void launch_expand_dnn_tc(const NodeView &par, int64_t p_first, int64_t c_begin, int64_t c_end, int A, float gk,
+                          const float *img, const NodeOut &out, cudaStream_t st, Profiler *prof) {
+  const int64_t n = c_end - c_begin;
+  if (n <= 0) return;
+  const int64_t nparents = (c_end - 1) / A - c_begin / A + 1;
+  // the same algorithmic FLOPs as the fp32 path (launch_expand_dnn)
+  if (prof) prof->begin(KC_EXPAND_DNN, 2.0 * (30100.0 * (double)n + 10000.0 * (double)nparents), st);
+  const size_t smem = dnn_tc_smem(A);
+  smem_optin((const void *)k_dnn_tc, (int)smem);
+  const int64_t tiles = (n + 127) / 128;
+  const unsigned grid = (unsigned)std::min<int64_t>((tiles + 1) / 2, sm_count_current());
+  k_dnn_tc<<<grid, kTcThreadsDnn, smem, st>>>(par, p_first, c_begin, c_end, A, gk, img, out);
+  if (prof) prof->end(st);
+}
+
+bool dnn_tc_ok(int A) { return dnn_tc_smem(A) <= 227 * 1024 - 1024; }
+
+// MLP2 weights (w1 [H][I], b1 [H], w2 [A][H], b2 [A]) -> the k_mlp_tc image
+size_t mlp_tc_image_bytes(int I, int H, int A) { return mlp_tc_shape(I, H, A).total; }
+bool mlp_tc_ok(int I, int H, int A) {
+  const MlpTcShape s = mlp_tc_shape(I, H, A);
+  return s.IK <= 128 && H % 16 == 0 && H <= 256 && s.NA <= 64 && s.total + 128 <= 227 * 1024 - 1024;
+}
+void mlp_tc_repack(const float *w1, const float *b1, const float *w2, const float *b2, int I, int H, int A,
+                   uint8_t *out) {
+  const MlpTcShape s = mlp_tc_shape(I, H, A);
+  memset(out, 0, s.total);
+  float *W1 = (float *)out, *B1 = (float *)(out + s.b1_off), *W2 = (float *)(out + s.w2_off),
+        *B2 = (float *)(out + s.b2_off);
+  for (int u = 0; u < H; ++u)
+    for (int i = 0; i < I; ++i) W1[kmajor_index(u, i, H)] = tf32_round_host(w1[(size_t)u * I + i]);
+  for (int u = 0; u < H; ++u) B1[u] = b1[u];
+  for (int a = 0; a < A; ++a)
+    for (int u = 0; u < H; ++u) W2[kmajor_index(a, u, s.NA)] = tf32_round_host(w2[(size_t)a * H + u]);
+  for (int a = 0; a < A; ++a) B2[a] = b2[a];
+}
+
+void launch_mlp_tc(const NodeView &v, int64_t n, const uint8_t *img, int I, int H, int A, int mode, float gd,
+                   float *out, int feat_f32, cudaStream_t st) {
+  if (n <= 0) return;
+  const MlpTcShape sh = mlp_tc_shape(I, H, A);
+  const size_t smem = sh.total + 128;
+  smem_optin((const void *)k_mlp_tc, (int)smem);
+  const unsigned grid = (unsigned)std::min<int64_t>((n + 127) / 128, sm_count_current());
+  k_mlp_tc<<<grid, kTcThreadsMlp, smem, st>>>(v.state, v.state_stride, img, sh, n, mode, gd, v.cum, out, feat_f32);
+}
+
+}  // namespace bcts

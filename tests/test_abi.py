@@ -180,3 +180,13 @@ def test_bench_self_launches_world2_reference_on_cpu():
     assert len(lines) == 1, r.stdout[-2000:]
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+
+
+def test_python_flags_match_header():
+    """The binding's BCTS_F_* constants are the header's (argument marshalling only)."""
+    import paper_2107_01715_b200 as P
+    hdr = open(os.path.join(ROOT, "include", "bcts.h")).read()
+    for name in ("CLAMP_PENALTY", "SIMT_NET", "MATERIALIZE_LEAVES", "SEPARATE_BACKUP", "NO_PROLOGUE_FOLD", "NO_GRAPH",
+                 "TF32"):
+        v = int(re.search(r"#define BCTS_F_%s (0x[0-9a-fA-F]+)u" % name, hdr)[1], 16)
+        assert getattr(P, "F_" + name) == v, name
