@@ -58,12 +58,9 @@ __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8])
                "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
                : "memory");
 }
-// fp32 -> tf32 (round to nearest, ties away from zero; low 13 bits cleared)
-__device__ __forceinline__ uint32_t tf32_bits(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return r;
-}
+// fp32 -> tf32 (round to nearest, ties away from zero; low 13 bits cleared): the integer form of
+// cvt.rna.tf32.f32 for finite inputs (the PTX instruction is emulated with an extra Inf/NaN test)
+__device__ __forceinline__ uint32_t tf32_bits(float x) { return (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u; }
 // one bulk copy per 32 KB piece (the whole image completes `bar`)
 __device__ __forceinline__ void load_weights(uint8_t *dst, const void *src, uint32_t bytes, uint64_t *bar) {
   mbar_expect_tx(bar, bytes);
@@ -106,6 +103,8 @@ __global__ void __launch_bounds__(kTcThreadsDnn, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
+  pdl_wait();      // parent states: the previous kernel's output (the weight copy above overlaps its tail)
+  pdl_trigger();
   const int64_t n = c_end - c_begin, ntiles = (n + 127) / 128;
 
   if (warp == 0) {   // ---------------------------------------------------------- MMA issuer
@@ -143,13 +142,15 @@ __global__ void __launch_bounds__(kTcThreadsDnn, 1)
       // A0: the parent's state, rounded to tf32; columns 100..103 and invalid rows are zero
       {
         const float4 *ps = (const float4 *)(par.state + (p - p_first) * par.state_stride);
+        float4 x4[kDnnS / 4];   // all 25 loads in flight at once (one L2 round trip, not four)
+#pragma unroll
+        for (int e = 0; e < kDnnS / 4; ++e) x4[e] = valid ? __ldg(ps + e) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
         for (int j0 = 0; j0 < kTcK; j0 += 32) {
           uint32_t r[32];
 #pragma unroll
           for (int e = 0; e < 32; e += 4) {
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (valid && j0 + e < kDnnS) v = __ldg(ps + (j0 + e) / 4);
+            const float4 v = j0 + e < kDnnS ? x4[(j0 + e) / 4] : make_float4(0.f, 0.f, 0.f, 0.f);
             r[e] = tf32_bits(v.x);
             r[e + 1] = tf32_bits(v.y);
             r[e + 2] = tf32_bits(v.z);
@@ -172,11 +173,7 @@ __global__ void __launch_bounds__(kTcThreadsDnn, 1)
         mbar_wait(&d_full[s], (uint32_t)L & 1u);
         tc_fence_after();
         const float *b = sB + L * kTcN;
-#pragma unroll
-        for (int j0 = 0; j0 < kTcN; j0 += 16) {
-          uint32_t v[16];
-          tmem_ld16_nw(tD + (uint32_t)j0, v);
-          tmem_wait16(v);
+        auto proc = [&](int j0, const uint32_t(&v)[16]) {
           if (L < 3) {   // hidden layer: relu(D + b (+ W1[:, 100 + a])) -> tf32 -> A columns j0..
             uint32_t r[16];
 #pragma unroll
@@ -211,6 +208,24 @@ __global__ void __launch_bounds__(kTcThreadsDnn, 1)
             if (j0 <= kDnnS && kDnnS < j0 + 16)
               out.cum[c - c_begin] = fmaf(gk, __uint_as_float(v[kDnnS - j0]) + b[kDnnS], rpar);
           }
+        };
+        {   // columns 0..63: four loads, one wait
+          uint32_t v[4][16];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) tmem_ld16_nw(tD + 16u * u, v[u]);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) tmem_wait16(v[u]);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) proc(16 * u, v[u]);
+        }
+        {   // columns 64..111: three loads, one wait
+          uint32_t v[3][16];
+#pragma unroll
+          for (int u = 0; u < 3; ++u) tmem_ld16_nw(tD + 64u + 16u * u, v[u]);
+#pragma unroll
+          for (int u = 0; u < 3; ++u) tmem_wait16(v[u]);
+#pragma unroll
+          for (int u = 0; u < 3; ++u) proc(64 + 16 * u, v[u]);
         }
         if (L < 3) {
           tmem_wait_st();
@@ -252,19 +267,58 @@ __host__ __device__ inline MlpTcShape mlp_tc_shape(int I, int H, int A) {
   return s;
 }
 
+// A0 of node `node` (features -> tf32; columns I..IK-1 and rows past n zero) into TMEM columns 0..
+// All of the row's loads are issued before the first store (one memory round trip per tile).
+__device__ __forceinline__ void mlp_load_a0(const uint8_t *__restrict__ states, int64_t stride, int64_t node,
+                                            int64_t n, const MlpTcShape &sh, int feat_f32, uint32_t tl) {
+  const bool valid = node < n;
+  const uint8_t *srow = states + (valid ? node : 0) * stride;
+  if (feat_f32) {   // 100 fp32 state values (DNN env): 25 float4
+    float4 x4[kDnnS / 4];
+#pragma unroll
+    for (int e = 0; e < kDnnS / 4; ++e) x4[e] = valid ? __ldg((const float4 *)srow + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int j0 = 0; j0 < kTcK; j0 += 8) {
+      const float4 v0 = j0 < kDnnS ? x4[j0 / 4] : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 v1 = j0 + 4 < kDnnS ? x4[j0 / 4 + 1] : make_float4(0.f, 0.f, 0.f, 0.f);
+      const uint32_t r[8] = {tf32_bits(v0.x), tf32_bits(v0.y), tf32_bits(v0.z), tf32_bits(v0.w),
+                             tf32_bits(v1.x), tf32_bits(v1.y), tf32_bits(v1.z), tf32_bits(v1.w)};
+      tmem_st8(tl + (uint32_t)j0, r);
+    }
+  } else {          // 64 state bytes / 256 (INT_HASH): exact in tf32
+    uint4 w4[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) w4[e] = valid ? __ldg((const uint4 *)srow + e) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+    for (int j0 = 0; j0 < 64; j0 += 8) {
+      const uint4 w = w4[j0 / 16];
+      const uint32_t lo = (j0 & 8) ? w.z : w.x, hi = (j0 & 8) ? w.w : w.y;
+      uint32_t r[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        r[e] = __float_as_uint((float)((((e < 4 ? lo : hi) >> (8 * (e & 3))) & 0xFFu)) * (1.0f / 256.0f));
+      tmem_st8(tl + (uint32_t)j0, r);
+    }
+  }
+}
+
+// The next tile's A0 is loaded while the current tile's layer-2 MMAs run (A0's columns are free
+// once layer 1 is done); each barrier completes once per tile, so tile i waits parity i & 1.
 __global__ void __launch_bounds__(kTcThreadsMlp, 1)
     k_mlp_tc(const uint8_t *__restrict__ states, int64_t stride, const uint8_t *__restrict__ img, MlpTcShape sh,
              int64_t n, int mode, float gd, const float *__restrict__ cum, float *__restrict__ out, int feat_f32) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((128u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 127u)) & 127u);
   const float *sb1 = (const float *)(smem + sh.b1_off), *sb2 = (const float *)(smem + sh.b2_off);
-  __shared__ __align__(8) uint64_t wbar, a_ready, d_full;
+  __shared__ __align__(8) uint64_t wbar, a0_ready, a1_ready, d1_full, d2_full;
   __shared__ uint32_t tmem_slot;
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
   if (threadIdx.x == 0) {
     mbar_init(&wbar, 1);
-    mbar_init(&a_ready, 128);
-    mbar_init(&d_full, 1);
+    mbar_init(&a0_ready, 128);
+    mbar_init(&a1_ready, 128);
+    mbar_init(&d1_full, 1);
+    mbar_init(&d2_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     load_weights(smem, img, sh.total, &wbar);
   }
@@ -277,6 +331,8 @@ __global__ void __launch_bounds__(kTcThreadsMlp, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
+  pdl_wait();      // node states: the previous kernel's output (the weight copy above overlaps its tail)
+  pdl_trigger();
   const int64_t ntiles = (n + 127) / 128;
 
   if (warp == 0) {   // ---------------------------------------------------------- MMA issuer
@@ -285,71 +341,74 @@ __global__ void __launch_bounds__(kTcThreadsMlp, 1)
     const uint32_t w1 = saddr(smem), w2 = saddr(smem + sh.w2_off);
     const uint32_t p1 = (uint32_t)sh.H * 16u, p2 = (uint32_t)sh.NA * 16u;
     mbar_wait(&wbar, 0);
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      mbar_wait(&a_ready, 0);   // two completions per tile: A0 (parity 0), A1 (parity 1)
+    uint32_t i = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+      mbar_wait(&a0_ready, i & 1u);
+      if (i) mbar_wait(&d2_full, (i - 1) & 1u);   // the previous tile's layer 2 has read A1 (= D1's columns)
       tc_fence_after();
       for (int kk = 0; kk < sh.IK / 8; ++kk)
         mma_tf32_ts(tmem + 128u, tmem + 8u * kk, desc_kmajor(w1 + (uint32_t)(2 * kk) * p1, p1), id1, kk != 0, elected);
-      commit_pred(&d_full, elected);
+      commit_pred(&d1_full, elected);
       __syncwarp();
-      mbar_wait(&a_ready, 1);
+      mbar_wait(&a1_ready, i & 1u);
       tc_fence_after();
       for (int kk = 0; kk < sh.H / 8; ++kk)
         mma_tf32_ts(tmem + 384u, tmem + 128u + 8u * kk, desc_kmajor(w2 + (uint32_t)(2 * kk) * p2, p2), id2, kk != 0,
                     elected);
-      commit_pred(&d_full, elected);
+      commit_pred(&d2_full, elected);
       __syncwarp();
     }
   } else if (warp >= 4) {   // ------------------------------------------------- epilogue
     const int q = warp & 3, m = q * 32 + lane;
     const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    if (blockIdx.x < ntiles) {
+      mlp_load_a0(states, stride, (int64_t)blockIdx.x * 128 + m, n, sh, feat_f32, tl);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&a0_ready);
+    }
+    uint32_t i = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
       const int64_t node = t * 128 + m;
-      const bool valid = node < n;
-      const uint8_t *srow = states + (valid ? node : 0) * stride;
-      // A0: features -> tf32 (columns I..IK-1 and invalid rows zero)
-      for (int j0 = 0; j0 < sh.IK; j0 += 8) {
-        uint32_t r[8];
-        if (feat_f32) {
-          float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0;
-          if (valid && j0 < sh.I) v0 = __ldg((const float4 *)srow + j0 / 4);
-          if (valid && j0 + 4 < sh.I) v1 = __ldg((const float4 *)srow + j0 / 4 + 1);
-          r[0] = tf32_bits(v0.x); r[1] = tf32_bits(v0.y); r[2] = tf32_bits(v0.z); r[3] = tf32_bits(v0.w);
-          r[4] = tf32_bits(v1.x); r[5] = tf32_bits(v1.y); r[6] = tf32_bits(v1.z); r[7] = tf32_bits(v1.w);
-        } else {   // bytes / 256: exact in tf32
-          const uint2 w = valid && j0 < sh.I ? __ldg((const uint2 *)(srow + j0)) : make_uint2(0u, 0u);
-#pragma unroll
-          for (int e = 0; e < 8; ++e)
-            r[e] = __float_as_uint((float)((((e < 4 ? w.x : w.y) >> (8 * (e & 3))) & 0xFFu)) * (1.0f / 256.0f));
-        }
-        tmem_st8(tl + (uint32_t)j0, r);
-      }
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(&a_ready);
-      // layer 1: relu(D1 + b1) -> tf32 -> A1 (the same columns)
-      mbar_wait(&d_full, 0);
+      // layer 1: relu(D1 + b1) -> tf32 -> A1 (the same columns), four 16-column loads per wait
+      mbar_wait(&d1_full, i & 1u);
       tc_fence_after();
-      for (int j0 = 0; j0 < sh.H; j0 += 16) {
-        uint32_t v[16];
-        tmem_ld16_nw(tl + 128u + (uint32_t)j0, v);
-        tmem_wait16(v);
-        uint32_t lo[8], hi[8];
+      for (int j0 = 0; j0 < sh.H; j0 += 64) {
+        uint32_t v[4][16];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          lo[e] = tf32_bits(fmaxf(__uint_as_float(v[e]) + sb1[j0 + e], 0.0f));
-          hi[e] = tf32_bits(fmaxf(__uint_as_float(v[e + 8]) + sb1[j0 + e + 8], 0.0f));
+        for (int u = 0; u < 4; ++u)
+          if (j0 + 16 * u < sh.H) tmem_ld16_nw(tl + 128u + (uint32_t)(j0 + 16 * u), v[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (j0 + 16 * u < sh.H) tmem_wait16(v[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (j0 + 16 * u >= sh.H) break;
+          uint32_t lo[8], hi[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            lo[e] = tf32_bits(fmaxf(__uint_as_float(v[u][e]) + sb1[j0 + 16 * u + e], 0.0f));
+            hi[e] = tf32_bits(fmaxf(__uint_as_float(v[u][e + 8]) + sb1[j0 + 16 * u + e + 8], 0.0f));
+          }
+          tmem_st8(tl + 128u + (uint32_t)(j0 + 16 * u), lo);
+          tmem_st8(tl + 128u + (uint32_t)(j0 + 16 * u) + 8u, hi);
         }
-        tmem_st8(tl + 128u + (uint32_t)j0, lo);
-        tmem_st8(tl + 128u + (uint32_t)j0 + 8u, hi);
       }
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(&a_ready);
+      mbar_arrive(&a1_ready);
+      // the next tile's features while layer 2 runs
+      if (t + gridDim.x < ntiles) {
+        mlp_load_a0(states, stride, (t + gridDim.x) * 128 + m, n, sh, feat_f32, tl);
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&a0_ready);
+      }
       // layer 2: Q = D2 + b2 -> rows / max / total
-      mbar_wait(&d_full, 1);
+      mbar_wait(&d2_full, i & 1u);
       tc_fence_after();
       float best = -INFINITY;
+      const bool valid = node < n;
       for (int j0 = 0; j0 < sh.NA; j0 += 16) {
         uint32_t v[16];
         tmem_ld16_nw(tl + 384u + (uint32_t)j0, v);
@@ -424,7 +483,7 @@ void launch_expand_dnn_tc(const NodeView &par, int64_t p_first, int64_t c_begin,
   smem_optin((const void *)k_dnn_tc, (int)smem);
   const int64_t tiles = (n + 127) / 128;
   const unsigned grid = (unsigned)std::min<int64_t>((tiles + 1) / 2, sm_count_current());
-  k_dnn_tc<<<grid, kTcThreadsDnn, smem, st>>>(par, p_first, c_begin, c_end, A, gk, img, out);
+  launch_pdl(k_dnn_tc, dim3(grid), dim3(kTcThreadsDnn), smem, st, par, p_first, c_begin, c_end, A, gk, img, out);
   if (prof) prof->end(st);
 }
 
@@ -457,7 +516,8 @@ void launch_mlp_tc(const NodeView &v, int64_t n, const uint8_t *img, int I, int 
   const size_t smem = sh.total + 128;
   smem_optin((const void *)k_mlp_tc, (int)smem);
   const unsigned grid = (unsigned)std::min<int64_t>((n + 127) / 128, sm_count_current());
-  k_mlp_tc<<<grid, kTcThreadsMlp, smem, st>>>(v.state, v.state_stride, img, sh, n, mode, gd, v.cum, out, feat_f32);
+  launch_pdl(k_mlp_tc, dim3(grid), dim3(kTcThreadsMlp), smem, st, v.state, v.state_stride, img, sh, n, mode, gd, v.cum,
+             out, feat_f32);
 }
 
 }  // namespace bcts
