@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(kTcThreadsDnn, 1)
   if (warp == 0) {   // ---------------------------------------------------------- MMA issuer
     constexpr uint32_t idesc = idesc_tf32(128, kTcN);
     const uint32_t elected = elect_one();
-    mbar_wait(&wbar, 0);
+    mbar_wait_spin(&wbar, 0);
     const uint32_t wbase = saddr(smem);
     // tiles in pairs (slot 0: t, slot 1: t + grid), layers interleaved across the pair so one
     // slot's MMAs run while the other slot's epilogue works. Each slot's barriers complete four
@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(kTcThreadsDnn, 1)
       const int nslot = t0 + gridDim.x < ntiles ? 2 : 1;
       for (int L = 0; L < 4; ++L)
         for (int s = 0; s < nslot; ++s) {
-          mbar_wait(&a_ready[s], (uint32_t)L & 1u);
+          mbar_wait_spin(&a_ready[s], (uint32_t)L & 1u);
           tc_fence_after();
           const uint32_t tA = tmem + 256u * s, tD = tA + 128u;
 #pragma unroll
@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(kTcThreadsDnn, 1)
       const float rpar = valid && par.cum ? par.cum[p - p_first] : 0.0f;
       float *srow = (float *)(out.state + (valid ? c - c_begin : 0) * out.state_stride);
       for (int L = 0; L < 4; ++L) {
-        mbar_wait(&d_full[s], (uint32_t)L & 1u);
+        mbar_wait_spin(&d_full[s], (uint32_t)L & 1u);
         tc_fence_after();
         const float *b = sB + L * kTcN;
         auto proc = [&](int j0, const uint32_t(&v)[16]) {
@@ -340,17 +340,17 @@ __global__ void __launch_bounds__(kTcThreadsMlp, 1)
     const uint32_t id1 = idesc_tf32(128, sh.H), id2 = idesc_tf32(128, sh.NA);
     const uint32_t w1 = saddr(smem), w2 = saddr(smem + sh.w2_off);
     const uint32_t p1 = (uint32_t)sh.H * 16u, p2 = (uint32_t)sh.NA * 16u;
-    mbar_wait(&wbar, 0);
+    mbar_wait_spin(&wbar, 0);
     uint32_t i = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
-      mbar_wait(&a0_ready, i & 1u);
-      if (i) mbar_wait(&d2_full, (i - 1) & 1u);   // the previous tile's layer 2 has read A1 (= D1's columns)
+      mbar_wait_spin(&a0_ready, i & 1u);
+      if (i) mbar_wait_spin(&d2_full, (i - 1) & 1u);   // the previous tile's layer 2 has read A1 (= D1's columns)
       tc_fence_after();
       for (int kk = 0; kk < sh.IK / 8; ++kk)
         mma_tf32_ts(tmem + 128u, tmem + 8u * kk, desc_kmajor(w1 + (uint32_t)(2 * kk) * p1, p1), id1, kk != 0, elected);
       commit_pred(&d1_full, elected);
       __syncwarp();
-      mbar_wait(&a1_ready, i & 1u);
+      mbar_wait_spin(&a1_ready, i & 1u);
       tc_fence_after();
       for (int kk = 0; kk < sh.H / 8; ++kk)
         mma_tf32_ts(tmem + 384u, tmem + 128u + 8u * kk, desc_kmajor(w2 + (uint32_t)(2 * kk) * p2, p2), id2, kk != 0,
@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(kTcThreadsMlp, 1)
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
       const int64_t node = t * 128 + m;
       // layer 1: relu(D1 + b1) -> tf32 -> A1 (the same columns), four 16-column loads per wait
-      mbar_wait(&d1_full, i & 1u);
+      mbar_wait_spin(&d1_full, i & 1u);
       tc_fence_after();
       for (int j0 = 0; j0 < sh.H; j0 += 64) {
         uint32_t v[4][16];
@@ -405,7 +405,7 @@ __global__ void __launch_bounds__(kTcThreadsMlp, 1)
         mbar_arrive(&a0_ready);
       }
       // layer 2: Q = D2 + b2 -> rows / max / total
-      mbar_wait(&d2_full, i & 1u);
+      mbar_wait_spin(&d2_full, i & 1u);
       tc_fence_after();
       float best = -INFINITY;
       const bool valid = node < n;
