@@ -45,8 +45,9 @@
 extern "C" {
 #endif
 
-#define BCTS_ABI_VERSION 5   /* 2: env_weights fields + BCTS_ENV_DNN; 3: bcts_search_pruned; 4: bcts_kernel_profile largest-launch fields;
-                                5: NCCL (nccl_unique_id / rank / world, BCTS_ERR_NCCL), caller workspace, ms_* stats, flags 0x10-0x20 */
+#define BCTS_ABI_VERSION 6   /* 2: env_weights fields + BCTS_ENV_DNN; 3: bcts_search_pruned; 4: bcts_kernel_profile largest-launch fields;
+                                5: NCCL (nccl_unique_id / rank / world, BCTS_ERR_NCCL), caller workspace, ms_* stats, flags 0x10-0x20;
+                                6: BCTS_F_TF32 (NEXT-1 on the tensor cores) */
 
 typedef struct bcts_handle_t *bcts_handle;
 

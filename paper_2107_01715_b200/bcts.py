@@ -17,7 +17,7 @@ ENV_TABULAR, ENV_INT_HASH, ENV_ATARI_HASH, ENV_DNN = 1, 2, 3, 4
 NET_TABLE, NET_MLP2_F32, NET_NATURE_BF16, NET_RAINBOW_BF16 = 1, 2, 3, 4
 F_CLAMP_PENALTY, F_SIMT_NET, F_MATERIALIZE_LEAVES, F_SEPARATE_BACKUP = 0x1, 0x2, 0x4, 0x8
 F_NO_PROLOGUE_FOLD, F_NO_GRAPH, F_TF32 = 0x10, 0x20, 0x40
-ABI_VERSION = 5
+ABI_VERSION = 6
 PRUNE_NONE, PRUNE_BOUND, PRUNE_BEAM = 0, 1, 2
 STATUS = {0: "BCTS_OK", 1: "BCTS_ERR_INVALID_ARG", 2: "BCTS_ERR_UNSUPPORTED", 3: "BCTS_ERR_OUT_OF_MEMORY",
           4: "BCTS_ERR_BUDGET", 5: "BCTS_ERR_CUDA", 6: "BCTS_ERR_NCCL", 7: "BCTS_ERR_NUMERIC"}
