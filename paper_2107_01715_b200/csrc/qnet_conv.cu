@@ -785,7 +785,7 @@ __global__ void __launch_bounds__(kC23Threads, 1)
       mbar_init(&in_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&a2full[i], 128);
+      mbar_init(&a2full[i], 256);
       mbar_init(&a2empty[i], 1);
     }
     mbar_init(&t3full, 1);
@@ -868,11 +868,13 @@ __global__ void __launch_bounds__(kC23Threads, 1)
     }
   } else if (warp < 10) {   // --------------------------- conv2 epilogue -> act2 in SMEM (SW128)
     // lane quarter q: lanes 32 q .. 32 q + 31 = output channel c of tap half (q >= 2); part = which
-    // 48 of T2's 96 columns this warp reads. Lower part 0 finishes rows 0..47 (needs D_hi[1..48]),
-    // upper part 1 rows 48..88 (needs D_lo[48..88]); the other two parts only hand their columns
-    // over: hand-off row of channel c (buffer li & 1): [0, 48) = D_hi[1..48], [48, 89) = D_lo[48..88].
+    // 48 of T2's 96 columns this warp reads. Every warp finishes ~22 of the 89 full-width rows:
+    // lower part 0 rows 0..23, upper part 0 24..47, lower part 1 48..67, upper part 1 68..88; out[n]
+    // = D_lo[n] + D_hi[n + 1], the missing half through the hand-off row of channel c:
+    // A [0, 24) = D_hi[1..24], B [24, 48) = D_lo[24..47], C [48, 68) = D_hi[49..68],
+    // D [68, 89) = D_lo[68..88], E [89] = D_hi[48].
     const int q = warp & 3, part = (warp - 2) >> 2;
-    const bool upper = q >= 2, reader_only = !upper && part == 0;
+    const bool upper = q >= 2;
     const int c = 32 * (q & 1) + lane;
     const float bc = sb2[c];
     const uint32_t lanes = (uint32_t)(q * 32) << 16;
@@ -922,50 +924,66 @@ __global__ void __launch_bounds__(kC23Threads, 1)
       mbar_arrive(&t2empty);
       float *xrow = sX2 + c * kX2Ld;
       const auto f = [&](int i) { return __uint_as_float(v[i]); };
-      // single hand-off buffer: the writers of image li wait (barrier 4) until lower part 0 has
-      // read image li-1's rows (it arrives without waiting); upper part 1 reads before it writes
-      if (!reader_only && li > 0) asm volatile("bar.sync 4, 256;" ::: "memory");
-      if (upper && part == 0) {          // v = D_hi[0..47] -> xrow[j] = D_hi[j + 1], j < 47
+      // single hand-off buffer: every warp has read image li-1's rows before any warp writes li's
+      if (li > 0) asm volatile("bar.sync 4, 256;" ::: "memory");
+      if (upper && part == 0) {          // v = D_hi[0..47]: A = xrow[0, 24) <- D_hi[1..24]
 #pragma unroll
-        for (int j = 0; j < 44; j += 4) *(float4 *)(xrow + j) = make_float4(f(j + 1), f(j + 2), f(j + 3), f(j + 4));
-        xrow[44] = f(45);
-        xrow[45] = f(46);
-        xrow[46] = f(47);
-      } else if (upper) {                // v = D_hi[48..95]
-        xrow[47] = f(0);
-      } else if (part == 1) {            // v = D_lo[48..95] -> xrow[48..88]
+        for (int j = 0; j < 24; j += 4) *(float4 *)(xrow + j) = make_float4(f(j + 1), f(j + 2), f(j + 3), f(j + 4));
+      } else if (upper) {                // v = D_hi[48..95]: C = xrow[48, 68) <- D_hi[49..68], E = xrow[89] <- D_hi[48]
 #pragma unroll
-        for (int j = 0; j < 40; j += 4) *(float4 *)(xrow + 48 + j) = make_float4(f(j), f(j + 1), f(j + 2), f(j + 3));
+        for (int j = 0; j < 20; j += 4) *(float4 *)(xrow + 48 + j) = make_float4(f(j + 1), f(j + 2), f(j + 3), f(j + 4));
+        xrow[89] = f(0);
+      } else if (part == 0) {            // v = D_lo[0..47]: B = xrow[24, 48) <- D_lo[24..47]
+#pragma unroll
+        for (int j = 24; j < 48; j += 4) *(float4 *)(xrow + j) = make_float4(f(j), f(j + 1), f(j + 2), f(j + 3));
+      } else {                           // v = D_lo[48..95]: D = xrow[68, 89) <- D_lo[68..88]
+#pragma unroll
+        for (int j = 20; j < 40; j += 4) *(float4 *)(xrow + 48 + j) = make_float4(f(j), f(j + 1), f(j + 2), f(j + 3));
         xrow[88] = f(40);
       }
       asm volatile("bar.sync 3, 256;" ::: "memory");   // the 8 conv2-epilogue warps
-      if (upper == (part == 1)) {        // the two finishing parts
-        mbar_wait_spin(&a2empty[b], ph ^ 1u);                 // conv3 of image li-2 is done with sA2[b]
-        uint8_t *a2 = sA2 + b * kC23A2;
-        if (!upper) {                    // rows 0..47: own D_lo[n] + D_hi[n + 1]
+      mbar_wait_spin(&a2empty[b], ph ^ 1u);              // conv3 of image li-2 is done with sA2[b]
+      uint8_t *a2 = sA2 + b * kC23A2;
+      if (!upper && part == 0) {         // rows 0..23: own D_lo[n] + D_hi[n + 1] (A)
 #pragma unroll
-          for (int n4 = 0; n4 < 48; n4 += 4) {
-            const float4 t = *(const float4 *)(xrow + n4);
-            emit(a2, n4, f(n4) + t.x);
-            emit(a2, n4 + 1, f(n4 + 1) + t.y);
-            emit(a2, n4 + 2, f(n4 + 2) + t.z);
-            emit(a2, n4 + 3, f(n4 + 3) + t.w);
-          }
-        } else {                         // rows 48..88: D_lo[n] + own D_hi[n + 1] (= v[n - 47])
-#pragma unroll
-          for (int n4 = 48; n4 < 88; n4 += 4) {
-            const float4 t = *(const float4 *)(xrow + n4);
-            emit(a2, n4, t.x + f(n4 - 47));
-            emit(a2, n4 + 1, t.y + f(n4 - 46));
-            emit(a2, n4 + 2, t.z + f(n4 - 45));
-            emit(a2, n4 + 3, t.w + f(n4 - 44));
-          }
-          emit(a2, 88, xrow[88] + f(41));
+        for (int n4 = 0; n4 < 24; n4 += 4) {
+          const float4 t = *(const float4 *)(xrow + n4);
+          emit(a2, n4, f(n4) + t.x);
+          emit(a2, n4 + 1, f(n4 + 1) + t.y);
+          emit(a2, n4 + 2, f(n4 + 2) + t.z);
+          emit(a2, n4 + 3, f(n4 + 3) + t.w);
         }
-        if (reader_only && li + 1 < n_my) asm volatile("bar.arrive 4, 256;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive(&a2full[b]);
+      } else if (part == 0) {            // rows 24..47: D_lo[n] (B) + own D_hi[n + 1] (row 47: E)
+#pragma unroll
+        for (int n4 = 24; n4 < 48; n4 += 4) {
+          const float4 t = *(const float4 *)(xrow + n4);
+          emit(a2, n4, t.x + f(n4 + 1));
+          emit(a2, n4 + 1, t.y + f(n4 + 2));
+          emit(a2, n4 + 2, t.z + f(n4 + 3));
+          emit(a2, n4 + 3, t.w + (n4 + 4 < 48 ? f(n4 + 4) : xrow[89]));
+        }
+      } else if (!upper) {               // rows 48..67: own D_lo[n] (v[n - 48]) + D_hi[n + 1] (C)
+#pragma unroll
+        for (int n4 = 48; n4 < 68; n4 += 4) {
+          const float4 t = *(const float4 *)(xrow + n4);
+          emit(a2, n4, f(n4 - 48) + t.x);
+          emit(a2, n4 + 1, f(n4 - 47) + t.y);
+          emit(a2, n4 + 2, f(n4 - 46) + t.z);
+          emit(a2, n4 + 3, f(n4 - 45) + t.w);
+        }
+      } else {                           // rows 68..88: D_lo[n] (D) + own D_hi[n + 1] (v[n - 47])
+#pragma unroll
+        for (int n4 = 68; n4 < 88; n4 += 4) {
+          const float4 t = *(const float4 *)(xrow + n4);
+          emit(a2, n4, t.x + f(n4 - 47));
+          emit(a2, n4 + 1, t.y + f(n4 - 46));
+          emit(a2, n4 + 2, t.z + f(n4 - 45));
+          emit(a2, n4 + 3, t.w + f(n4 - 44));
+        }
+        emit(a2, 88, xrow[88] + f(41));
       }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&a2full[b]);
     }
   } else {   // ------------------------------------------- conv3 epilogue -> act3 (dense), warps 10-13
     const int q = warp & 3;                 // TMEM lane quarter; q < 2: tap a (lower half), q >= 2: tap b
