@@ -267,37 +267,47 @@ __host__ __device__ inline MlpTcShape mlp_tc_shape(int I, int H, int A) {
   return s;
 }
 
-// A0 of node `node` (features -> tf32; columns I..IK-1 and rows past n zero) into TMEM columns 0..
-// All of the row's loads are issued before the first store (one memory round trip per tile).
-__device__ __forceinline__ void mlp_load_a0(const uint8_t *__restrict__ states, int64_t stride, int64_t node,
-                                            int64_t n, const MlpTcShape &sh, int feat_f32, uint32_t tl) {
+// A0 of node `node` (features -> tf32; columns I..IK-1 and rows past n zero) into TMEM columns 0..,
+// in two steps: mlp_fetch_a0 issues the row's loads into registers (a tile ahead of their use),
+// mlp_store_a0 rounds and stores them. Bytes (INT_HASH) travel in the first four float4 as raw bits.
+struct MlpA0 {
+  float4 x[kDnnS / 4];
+};
+__device__ __forceinline__ void mlp_fetch_a0(const uint8_t *__restrict__ states, int64_t stride, int64_t node,
+                                             int64_t n, int feat_f32, MlpA0 &r) {
   const bool valid = node < n;
   const uint8_t *srow = states + (valid ? node : 0) * stride;
   if (feat_f32) {   // 100 fp32 state values (DNN env): 25 float4
-    float4 x4[kDnnS / 4];
 #pragma unroll
-    for (int e = 0; e < kDnnS / 4; ++e) x4[e] = valid ? __ldg((const float4 *)srow + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int e = 0; e < kDnnS / 4; ++e) r.x[e] = valid ? __ldg((const float4 *)srow + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+  } else {          // 64 state bytes (INT_HASH)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint4 w = valid ? __ldg((const uint4 *)srow + e) : make_uint4(0u, 0u, 0u, 0u);
+      r.x[e] = make_float4(__uint_as_float(w.x), __uint_as_float(w.y), __uint_as_float(w.z), __uint_as_float(w.w));
+    }
+  }
+}
+__device__ __forceinline__ void mlp_store_a0(const MlpA0 &r, int feat_f32, uint32_t tl) {
+  if (feat_f32) {
 #pragma unroll
     for (int j0 = 0; j0 < kTcK; j0 += 8) {
-      const float4 v0 = j0 < kDnnS ? x4[j0 / 4] : make_float4(0.f, 0.f, 0.f, 0.f);
-      const float4 v1 = j0 + 4 < kDnnS ? x4[j0 / 4 + 1] : make_float4(0.f, 0.f, 0.f, 0.f);
-      const uint32_t r[8] = {tf32_bits(v0.x), tf32_bits(v0.y), tf32_bits(v0.z), tf32_bits(v0.w),
+      const float4 v0 = j0 < kDnnS ? r.x[j0 / 4] : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 v1 = j0 + 4 < kDnnS ? r.x[j0 / 4 + 1] : make_float4(0.f, 0.f, 0.f, 0.f);
+      const uint32_t q[8] = {tf32_bits(v0.x), tf32_bits(v0.y), tf32_bits(v0.z), tf32_bits(v0.w),
                              tf32_bits(v1.x), tf32_bits(v1.y), tf32_bits(v1.z), tf32_bits(v1.w)};
-      tmem_st8(tl + (uint32_t)j0, r);
+      tmem_st8(tl + (uint32_t)j0, q);
     }
-  } else {          // 64 state bytes / 256 (INT_HASH): exact in tf32
-    uint4 w4[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) w4[e] = valid ? __ldg((const uint4 *)srow + e) : make_uint4(0u, 0u, 0u, 0u);
+  } else {          // bytes / 256: exact in tf32
 #pragma unroll
     for (int j0 = 0; j0 < 64; j0 += 8) {
-      const uint4 w = w4[j0 / 16];
-      const uint32_t lo = (j0 & 8) ? w.z : w.x, hi = (j0 & 8) ? w.w : w.y;
-      uint32_t r[8];
+      const float4 w = r.x[j0 / 16];
+      const uint32_t lo = __float_as_uint((j0 & 8) ? w.z : w.x), hi = __float_as_uint((j0 & 8) ? w.w : w.y);
+      uint32_t q[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e)
-        r[e] = __float_as_uint((float)((((e < 4 ? lo : hi) >> (8 * (e & 3))) & 0xFFu)) * (1.0f / 256.0f));
-      tmem_st8(tl + (uint32_t)j0, r);
+        q[e] = __float_as_uint((float)((((e < 4 ? lo : hi) >> (8 * (e & 3))) & 0xFFu)) * (1.0f / 256.0f));
+      tmem_st8(tl + (uint32_t)j0, q);
     }
   }
 }
@@ -361,8 +371,10 @@ __global__ void __launch_bounds__(kTcThreadsMlp, 1)
   } else if (warp >= 4) {   // ------------------------------------------------- epilogue
     const int q = warp & 3, m = q * 32 + lane;
     const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+    MlpA0 a0;
     if (blockIdx.x < ntiles) {
-      mlp_load_a0(states, stride, (int64_t)blockIdx.x * 128 + m, n, sh, feat_f32, tl);
+      mlp_fetch_a0(states, stride, (int64_t)blockIdx.x * 128 + m, n, feat_f32, a0);
+      mlp_store_a0(a0, feat_f32, tl);
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&a0_ready);
@@ -370,6 +382,9 @@ __global__ void __launch_bounds__(kTcThreadsMlp, 1)
     uint32_t i = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
       const int64_t node = t * 128 + m;
+      // the next tile's row: loads in flight during this tile's layer 1, stored after it
+      const bool has_next = t + gridDim.x < ntiles;
+      if (has_next) mlp_fetch_a0(states, stride, (t + gridDim.x) * 128 + m, n, feat_f32, a0);
       // layer 1: relu(D1 + b1) -> tf32 -> A1 (the same columns), four 16-column loads per wait
       mbar_wait_spin(&d1_full, i & 1u);
       tc_fence_after();
@@ -398,8 +413,8 @@ __global__ void __launch_bounds__(kTcThreadsMlp, 1)
       tc_fence_before();
       mbar_arrive(&a1_ready);
       // the next tile's features while layer 2 runs
-      if (t + gridDim.x < ntiles) {
-        mlp_load_a0(states, stride, (t + gridDim.x) * 128 + m, n, sh, feat_f32, tl);
+      if (has_next) {
+        mlp_store_a0(a0, feat_f32, tl);
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&a0_ready);
