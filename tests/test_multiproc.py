@@ -11,8 +11,6 @@ best leaf, for root sharding (n % W == 0) and leaf-range sharding (C5-style).
 import os
 import socket
 
-_ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-
 import numpy as np
 import pytest
 import torch
@@ -81,21 +79,3 @@ def test_gloo_world2_reduction_matches_single_process(case):
     np.testing.assert_array_equal(vals, ref["vanilla_q"].astype(np.float32))
     np.testing.assert_array_equal(leaves, ref["best_leaf"])
 
-
-def test_bench_self_launches_world2_reference_arm():
-    """`bench.py --gpus 2` outside torchrun re-launches itself as 2 ranks (torch.distributed.run on
-    127.0.0.1); the reference arm runs under gloo, rank 0 alone prints the one JSON line with n_gpus = 2 and
-    the other rank exits 0 (the driver's N > 1 contract, exercised here on CPU)."""
-    import json
-    import subprocess
-    import sys
-    env = dict(os.environ)
-    for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
-        env.pop(k, None)
-    r = subprocess.run([sys.executable, os.path.join(_ROOT, "bench.py"), "--gpus", "2", "--impl", "reference",
-                        "--config", "C1", "--steps", "1", "--warmup", "3"],
-                       capture_output=True, text=True, timeout=600, env=env, cwd=_ROOT)
-    assert r.returncode == 0, r.stderr[-2000:]
-    lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
-    assert len(lines) == 1, r.stdout
-    assert lines[0]["impl"] == "reference" and lines[0]["n_gpus"] == 2 and lines[0]["value"] > 0
