@@ -112,3 +112,48 @@ def test_tf32_is_opt_in():
     m = Oracle.from_config(cfg).search(roots, 2, float(np.float32(cfg.gamma)), 1.0, 1, mode=1, threads=THREADS)
     np.testing.assert_array_equal(a["vanilla_q"].cpu().numpy(), m["vanilla_q"].astype(np.float32))
     assert not np.array_equal(b["vanilla_q"].cpu().numpy(), m["vanilla_q"].astype(np.float32))
+
+
+def _host(out):
+    return {k: (v.cpu().numpy() if hasattr(v, "cpu") else v) for k, v in out.items()}
+
+
+@pytest.mark.parametrize("cname,n,d,ws", [("D10", 5, 4, 4 << 20), ("C2", 37, 4, (1 << 20) + 40 * 1000)])
+def test_tf32_chunking_and_shards_bit_identical(cname, n, d, ws):
+    """The tf32 path is deterministic per node (a tile's row sums do not depend on the other rows of the
+    tile), so chunked searches (small workspace) and virtual multi-GPU shards (max over packed keys) give
+    the unchunked search bit for bit, as on the fp32 path."""
+    cfg = cfg_of(cname)
+    roots = cfg.roots(n)
+    rd = dev(roots)
+    ref = _host(handle(cfg, P.F_TF32).search(rd, n, d, cfg.gamma, 1.0, 1, extra=True))
+    small = P.Handle.from_config(cfg, flags=P.F_TF32, workspace_bytes_max=ws)
+    ch = _host(small.search(rd, n, d, cfg.gamma, 1.0, 1, extra=True))
+    assert ch["stats"]["chunks"] > 1
+    h = handle(cfg, P.F_TF32)
+    keys = []
+    for rank in range(3):
+        b, e = P.shard_range(n, d, cfg.A, rank, 3)
+        k = torch.empty(n * cfg.A, dtype=torch.int64, device=DEV)
+        h.keys_init(k)
+        h.search_shard(rd, n, d, cfg.gamma, b, e, k)
+        keys.append(k)
+    red = torch.maximum(torch.maximum(keys[0], keys[1]), keys[2])
+    sh = _host(h.finalize(rd, n, d, cfg.gamma, 1.0, 1, red))
+    for key in ("actions", "root_q", "vanilla_q", "best_leaf"):
+        np.testing.assert_array_equal(ch[key], ref[key])
+        np.testing.assert_array_equal(sh[key], ref[key])
+    small.close()
+
+
+def test_tf32_pruned_bound_equals_unpruned():
+    """NEXT-4 on the tf32 path: the exact BOUND rule (R31) prunes only subtrees that cannot hold a group's
+    max, so the pruned search equals the unpruned tf32 search bit for bit."""
+    cfg = cfg_of("D10")
+    roots = cfg.roots(6)
+    h = handle(cfg, P.F_TF32)
+    ref = _host(h.search(dev(roots), 6, 4, cfg.gamma, 1.0, 1, extra=True))
+    out = _host(h.search_pruned(dev(roots), 6, 4, cfg.gamma, 1, 2, 1, -5.0, 5.0, -50.0, 50.0, beta=1.0,
+                                correction=1))
+    for key in ("actions", "root_q", "vanilla_q", "best_leaf"):
+        np.testing.assert_array_equal(out[key], ref[key])
