@@ -26,6 +26,7 @@ struct bcts_handle_t {
   int32_t *d_next = nullptr;
   float *d_envw = nullptr;   // DNN env image (dnn_repack)
   float *d_envw_tc = nullptr;   // DNN env image of the tf32 tensor-core path (dnn_tc_repack)
+  std::vector<float> envw_tc_bias;   // its biases [4][112] (host: a kernel parameter)
   EnvModel em;
   float *d_rew = nullptr;
   Net net;
@@ -954,6 +955,8 @@ bcts_status bcts_create(const bcts_config *cfg, bcts_handle *out) {
         return BCTS_ERR_CUDA;
       }
       h->em.dnn_tc = h->d_envw_tc;
+      h->envw_tc_bias.assign(tc.begin() + kDnnTcBiasOffset, tc.begin() + kDnnTcBiasOffset + 4 * 112);
+      h->em.dnn_tc_bias = h->envw_tc_bias.data();
     }
   }
   std::string err;

@@ -83,6 +83,7 @@ struct EnvModel {
   const float *tab_rew = nullptr;     // TABULAR [nS*A]
   const float *dnn = nullptr;         // DNN: smem image (kDnnImg floats) followed by W1A [A][100]
   const float *dnn_tc = nullptr;      // DNN, BCTS_F_TF32: the k_dnn_tc image (tf32_tc.cu)
+  const float *dnn_tc_bias = nullptr; // DNN, BCTS_F_TF32: HOST copy of the image's biases [4][112] (kernel parameter)
 };
 constexpr int kDnnS = 100;                         // DNN state width
 constexpr int kDnnImg = 3 * 10000 + 10400 + 404;   // W1T|W2T|W3T|W4T[100][104]|b1|b2|b3|b4[104] floats
@@ -100,7 +101,9 @@ size_t dnn_tc_image_floats(int A);
 void dnn_tc_repack(const float *blob, int A, float *out);
 bool dnn_tc_ok(int A);
 void launch_expand_dnn_tc(const NodeView &par, int64_t p_first, int64_t c_begin, int64_t c_end, int A, float gk,
-                          const float *img, const NodeOut &out, cudaStream_t st, Profiler *prof);
+                          const float *img, const float *bias_host, const NodeOut &out, cudaStream_t st,
+                          Profiler *prof);
+constexpr size_t kDnnTcBiasOffset = 4 * 26 * 112 * 4;   // floats of the image before the biases (4 layer images)
 size_t mlp_tc_image_bytes(int I, int H, int A);
 bool mlp_tc_ok(int I, int H, int A);
 void mlp_tc_repack(const float *w1, const float *b1, const float *w2, const float *b2, int I, int H, int A,

@@ -128,7 +128,7 @@ void launch_expand(int env, const NodeView &par, int64_t p_first, int64_t c_begi
   if (n <= 0) return;
   const int64_t nparents = (c_end - 1) / A - c_begin / A + 1;
   if (env == BCTS_ENV_DNN) {
-    if (em.dnn_tc) launch_expand_dnn_tc(par, p_first, c_begin, c_end, A, gk, em.dnn_tc, out, st, prof);
+    if (em.dnn_tc) launch_expand_dnn_tc(par, p_first, c_begin, c_end, A, gk, em.dnn_tc, em.dnn_tc_bias, out, st, prof);
     else launch_expand_dnn(par, p_first, c_begin, c_end, A, gk, em.dnn, out, st, prof);
     return;
   }

@@ -31,6 +31,7 @@ constexpr int kTcN = 112;            // DNN layer outputs (100, or 101 for the l
 constexpr uint32_t kTcPlane = kTcN * 16;                       // one 4-wide K chunk of a DNN layer
 constexpr uint32_t kTcLayerBytes = (kTcK / 4) * kTcPlane;      // 46,592 B per DNN layer image
 constexpr int kTcDnnFloats = (int)(4 * kTcLayerBytes / 4) + 4 * kTcN;   // 4 layers + biases [4][112]
+static_assert(kDnnTcBiasOffset == 4 * kTcLayerBytes / 4 && kTcN == 112, "engine.h's bias offset");
 
 // K-major SWIZZLE_NONE descriptor: LBO = K-chunk stride, SBO = 8-row-group stride (128 B).
 __device__ __forceinline__ uint64_t desc_kmajor(uint32_t addr, uint32_t plane_bytes) {
@@ -75,9 +76,12 @@ __device__ __forceinline__ void load_weights(uint8_t *dst, const void *src, uint
 // 0..99 = s', unit 100 = r; R' = fmaf(gk, r, R). The action part of layer 1 is the one-hot column
 // W1[:, 100 + a], added in fp32 in the epilogue (exact: the one-hot product is the weight itself).
 // TMEM per slot s: A at columns 256 s .. +104, D at 256 s + 128 .. +112.
+struct DnnTcBias {   // the four layers' biases as a kernel parameter: constant-bank operands of the FADDs
+  float b[4][kTcN];
+};
 __global__ void __launch_bounds__(kTcThreadsDnn, 1)
     k_dnn_tc(NodeView par, int64_t p_first, int64_t c_begin, int64_t c_end, int A, float gk,
-             const float *__restrict__ img, NodeOut out) {
+             const float *__restrict__ img, NodeOut out, const __grid_constant__ DnnTcBias bias) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((128u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 127u)) & 127u);
   const float *sB = (const float *)(smem + 4 * kTcLayerBytes);   // biases [4][112]
@@ -169,10 +173,11 @@ __global__ void __launch_bounds__(kTcThreadsDnn, 1)
       }
       const float rpar = valid && par.cum ? par.cum[p - p_first] : 0.0f;
       float *srow = (float *)(out.state + (valid ? c - c_begin : 0) * out.state_stride);
+#pragma unroll
       for (int L = 0; L < 4; ++L) {
         mbar_wait_spin(&d_full[s], (uint32_t)L & 1u);
         tc_fence_after();
-        const float *b = sB + L * kTcN;
+        const float *b = bias.b[L];
         auto proc = [&](int j0, const uint32_t(&v)[16]) {
           if (L < 3) {   // hidden layer: relu(D + b (+ W1[:, 100 + a])) -> tf32 -> A columns j0..
             uint32_t r[16];
@@ -488,7 +493,8 @@ void dnn_tc_repack(const float *blob, int A, float *out) {
 static size_t dnn_tc_smem(int A) { return dnn_tc_image_floats(A) * 4 + 128; }
 
 void launch_expand_dnn_tc(const NodeView &par, int64_t p_first, int64_t c_begin, int64_t c_end, int A, float gk,
-                          const float *img, const NodeOut &out, cudaStream_t st, Profiler *prof) {
+                          const float *img, const float *bias_host, const NodeOut &out, cudaStream_t st,
+                          Profiler *prof) {
   const int64_t n = c_end - c_begin;
   if (n <= 0) return;
   const int64_t nparents = (c_end - 1) / A - c_begin / A + 1;
@@ -498,7 +504,9 @@ void launch_expand_dnn_tc(const NodeView &par, int64_t p_first, int64_t c_begin,
   smem_optin((const void *)k_dnn_tc, (int)smem);
   const int64_t tiles = (n + 127) / 128;
   const unsigned grid = (unsigned)std::min<int64_t>((tiles + 1) / 2, sm_count_current());
-  launch_pdl(k_dnn_tc, dim3(grid), dim3(kTcThreadsDnn), smem, st, par, p_first, c_begin, c_end, A, gk, img, out);
+  DnnTcBias bias;
+  memcpy(bias.b, bias_host, sizeof(bias.b));
+  launch_pdl(k_dnn_tc, dim3(grid), dim3(kTcThreadsDnn), smem, st, par, p_first, c_begin, c_end, A, gk, img, out, bias);
   if (prof) prof->end(st);
 }
 
