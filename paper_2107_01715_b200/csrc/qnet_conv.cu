@@ -305,17 +305,19 @@ __device__ __forceinline__ uint32_t u8pair_f16x2(uint32_t w, uint32_t sel) {
   return h2_minus1024(__byte_perm(w, 0x64646464u, sel));
 }
 // Converter warp-task T (0..27) and lane -> noise group (0..881) or -1. s2d row band Y = the 4 frame
-// rows 4Y..4Y+3 (42 groups). Tasks 0-20: band T, lane = (row j = lane/8, first quad X = 2(lane%8) +
-// (j&1)): the 8-byte slot of quad (j, X) is (j + 2X + 10Y) mod 16, so both store instructions of the
-// task hit all 16 bank pairs exactly twice. Tasks 21-27: the 10 remaining groups of bands 3(T-21) ..
-// +2 (first quads X = 16/18/20 on rows 0, 2 and 17/19 on rows 1, 3), <= 3 lanes per bank pair;
-// lanes 30, 31 of those tasks get -1 (the caller gives them a duplicate of lanes 28, 29).
+// rows 4Y..4Y+3 (42 groups k = 0..41 of group 42Y + k). An 8-byte store instruction is served per
+// half-warp (measured: ncu counts 4 wavefronts, not 2, when only the whole warp covers the banks), so
+// tasks 0-20 (band T) give lanes 0-15 the groups k = {0..3, 11..14, 21..24, 32..35} and lanes 16-31
+// those + 4: in each half the 16 stores of quad h (h = 0, 1) hit 16 distinct bank pairs (a perfect
+// matching of the groups' (quad 0, quad 1) bank pairs; one wavefront per half). Tasks 21-27: the 10
+// remaining groups of bands 3(T-21) .. +2 (first quads X = 16/18/20 on rows 0, 2 and 17/19 on rows
+// 1, 3); lanes 30, 31 of those tasks get -1 (the caller gives them a duplicate of lanes 28, 29).
 __device__ __forceinline__ int sib_group(int T, int i) {
   int Y, j, X;
   if (T < 21) {
-    Y = T;
-    j = i >> 3;
-    X = 2 * (i & 7) + (j & 1);
+    const int ii = i & 15;
+    const int row4 = ii >> 2;   // base k = 0, 11, 21, 32
+    return 42 * T + 10 * row4 + ((row4 + 1) >> 1) + (ii & 3) + 4 * (i >> 4);
   } else {
     if (i >= 30) return -1;
     Y = 3 * (T - 21) + i / 10;
