@@ -572,3 +572,79 @@ def test_int_hash_mlp2_leaf_value_matches_torch():
         q = F.linear(F.relu(F.linear(x, W["l1.w"], W["l1.b"])), W["l2.w"], W["l2.b"]).numpy()
         np.testing.assert_allclose(o.qrow(s, mode=0), q, rtol=0, atol=1e-12)
         np.testing.assert_allclose(o.qrow(s, mode=1), q, rtol=0, atol=5e-6)
+
+
+# ------------------------------------------------ hash env steps pinned to published hash vectors
+# ENV_SPEC builds both synthetic envs from two standard mixers. They are pinned here to
+# values published with the mixers themselves, so the env steps below are checked against a reference
+# that is not the oracle's code: splitmix64 (Steele, Lea & Flood 2014 / Vigna's SplitMix64) from seed
+# 1234567 yields 6457827717110365317, 3203168211198807973, 9817491932198370423, 4593380528125082431,
+# 16408922859458223821; MurmurHash3's fmix32 maps 0 -> 0 and 1 -> 0x514E28B7.
+_M64 = (1 << 64) - 1
+
+
+def _splitmix64_finalizer(z):
+    z ^= z >> 30
+    z = (z * 0xBF58476D1CE4E5B9) & _M64
+    z ^= z >> 27
+    z = (z * 0x94D049BB133111EB) & _M64
+    return z ^ (z >> 31)
+
+
+def _fmix32(h):
+    h ^= h >> 16
+    h = (h * 0x85EBCA6B) & 0xFFFFFFFF
+    h ^= h >> 13
+    h = (h * 0xC2B2AE35) & 0xFFFFFFFF
+    return h ^ (h >> 16)
+
+
+def test_mixers_match_published_vectors():
+    s, out = 1234567, []
+    for _ in range(5):
+        s = (s + 0x9E3779B97F4A7C15) & _M64
+        out.append(_splitmix64_finalizer(s))
+    assert out == [6457827717110365317, 3203168211198807973, 9817491932198370423, 4593380528125082431,
+                   16408922859458223821]
+    assert _fmix32(0) == 0 and _fmix32(1) == 0x514E28B7
+
+
+def test_atari_hash_step_is_the_env_spec_over_splitmix64():
+    """ATARI_HASH step (ENV_SPEC, frame stack P:355) with the pinned splitmix64: k' = mix64(key ^
+    0x9E3779B97F4A7C15 (a + 1)); pixel p: new top byte = old top byte ^ byte p % 8 of mix64(k' + p / 8),
+    the other three frames shift down; r = +1 / -1 / 0 from k' >> 61 = 7 / 0 / else."""
+    cfg = config("C3")
+    o = Oracle.from_config(cfg)
+    roots = atari_roots(3, 4242)
+    for rec in roots:
+        key = int(rec[:8].view(np.uint64)[0])
+        words = rec[16:].view(np.uint32).astype(np.uint64)
+        for a in (0, 7, 17):
+            child, r = o.step(rec, a)
+            k2 = _splitmix64_finalizer(key ^ ((0x9E3779B97F4A7C15 * (a + 1)) & _M64))
+            assert int(child[:8].view(np.uint64)[0]) == k2
+            assert r == (1.0 if k2 >> 61 == 7 else -1.0 if k2 >> 61 == 0 else 0.0)
+            noise = np.array([(_splitmix64_finalizer((k2 + p // 8) & _M64) >> (8 * (p % 8))) & 0xFF
+                              for p in range(words.size)], dtype=np.uint64)
+            want = (words >> np.uint64(8)) | (((words >> np.uint64(24)) ^ noise) << np.uint64(24))
+            np.testing.assert_array_equal(child[16:].view(np.uint32), want.astype(np.uint32))
+
+
+def test_int_hash_step_is_the_env_spec_over_fmix32():
+    """INT_HASH step (ENV_SPEC) with the pinned fmix32: s'[w] = fmix32(s[w] ^ rotl(s[w + 1 mod 16], 13) ^
+    0x9E3779B9 (a + 1) ^ 0x85EBCA6B w); r = +1 / -1 / 0 from s'[0] >> 30 = 3 / 0 / else."""
+    cfg = config("C2")
+    o = Oracle.from_config(cfg)
+    for rec in int_roots(4, 4343):
+        s = [int(x) for x in rec.view(np.uint32)]
+        for a in range(4):
+            child, r = o.step(rec, a)
+            want = []
+            for w in range(16):
+                nx = s[(w + 1) % 16]
+                rot = ((nx << 13) | (nx >> 19)) & 0xFFFFFFFF
+                v = s[w] ^ rot ^ ((0x9E3779B9 * (a + 1)) & 0xFFFFFFFF) ^ ((0x85EBCA6B * w) & 0xFFFFFFFF)
+                want.append(_fmix32(v))
+            assert [int(x) for x in child.view(np.uint32)] == want
+            t = want[0] >> 30
+            assert r == (1.0 if t == 3 else -1.0 if t == 0 else 0.0)
