@@ -388,6 +388,10 @@ bcts_status run_shard(bcts_handle h, const void *roots, int32_t d, float gamma, 
     NodeView prev = root_view(h->env, roots, lo[0]);
     int64_t vbase = lo[0];   // global level index of prev's element 0
     int expanded = 0;
+    // the tf32 DNN forward model expands all of the chunk's levels in one cooperative launch
+    const bool multi_level = h->env == BCTS_ENV_DNN && h->em.dnn_tc;
+    DnnTcLevel mlev[kMaxDepth];
+    int n_mlev = 0;
     for (int k = 1; k <= dm; ++k) {
       if (k == 1 && pf && pf->ne) {   // level 1 = the prologue front end's children (slots n .. n + nA)
         const int64_t nr = pf->ne / (A + 1);
@@ -400,10 +404,28 @@ bcts_status run_shard(bcts_handle h, const void *roots, int32_t d, float gamma, 
         continue;
       }
       const LevelBuf &b = ((dm - k) % 2 == 0) ? big : small;
-      launch_expand(h->env, prev, vbase, lo[k], hi[k], A, g[k - 1], h->em, out_of(h->env, b), h->st, &h->prof);
+      if (multi_level) {   // gathered: all levels in one cooperative launch below
+        DnnTcLevel &lv = mlev[n_mlev++];
+        lv.par = prev;
+        lv.p_first = vbase;
+        lv.c_begin = lo[k];
+        lv.c_end = hi[k];
+        lv.gk = g[k - 1];
+        lv.out = out_of(h->env, b);
+      } else {
+        launch_expand(h->env, prev, vbase, lo[k], hi[k], A, g[k - 1], h->em, out_of(h->env, b), h->st, &h->prof);
+        ++lvl_launch;
+        ++expanded;
+      }
       prev = view_of(h->env, b);
       vbase = lo[k];
       trans += hi[k] - lo[k];
+    }
+    if (n_mlev) {
+      if (launch_expand_dnn_tc_levels(mlev, n_mlev, A, h->em.dnn_tc, h->em.dnn_tc_bias, h->st, &h->prof)) {
+        const cudaError_t e = cudaGetLastError();
+        return fail(h, BCTS_ERR_CUDA, std::string("multi-level DNN expansion launch: ") + cudaGetErrorString(e));
+      }
       ++lvl_launch;
       ++expanded;
     }

@@ -103,6 +103,20 @@ bool dnn_tc_ok(int A);
 void launch_expand_dnn_tc(const NodeView &par, int64_t p_first, int64_t c_begin, int64_t c_end, int A, float gk,
                           const float *img, const float *bias_host, const NodeOut &out, cudaStream_t st,
                           Profiler *prof);
+// several consecutive levels (level k+1's parents = level k's output) in ONE cooperative launch: the
+// weights and TMEM stay put and a grid barrier separates the levels; nonzero if the launch failed
+struct DnnTcLevel {
+  NodeView par;
+  int64_t p_first = 0, c_begin = 0, c_end = 0;
+  float gk = 0.f;
+  NodeOut out;
+};
+struct DnnTcLevels {
+  int n = 0;
+  DnnTcLevel lv[kMaxDepth];
+};
+int launch_expand_dnn_tc_levels(const DnnTcLevel *lvs, int nlev, int A, const float *img, const float *bias_host,
+                                cudaStream_t st, Profiler *prof);
 constexpr size_t kDnnTcBiasOffset = 4 * 26 * 112 * 4;   // floats of the image before the biases (4 layer images)
 size_t mlp_tc_image_bytes(int I, int H, int A);
 bool mlp_tc_ok(int I, int H, int A);

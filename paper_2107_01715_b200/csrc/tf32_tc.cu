@@ -18,8 +18,12 @@
 #include <algorithm>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "engine.h"
 #include "ptx.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace bcts {
 namespace {
@@ -79,9 +83,13 @@ __device__ __forceinline__ void load_weights(uint8_t *dst, const void *src, uint
 struct DnnTcBias {   // the four layers' biases as a kernel parameter: constant-bank operands of the FADDs
   float b[4][kTcN];
 };
+// One launch may expand several consecutive levels (DnnTcLevels.n > 1, cooperative launch): every CTA
+// keeps the weights and TMEM across the levels and a grid-wide barrier separates them (level k+1's
+// parents are level k's children, written by other CTAs). Parent states are read through L2 (ld.cg),
+// never the non-coherent path, since they may have been written earlier in the same launch.
 __global__ void __launch_bounds__(kTcThreadsDnn, 1)
-    k_dnn_tc(NodeView par, int64_t p_first, int64_t c_begin, int64_t c_end, int A, float gk,
-             const float *__restrict__ img, NodeOut out, const __grid_constant__ DnnTcBias bias) {
+    k_dnn_tc(const __grid_constant__ DnnTcLevels levels, int A, const float *__restrict__ img,
+             const __grid_constant__ DnnTcBias bias) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((128u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 127u)) & 127u);
   const float *sB = (const float *)(smem + 4 * kTcLayerBytes);   // biases [4][112]
@@ -109,6 +117,12 @@ __global__ void __launch_bounds__(kTcThreadsDnn, 1)
   const uint32_t tmem = tmem_slot;
   pdl_wait();      // parent states: the previous kernel's output (the weight copy above overlaps its tail)
   pdl_trigger();
+  for (int lv = 0; lv < levels.n; ++lv) {
+  const DnnTcLevel &LV = levels.lv[lv];
+  const NodeView &par = LV.par;
+  const NodeOut &out = LV.out;
+  const int64_t p_first = LV.p_first, c_begin = LV.c_begin, c_end = LV.c_end;
+  const float gk = LV.gk;
   const int64_t n = c_end - c_begin, ntiles = (n + 127) / 128;
 
   if (warp == 0) {   // ---------------------------------------------------------- MMA issuer
@@ -148,7 +162,7 @@ __global__ void __launch_bounds__(kTcThreadsDnn, 1)
         const float4 *ps = (const float4 *)(par.state + (p - p_first) * par.state_stride);
         float4 x4[kDnnS / 4];   // all 25 loads in flight at once (one L2 round trip, not four)
 #pragma unroll
-        for (int e = 0; e < kDnnS / 4; ++e) x4[e] = valid ? __ldg(ps + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int e = 0; e < kDnnS / 4; ++e) x4[e] = valid ? __ldcg(ps + e) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
         for (int j0 = 0; j0 < kTcK; j0 += 32) {
           uint32_t r[32];
@@ -171,7 +185,7 @@ __global__ void __launch_bounds__(kTcThreadsDnn, 1)
         tc_fence_before();
         mbar_arrive(&a_ready[s]);
       }
-      const float rpar = valid && par.cum ? par.cum[p - p_first] : 0.0f;
+      const float rpar = valid && par.cum ? __ldcg(par.cum + (p - p_first)) : 0.0f;
       float *srow = (float *)(out.state + (valid ? c - c_begin : 0) * out.state_stride);
 #pragma unroll
       for (int L = 0; L < 4; ++L) {
@@ -240,6 +254,11 @@ __global__ void __launch_bounds__(kTcThreadsDnn, 1)
       }
     }
   }
+  if (lv + 1 < levels.n) {   // the whole level written before any CTA reads it as parents
+    __threadfence();
+    cg::this_grid().sync();
+  }
+  }   // levels
   tc_fence_before();
   __syncthreads();
   if (warp == 0) {
@@ -495,19 +514,47 @@ static size_t dnn_tc_smem(int A) { return dnn_tc_image_floats(A) * 4 + 128; }
 void launch_expand_dnn_tc(const NodeView &par, int64_t p_first, int64_t c_begin, int64_t c_end, int A, float gk,
                           const float *img, const float *bias_host, const NodeOut &out, cudaStream_t st,
                           Profiler *prof) {
-  const int64_t n = c_end - c_begin;
-  if (n <= 0) return;
-  const int64_t nparents = (c_end - 1) / A - c_begin / A + 1;
-  // the same algorithmic FLOPs as the fp32 path (launch_expand_dnn)
-  if (prof) prof->begin(KC_EXPAND_DNN, 2.0 * (30100.0 * (double)n + 10000.0 * (double)nparents), st);
+  DnnTcLevel lv;
+  lv.par = par;
+  lv.p_first = p_first;
+  lv.c_begin = c_begin;
+  lv.c_end = c_end;
+  lv.gk = gk;
+  lv.out = out;
+  launch_expand_dnn_tc_levels(&lv, 1, A, img, bias_host, st, prof);
+}
+
+int launch_expand_dnn_tc_levels(const DnnTcLevel *lvs, int nlev, int A, const float *img, const float *bias_host,
+                                cudaStream_t st, Profiler *prof) {
+  DnnTcLevels L;
+  L.n = 0;
+  double flops = 0.0;
+  int64_t max_tiles = 0;
+  for (int k = 0; k < nlev; ++k) {
+    const int64_t n = lvs[k].c_end - lvs[k].c_begin;
+    if (n <= 0) continue;
+    const int64_t nparents = (lvs[k].c_end - 1) / A - lvs[k].c_begin / A + 1;
+    // the same algorithmic FLOPs as the fp32 path (launch_expand_dnn)
+    flops += 2.0 * (30100.0 * (double)n + 10000.0 * (double)nparents);
+    max_tiles = std::max<int64_t>(max_tiles, (n + 127) / 128);
+    L.lv[L.n++] = lvs[k];
+  }
+  if (!L.n) return 0;
+  if (prof) prof->begin(KC_EXPAND_DNN, flops, st);
   const size_t smem = dnn_tc_smem(A);
   smem_optin((const void *)k_dnn_tc, (int)smem);
-  const int64_t tiles = (n + 127) / 128;
-  const unsigned grid = (unsigned)std::min<int64_t>((tiles + 1) / 2, sm_count_current());
+  const unsigned grid = (unsigned)std::min<int64_t>((max_tiles + 1) / 2, sm_count_current());
   DnnTcBias bias;
   memcpy(bias.b, bias_host, sizeof(bias.b));
-  launch_pdl(k_dnn_tc, dim3(grid), dim3(kTcThreadsDnn), smem, st, par, p_first, c_begin, c_end, A, gk, img, out, bias);
+  cudaError_t e;
+  if (L.n == 1) {
+    e = launch_pdl(k_dnn_tc, dim3(grid), dim3(kTcThreadsDnn), smem, st, L, A, img, bias);
+  } else {   // grid-wide barriers between the levels: every CTA must be resident (one per SM)
+    void *args[] = {(void *)&L, (void *)&A, (void *)&img, (void *)&bias};
+    e = cudaLaunchCooperativeKernel((const void *)k_dnn_tc, dim3(grid), dim3(kTcThreadsDnn), args, smem, st);
+  }
   if (prof) prof->end(st);
+  return e == cudaSuccess ? 0 : -1;
 }
 
 bool dnn_tc_ok(int A) { return dnn_tc_smem(A) <= 227 * 1024 - 1024; }
