@@ -155,11 +155,12 @@ def test_conv_nets_small_trees(cname, n, d):
 
 
 @pytest.mark.parametrize("net,A,n,d", [(NET_RAINBOW_BF16, 7, 2, 2), (NET_RAINBOW_BF16, 2, 3, 3),
-                                        (NET_RAINBOW_BF16, 33, 1, 1), (NET_NATURE_BF16, 5, 2, 2)])
+                                        (NET_RAINBOW_BF16, 33, 1, 1), (NET_NATURE_BF16, 5, 2, 2),
+                                        (NET_RAINBOW_BF16, 64, 1, 2), (NET_NATURE_BF16, 64, 2, 1)])
 def test_conv_nets_unusual_action_counts(net, A, n, d):
     """Action counts that are not multiples of the head's 4-action chunks or of the expansion's
-    CTA split (A = 7, 5), the minimum A = 2, and A > 32 (two lanes per action in the finalize warp),
-    against the oracle."""
+    CTA split (A = 7, 5), the minimum A = 2, A > 32 (two lanes per action in the finalize warp) and the
+    maximum A = 64 (the fused head's 16 action chunks), against the oracle."""
     cfg = Config(f"A{A}", ENV_ATARI_HASH, net, A, d, n, 0.99, 1.0, seed=40 + A, wseed=140 + A)
     h = handle(cfg)
     o = Oracle.from_config(cfg)

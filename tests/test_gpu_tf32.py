@@ -157,3 +157,22 @@ def test_tf32_pruned_bound_equals_unpruned():
                                 correction=1))
     for key in ("actions", "root_q", "vanilla_q", "best_leaf"):
         np.testing.assert_array_equal(out[key], ref[key])
+
+
+def test_max_action_count_mlp_fp32_and_tf32():
+    """A = 64 (the ABI's maximum; 4 N = 16 chunks of layer 2 in k_mlp_tc) on the INT_HASH env with the
+    MLP2 net: the fp32 default bit-exact vs the oracle's fp32 mirror, the tf32 path within R34's
+    tolerance of the fp64 oracle."""
+    from synth.inputs import Config, ENV_INT_HASH, NET_MLP2_F32
+    cfg = Config("I64", ENV_INT_HASH, NET_MLP2_F32, 64, 2, 12, 0.99, 1.0, seed=64, wseed=164)
+    roots = cfg.roots()
+    o = Oracle.from_config(cfg)
+    g32 = float(np.float32(cfg.gamma))
+    a = _host(handle(cfg, 0).search(dev(roots), 12, 2, cfg.gamma, 1.0, 1, extra=True))
+    m = o.search(roots, 2, g32, 1.0, 1, mode=1, threads=THREADS)
+    np.testing.assert_array_equal(a["vanilla_q"], m["vanilla_q"].astype(np.float32))
+    np.testing.assert_array_equal(a["actions"], m["actions"])
+    b = _host(handle(cfg, P.F_TF32).search(dev(roots), 12, 2, cfg.gamma, 1.0, 1, extra=True))
+    r = o.search(roots, 2, g32, 1.0, 1, mode=0, threads=THREADS)
+    assert rel_err(b["root_q"], r["root_q"]).max() <= RTOL_TF32
+    assert action_agreement(b["actions"], r["root_q"], RTOL_TF32)[0] >= 0.999
