@@ -176,3 +176,16 @@ def test_max_action_count_mlp_fp32_and_tf32():
     r = o.search(roots, 2, g32, 1.0, 1, mode=0, threads=THREADS)
     assert rel_err(b["root_q"], r["root_q"]).max() <= RTOL_TF32
     assert action_agreement(b["actions"], r["root_q"], RTOL_TF32)[0] >= 0.999
+
+
+def test_tf32_deep_tree_error_does_not_grow():
+    """D2 at depth 12 (48 tf32 layer applications on the deepest paths, one cooperative launch for the 12
+    levels): root Q stays within the same R34 tolerance of the fp64 oracle as at depth 8."""
+    cfg = cfg_of("D2")
+    roots = cfg.roots(8)
+    out = _host(handle(cfg, P.F_TF32).search(dev(roots), 8, 12, cfg.gamma, 1.0, 1, extra=True))
+    r = Oracle.from_config(cfg).search(roots, 12, float(np.float32(cfg.gamma)), 1.0, 1, mode=0, threads=THREADS)
+    eq = rel_err(out["root_q"], r["root_q"]).max()
+    print(f"D2 d=12: root_q rel err {eq:.2e}")
+    assert eq <= RTOL_TF32
+    assert action_agreement(out["actions"], r["root_q"], RTOL_TF32)[0] >= 0.999
