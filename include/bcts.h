@@ -105,8 +105,10 @@ typedef enum {
 #define BCTS_F_TF32 0x40u /* NEXT-1 on the tensor cores: the DNN forward model (BCTS_ENV_DNN) and the MLP2
                            * net run as tcgen05 kind::tf32 GEMMs (operands rounded to tf32, fp32
                            * accumulation in the MMA's order). NOT bit-exact with the fp32 default:
-                           * within the tf32 tolerance of the fp64 oracle (R34). Other
-                           * envs / nets ignore it. */
+                           * within the tf32 tolerance of the fp64 oracle (R34). A DNN
+                           * search expands each chunk's levels in one cooperative launch (one CTA
+                           * per SM, all resident): if that launch cannot be made (e.g. another
+                           * context holds SMs) the call fails with CUDA. Other envs / nets ignore it. */
 
 typedef struct {
   uint32_t abi_version;     /* must be BCTS_ABI_VERSION */
