@@ -409,72 +409,74 @@ __global__ void __launch_bounds__(kSibThreads, 1)
     const uint32_t elected = elect_one();
     mbar_wait(&wbar, 0);
     const uint64_t wsh = desc_sw128(saddr(sWsh)), wnw = desc_sw128(saddr(sWnw));
-    // shared part P(q): 4 tiles x 4 taps x 3 K-steps into TMEM buffer q & 1
-    auto issue_shared = [&](int64_t q) {
+    // shared part P(q): 4 tiles x 4 taps x 3 K-steps into TMEM buffer q & 1. Descriptors are the
+    // ring / buffer base descriptor plus constant row offsets (16-byte units in the address field).
+    const uint64_t dsh0 = desc_planar(saddr(sSh), kSibPlane), dnw0 = desc_planar(saddr(sNw), kSibPlane);
+    auto issue_shared = [&](int q) {
       const uint32_t sb = (uint32_t)q & 1u;
       tc_fence_after();
-      const uint32_t abase = saddr(sSh + sb * kSharedBytes);
+      const uint64_t db = dsh0 + ((sb * kSharedBytes) >> 4);
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
         for (int tap = 0; tap < 4; ++tap)
 #pragma unroll
           for (int kk = 0; kk < 3; ++kk) {
-            const uint32_t a = abase + (uint32_t)(2 * kk) * kSibPlane +
-                               (uint32_t)(mt * 128 + (tap >> 1) * 21 + (tap & 1)) * 16u;
+            const uint32_t a_off = (uint32_t)(2 * kk) * (kSibPlane >> 4) + (uint32_t)(mt * 128 + (tap >> 1) * 21 + (tap & 1));
             const int kw = tap * 48 + 16 * kk;
             const uint32_t w_off = (uint32_t)(kw >> 6) * (N * 128) + (uint32_t)((kw & 63) * 2);
-            mma_pred(tmem + sb * 128 + (uint32_t)(mt * N), desc_planar(a, kSibPlane), wsh + (w_off >> 4), idesc,
-                     (tap | kk) != 0, elected);
+            mma_pred(tmem + sb * 128 + (uint32_t)(mt * N), db + a_off, wsh + (w_off >> 4), idesc, (tap | kk) != 0,
+                     elected);
           }
       commit_pred(&sh_empty[sb], elected);
       commit_pred(&p_full[sb], elected);
     };
-    int64_t cur_p = -1, issued = -1;   // highest parent whose P has been issued
-    uint32_t j = 0;
-    int64_t k = 0;                     // parent of the current child, relative to pfirst_cta
-    int ca = (int)(c_begin + i0 - pfirst_cta * A);   // child index within its parent (no per-child division)
-    for (int64_t img = i0; img < i1; ++img, ++j, ++ca) {
-      if (ca == A) { ca = 0; ++k; }
-      const int64_t p = pfirst_cta + k;
-      if (p != cur_p) {
-        if (issued < k) {      // P(k) not issued ahead (first parent, or the lookahead found it not ready)
-          const uint32_t sb = (uint32_t)k & 1u, ph = (uint32_t)(k >> 1) & 1u;
-          mbar_wait(&sh_full[sb], ph);
-          mbar_wait(&p_empty[sb], ph ^ 1u);
-          issue_shared(k);
-          issued = k;
-        }
-        cur_p = p;
+    // parents outer, children inner (32-bit counters); the waits spin: this warp's loop is on the
+    // critical path (the tensor pipe idles while it does anything but issue)
+    int issued = -1;                   // highest parent whose P has been issued
+    uint32_t j = 0, nb = 0, nph = 0;   // child counter; new-image ring slot / phase
+    int a0 = (int)(c_begin + i0 - pfirst_cta * A);   // first child's index within its parent
+    int64_t img = i0;
+    for (int kq = 0; kq < (int)npar; ++kq) {
+      if (issued < kq) {   // P(kq) not issued ahead (first parent, or the lookahead found it not ready)
+        const uint32_t sb = (uint32_t)kq & 1u, ph = ((uint32_t)kq >> 1) & 1u;
+        mbar_wait_spin(&sh_full[sb], ph);
+        mbar_wait_spin(&p_empty[sb], ph ^ 1u);
+        issue_shared(kq);
+        issued = kq;
       }
-      // new frame of child img: 4 tiles x 4 taps x 1 K-step
-      const uint32_t nb = j % kNewRing, nph = (j / kNewRing) & 1u;
-      const uint32_t cb = j & 1u, cph = (j >> 1) & 1u;
-      mbar_wait(&n_full[nb], nph);
-      mbar_wait(&c_empty[cb], cph ^ 1u);
-      tc_fence_after();
-      const uint32_t nbase = saddr(sNw + nb * kNewBytes);
+      const int a_end = (int)(i1 - img < (int64_t)(A - a0) ? a0 + (i1 - img) : (int64_t)A);
+      for (int a = a0; a < a_end; ++a, ++img, ++j) {
+        // new frame of child img: 4 tiles x 4 taps x 1 K-step
+        const uint32_t cb = j & 1u, cph = (j >> 1) & 1u;
+        mbar_wait_spin(&n_full[nb], nph);
+        mbar_wait_spin(&c_empty[cb], cph ^ 1u);
+        tc_fence_after();
+        const uint64_t dn = dnw0 + ((nb * kNewBytes) >> 4);
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt)
+        for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-        for (int tap = 0; tap < 4; ++tap) {
-          const uint32_t a = nbase + (uint32_t)(mt * 128 + (tap >> 1) * 21 + (tap & 1)) * 16u;
-          const uint32_t w_off = (uint32_t)((tap * 16) * 2);
-          mma_pred(tmem + 256 + cb * 128 + (uint32_t)(mt * N), desc_planar(a, kSibPlane), wnw + (w_off >> 4), idesc,
-                   tap != 0, elected);
+          for (int tap = 0; tap < 4; ++tap)
+            mma_pred(tmem + 256 + cb * 128 + (uint32_t)(mt * N), dn + (uint32_t)(mt * 128 + (tap >> 1) * 21 + (tap & 1)),
+                     wnw + (uint32_t)((tap * 16 * 2) >> 4), idesc, tap != 0, elected);
+        commit_pred(&n_empty[nb], elected);
+        commit_pred(&c_full[cb], elected);
+        if (++nb == (uint32_t)kNewRing) {
+          nb = 0;
+          nph ^= 1u;
         }
-      commit_pred(&n_empty[nb], elected);
-      commit_pred(&c_full[cb], elected);
-      // lookahead: P(k+1) as soon as its shared image and TMEM buffer are ready (warp-uniform test)
-      if (issued == k && k + 1 < npar) {
-        const uint32_t sb = (uint32_t)(k + 1) & 1u, ph = (uint32_t)((k + 1) >> 1) & 1u;
-        const uint32_t ready = (mbar_test(&sh_full[sb], ph) && mbar_test(&p_empty[sb], ph ^ 1u)) ? 1u : 0u;
-        if (__shfl_sync(0xffffffffu, ready, 0)) {
-          issue_shared(k + 1);
-          issued = k + 1;
+        // lookahead: P(kq+1) as soon as its shared image and TMEM buffer are ready (warp-uniform test)
+        if (issued == kq && kq + 1 < (int)npar) {
+          const uint32_t sb = (uint32_t)(kq + 1) & 1u, ph = ((uint32_t)(kq + 1) >> 1) & 1u;
+          const uint32_t ready = (mbar_test(&sh_full[sb], ph) && mbar_test(&p_empty[sb], ph ^ 1u)) ? 1u : 0u;
+          if (__shfl_sync(0xffffffffu, ready, 0)) {
+            issue_shared(kq + 1);
+            issued = kq + 1;
+          }
         }
+        __syncwarp();
       }
-      __syncwarp();
+      a0 = 0;
     }
   } else if (warp < 9) {
     // ---------------------------------------------- epilogue: relu(P + C_a + b) -> conv2's s2d(2) SW128 input
@@ -504,15 +506,13 @@ __global__ void __launch_bounds__(kSibThreads, 1)
       else soff2[mt >> 1] = o;
     }
     uint32_t vp[4][16];
-    int64_t cur_p = -1;
     uint32_t j = 0;
-    int64_t kk = 0;
-    int ca = (int)(c_begin + i0 - pfirst_cta * A);
-    for (int64_t img = i0; img < i1; ++img, ++j, ++ca) {
-      if (ca == A) { ca = 0; ++kk; }
-      const int64_t p = pfirst_cta + kk;
-      if (p != cur_p) {
-        const uint32_t k = (uint32_t)kk, sb = k & 1u, ph = (k >> 1) & 1u;
+    int a0 = (int)(c_begin + i0 - pfirst_cta * A);
+    int64_t img = i0;
+    const uint32_t stage0 = saddr(sStage0);
+    for (int kq = 0; kq < (int)npar; ++kq) {   // parents outer, children inner (32-bit counters)
+      {
+        const uint32_t sb = (uint32_t)kq & 1u, ph = ((uint32_t)kq >> 1) & 1u;
         mbar_wait(&p_full[sb], ph);
         tc_fence_after();
 #pragma unroll
@@ -526,14 +526,15 @@ __global__ void __launch_bounds__(kSibThreads, 1)
 #pragma unroll
           for (int e = 0; e < 16; ++e)   // Pb = P * 2^-14 + bias, once per parent
             vp[mt][e] = __float_as_uint(fmaf(__uint_as_float(vp[mt][e]), kSibScale, sbias[c0 + e]));
-        cur_p = p;
       }
+      const int a_end = (int)(i1 - img < (int64_t)(A - a0) ? a0 + (i1 - img) : (int64_t)A);
+      for (int a = a0; a < a_end; ++a, ++img, ++j) {
       const uint32_t cb = j & 1u, cph = (j >> 1) & 1u;
       mbar_wait(&c_full[cb], cph);
       tc_fence_after();
       uint8_t *oimg = out + img * (int64_t)P.out_img_bytes;
       // staging buffer j&1 is free once the bulk store of child j-2 has read it (<= 1 group pending)
-      uint8_t *sStage = sStage0 + (j & 1u) * (2 * kStageBlk);
+      const uint32_t sStage = stage0 + (j & 1u) * (2 * kStageBlk);
       if (threadIdx.x == 32) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
       epi_bar();
 #pragma unroll
@@ -552,7 +553,6 @@ __global__ void __launch_bounds__(kSibThreads, 1)
         for (int u = 0; u < 2; ++u) {
           const int mt = 2 * hf + u;
           const uint32_t o = (soff2[mt >> 1] >> (16 * (mt & 1))) & 0xFFFFu;
-          if (o == 0xFFFFu) continue;
           uint32_t pk[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) {   // relu(C * 2^-14 + Pb) -> bf16 (ReLU on the packed pair)
@@ -561,9 +561,14 @@ __global__ void __launch_bounds__(kSibThreads, 1)
                                     make_float2(__uint_as_float(vp[mt][2 * e]), __uint_as_float(vp[mt][2 * e + 1])));
             pk[e] = bf16x2_relu(xy.x, xy.y);
           }
+          // into the staging image, in act1's global SW128 layout; rows of the discarded full-width
+          // columns (o = 0xFFFF) are skipped by a predicate, not a branch (no reconvergence per tile)
 #pragma unroll
-          for (int h2 = 0; h2 < 2; ++h2)   // into the staging image, in act1's global SW128 layout
-            *(uint4 *)(sStage + (o ^ (16u * h2))) = make_uint4(pk[4 * h2], pk[4 * h2 + 1], pk[4 * h2 + 2], pk[4 * h2 + 3]);
+          for (int h2 = 0; h2 < 2; ++h2)
+            asm volatile("{\n.reg .pred p;\nsetp.ne.u32 p, %0, 65535;\n@p st.shared.v4.b32 [%1], {%2, %3, %4, %5};\n}\n"
+                         ::"r"(o), "r"(sStage + (o ^ (16u * h2))), "r"(pk[4 * h2]), "r"(pk[4 * h2 + 1]),
+                         "r"(pk[4 * h2 + 2]), "r"(pk[4 * h2 + 3])
+                         : "memory");
         }
       }
       // whole image staged: the TMA engine writes the two row blocks to global (async)
@@ -572,11 +577,13 @@ __global__ void __launch_bounds__(kSibThreads, 1)
       if (threadIdx.x == 32) {
         for (int q = 0; q < 2; ++q)
           asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(oimg + q * P.out_plane * 8u),
-                       "r"(saddr(sStage) + q * kStageBlk), "r"(kStageBlk)
+                       "r"(sStage + q * kStageBlk), "r"(kStageBlk)
                        : "memory");
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
-    }
+      }   // children
+      a0 = 0;
+    }     // parents
   } else {
     // ---------------------------------------------- converters (7 warps)
     const int t = threadIdx.x - 288;   // 0..223
@@ -645,57 +652,53 @@ __global__ void __launch_bounds__(kSibThreads, 1)
         issue_par(q + 1);
       }
     };
-    int64_t cur_p = -1, loaded = -1;   // highest parent loaded (shared image converted, pn_next set)
-    uint32_t k = 0, j = 0;
-    uint64_t pkey = 0;
-    float pcum = 0.0f;
-    bool first_child = false;
-    int64_t kk = 0;
-    int a = (int)(c_begin + i0 - pfirst_cta * A);   // child index within its parent = its action (R1)
-    for (int64_t img = i0; img < i1; ++img, ++j, ++a) {
-      if (a == A) { a = 0; ++kk; }
-      const int64_t p = pfirst_cta + kk;
-      const int64_t pl = p - p_first;
-      if (p != cur_p) {   // a new parent: newest-frame bytes (registers), key, cumulative reward
-        k = (uint32_t)kk;
-        if (loaded < (int64_t)k) {   // first parent of the CTA (later ones are loaded ahead)
-          load_parent(k);
-          loaded = k;
-        }
+    // Parents outer, children inner (32-bit counters). The A child keys of a parent are computed
+    // once per parent, lane l holding those of actions l and l + 32 (A <= kMaxA = 64), and each
+    // child takes its key with two shuffles instead of every converter thread re-hashing it.
+    uint32_t nb = 0, nph = 0;                        // new-image ring slot / phase of child j
+    int a0 = (int)(c_begin + i0 - pfirst_cta * A);   // first child's index within its parent = its action (R1)
+    int64_t img = i0;
+    if (npar > 0) load_parent(0);
+    for (int kq = 0; kq < (int)npar; ++kq) {
+      const int64_t pl = pfirst_cta + kq - p_first;
 #pragma unroll
-        for (int it = 0; it < kTasks; ++it) pn[it] = pn_next[it];
-        pkey = *(const uint64_t *)((const uint8_t *)par.key + pl * par.key_stride);   // once per parent
-        pcum = par.cum ? par.cum[pl] : 0.0f;
-        cur_p = p;
-        first_child = true;
-      }
-      const uint64_t k2 = mix64d(pkey ^ (0x9E3779B97F4A7C15ull * (uint64_t)(a + 1)));   // child key
-      if (t == 0) {
-        const uint32_t tt = (uint32_t)(k2 >> 61);
-        const float rw = tt == 7u ? 1.0f : (tt == 0u ? -1.0f : 0.0f);
-        cum_out[img] = fmaf(gk, rw, pcum);   // R_d = fmaf(g[d-1], r, R_{d-1})
-      }
-      const uint32_t nb = j % kNewRing, nph = (j / kNewRing) & 1u;
-      mbar_wait(&n_empty[nb], nph ^ 1u);
-      uint8_t *nw = sNw + nb * kNewBytes;
-      // noise group g: h = mix64(k2 + g) covers pixels 8g..8g+7 = quads 2g (low word) and 2g+1
-#pragma unroll
-      for (int it = 0; it < kTasks; ++it) {
-        const int g = tg[it];
-        const uint64_t h = mix64d(k2 + (uint64_t)g);
-        const uint32_t b0 = pn[it].x ^ (uint32_t)h, b1 = pn[it].y ^ (uint32_t)(h >> 32);
-        *(uint2 *)(nw + tdst[it][0]) = make_uint2(u8pair_f16x2(b0, 0x4140u), u8pair_f16x2(b0, 0x4342u));
-        *(uint2 *)(nw + tdst[it][1]) = make_uint2(u8pair_f16x2(b1, 0x4140u), u8pair_f16x2(b1, 0x4342u));
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive(&n_full[nb]);
-      if (first_child) {   // lookahead: load the next parent while the pipeline works on this child
-        first_child = false;
-        if ((int64_t)k + 1 < npar) {
-          load_parent(k + 1);
-          loaded = k + 1;
+      for (int it = 0; it < kTasks; ++it) pn[it] = pn_next[it];
+      const uint64_t pkey = *(const uint64_t *)((const uint8_t *)par.key + pl * par.key_stride);
+      const float pcum = par.cum ? par.cum[pl] : 0.0f;
+      const int l = t & 31;
+      const uint64_t klo = mix64d(pkey ^ (0x9E3779B97F4A7C15ull * (uint64_t)(l + 1)));   // child key, a = l
+      const uint64_t khi = A > 32 ? mix64d(pkey ^ (0x9E3779B97F4A7C15ull * (uint64_t)(l + 33))) : 0ull;
+      const int a_end = (int)(i1 - img < (int64_t)(A - a0) ? a0 + (i1 - img) : (int64_t)A);
+      for (int a = a0; a < a_end; ++a, ++img) {
+        const uint64_t kv = a < 32 ? klo : khi;
+        const uint64_t k2 = ((uint64_t)__shfl_sync(0xffffffffu, (uint32_t)(kv >> 32), a & 31) << 32) |
+                            __shfl_sync(0xffffffffu, (uint32_t)kv, a & 31);
+        if (t == 0) {
+          const uint32_t tt = (uint32_t)(k2 >> 61);
+          const float rw = tt == 7u ? 1.0f : (tt == 0u ? -1.0f : 0.0f);
+          cum_out[img] = fmaf(gk, rw, pcum);   // R_d = fmaf(g[d-1], r, R_{d-1})
         }
+        mbar_wait(&n_empty[nb], nph ^ 1u);
+        uint8_t *nw = sNw + nb * kNewBytes;
+        // noise group g: h = mix64(k2 + g) covers pixels 8g..8g+7 = quads 2g (low word) and 2g+1
+#pragma unroll
+        for (int it = 0; it < kTasks; ++it) {
+          const int g = tg[it];
+          const uint64_t h = mix64d(k2 + (uint64_t)g);
+          const uint32_t b0 = pn[it].x ^ (uint32_t)h, b1 = pn[it].y ^ (uint32_t)(h >> 32);
+          *(uint2 *)(nw + tdst[it][0]) = make_uint2(u8pair_f16x2(b0, 0x4140u), u8pair_f16x2(b0, 0x4342u));
+          *(uint2 *)(nw + tdst[it][1]) = make_uint2(u8pair_f16x2(b1, 0x4140u), u8pair_f16x2(b1, 0x4342u));
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&n_full[nb]);
+        if (++nb == (uint32_t)kNewRing) {
+          nb = 0;
+          nph ^= 1u;
+        }
+        // lookahead: after the parent's first child, load the next parent while the pipeline works
+        if (a == a0 && kq + 1 < (int)npar) load_parent(kq + 1);
       }
+      a0 = 0;
     }
   }
   if (threadIdx.x == 32) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
