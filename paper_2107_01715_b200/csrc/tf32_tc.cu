@@ -16,6 +16,7 @@
 // (8-row x 16-byte core matrices; LBO = one 4-wide K chunk = Npad * 16 B, SBO = 128 B); an MMA
 // (K = 8) reads two chunks.
 #include <algorithm>
+#include <type_traits>
 #include <vector>
 
 #include <cooperative_groups.h>
@@ -28,8 +29,8 @@ namespace cg = cooperative_groups;
 namespace bcts {
 namespace {
 
-constexpr int kTcThreadsDnn = 384;   // warp 0 MMA issuer; warps 4-7 / 8-11: epilogue of tile slot 0 / 1
-constexpr int kTcThreadsMlp = 256;   // warp 0 MMA issuer; warps 4-7: epilogue
+constexpr int kTcThreadsDnn = 640;   // warp 0 MMA issuer; warps 4-11 / 12-19: epilogue of tile slot 0 / 1
+constexpr int kTcThreadsMlp = 384;   // warp 0 MMA issuer; warps 4-11: epilogue (lane quarter x column half)
 constexpr int kTcK = 104;            // DNN state width 100 padded to a multiple of 8 (tf32 MMA K)
 constexpr int kTcN = 112;            // DNN layer outputs (100, or 101 for the last) padded to 16
 constexpr uint32_t kTcPlane = kTcN * 16;                       // one 4-wide K chunk of a DNN layer
@@ -100,7 +101,7 @@ __global__ void __launch_bounds__(kTcThreadsDnn, 1)
   if (threadIdx.x == 0) {
     mbar_init(&wbar, 1);
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&a_ready[s], 128);
+      mbar_init(&a_ready[s], 256);
       mbar_init(&d_full[s], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -150,109 +151,101 @@ __global__ void __launch_bounds__(kTcThreadsDnn, 1)
         }
     }
   } else if (warp >= 4) {   // ------------------------------------------ epilogue, slot s
-    const int s = (warp - 4) >> 2, q = warp & 3, m = q * 32 + lane;
+    // 8 warps per slot: lane quarter q (= warp % 4, the TMEM lanes a warp may access) x column half h
+    // (h = 0: units / inputs 0..63, h = 1: 64..111), so each thread handles half of one node's row;
+    // the half is a compile-time constant of each instantiation (warp-uniform dispatch below)
+    const int s = (warp - 4) >> 3, q = warp & 3, m = q * 32 + lane;
     const uint32_t tA = tmem + ((uint32_t)(q * 32) << 16) + 256u * s, tD = tA + 128u;
-    for (int64_t t = blockIdx.x + (int64_t)s * gridDim.x; t < ntiles; t += 2 * (int64_t)gridDim.x) {
-      const int64_t c = c_begin + t * 128 + m;
-      const bool valid = c < c_end;
-      const int64_t p = valid ? c / A : c_begin / A;
-      const int a = valid ? (int)(c - p * A) : 0;
-      // A0: the parent's state, rounded to tf32; columns 100..103 and invalid rows are zero
-      {
-        const float4 *ps = (const float4 *)(par.state + (p - p_first) * par.state_stride);
-        float4 x4[kDnnS / 4];   // all 25 loads in flight at once (one L2 round trip, not four)
+    auto epilogue = [&](auto half) {
+      constexpr int h = decltype(half)::value;
+      constexpr int j_lo = h ? 64 : 0, j_hi = h ? kTcN : 64, a_hi = h ? kTcK : 64;
+      constexpr int nf4 = ((h ? kDnnS : 64) - j_lo) / 4;   // float4 of the parent state this half loads
+      for (int64_t t = blockIdx.x + (int64_t)s * gridDim.x; t < ntiles; t += 2 * (int64_t)gridDim.x) {
+        const int64_t c = c_begin + t * 128 + m;
+        const bool valid = c < c_end;
+        const int64_t p = valid ? c / A : c_begin / A;
+        const int a = valid ? (int)(c - p * A) : 0;
+        {   // A0: the parent's state (this half's columns) rounded to tf32; columns 100..103, invalid rows: 0
+          const float4 *ps = (const float4 *)(par.state + (p - p_first) * par.state_stride) + j_lo / 4;
+          float4 x4[nf4];   // the half row's loads in flight at once (one L2 round trip)
 #pragma unroll
-        for (int e = 0; e < kDnnS / 4; ++e) x4[e] = valid ? __ldcg(ps + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int e = 0; e < nf4; ++e) x4[e] = valid ? __ldcg(ps + e) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int j0 = 0; j0 < kTcK; j0 += 32) {
-          uint32_t r[32];
-#pragma unroll
-          for (int e = 0; e < 32; e += 4) {
-            const float4 v = j0 + e < kDnnS ? x4[(j0 + e) / 4] : make_float4(0.f, 0.f, 0.f, 0.f);
-            r[e] = tf32_bits(v.x);
-            r[e + 1] = tf32_bits(v.y);
-            r[e + 2] = tf32_bits(v.z);
-            r[e + 3] = tf32_bits(v.w);
+          for (int j = j_lo; j < a_hi; j += 8) {
+            const int e = (j - j_lo) / 4;
+            const float4 v0 = e < nf4 ? x4[e] : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4 v1 = e + 1 < nf4 ? x4[e + 1] : make_float4(0.f, 0.f, 0.f, 0.f);
+            const uint32_t r8[8] = {tf32_bits(v0.x), tf32_bits(v0.y), tf32_bits(v0.z), tf32_bits(v0.w),
+                                    tf32_bits(v1.x), tf32_bits(v1.y), tf32_bits(v1.z), tf32_bits(v1.w)};
+            tmem_st8(tA + (uint32_t)j, r8);
           }
-          if (j0 + 32 <= kTcK) {
-            tmem_st32(tA + (uint32_t)j0, r);
-          } else {
-            const uint32_t r8[8] = {r[0], r[1], r[2], r[3], r[4], r[5], r[6], r[7]};
-            tmem_st8(tA + (uint32_t)j0, r8);
-          }
-        }
-        tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive(&a_ready[s]);
-      }
-      const float rpar = valid && par.cum ? __ldcg(par.cum + (p - p_first)) : 0.0f;
-      float *srow = (float *)(out.state + (valid ? c - c_begin : 0) * out.state_stride);
-#pragma unroll
-      for (int L = 0; L < 4; ++L) {
-        mbar_wait_spin(&d_full[s], (uint32_t)L & 1u);
-        tc_fence_after();
-        const float *b = bias.b[L];
-        auto proc = [&](int j0, const uint32_t(&v)[16]) {
-          if (L < 3) {   // hidden layer: relu(D + b (+ W1[:, 100 + a])) -> tf32 -> A columns j0..
-            uint32_t r[16];
-#pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              const int u = j0 + e;
-              float x = 0.0f;
-              if (u < kDnnS) {
-                x = __uint_as_float(v[e]) + b[u];
-                if (L == 0) x += sW1A[a * kDnnS + u];
-                x = fmaxf(x, 0.0f);
-              }
-              r[e] = tf32_bits(x);
-            }
-            if (j0 + 16 <= kTcK) {
-              const uint32_t(&lo)[8] = *(const uint32_t(*)[8])r;
-              const uint32_t(&hi)[8] = *(const uint32_t(*)[8])(r + 8);
-              tmem_st8(tA + (uint32_t)j0, lo);
-              tmem_st8(tA + (uint32_t)j0 + 8u, hi);
-            } else if (j0 < kTcK) {
-              const uint32_t(&lo)[8] = *(const uint32_t(*)[8])r;
-              tmem_st8(tA + (uint32_t)j0, lo);
-            }
-          } else if (valid) {   // output layer: s' (units 0..99) and r (unit 100)
-#pragma unroll
-            for (int e = 0; e < 16; e += 4) {
-              const int u = j0 + e;
-              if (u < kDnnS)
-                *(float4 *)(srow + u) = make_float4(__uint_as_float(v[e]) + b[u], __uint_as_float(v[e + 1]) + b[u + 1],
-                                                    __uint_as_float(v[e + 2]) + b[u + 2],
-                                                    __uint_as_float(v[e + 3]) + b[u + 3]);
-            }
-            if (j0 <= kDnnS && kDnnS < j0 + 16)
-              out.cum[c - c_begin] = fmaf(gk, __uint_as_float(v[kDnnS - j0]) + b[kDnnS], rpar);
-          }
-        };
-        {   // columns 0..63: four loads, one wait
-          uint32_t v[4][16];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) tmem_ld16_nw(tD + 16u * u, v[u]);
-#pragma unroll
-          for (int u = 0; u < 4; ++u) tmem_wait16(v[u]);
-#pragma unroll
-          for (int u = 0; u < 4; ++u) proc(16 * u, v[u]);
-        }
-        {   // columns 64..111: three loads, one wait
-          uint32_t v[3][16];
-#pragma unroll
-          for (int u = 0; u < 3; ++u) tmem_ld16_nw(tD + 64u + 16u * u, v[u]);
-#pragma unroll
-          for (int u = 0; u < 3; ++u) tmem_wait16(v[u]);
-#pragma unroll
-          for (int u = 0; u < 3; ++u) proc(64 + 16 * u, v[u]);
-        }
-        if (L < 3) {
           tmem_wait_st();
           tc_fence_before();
           mbar_arrive(&a_ready[s]);
         }
+        const float rpar = valid && par.cum ? __ldcg(par.cum + (p - p_first)) : 0.0f;
+        float *srow = (float *)(out.state + (valid ? c - c_begin : 0) * out.state_stride);
+#pragma unroll
+        for (int L = 0; L < 4; ++L) {
+          mbar_wait_spin(&d_full[s], (uint32_t)L & 1u);
+          tc_fence_after();
+          const float *b = bias.b[L];
+#pragma unroll
+          for (int j2 = j_lo; j2 < j_hi; j2 += 32) {   // two 16-column loads per wait (register budget)
+            uint32_t v[2][16];
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+              if (j2 + 16 * u < j_hi) tmem_ld16_nw(tD + (uint32_t)(j2 + 16 * u), v[u]);
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+              if (j2 + 16 * u < j_hi) tmem_wait16(v[u]);
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const int j0 = j2 + 16 * u;
+              if (j0 >= j_hi) continue;
+              if (L < 3) {   // hidden layer: relu(D + b (+ W1[:, 100 + a])) -> tf32 -> A columns j0..
+                uint32_t r[16];
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                  const int uu = j0 + e;
+                  float x = 0.0f;
+                  if (uu < kDnnS) {
+                    x = __uint_as_float(v[u][e]) + b[uu];
+                    if (L == 0) x += sW1A[a * kDnnS + uu];
+                    x = fmaxf(x, 0.0f);
+                  }
+                  r[e] = tf32_bits(x);
+                }
+                if (j0 + 16 <= kTcK) {
+                  tmem_st8(tA + (uint32_t)j0, *(const uint32_t(*)[8])r);
+                  tmem_st8(tA + (uint32_t)j0 + 8u, *(const uint32_t(*)[8])(r + 8));
+                } else if (j0 < kTcK) {
+                  tmem_st8(tA + (uint32_t)j0, *(const uint32_t(*)[8])r);
+                }
+              } else if (valid) {   // output layer: s' (units 0..99) and r (unit 100)
+#pragma unroll
+                for (int e = 0; e < 16; e += 4) {
+                  const int uu = j0 + e;
+                  if (uu < kDnnS)
+                    *(float4 *)(srow + uu) =
+                        make_float4(__uint_as_float(v[u][e]) + b[uu], __uint_as_float(v[u][e + 1]) + b[uu + 1],
+                                    __uint_as_float(v[u][e + 2]) + b[uu + 2], __uint_as_float(v[u][e + 3]) + b[uu + 3]);
+                }
+                if (j0 <= kDnnS && kDnnS < j0 + 16)
+                  out.cum[c - c_begin] = fmaf(gk, __uint_as_float(v[u][kDnnS - j0]) + b[kDnnS], rpar);
+              }
+            }
+          }
+          if (L < 3) {
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(&a_ready[s]);
+          }
+        }
       }
-    }
+    };
+    if (((warp - 4) >> 2) & 1) epilogue(std::integral_constant<int, 1>{});
+    else epilogue(std::integral_constant<int, 0>{});
   }
   if (lv + 1 < levels.n) {   // the whole level written before any CTA reads it as parents
     __threadfence();
@@ -293,18 +286,24 @@ __host__ __device__ inline MlpTcShape mlp_tc_shape(int I, int H, int A) {
 
 // A0 of node `node` (features -> tf32; columns I..IK-1 and rows past n zero) into TMEM columns 0..,
 // in two steps: mlp_fetch_a0 issues the row's loads into registers (a tile ahead of their use),
-// mlp_store_a0 rounds and stores them. Bytes (INT_HASH) travel in the first four float4 as raw bits.
+// mlp_store_a0 rounds and stores them. Half H of the epilogue handles columns 64 H .. 64 H + 63:
+// fp32 features (DNN env) 0..63 / 64..99 (+ zero padding to IK); the 64 state bytes (INT_HASH,
+// exact in tf32 after / 256) all belong to half 0 and travel in the first four float4 as raw bits.
+template <int H>
 struct MlpA0 {
-  float4 x[kDnnS / 4];
+  float4 x[H ? (kDnnS - 64) / 4 : 16];
 };
+template <int H>
 __device__ __forceinline__ void mlp_fetch_a0(const uint8_t *__restrict__ states, int64_t stride, int64_t node,
-                                             int64_t n, int feat_f32, MlpA0 &r) {
+                                             int64_t n, int feat_f32, MlpA0<H> &r) {
+  constexpr int nf4 = H ? (kDnnS - 64) / 4 : 16;
   const bool valid = node < n;
   const uint8_t *srow = states + (valid ? node : 0) * stride;
-  if (feat_f32) {   // 100 fp32 state values (DNN env): 25 float4
+  if (feat_f32) {   // fp32 state values 64 H .. (DNN env)
 #pragma unroll
-    for (int e = 0; e < kDnnS / 4; ++e) r.x[e] = valid ? __ldg((const float4 *)srow + e) : make_float4(0.f, 0.f, 0.f, 0.f);
-  } else {          // 64 state bytes (INT_HASH)
+    for (int e = 0; e < nf4; ++e)
+      r.x[e] = valid ? __ldg((const float4 *)srow + 16 * H + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+  } else if (H == 0) {   // 64 state bytes (INT_HASH)
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const uint4 w = valid ? __ldg((const uint4 *)srow + e) : make_uint4(0u, 0u, 0u, 0u);
@@ -312,17 +311,20 @@ __device__ __forceinline__ void mlp_fetch_a0(const uint8_t *__restrict__ states,
     }
   }
 }
-__device__ __forceinline__ void mlp_store_a0(const MlpA0 &r, int feat_f32, uint32_t tl) {
+template <int H>
+__device__ __forceinline__ void mlp_store_a0(const MlpA0<H> &r, int feat_f32, uint32_t tl) {
+  constexpr int nf4 = H ? (kDnnS - 64) / 4 : 16;
   if (feat_f32) {
 #pragma unroll
-    for (int j0 = 0; j0 < kTcK; j0 += 8) {
-      const float4 v0 = j0 < kDnnS ? r.x[j0 / 4] : make_float4(0.f, 0.f, 0.f, 0.f);
-      const float4 v1 = j0 + 4 < kDnnS ? r.x[j0 / 4 + 1] : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j = 64 * H; j < (H ? kTcK : 64); j += 8) {
+      const int e = (j - 64 * H) / 4;
+      const float4 v0 = e < nf4 ? r.x[e] : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 v1 = e + 1 < nf4 ? r.x[e + 1] : make_float4(0.f, 0.f, 0.f, 0.f);
       const uint32_t q[8] = {tf32_bits(v0.x), tf32_bits(v0.y), tf32_bits(v0.z), tf32_bits(v0.w),
                              tf32_bits(v1.x), tf32_bits(v1.y), tf32_bits(v1.z), tf32_bits(v1.w)};
-      tmem_st8(tl + (uint32_t)j0, q);
+      tmem_st8(tl + (uint32_t)j, q);
     }
-  } else {          // bytes / 256: exact in tf32
+  } else if (H == 0) {   // bytes / 256: exact in tf32
 #pragma unroll
     for (int j0 = 0; j0 < 64; j0 += 8) {
       const float4 w = r.x[j0 / 16];
@@ -349,8 +351,8 @@ __global__ void __launch_bounds__(kTcThreadsMlp, 1)
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
   if (threadIdx.x == 0) {
     mbar_init(&wbar, 1);
-    mbar_init(&a0_ready, 128);
-    mbar_init(&a1_ready, 128);
+    mbar_init(&a0_ready, 256);
+    mbar_init(&a1_ready, 256);
     mbar_init(&d1_full, 1);
     mbar_init(&d2_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -393,78 +395,88 @@ __global__ void __launch_bounds__(kTcThreadsMlp, 1)
       __syncwarp();
     }
   } else if (warp >= 4) {   // ------------------------------------------------- epilogue
+    // 8 warps: lane quarter q (= warp % 4) x column half (features 0..63 / 64.., hidden units
+    // [0, hs) / [hs, H)); layer 2 (NA <= 64 columns) is read by half 0 alone
     const int q = warp & 3, m = q * 32 + lane;
     const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
-    MlpA0 a0;
-    if (blockIdx.x < ntiles) {
-      mlp_fetch_a0(states, stride, (int64_t)blockIdx.x * 128 + m, n, feat_f32, a0);
-      mlp_store_a0(a0, feat_f32, tl);
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(&a0_ready);
-    }
-    uint32_t i = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
-      const int64_t node = t * 128 + m;
-      // the next tile's row: loads in flight during this tile's layer 1, stored after it
-      const bool has_next = t + gridDim.x < ntiles;
-      if (has_next) mlp_fetch_a0(states, stride, (t + gridDim.x) * 128 + m, n, feat_f32, a0);
-      // layer 1: relu(D1 + b1) -> tf32 -> A1 (the same columns), four 16-column loads per wait
-      mbar_wait_spin(&d1_full, i & 1u);
-      tc_fence_after();
-      for (int j0 = 0; j0 < sh.H; j0 += 64) {
-        uint32_t v[4][16];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (j0 + 16 * u < sh.H) tmem_ld16_nw(tl + 128u + (uint32_t)(j0 + 16 * u), v[u]);
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (j0 + 16 * u < sh.H) tmem_wait16(v[u]);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (j0 + 16 * u >= sh.H) break;
-          uint32_t lo[8], hi[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            lo[e] = tf32_bits(fmaxf(__uint_as_float(v[u][e]) + sb1[j0 + 16 * u + e], 0.0f));
-            hi[e] = tf32_bits(fmaxf(__uint_as_float(v[u][e + 8]) + sb1[j0 + 16 * u + e + 8], 0.0f));
-          }
-          tmem_st8(tl + 128u + (uint32_t)(j0 + 16 * u), lo);
-          tmem_st8(tl + 128u + (uint32_t)(j0 + 16 * u) + 8u, hi);
-        }
-      }
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(&a1_ready);
-      // the next tile's features while layer 2 runs
-      if (has_next) {
-        mlp_store_a0(a0, feat_f32, tl);
+    const int hs = (sh.H / 2 + 15) / 16 * 16;
+    auto epilogue = [&](auto half) {
+      constexpr int h = decltype(half)::value;
+      const int u_lo = h ? hs : 0, u_hi = h ? sh.H : hs;
+      MlpA0<h> a0;
+      if (blockIdx.x < ntiles) {
+        mlp_fetch_a0<h>(states, stride, (int64_t)blockIdx.x * 128 + m, n, feat_f32, a0);
+        mlp_store_a0<h>(a0, feat_f32, tl);
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&a0_ready);
       }
-      // layer 2: Q = D2 + b2 -> rows / max / total
-      mbar_wait_spin(&d2_full, i & 1u);
-      tc_fence_after();
-      float best = -INFINITY;
-      const bool valid = node < n;
-      for (int j0 = 0; j0 < sh.NA; j0 += 16) {
-        uint32_t v[16];
-        tmem_ld16_nw(tl + 384u + (uint32_t)j0, v);
-        tmem_wait16(v);
+      uint32_t i = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+        const int64_t node = t * 128 + m;
+        // the next tile's row: loads in flight during this tile's layer 1, stored after it
+        const bool has_next = t + gridDim.x < ntiles;
+        if (has_next) mlp_fetch_a0<h>(states, stride, (t + gridDim.x) * 128 + m, n, feat_f32, a0);
+        // layer 1: relu(D1 + b1) -> tf32 -> A1 (the same columns), four 16-column loads per wait
+        mbar_wait_spin(&d1_full, i & 1u);
+        tc_fence_after();
+        for (int j0 = u_lo; j0 < u_hi; j0 += 64) {
+          uint32_t v[4][16];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const int a = j0 + e;
-          if (a < sh.A) {
-            const float qv = __uint_as_float(v[e]) + sb2[a];
-            best = fmaxf(best, qv);
-            if (valid && mode == MODE_ROWS) out[node * sh.A + a] = qv;
+          for (int u = 0; u < 4; ++u)
+            if (j0 + 16 * u < u_hi) tmem_ld16_nw(tl + 128u + (uint32_t)(j0 + 16 * u), v[u]);
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (j0 + 16 * u < u_hi) tmem_wait16(v[u]);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (j0 + 16 * u >= u_hi) break;
+            uint32_t lo[8], hi[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              lo[e] = tf32_bits(fmaxf(__uint_as_float(v[u][e]) + sb1[j0 + 16 * u + e], 0.0f));
+              hi[e] = tf32_bits(fmaxf(__uint_as_float(v[u][e + 8]) + sb1[j0 + 16 * u + e + 8], 0.0f));
+            }
+            tmem_st8(tl + 128u + (uint32_t)(j0 + 16 * u), lo);
+            tmem_st8(tl + 128u + (uint32_t)(j0 + 16 * u) + 8u, hi);
           }
         }
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&a1_ready);
+        // the next tile's features while layer 2 runs
+        if (has_next) {
+          mlp_store_a0<h>(a0, feat_f32, tl);
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(&a0_ready);
+        }
+        if (h == 0) {   // layer 2: Q = D2 + b2 -> rows / max / total
+          mbar_wait_spin(&d2_full, i & 1u);
+          tc_fence_after();
+          float best = -INFINITY;
+          const bool valid = node < n;
+          for (int j0 = 0; j0 < sh.NA; j0 += 16) {
+            uint32_t v[16];
+            tmem_ld16_nw(tl + 384u + (uint32_t)j0, v);
+            tmem_wait16(v);
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const int a = j0 + e;
+              if (a < sh.A) {
+                const float qv = __uint_as_float(v[e]) + sb2[a];
+                best = fmaxf(best, qv);
+                if (valid && mode == MODE_ROWS) out[node * sh.A + a] = qv;
+              }
+            }
+          }
+          if (valid && mode != MODE_ROWS) out[node] = mode == MODE_ROWMAX ? best : fmaf(gd, best, cum ? cum[node] : 0.0f);
+          tc_fence_before();
+        }
       }
-      if (valid && mode != MODE_ROWS) out[node] = mode == MODE_ROWMAX ? best : fmaf(gd, best, cum ? cum[node] : 0.0f);
-      tc_fence_before();
-    }
+    };
+    if (((warp - 4) >> 2) & 1) epilogue(std::integral_constant<int, 1>{});
+    else epilogue(std::integral_constant<int, 0>{});
   }
   tc_fence_before();
   __syncthreads();

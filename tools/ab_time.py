@@ -1,4 +1,4 @@
-"""Same-box A/B timing of a package copy: python tools/ab_time.py PKG_ROOT [CONFIG] [STEPS] [ROUNDS]
+"""Same-box A/B timing of a package copy: python tools/ab_time.py PKG_ROOT [CONFIG] [STEPS] [ROUNDS] [tf32]
 
 PKG_ROOT holds a paper_2107_01715_b200/ (e.g. gpurun_exp/base built from HEAD, or . for the working tree).
 Prints the device-timed step (L2 flushed before each step, CUDA events) and the per-class kernel times
@@ -10,7 +10,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def run(pkg_root, cname, steps):
+def run(pkg_root, cname, steps, tf32=False):
     sys.path.insert(0, os.path.abspath(pkg_root))
     sys.path.insert(1, ROOT)
     import numpy as np
@@ -19,7 +19,7 @@ def run(pkg_root, cname, steps):
     assert P.__file__.startswith(os.path.abspath(pkg_root)), P.__file__
     from synth.inputs import config
     cfg = config(cname)
-    h = P.Handle.from_config(cfg)
+    h = P.Handle.from_config(cfg, flags=P.F_TF32 if tf32 else 0)
     roots = torch.from_numpy(cfg.roots().view(np.uint8).copy()).cuda()
     n = roots.shape[0]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -43,7 +43,7 @@ def run(pkg_root, cname, steps):
     prof = h.profile_read()
     h.profile(False)
     cls = " ".join(f"{k} {v['ms'] / steps:.4f}" for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"]))
-    print(f"{pkg_root}: {cname} step mean {np.mean(ts):.4f} ms median {np.median(ts):.4f} | {cls}", flush=True)
+    print(f"{pkg_root}: {cname}{' tf32' if tf32 else ''} step mean {np.mean(ts):.4f} ms median {np.median(ts):.4f} | {cls}", flush=True)
 
 
 if __name__ == "__main__":
@@ -52,9 +52,11 @@ if __name__ == "__main__":
     cname = sys.argv[2] if len(sys.argv) > 2 else "C5"
     steps = int(sys.argv[3]) if len(sys.argv) > 3 else 20
     rounds = int(sys.argv[4]) if len(sys.argv) > 4 else 1
+    tf32 = len(sys.argv) > 5 and sys.argv[5] == "tf32"
     if len(roots) == 1 and rounds == 1:
-        run(roots[0], cname, steps)
+        run(roots[0], cname, steps, tf32)
     else:   # one fresh process per measurement (each imports its own package copy)
         for _ in range(rounds):
             for r in roots:
-                subprocess.run([sys.executable, os.path.abspath(__file__), r, cname, str(steps)], check=True)
+                subprocess.run([sys.executable, os.path.abspath(__file__), r, cname, str(steps), "1"] + (["tf32"] if tf32 else []),
+                               check=True)
