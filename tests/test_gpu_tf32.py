@@ -189,3 +189,30 @@ def test_tf32_deep_tree_error_does_not_grow():
     print(f"D2 d=12: root_q rel err {eq:.2e}")
     assert eq <= RTOL_TF32
     assert action_agreement(out["actions"], r["root_q"], RTOL_TF32)[0] >= 0.999
+
+
+@pytest.mark.parametrize("H,A", [(48, 5), (16, 3), (208, 7)])
+def test_tf32_mlp_hidden_widths(H, A):
+    """k_mlp_tc splits the hidden units between two epilogue halves at hs = ceil16(H / 2): H = 48 (halves of
+    32 + 16), H = 16 (half 1 empty), H = 208 (112 + 96). INT_HASH + MLP2 with mlp_hidden = H: the tf32 path
+    within R34's tolerance of the fp64 oracle, the fp32 default bit-exact vs the oracle's fp32 mirror."""
+    from synth.inputs import ENV_INT_HASH, NET_MLP2_F32, int_roots, make_weights
+    w = make_weights(NET_MLP2_F32, A, 300 + H, mlp_in=64, mlp_hidden=H)[0]
+    roots = int_roots(9, 40 + H)
+    o = Oracle(ENV_INT_HASH, A, NET_MLP2_F32, weights=w, mlp_in=64, mlp_hidden=H)
+    g32 = float(np.float32(0.97))
+    ht = P.Handle(ENV_INT_HASH, A, NET_MLP2_F32, weights=w, mlp_in=64, mlp_hidden=H, flags=P.F_TF32)
+    hf = P.Handle(ENV_INT_HASH, A, NET_MLP2_F32, weights=w, mlp_in=64, mlp_hidden=H)
+    try:
+        b = _host(ht.search(dev(roots), 9, 3, 0.97, 1.0, 1, extra=True))
+        a = _host(hf.search(dev(roots), 9, 3, 0.97, 1.0, 1, extra=True))
+    finally:
+        ht.close()
+        hf.close()
+    m = o.search(roots, 3, g32, 1.0, 1, mode=1, threads=THREADS)
+    np.testing.assert_array_equal(a["vanilla_q"], m["vanilla_q"].astype(np.float32))
+    r = o.search(roots, 3, g32, 1.0, 1, mode=0, threads=THREADS)
+    eq = rel_err(b["root_q"], r["root_q"]).max()
+    print(f"H={H} A={A}: tf32 root_q rel err {eq:.2e}")
+    assert eq <= RTOL_TF32
+    assert action_agreement(b["actions"], r["root_q"], RTOL_TF32)[0] >= 0.999
