@@ -529,59 +529,59 @@ __global__ void __launch_bounds__(kSibThreads, 1)
       }
       const int a_end = (int)(i1 - img < (int64_t)(A - a0) ? a0 + (i1 - img) : (int64_t)A);
       for (int a = a0; a < a_end; ++a, ++img, ++j) {
-      const uint32_t cb = j & 1u, cph = (j >> 1) & 1u;
-      mbar_wait(&c_full[cb], cph);
-      tc_fence_after();
-      uint8_t *oimg = out + img * (int64_t)P.out_img_bytes;
-      // staging buffer j&1 is free once the bulk store of child j-2 has read it (<= 1 group pending)
-      const uint32_t sStage = stage0 + (j & 1u) * (2 * kStageBlk);
-      if (threadIdx.x == 32) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-      epi_bar();
+        const uint32_t cb = j & 1u, cph = (j >> 1) & 1u;
+        mbar_wait(&c_full[cb], cph);
+        tc_fence_after();
+        uint8_t *oimg = out + img * (int64_t)P.out_img_bytes;
+        // staging buffer j&1 is free once the bulk store of child j-2 has read it (<= 1 group pending)
+        const uint32_t sStage = stage0 + (j & 1u) * (2 * kStageBlk);
+        if (threadIdx.x == 32) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        epi_bar();
 #pragma unroll
-      for (int hf = 0; hf < 2; ++hf) {   // two tiles at a time (register budget)
-        uint32_t vc[2][16];
+        for (int hf = 0; hf < 2; ++hf) {   // two tiles at a time (register budget)
+          uint32_t vc[2][16];
 #pragma unroll
-        for (int u = 0; u < 2; ++u)
-          tmem_ld16_nw(tmem + lanes + 256 + cb * 128 + (uint32_t)((2 * hf + u) * N + c0), vc[u]);
+          for (int u = 0; u < 2; ++u)
+            tmem_ld16_nw(tmem + lanes + 256 + cb * 128 + (uint32_t)((2 * hf + u) * N + c0), vc[u]);
 #pragma unroll
-        for (int u = 0; u < 2; ++u) tmem_wait16(vc[u]);
-        if (hf == 1) {
-          tc_fence_before();
-          mbar_arrive(&c_empty[cb]);
-        }
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int mt = 2 * hf + u;
-          const uint32_t o = (soff2[mt >> 1] >> (16 * (mt & 1))) & 0xFFFFu;
-          uint32_t pk[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {   // relu(C * 2^-14 + Pb) -> bf16 (ReLU on the packed pair)
-            const float2 xy = ffma2(make_float2(__uint_as_float(vc[u][2 * e]), __uint_as_float(vc[u][2 * e + 1])),
-                                    make_float2(kSibScale, kSibScale),
-                                    make_float2(__uint_as_float(vp[mt][2 * e]), __uint_as_float(vp[mt][2 * e + 1])));
-            pk[e] = bf16x2_relu(xy.x, xy.y);
+          for (int u = 0; u < 2; ++u) tmem_wait16(vc[u]);
+          if (hf == 1) {
+            tc_fence_before();
+            mbar_arrive(&c_empty[cb]);
           }
-          // into the staging image, in act1's global SW128 layout; rows of the discarded full-width
-          // columns (o = 0xFFFF) are skipped by a predicate, not a branch (no reconvergence per tile)
 #pragma unroll
-          for (int h2 = 0; h2 < 2; ++h2)
-            asm volatile("{\n.reg .pred p;\nsetp.ne.u32 p, %0, 65535;\n@p st.shared.v4.b32 [%1], {%2, %3, %4, %5};\n}\n"
-                         ::"r"(o), "r"(sStage + (o ^ (16u * h2))), "r"(pk[4 * h2]), "r"(pk[4 * h2 + 1]),
-                         "r"(pk[4 * h2 + 2]), "r"(pk[4 * h2 + 3])
+          for (int u = 0; u < 2; ++u) {
+            const int mt = 2 * hf + u;
+            const uint32_t o = (soff2[mt >> 1] >> (16 * (mt & 1))) & 0xFFFFu;
+            uint32_t pk[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {   // relu(C * 2^-14 + Pb) -> bf16 (ReLU on the packed pair)
+              const float2 xy = ffma2(make_float2(__uint_as_float(vc[u][2 * e]), __uint_as_float(vc[u][2 * e + 1])),
+                                      make_float2(kSibScale, kSibScale),
+                                      make_float2(__uint_as_float(vp[mt][2 * e]), __uint_as_float(vp[mt][2 * e + 1])));
+              pk[e] = bf16x2_relu(xy.x, xy.y);
+            }
+            // into the staging image, in act1's global SW128 layout; rows of the discarded full-width
+            // columns (o = 0xFFFF) are skipped by a predicate, not a branch (no reconvergence per tile)
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2)
+              asm volatile("{\n.reg .pred p;\nsetp.ne.u32 p, %0, 65535;\n@p st.shared.v4.b32 [%1], {%2, %3, %4, %5};\n}\n"
+                           ::"r"(o), "r"(sStage + (o ^ (16u * h2))), "r"(pk[4 * h2]), "r"(pk[4 * h2 + 1]),
+                           "r"(pk[4 * h2 + 2]), "r"(pk[4 * h2 + 3])
+                           : "memory");
+          }
+        }
+        // whole image staged: the TMA engine writes the two row blocks to global (async)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        epi_bar();
+        if (threadIdx.x == 32) {
+          for (int q = 0; q < 2; ++q)
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(oimg + q * P.out_plane * 8u),
+                         "r"(sStage + q * kStageBlk), "r"(kStageBlk)
                          : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
       }
-      // whole image staged: the TMA engine writes the two row blocks to global (async)
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      epi_bar();
-      if (threadIdx.x == 32) {
-        for (int q = 0; q < 2; ++q)
-          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(oimg + q * P.out_plane * 8u),
-                       "r"(sStage + q * kStageBlk), "r"(kStageBlk)
-                       : "memory");
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      }
-      }   // children
       a0 = 0;
     }     // parents
   } else {
