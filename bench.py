@@ -434,7 +434,10 @@ def main():
         e2e_s = float(t.item())
     e2e = {"value": total_nodes / e2e_s, "unit": "nodes/s", "h2d_bytes_per_step": int(pin_roots.numel()),
            "d2h_bytes_per_step": int(pin_act.numel() * 4 + pin_q.numel() * 4), "ms_per_step": e2e_s * 1e3,
-           "decisions_per_s": n / e2e_s}
+           "decisions_per_s": n / e2e_s,
+           # this rank's per-call wall times (the value above is their mean, max over ranks)
+           "ms_median": float(np.median(e2e_times)) * 1e3, "ms_min": min(e2e_times) * 1e3,
+           "ms_max": max(e2e_times) * 1e3}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
