@@ -171,6 +171,7 @@ bool tma_plan(TmaPlan &P, const Layer &L, const void *in, int64_t cap_img);
 // Fused Rainbow head (qnet_tma.cu, k_zhead): z_v + z_a + dueling C51 + max_a in one kernel.
 // The head biases travel as a __grid_constant__ kernel parameter: every lane of a warp reads
 // the same (action, atom) bias, so they are broadcast constant-bank loads (no L1 latency).
+constexpr int kHeadChunkRows = 208;   // fused head: rows per z_a chunk (4 actions x 51 atoms, padded to 16)
 struct HeadBias {
   float v[64];         // z_v bias (atoms)
   float sum[64];       // sum over actions of the z_a bias
@@ -262,7 +263,7 @@ struct Net {
   Layer c1, c2, c3, fc_h, z_v, z_a, fc2;
   int atoms = 51;
   float vmin = -10.f, vmax = 10.f;
-  const __nv_bfloat16 *wa64 = nullptr;   // fused head: z_a weights, 64 rows per action
+  const __nv_bfloat16 *wa64 = nullptr;   // fused head: z_a weights, chunks of 4 actions x 51 rows (kHeadChunkRows)
   const float *ba64 = nullptr;
   const __nv_bfloat16 *wsum = nullptr;   // fused head: sum_a W_a (bf16 hi | lo), [128][512]
   const float *bsum = nullptr;           // fused head: sum_a b_a [64]

@@ -560,8 +560,18 @@ int net_build(Net &net, const bcts_config &cfg, std::string &err) {
         for (int a = 0; a < A; ++a) bacc += (double)ba64[(size_t)a * 64 + t];
         bs[t] = (float)bacc;
       }
+      // the fused head streams z_a in chunks of 4 actions packed at 51 rows each (chunk c: rows
+      // kHeadChunkRows c + 51 s + t for action 4 c + s; rows 204..207 of a chunk zero), so a
+      // chunk's MMA is N = 208 instead of 4 x 64 padded rows
+      const int nch = (A + 3) / 4;
+      std::vector<__nv_bfloat16> wpk((size_t)nch * kHeadChunkRows * 512, __float2bfloat16_rn(0.0f));
+      for (int a = 0; a < A; ++a)
+        for (int t = 0; t < atoms; ++t)
+          for (int c = 0; c < 512; ++c)
+            wpk[((size_t)(a / 4) * kHeadChunkRows + (size_t)(a % 4) * atoms + t) * 512 + c] =
+                wa64[((size_t)a * 64 + t) * 512 + c];
       void *dw = nullptr, *db = nullptr, *dws = nullptr, *dbs = nullptr;
-      if (upload(net, wa64.data(), wa64.size() * 2, &dw) != cudaSuccess ||
+      if (upload(net, wpk.data(), wpk.size() * 2, &dw) != cudaSuccess ||
           upload(net, ba64.data(), ba64.size() * 4, &db) != cudaSuccess ||
           upload(net, ws.data(), ws.size() * 2, &dws) != cudaSuccess ||
           upload(net, bs.data(), bs.size() * 4, &dbs) != cudaSuccess) {

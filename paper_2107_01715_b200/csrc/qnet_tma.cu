@@ -564,8 +564,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 //               by linearity; sum_a W_a is carried as a bf16 hi + lo pair (K = 1024
 //               over [h_a; h_a]), i.e. to ~2^-16 relative, and sum_a b_a is added in
 //               fp32 -> mean_t = (S_t + sum_a b_a,t) / A.
-//   chunk c   : z_a for actions 4c..4c+3 (64 TMEM columns per action: 51 atoms + zero
-//               pad) -> logits = (v - mean) + z_a -> softmax expectation -> max_a.
+//   chunk c   : z_a for actions 4c..4c+3 (51 TMEM columns per action, packed: N = 208 for
+//               4 actions, the weights streamed as kHeadChunkRows-row boxes) -> logits =
+//               (v - mean) + z_a -> softmax expectation -> max_a.
 // h_a (128 KB) stays resident in SMEM; h_v and the weight k-blocks stream through a
 // 3-stage ring. TMEM: two 256-column accumulators, alternating by job parity.
 constexpr int kHeadStages = 3, kHeadSlot = 32768, kHeadA = 8 * 16384;
@@ -604,7 +605,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
   // (the finalize prologue's [roots | level-1 children]): Q rows -> rows_out
   // ns: work items per 128-row tile, each taking a contiguous slice of the action chunks
   // (MODE_ROWS only: tiny batches spread their z_a weight stream over ns CTAs; ns = 1 otherwise)
-  static_assert(ATOMS <= 64, "one action per 64 TMEM columns");
+  static_assert(ATOMS * 4 <= kHeadChunkRows && kHeadChunkRows <= 256, "4 actions per z_a chunk");
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024u - ((uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u);
   uint8_t *sA = smem, *sRing = smem + kHeadA;
@@ -668,8 +669,8 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
         }
         for (int c = c_lo; c < c_hi; ++c)
           for (int kb = 0; kb < 8; ++kb, ++it) {
-            const int st = slot_wait(kHeadSlot);
-            tma_2d(saddr(sRing + st * kHeadSlot), &mapBa, kb * 64, c * 256, &full[st]);
+            const int st = slot_wait(kHeadChunkRows * 128);
+            tma_2d(saddr(sRing + st * kHeadSlot), &mapBa, kb * 64, c * kHeadChunkRows, &full[st]);
           }
       }
     }
@@ -689,7 +690,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
           tc_fence_after();
         }
         const int c = c_lo + j - 2;
-        const int nt = j < 2 ? 64 : (c < nch - 1 ? 256 : (A - 4 * c) * 64);
+        const int nt = j < 2 ? 64 : (min(4, A - 4 * c) * ATOMS + 15) / 16 * 16;   // 208 for 4 actions
         const uint32_t idesc = idesc_bf16(kBM, nt);
         const int nkb = j == 1 ? 16 : 8;
         for (int kb = 0; kb < nkb; ++kb, ++it) {
@@ -752,7 +753,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
         tc_fence_after();
         const int na = min(4, A - 4 * c);
         for (int s = grp; s < na; s += 2) {
-          tmem_ld64(tmem + b * 256 + lanes + (uint32_t)(s * 64), x);
+          tmem_ld64(tmem + b * 256 + lanes + (uint32_t)(s * ATOMS), x);   // action s: columns 51 s ..
           const int a = 4 * c + s;
           float mx = -INFINITY;
 #pragma unroll
@@ -1022,7 +1023,8 @@ bool head_plan(HeadPlan &H, const __nv_bfloat16 *hid, int64_t cap, const __nv_bf
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   };
   if (!enc(H.mapAv, hid, 512, (uint64_t)cap, 1024, 128) || !enc(H.mapAa, hid + 512, 512, (uint64_t)cap, 1024, 128) ||
-      !enc(H.mapBv, wv64, 512, 64, 512, 64) || !enc(H.mapBa, wa64, 512, (uint64_t)A * 64, 512, 256) ||
+      !enc(H.mapBv, wv64, 512, 64, 512, 64) ||
+      !enc(H.mapBa, wa64, 512, (uint64_t)((A + 3) / 4) * kHeadChunkRows, 512, kHeadChunkRows) ||
       !enc(H.mapBs, wsum, 512, 128, 512, 64))
     return false;
 
