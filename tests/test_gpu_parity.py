@@ -506,6 +506,22 @@ def test_head_backup_bit_identical(cname, n, d):
     assert a["stats"]["kernel_launches"] < b["stats"]["kernel_launches"]
 
 
+def test_fused_leaves_more_than_32_actions():
+    """A = 40 (> 32): k_conv1_sib reads the child keys of actions 32..39 from the second per-parent lane
+    table (each lane hashes actions l and l + 32 once per parent). Fused vs materialised leaves (the
+    materialised path hashes every child in k_expand_atari) and the whole search vs the oracle."""
+    cfg = Config("A40", ENV_ATARI_HASH, NET_NATURE_BF16, 40, 2, 2, 0.99, 1.0, seed=40, wseed=140)
+    roots = cfg.roots()
+    a = run(handle(cfg), roots, 2, cfg.gamma, 1.0, 1)
+    b = run(handle(cfg, flags=P.F_MATERIALIZE_LEAVES), roots, 2, cfg.gamma, 1.0, 1)
+    scale = np.abs(b["vanilla_q"]).max(axis=1, keepdims=True)
+    assert (np.abs(a["vanilla_q"] - b["vanilla_q"]) <= 1e-4 * scale).all()
+    assert (a["best_leaf"] == b["best_leaf"]).mean() >= 0.9
+    r = Oracle.from_config(cfg).search(roots, 2, float(np.float32(cfg.gamma)), 1.0, 1, mode=0, threads=THREADS)
+    assert rel_err(a["root_q"], r["root_q"]).max() <= RTOL_BF16_SEARCH
+    assert action_agreement(a["actions"], r["root_q"], RTOL_BF16_SEARCH)[0] >= 0.999
+
+
 @pytest.mark.parametrize("cname,n,d", [("C3", 3, 2), ("C5", 1, 2), ("C5", 1, 3), ("C4", 2, 3)])
 def test_fused_leaves_match_materialized(cname, n, d):
     """k_conv1_sib (leaf expansion fused into conv1, sibling-factorised, fp16 operands with exact
