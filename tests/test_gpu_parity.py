@@ -506,6 +506,21 @@ def test_head_backup_bit_identical(cname, n, d):
     assert a["stats"]["kernel_launches"] < b["stats"]["kernel_launches"]
 
 
+@pytest.mark.parametrize("A", [5, 7, 33])
+def test_rainbow_head_chunk_tails(A):
+    """k_zhead packs z_a in chunks of 4 actions x 51 rows (N = 208); the last chunk holds 1 (A = 5, 33 -> N = 64)
+    or 3 (A = 7 -> N = 160) actions. Whole depth-2 searches vs the oracle (bf16 search tolerance, actions under
+    the near-tie rule), spread head weights so the check discriminates."""
+    cfg = Config(f"R{A}", ENV_ATARI_HASH, NET_RAINBOW_BF16, A, 2, 2, 0.99, 1.0, seed=50 + A, wseed=150 + A,
+                 extra={"head_scale": 64.0})
+    roots = cfg.roots()
+    g = run(handle(cfg), roots, 2, cfg.gamma, 1.0, 1)
+    r = Oracle.from_config(cfg).search(roots, 2, float(np.float32(cfg.gamma)), 1.0, 1, mode=0, threads=THREADS)
+    assert rel_err(g["root_q"], r["root_q"]).max() <= RTOL_BF16_SEARCH
+    assert rel_err(g["vanilla_q"], r["vanilla_q"]).max() <= RTOL_BF16_SEARCH
+    assert action_agreement(g["actions"], r["root_q"], RTOL_BF16_SEARCH)[0] >= 0.999
+
+
 def test_fused_leaves_more_than_32_actions():
     """A = 40 (> 32): k_conv1_sib reads the child keys of actions 32..39 from the second per-parent lane
     table (each lane hashes actions l and l + 32 once per parent). Fused vs materialised leaves (the
