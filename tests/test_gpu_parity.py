@@ -521,18 +521,22 @@ def test_rainbow_head_chunk_tails(A):
     assert action_agreement(g["actions"], r["root_q"], RTOL_BF16_SEARCH)[0] >= 0.999
 
 
-def test_fused_leaves_more_than_32_actions():
+@pytest.mark.parametrize("A,n,d", [(40, 2, 2), (2, 5, 3), (3, 7, 3)])
+def test_fused_leaves_action_counts(A, n, d):
     """A = 40 (> 32): k_conv1_sib reads the child keys of actions 32..39 from the second per-parent lane
-    table (each lane hashes actions l and l + 32 once per parent). Fused vs materialised leaves (the
-    materialised path hashes every child in k_expand_atari) and the whole search vs the oracle."""
-    cfg = Config("A40", ENV_ATARI_HASH, NET_NATURE_BF16, 40, 2, 2, 0.99, 1.0, seed=40, wseed=140)
+    table (each lane hashes actions l and l + 32 once per parent); A = 2, 3: a parent switch every 2-3
+    children in every role's loop. Fused vs materialised leaves (the materialised path hashes every child
+    in k_expand_atari) and the whole search vs the oracle."""
+    cfg = Config(f"A{A}", ENV_ATARI_HASH, NET_NATURE_BF16, A, d, n, 0.99, 1.0, seed=40 + A, wseed=140 + A)
     roots = cfg.roots()
-    a = run(handle(cfg), roots, 2, cfg.gamma, 1.0, 1)
-    b = run(handle(cfg, flags=P.F_MATERIALIZE_LEAVES), roots, 2, cfg.gamma, 1.0, 1)
+    a = run(handle(cfg), roots, d, cfg.gamma, 1.0, 1)
+    b = run(handle(cfg, flags=P.F_MATERIALIZE_LEAVES), roots, d, cfg.gamma, 1.0, 1)
+    # the two paths round act1 to bf16 after different fp32 sums (R17/R18): ~1e-5 absolute, which is above
+    # 1e-4 relative for a root whose |Q| is ~0.02 (no reward on its paths), so R18's search tolerance
     scale = np.abs(b["vanilla_q"]).max(axis=1, keepdims=True)
-    assert (np.abs(a["vanilla_q"] - b["vanilla_q"]) <= 1e-4 * scale).all()
+    assert (np.abs(a["vanilla_q"] - b["vanilla_q"]) <= RTOL_BF16_SEARCH * scale).all()
     assert (a["best_leaf"] == b["best_leaf"]).mean() >= 0.9
-    r = Oracle.from_config(cfg).search(roots, 2, float(np.float32(cfg.gamma)), 1.0, 1, mode=0, threads=THREADS)
+    r = Oracle.from_config(cfg).search(roots, d, float(np.float32(cfg.gamma)), 1.0, 1, mode=0, threads=THREADS)
     assert rel_err(a["root_q"], r["root_q"]).max() <= RTOL_BF16_SEARCH
     assert action_agreement(a["actions"], r["root_q"], RTOL_BF16_SEARCH)[0] >= 0.999
 
