@@ -514,7 +514,11 @@ def test_rainbow_head_chunk_tails(A):
     cfg = Config(f"R{A}", ENV_ATARI_HASH, NET_RAINBOW_BF16, A, 2, 2, 0.99, 1.0, seed=50 + A, wseed=150 + A,
                  extra={"head_scale": 64.0})
     roots = cfg.roots()
-    g = run(handle(cfg), roots, 2, cfg.gamma, 1.0, 1)
+    h = P.Handle.from_config(cfg)   # not cached: each conv-net handle binds ~7 GB of net scratch
+    try:
+        g = run(h, roots, 2, cfg.gamma, 1.0, 1)
+    finally:
+        h.close()
     r = Oracle.from_config(cfg).search(roots, 2, float(np.float32(cfg.gamma)), 1.0, 1, mode=0, threads=THREADS)
     assert rel_err(g["root_q"], r["root_q"]).max() <= RTOL_BF16_SEARCH
     assert rel_err(g["vanilla_q"], r["vanilla_q"]).max() <= RTOL_BF16_SEARCH
@@ -529,8 +533,13 @@ def test_fused_leaves_action_counts(A, n, d):
     in k_expand_atari) and the whole search vs the oracle."""
     cfg = Config(f"A{A}", ENV_ATARI_HASH, NET_NATURE_BF16, A, d, n, 0.99, 1.0, seed=40 + A, wseed=140 + A)
     roots = cfg.roots()
-    a = run(handle(cfg), roots, d, cfg.gamma, 1.0, 1)
-    b = run(handle(cfg, flags=P.F_MATERIALIZE_LEAVES), roots, d, cfg.gamma, 1.0, 1)
+    ha, hb = P.Handle.from_config(cfg), P.Handle.from_config(cfg, flags=P.F_MATERIALIZE_LEAVES)   # not cached
+    try:
+        a = run(ha, roots, d, cfg.gamma, 1.0, 1)
+        b = run(hb, roots, d, cfg.gamma, 1.0, 1)
+    finally:
+        ha.close()
+        hb.close()
     # the two paths round act1 to bf16 after different fp32 sums (R17/R18): ~1e-5 absolute, which is above
     # 1e-4 relative for a root whose |Q| is ~0.02 (no reward on its paths), so R18's search tolerance
     scale = np.abs(b["vanilla_q"]).max(axis=1, keepdims=True)
