@@ -17,3 +17,19 @@ def pytest_configure(config):
 def has_gpu():
     import torch
     return torch.cuda.is_available()
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _close_cached_handles(request):
+    """GPU test modules cache their library handles in a module-level `_handles` dict (one handle per
+    config and flag set); each conv-net handle binds several GB of net scratch, so close them when the
+    module is done instead of holding every module's handles until the process exits."""
+    yield
+    cache = getattr(request.module, "_handles", None)
+    if isinstance(cache, dict):
+        for h in cache.values():
+            try:
+                h.close()
+            except Exception:
+                pass
+        cache.clear()
