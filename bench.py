@@ -29,9 +29,10 @@ METRIC = "tree nodes expanded+evaluated/sec and root decisions/sec at depth 4, A
 
 def nodes_per_root(A, d, corr):
     """Algorithmic per-root counts: expanded = sum_{k=1..d} A^k,
-    evaluated = A^d + corr*(1 + [d>=2]*A) (+1 at d=0)."""
+    evaluated = A^d + [corr]*(1 + [d>=2]*A) (+1 at d=0): the BCTS terms (Eq. 5 or Lemma 2's exact
+    biases alike) need the root row and, at d >= 2, the level-1 rows."""
     expanded = sum(A ** k for k in range(1, d + 1))
-    evaluated = (A ** d + (corr * (1 + (A if d >= 2 else 0))) if d >= 1 else 1)
+    evaluated = (A ** d + ((1 if corr else 0) * (1 + (A if d >= 2 else 0))) if d >= 1 else 1)
     return expanded, evaluated
 
 
@@ -170,14 +171,18 @@ def dtype_of(cfg):
     return "bf16" if cfg.net in (3, 4) else "f32"
 
 
-def workload_of(cfg, n):
+CORRECTION_NAMES = {0: "correction off (vanilla TS)", 1: "correction on", 2: "correction on (Lemma 2 exact biases)"}
+
+
+def workload_of(cfg, n, corr=1):
     base = f"{cfg.name}: Batch-BFS+BCTS, A={cfg.A}, depth={cfg.depth}, {n} root(s), "
+    cn = CORRECTION_NAMES[corr]
     if cfg.net in (3, 4):
-        return base + f"{'Rainbow' if cfg.net == 4 else 'Nature'}-shaped bf16 Q-net (random init), correction on"
+        return base + f"{'Rainbow' if cfg.net == 4 else 'Nature'}-shaped bf16 Q-net (random init), {cn}"
     if cfg.env == 4:
         return base + ("random-DNN forward model (3x100 hidden, P:340-341) + MLP2 100-256-A fp32 leaf net "
-                       "(random init), correction on")
-    return base + "hash env + MLP2/table leaf values, correction on"
+                       f"(random init), {cn}")
+    return base + f"hash env + MLP2/table leaf values, {cn}"
 
 
 # ------------------------------------------------------------------ CPU oracle leg
@@ -229,7 +234,7 @@ def run_reference(args, cfg, world, rank):
     o = Oracle.from_config(cfg, tab=tab_of(cfg))
     root = cfg.roots(1)
     A, d = cfg.A, cfg.depth
-    exp, ev = nodes_per_root(A, d, 1)
+    exp, ev = nodes_per_root(A, d, args.correction)
     per_task = (exp + A ** d) / (A * A)
     ntask = min(threads, A * A)
     times = []
@@ -245,7 +250,7 @@ def run_reference(args, cfg, world, rank):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "decisions_per_s": value / (exp + ev), "metric_note": metric_of(cfg),
-            "config": {"workload": workload_of(cfg, cfg.n_roots) + f"; each step = {ntask} depth-2 subtrees "
+            "config": {"workload": workload_of(cfg, cfg.n_roots, args.correction) + f"; each step = {ntask} depth-2 subtrees "
                                    "(bounded sample)",
                        "roots": cfg.n_roots, "depth": d, "A": A},
             "cpu_baseline": {"value": value, "unit": "nodes/s", "cores": threads, "kind": "oracle",
@@ -269,6 +274,8 @@ def main():
     ap.add_argument("--tf32", action="store_true",
                     help="BCTS_F_TF32: DNN forward model / MLP2 on tcgen05 kind::tf32 (within the tf32 tolerance)")
     ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--correction", type=int, choices=(0, 1, 2), default=1,
+                    help="correction_on: 0 vanilla TS, 1 BCTS Eq. 5 (the headline), 2 Lemma 2 exact biases (NEXT-2)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
@@ -294,7 +301,7 @@ def main():
     # search is then collective inside the library: each rank scores its leaf range and one
     # ncclAllReduce(MAX) of the packed root keys runs on the handle's stream
     h = world_handle(cfg, tab=tab_of(cfg), device=local, flags=flags)
-    n, d, A, corr = cfg.n_roots, cfg.depth, cfg.A, 1
+    n, d, A, corr = cfg.n_roots, cfg.depth, cfg.A, args.correction
     roots_np = cfg.roots()
     roots = torch.from_numpy(roots_np.view(np.uint8).reshape(n, -1).copy()).to(dev)
     act = torch.empty(n, dtype=torch.int32, device=dev)
@@ -452,7 +459,7 @@ def main():
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "tf32" if (args.tf32 and cfg.net not in (3, 4)) else dtype_of(cfg), "data": "synthetic",
                 "decisions_per_s": n / (step_ms / 1e3),
-                "config": {"workload": workload_of(cfg, n),
+                "config": {"workload": workload_of(cfg, n, corr),
                            "roots": n, "depth": d, "A": A, "nodes_per_decision": exp + ev,
                            "parallelism": (f"leaf-range shards x{world}, one NCCL max all-reduce of the "
                                            f"{n * A} packed root keys inside the library") if world > 1
